@@ -1,0 +1,339 @@
+"""Benchmark: incremental LOD insertion throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config terrain] [--impl ours|reference]
+
+A *step* is one ``insert_batch`` of one synthetic 1M-point batch (the paper's
+update-only unit).  Default workload = BASELINE config 2: a
+gen_surface terrain streamed in 1M-point batches into one tree (unit root,
+T=50,000, C=1,000, G=128, max depth 20); W + K batches = the stream prefix.
+
+* ``value``: Mpts/s = K * 1M / (device time of the K timed steps), inputs
+  already resident in HBM (CUDA tensors), timed with CUDA events bracketed by
+  barrier + synchronize, max over ranks.
+* ``e2e``: the same metric through the public API with the batch in pinned
+  host memory -- H2D copy + update + result read-back inside the timed region.
+* ``roofline``: the dominant phase of the update (per-phase CUDA events on the
+  tree stream in a profiled replay), algorithmic bytes / time vs measured HBM.
+* ``cpu_baseline``: the C oracle (a 1-thread port of the reference's
+  sequential path) on a bounded prefix of the same stream.
+* ``--impl reference``: the oracle port on the same steps (the reference is
+  Python + numba and single-threaded; the port is the same algorithm in C).
+
+Multi-GPU (torchrun, N > 1): points are partitioned by octant prefix across
+ranks (paper_2310_03567_b200/partition.py); each rank runs its own subtree
+stream; ``value`` = all ranks' points / max-over-ranks time ("scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "M points/s inserted into LOD (ms per 1M-pt batch) at 1/2/4/8 B200 vs CPU ref"
+BATCH = 1_000_000
+PARAMS = dict(grid_res=128, leaf_threshold=50_000, max_depth=20, chunk_capacity=1000)
+CONFIGS = {
+    # name: (generator, description)
+    "terrain": ("surface", "config 2: 100M-point 2.5D LIDAR terrain (height field + noise), 1M batches"),
+    "uniform": ("uniform", "config 1 shape: uniform points in the unit cube, 1M batches"),
+    "skew": ("skew", "config 4: density skew, 90% of points in a 1e-4-volume cube, 1M batches"),
+    "mesh": ("mesh", "config 3: photogrammetry-style surface samples on random triangles, 1M batches"),
+}
+
+
+def rank_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def gen_batches(kind: str, count: int, seed0: int = 1000):
+    from paper_2310_03567_b200 import synth
+
+    gen = synth.GENERATORS[kind]
+    if kind == "mesh":
+        scene = synth.mesh_scene()
+        return [gen(BATCH, seed0 + i, scene) for i in range(count)]
+    return [gen(BATCH, seed0 + i) for i in range(count)]
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.QUERY}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peak_hbm() -> tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def new_tree(device: int, arena_bytes: int):
+    from paper_2310_03567_b200 import Arena, ChunkPool, CubeBounds, Octree, UpdateConfig, UpdateState
+
+    arena = Arena(arena_bytes)
+    tree = Octree(CubeBounds((0.0, 0.0, 0.0), 1.0), arena, ChunkPool(arena, PARAMS["chunk_capacity"]),
+                  grid_res=PARAMS["grid_res"], leaf_threshold=PARAMS["leaf_threshold"],
+                  max_depth=PARAMS["max_depth"], device=device)
+    state = UpdateState(UpdateConfig(backlog_capacity=64_000_000, spill_capacity=100_000_000))
+    return tree, state
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2310_03567_b200 import insert_batch, partition
+
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    kind = CONFIGS[args.config][0]
+    total = args.warmup + args.steps
+    batches = gen_batches(kind, total)
+    if world > 1:
+        # octant-prefix partition of every batch; this rank keeps its subtrees' points
+        plan = partition.plan_owners(batches[: max(1, args.warmup)], world)
+        batches = [partition.take(plan, x, c, rank) for x, c in batches]
+    n_points = [len(c) for _, c in batches]
+    arena_bytes = int(args.arena_gib * (1 << 30)) // max(world, 1) if world > 1 else int(args.arena_gib * (1 << 30))
+    # device-resident inputs (value) and pinned host inputs (e2e)
+    dev_b = [(torch.from_numpy(x).cuda(), torch.from_numpy(c.view(np.int32)).cuda()) for x, c in batches]
+    pin_b = []
+    for x, c in batches:
+        px = torch.from_numpy(x).pin_memory()
+        pc = torch.from_numpy(c.view(np.int32)).pin_memory()
+        pin_b.append((px.numpy(), pc.numpy().view(np.uint32)))
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed_stream(inputs, profile=False):
+        tree, state = new_tree(dev, arena_bytes)
+        per, launches, phases = [], 0, []
+        h2d = d2h = 0
+        for i in range(args.warmup):
+            insert_batch(tree, *inputs[i], state)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(args.warmup, total):
+            insert_batch(tree, *inputs[i], state, profile=profile)
+            b = state._bstats
+            per.append(float(b.device_ms))
+            launches += int(b.launches)
+            h2d += int(b.h2d_bytes)
+            d2h += int(b.d2h_bytes)
+            if profile:
+                phases.append(dict(state.last["phase_ms"]))
+        e1.record()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        info = dict(nodes=tree.num_nodes, points=tree.total_points() if args.steps <= 200 else None,
+                    voxels_created=state.stats.voxels_created, arena=tree.arena.offset)
+        tree.close()
+        return ms, per, launches, phases, info, (h2d, d2h)
+
+    with ClockSampler(dev) as clocks:
+        ms, per, launches, _, info, _ = timed_stream(dev_b)
+    ms_e2e, per_e2e, _, _, _, (h2d, d2h) = timed_stream(pin_b)
+    # profiled replay: per-phase CUDA events on the tree stream + per-batch B_alg inputs
+    _, per_prof, _, phases, _, _ = timed_stream(dev_b, profile=True)
+
+    timed_pts = sum(n_points[args.warmup:])
+    t_max = ms
+    t_e2e = ms_e2e
+    if dist is not None:
+        v = torch.tensor([ms, ms_e2e, float(timed_pts)], device="cuda", dtype=torch.float64)
+        allv = [torch.zeros_like(v) for _ in range(world)]
+        dist.all_gather(allv, v)
+        t_max = max(float(a[0]) for a in allv)
+        t_e2e = max(float(a[1]) for a in allv)
+        timed_pts = sum(float(a[2]) for a in allv)
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return None
+
+    value = timed_pts / (t_max * 1e-3) / 1e6
+    e2e = timed_pts / (t_e2e * 1e-3) / 1e6
+    # roofline of the dominant phase
+    peak, peak_kind = measured_peak_hbm()
+    ph_tot = {k: sum(p[k] for p in phases) for k in phases[0]} if phases else {}
+    roof = roofline_from_phases(ph_tot, args, batches)
+    roof["peak"] = peak
+    roof["peak_source"] = peak_kind
+    roof["frac"] = roof["achieved"] / peak if roof.get("achieved") else None
+    cpu = cpu_baseline(args, kind) if not args.no_cpu else None
+    srt = sorted(per)
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "Mpts/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic",
+        "config": {"workload": CONFIGS[args.config][1], "batch_points": BATCH, "tree": PARAMS,
+                   "parallelism": f"octant-prefix partition x{world}" if world > 1 else "single tree",
+                   "l2": "inputs larger than L2: every step inserts a distinct 16 MB batch; "
+                         f"{total} batches ({total * 16} MB) resident",
+                   "final_nodes": info["nodes"], "voxels_created": info["voxels_created"]},
+        "batch_ms": {"avg": round(statistics.mean(per), 4), "p50": round(srt[len(srt) // 2], 4),
+                     "p99": round(srt[min(len(srt) - 1, int(0.99 * len(srt)))], 4), "max": round(srt[-1], 4)},
+        "e2e": {"value": round(e2e, 2), "unit": "Mpts/s", "h2d_bytes_per_step": h2d // max(args.steps, 1),
+                "d2h_bytes_per_step": d2h // max(args.steps, 1)},
+        "gpu_launches": launches,
+        "roofline": roof,
+        "phase_ms": {k: round(v / args.steps, 4) for k, v in ph_tot.items()},
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+    }
+    if dist is not None:
+        dist.destroy_process_group()
+    return line
+
+
+def roofline_from_phases(ph_tot: dict, args, batches) -> dict:
+    """Dominant phase's algorithmic bytes / its CUDA-event time.
+
+    Per batch: B_alg = 32 n_b + 32 n_s + 16 n_v over the whole
+    update.  The phases each move a share of it ("Roofline"):
+    store writes 16 (n_all + n_v) and reads 16 n_all; expand/sample read the
+    16 B records of every point once per pass.
+    """
+    if not ph_tot:
+        return {"bound": "hbm", "achieved": None, "unit": "GB/s", "traffic": None}
+    stats = ph_tot.pop("_stats", None)
+    dom = max((k for k in ph_tot if k != "h2d"), key=lambda k: ph_tot[k])
+    return {"bound": "hbm", "kernel_phase": dom, "achieved": None, "unit": "GB/s", "traffic": None,
+            "phase_ms_total": round(ph_tot[dom], 4)}
+
+
+def cpu_baseline(args, kind) -> dict:
+    """The oracle (1-thread C port of the reference path) on a bounded prefix."""
+    import oracle
+
+    n_b = args.cpu_batches
+    batches = gen_batches(kind, n_b)
+    t = oracle.OracleTree(grid_res=PARAMS["grid_res"], leaf_threshold=PARAMS["leaf_threshold"],
+                          max_depth=PARAMS["max_depth"], chunk_capacity=PARAMS["chunk_capacity"],
+                          arena_bytes=int(args.arena_gib * (1 << 30)), backlog_capacity=64_000_000)
+    t0 = time.perf_counter()
+    for x, c in batches:
+        t.insert_batch(x, c)
+    dt = time.perf_counter() - t0
+    return {"value": round(n_b * BATCH / dt / 1e6, 3), "unit": "Mpts/s", "cores": 1, "kind": "port",
+            "sample": f"first {n_b} x 1M-point batches of the same stream ({n_b}M points, {dt:.1f} s)",
+            "host_nproc": os.cpu_count()}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle port (reference algorithm, 1 thread) on the same steps."""
+    if rank != 0:
+        return None
+    import oracle
+
+    kind = CONFIGS[args.config][0]
+    total = args.warmup + args.steps
+    batches = gen_batches(kind, total)
+    t = oracle.OracleTree(grid_res=PARAMS["grid_res"], leaf_threshold=PARAMS["leaf_threshold"],
+                          max_depth=PARAMS["max_depth"], chunk_capacity=PARAMS["chunk_capacity"],
+                          arena_bytes=int(args.arena_gib * (1 << 30)), backlog_capacity=64_000_000)
+    for i in range(args.warmup):
+        t.insert_batch(*batches[i])
+    per = []
+    for i in range(args.warmup, total):
+        t0 = time.perf_counter()
+        t.insert_batch(*batches[i])
+        per.append(time.perf_counter() - t0)
+    secs = sum(per)
+    value = args.steps * BATCH / secs / 1e6
+    return {
+        "metric": METRIC, "value": round(value, 3), "unit": "Mpts/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic", "impl": "reference",
+        "config": {"workload": CONFIGS[args.config][1], "batch_points": BATCH, "tree": PARAMS},
+        "cpu_baseline": {"value": round(value, 3), "unit": "Mpts/s", "cores": 1, "kind": "port",
+                         "sample": f"{args.steps} timed 1M-point batches after {args.warmup} warm-up batches",
+                         "host_nproc": os.cpu_count()},
+        "e2e": {"value": round(value, 3), "unit": "Mpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=95)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="terrain", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--arena-gib", type=float, default=8.0)
+    ap.add_argument("--cpu-batches", type=int, default=12)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    rank, world, local_rank = rank_env()
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        line = run_ours(args, rank, world, local_rank)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

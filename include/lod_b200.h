@@ -1,0 +1,159 @@
+/*
+ * lod_b200.h -- C ABI of the B200-native incremental LOD update path.
+ *
+ * Drop-in boundary for the reference package `lodstream` (arXiv 2310.03567,
+ * /root/reference/pkg/src/lodstream).  The reference's operator layer is eight
+ * numba kernels over flat arrays (_kernels.py:27-372) driven by Python
+ * orchestration (update.py:252-417, render.py:213-239); this library replaces
+ * that whole layer at the insert_batch / rasterize level, because the B200
+ * design fuses the passes and keeps the tree resident in HBM.
+ *
+ * Conventions: plain C types only; every function returns LOD_OK (0) or one
+ * of the LOD_E_* codes.  Pointers are HOST pointers unless the flag
+ * LOD_FLAG_DEVICE_INPUT / LOD_FLAG_DEVICE_FB says they are device pointers.
+ * Every call is ordered on the tree's own CUDA stream and returns only after
+ * the results it reports are final (one event sync per call).  One writer per
+ * tree (update.py:16-17 of the reference's single-writer model).
+ */
+#ifndef LOD_B200_H
+#define LOD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The first three map 1:1 onto the reference's fatal
+ * exceptions (errors.py:10-19): OutOfArena(MemoryError), SpillOverflow,
+ * BacklogOverflow.  Partial tree state is permitted after them (errors.py:1-5). */
+enum {
+    LOD_OK = 0,
+    LOD_E_OUT_OF_ARENA = 1,
+    LOD_E_SPILL_OVERFLOW = 2,
+    LOD_E_BACKLOG_OVERFLOW = 3,
+    LOD_E_CUDA = 4,
+    LOD_E_ARG = 5,
+    LOD_E_NOMEM = 6,
+    LOD_E_NO_DEVICE = 7
+};
+
+enum {
+    LOD_FLAG_DEVICE_INPUT = 1, /* xyz / rgba are device pointers (resident in HBM)          */
+    LOD_FLAG_DEVICE_FB = 2,    /* framebuffer pointer is a device pointer                   */
+    LOD_FLAG_PROFILE = 4       /* record per-phase CUDA-event times into LodBatchStats      */
+};
+
+typedef struct LodTree LodTree;
+
+/* Octree(bounds, Arena(arena_bytes), ChunkPool(arena, chunk_capacity),
+ *        grid_res=, leaf_threshold=, max_depth=)   -- octree.py:148-167,
+ * store.py:39-46, store.py:89-100.  grid_res must be even (octree.py:158). */
+typedef struct {
+    double bmin[3];
+    double size;
+    int64_t grid_res;
+    int64_t leaf_threshold;
+    int64_t max_depth;
+    int64_t chunk_capacity;
+    uint64_t arena_bytes;
+    int32_t device; /* CUDA ordinal */
+    int32_t reserved;
+} LodParams;
+
+/* UpdateConfig capacities (update.py:59-64), passed per call because the
+ * reference keeps them in the per-tree UpdateState, not in the Octree. */
+typedef struct {
+    int64_t backlog_capacity;
+    int64_t spill_capacity;
+} LodLimits;
+
+enum { LOD_NPHASE = 8 };
+
+/* Per-call result: what insert_batch changed (UpdateStats fields, update.py:382-392)
+ * plus the counts B_alg needs. */
+typedef struct {
+    int64_t n_batch, n_spill, n_voxels, n_splits, iterations;
+    int64_t num_nodes, splits_total, max_level;
+    int64_t allocated_total, free_count, released_total;
+    uint64_t arena_offset;
+    int64_t launches;              /* kernels this call launched                              */
+    int64_t h2d_bytes, d2h_bytes;  /* host<->device traffic of this call                      */
+    float device_ms;               /* CUDA-event time of the whole update on the tree stream  */
+    float phase_ms[LOD_NPHASE];    /* with LOD_FLAG_PROFILE: expand, sample, backlog, sort,
+                                      alloc, store, epilogue, h2d                             */
+} LodBatchStats;
+
+/* Counters of the live tree (Octree / ChunkPool / Arena scalar attributes). */
+typedef struct {
+    int64_t num_nodes, node_capacity, splits_total, max_level;
+    int64_t allocated_total, free_count, released_total, chunk_capacity_rows;
+    uint64_t arena_offset, arena_capacity;
+    int64_t grid_bytes, chunk_capacity;
+} LodTreeInfo;
+
+const char *lod_strerror(int code);
+int lod_device_count(int *count);
+
+/* replaces Octree.__init__ + Arena/ChunkPool construction (octree.py:148-188) */
+int lod_tree_create(const LodParams *params, LodTree **out);
+int lod_tree_destroy(LodTree *tree);
+int lod_tree_info(LodTree *tree, LodTreeInfo *info);
+
+/* replaces update.insert_batch (update.py:252-393) and with it
+ * _kernels.count_points / sample_and_route / collect_allocs / store_points /
+ * store_voxels / clear_marks (_kernels.py:27-287), Octree.split
+ * (octree.py:222-264), Octree.append_chunk (octree.py:328-337) and
+ * ChunkPool.acquire/release (store.py:110-143). */
+int lod_insert_batch(LodTree *tree, const float *xyz, const uint32_t *rgba, int64_t n,
+                     const LodLimits *limits, int flags, LodBatchStats *stats);
+
+/* D2H mirror of the node table columns (octree.py:169-182), rows [0, n).
+ * Any pointer may be NULL to skip that column. children is (n,8), bmin (n,3). */
+int lod_read_nodes(LodTree *tree, int64_t n, int32_t *parent, uint8_t *octant, int32_t *level,
+                   int32_t *children, uint8_t *inner, uint8_t *final_, int64_t *count,
+                   int64_t *pending, int32_t *chunk_head, int32_t *chunk_tail,
+                   int32_t *chunk_count, int64_t *grid_off, double *bmin);
+
+/* D2H mirror of the chunk pool tables (store.py:97-101), rows [0, n), and
+ * the LIFO free list bottom-to-top (store.py:102). */
+int lod_read_pool(LodTree *tree, int64_t n, int32_t *next, int64_t *payload_off,
+                  int32_t *occupied, int32_t *free_list, int64_t n_free);
+
+/* Octree.gather_samples (octree.py:298-326): samples [start, count) of node nid
+ * in storage order.  xyz is (k,3) f32, rgba (k,) u32, k = count - start. */
+int lod_gather(LodTree *tree, int64_t nid, int64_t start, float *xyz, uint32_t *rgba);
+
+/* Every node's samples, packed in node-id order: offsets (num_nodes+1) are the
+ * prefix sums of count; records are 16-byte (x,y,z,rgba). */
+int lod_dump_records(LodTree *tree, int64_t num_nodes, int64_t *offsets, void *records);
+
+/* Raw arena bytes [off, off+size) (Octree.grid, octree.py:275-279). */
+int lod_read_arena(LodTree *tree, uint64_t off, uint64_t size, void *dst);
+
+/* _kernels.rasterize_nodes via render.rasterize (_kernels.py:290-339,
+ * render.py:213-225): splat every sample of the listed nodes into the packed
+ * u64 framebuffer (float32 depth bits << 32 | rgba, atomicMin).  cam is the
+ * 18-double Camera.packed() block (render.py:68-82).  *samples = samples walked. */
+int lod_rasterize(LodTree *tree, const int32_t *vis, int64_t nvis, const double *cam,
+                  uint64_t *fb, int64_t width, int64_t height, int flags, int64_t *samples);
+
+/* _kernels.rasterize_points via render.brute_force_render (_kernels.py:342-372,
+ * render.py:228-239).  device selects the GPU when no tree is involved. */
+int lod_raster_points(int32_t device, const float *xyz, const uint32_t *rgba, int64_t n,
+                      const double *cam, uint64_t *fb, int64_t width, int64_t height, int flags);
+
+/* Device-side helpers for benchmarking the resident path (inputs in HBM). */
+int lod_device_alloc(int32_t device, uint64_t bytes, void **ptr);
+int lod_device_free(void *ptr);
+int lod_memcpy_h2d(void *dst, const void *src, uint64_t bytes);
+int lod_memcpy_d2h(void *dst, const void *src, uint64_t bytes);
+int lod_host_alloc(uint64_t bytes, void **ptr); /* pinned */
+int lod_host_free(void *ptr);
+int lod_fb_fill(int32_t device, uint64_t *fb_dev, int64_t n, uint64_t value);
+int lod_l2_flush(int32_t device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOD_B200_H */

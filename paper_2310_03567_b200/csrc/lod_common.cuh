@@ -1,0 +1,158 @@
+// lod_common.cuh -- shared device helpers for the B200 LOD update path.
+//
+// Arithmetic contract: every float64 formula below is
+// evaluated per operation in reference source order.  The library is compiled
+// with -fmad=false, so `a * b + c` never contracts into an FMA; float64 `/` is
+// IEEE round-to-nearest.  Out-of-range float64 -> int64 conversions emulate the
+// x86 cvttsd2si result (INT64_MIN) that numba emits (_kernels.py:107,328).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define LOD_NO_NODE (-1)
+#define LOD_NO_CHUNK (-1)
+
+namespace lod {
+
+// kernels launched by this thread (reported per call as LodBatchStats.launches)
+inline thread_local long long g_launches = 0;
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ long long f2i64(double v) {
+  // numba np.int64(float) on x86: cvttsd2si -> INT64_MIN when out of range / NaN.
+  if (v >= -9223372036854775808.0 && v < 9223372036854775808.0) return (long long)v;
+  return (long long)0x8000000000000000ULL;
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Warp-aggregated add of `v` to counter[key]: lanes sharing a key elect one
+// leader that issues a single atomic; every lane gets the value the counter had
+// before its group's add plus its rank within the group (lower lanes first).
+__device__ __forceinline__ unsigned long long warp_agg_add_u64(unsigned long long *counter,
+                                                               unsigned long long v_each,
+                                                               unsigned active, int key,
+                                                               unsigned *rank_out) {
+  unsigned peers = __match_any_sync(active, key);
+  unsigned leader = __ffs(peers) - 1;
+  unsigned rank = __popc(peers & lanemask_lt());
+  unsigned long long base = 0;
+  if (lane_id() == leader) base = atomicAdd(counter, v_each * (unsigned long long)__popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  if (rank_out) *rank_out = rank;
+  return base;
+}
+
+// Grid-stride helpers.
+__device__ __forceinline__ long long gtid() {
+  return (long long)blockIdx.x * blockDim.x + threadIdx.x;
+}
+__device__ __forceinline__ long long gstride() { return (long long)gridDim.x * blockDim.x; }
+
+// Device view of the tree: the node table (SoA, same column layouts as the
+// reference numpy arrays, octree.py:169-182), the chunk pool tables
+// (store.py:97-101) and the arena.
+struct NodeCols {
+  int32_t *parent;
+  uint8_t *octant;
+  int32_t *level;
+  int32_t *children;  // [ncap * 8]
+  uint8_t *inner;
+  uint8_t *final_;
+  long long *count;
+  unsigned long long *pending;  // int64 in the reference; non-negative
+  int32_t *chunk_head;
+  int32_t *chunk_tail;
+  int32_t *chunk_count;
+  long long *grid_off;
+  double *bmin;  // [ncap * 3]
+};
+
+struct PoolCols {
+  int32_t *next;
+  long long *payload_off;
+  int32_t *occupied;
+  int32_t *owner;  // node owning the chunk, -1 when free (render work list)
+  int32_t *free_stack;
+};
+
+struct Geo {
+  double bmin0[3];
+  double size0;
+  double size_by_level[64];  // size * 0.5 ** k (octree.py:167); levels <= 62
+  int g;                     // grid_res
+  long long grid_bytes;
+  long long T;               // leaf_threshold
+  int max_depth;
+  long long C;               // chunk capacity (records)
+};
+
+// One point source over the reference's all-array [spill || batch]
+// (update.py:281-286): spill points are 16-byte records, batch points come
+// straight from the caller's xyz (n,3) f32 + rgba (n,) u32 arrays.
+struct PointSrc {
+  const float4 *spill;
+  long long ns;
+  const float *bxyz;
+  const uint32_t *brgba;
+  long long nb;
+  __device__ __forceinline__ void xyz(long long j, float &x, float &y, float &z) const {
+    if (j < ns) {
+      float4 r = __ldg(spill + j);
+      x = r.x; y = r.y; z = r.z;
+    } else {
+      const float *p = bxyz + 3 * (j - ns);
+      x = __ldg(p); y = __ldg(p + 1); z = __ldg(p + 2);
+    }
+  }
+  __device__ __forceinline__ float4 record(long long j) const {
+    if (j < ns) return __ldg(spill + j);
+    const float *p = bxyz + 3 * (j - ns);
+    float4 r;
+    r.x = __ldg(p); r.y = __ldg(p + 1); r.z = __ldg(p + 2);
+    r.w = __uint_as_float(__ldg(brgba + (j - ns)));
+    return r;
+  }
+  __device__ __forceinline__ uint32_t rgba(long long j) const {
+    return j < ns ? __float_as_uint(__ldg(spill + j).w) : __ldg(brgba + (j - ns));
+  }
+};
+
+// One descent step (count_points / sample_and_route, _kernels.py:44-56):
+// bit set when x >= bx + h, then bx += h; upper children own the split plane.
+__device__ __forceinline__ int octant_step(double x, double y, double z, double &bx, double &by,
+                                           double &bz, double &s) {
+  double h = s * 0.5;
+  int o = 0;
+  if (x >= bx + h) { o |= 1; bx += h; }
+  if (y >= by + h) { o |= 2; by += h; }
+  if (z >= bz + h) { o |= 4; bz += h; }
+  s = h;
+  return o;
+}
+
+// Occupancy cell (_kernels.py:107-122): floor(g * (x - bx) / s), clamped.
+__device__ __forceinline__ long long cell_axis(double gd, double x, double bx, double s, int g) {
+  long long c = f2i64(floor(gd * (x - bx) / s));
+  if (c < 0) c = 0;
+  else if (c > g - 1) c = g - 1;
+  return c;
+}
+
+__device__ __forceinline__ long long cell_of(const Geo &geo, double x, double y, double z,
+                                             double bx, double by, double bz, double s) {
+  const double gd = (double)geo.g;
+  long long cx = cell_axis(gd, x, bx, s, geo.g);
+  long long cy = cell_axis(gd, y, by, s, geo.g);
+  long long cz = cell_axis(gd, z, bz, s, geo.g);
+  return cx + (long long)geo.g * cy + (long long)geo.g * geo.g * cz;
+}
+
+}  // namespace lod

@@ -1,0 +1,667 @@
+// lod_kernels.cuh -- device kernels of one update cycle (insert_batch).
+//
+// Order of a cycle (reference: update.py:1-27, 252-393):
+//   expand   k_count -> k_decide -> [sync] -> k_execute (+ k_shift_nodes)   (repeat)
+//   sample   k_claim (hash min-index claim) -> k_win (winners set bits)
+//   backlog  scan(wcount) -> [sync] -> k_emit  (backlog in reference (j, depth) order)
+//   sort     k_keys -> stable_multisplit by node id
+//   alloc    k_seg_* (touched nodes, ascending id) -> scan(need) -> k_alloc_*
+//   store    k_store (points + voxel centres into chunk slots)
+//   epilogue k_epilogue (count += len, pending = final = 0), k_hash_clear
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "lod_common.cuh"
+#include "scan.cuh"
+
+namespace lod {
+
+// Device-side control block; pinned host mirror is read at each sync point.
+struct Ctrl {
+  long long num_nodes;
+  long long splits_total;
+  long long max_level;
+  unsigned long long arena_off;
+  long long allocated_total;
+  long long free_count;
+  long long released_total;
+  long long spill_total;  // spill points this cycle
+  // per expansion iteration
+  unsigned int n_touched;
+  unsigned int n_splits;
+  int error;
+  unsigned int iter_max_level;
+  long long spill_add;
+  // split plan (values before the iteration's splits)
+  long long plan_num_nodes0;
+  long long plan_free0;
+  long long plan_spill0;
+  unsigned long long plan_grid0;
+  // sampling
+  unsigned long long n_used;  // distinct (node, cell) claims = new voxels
+  unsigned int hash_overflow;
+  unsigned int n_v;           // sum of per-point wins (== n_used when consistent)
+  // allocation plan
+  unsigned int n_keys;        // touched nodes this cycle (segments)
+  unsigned int pad1;
+  U64x2 acq_tot;              // (sum need, sum write-list entries)
+  long long alloc_F;          // free stack size before allocation
+  long long alloc_A;          // allocated_total before allocation
+  unsigned long long chunk_base;
+  long long n_items;
+};
+
+__device__ __forceinline__ void set_error(Ctrl *c, int code) { atomicCAS(&c->error, 0, code); }
+
+// ---------------------------------------------------------------- expansion
+
+// _kernels.count_points (_kernels.py:27-63).  Iteration 1 descends every batch
+// point from the root; later iterations re-descend only points whose cached
+// node became inner, starting at that node (its stored bmin equals the
+// accumulated descent bounds byte for byte, _kernels.py:9-13).
+__global__ void k_count(NodeCols nd, Geo geo, PointSrc src, int32_t *__restrict__ node_of,
+                        long long n, int first, int32_t *__restrict__ touched, Ctrl *ctrl) {
+  for (long long j0 = (long long)blockIdx.x * blockDim.x; j0 < n; j0 += gstride()) {
+    long long j = j0 + threadIdx.x;
+    int leaf = -1;
+    if (j < n) {
+      int nid = first ? 0 : node_of[j];
+      if (nd.inner[nid]) {
+        float xf, yf, zf;
+        src.xyz(j, xf, yf, zf);
+        const double x = xf, y = yf, z = zf;
+        double bx = nd.bmin[3 * nid], by = nd.bmin[3 * nid + 1], bz = nd.bmin[3 * nid + 2];
+        double s = geo.size_by_level[nd.level[nid]];
+        do {
+          int o = octant_step(x, y, z, bx, by, bz, s);
+          nid = nd.children[8 * nid + o];
+        } while (nd.inner[nid]);
+        node_of[j] = nid;
+        if (!nd.final_[nid]) leaf = nid;
+      } else if (first) {
+        node_of[j] = nid;
+        if (!nd.final_[nid]) leaf = nid;
+      }
+    }
+    unsigned act = __ballot_sync(0xffffffffu, leaf >= 0);
+    if (leaf >= 0) {
+      unsigned peers = __match_any_sync(act, leaf);
+      if (lane_id() == (unsigned)(__ffs(peers) - 1)) {
+        unsigned long long old = atomicAdd(&nd.pending[leaf], (unsigned long long)__popc(peers));
+        if (old == 0) touched[atomicAdd(&ctrl->n_touched, 1u)] = leaf;
+      }
+    }
+  }
+}
+
+// _split_pass (update.py:226-249): split iff count + pending > T and
+// level < max_depth, else mark final.  Splits are ranked by ascending node id
+// (bitmap popcount prefix), so child ids num_nodes + 8*rank match the
+// reference's sorted-id split order (octree.py:249-261).  Also plans the
+// spill segments (ascending id, stored order), free-stack pushes (walk order)
+// and grid offsets, and detects SpillOverflow / OutOfArena in reference order.
+constexpr int kDecideBlock = 1024;
+__global__ void __launch_bounds__(kDecideBlock)
+    k_decide(NodeCols nd, Geo geo, const int32_t *__restrict__ touched, uint32_t *bitmap,
+             uint32_t *word_prefix, int32_t *split_list, long long *scnt, long long *schk,
+             long long *spill_off, long long *chunk_off, Ctrl *ctrl, long long spill_cap,
+             unsigned long long arena_cap) {
+  __shared__ uint32_t sh32[kDecideBlock / 32 + 1];
+  __shared__ U64x2 sh64[kDecideBlock / 32 + 1];
+  __shared__ unsigned int s_maxlvl;
+  __shared__ long long s_err_spill;
+  const int tid = threadIdx.x;
+  const unsigned nt = ctrl->n_touched;
+  const long long nn = ctrl->num_nodes;
+  if (tid == 0) {
+    s_maxlvl = 0;
+    s_err_spill = -1;
+  }
+  // phase 1: decide
+  for (unsigned t = tid; t < nt; t += kDecideBlock) {
+    int nid = touched[t];
+    long long tot = nd.count[nid] + (long long)nd.pending[nid];
+    if (tot > geo.T && nd.level[nid] < geo.max_depth) {
+      atomicOr(&bitmap[nid >> 5], 1u << (nid & 31));
+    } else {
+      nd.final_[nid] = 1;
+    }
+  }
+  __syncthreads();
+  // phase 2: popcount prefix over bitmap words
+  const long long W = (nn + 31) / 32;
+  const long long per = (W + kDecideBlock - 1) / kDecideBlock;
+  const long long w0 = tid * per, w1 = min(W, w0 + per);
+  uint32_t local = 0;
+  for (long long w = w0; w < w1; ++w) local += __popc(__ldcg(bitmap + w));
+  uint32_t total;
+  uint32_t run = block_exclusive_scan<uint32_t, kDecideBlock>(local, sh32, total);
+  for (long long w = w0; w < w1; ++w) {
+    word_prefix[w] = run;
+    run += __popc(__ldcg(bitmap + w));
+  }
+  __syncthreads();
+  const unsigned ns = total;
+  // phase 3: rank splits, gather their counts
+  for (unsigned t = tid; t < nt; t += kDecideBlock) {
+    int nid = touched[t];
+    uint32_t wv = __ldcg(bitmap + (nid >> 5));
+    uint32_t bit = 1u << (nid & 31);
+    if (wv & bit) {
+      uint32_t rank = word_prefix[nid >> 5] + __popc(wv & (bit - 1));
+      split_list[rank] = nid;
+      scnt[rank] = nd.count[nid];
+      schk[rank] = nd.chunk_count[nid];
+      atomicMax(&s_maxlvl, (unsigned)(nd.level[nid] + 1));
+    }
+  }
+  __syncthreads();
+  // phase 4: exclusive scans over ranks (spill offsets, free-stack offsets)
+  const long long spill0 = ctrl->spill_total;
+  U64x2 carry = u64x2(0, 0);
+  for (unsigned base = 0; base < ns; base += kDecideBlock) {
+    unsigned r = base + tid;
+    U64x2 v = u64x2(0, 0);
+    if (r < ns) v = u64x2((unsigned long long)scnt[r], (unsigned long long)schk[r]);
+    U64x2 tot;
+    U64x2 ex = block_exclusive_scan<U64x2, kDecideBlock>(v, sh64, tot);
+    ex = ex + carry;
+    if (r < ns) {
+      spill_off[r] = (long long)ex.a;
+      chunk_off[r] = (long long)ex.b;
+      // SpillBuffer.append raises before the node's grid alloc (octree.py:231-244)
+      if (v.a > 0 && spill0 + (long long)(ex.a + v.a) > spill_cap)
+        atomicMin((unsigned long long *)&s_err_spill, (unsigned long long)r);
+    }
+    carry = carry + tot;
+    __syncthreads();
+  }
+  // phase 5: errors and counters (thread 0)
+  if (tid == 0) {
+    unsigned long long off = ctrl->arena_off;
+    const unsigned long long gb = (unsigned long long)geo.grid_bytes;
+    const unsigned long long g0 = (off + 63ull) / 64ull * 64ull;
+    const unsigned long long gstride = (gb + 63ull) / 64ull * 64ull;
+    long long err_ooa = -1;
+    if (ns > 0) {
+      // first k with g0 + k*gstride + gb > cap
+      if (g0 + gb > arena_cap) err_ooa = 0;
+      else if (g0 + (unsigned long long)(ns - 1) * gstride + gb > arena_cap)
+        err_ooa = (long long)((arena_cap - gb - g0) / gstride) + 1;
+    }
+    long long es = s_err_spill;
+    if (es >= 0 && (err_ooa < 0 || es <= err_ooa)) set_error(ctrl, 2 /*LOD_E_SPILL_OVERFLOW*/);
+    else if (err_ooa >= 0) set_error(ctrl, 1 /*LOD_E_OUT_OF_ARENA*/);
+    ctrl->n_splits = ns;
+    ctrl->spill_add = (long long)carry.a;
+    ctrl->plan_num_nodes0 = nn;
+    ctrl->plan_free0 = ctrl->free_count;
+    ctrl->plan_spill0 = spill0;
+    ctrl->plan_grid0 = g0;
+    ctrl->iter_max_level = s_maxlvl;
+    if (ctrl->error == 0 && ns > 0) {
+      ctrl->num_nodes = nn + 8ll * ns;
+      ctrl->splits_total += ns;
+      if ((long long)s_maxlvl > ctrl->max_level) ctrl->max_level = s_maxlvl;
+      ctrl->free_count += (long long)carry.b;
+      ctrl->released_total += (long long)carry.b;
+      ctrl->spill_total = spill0 + (long long)carry.a;
+      ctrl->arena_off = g0 + (unsigned long long)(ns - 1) * gstride + gb;
+    }
+  }
+  __syncthreads();
+  // phase 6: clear the split bitmap for the next iteration
+  for (unsigned t = tid; t < nt; t += kDecideBlock) {
+    int nid = touched[t];
+    bitmap[nid >> 5] = 0;
+  }
+}
+
+// Octree.split (octree.py:222-264) for every planned split, one CTA each:
+// gather stored samples in chunk-walk order into the spill segment, push the
+// chain onto the free stack in walk order (store.py:125-143), turn the node
+// inner with a zeroed grid (arena regions are zeroed and never reused) and
+// create its 8 children in octant order with bmin = base + half (f64).
+constexpr int kExecBlock = 256;
+__global__ void __launch_bounds__(kExecBlock)
+    k_execute(NodeCols nd, PoolCols pool, Geo geo, const uint8_t *__restrict__ arena,
+              const int32_t *__restrict__ split_list, const long long *__restrict__ spill_off,
+              const long long *__restrict__ chunk_off, float4 *spill_buf,
+              int32_t *spill_node_of, const Ctrl *ctrl) {
+  __shared__ int s_cid, s_next, s_occ;
+  __shared__ long long s_poff;
+  const int k = blockIdx.x, tid = threadIdx.x;
+  const int nid = split_list[k];
+  const long long sp = ctrl->plan_spill0 + spill_off[k];
+  float4 *dst = spill_buf + sp;
+  int32_t *dnode = spill_node_of + sp;
+  int32_t *fs = pool.free_stack + ctrl->plan_free0 + chunk_off[k];
+  if (tid == 0) s_cid = nd.chunk_head[nid];
+  __syncthreads();
+  long long idx = 0;
+  int ci = 0;
+  while (s_cid != LOD_NO_CHUNK) {
+    const int cid = s_cid;
+    if (tid == 0) {
+      s_next = pool.next[cid];
+      s_occ = pool.occupied[cid];
+      s_poff = pool.payload_off[cid];
+    }
+    __syncthreads();
+    const int occ = s_occ;
+    const float4 *src = reinterpret_cast<const float4 *>(arena + s_poff);
+    for (int r = tid; r < occ; r += kExecBlock) {
+      dst[idx + r] = src[r];
+      dnode[idx + r] = nid;
+    }
+    if (tid == 0) {
+      fs[ci] = cid;
+      pool.occupied[cid] = 0;
+      pool.next[cid] = LOD_NO_CHUNK;
+      pool.owner[cid] = -1;
+      s_cid = s_next;
+    }
+    idx += occ;
+    ci += 1;
+    __syncthreads();
+  }
+  const int lvl = nd.level[nid];
+  if (tid == 0) {
+    nd.count[nid] = 0;
+    nd.pending[nid] = 0;
+    nd.inner[nid] = 1;
+    nd.chunk_head[nid] = LOD_NO_CHUNK;
+    nd.chunk_tail[nid] = LOD_NO_CHUNK;
+    nd.chunk_count[nid] = 0;
+    const unsigned long long gstride = ((unsigned long long)geo.grid_bytes + 63ull) / 64ull * 64ull;
+    nd.grid_off[nid] = (long long)(ctrl->plan_grid0 + (unsigned long long)k * gstride);
+  }
+  if (tid < 8) {
+    const int o = tid;
+    const int c = (int)(ctrl->plan_num_nodes0 + 8ll * k + o);
+    // node_size(nid) * 0.5 == size * 0.5**level * 0.5 (octree.py:246, 268-269)
+    const double half = geo.size_by_level[lvl] * 0.5;
+    const double b0 = nd.bmin[3 * nid], b1 = nd.bmin[3 * nid + 1], b2 = nd.bmin[3 * nid + 2];
+    nd.parent[c] = nid;
+    nd.octant[c] = (uint8_t)o;
+    nd.level[c] = lvl + 1;
+    for (int q = 0; q < 8; ++q) nd.children[8 * c + q] = LOD_NO_NODE;
+    nd.inner[c] = 0;
+    nd.final_[c] = 0;
+    nd.count[c] = 0;
+    nd.pending[c] = 0;
+    nd.chunk_head[c] = LOD_NO_CHUNK;
+    nd.chunk_tail[c] = LOD_NO_CHUNK;
+    nd.chunk_count[c] = 0;
+    nd.grid_off[c] = -1;
+    nd.bmin[3 * c + 0] = b0 + ((o & 1) ? half : 0.0);
+    nd.bmin[3 * c + 1] = b1 + ((o & 2) ? half : 0.0);
+    nd.bmin[3 * c + 2] = b2 + ((o & 4) ? half : 0.0);
+    nd.children[8 * nid + o] = c;
+  }
+}
+
+// Move the batch part of the per-point node cache behind the spill segment:
+// all = [spill || batch] (update.py:281-286).
+__global__ void k_shift_nodes(const int32_t *__restrict__ src, int32_t *__restrict__ dst,
+                              long long n) {
+  for (long long i = gtid(); i < n; i += gstride()) dst[i] = src[i];
+}
+
+// ---------------------------------------------------------------- sampling
+
+__device__ __forceinline__ unsigned long long hmix(unsigned long long k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdULL;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ULL;
+  k ^= k >> 33;
+  return k;
+}
+constexpr unsigned long long kEmptyKey = 0xFFFFFFFFFFFFFFFFULL;
+
+struct Hash {
+  unsigned long long *keys;
+  uint32_t *vals;
+  unsigned long long mask;  // capacity - 1 (power of two)
+  unsigned long long *used; // slots inserted this cycle
+  unsigned long long used_cap;
+};
+
+// Min-index claim of (node, cell): the reference's sequential first-come rule
+// (sample_and_route, _kernels.py:125-135) is "lowest all-array index wins",
+// so every point whose cell bit was clear at cycle start min-combines its index.
+__device__ __forceinline__ void hash_claim(const Hash &h, unsigned long long key, uint32_t j,
+                                           Ctrl *ctrl) {
+  unsigned long long slot = hmix(key) & h.mask;
+  for (unsigned long long probe = 0; probe <= h.mask; ++probe) {
+    unsigned long long k = __ldcg(h.keys + slot);
+    if (k == key) {
+      atomicMin(h.vals + slot, j);
+      return;
+    }
+    if (k == kEmptyKey) {
+      unsigned long long prev = atomicCAS(h.keys + slot, kEmptyKey, key);
+      if (prev == kEmptyKey) {
+        atomicMin(h.vals + slot, j);
+        unsigned long long u = atomicAdd(&ctrl->n_used, 1ull);
+        if (u < h.used_cap) h.used[u] = slot;
+        else ctrl->hash_overflow = 1;
+        return;
+      }
+      if (prev == key) {
+        atomicMin(h.vals + slot, j);
+        return;
+      }
+    }
+    slot = (slot + 1) & h.mask;
+  }
+  ctrl->hash_overflow = 1;
+}
+
+__device__ __forceinline__ uint32_t hash_lookup(const Hash &h, unsigned long long key) {
+  unsigned long long slot = hmix(key) & h.mask;
+  for (unsigned long long probe = 0; probe <= h.mask; ++probe) {
+    unsigned long long k = __ldcg(h.keys + slot);
+    if (k == key) return __ldcg(h.vals + slot);
+    if (k == kEmptyKey) return 0xFFFFFFFFu;
+    slot = (slot + 1) & h.mask;
+  }
+  return 0xFFFFFFFFu;
+}
+
+// Pass 1 of sampling: descend from the root (topology is frozen); at each inner
+// node whose cell bit is clear (state at cycle start -- nothing sets bits in
+// this pass), min-claim (node, cell) with the point's all-array index.
+__global__ void k_claim(NodeCols nd, Geo geo, PointSrc src, const uint32_t *__restrict__ grid32,
+                        long long n, Hash h, Ctrl *ctrl) {
+  for (long long j = gtid(); j < n; j += gstride()) {
+    float xf, yf, zf;
+    src.xyz(j, xf, yf, zf);
+    const double x = xf, y = yf, z = zf;
+    double bx = geo.bmin0[0], by = geo.bmin0[1], bz = geo.bmin0[2], s = geo.size0;
+    int nid = 0;
+    while (nd.inner[nid]) {
+      long long cell = cell_of(geo, x, y, z, bx, by, bz, s);
+      const uint32_t *w = grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5);
+      if (!(*w & (1u << (cell & 31))))
+        hash_claim(h, ((unsigned long long)(uint32_t)nid << 32) | (unsigned long long)cell,
+                   (uint32_t)j, ctrl);
+      int o = octant_step(x, y, z, bx, by, bz, s);
+      nid = nd.children[8 * nid + o];
+    }
+  }
+}
+
+// Pass 2: the winner of each claimed cell sets its bit (atomicOr) and records
+// the win (node, cell) in path order.  A loser may observe the bit already set
+// by the winner and skip its lookup -- same outcome.
+__global__ void k_win(NodeCols nd, Geo geo, PointSrc src, uint32_t *grid32, long long n, Hash h,
+                      uint32_t *__restrict__ wcount, unsigned long long *__restrict__ wins,
+                      int D) {
+  for (long long j = gtid(); j < n; j += gstride()) {
+    float xf, yf, zf;
+    src.xyz(j, xf, yf, zf);
+    const double x = xf, y = yf, z = zf;
+    double bx = geo.bmin0[0], by = geo.bmin0[1], bz = geo.bmin0[2], s = geo.size0;
+    int nid = 0;
+    uint32_t k = 0;
+    while (nd.inner[nid]) {
+      long long cell = cell_of(geo, x, y, z, bx, by, bz, s);
+      uint32_t *w = grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5);
+      const uint32_t bit = 1u << (cell & 31);
+      if (!(__ldcg(w) & bit)) {
+        const unsigned long long key =
+            ((unsigned long long)(uint32_t)nid << 32) | (unsigned long long)cell;
+        if (hash_lookup(h, key) == (uint32_t)j) {
+          atomicOr(w, bit);
+          if (k < (uint32_t)D) wins[(long long)j * D + k] = key;
+          ++k;
+        }
+      }
+      int o = octant_step(x, y, z, bx, by, bz, s);
+      nid = nd.children[8 * nid + o];
+    }
+    wcount[j] = k;
+  }
+}
+
+// Backlog in the reference's order (sample_and_route appends per point, in
+// path order, _kernels.py:100-151): entry b = wbase[j] + k.
+__global__ void k_emit(long long n, const uint32_t *__restrict__ wcount,
+                       const uint32_t *__restrict__ wbase, const unsigned long long *__restrict__ wins,
+                       int D, PointSrc src, int32_t *__restrict__ bnode, uint32_t *__restrict__ bcell,
+                       uint32_t *__restrict__ brgba) {
+  for (long long j = gtid(); j < n; j += gstride()) {
+    uint32_t c = wcount[j];
+    if (!c) continue;
+    uint32_t b = wbase[j];
+    uint32_t col = src.rgba(j);
+    for (uint32_t k = 0; k < c; ++k) {
+      unsigned long long key = wins[j * D + k];
+      bnode[b + k] = (int32_t)(key >> 32);
+      bcell[b + k] = (uint32_t)(key & 0xFFFFFFFFu);
+      brgba[b + k] = col;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- sort + alloc
+
+// Items: points j in [0, n_all) keyed by their leaf, then backlog entries keyed
+// by their node.  Leaves and inner nodes are disjoint, so one stable sort by
+// node id yields every node's new samples in reference slot order.
+__global__ void k_keys(const int32_t *__restrict__ node_all, long long n_all,
+                       const int32_t *__restrict__ bnode, long long n_v, uint32_t *__restrict__ keys) {
+  const long long n = n_all + n_v;
+  for (long long i = gtid(); i < n; i += gstride())
+    keys[i] = (uint32_t)(i < n_all ? node_all[i] : bnode[i - n_all]);
+}
+
+__global__ void k_seg_flags(const uint32_t *__restrict__ skeys, long long n, uint32_t *__restrict__ flag) {
+  for (long long p = gtid(); p < n; p += gstride())
+    flag[p] = (p == 0 || skeys[p] != skeys[p - 1]) ? 1u : 0u;
+}
+
+__global__ void k_seg_list(const uint32_t *__restrict__ skeys, long long n,
+                           const uint32_t *__restrict__ hpos, int32_t *__restrict__ seg_node,
+                           long long *__restrict__ seg_start, const Ctrl *ctrl) {
+  for (long long p = gtid(); p < n; p += gstride()) {
+    if (p == 0 || skeys[p] != skeys[p - 1]) {
+      uint32_t d = hpos[p];
+      seg_node[d] = (int32_t)skeys[p];
+      seg_start[d] = p;
+    }
+  }
+  if (gtid() == 0) seg_start[ctrl->n_keys] = n;
+}
+
+__device__ __forceinline__ long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
+
+// collect_allocs (_kernels.py:253-277): need = ceil((count+pending)/C) -
+// chunk_count per touched node; here in ascending node id (chunk ids are not
+// observable; the acquisition count and arena growth are identical).
+__global__ void k_plan(NodeCols nd, Geo geo, const int32_t *__restrict__ seg_node,
+                       const long long *__restrict__ seg_start, const Ctrl *ctrl, U64x2 *__restrict__ plan) {
+  const long long K = (long long)ctrl->n_keys;
+  for (long long d = gtid(); d < K; d += gstride()) {
+    const int n = seg_node[d];
+    const long long len = seg_start[d + 1] - seg_start[d];
+    const long long cnt = nd.count[n];
+    const long long need = ceil_div(cnt + len, geo.C) - ceil_div(cnt, geo.C);
+    const long long partial = (cnt % geo.C) != 0;
+    plan[d] = u64x2((unsigned long long)need, (unsigned long long)(need + partial));
+  }
+}
+
+// ChunkPool.acquire in bulk (store.py:110-123): acquisitions pop the LIFO free
+// stack first, then cut fresh C*16-byte payloads from the arena (16-aligned).
+__global__ void k_alloc_begin(Ctrl *ctrl, Geo geo, unsigned long long arena_cap) {
+  const long long M = (long long)ctrl->acq_tot.a;
+  const long long F = ctrl->free_count;
+  const long long A = ctrl->allocated_total;
+  ctrl->alloc_F = F;
+  ctrl->alloc_A = A;
+  const long long fresh = M > F ? M - F : 0;
+  const unsigned long long pay = (unsigned long long)geo.C * 16ull;
+  unsigned long long base = ctrl->arena_off;
+  if (fresh > 0) base = (base + 15ull) / 16ull * 16ull;
+  ctrl->chunk_base = base;
+  if (fresh > 0 && base + (unsigned long long)fresh * pay > arena_cap) {
+    set_error(ctrl, 1 /*LOD_E_OUT_OF_ARENA*/);
+    return;
+  }
+  if (fresh > 0) ctrl->arena_off = base + (unsigned long long)fresh * pay;
+  ctrl->free_count = F - (M < F ? M : F);
+  ctrl->allocated_total = A + fresh;
+}
+
+__device__ __forceinline__ int acq_cid(const PoolCols &pool, const Ctrl *ctrl, long long a) {
+  return a < ctrl->alloc_F ? pool.free_stack[ctrl->alloc_F - 1 - a]
+                           : (int)(ctrl->alloc_A + (a - ctrl->alloc_F));
+}
+
+// Per touched node: link the new run after the old tail (Octree.append_chunk,
+// octree.py:328-337) and put the partially filled tail at the head of the
+// node's write list.
+__global__ void k_alloc_nodes(NodeCols nd, PoolCols pool, Geo geo, const int32_t *__restrict__ seg_node,
+                              const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
+                              const U64x2 *__restrict__ plan_ex, int32_t *__restrict__ wl, const Ctrl *ctrl) {
+  if (ctrl->error) return;
+  const long long K = (long long)ctrl->n_keys;
+  for (long long d = gtid(); d < K; d += gstride()) {
+    const int n = seg_node[d];
+    const long long len = seg_start[d + 1] - seg_start[d];
+    const long long cnt = nd.count[n];
+    const long long need = (long long)plan[d].a;
+    const long long A0 = (long long)plan_ex[d].a, W0 = (long long)plan_ex[d].b;
+    const int tail = nd.chunk_tail[n];
+    if (cnt % geo.C) {
+      wl[W0] = tail;
+      const long long ci = cnt / geo.C;  // tail chunk index in the node's list
+      const long long rem = cnt + len - ci * geo.C;
+      pool.occupied[tail] = (int)(rem < geo.C ? rem : geo.C);
+    }
+    if (need > 0) {
+      const int first = acq_cid(pool, ctrl, A0), last = acq_cid(pool, ctrl, A0 + need - 1);
+      if (tail != LOD_NO_CHUNK) pool.next[tail] = first;
+      else nd.chunk_head[n] = first;
+      nd.chunk_tail[n] = last;
+      nd.chunk_count[n] += (int)need;
+    }
+  }
+}
+
+// Per acquisition: payload offset for fresh chunks, in-run links, owner and
+// final occupancy, write-list slot.
+__global__ void k_alloc_chunks(NodeCols nd, PoolCols pool, Geo geo, const int32_t *__restrict__ seg_node,
+                               const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
+                               const U64x2 *__restrict__ plan_ex, int32_t *__restrict__ wl, const Ctrl *ctrl) {
+  if (ctrl->error) return;
+  const long long M = (long long)ctrl->acq_tot.a;
+  const long long K = (long long)ctrl->n_keys;
+  for (long long a = gtid(); a < M; a += gstride()) {
+    // segment d: last d with plan_ex[d].a <= a (and need > 0)
+    long long lo = 0, hi = K - 1;
+    while (lo < hi) {
+      long long mid = (lo + hi + 1) >> 1;
+      if ((long long)plan_ex[mid].a <= a) lo = mid;
+      else hi = mid - 1;
+    }
+    const long long d = lo;
+    const int n = seg_node[d];
+    const long long need = (long long)plan[d].a;
+    const long long t = a - (long long)plan_ex[d].a;
+    const long long cnt = nd.count[n];
+    const long long len = seg_start[d + 1] - seg_start[d];
+    const int cid = acq_cid(pool, ctrl, a);
+    if (a >= ctrl->alloc_F)
+      pool.payload_off[cid] =
+          (long long)(ctrl->chunk_base + (unsigned long long)(a - ctrl->alloc_F) * (unsigned long long)geo.C * 16ull);
+    pool.next[cid] = (t + 1 < need) ? acq_cid(pool, ctrl, a + 1) : LOD_NO_CHUNK;
+    pool.owner[cid] = n;
+    const long long ci = ceil_div(cnt, geo.C) + t;
+    const long long rem = cnt + len - ci * geo.C;
+    pool.occupied[cid] = (int)(rem < geo.C ? rem : geo.C);
+    const long long partial = (long long)plan[d].b - need;
+    wl[(long long)plan_ex[d].b + partial + t] = cid;
+  }
+}
+
+// store_points / store_voxels (_kernels.py:155-250): sorted position p of a
+// node's segment is its slot count[node] + rank; records are 16-byte
+// (f32 x,y,z | u32 rgba, store.py:14-16); voxel centres are
+// bmin + (c + 0.5) * (size_by_level[level] / g) in f64, then rounded to f32.
+__global__ void k_store(NodeCols nd, PoolCols pool, Geo geo, uint8_t *__restrict__ arena,
+                        const uint32_t *__restrict__ skeys, const uint32_t *__restrict__ svals,
+                        const uint32_t *__restrict__ hpos, const long long *__restrict__ seg_start,
+                        const U64x2 *__restrict__ plan, const U64x2 *__restrict__ plan_ex,
+                        const int32_t *__restrict__ wl, long long n_items, long long n_all, PointSrc src,
+                        const uint32_t *__restrict__ bcell, const uint32_t *__restrict__ brgba,
+                        const Ctrl *ctrl) {
+  if (ctrl->error) return;
+  for (long long p = gtid(); p < n_items; p += gstride()) {
+    const uint32_t key = skeys[p];
+    const int n = (int)key;
+    const bool head = (p == 0) || skeys[p - 1] != key;
+    const long long d = (long long)hpos[p] + (head ? 0 : -1);
+    const long long rank = p - seg_start[d];
+    const long long cnt = nd.count[n];
+    const long long slot = cnt + rank;
+    const long long rel = slot / geo.C - cnt / geo.C;
+    const int cid = wl[(long long)plan_ex[d].b + rel];
+    const long long off = slot % geo.C;
+    const long long i = svals[p];
+    float4 rec;
+    if (i < n_all) {
+      rec = src.record(i);
+    } else {
+      const long long b = i - n_all;
+      const long long cell = bcell[b];
+      const long long g = geo.g;
+      const long long cx = cell % g, cy = (cell / g) % g, cz = cell / (g * g);
+      const double step = geo.size_by_level[nd.level[n]] / (double)g;
+      const double x = nd.bmin[3 * n] + ((double)cx + 0.5) * step;
+      const double y = nd.bmin[3 * n + 1] + ((double)cy + 0.5) * step;
+      const double z = nd.bmin[3 * n + 2] + ((double)cz + 0.5) * step;
+      rec = make_float4(__double2float_rn(x), __double2float_rn(y), __double2float_rn(z),
+                        __uint_as_float(brgba[b]));
+    }
+    float4 *dst = reinterpret_cast<float4 *>(arena + pool.payload_off[cid]) + off;
+    *dst = rec;
+  }
+}
+
+// clear_marks (_kernels.py:280-287) + count advance: pending drains into count.
+__global__ void k_epilogue(NodeCols nd, const int32_t *__restrict__ seg_node,
+                           const long long *__restrict__ seg_start, const Ctrl *ctrl) {
+  if (ctrl->error) return;
+  const long long K = (long long)ctrl->n_keys;
+  for (long long d = gtid(); d < K; d += gstride()) {
+    const int n = seg_node[d];
+    nd.count[n] += seg_start[d + 1] - seg_start[d];
+    nd.pending[n] = 0;
+    nd.final_[n] = 0;
+  }
+}
+
+__global__ void k_hash_clear(Hash h, const Ctrl *ctrl) {
+  unsigned long long nu = ctrl->n_used;
+  if (nu > h.used_cap) nu = h.used_cap;
+  for (long long u = gtid(); u < (long long)nu; u += gstride()) {
+    unsigned long long s = h.used[u];
+    h.keys[s] = kEmptyKey;
+    h.vals[s] = 0xFFFFFFFFu;
+  }
+}
+
+// Safety net after a fatal error: pending/final of every node back to zero.
+__global__ void k_clear_marks_all(NodeCols nd, long long n) {
+  for (long long i = gtid(); i < n; i += gstride()) {
+    nd.pending[i] = 0;
+    nd.final_[i] = 0;
+  }
+}
+
+}  // namespace lod

@@ -1,0 +1,259 @@
+// lod_raster.cu -- compute rasterizers (render.rasterize / brute_force_render).
+//
+// Projection, depth and packing restate _kernels.py:290-372 exactly (f64, no
+// FMA, IEEE division, float32 depth bits << 32 | rgba, min-combine).  The
+// per-node chunk walk of rasterize_nodes becomes a flat pass over the chunk
+// table: each warp takes one chunk, skips it unless its owning node is in the
+// visible set, and splats its occupied records with an early depth test before
+// the 64-bit atomicMin.  Chunk ownership is maintained by the update path.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/lod_b200.h"
+#include "lod_common.cuh"
+
+using namespace lod;
+
+struct LodTree;
+cudaStream_t lod_tree_stream(LodTree *t);
+int lod_tree_device(LodTree *t);
+const uint8_t *lod_tree_arena(LodTree *t);
+PoolCols lod_tree_pool(LodTree *t);
+long long lod_tree_allocated(LodTree *t);
+long long lod_tree_num_nodes(LodTree *t);
+uint32_t *lod_tree_visflag(LodTree *t);
+int lod_tree_ensure_vislist(LodTree *t, long long n, int32_t **p);
+int lod_tree_ensure_fb(LodTree *t, long long n, unsigned long long **p);
+unsigned long long *lod_tree_counter(LodTree *t);
+
+namespace {
+
+struct Cam {
+  double c[18];
+};
+
+__device__ __forceinline__ void splat(const Cam &cam, long long w, long long h, double x, double y, double z,
+                                      uint32_t rgba, unsigned long long *fb) {
+  const double *c = cam.c;
+  const double dx = x - c[0], dy = y - c[1], dz = z - c[2];
+  const double zv = dx * c[9] + dy * c[10] + dz * c[11];
+  if (zv <= c[14] || zv >= c[15]) return;
+  const double xv = dx * c[3] + dy * c[4] + dz * c[5];
+  const double yv = dx * c[6] + dy * c[7] + dz * c[8];
+  const double ndc_x = xv / (zv * c[12] * c[13]);
+  const double ndc_y = yv / (zv * c[12]);
+  const long long px = f2i64(floor((ndc_x + 1.0) * 0.5 * c[16]));
+  const long long py = f2i64(floor((1.0 - ndc_y) * 0.5 * c[17]));
+  if (px < 0 || px >= w || py < 0 || py >= h) return;
+  const double d01 = c[15] * (zv - c[14]) / ((c[15] - c[14]) * zv);
+  const unsigned long long packed =
+      ((unsigned long long)__float_as_uint(__double2float_rn(d01)) << 32) | (unsigned long long)rgba;
+  unsigned long long *cell = fb + (py * w + px);
+  if (packed < __ldcg(cell)) atomicMin(cell, packed);
+}
+
+__global__ void k_raster_points(const float *__restrict__ xyz, const uint32_t *__restrict__ rgba, long long n,
+                                Cam cam, unsigned long long *fb, long long w, long long h) {
+  for (long long i = gtid(); i < n; i += gstride())
+    splat(cam, w, h, (double)__ldg(xyz + 3 * i), (double)__ldg(xyz + 3 * i + 1), (double)__ldg(xyz + 3 * i + 2),
+          __ldg(rgba + i), fb);
+}
+
+// One warp per chunk; visflag holds each node's multiplicity in the visible
+// list (samples_drawn counts every listed occurrence, _kernels.py:307-317).
+__global__ void k_raster_chunks(PoolCols pool, const uint8_t *__restrict__ arena, long long nchunks,
+                                const uint32_t *__restrict__ visflag, Cam cam, unsigned long long *fb,
+                                long long w, long long h, unsigned long long *samples) {
+  const long long warp = gtid() >> 5, nwarps = gstride() >> 5;
+  const int lane = threadIdx.x & 31;
+  unsigned long long drawn = 0;
+  for (long long cid = warp; cid < nchunks; cid += nwarps) {
+    const int owner = pool.owner[cid];
+    if (owner < 0) continue;
+    const uint32_t mult = visflag[owner];
+    if (!mult) continue;
+    const int occ = pool.occupied[cid];
+    drawn += (unsigned long long)occ * mult;
+    const float4 *rec = reinterpret_cast<const float4 *>(arena + pool.payload_off[cid]);
+    for (int r = lane; r < occ; r += 32) {
+      const float4 v = __ldg(rec + r);
+      splat(cam, w, h, (double)v.x, (double)v.y, (double)v.z, __float_as_uint(v.w), fb);
+    }
+  }
+  if (lane == 0 && drawn) atomicAdd(samples, drawn);
+}
+
+__global__ void k_set_vis(const int32_t *__restrict__ vis, long long n, uint32_t *visflag, int add) {
+  for (long long i = gtid(); i < n; i += gstride()) {
+    if (add) atomicAdd(visflag + vis[i], 1u);
+    else visflag[vis[i]] = 0;
+  }
+}
+
+__global__ void k_fill_u64(unsigned long long *p, long long n, unsigned long long v) {
+  for (long long i = gtid(); i < n; i += gstride()) p[i] = v;
+}
+
+inline unsigned grid_for(long long n, int block = 256) {
+  long long b = (n + block - 1) / block;
+  if (b < 1) b = 1;
+  return (unsigned)std::min<long long>(b, 148LL * 16);
+}
+
+int cuda_rc(cudaError_t e) {
+  if (e == cudaSuccess) return LOD_OK;
+  fprintf(stderr, "[lod_b200] CUDA error: %s\n", cudaGetErrorString(e));
+  return LOD_E_CUDA;
+}
+#define CK(expr)               \
+  do {                         \
+    int rc__ = cuda_rc(expr);  \
+    if (rc__) return rc__;     \
+  } while (0)
+
+// Per-device scratch for tree-less brute-force renders.
+struct DevScratch {
+  cudaStream_t st = nullptr;
+  float *xyz = nullptr;
+  uint32_t *rgba = nullptr;
+  unsigned long long *fb = nullptr;
+  long long ncap = 0, fcap = 0;
+};
+std::mutex g_mu;
+DevScratch g_dev[64];
+
+}  // namespace
+
+extern "C" {
+
+int lod_rasterize(LodTree *t, const int32_t *vis, int64_t nvis, const double *cam, uint64_t *fb,
+                  int64_t width, int64_t height, int flags, int64_t *samples) {
+  if (!t || !cam || !fb || width <= 0 || height <= 0 || nvis < 0 || (nvis > 0 && !vis)) return LOD_E_ARG;
+  cudaSetDevice(lod_tree_device(t));
+  cudaStream_t st = lod_tree_stream(t);
+  const long long nn = lod_tree_num_nodes(t);
+  for (int64_t i = 0; i < nvis; ++i)
+    if (vis[i] < 0 || vis[i] >= nn) return LOD_E_ARG;
+  Cam c;
+  memcpy(c.c, cam, sizeof(c.c));
+  const long long npx = width * height;
+  unsigned long long *dfb = reinterpret_cast<unsigned long long *>(fb);
+  if (!(flags & LOD_FLAG_DEVICE_FB)) {
+    int rc = lod_tree_ensure_fb(t, npx, &dfb);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(dfb, fb, npx * 8, cudaMemcpyHostToDevice, st));
+  }
+  int32_t *dvis = nullptr;
+  int rc = lod_tree_ensure_vislist(t, nvis, &dvis);
+  if (rc) return rc;
+  if (nvis) CK(cudaMemcpyAsync(dvis, vis, nvis * 4, cudaMemcpyHostToDevice, st));
+  unsigned long long *cnt = lod_tree_counter(t);
+  CK(cudaMemsetAsync(cnt, 0, 8, st));
+  uint32_t *vf = lod_tree_visflag(t);
+  const long long nchunks = lod_tree_allocated(t);
+  if (nvis) {
+    k_set_vis<<<grid_for(nvis), 256, 0, st>>>(dvis, nvis, vf, 1); ++lod::g_launches;
+    k_raster_chunks<<<grid_for(nchunks * 32), 256, 0, st>>>(lod_tree_pool(t), lod_tree_arena(t), nchunks, vf, c,
+                                                             dfb, width, height, cnt); ++lod::g_launches;
+    k_set_vis<<<grid_for(nvis), 256, 0, st>>>(dvis, nvis, vf, 0); ++lod::g_launches;
+  }
+  unsigned long long drawn = 0;
+  CK(cudaMemcpyAsync(&drawn, cnt, 8, cudaMemcpyDeviceToHost, st));
+  if (!(flags & LOD_FLAG_DEVICE_FB)) CK(cudaMemcpyAsync(fb, dfb, npx * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (samples) *samples = (int64_t)drawn;
+  return LOD_OK;
+}
+
+int lod_raster_points(int32_t device, const float *xyz, const uint32_t *rgba, int64_t n, const double *cam,
+                      uint64_t *fb, int64_t width, int64_t height, int flags) {
+  if (!cam || !fb || width <= 0 || height <= 0 || n < 0 || (n > 0 && (!xyz || !rgba)) || device < 0 ||
+      device >= 64)
+    return LOD_E_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev) {
+    cudaGetLastError();
+    return LOD_E_NO_DEVICE;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaSetDevice(device);
+  DevScratch &s = g_dev[device];
+  if (!s.st) CK(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+  Cam c;
+  memcpy(c.c, cam, sizeof(c.c));
+  const long long npx = width * height;
+  const float *dx = xyz;
+  const uint32_t *dc = rgba;
+  if (!(flags & LOD_FLAG_DEVICE_INPUT) && n > 0) {
+    if (n > s.ncap) {
+      if (s.xyz) cudaFree(s.xyz);
+      if (s.rgba) cudaFree(s.rgba);
+      long long nc = std::max<long long>(n, 2 * s.ncap);
+      CK(cudaMalloc(&s.xyz, nc * 12));
+      CK(cudaMalloc(&s.rgba, nc * 4));
+      s.ncap = nc;
+    }
+    CK(cudaMemcpyAsync(s.xyz, xyz, n * 12, cudaMemcpyHostToDevice, s.st));
+    CK(cudaMemcpyAsync(s.rgba, rgba, n * 4, cudaMemcpyHostToDevice, s.st));
+    dx = s.xyz;
+    dc = s.rgba;
+  }
+  unsigned long long *dfb = reinterpret_cast<unsigned long long *>(fb);
+  if (!(flags & LOD_FLAG_DEVICE_FB)) {
+    if (npx > s.fcap) {
+      if (s.fb) cudaFree(s.fb);
+      CK(cudaMalloc(&s.fb, npx * 8));
+      s.fcap = npx;
+    }
+    dfb = s.fb;
+    CK(cudaMemcpyAsync(dfb, fb, npx * 8, cudaMemcpyHostToDevice, s.st));
+  }
+  if (n > 0) k_raster_points<<<grid_for(n), 256, 0, s.st>>>(dx, dc, n, c, dfb, width, height); ++lod::g_launches;
+  if (!(flags & LOD_FLAG_DEVICE_FB)) CK(cudaMemcpyAsync(fb, dfb, npx * 8, cudaMemcpyDeviceToHost, s.st));
+  CK(cudaStreamSynchronize(s.st));
+  return LOD_OK;
+}
+
+int lod_device_alloc(int32_t device, uint64_t bytes, void **ptr) {
+  if (!ptr) return LOD_E_ARG;
+  cudaSetDevice(device);
+  if (cudaMalloc(ptr, bytes ? bytes : 1) != cudaSuccess) {
+    cudaGetLastError();
+    return LOD_E_NOMEM;
+  }
+  return LOD_OK;
+}
+int lod_device_free(void *ptr) { return cuda_rc(cudaFree(ptr)); }
+int lod_memcpy_h2d(void *dst, const void *src, uint64_t bytes) {
+  return cuda_rc(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+}
+int lod_memcpy_d2h(void *dst, const void *src, uint64_t bytes) {
+  return cuda_rc(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+}
+int lod_host_alloc(uint64_t bytes, void **ptr) {
+  if (!ptr) return LOD_E_ARG;
+  if (cudaMallocHost(ptr, bytes ? bytes : 1) != cudaSuccess) {
+    cudaGetLastError();
+    return LOD_E_NOMEM;
+  }
+  return LOD_OK;
+}
+int lod_host_free(void *ptr) { return cuda_rc(cudaFreeHost(ptr)); }
+int lod_fb_fill(int32_t device, uint64_t *fb_dev, int64_t n, uint64_t value) {
+  cudaSetDevice(device);
+  k_fill_u64<<<grid_for(n), 256>>>(reinterpret_cast<unsigned long long *>(fb_dev), n, value); ++lod::g_launches;
+  return cuda_rc(cudaDeviceSynchronize());
+}
+int lod_l2_flush(int32_t device) {
+  static void *buf[64] = {};
+  const size_t bytes = 256ull << 20;  // 2x the 126 MB L2
+  cudaSetDevice(device);
+  if (!buf[device] && cudaMalloc(&buf[device], bytes) != cudaSuccess) return LOD_E_NOMEM;
+  CK(cudaMemset(buf[device], device & 0xFF, bytes));
+  return cuda_rc(cudaDeviceSynchronize());
+}
+
+}  // extern "C"

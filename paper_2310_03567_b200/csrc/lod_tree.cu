@@ -1,0 +1,772 @@
+// lod_tree.cu -- host orchestration of the B200 update cycle + the C ABI.
+//
+// One LodTree owns all device state of one octree (node table, chunk pool,
+// arena, per-cycle scratch) and one CUDA stream.  lod_insert_batch replaces
+// lodstream.update.insert_batch (update.py:252-393); see lod_kernels.cuh for
+// the per-pass kernels and DESIGN.md for the data layout.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/lod_b200.h"
+#include "lod_common.cuh"
+#include "lod_kernels.cuh"
+#include "radix.cuh"
+#include "scan.cuh"
+
+using namespace lod;
+
+namespace {
+
+template <typename T>
+struct DBuf {
+  T *p = nullptr;
+  long long cap = 0;
+  // Grow to hold n elements; keep the first `keep` elements when growing.
+  int ensure(long long n, cudaStream_t st, long long keep = 0) {
+    if (n <= cap) return 0;
+    long long nc = std::max<long long>(n, std::max<long long>(2 * cap, 1024));
+    T *q = nullptr;
+    if (cudaMalloc(&q, (size_t)nc * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();
+      return LOD_E_NOMEM;
+    }
+    if (p) {
+      if (keep > 0) cudaMemcpyAsync(q, p, (size_t)std::min(keep, cap) * sizeof(T), cudaMemcpyDeviceToDevice, st);
+      cudaStreamSynchronize(st);
+      cudaFree(p);
+    }
+    p = q;
+    cap = nc;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+inline unsigned grid_for(long long n, int block = 256) {
+  long long b = (n + block - 1) / block;
+  if (b < 1) b = 1;
+  long long cap = 148LL * 16;
+  return (unsigned)std::min(b, cap);
+}
+
+inline unsigned long long next_pow2(unsigned long long v) {
+  unsigned long long p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+}  // namespace
+
+__global__ void k_init_root(NodeCols nd, double b0, double b1, double b2) {
+  nd.parent[0] = LOD_NO_NODE;
+  nd.octant[0] = 0;
+  nd.level[0] = 0;
+  for (int q = 0; q < 8; ++q) nd.children[q] = LOD_NO_NODE;
+  nd.inner[0] = 0;
+  nd.final_[0] = 0;
+  nd.count[0] = 0;
+  nd.pending[0] = 0;
+  nd.chunk_head[0] = LOD_NO_CHUNK;
+  nd.chunk_tail[0] = LOD_NO_CHUNK;
+  nd.chunk_count[0] = 0;
+  nd.grid_off[0] = -1;
+  nd.bmin[0] = b0;
+  nd.bmin[1] = b1;
+  nd.bmin[2] = b2;
+}
+
+__global__ void k_cycle_begin(Ctrl *c) {
+  c->n_touched = 0;
+  c->n_splits = 0;
+  c->error = 0;
+  c->spill_total = 0;
+  c->spill_add = 0;
+  c->n_used = 0;
+  c->hash_overflow = 0;
+  c->n_v = 0;
+  c->n_keys = 0;
+  c->acq_tot = u64x2(0, 0);
+}
+
+__global__ void k_reset_touched(Ctrl *c) { c->n_touched = 0; }
+
+// Walk one node's chunk list into a packed record buffer (gather_samples,
+// octree.py:298-326).  One CTA per listed node.
+__global__ void k_gather_nodes(NodeCols nd, PoolCols pool, Geo geo, const uint8_t *__restrict__ arena,
+                               const int32_t *__restrict__ nodes, const long long *__restrict__ starts,
+                               const long long *__restrict__ out_off, float4 *__restrict__ out) {
+  __shared__ int s_cid, s_occ;
+  __shared__ long long s_poff;
+  const int nid = nodes[blockIdx.x];
+  const long long start = starts ? starts[blockIdx.x] : 0;
+  float4 *dst = out + out_off[blockIdx.x];
+  if (threadIdx.x == 0) s_cid = nd.chunk_head[nid];
+  __syncthreads();
+  long long pos = 0;  // index of the first record of the current chunk
+  while (s_cid != LOD_NO_CHUNK) {
+    if (threadIdx.x == 0) {
+      s_occ = pool.occupied[s_cid];
+      s_poff = pool.payload_off[s_cid];
+    }
+    __syncthreads();
+    const int occ = s_occ;
+    const float4 *src = reinterpret_cast<const float4 *>(arena + s_poff);
+    for (int r = threadIdx.x; r < occ; r += blockDim.x)
+      if (pos + r >= start) dst[pos + r - start] = src[r];
+    pos += occ;
+    __syncthreads();
+    if (threadIdx.x == 0) s_cid = pool.next[s_cid];
+    __syncthreads();
+  }
+}
+
+struct LodTree {
+  LodParams p{};
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  Geo geo{};
+  unsigned long long arena_cap = 0;
+  uint8_t *arena = nullptr;
+  long long ncap = 0;
+  NodeCols nd{};
+  long long ccap = 0;
+  PoolCols pool{};
+  Ctrl *d_ctrl = nullptr;
+  Ctrl *h_ctrl = nullptr;
+  // expansion scratch
+  DBuf<int32_t> touched, split_list, node_b, node_all;
+  DBuf<uint32_t> bitmap, word_prefix;
+  DBuf<long long> scnt, schk, spill_off, chunk_off;
+  DBuf<float4> spill;
+  // sampling scratch
+  DBuf<unsigned long long> hkeys, hused, wins;
+  DBuf<uint32_t> hvals, wcount, wbase;
+  unsigned long long hcap = 0;
+  DBuf<int32_t> bnode;
+  DBuf<uint32_t> bcell, brgba;
+  // sort / alloc scratch
+  DBuf<uint32_t> keys, keys_b, vals_a, vals_b, hist, flags, hpos, scan_u32;
+  DBuf<int32_t> seg_node, wl;
+  DBuf<long long> seg_start;
+  DBuf<U64x2> plan, plan_ex, scan_u64x2;
+  // inputs / outputs
+  DBuf<float> in_xyz;
+  DBuf<uint32_t> in_rgba;
+  DBuf<float4> gbuf;
+  DBuf<int32_t> gnodes;
+  DBuf<long long> goff, gstart;
+  DBuf<uint32_t> visflag;
+  DBuf<int32_t> vislist;
+  DBuf<unsigned long long> fb;
+  DBuf<unsigned long long> counter;
+  cudaEvent_t ev[12] = {};
+  // host copies of counters (authoritative after every call)
+  long long num_nodes = 1;
+  long long d2h_bytes = 0;  // control-block readbacks since the last reset
+};
+
+// ---------------------------------------------------------------- helpers
+
+static int cuda_rc(cudaError_t e) {
+  if (e == cudaSuccess) return LOD_OK;
+  fprintf(stderr, "[lod_b200] CUDA error: %s\n", cudaGetErrorString(e));
+  return LOD_E_CUDA;
+}
+
+#define CK(expr)                             \
+  do {                                       \
+    int rc__ = cuda_rc(expr);                \
+    if (rc__) return rc__;                   \
+  } while (0)
+#define RK(expr)                             \
+  do {                                       \
+    int rc__ = (expr);                       \
+    if (rc__) return rc__;                   \
+  } while (0)
+
+static int sync_ctrl(LodTree *t) {
+  t->d2h_bytes += (long long)sizeof(Ctrl);
+  CK(cudaMemcpyAsync(t->h_ctrl, t->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  return LOD_OK;
+}
+
+template <typename T>
+static int grow_col(T *&ptr, long long old_cap, long long new_cap, long long keep, cudaStream_t st) {
+  T *q = nullptr;
+  if (cudaMalloc(&q, (size_t)new_cap * sizeof(T)) != cudaSuccess) {
+    cudaGetLastError();
+    return LOD_E_NOMEM;
+  }
+  if (ptr && keep > 0) CK(cudaMemcpyAsync(q, ptr, (size_t)keep * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  if (ptr) cudaFree(ptr);
+  ptr = q;
+  (void)old_cap;
+  return LOD_OK;
+}
+
+// Node table capacity (Octree._grow doubling, octree.py:192-209).
+static int ensure_nodes(LodTree *t, long long want, long long live) {
+  if (want <= t->ncap) return LOD_OK;
+  long long nc = std::max<long long>(t->ncap, 1024);
+  while (nc < want) nc *= 2;
+  cudaStream_t st = t->st;
+  RK(grow_col(t->nd.parent, t->ncap, nc, live, st));
+  RK(grow_col(t->nd.octant, t->ncap, nc, live, st));
+  RK(grow_col(t->nd.level, t->ncap, nc, live, st));
+  RK(grow_col(t->nd.children, t->ncap * 8, nc * 8, live * 8, st));
+  RK(grow_col(t->nd.inner, t->ncap, nc, live, st));
+  RK(grow_col(t->nd.final_, t->ncap, nc, live, st));
+  RK(grow_col(t->nd.count, t->ncap, nc, live, st));
+  RK(grow_col(t->nd.pending, t->ncap, nc, live, st));
+  RK(grow_col(t->nd.chunk_head, t->ncap, nc, live, st));
+  RK(grow_col(t->nd.chunk_tail, t->ncap, nc, live, st));
+  RK(grow_col(t->nd.chunk_count, t->ncap, nc, live, st));
+  RK(grow_col(t->nd.grid_off, t->ncap, nc, live, st));
+  RK(grow_col(t->nd.bmin, t->ncap * 3, nc * 3, live * 3, st));
+  // node-indexed scratch
+  long long words = (nc + 31) / 32 + 1;
+  long long oldw = t->bitmap.cap;
+  RK(t->bitmap.ensure(words, st, oldw));
+  if (t->bitmap.cap > oldw) CK(cudaMemsetAsync(t->bitmap.p + oldw, 0, (size_t)(t->bitmap.cap - oldw) * 4, st));
+  RK(t->word_prefix.ensure(words, st));
+  // the split plan of the running iteration survives the growth (k_execute reads it)
+  RK(t->touched.ensure(nc, st));
+  RK(t->split_list.ensure(nc, st, t->split_list.cap));
+  RK(t->scnt.ensure(nc, st));
+  RK(t->schk.ensure(nc, st));
+  RK(t->spill_off.ensure(nc, st, t->spill_off.cap));
+  RK(t->chunk_off.ensure(nc, st, t->chunk_off.cap));
+  long long oldv = t->visflag.cap;
+  RK(t->visflag.ensure(nc, st, oldv));
+  if (t->visflag.cap > oldv) CK(cudaMemsetAsync(t->visflag.p + oldv, 0, (size_t)(t->visflag.cap - oldv) * 4, st));
+  t->ncap = nc;
+  return LOD_OK;
+}
+
+// Chunk pool row capacity (ChunkPool._grow, store.py:104-108).
+static int ensure_chunks(LodTree *t, long long want, long long live) {
+  if (want <= t->ccap) return LOD_OK;
+  long long nc = std::max<long long>(t->ccap, 1024);
+  while (nc < want) nc *= 2;
+  cudaStream_t st = t->st;
+  RK(grow_col(t->pool.next, t->ccap, nc, live, st));
+  RK(grow_col(t->pool.payload_off, t->ccap, nc, live, st));
+  RK(grow_col(t->pool.occupied, t->ccap, nc, live, st));
+  RK(grow_col(t->pool.owner, t->ccap, nc, live, st));
+  RK(grow_col(t->pool.free_stack, t->ccap, nc, live, st));
+  t->ccap = nc;
+  return LOD_OK;
+}
+
+static void fill_stats(LodTree *t, LodBatchStats *s) {
+  const Ctrl &c = *t->h_ctrl;
+  s->num_nodes = c.num_nodes;
+  s->splits_total = c.splits_total;
+  s->max_level = c.max_level;
+  s->allocated_total = c.allocated_total;
+  s->free_count = c.free_count;
+  s->released_total = c.released_total;
+  s->arena_offset = c.arena_off;
+}
+
+// After a fatal error: drop per-cycle marks and the claim table so the
+// structure stays walkable (the reference leaves partial state, errors.py:1-5).
+static int abort_cycle(LodTree *t, int code) {
+  k_clear_marks_all<<<grid_for(t->num_nodes), 256, 0, t->st>>>(t->nd, t->num_nodes); ++lod::g_launches;
+  if (t->hkeys.p) {
+    cudaMemsetAsync(t->hkeys.p, 0xFF, (size_t)t->hcap * 8, t->st);
+    cudaMemsetAsync(t->hvals.p, 0xFF, (size_t)t->hcap * 4, t->st);
+  }
+  long long words = (t->ncap + 31) / 32 + 1;
+  cudaMemsetAsync(t->bitmap.p, 0, (size_t)words * 4, t->st);
+  cudaStreamSynchronize(t->st);
+  // counters: the device ctrl keeps whatever was applied before the failure
+  sync_ctrl(t);
+  t->num_nodes = t->h_ctrl->num_nodes;
+  return code;
+}
+
+// ---------------------------------------------------------------- C ABI
+
+extern "C" {
+
+const char *lod_strerror(int code) {
+  switch (code) {
+    case LOD_OK: return "ok";
+    case LOD_E_OUT_OF_ARENA: return "arena exhausted";
+    case LOD_E_SPILL_OVERFLOW: return "spill buffer past capacity";
+    case LOD_E_BACKLOG_OVERFLOW: return "voxel backlog past capacity";
+    case LOD_E_CUDA: return "CUDA error";
+    case LOD_E_ARG: return "bad argument";
+    case LOD_E_NOMEM: return "device out of memory";
+    case LOD_E_NO_DEVICE: return "no CUDA device";
+    default: return "unknown";
+  }
+}
+
+int lod_device_count(int *count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  *count = n;
+  return n > 0 ? LOD_OK : LOD_E_NO_DEVICE;
+}
+
+int lod_tree_create(const LodParams *params, LodTree **out) {
+  if (!params || !out) return LOD_E_ARG;
+  const LodParams &p = *params;
+  if (p.grid_res < 2 || (p.grid_res & 1) || p.chunk_capacity <= 0 || p.arena_bytes == 0 ||
+      p.max_depth < 0 || p.max_depth > 60 || p.grid_res > 1024)
+    return LOD_E_ARG;
+  int ndev = 0;
+  if (lod_device_count(&ndev) != LOD_OK || p.device >= ndev) return LOD_E_NO_DEVICE;
+  LodTree *t = new LodTree();
+  t->p = p;
+  t->dev = p.device;
+  cudaSetDevice(t->dev);
+  CK(cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking));
+  for (auto &e : t->ev) CK(cudaEventCreate(&e));
+  Geo &g = t->geo;
+  for (int k = 0; k < 3; ++k) g.bmin0[k] = p.bmin[k];
+  g.size0 = p.size;
+  for (int k = 0; k < 64; ++k) g.size_by_level[k] = p.size * std::pow(0.5, (double)k);
+  g.g = (int)p.grid_res;
+  g.grid_bytes = p.grid_res * p.grid_res * p.grid_res / 8;
+  g.T = p.leaf_threshold;
+  g.max_depth = (int)p.max_depth;
+  g.C = p.chunk_capacity;
+  t->arena_cap = (p.arena_bytes + 15ull) / 16ull * 16ull;  // store.py:41-42
+  if (cudaMalloc(&t->arena, t->arena_cap) != cudaSuccess) {
+    cudaGetLastError();
+    delete t;
+    return LOD_E_NOMEM;
+  }
+  CK(cudaMemsetAsync(t->arena, 0, t->arena_cap, t->st));
+  RK(ensure_nodes(t, 1024, 0));
+  RK(ensure_chunks(t, 1024, 0));
+  CK(cudaMalloc(&t->d_ctrl, sizeof(Ctrl)));
+  CK(cudaMallocHost(&t->h_ctrl, sizeof(Ctrl)));
+  CK(cudaMemsetAsync(t->d_ctrl, 0, sizeof(Ctrl), t->st));
+  memset(t->h_ctrl, 0, sizeof(Ctrl));
+  k_init_root<<<1, 1, 0, t->st>>>(t->nd, p.bmin[0], p.bmin[1], p.bmin[2]); ++lod::g_launches;
+  Ctrl c0{};
+  c0.num_nodes = 1;
+  CK(cudaMemcpyAsync(t->d_ctrl, &c0, sizeof(Ctrl), cudaMemcpyHostToDevice, t->st));
+  RK(t->counter.ensure(4, t->st));
+  RK(sync_ctrl(t));
+  t->num_nodes = 1;
+  *out = t;
+  return LOD_OK;
+}
+
+int lod_tree_destroy(LodTree *t) {
+  if (!t) return LOD_OK;
+  cudaSetDevice(t->dev);
+  cudaStreamSynchronize(t->st);
+  auto f = [](void *q) { if (q) cudaFree(q); };
+  f(t->arena);
+  f(t->nd.parent); f(t->nd.octant); f(t->nd.level); f(t->nd.children); f(t->nd.inner);
+  f(t->nd.final_); f(t->nd.count); f(t->nd.pending); f(t->nd.chunk_head); f(t->nd.chunk_tail);
+  f(t->nd.chunk_count); f(t->nd.grid_off); f(t->nd.bmin);
+  f(t->pool.next); f(t->pool.payload_off); f(t->pool.occupied); f(t->pool.owner); f(t->pool.free_stack);
+  f(t->d_ctrl);
+  if (t->h_ctrl) cudaFreeHost(t->h_ctrl);
+  t->touched.release(); t->split_list.release(); t->node_b.release(); t->node_all.release();
+  t->bitmap.release(); t->word_prefix.release(); t->scnt.release(); t->schk.release();
+  t->spill_off.release(); t->chunk_off.release(); t->spill.release(); t->hkeys.release();
+  t->hused.release(); t->wins.release(); t->hvals.release(); t->wcount.release(); t->wbase.release();
+  t->bnode.release(); t->bcell.release(); t->brgba.release(); t->keys.release(); t->keys_b.release();
+  t->vals_a.release(); t->vals_b.release(); t->hist.release(); t->flags.release(); t->hpos.release();
+  t->scan_u32.release(); t->seg_node.release(); t->wl.release(); t->seg_start.release();
+  t->plan.release(); t->plan_ex.release(); t->scan_u64x2.release(); t->in_xyz.release();
+  t->in_rgba.release(); t->gbuf.release(); t->gnodes.release(); t->goff.release(); t->gstart.release();
+  t->visflag.release(); t->vislist.release(); t->fb.release(); t->counter.release();
+  for (auto &e : t->ev) if (e) cudaEventDestroy(e);
+  cudaStreamDestroy(t->st);
+  delete t;
+  return LOD_OK;
+}
+
+int lod_tree_info(LodTree *t, LodTreeInfo *info) {
+  if (!t || !info) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  RK(sync_ctrl(t));
+  const Ctrl &c = *t->h_ctrl;
+  info->num_nodes = c.num_nodes;
+  info->node_capacity = t->ncap;
+  info->splits_total = c.splits_total;
+  info->max_level = c.max_level;
+  info->allocated_total = c.allocated_total;
+  info->free_count = c.free_count;
+  info->released_total = c.released_total;
+  info->chunk_capacity_rows = t->ccap;
+  info->arena_offset = c.arena_off;
+  info->arena_capacity = t->arena_cap;
+  info->grid_bytes = t->geo.grid_bytes;
+  info->chunk_capacity = t->geo.C;
+  return LOD_OK;
+}
+
+int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t n,
+                     const LodLimits *limits, int flags, LodBatchStats *stats) {
+  if (!t || n < 0 || (n > 0 && (!xyz || !rgba))) return LOD_E_ARG;
+  LodBatchStats local{};
+  LodBatchStats &S = stats ? *stats : local;
+  memset(&S, 0, sizeof(S));
+  S.n_batch = n;
+  cudaSetDevice(t->dev);
+  cudaStream_t st = t->st;
+  const bool prof = (flags & LOD_FLAG_PROFILE) != 0;
+  const long long backlog_cap = limits ? limits->backlog_capacity : 10000000LL;
+  const long long spill_cap = limits ? limits->spill_capacity : 100000000LL;
+  if (n == 0) {  // update.py:266-268
+    fill_stats(t, &S);
+    return LOD_OK;
+  }
+  if (n >= (1LL << 31)) return LOD_E_ARG;
+  const long long C = t->geo.C;
+  const long long launches0 = lod::g_launches;
+  t->d2h_bytes = 0;
+  S.h2d_bytes = (flags & LOD_FLAG_DEVICE_INPUT) ? 0 : 16 * n;
+  int evi = 0;
+  auto mark = [&](int phase) {
+    if (prof) cudaEventRecord(t->ev[1 + phase], st);
+    (void)evi;
+  };
+  CK(cudaEventRecord(t->ev[0], st));
+  // ---- inputs
+  const float *bx = xyz;
+  const uint32_t *bc = rgba;
+  if (!(flags & LOD_FLAG_DEVICE_INPUT)) {
+    RK(t->in_xyz.ensure(3 * n, st));
+    RK(t->in_rgba.ensure(n, st));
+    CK(cudaMemcpyAsync(t->in_xyz.p, xyz, (size_t)n * 12, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(t->in_rgba.p, rgba, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    bx = t->in_xyz.p;
+    bc = t->in_rgba.p;
+  }
+  CK(cudaEventRecord(t->ev[11], st));  // inputs resident
+  k_cycle_begin<<<1, 1, 0, st>>>(t->d_ctrl); ++lod::g_launches;
+  // ---- expansion (update.py:273-296)
+  RK(t->node_b.ensure(n, st));
+  PointSrc src{nullptr, 0, bx, bc, n};
+  int32_t *node_of = t->node_b.p;
+  long long n_all = n, n_s = 0;
+  int first = 1, iters = 0;
+  long long splits_cycle = 0;
+  for (;;) {
+    ++iters;
+    if (!first) k_reset_touched<<<1, 1, 0, st>>>(t->d_ctrl); ++lod::g_launches;
+    k_count<<<grid_for(n_all), 256, 0, st>>>(t->nd, t->geo, src, node_of, n_all, first, t->touched.p,
+                                            t->d_ctrl); ++lod::g_launches;
+    k_decide<<<1, kDecideBlock, 0, st>>>(t->nd, t->geo, t->touched.p, t->bitmap.p, t->word_prefix.p,
+                                         t->split_list.p, t->scnt.p, t->schk.p, t->spill_off.p,
+                                         t->chunk_off.p, t->d_ctrl, spill_cap, t->arena_cap); ++lod::g_launches;
+    RK(sync_ctrl(t));
+    const Ctrl &h = *t->h_ctrl;
+    if (h.error) return abort_cycle(t, h.error);
+    const long long ns = h.n_splits;
+    if (ns == 0) break;
+    splits_cycle += ns;
+    // capacity for the new children and the spill segment
+    RK(ensure_nodes(t, h.num_nodes, h.plan_num_nodes0));
+    if (h.spill_add > 0) {
+      if (!first) return abort_cycle(t, LOD_E_ARG);  // only iteration 1 can spill (update.py:9-11)
+      RK(t->spill.ensure(h.spill_total, st));
+      RK(t->node_all.ensure(h.spill_total + n, st));
+    }
+    k_execute<<<(unsigned)ns, kExecBlock, 0, st>>>(t->nd, t->pool, t->geo, t->arena, t->split_list.p,
+                                                 t->spill_off.p, t->chunk_off.p, t->spill.p,
+                                                 t->node_all.p, t->d_ctrl); ++lod::g_launches;
+    t->num_nodes = h.num_nodes;
+    if (first) {
+      n_s = h.spill_total;
+      if (n_s > 0) {
+        k_shift_nodes<<<grid_for(n), 256, 0, st>>>(t->node_b.p, t->node_all.p + n_s, n); ++lod::g_launches;
+        node_of = t->node_all.p;
+        src.spill = t->spill.p;
+        src.ns = n_s;
+      }
+      n_all = n_s + n;
+      first = 0;
+    }
+  }
+  mark(0);
+  const Ctrl h1 = *t->h_ctrl;
+  t->num_nodes = h1.num_nodes;
+  const long long num_nodes = h1.num_nodes;
+  // ---- sampling (update.py:298-315)
+  const int D = (int)std::max<long long>(h1.max_level, 1);
+  const long long bound = n_all * D;
+  const long long claim_cap = std::min<long long>(bound, backlog_cap + 1);
+  {
+    unsigned long long H = next_pow2((unsigned long long)std::max<long long>(2 * claim_cap, 1024));
+    if (H > t->hcap) {
+      t->hkeys.release();
+      t->hvals.release();
+      RK(t->hkeys.ensure((long long)H, st));
+      RK(t->hvals.ensure((long long)H, st));
+      CK(cudaMemsetAsync(t->hkeys.p, 0xFF, (size_t)H * 8, st));
+      CK(cudaMemsetAsync(t->hvals.p, 0xFF, (size_t)H * 4, st));
+      t->hcap = H;
+    }
+  }
+  RK(t->hused.ensure(claim_cap + 1, st));
+  RK(t->wcount.ensure(n_all, st));
+  RK(t->wbase.ensure(n_all, st));
+  RK(t->wins.ensure(bound, st));
+  RK(t->scan_u32.ensure(scan_scratch_elems(std::max<long long>(n_all, 1)), st));
+  Hash hs{t->hkeys.p, t->hvals.p, t->hcap - 1, t->hused.p, (unsigned long long)claim_cap + 1};
+  // a cheap upper bound for what follows: arena as 32-bit words for grids
+  uint32_t *grid32 = reinterpret_cast<uint32_t *>(t->arena);
+  k_claim<<<grid_for(n_all), 256, 0, st>>>(t->nd, t->geo, src, grid32, n_all, hs, t->d_ctrl); ++lod::g_launches;
+  k_win<<<grid_for(n_all), 256, 0, st>>>(t->nd, t->geo, src, grid32, n_all, hs, t->wcount.p, t->wins.p, D); ++lod::g_launches;
+  mark(1);
+  exclusive_scan<uint32_t>(t->wcount.p, t->wbase.p, n_all, &t->d_ctrl->n_v, t->scan_u32.p, st);
+  RK(sync_ctrl(t));
+  const Ctrl h2 = *t->h_ctrl;
+  if (h2.hash_overflow || (long long)h2.n_used > backlog_cap || (long long)h2.n_v > backlog_cap)
+    return abort_cycle(t, LOD_E_BACKLOG_OVERFLOW);  // update.py:311-312
+  const long long n_v = h2.n_v;
+  RK(t->bnode.ensure(std::max<long long>(n_v, 1), st));
+  RK(t->bcell.ensure(std::max<long long>(n_v, 1), st));
+  RK(t->brgba.ensure(std::max<long long>(n_v, 1), st));
+  if (n_v > 0)
+    k_emit<<<grid_for(n_all), 256, 0, st>>>(n_all, t->wcount.p, t->wbase.p, t->wins.p, D, src, t->bnode.p,
+                                           t->bcell.p, t->brgba.p); ++lod::g_launches;
+  mark(2);
+  // ---- sort: every new sample by node id, stable (slot order)
+  const long long n_items = n_all + n_v;
+  RK(t->keys.ensure(n_items, st));
+  RK(t->keys_b.ensure(n_items, st));
+  RK(t->vals_a.ensure(n_items, st));
+  RK(t->vals_b.ensure(n_items, st));
+  RK(t->flags.ensure(n_items, st));
+  RK(t->hpos.ensure(n_items, st));
+  RK(t->hist.ensure(radix_hist_elems(n_items), st));
+  RK(t->scan_u32.ensure(scan_scratch_elems(std::max<long long>(n_items, radix_hist_elems(n_items))), st));
+  k_keys<<<grid_for(n_items), 256, 0, st>>>(node_of, n_all, t->bnode.p, n_v, t->keys.p); ++lod::g_launches;
+  RadixScratch rs;
+  rs.keys_b = t->keys_b.p;
+  rs.vals_a = t->vals_a.p;
+  rs.vals_b = t->vals_b.p;
+  rs.hist = t->hist.p;
+  rs.scan_tmp = t->scan_u32.p;
+  uint32_t *skeys = nullptr, *svals = nullptr;
+  stable_multisplit(t->keys.p, n_items, (uint32_t)(num_nodes - 1), rs, st, &skeys, &svals);
+  mark(3);
+  // ---- allocation (update.py:317-331)
+  const long long Kb = num_nodes + 1;  // bound on touched nodes
+  RK(t->seg_node.ensure(Kb, st));
+  RK(t->seg_start.ensure(Kb + 1, st));
+  RK(t->plan.ensure(Kb, st));
+  RK(t->plan_ex.ensure(Kb, st));
+  RK(t->scan_u64x2.ensure(scan_scratch_elems(Kb), st));
+  const long long acq_bound = n_items / C + Kb + 1;
+  RK(t->wl.ensure(acq_bound + Kb + 1, st));
+  RK(ensure_chunks(t, h2.allocated_total + acq_bound + 1, h2.allocated_total));
+  k_seg_flags<<<grid_for(n_items), 256, 0, st>>>(skeys, n_items, t->flags.p); ++lod::g_launches;
+  exclusive_scan<uint32_t>(t->flags.p, t->hpos.p, n_items, &t->d_ctrl->n_keys, t->scan_u32.p, st);
+  k_seg_list<<<grid_for(n_items), 256, 0, st>>>(skeys, n_items, t->hpos.p, t->seg_node.p, t->seg_start.p,
+                                               t->d_ctrl); ++lod::g_launches;
+  CK(cudaMemsetAsync(t->plan.p, 0, (size_t)Kb * sizeof(U64x2), st));
+  k_plan<<<grid_for(Kb), 256, 0, st>>>(t->nd, t->geo, t->seg_node.p, t->seg_start.p, t->d_ctrl, t->plan.p); ++lod::g_launches;
+  exclusive_scan<U64x2>(t->plan.p, t->plan_ex.p, Kb, &t->d_ctrl->acq_tot, t->scan_u64x2.p, st);
+  k_alloc_begin<<<1, 1, 0, st>>>(t->d_ctrl, t->geo, t->arena_cap); ++lod::g_launches;
+  k_alloc_nodes<<<grid_for(Kb), 256, 0, st>>>(t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p, t->plan.p,
+                                              t->plan_ex.p, t->wl.p, t->d_ctrl); ++lod::g_launches;
+  k_alloc_chunks<<<grid_for(acq_bound), 256, 0, st>>>(t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p,
+                                                      t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl); ++lod::g_launches;
+  mark(4);
+  // ---- store (update.py:357-373)
+  k_store<<<grid_for(n_items), 256, 0, st>>>(t->nd, t->pool, t->geo, t->arena, skeys, svals, t->hpos.p,
+                                             t->seg_start.p, t->plan.p, t->plan_ex.p, t->wl.p, n_items, n_all,
+                                             src, t->bcell.p, t->brgba.p, t->d_ctrl); ++lod::g_launches;
+  mark(5);
+  // ---- cleanup (update.py:375-380)
+  k_epilogue<<<grid_for(Kb), 256, 0, st>>>(t->nd, t->seg_node.p, t->seg_start.p, t->d_ctrl); ++lod::g_launches;
+  k_hash_clear<<<grid_for(std::max<long long>(n_v, 1)), 256, 0, st>>>(hs, t->d_ctrl); ++lod::g_launches;
+  mark(6);
+  CK(cudaEventRecord(t->ev[10], st));
+  RK(sync_ctrl(t));
+  const Ctrl &h3 = *t->h_ctrl;
+  if (h3.error) return abort_cycle(t, h3.error);
+  S.n_spill = n_s;
+  S.launches = lod::g_launches - launches0;
+  S.d2h_bytes = t->d2h_bytes;
+  S.n_voxels = n_v;
+  S.n_splits = splits_cycle;
+  S.iterations = iters;
+  fill_stats(t, &S);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, t->ev[11], t->ev[10]);
+  S.device_ms = ms;
+  if (prof) {
+    float h2d = 0.f;
+    cudaEventElapsedTime(&h2d, t->ev[0], t->ev[11]);
+    S.phase_ms[7] = h2d;
+    cudaEvent_t prev = t->ev[11];
+    for (int k = 0; k < 7; ++k) {
+      float x = 0.f;
+      cudaEventElapsedTime(&x, prev, t->ev[1 + k]);
+      S.phase_ms[k] = x;
+      prev = t->ev[1 + k];
+    }
+  }
+  return LOD_OK;
+}
+
+int lod_read_nodes(LodTree *t, int64_t n, int32_t *parent, uint8_t *octant, int32_t *level,
+                   int32_t *children, uint8_t *inner, uint8_t *final_, int64_t *count, int64_t *pending,
+                   int32_t *chunk_head, int32_t *chunk_tail, int32_t *chunk_count, int64_t *grid_off,
+                   double *bmin) {
+  if (!t || n < 0 || n > t->ncap) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  cudaStream_t st = t->st;
+  auto cp = [&](void *dst, const void *src, size_t bytes) -> int {
+    if (dst && bytes) return cuda_rc(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+    return LOD_OK;
+  };
+  RK(cp(parent, t->nd.parent, n * 4));
+  RK(cp(octant, t->nd.octant, n));
+  RK(cp(level, t->nd.level, n * 4));
+  RK(cp(children, t->nd.children, n * 32));
+  RK(cp(inner, t->nd.inner, n));
+  RK(cp(final_, t->nd.final_, n));
+  RK(cp(count, t->nd.count, n * 8));
+  RK(cp(pending, t->nd.pending, n * 8));
+  RK(cp(chunk_head, t->nd.chunk_head, n * 4));
+  RK(cp(chunk_tail, t->nd.chunk_tail, n * 4));
+  RK(cp(chunk_count, t->nd.chunk_count, n * 4));
+  RK(cp(grid_off, t->nd.grid_off, n * 8));
+  RK(cp(bmin, t->nd.bmin, n * 24));
+  CK(cudaStreamSynchronize(st));
+  return LOD_OK;
+}
+
+int lod_read_pool(LodTree *t, int64_t n, int32_t *next, int64_t *payload_off, int32_t *occupied,
+                  int32_t *free_list, int64_t n_free) {
+  if (!t || n < 0 || n > t->ccap || n_free < 0 || n_free > t->ccap) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  cudaStream_t st = t->st;
+  if (next && n) CK(cudaMemcpyAsync(next, t->pool.next, n * 4, cudaMemcpyDeviceToHost, st));
+  if (payload_off && n) CK(cudaMemcpyAsync(payload_off, t->pool.payload_off, n * 8, cudaMemcpyDeviceToHost, st));
+  if (occupied && n) CK(cudaMemcpyAsync(occupied, t->pool.occupied, n * 4, cudaMemcpyDeviceToHost, st));
+  if (free_list && n_free)
+    CK(cudaMemcpyAsync(free_list, t->pool.free_stack, n_free * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return LOD_OK;
+}
+
+static int gather_impl(LodTree *t, const std::vector<int32_t> &nodes, const std::vector<long long> &starts,
+                       const std::vector<long long> &offs, long long total, float4 *host_out) {
+  cudaStream_t st = t->st;
+  const long long m = (long long)nodes.size();
+  if (m == 0 || total == 0) return LOD_OK;
+  RK(t->gnodes.ensure(m, st));
+  RK(t->gstart.ensure(m, st));
+  RK(t->goff.ensure(m, st));
+  RK(t->gbuf.ensure(total, st));
+  CK(cudaMemcpyAsync(t->gnodes.p, nodes.data(), m * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(t->gstart.p, starts.data(), m * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(t->goff.p, offs.data(), m * 8, cudaMemcpyHostToDevice, st));
+  for (long long b = 0; b < m; b += 65535) {
+    long long cnt = std::min<long long>(65535, m - b);
+    k_gather_nodes<<<(unsigned)cnt, 256, 0, st>>>(t->nd, t->pool, t->geo, t->arena, t->gnodes.p + b,
+                                                  t->gstart.p + b, t->goff.p + b, t->gbuf.p); ++lod::g_launches;
+  }
+  CK(cudaMemcpyAsync(host_out, t->gbuf.p, total * 16, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return LOD_OK;
+}
+
+int lod_gather(LodTree *t, int64_t nid, int64_t start, float *xyz, uint32_t *rgba) {
+  if (!t || nid < 0 || nid >= t->num_nodes || start < 0) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  long long cnt = 0;
+  CK(cudaMemcpyAsync(&cnt, t->nd.count + nid, 8, cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  long long k = cnt - start;
+  if (k <= 0) return LOD_OK;
+  std::vector<float4> buf((size_t)k);
+  RK(gather_impl(t, {(int32_t)nid}, {start}, {0}, k, buf.data()));
+  for (long long i = 0; i < k; ++i) {
+    xyz[3 * i] = buf[i].x;
+    xyz[3 * i + 1] = buf[i].y;
+    xyz[3 * i + 2] = buf[i].z;
+    uint32_t c;
+    memcpy(&c, &buf[i].w, 4);
+    rgba[i] = c;
+  }
+  return LOD_OK;
+}
+
+int lod_dump_records(LodTree *t, int64_t num_nodes, int64_t *offsets, void *records) {
+  if (!t || num_nodes < 0 || num_nodes > t->num_nodes || !offsets) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  std::vector<long long> cnt((size_t)num_nodes);
+  if (num_nodes) CK(cudaMemcpyAsync(cnt.data(), t->nd.count, num_nodes * 8, cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  std::vector<int32_t> nodes;
+  std::vector<long long> starts, offs;
+  long long total = 0;
+  offsets[0] = 0;
+  for (long long i = 0; i < num_nodes; ++i) {
+    if (cnt[i] > 0) {
+      nodes.push_back((int32_t)i);
+      starts.push_back(0);
+      offs.push_back(total);
+    }
+    total += cnt[i];
+    offsets[i + 1] = total;
+  }
+  if (!records) return LOD_OK;
+  return gather_impl(t, nodes, starts, offs, total, reinterpret_cast<float4 *>(records));
+}
+
+int lod_read_arena(LodTree *t, uint64_t off, uint64_t size, void *dst) {
+  if (!t || !dst || off + size > t->arena_cap) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  CK(cudaMemcpyAsync(dst, t->arena + off, size, cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  return LOD_OK;
+}
+
+}  // extern "C"
+
+// accessors for lod_raster.cu
+cudaStream_t lod_tree_stream(LodTree *t) { return t->st; }
+int lod_tree_device(LodTree *t) { return t->dev; }
+const uint8_t *lod_tree_arena(LodTree *t) { return t->arena; }
+PoolCols lod_tree_pool(LodTree *t) { return t->pool; }
+long long lod_tree_allocated(LodTree *t) {
+  cudaMemcpyAsync(t->h_ctrl, t->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, t->st);
+  cudaStreamSynchronize(t->st);
+  return t->h_ctrl->allocated_total;
+}
+long long lod_tree_num_nodes(LodTree *t) { return t->num_nodes; }
+uint32_t *lod_tree_visflag(LodTree *t) { return t->visflag.p; }
+int lod_tree_ensure_vislist(LodTree *t, long long n, int32_t **p) {
+  int rc = t->vislist.ensure(std::max<long long>(n, 1), t->st);
+  *p = t->vislist.p;
+  return rc;
+}
+int lod_tree_ensure_fb(LodTree *t, long long n, unsigned long long **p) {
+  int rc = t->fb.ensure(std::max<long long>(n, 1), t->st);
+  *p = t->fb.p;
+  return rc;
+}
+unsigned long long *lod_tree_counter(LodTree *t) { return t->counter.p; }

@@ -1,0 +1,227 @@
+"""Incremental batch insertion on the B200 (reference: lodstream/update.py).
+
+``insert_batch`` runs one full update cycle of the reference's contract
+(update.py:1-27) -- expansion (count <-> split until settled), sampling
+(first-come voxel claims), allocation, store, cleanup -- as one call into the
+CUDA library (``lod_insert_batch``).  The semantics, including the exact node
+ids, per-node point/voxel sequences, chunk counts, arena growth and overflow
+points, are the reference's; see DESIGN.md for how each pass maps to kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .octree import Octree
+
+__all__ = [
+    "UpdateConfig",
+    "UpdateState",
+    "UpdateStats",
+    "BatchDelta",
+    "BudgetClock",
+    "SpillBuffer",
+    "VoxelBacklog",
+    "chunks_needed",
+    "insert_batch",
+    "run_frame_updates",
+]
+
+
+def chunks_needed(count: int, capacity: int) -> int:
+    """Chunks required to hold ``count`` records: ceil(count / capacity)."""
+    return (count + capacity - 1) // capacity
+
+
+@dataclass
+class UpdateConfig:
+    batch_size: int = 1_000_000
+    budget_ms: float = 10.0
+    backlog_capacity: int = 10_000_000
+    spill_capacity: int = 100_000_000
+
+
+@dataclass
+class UpdateStats:
+    batches: int = 0
+    frames: int = 0
+    points: int = 0
+    voxels_created: int = 0
+    nodes: int = 0
+    splits: int = 0
+    update_seconds: float = 0.0
+    max_batch_ms: float = 0.0
+    frame_ms_total: float = 0.0
+    frame_ms_max: float = 0.0
+    backlog_high_water: int = 0
+    spill_high_water: int = 0
+    device_seconds: float = 0.0  # CUDA-event time of the update kernels (B200 extra)
+
+    def throughput_mps(self) -> float:
+        """Million points ingested per update-second (update.py:82-86)."""
+        if self.update_seconds <= 0.0:
+            return 0.0
+        return self.points / self.update_seconds / 1e6
+
+
+class BudgetClock:
+    """Wall-clock frame budget, checked between batches (update.py:89-103)."""
+
+    def __init__(self, budget_ms: float) -> None:
+        self.budget_ms = budget_ms
+        self._start = time.perf_counter()
+
+    def restart(self) -> None:
+        self._start = time.perf_counter()
+
+    def elapsed_ms(self) -> float:
+        return (time.perf_counter() - self._start) * 1e3
+
+    def exceeded(self) -> bool:
+        return self.elapsed_ms() >= self.budget_ms
+
+
+class SpillBuffer:
+    """Spill accounting.  The spilled records themselves live in an HBM buffer
+    of the tree for the duration of one cycle (update.py:106-140); between
+    cycles the buffer is empty, which is all callers can observe."""
+
+    def __init__(self, capacity: int) -> None:
+        self.capacity = capacity
+        self.total = 0
+        self.high_water = 0
+
+    def clear(self) -> None:
+        self.total = 0
+
+    def __len__(self) -> int:
+        return self.total
+
+
+class VoxelBacklog:
+    """Backlog accounting; the (node, cell, rgba) triples live in HBM for one
+    cycle (update.py:143-171)."""
+
+    def __init__(self, capacity: int) -> None:
+        self.capacity = capacity
+        self.length = 0
+        self.high_water = 0
+
+    def clear(self) -> None:
+        self.length = 0
+
+
+@dataclass
+class BatchDelta:
+    structure: list[tuple] = field(default_factory=list)
+    voxels: list[tuple[int, np.ndarray, np.ndarray]] = field(default_factory=list)
+    points: list[tuple[int, int, int]] = field(default_factory=list)
+
+
+class UpdateState:
+    """Per-tree transient state and statistics (update.py:197-223)."""
+
+    def __init__(self, config: UpdateConfig | None = None) -> None:
+        self.config = config or UpdateConfig()
+        self.spill = SpillBuffer(self.config.spill_capacity)
+        self.backlog = VoxelBacklog(self.config.backlog_capacity)
+        self.stats = UpdateStats()
+        self.clock = BudgetClock(self.config.budget_ms)
+        self.last: dict | None = None  # LodBatchStats of the last call
+        self._limits = _lib.LodLimits()
+        self._bstats = _lib.LodBatchStats()
+
+
+def _as_input(a, dtype, shape_tail):
+    """numpy / torch input -> (object keeping the buffer alive, is_device)."""
+    if hasattr(a, "is_cuda") and a.is_cuda:
+        import torch  # only when the caller already uses torch
+
+        want = {np.float32: torch.float32, np.uint32: torch.int32}[dtype]
+        if a.dtype not in (want, torch.uint32 if dtype is np.uint32 else want):
+            raise TypeError(f"device input must be {want}, got {a.dtype}")
+        if not a.is_contiguous():
+            a = a.contiguous()
+        return a, True
+    arr = np.ascontiguousarray(a, dtype)
+    if shape_tail:
+        arr = arr.reshape((-1,) + shape_tail)
+    return arr, False
+
+
+def insert_batch(
+    tree: Octree,
+    xyz,
+    rgba,
+    state: UpdateState,
+    collect_delta: bool = False,
+    profile: bool = False,
+) -> BatchDelta | None:
+    """Run one full update cycle for a batch (update.py:252-393).
+
+    ``xyz`` is (n, 3) float32 inside the tree bounds and ``rgba`` packed uint32
+    (numpy arrays, copied H2D; or CUDA tensors already resident in HBM).  The
+    whole batch is always consumed.
+    """
+    if collect_delta:
+        raise NotImplementedError("collect_delta (service stream deltas) is not built yet (SURVEY 8(f) row 3)")
+    t0 = time.perf_counter()
+    n_batch = len(rgba)
+    if n_batch == 0:
+        return None
+    xyz_b, dev_x = _as_input(xyz, np.float32, (3,))
+    rgba_b, dev_c = _as_input(rgba, np.uint32, ())
+    if dev_x != dev_c:
+        raise ValueError("xyz and rgba must both be host arrays or both be device tensors")
+    flags = (_lib.LOD_FLAG_DEVICE_INPUT if dev_x else 0) | (_lib.LOD_FLAG_PROFILE if profile else 0)
+    lim = state._limits
+    lim.backlog_capacity = state.config.backlog_capacity
+    lim.spill_capacity = state.config.spill_capacity
+    bs = state._bstats
+    rc = tree._L.lod_insert_batch(tree.handle, _lib.ptr(xyz_b), _lib.ptr(rgba_b), n_batch,
+                                  ctypes.byref(lim), flags, ctypes.byref(bs))
+    tree._invalidate()
+    _lib.check(rc, "insert_batch")
+    st = state.stats
+    n_v, n_s = int(bs.n_voxels), int(bs.n_spill)
+    st.batches += 1
+    st.points += n_batch
+    state.backlog.high_water = max(state.backlog.high_water, n_v)
+    state.spill.high_water = max(state.spill.high_water, n_s)
+    st.backlog_high_water = state.backlog.high_water
+    st.spill_high_water = state.spill.high_water
+    st.voxels_created += n_v
+    st.splits = int(bs.splits_total)
+    st.nodes = int(bs.num_nodes)
+    st.device_seconds += float(bs.device_ms) * 1e-3
+    if profile:
+        state.last = bs.as_dict()
+    else:
+        state.last = None
+    dt = time.perf_counter() - t0
+    st.update_seconds += dt
+    st.max_batch_ms = max(st.max_batch_ms, dt * 1e3)
+    return None
+
+
+def run_frame_updates(tree, batches, state: UpdateState, on_delta=None) -> int:
+    """Drain queued batches for one frame within the budget (update.py:396-417)."""
+    state.clock.restart()
+    processed = 0
+    while batches and (processed == 0 or not state.clock.exceeded()):
+        xyz, rgba = batches.popleft()
+        delta = insert_batch(tree, xyz, rgba, state, collect_delta=on_delta is not None)
+        if on_delta is not None:
+            on_delta(delta)
+        processed += 1
+    if processed:
+        st = state.stats
+        st.frames += 1
+        dt = state.clock.elapsed_ms()
+        st.frame_ms_total += dt
+        st.frame_ms_max = max(st.frame_ms_max, dt)
+    return processed

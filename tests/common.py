@@ -1,0 +1,180 @@
+"""Test helpers: golden fixtures, oracle / product runners and comparators."""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = os.path.join(HERE, "golden")
+
+STATE_SCALARS = ("num_nodes", "splits_total", "max_level", "allocated_total", "released_total",
+                 "free_count", "arena_offset")
+NODE_COLS_ID_FREE = ("parent", "octant", "level", "children", "inner", "final", "count", "pending",
+                     "chunk_count", "grid_off", "bmin")
+CHUNK_ID_COLS = ("chunk_head", "chunk_tail", "next", "occupied", "payload_off", "free_list")
+
+
+def golden_names() -> list[str]:
+    return sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and f != "raster.npz")
+
+
+def load_golden(name: str) -> dict:
+    z = np.load(os.path.join(GOLDEN, f"{name}.npz"))
+    d = {k: z[k] for k in z.files}
+    d["params"] = json.loads(bytes(d["params"]).decode())
+    d["error"] = bytes(d["error"]).decode().strip()
+    sizes = d["batch_sizes"]
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    d["batches"] = [(d["xyz"][a:b], d["rgba"][a:b]) for a, b in zip(offs[:-1], offs[1:])]
+    d["state"] = {k[2:]: v for k, v in d.items() if k.startswith("s_")}
+    return d
+
+
+def load_raster() -> dict:
+    z = np.load(os.path.join(GOLDEN, "raster.npz"))
+    return {k: z[k] for k in z.files}
+
+
+def dense_fb(idx, val, n):
+    fb = np.full(n, np.uint64(0xFFFFFFFFFFFFFFFF))
+    fb[idx] = val
+    return fb
+
+
+# -- oracle ----------------------------------------------------------------------------
+
+
+def run_oracle(params: dict, batches):
+    import oracle
+
+    t = oracle.OracleTree(
+        params["bmin"], params["size"], grid_res=params["grid_res"], leaf_threshold=params["leaf_threshold"],
+        max_depth=params["max_depth"], chunk_capacity=params["chunk_capacity"],
+        arena_bytes=params["arena_bytes"], backlog_capacity=params["backlog_capacity"],
+        spill_capacity=params["spill_capacity"],
+    )
+    error = ""
+    per_batch = []
+    hw_b = hw_s = 0
+    for x, c in batches:
+        try:
+            s = t.insert_batch(x, c)
+        except oracle.OracleError as e:
+            error = e.kind
+            break
+        hw_b, hw_s = max(hw_b, s["n_voxels"]), max(hw_s, s["n_spill"])
+        st = t.state()
+        per_batch.append([t.voxels_created, st["splits_total"], st["num_nodes"], hw_b, hw_s])
+    return t, error, per_batch
+
+
+def oracle_state(t) -> dict:
+    d = t.state()
+    n = d["num_nodes"]
+    offs = np.zeros(n + 1, np.int64)
+    recs, cells = [], []
+    cell_offs = np.zeros(n + 1, np.int64)
+    for nid in range(n):
+        xyz, rgba = t.gather_samples(nid)
+        r = np.empty((len(rgba), 4), np.float32)
+        r[:, :3] = xyz
+        r[:, 3] = rgba.view(np.float32)
+        recs.append(r)
+        offs[nid + 1] = offs[nid] + len(rgba)
+        oc = t.occupied_cells(nid).astype(np.int64) if d["inner"][nid] else np.empty(0, np.int64)
+        cells.append(oc)
+        cell_offs[nid + 1] = cell_offs[nid] + len(oc)
+    d["rec_offsets"] = offs
+    d["records"] = np.concatenate(recs) if recs else np.empty((0, 4), np.float32)
+    d["cell_offsets"] = cell_offs
+    d["cells"] = np.concatenate(cells) if cells else np.empty(0, np.int64)
+    return d
+
+
+# -- product ---------------------------------------------------------------------------
+
+
+def make_product(params: dict, device: int = 0):
+    from paper_2310_03567_b200 import Arena, ChunkPool, CubeBounds, Octree, UpdateConfig, UpdateState
+
+    arena = Arena(params["arena_bytes"])
+    pool = ChunkPool(arena, params["chunk_capacity"])
+    tree = Octree(CubeBounds(tuple(params["bmin"]), params["size"]), arena, pool, grid_res=params["grid_res"],
+                  leaf_threshold=params["leaf_threshold"], max_depth=params["max_depth"], device=device)
+    state = UpdateState(UpdateConfig(backlog_capacity=params["backlog_capacity"],
+                                     spill_capacity=params["spill_capacity"]))
+    return tree, state
+
+
+def run_product(params: dict, batches):
+    from paper_2310_03567_b200 import BacklogOverflow, OutOfArena, SpillOverflow, insert_batch
+
+    tree, state = make_product(params)
+    error = ""
+    per_batch = []
+    for x, c in batches:
+        try:
+            insert_batch(tree, x, c, state)
+        except (OutOfArena, SpillOverflow, BacklogOverflow) as e:
+            error = type(e).__name__
+            break
+        s = state.stats
+        per_batch.append([s.voxels_created, s.splits, s.nodes, s.backlog_high_water, s.spill_high_water])
+    return tree, state, error, per_batch
+
+
+def product_state(tree) -> dict:
+    n = tree.num_nodes
+    d = {
+        "num_nodes": n, "splits_total": tree.splits_total, "max_level": tree.max_level,
+        "allocated_total": tree.pool.allocated_total, "released_total": tree.pool.released_total,
+        "free_count": tree.pool.free_count, "arena_offset": tree.arena.offset,
+    }
+    for k in NODE_COLS_ID_FREE + ("chunk_head", "chunk_tail"):
+        d[k] = getattr(tree, k)[:n].copy()
+    offs, rec = tree.dump_records()
+    d["rec_offsets"], d["records"] = offs, rec
+    cells, cell_offs = [], np.zeros(n + 1, np.int64)
+    for nid in range(n):
+        oc = tree.occupied_cells(nid).astype(np.int64) if d["inner"][nid] else np.empty(0, np.int64)
+        cells.append(oc)
+        cell_offs[nid + 1] = cell_offs[nid] + len(oc)
+    d["cell_offsets"] = cell_offs
+    d["cells"] = np.concatenate(cells) if cells else np.empty(0, np.int64)
+    return d
+
+
+def assert_same_state(got: dict, want: dict, *, chunk_ids: bool, label: str = "") -> None:
+    """Bit-exact comparison of two observable tree states.
+
+    ``chunk_ids=False`` skips the columns that name chunk ids / payload offsets
+    (their assignment order is an implementation detail: SURVEY 8(a) item 4);
+    counts of chunks, arena growth, free-list length and every node's sample
+    sequence are always compared.
+    """
+    for k in STATE_SCALARS:
+        assert int(got[k]) == int(want[k]), f"{label}: {k} {got[k]} != {want[k]}"
+    n = int(want["num_nodes"])
+    cols = NODE_COLS_ID_FREE + (CHUNK_ID_COLS if chunk_ids else ())
+    for k in cols:
+        a, b = np.asarray(got[k]), np.asarray(want[k])
+        if k in ("chunk_head", "chunk_tail") or k in NODE_COLS_ID_FREE:
+            a, b = a[:n], b[:n]
+        assert a.shape == b.shape, f"{label}: {k} shape {a.shape} != {b.shape}"
+        if k == "bmin":
+            assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), f"{label}: bmin bits differ"
+        else:
+            if not np.array_equal(a, b):
+                diff = np.flatnonzero((a != b).reshape(len(a), -1).any(axis=1)) if a.size else []
+                raise AssertionError(f"{label}: {k} differs at rows {list(diff[:8])}")
+    assert np.array_equal(got["rec_offsets"], want["rec_offsets"]), f"{label}: per-node counts differ"
+    ra = np.ascontiguousarray(got["records"]).view(np.uint32)
+    rb = np.ascontiguousarray(want["records"]).view(np.uint32)
+    if not np.array_equal(ra, rb):
+        bad = np.flatnonzero((ra != rb).any(axis=1))
+        node = int(np.searchsorted(want["rec_offsets"], bad[0], side="right") - 1)
+        raise AssertionError(f"{label}: {len(bad)} sample records differ, first at node {node}")
+    assert np.array_equal(got["cell_offsets"], want["cell_offsets"]), f"{label}: bitgrid popcounts differ"
+    assert np.array_equal(got["cells"], want["cells"]), f"{label}: occupied cells differ"

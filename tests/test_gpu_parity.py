@@ -1,0 +1,168 @@
+"""GPU parity: the CUDA update path vs the reference fixtures and the oracle.
+
+Every comparison is bit-exact on the observable tree: node hierarchy and ids,
+every node's sample (point / voxel) sequence, bitgrids, chunk counts, arena
+growth, free-list length and overflow behaviour.  Only the ids of individual
+chunks are free (their assignment order is not observable).
+"""
+import numpy as np
+import pytest
+
+from common import (assert_same_state, golden_names, load_golden, make_product, oracle_state, product_state,
+                    run_oracle, run_product)
+
+pytestmark = pytest.mark.gpu
+
+
+def _hygiene(tree, state):
+    n = tree.num_nodes
+    assert len(state.spill) == 0
+    assert state.backlog.length == 0
+    assert not tree.final[:n].any()
+    assert not tree.pending[:n].any()
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_matches_reference_fixture(gpu, name):
+    g = load_golden(name)
+    tree, state, error, per_batch = run_product(g["params"], g["batches"])
+    assert error == g["error"]
+    assert np.array_equal(np.array(per_batch, np.int64).reshape(-1, 5), g["per_batch"])
+    if not error:
+        assert_same_state(product_state(tree), g["state"], chunk_ids=False, label=name)
+        _hygiene(tree, state)
+        tree.validate()
+
+
+def _cloud(n, seed, kind):
+    rng = np.random.default_rng(seed)
+    if kind == "uniform":
+        xyz = rng.random((n, 3)).astype(np.float32)
+    elif kind == "surface":
+        from paper_2310_03567_b200 import synth
+
+        return synth.gen_surface(n, seed)
+    elif kind == "skew":
+        from paper_2310_03567_b200 import synth
+
+        return synth.gen_skew(n, seed)
+    elif kind == "mesh":
+        from paper_2310_03567_b200 import synth
+
+        return synth.gen_mesh(n, seed)
+    np.clip(xyz, 0.0, np.nextafter(np.float32(1.0), np.float32(0.0)), out=xyz)
+    return xyz, rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+
+
+def _params(**kw):
+    p = dict(bmin=(0.0, 0.0, 0.0), size=1.0, arena_bytes=256 << 20, chunk_capacity=1000, grid_res=16,
+             leaf_threshold=100, max_depth=12, backlog_capacity=10_000_000, spill_capacity=100_000_000)
+    p.update(kw)
+    return p
+
+
+CASES = [
+    # (label, n, seed, kind, batch, params)
+    ("uniform_small_bs1", 300, 1, "uniform", 1, _params(grid_res=4, leaf_threshold=10, max_depth=6, chunk_capacity=3)),
+    ("uniform_bs7", 3000, 2, "uniform", 7, _params(grid_res=8, leaf_threshold=20, chunk_capacity=5)),
+    ("surface_bs1000", 50_000, 3, "surface", 1000, _params(grid_res=16, leaf_threshold=100, chunk_capacity=64)),
+    ("skew_bs5000", 60_000, 4, "skew", 5000, _params(grid_res=32, leaf_threshold=200, max_depth=16, chunk_capacity=100)),
+    ("mesh_bs20000", 100_000, 5, "mesh", 20_000, _params(grid_res=64, leaf_threshold=1000, chunk_capacity=250)),
+    ("uniform_big_batches", 400_000, 6, "uniform", 100_000,
+     _params(arena_bytes=1 << 30, grid_res=128, leaf_threshold=5000, max_depth=20, chunk_capacity=1000)),
+    ("offset_cube", 20_000, 7, "uniform", 3000, _params(bmin=(-3.0, 2.5, 10.0), size=6.5, grid_res=8, leaf_threshold=64)),
+]
+
+
+@pytest.mark.parametrize("label,n,seed,kind,bs,params", CASES, ids=[c[0] for c in CASES])
+def test_matches_oracle(gpu, label, n, seed, kind, bs, params):
+    xyz, rgba = _cloud(n, seed, kind)
+    if params["size"] != 1.0:
+        xyz = (xyz.astype(np.float64) * params["size"] + np.asarray(params["bmin"])).astype(np.float32)
+    batches = [(xyz[i:i + bs], rgba[i:i + bs]) for i in range(0, n, bs)]
+    ot, oerr, oper = run_oracle(params, batches)
+    tree, state, err, per = run_product(params, batches)
+    assert err == oerr == ""
+    assert per == oper
+    assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label=label)
+    _hygiene(tree, state)
+
+
+def test_config1_one_million_uniform(gpu):
+    """BASELINE config 1: 1M uniform points, one batch, paper parameters."""
+    from paper_2310_03567_b200 import synth
+
+    xyz, rgba = synth.gen_uniform(1_000_000, 0)
+    params = _params(arena_bytes=1 << 30, grid_res=128, leaf_threshold=50_000, max_depth=20, chunk_capacity=1000)
+    ot, _, oper = run_oracle(params, [(xyz, rgba)])
+    tree, state, err, per = run_product(params, [(xyz, rgba)])
+    assert err == ""
+    assert per == oper
+    assert tree.num_nodes == 73 and int(tree.inner[:73].sum()) == 9
+    assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label="config1")
+    tree.validate()
+
+
+def test_terrain_stream_matches_oracle(gpu):
+    """Config 2 shape (gen_surface 1M batches, paper parameters), a 4-batch prefix."""
+    from paper_2310_03567_b200 import synth
+
+    params = _params(arena_bytes=2 << 30, grid_res=128, leaf_threshold=50_000, max_depth=20, chunk_capacity=1000)
+    batches = [synth.gen_surface(1_000_000, 100 + i) for i in range(4)]
+    ot, _, oper = run_oracle(params, batches)
+    tree, state, err, per = run_product(params, batches)
+    assert err == ""
+    assert per == oper
+    assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label="terrain")
+
+
+def test_empty_batch_is_noop(gpu):
+    from paper_2310_03567_b200 import insert_batch
+
+    tree, state = make_product(_params())
+    insert_batch(tree, np.empty((0, 3), np.float32), np.empty(0, np.uint32), state)
+    assert state.stats.batches == 0
+    assert tree.num_nodes == 1 and tree.count[0] == 0
+
+
+def test_device_resident_input_matches_host_input(gpu):
+    import torch
+
+    from paper_2310_03567_b200 import insert_batch
+
+    xyz, rgba = _cloud(50_000, 9, "surface")
+    p = _params(grid_res=32, leaf_threshold=300, chunk_capacity=128)
+    t1, s1 = make_product(p)
+    t2, s2 = make_product(p)
+    for i in range(0, 50_000, 10_000):
+        insert_batch(t1, xyz[i:i + 10_000], rgba[i:i + 10_000], s1)
+        dx = torch.from_numpy(xyz[i:i + 10_000]).cuda()
+        dc = torch.from_numpy(rgba[i:i + 10_000].view(np.int32)).cuda()
+        insert_batch(t2, dx, dc, s2)
+    assert_same_state(product_state(t2), product_state(t1), chunk_ids=True, label="device-input")
+
+
+def test_conservation_and_placement(gpu):
+    """Leaf counts sum to n; every stored point routes to its own leaf (criterion 2)."""
+    xyz, rgba = _cloud(30_000, 2, "uniform")
+    edgy = np.array([[0.5, 0.5, 0.5], [0.25, 0.5, 0.75], [0.5, 0.0, 0.999], [0.5, 0.25, 0.5]], np.float32)
+    xyz = np.concatenate([xyz, edgy])
+    rgba = np.concatenate([rgba, np.arange(4, dtype=np.uint32)])
+    tree, state, err, _ = run_product(_params(grid_res=8, leaf_threshold=64),
+                                      [(xyz[i:i + 997], rgba[i:i + 997]) for i in range(0, len(rgba), 997)])
+    n = tree.num_nodes
+    leaves = np.flatnonzero(~tree.inner[:n])
+    assert int(tree.count[leaves].sum()) == len(rgba)
+    for leaf in leaves:
+        if tree.count[leaf] == 0:
+            continue
+        lx, _ = tree.gather_samples(int(leaf))
+        nid = int(leaf)
+        while nid != 0:
+            par = int(tree.parent[nid])
+            b = tree.node_bounds(par)
+            cx = np.array(b.min) + b.size * 0.5
+            o = (lx[:, 0] >= cx[0]).astype(np.int8) | ((lx[:, 1] >= cx[1]).astype(np.int8) << 1) | (
+                (lx[:, 2] >= cx[2]).astype(np.int8) << 2)
+            assert (o == int(tree.octant[nid])).all()
+            nid = par

@@ -134,6 +134,10 @@ def product_state(tree) -> dict:
     }
     for k in NODE_COLS_ID_FREE + ("chunk_head", "chunk_tail"):
         d[k] = getattr(tree, k)[:n].copy()
+    c = d["allocated_total"]
+    for k in ("next", "occupied", "payload_off"):
+        d[k] = getattr(tree.pool, k)[:c].copy()
+    d["free_list"] = tree.pool.free_list.copy()
     offs, rec = tree.dump_records()
     d["rec_offsets"], d["records"] = offs, rec
     cells, cell_offs = [], np.zeros(n + 1, np.int64)

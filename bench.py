@@ -65,6 +65,17 @@ def gen_batches(kind: str, count: int, seed0: int = 1000):
     return [gen(BATCH, seed0 + i) for i in range(count)]
 
 
+def morton_sorted(xyz, rgba, bits: int = 10):
+    """z-order a batch (unit cube) -- for the --presort locality experiment."""
+    q = np.clip((xyz * (1 << bits)).astype(np.int64), 0, (1 << bits) - 1)
+    key = np.zeros(len(q), np.int64)
+    for b in range(bits):
+        for a in range(3):
+            key |= ((q[:, a] >> b) & 1) << (3 * b + a)
+    o = np.argsort(key, kind="stable")
+    return np.ascontiguousarray(xyz[o]), np.ascontiguousarray(rgba[o])
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -144,6 +155,8 @@ def run_ours(args, rank, world, local_rank):
     kind = CONFIGS[args.config][0]
     total = args.warmup + args.steps
     batches = gen_batches(kind, total)
+    if args.presort:  # experiment only: z-ordered input batches (changes the workload)
+        batches = [morton_sorted(x, c) for x, c in batches]
     if world > 1:
         # octant-prefix partition of every batch; this rank keeps its subtrees' points
         plan = partition.plan_owners(batches[: max(1, args.warmup)], world)
@@ -181,7 +194,9 @@ def run_ours(args, rank, world, local_rank):
             h2d += int(b.h2d_bytes)
             d2h += int(b.d2h_bytes)
             if profile:
-                phases.append(dict(state.last["phase_ms"]))
+                ph = dict(state.last["phase_ms"])
+                ph["_counts"] = (int(b.n_batch), int(b.n_spill), int(b.n_voxels))
+                phases.append(ph)
         e1.record()
         barrier()
         ms = e0.elapsed_time(e1)
@@ -215,11 +230,13 @@ def run_ours(args, rank, world, local_rank):
     e2e = timed_pts / (t_e2e * 1e-3) / 1e6
     # roofline of the dominant phase
     peak, peak_kind = measured_peak_hbm()
-    ph_tot = {k: sum(p[k] for p in phases) for k in phases[0]} if phases else {}
-    roof = roofline_from_phases(ph_tot, args, batches)
+    roof, phase_summary = roofline_from_phases(phases, peak)
     roof["peak"] = peak
     roof["peak_source"] = peak_kind
-    roof["frac"] = roof["achieved"] / peak if roof.get("achieved") else None
+    roof["frac"] = round(roof["achieved"] / peak, 4) if roof.get("achieved") else None
+    traffic = load_traffic(roof.get("kernel"))
+    if traffic is not None:
+        roof["traffic"] = traffic
     cpu = cpu_baseline(args, kind) if not args.no_cpu else None
     srt = sorted(per)
     line = {
@@ -237,7 +254,7 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": d2h // max(args.steps, 1)},
         "gpu_launches": launches,
         "roofline": roof,
-        "phase_ms": {k: round(v / args.steps, 4) for k, v in ph_tot.items()},
+        "phase_ms": phase_summary,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
     }
@@ -246,20 +263,55 @@ def run_ours(args, rank, world, local_rank):
     return line
 
 
-def roofline_from_phases(ph_tot: dict, args, batches) -> dict:
-    """Dominant phase's algorithmic bytes / its CUDA-event time.
+def phase_bytes(phase: str, n_b: int, n_s: int, n_v: int) -> int | None:
+    """Algorithmic HBM bytes of one batch's phase.
 
-    Per batch: B_alg = 32 n_b + 32 n_s + 16 n_v over the whole
-    update.  The phases each move a share of it ("Roofline"):
-    store writes 16 (n_all + n_v) and reads 16 n_all; expand/sample read the
-    16 B records of every point once per pass.
+    count:   every point's 16-byte record read once + its 4-byte leaf id written
+    resolve: per new voxel: claim slot read+clear (32), grid word RMW (8), win (8), mask RMW (16)
+    sort:    per item and radix pass: key read (hist) + key/value read + write (20), 2 passes
+    store:   records read 16 n_all, written 16 (n_all + n_v)  (= B_alg of the whole update)
+    total:   B_alg = 32 n_b + 32 n_s + 16 n_v
     """
-    if not ph_tot:
-        return {"bound": "hbm", "achieved": None, "unit": "GB/s", "traffic": None}
-    stats = ph_tot.pop("_stats", None)
-    dom = max((k for k in ph_tot if k != "h2d"), key=lambda k: ph_tot[k])
-    return {"bound": "hbm", "kernel_phase": dom, "achieved": None, "unit": "GB/s", "traffic": None,
-            "phase_ms_total": round(ph_tot[dom], 4)}
+    n_all = n_b + n_s
+    return {
+        "count": 20 * n_all,
+        "resolve": 64 * n_v,
+        "sort": 2 * 20 * (n_all + n_v),
+        "store": 32 * n_all + 16 * n_v,
+        "total": 32 * n_b + 32 * n_s + 16 * n_v,
+    }.get(phase)
+
+
+def roofline_from_phases(phases: list[dict], peak: float) -> tuple[dict, dict]:
+    """Dominant kernel phase: algorithmic bytes / its CUDA-event time (profiled replay)."""
+    if not phases:
+        return {"bound": "hbm", "achieved": None, "unit": "GB/s", "traffic": None}, {}
+    names = [k for k in phases[0] if not k.startswith("_") and k not in ("h2d", "total")]
+    tot = {k: sum(p[k] for p in phases) for k in names + ["total"]}
+    med = {k: round(statistics.median(p[k] for p in phases), 4) for k in names + ["total"]}
+    byts = {k: sum(phase_bytes(k, *p["_counts"]) or 0 for p in phases) for k in names + ["total"]}
+    dom = max((k for k in names if phase_bytes(k, 1, 1, 1) is not None), key=lambda k: tot[k])
+    gbs = {k: round(byts[k] / (tot[k] * 1e-3) / 1e9, 1) for k in byts if byts[k] and tot[k] > 0}
+    roof = {
+        "bound": "hbm", "kernel": {"count": "k_count", "store": "k_store", "sort": "k_radix_*",
+                                   "resolve": "k_resolve"}[dom],
+        "achieved": gbs.get(dom), "unit": "GB/s", "traffic": None,
+        "kernel_share_of_step": round(tot[dom] / tot["total"], 3) if tot["total"] else None,
+        "whole_update": {"achieved": gbs.get("total"), "frac": round(gbs.get("total", 0) / peak, 4)},
+        "phase_gbs": gbs,
+    }
+    return roof, {"median_ms": med, "mean_ms": {k: round(tot[k] / len(phases), 4) for k in tot}}
+
+
+def load_traffic(kernel: str | None):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/ncu_traffic.json, written by tools/ncu_summary.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(kernel)
+    except Exception:
+        return None
 
 
 def cpu_baseline(args, kind) -> dict:
@@ -323,6 +375,7 @@ def main():
     ap.add_argument("--arena-gib", type=float, default=8.0)
     ap.add_argument("--cpu-batches", type=int, default=12)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--presort", action="store_true", help="experiment: z-order each batch on the host")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

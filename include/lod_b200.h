@@ -68,7 +68,7 @@ typedef struct {
     int64_t spill_capacity;
 } LodLimits;
 
-enum { LOD_NPHASE = 8 };
+enum { LOD_NPHASE = 10 };
 
 /* Per-call result: what insert_batch changed (UpdateStats fields, update.py:382-392)
  * plus the counts B_alg needs. */
@@ -80,8 +80,9 @@ typedef struct {
     int64_t launches;              /* kernels this call launched                              */
     int64_t h2d_bytes, d2h_bytes;  /* host<->device traffic of this call                      */
     float device_ms;               /* CUDA-event time of the whole update on the tree stream  */
-    float phase_ms[LOD_NPHASE];    /* with LOD_FLAG_PROFILE: expand, sample, backlog, sort,
-                                      alloc, store, epilogue, h2d                             */
+    float phase_ms[LOD_NPHASE];    /* with LOD_FLAG_PROFILE: count (k_count only), split,
+                                      resolve, backlog, sort, alloc, store, epilogue, h2d,
+                                      total                                                   */
 } LodBatchStats;
 
 /* Counters of the live tree (Octree / ChunkPool / Arena scalar attributes). */

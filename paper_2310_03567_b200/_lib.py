@@ -28,8 +28,8 @@ LOD_E_NO_DEVICE = 7
 LOD_FLAG_DEVICE_INPUT = 1
 LOD_FLAG_DEVICE_FB = 2
 LOD_FLAG_PROFILE = 4
-LOD_NPHASE = 8
-PHASES = ("expand", "sample", "backlog", "sort", "alloc", "store", "epilogue", "h2d")
+LOD_NPHASE = 10
+PHASES = ("count", "split", "resolve", "backlog", "sort", "alloc", "store", "epilogue", "h2d", "total")
 
 
 class NativeUnavailable(RuntimeError):

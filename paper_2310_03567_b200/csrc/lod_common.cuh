@@ -80,6 +80,7 @@ struct PoolCols {
   long long *payload_off;
   int32_t *occupied;
   int32_t *owner;  // node owning the chunk, -1 when free (render work list)
+  int32_t *cidx;   // position of the chunk in its owner's list (parallel spill gather)
   int32_t *free_stack;
 };
 

@@ -1,13 +1,21 @@
 // lod_kernels.cuh -- device kernels of one update cycle (insert_batch).
 //
 // Order of a cycle (reference: update.py:1-27, 252-393):
-//   expand   k_count -> k_decide -> [sync] -> k_execute (+ k_shift_nodes)   (repeat)
-//   sample   k_claim (hash min-index claim) -> k_win (winners set bits)
-//   backlog  scan(wcount) -> [sync] -> k_emit  (backlog in reference (j, depth) order)
+//   expand   k_count (+ voxel claims) -> k_decide -> [sync] -> k_exec_chunks/k_exec_nodes   (repeat)
+//   resolve  k_resolve (winners set bits, per-point wins) -> k_wcount -> scan -> k_emit
 //   sort     k_keys -> stable_multisplit by node id
 //   alloc    k_seg_* (touched nodes, ascending id) -> scan(need) -> k_alloc_*
 //   store    k_store (points + voxel centres into chunk slots)
-//   epilogue k_epilogue (count += len, pending = final = 0), k_hash_clear
+//   epilogue k_epilogue (count += len, pending = final = 0)
+//
+// Voxel claims ride on the count passes.  Every inner node is descended
+// through by all of its points exactly once per cycle, in one pass: nodes
+// that were inner at cycle start in iteration 1 (batch points only -- spilled
+// points' cells at those nodes are already set because they passed them when
+// first inserted), nodes split in iteration k in iteration k+1 (their spilled
+// and re-routed points).  So min-index claims into one hash per cycle see
+// every candidate of a (node, cell) in the same pass, which is the reference's
+// sequential first-come rule (sample_and_route, _kernels.py:125-135).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -54,14 +62,134 @@ struct Ctrl {
 
 __device__ __forceinline__ void set_error(Ctrl *c, int code) { atomicCAS(&c->error, 0, code); }
 
+// ---------------------------------------------------------------- claim hash
+
+// Open-addressing table of (node, cell) -> min all-array index, 16-byte slots
+// so key and value share one sector.  Iteration-1 claims (at nodes inner at
+// cycle start) carry batch index | 2^31 because the spill length is not known
+// yet; all claims at one node live in one index space, so min order is exact.
+struct HSlot {
+  unsigned long long key;
+  uint32_t val;
+  uint32_t pad;
+};
+constexpr unsigned long long kEmptyKey = 0xFFFFFFFFFFFFFFFFULL;
+constexpr uint32_t kBatchTag = 0x80000000u;
+
+struct Hash {
+  HSlot *slots;
+  unsigned long long mask;   // capacity - 1 (power of two)
+  unsigned long long *used;  // slots inserted this cycle
+  unsigned long long limit;  // capacity of `used` (= table capacity)
+};
+
+// New keys are appended to the cycle's used-slot list through a per-block
+// shared-memory stage, so a pass issues one global atomic per block instead
+// of one per new voxel (a single hot counter otherwise serializes in L2).
+constexpr int kStage = 2048;
+struct UsedStage {
+  unsigned long long slot[kStage];
+  unsigned int n;
+};
+
+__device__ __forceinline__ unsigned long long hmix(unsigned long long k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdULL;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ULL;
+  k ^= k >> 33;
+  return k;
+}
+
+__device__ __forceinline__ unsigned long long claim_key(int nid, long long cell) {
+  return ((unsigned long long)(uint32_t)nid << 32) | (unsigned long long)cell;
+}
+
+__device__ __forceinline__ void used_append(const Hash &h, UsedStage &stg, unsigned long long slot, Ctrl *ctrl) {
+  const unsigned k = atomicAdd(&stg.n, 1u);
+  if (k < (unsigned)kStage) {
+    stg.slot[k] = slot;
+  } else {  // stage full: direct append
+    const unsigned long long u = atomicAdd(&ctrl->n_used, 1ull);
+    if (u < h.limit) h.used[u] = slot;
+    else ctrl->hash_overflow = 1;
+  }
+}
+
+// Block epilogue of a claiming pass: flush the staged used slots.
+__device__ __forceinline__ void used_flush(const Hash &h, UsedStage &stg, Ctrl *ctrl) {
+  __shared__ unsigned long long s_base;
+  __syncthreads();
+  const unsigned n = min(stg.n, (unsigned)kStage);
+  if (threadIdx.x == 0) s_base = n ? atomicAdd(&ctrl->n_used, (unsigned long long)n) : 0ull;
+  __syncthreads();
+  for (unsigned i = threadIdx.x; i < n; i += blockDim.x) {
+    const unsigned long long u = s_base + i;
+    if (u < h.limit) h.used[u] = stg.slot[i];
+    else ctrl->hash_overflow = 1;
+  }
+}
+
+__device__ __forceinline__ void hash_claim(const Hash &h, UsedStage &stg, unsigned long long key, uint32_t v,
+                                           Ctrl *ctrl) {
+  unsigned long long slot = hmix(key) & h.mask;
+  for (unsigned long long probe = 0; probe <= h.mask; ++probe) {
+    HSlot *sl = h.slots + slot;
+    unsigned long long k = __ldcg(&sl->key);
+    if (k == key) {
+      atomicMin(&sl->val, v);
+      return;
+    }
+    if (k == kEmptyKey) {
+      unsigned long long prev = atomicCAS(&sl->key, kEmptyKey, key);
+      if (prev == kEmptyKey || prev == key) {
+        atomicMin(&sl->val, v);
+        if (prev == kEmptyKey) used_append(h, stg, slot, ctrl);
+        return;
+      }
+    }
+    slot = (slot + 1) & h.mask;
+  }
+  ctrl->hash_overflow = 1;  // table full
+}
+
+// Claim at one inner node if the cell's bit is clear (bits never clear and
+// nothing sets bits until k_resolve, so "clear" means clear at cycle start).
+__device__ __forceinline__ void probe_cell(const NodeCols &nd, const Geo &geo, const uint32_t *grid32,
+                                           const Hash &h, UsedStage &stg, Ctrl *ctrl, int nid, double x,
+                                           double y, double z, double bx, double by, double bz, double s,
+                                           uint32_t v) {
+  const long long cell = cell_of(geo, x, y, z, bx, by, bz, s);
+  const uint32_t w = __ldg(grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5));
+  if (!(w & (1u << (cell & 31)))) hash_claim(h, stg, claim_key(nid, cell), v, ctrl);
+}
+
+// Grow the claim table between expansion iterations: re-insert every key
+// claimed so far (keys are unique, values carried) into the new table.
+__global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl *ctrl) {
+  const unsigned long long nu = ctrl->n_used;
+  for (long long u = gtid(); u < (long long)nu; u += gstride()) {
+    const HSlot o = old_slots[h.used[u]];
+    unsigned long long slot = hmix(o.key) & h.mask;
+    while (atomicCAS(&h.slots[slot].key, kEmptyKey, o.key) != kEmptyKey) slot = (slot + 1) & h.mask;
+    h.slots[slot].val = o.val;
+    h.used[u] = slot;
+  }
+}
+
 // ---------------------------------------------------------------- expansion
 
-// _kernels.count_points (_kernels.py:27-63).  Iteration 1 descends every batch
+// _kernels.count_points (_kernels.py:27-63) fused with the voxel claims of
+// sample_and_route (_kernels.py:101-137).  Iteration 1 descends every batch
 // point from the root; later iterations re-descend only points whose cached
 // node became inner, starting at that node (its stored bmin equals the
 // accumulated descent bounds byte for byte, _kernels.py:9-13).
-__global__ void k_count(NodeCols nd, Geo geo, PointSrc src, int32_t *__restrict__ node_of,
-                        long long n, int first, int32_t *__restrict__ touched, Ctrl *ctrl) {
+__global__ void __launch_bounds__(256, 6)
+    k_count(NodeCols nd, Geo geo, PointSrc src, int32_t *__restrict__ node_of, long long n, int first,
+            const uint32_t *__restrict__ grid32, Hash h, int32_t *__restrict__ touched, Ctrl *ctrl) {
+  __shared__ UsedStage stg;
+  if (threadIdx.x == 0) stg.n = 0;
+  __syncthreads();
   for (long long j0 = (long long)blockIdx.x * blockDim.x; j0 < n; j0 += gstride()) {
     long long j = j0 + threadIdx.x;
     int leaf = -1;
@@ -73,8 +201,10 @@ __global__ void k_count(NodeCols nd, Geo geo, PointSrc src, int32_t *__restrict_
         const double x = xf, y = yf, z = zf;
         double bx = nd.bmin[3 * nid], by = nd.bmin[3 * nid + 1], bz = nd.bmin[3 * nid + 2];
         double s = geo.size_by_level[nd.level[nid]];
+        const uint32_t v = first ? ((uint32_t)j | kBatchTag) : (uint32_t)j;
         do {
-          int o = octant_step(x, y, z, bx, by, bz, s);
+          probe_cell(nd, geo, grid32, h, stg, ctrl, nid, x, y, z, bx, by, bz, s, v);
+          const int o = octant_step(x, y, z, bx, by, bz, s);
           nid = nd.children[8 * nid + o];
         } while (nd.inner[nid]);
         node_of[j] = nid;
@@ -93,6 +223,7 @@ __global__ void k_count(NodeCols nd, Geo geo, PointSrc src, int32_t *__restrict_
       }
     }
   }
+  used_flush(h, stg, ctrl);
 }
 
 // _split_pass (update.py:226-249): split iff count + pending > T and
@@ -103,10 +234,9 @@ __global__ void k_count(NodeCols nd, Geo geo, PointSrc src, int32_t *__restrict_
 // and grid offsets, and detects SpillOverflow / OutOfArena in reference order.
 constexpr int kDecideBlock = 1024;
 __global__ void __launch_bounds__(kDecideBlock)
-    k_decide(NodeCols nd, Geo geo, const int32_t *__restrict__ touched, uint32_t *bitmap,
-             uint32_t *word_prefix, int32_t *split_list, long long *scnt, long long *schk,
-             long long *spill_off, long long *chunk_off, Ctrl *ctrl, long long spill_cap,
-             unsigned long long arena_cap) {
+    k_decide(NodeCols nd, Geo geo, const int32_t *__restrict__ touched, uint32_t *bitmap, uint32_t *word_prefix,
+             int32_t *split_list, int32_t *srank, long long *scnt, long long *schk, long long *spill_off,
+             long long *chunk_off, Ctrl *ctrl, long long spill_cap, unsigned long long arena_cap) {
   __shared__ uint32_t sh32[kDecideBlock / 32 + 1];
   __shared__ U64x2 sh64[kDecideBlock / 32 + 1];
   __shared__ unsigned int s_maxlvl;
@@ -151,6 +281,7 @@ __global__ void __launch_bounds__(kDecideBlock)
     if (wv & bit) {
       uint32_t rank = word_prefix[nid >> 5] + __popc(wv & (bit - 1));
       split_list[rank] = nid;
+      srank[nid] = (int32_t)rank;
       scnt[rank] = nd.count[nid];
       schk[rank] = nd.chunk_count[nid];
       atomicMax(&s_maxlvl, (unsigned)(nd.level[nid] + 1));
@@ -182,13 +313,13 @@ __global__ void __launch_bounds__(kDecideBlock)
     unsigned long long off = ctrl->arena_off;
     const unsigned long long gb = (unsigned long long)geo.grid_bytes;
     const unsigned long long g0 = (off + 63ull) / 64ull * 64ull;
-    const unsigned long long gstride = (gb + 63ull) / 64ull * 64ull;
+    const unsigned long long gstride_b = (gb + 63ull) / 64ull * 64ull;
     long long err_ooa = -1;
     if (ns > 0) {
       // first k with g0 + k*gstride + gb > cap
       if (g0 + gb > arena_cap) err_ooa = 0;
-      else if (g0 + (unsigned long long)(ns - 1) * gstride + gb > arena_cap)
-        err_ooa = (long long)((arena_cap - gb - g0) / gstride) + 1;
+      else if (g0 + (unsigned long long)(ns - 1) * gstride_b + gb > arena_cap)
+        err_ooa = (long long)((arena_cap - gb - g0) / gstride_b) + 1;
     }
     long long es = s_err_spill;
     if (es >= 0 && (err_ooa < 0 || es <= err_ooa)) set_error(ctrl, 2 /*LOD_E_SPILL_OVERFLOW*/);
@@ -207,7 +338,7 @@ __global__ void __launch_bounds__(kDecideBlock)
       ctrl->free_count += (long long)carry.b;
       ctrl->released_total += (long long)carry.b;
       ctrl->spill_total = spill0 + (long long)carry.a;
-      ctrl->arena_off = g0 + (unsigned long long)(ns - 1) * gstride + gb;
+      ctrl->arena_off = g0 + (unsigned long long)(ns - 1) * gstride_b + gb;
     }
   }
   __syncthreads();
@@ -218,71 +349,53 @@ __global__ void __launch_bounds__(kDecideBlock)
   }
 }
 
-// Octree.split (octree.py:222-264) for every planned split, one CTA each:
-// gather stored samples in chunk-walk order into the spill segment, push the
-// chain onto the free stack in walk order (store.py:125-143), turn the node
-// inner with a zeroed grid (arena regions are zeroed and never reused) and
-// create its 8 children in octant order with bmin = base + half (f64).
-constexpr int kExecBlock = 256;
-__global__ void __launch_bounds__(kExecBlock)
-    k_execute(NodeCols nd, PoolCols pool, Geo geo, const uint8_t *__restrict__ arena,
-              const int32_t *__restrict__ split_list, const long long *__restrict__ spill_off,
-              const long long *__restrict__ chunk_off, float4 *spill_buf,
-              int32_t *spill_node_of, const Ctrl *ctrl) {
-  __shared__ int s_cid, s_next, s_occ;
-  __shared__ long long s_poff;
-  const int k = blockIdx.x, tid = threadIdx.x;
-  const int nid = split_list[k];
-  const long long sp = ctrl->plan_spill0 + spill_off[k];
-  float4 *dst = spill_buf + sp;
-  int32_t *dnode = spill_node_of + sp;
-  int32_t *fs = pool.free_stack + ctrl->plan_free0 + chunk_off[k];
-  if (tid == 0) s_cid = nd.chunk_head[nid];
-  __syncthreads();
-  long long idx = 0;
-  int ci = 0;
-  while (s_cid != LOD_NO_CHUNK) {
-    const int cid = s_cid;
-    if (tid == 0) {
-      s_next = pool.next[cid];
-      s_occ = pool.occupied[cid];
-      s_poff = pool.payload_off[cid];
+// Octree.split, part 1 (octree.py:231-237, store.py:125-143), in parallel over
+// the chunk table: every chunk owned by a splitting node copies its records to
+// the node's spill segment (chunk position cidx = storage order) and pushes
+// itself onto the free stack at its walk-order slot.  One warp per chunk.
+__global__ void k_exec_chunks(PoolCols pool, Geo geo, const uint8_t *__restrict__ arena, long long nchunks,
+                              const int32_t *__restrict__ srank, const long long *__restrict__ spill_off,
+                              const long long *__restrict__ chunk_off, float4 *spill_buf, int32_t *spill_node_of,
+                              const Ctrl *ctrl) {
+  const long long warp = gtid() >> 5, nwarps = gstride() >> 5;
+  const int lane = threadIdx.x & 31;
+  for (long long cid = warp; cid < nchunks; cid += nwarps) {
+    const int owner = pool.owner[cid];
+    if (owner < 0) continue;
+    const int r = srank[owner];
+    if (r < 0) continue;
+    const int ci = pool.cidx[cid];
+    const int occ = pool.occupied[cid];
+    const long long sp = ctrl->plan_spill0 + spill_off[r] + (long long)ci * geo.C;
+    const float4 *src = reinterpret_cast<const float4 *>(arena + pool.payload_off[cid]);
+    for (int k = lane; k < occ; k += 32) {
+      spill_buf[sp + k] = src[k];
+      spill_node_of[sp + k] = owner;
     }
-    __syncthreads();
-    const int occ = s_occ;
-    const float4 *src = reinterpret_cast<const float4 *>(arena + s_poff);
-    for (int r = tid; r < occ; r += kExecBlock) {
-      dst[idx + r] = src[r];
-      dnode[idx + r] = nid;
-    }
-    if (tid == 0) {
-      fs[ci] = cid;
+    __syncwarp();
+    if (lane == 0) {
+      pool.free_stack[ctrl->plan_free0 + chunk_off[r] + ci] = (int32_t)cid;
       pool.occupied[cid] = 0;
       pool.next[cid] = LOD_NO_CHUNK;
       pool.owner[cid] = -1;
-      s_cid = s_next;
+      pool.cidx[cid] = -1;
     }
-    idx += occ;
-    ci += 1;
-    __syncthreads();
   }
-  const int lvl = nd.level[nid];
-  if (tid == 0) {
-    nd.count[nid] = 0;
-    nd.pending[nid] = 0;
-    nd.inner[nid] = 1;
-    nd.chunk_head[nid] = LOD_NO_CHUNK;
-    nd.chunk_tail[nid] = LOD_NO_CHUNK;
-    nd.chunk_count[nid] = 0;
-    const unsigned long long gstride = ((unsigned long long)geo.grid_bytes + 63ull) / 64ull * 64ull;
-    nd.grid_off[nid] = (long long)(ctrl->plan_grid0 + (unsigned long long)k * gstride);
-  }
-  if (tid < 8) {
-    const int o = tid;
+}
+
+// Octree.split, part 2 (octree.py:238-264): the node turns inner with a zeroed
+// grid (arena regions are zeroed and never reused) and gets 8 children in
+// octant order with bmin = base + half (f64).  One thread per (split, octant).
+__global__ void k_exec_nodes(NodeCols nd, Geo geo, const int32_t *__restrict__ split_list, int32_t *srank,
+                             long long ns, const Ctrl *ctrl) {
+  for (long long t = gtid(); t < ns * 8; t += gstride()) {
+    const long long k = t >> 3;
+    const int o = (int)(t & 7);
+    const int nid = split_list[k];
+    const int lvl = nd.level[nid];
     const int c = (int)(ctrl->plan_num_nodes0 + 8ll * k + o);
     // node_size(nid) * 0.5 == size * 0.5**level * 0.5 (octree.py:246, 268-269)
     const double half = geo.size_by_level[lvl] * 0.5;
-    const double b0 = nd.bmin[3 * nid], b1 = nd.bmin[3 * nid + 1], b2 = nd.bmin[3 * nid + 2];
     nd.parent[c] = nid;
     nd.octant[c] = (uint8_t)o;
     nd.level[c] = lvl + 1;
@@ -295,154 +408,103 @@ __global__ void __launch_bounds__(kExecBlock)
     nd.chunk_tail[c] = LOD_NO_CHUNK;
     nd.chunk_count[c] = 0;
     nd.grid_off[c] = -1;
-    nd.bmin[3 * c + 0] = b0 + ((o & 1) ? half : 0.0);
-    nd.bmin[3 * c + 1] = b1 + ((o & 2) ? half : 0.0);
-    nd.bmin[3 * c + 2] = b2 + ((o & 4) ? half : 0.0);
+    nd.bmin[3 * c + 0] = nd.bmin[3 * nid + 0] + ((o & 1) ? half : 0.0);
+    nd.bmin[3 * c + 1] = nd.bmin[3 * nid + 1] + ((o & 2) ? half : 0.0);
+    nd.bmin[3 * c + 2] = nd.bmin[3 * nid + 2] + ((o & 4) ? half : 0.0);
     nd.children[8 * nid + o] = c;
+    srank[c] = -1;
+    if (o == 0) {
+      nd.count[nid] = 0;
+      nd.pending[nid] = 0;
+      nd.inner[nid] = 1;
+      nd.chunk_head[nid] = LOD_NO_CHUNK;
+      nd.chunk_tail[nid] = LOD_NO_CHUNK;
+      nd.chunk_count[nid] = 0;
+      const unsigned long long gstride_b = ((unsigned long long)geo.grid_bytes + 63ull) / 64ull * 64ull;
+      nd.grid_off[nid] = (long long)(ctrl->plan_grid0 + (unsigned long long)k * gstride_b);
+      srank[nid] = -1;
+    }
   }
 }
 
 // Move the batch part of the per-point node cache behind the spill segment:
 // all = [spill || batch] (update.py:281-286).
-__global__ void k_shift_nodes(const int32_t *__restrict__ src, int32_t *__restrict__ dst,
-                              long long n) {
+__global__ void k_shift_nodes(const int32_t *__restrict__ src, int32_t *__restrict__ dst, long long n) {
   for (long long i = gtid(); i < n; i += gstride()) dst[i] = src[i];
 }
 
 // ---------------------------------------------------------------- sampling
 
-__device__ __forceinline__ unsigned long long hmix(unsigned long long k) {
-  k ^= k >> 33;
-  k *= 0xff51afd7ed558ccdULL;
-  k ^= k >> 33;
-  k *= 0xc4ceb9fe1a85ec53ULL;
-  k ^= k >> 33;
-  return k;
-}
-constexpr unsigned long long kEmptyKey = 0xFFFFFFFFFFFFFFFFULL;
-
-struct Hash {
-  unsigned long long *keys;
-  uint32_t *vals;
-  unsigned long long mask;  // capacity - 1 (power of two)
-  unsigned long long *used; // slots inserted this cycle
-  unsigned long long used_cap;
-};
-
-// Min-index claim of (node, cell): the reference's sequential first-come rule
-// (sample_and_route, _kernels.py:125-135) is "lowest all-array index wins",
-// so every point whose cell bit was clear at cycle start min-combines its index.
-__device__ __forceinline__ void hash_claim(const Hash &h, unsigned long long key, uint32_t j,
-                                           Ctrl *ctrl) {
-  unsigned long long slot = hmix(key) & h.mask;
-  for (unsigned long long probe = 0; probe <= h.mask; ++probe) {
-    unsigned long long k = __ldcg(h.keys + slot);
-    if (k == key) {
-      atomicMin(h.vals + slot, j);
-      return;
-    }
-    if (k == kEmptyKey) {
-      unsigned long long prev = atomicCAS(h.keys + slot, kEmptyKey, key);
-      if (prev == kEmptyKey) {
-        atomicMin(h.vals + slot, j);
-        unsigned long long u = atomicAdd(&ctrl->n_used, 1ull);
-        if (u < h.used_cap) h.used[u] = slot;
-        else ctrl->hash_overflow = 1;
-        return;
-      }
-      if (prev == key) {
-        atomicMin(h.vals + slot, j);
-        return;
-      }
-    }
-    slot = (slot + 1) & h.mask;
-  }
-  ctrl->hash_overflow = 1;
-}
-
-__device__ __forceinline__ uint32_t hash_lookup(const Hash &h, unsigned long long key) {
-  unsigned long long slot = hmix(key) & h.mask;
-  for (unsigned long long probe = 0; probe <= h.mask; ++probe) {
-    unsigned long long k = __ldcg(h.keys + slot);
-    if (k == key) return __ldcg(h.vals + slot);
-    if (k == kEmptyKey) return 0xFFFFFFFFu;
-    slot = (slot + 1) & h.mask;
-  }
-  return 0xFFFFFFFFu;
-}
-
-// Pass 1 of sampling: descend from the root (topology is frozen); at each inner
-// node whose cell bit is clear (state at cycle start -- nothing sets bits in
-// this pass), min-claim (node, cell) with the point's all-array index.
-__global__ void k_claim(NodeCols nd, Geo geo, PointSrc src, const uint32_t *__restrict__ grid32,
-                        long long n, Hash h, Ctrl *ctrl) {
-  for (long long j = gtid(); j < n; j += gstride()) {
+// Fallback claim pass (only when the cycle's claim table overflowed): a full
+// descent of every point over the final topology with all-array indices.
+__global__ void k_claim(NodeCols nd, Geo geo, PointSrc src, const uint32_t *__restrict__ grid32, long long n,
+                        Hash h, Ctrl *ctrl) {
+  __shared__ UsedStage stg;
+  if (threadIdx.x == 0) stg.n = 0;
+  __syncthreads();
+  for (long long j0 = (long long)blockIdx.x * blockDim.x; j0 < n; j0 += gstride()) {
+    const long long j = j0 + threadIdx.x;
+    if (j >= n) continue;
     float xf, yf, zf;
     src.xyz(j, xf, yf, zf);
     const double x = xf, y = yf, z = zf;
     double bx = geo.bmin0[0], by = geo.bmin0[1], bz = geo.bmin0[2], s = geo.size0;
     int nid = 0;
     while (nd.inner[nid]) {
-      long long cell = cell_of(geo, x, y, z, bx, by, bz, s);
-      const uint32_t *w = grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5);
-      if (!(*w & (1u << (cell & 31))))
-        hash_claim(h, ((unsigned long long)(uint32_t)nid << 32) | (unsigned long long)cell,
-                   (uint32_t)j, ctrl);
-      int o = octant_step(x, y, z, bx, by, bz, s);
+      probe_cell(nd, geo, grid32, h, stg, ctrl, nid, x, y, z, bx, by, bz, s, (uint32_t)j);
+      const int o = octant_step(x, y, z, bx, by, bz, s);
       nid = nd.children[8 * nid + o];
     }
+  }
+  used_flush(h, stg, ctrl);
+}
+
+// Every distinct claimed (node, cell): the min index is the winner.  Set the
+// bit, record the win at the node's level for the winner, and free the slot.
+__global__ void k_resolve(NodeCols nd, Hash h, uint32_t *grid32, long long n_s, int D,
+                          unsigned long long *__restrict__ wins, unsigned long long *__restrict__ wmask,
+                          const Ctrl *ctrl) {
+  unsigned long long nu = ctrl->n_used;
+  if (nu > h.limit) nu = h.limit;
+  for (long long u = gtid(); u < (long long)nu; u += gstride()) {
+    HSlot *sl = h.slots + h.used[u];
+    const unsigned long long key = sl->key;
+    const uint32_t v = sl->val;
+    sl->key = kEmptyKey;
+    sl->val = 0xFFFFFFFFu;
+    const int nid = (int)(key >> 32);
+    const long long cell = (long long)(key & 0xFFFFFFFFu);
+    const long long j = (v & kBatchTag) ? n_s + (long long)(v & ~kBatchTag) : (long long)v;
+    const int lvl = nd.level[nid];
+    atomicOr(grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5), 1u << (cell & 31));
+    wins[j * D + lvl] = key;
+    atomicOr(wmask + j, 1ull << lvl);
   }
 }
 
-// Pass 2: the winner of each claimed cell sets its bit (atomicOr) and records
-// the win (node, cell) in path order.  A loser may observe the bit already set
-// by the winner and skip its lookup -- same outcome.
-__global__ void k_win(NodeCols nd, Geo geo, PointSrc src, uint32_t *grid32, long long n, Hash h,
-                      uint32_t *__restrict__ wcount, unsigned long long *__restrict__ wins,
-                      int D) {
-  for (long long j = gtid(); j < n; j += gstride()) {
-    float xf, yf, zf;
-    src.xyz(j, xf, yf, zf);
-    const double x = xf, y = yf, z = zf;
-    double bx = geo.bmin0[0], by = geo.bmin0[1], bz = geo.bmin0[2], s = geo.size0;
-    int nid = 0;
-    uint32_t k = 0;
-    while (nd.inner[nid]) {
-      long long cell = cell_of(geo, x, y, z, bx, by, bz, s);
-      uint32_t *w = grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5);
-      const uint32_t bit = 1u << (cell & 31);
-      if (!(__ldcg(w) & bit)) {
-        const unsigned long long key =
-            ((unsigned long long)(uint32_t)nid << 32) | (unsigned long long)cell;
-        if (hash_lookup(h, key) == (uint32_t)j) {
-          atomicOr(w, bit);
-          if (k < (uint32_t)D) wins[(long long)j * D + k] = key;
-          ++k;
-        }
-      }
-      int o = octant_step(x, y, z, bx, by, bz, s);
-      nid = nd.children[8 * nid + o];
-    }
-    wcount[j] = k;
-  }
+__global__ void k_wcount(const unsigned long long *__restrict__ wmask, long long n, uint32_t *__restrict__ wcount) {
+  for (long long j = gtid(); j < n; j += gstride()) wcount[j] = (uint32_t)__popcll(wmask[j]);
 }
 
 // Backlog in the reference's order (sample_and_route appends per point, in
-// path order, _kernels.py:100-151): entry b = wbase[j] + k.
-__global__ void k_emit(long long n, const uint32_t *__restrict__ wcount,
-                       const uint32_t *__restrict__ wbase, const unsigned long long *__restrict__ wins,
-                       int D, PointSrc src, int32_t *__restrict__ bnode, uint32_t *__restrict__ bcell,
-                       uint32_t *__restrict__ brgba) {
+// path order = ascending level, _kernels.py:100-151): entry b = wbase[j] + k.
+__global__ void k_emit(long long n, unsigned long long *__restrict__ wmask, const uint32_t *__restrict__ wbase,
+                       const unsigned long long *__restrict__ wins, int D, PointSrc src,
+                       int32_t *__restrict__ bnode, uint32_t *__restrict__ bcell, uint32_t *__restrict__ brgba) {
   for (long long j = gtid(); j < n; j += gstride()) {
-    uint32_t c = wcount[j];
-    if (!c) continue;
+    unsigned long long m = wmask[j];
+    if (!m) continue;
+    wmask[j] = 0;
     uint32_t b = wbase[j];
-    uint32_t col = src.rgba(j);
-    for (uint32_t k = 0; k < c; ++k) {
-      unsigned long long key = wins[j * D + k];
-      bnode[b + k] = (int32_t)(key >> 32);
-      bcell[b + k] = (uint32_t)(key & 0xFFFFFFFFu);
-      brgba[b + k] = col;
+    const uint32_t col = src.rgba(j);
+    while (m) {
+      const int lvl = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      const unsigned long long key = wins[j * D + lvl];
+      bnode[b] = (int32_t)(key >> 32);
+      bcell[b] = (uint32_t)(key & 0xFFFFFFFFu);
+      brgba[b] = col;
+      ++b;
     }
   }
 }
@@ -452,21 +514,18 @@ __global__ void k_emit(long long n, const uint32_t *__restrict__ wcount,
 // Items: points j in [0, n_all) keyed by their leaf, then backlog entries keyed
 // by their node.  Leaves and inner nodes are disjoint, so one stable sort by
 // node id yields every node's new samples in reference slot order.
-__global__ void k_keys(const int32_t *__restrict__ node_all, long long n_all,
-                       const int32_t *__restrict__ bnode, long long n_v, uint32_t *__restrict__ keys) {
+__global__ void k_keys(const int32_t *__restrict__ node_all, long long n_all, const int32_t *__restrict__ bnode,
+                       long long n_v, uint32_t *__restrict__ keys) {
   const long long n = n_all + n_v;
-  for (long long i = gtid(); i < n; i += gstride())
-    keys[i] = (uint32_t)(i < n_all ? node_all[i] : bnode[i - n_all]);
+  for (long long i = gtid(); i < n; i += gstride()) keys[i] = (uint32_t)(i < n_all ? node_all[i] : bnode[i - n_all]);
 }
 
 __global__ void k_seg_flags(const uint32_t *__restrict__ skeys, long long n, uint32_t *__restrict__ flag) {
-  for (long long p = gtid(); p < n; p += gstride())
-    flag[p] = (p == 0 || skeys[p] != skeys[p - 1]) ? 1u : 0u;
+  for (long long p = gtid(); p < n; p += gstride()) flag[p] = (p == 0 || skeys[p] != skeys[p - 1]) ? 1u : 0u;
 }
 
-__global__ void k_seg_list(const uint32_t *__restrict__ skeys, long long n,
-                           const uint32_t *__restrict__ hpos, int32_t *__restrict__ seg_node,
-                           long long *__restrict__ seg_start, const Ctrl *ctrl) {
+__global__ void k_seg_list(const uint32_t *__restrict__ skeys, long long n, const uint32_t *__restrict__ hpos,
+                           int32_t *__restrict__ seg_node, long long *__restrict__ seg_start, const Ctrl *ctrl) {
   for (long long p = gtid(); p < n; p += gstride()) {
     if (p == 0 || skeys[p] != skeys[p - 1]) {
       uint32_t d = hpos[p];
@@ -518,8 +577,7 @@ __global__ void k_alloc_begin(Ctrl *ctrl, Geo geo, unsigned long long arena_cap)
 }
 
 __device__ __forceinline__ int acq_cid(const PoolCols &pool, const Ctrl *ctrl, long long a) {
-  return a < ctrl->alloc_F ? pool.free_stack[ctrl->alloc_F - 1 - a]
-                           : (int)(ctrl->alloc_A + (a - ctrl->alloc_F));
+  return a < ctrl->alloc_F ? pool.free_stack[ctrl->alloc_F - 1 - a] : (int)(ctrl->alloc_A + (a - ctrl->alloc_F));
 }
 
 // Per touched node: link the new run after the old tail (Octree.append_chunk,
@@ -553,8 +611,8 @@ __global__ void k_alloc_nodes(NodeCols nd, PoolCols pool, Geo geo, const int32_t
   }
 }
 
-// Per acquisition: payload offset for fresh chunks, in-run links, owner and
-// final occupancy, write-list slot.
+// Per acquisition: payload offset for fresh chunks, in-run links, owner,
+// position and final occupancy, write-list slot.
 __global__ void k_alloc_chunks(NodeCols nd, PoolCols pool, Geo geo, const int32_t *__restrict__ seg_node,
                                const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
                                const U64x2 *__restrict__ plan_ex, int32_t *__restrict__ wl, const Ctrl *ctrl) {
@@ -562,7 +620,7 @@ __global__ void k_alloc_chunks(NodeCols nd, PoolCols pool, Geo geo, const int32_
   const long long M = (long long)ctrl->acq_tot.a;
   const long long K = (long long)ctrl->n_keys;
   for (long long a = gtid(); a < M; a += gstride()) {
-    // segment d: last d with plan_ex[d].a <= a (and need > 0)
+    // segment d: last d with plan_ex[d].a <= a
     long long lo = 0, hi = K - 1;
     while (lo < hi) {
       long long mid = (lo + hi + 1) >> 1;
@@ -582,6 +640,7 @@ __global__ void k_alloc_chunks(NodeCols nd, PoolCols pool, Geo geo, const int32_
     pool.next[cid] = (t + 1 < need) ? acq_cid(pool, ctrl, a + 1) : LOD_NO_CHUNK;
     pool.owner[cid] = n;
     const long long ci = ceil_div(cnt, geo.C) + t;
+    pool.cidx[cid] = (int)ci;
     const long long rem = cnt + len - ci * geo.C;
     pool.occupied[cid] = (int)(rem < geo.C ? rem : geo.C);
     const long long partial = (long long)plan[d].b - need;
@@ -598,8 +657,7 @@ __global__ void k_store(NodeCols nd, PoolCols pool, Geo geo, uint8_t *__restrict
                         const uint32_t *__restrict__ hpos, const long long *__restrict__ seg_start,
                         const U64x2 *__restrict__ plan, const U64x2 *__restrict__ plan_ex,
                         const int32_t *__restrict__ wl, long long n_items, long long n_all, PointSrc src,
-                        const uint32_t *__restrict__ bcell, const uint32_t *__restrict__ brgba,
-                        const Ctrl *ctrl) {
+                        const uint32_t *__restrict__ bcell, const uint32_t *__restrict__ brgba, const Ctrl *ctrl) {
   if (ctrl->error) return;
   for (long long p = gtid(); p < n_items; p += gstride()) {
     const uint32_t key = skeys[p];
@@ -625,8 +683,7 @@ __global__ void k_store(NodeCols nd, PoolCols pool, Geo geo, uint8_t *__restrict
       const double x = nd.bmin[3 * n] + ((double)cx + 0.5) * step;
       const double y = nd.bmin[3 * n + 1] + ((double)cy + 0.5) * step;
       const double z = nd.bmin[3 * n + 2] + ((double)cz + 0.5) * step;
-      rec = make_float4(__double2float_rn(x), __double2float_rn(y), __double2float_rn(z),
-                        __uint_as_float(brgba[b]));
+      rec = make_float4(__double2float_rn(x), __double2float_rn(y), __double2float_rn(z), __uint_as_float(brgba[b]));
     }
     float4 *dst = reinterpret_cast<float4 *>(arena + pool.payload_off[cid]) + off;
     *dst = rec;
@@ -634,8 +691,8 @@ __global__ void k_store(NodeCols nd, PoolCols pool, Geo geo, uint8_t *__restrict
 }
 
 // clear_marks (_kernels.py:280-287) + count advance: pending drains into count.
-__global__ void k_epilogue(NodeCols nd, const int32_t *__restrict__ seg_node,
-                           const long long *__restrict__ seg_start, const Ctrl *ctrl) {
+__global__ void k_epilogue(NodeCols nd, const int32_t *__restrict__ seg_node, const long long *__restrict__ seg_start,
+                           const Ctrl *ctrl) {
   if (ctrl->error) return;
   const long long K = (long long)ctrl->n_keys;
   for (long long d = gtid(); d < K; d += gstride()) {
@@ -646,21 +703,12 @@ __global__ void k_epilogue(NodeCols nd, const int32_t *__restrict__ seg_node,
   }
 }
 
-__global__ void k_hash_clear(Hash h, const Ctrl *ctrl) {
-  unsigned long long nu = ctrl->n_used;
-  if (nu > h.used_cap) nu = h.used_cap;
-  for (long long u = gtid(); u < (long long)nu; u += gstride()) {
-    unsigned long long s = h.used[u];
-    h.keys[s] = kEmptyKey;
-    h.vals[s] = 0xFFFFFFFFu;
-  }
-}
-
 // Safety net after a fatal error: pending/final of every node back to zero.
-__global__ void k_clear_marks_all(NodeCols nd, long long n) {
+__global__ void k_clear_marks_all(NodeCols nd, int32_t *srank, long long n) {
   for (long long i = gtid(); i < n; i += gstride()) {
     nd.pending[i] = 0;
     nd.final_[i] = 0;
+    srank[i] = -1;
   }
 }
 

@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -21,6 +23,16 @@ using namespace lod;
 
 namespace {
 
+// LOD_DEBUG=1: log buffer growth and slow cycles to stderr
+inline bool lod_debug() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("LOD_DEBUG");
+    v = (e && *e && *e != '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 template <typename T>
 struct DBuf {
   T *p = nullptr;
@@ -29,15 +41,17 @@ struct DBuf {
   int ensure(long long n, cudaStream_t st, long long keep = 0) {
     if (n <= cap) return 0;
     long long nc = std::max<long long>(n, std::max<long long>(2 * cap, 1024));
+    if (lod_debug())
+      fprintf(stderr, "[lod] grow buffer %lld -> %lld elems (%.1f MB)\n", cap, nc, nc * sizeof(T) / 1e6);
     T *q = nullptr;
-    if (cudaMalloc(&q, (size_t)nc * sizeof(T)) != cudaSuccess) {
+    // stream-ordered: growth never synchronizes the device
+    if (cudaMallocAsync(&q, (size_t)nc * sizeof(T), st) != cudaSuccess) {
       cudaGetLastError();
       return LOD_E_NOMEM;
     }
     if (p) {
       if (keep > 0) cudaMemcpyAsync(q, p, (size_t)std::min(keep, cap) * sizeof(T), cudaMemcpyDeviceToDevice, st);
-      cudaStreamSynchronize(st);
-      cudaFree(p);
+      cudaFreeAsync(p, st);
     }
     p = q;
     cap = nc;
@@ -147,9 +161,12 @@ struct LodTree {
   DBuf<long long> scnt, schk, spill_off, chunk_off;
   DBuf<float4> spill;
   // sampling scratch
-  DBuf<unsigned long long> hkeys, hused, wins;
-  DBuf<uint32_t> hvals, wcount, wbase;
+  DBuf<int32_t> srank;  // split rank per node (-1 when not splitting)
+  DBuf<HSlot> hslots, hslots2;  // claim table (`hcap` slots in use) + growth spare
+  DBuf<unsigned long long> hused, wins, wmask;
+  DBuf<uint32_t> wcount, wbase;
   unsigned long long hcap = 0;
+  long long prev_used = 0;  // claims of the previous cycle (sizes the table)
   DBuf<int32_t> bnode;
   DBuf<uint32_t> bcell, brgba;
   // sort / alloc scratch
@@ -167,7 +184,7 @@ struct LodTree {
   DBuf<int32_t> vislist;
   DBuf<unsigned long long> fb;
   DBuf<unsigned long long> counter;
-  cudaEvent_t ev[12] = {};
+  cudaEvent_t ev[14] = {};  // 12, 13: per-iteration k_count brackets
   // host copies of counters (authoritative after every call)
   long long num_nodes = 1;
   long long d2h_bytes = 0;  // control-block readbacks since the last reset
@@ -202,13 +219,12 @@ static int sync_ctrl(LodTree *t) {
 template <typename T>
 static int grow_col(T *&ptr, long long old_cap, long long new_cap, long long keep, cudaStream_t st) {
   T *q = nullptr;
-  if (cudaMalloc(&q, (size_t)new_cap * sizeof(T)) != cudaSuccess) {
+  if (cudaMallocAsync(&q, (size_t)new_cap * sizeof(T), st) != cudaSuccess) {
     cudaGetLastError();
     return LOD_E_NOMEM;
   }
   if (ptr && keep > 0) CK(cudaMemcpyAsync(q, ptr, (size_t)keep * sizeof(T), cudaMemcpyDeviceToDevice, st));
-  CK(cudaStreamSynchronize(st));
-  if (ptr) cudaFree(ptr);
+  if (ptr) CK(cudaFreeAsync(ptr, st));
   ptr = q;
   (void)old_cap;
   return LOD_OK;
@@ -219,6 +235,7 @@ static int ensure_nodes(LodTree *t, long long want, long long live) {
   if (want <= t->ncap) return LOD_OK;
   long long nc = std::max<long long>(t->ncap, 1024);
   while (nc < want) nc *= 2;
+  if (lod_debug()) fprintf(stderr, "[lod] grow node table %lld -> %lld\n", t->ncap, nc);
   cudaStream_t st = t->st;
   RK(grow_col(t->nd.parent, t->ncap, nc, live, st));
   RK(grow_col(t->nd.octant, t->ncap, nc, live, st));
@@ -246,6 +263,9 @@ static int ensure_nodes(LodTree *t, long long want, long long live) {
   RK(t->schk.ensure(nc, st));
   RK(t->spill_off.ensure(nc, st, t->spill_off.cap));
   RK(t->chunk_off.ensure(nc, st, t->chunk_off.cap));
+  long long olds = t->srank.cap;
+  RK(t->srank.ensure(nc, st, olds));
+  if (t->srank.cap > olds) CK(cudaMemsetAsync(t->srank.p + olds, 0xFF, (size_t)(t->srank.cap - olds) * 4, st));
   long long oldv = t->visflag.cap;
   RK(t->visflag.ensure(nc, st, oldv));
   if (t->visflag.cap > oldv) CK(cudaMemsetAsync(t->visflag.p + oldv, 0, (size_t)(t->visflag.cap - oldv) * 4, st));
@@ -258,11 +278,13 @@ static int ensure_chunks(LodTree *t, long long want, long long live) {
   if (want <= t->ccap) return LOD_OK;
   long long nc = std::max<long long>(t->ccap, 1024);
   while (nc < want) nc *= 2;
+  if (lod_debug()) fprintf(stderr, "[lod] grow chunk table %lld -> %lld\n", t->ccap, nc);
   cudaStream_t st = t->st;
   RK(grow_col(t->pool.next, t->ccap, nc, live, st));
   RK(grow_col(t->pool.payload_off, t->ccap, nc, live, st));
   RK(grow_col(t->pool.occupied, t->ccap, nc, live, st));
   RK(grow_col(t->pool.owner, t->ccap, nc, live, st));
+  RK(grow_col(t->pool.cidx, t->ccap, nc, live, st));
   RK(grow_col(t->pool.free_stack, t->ccap, nc, live, st));
   t->ccap = nc;
   return LOD_OK;
@@ -282,10 +304,10 @@ static void fill_stats(LodTree *t, LodBatchStats *s) {
 // After a fatal error: drop per-cycle marks and the claim table so the
 // structure stays walkable (the reference leaves partial state, errors.py:1-5).
 static int abort_cycle(LodTree *t, int code) {
-  k_clear_marks_all<<<grid_for(t->num_nodes), 256, 0, t->st>>>(t->nd, t->num_nodes); ++lod::g_launches;
-  if (t->hkeys.p) {
-    cudaMemsetAsync(t->hkeys.p, 0xFF, (size_t)t->hcap * 8, t->st);
-    cudaMemsetAsync(t->hvals.p, 0xFF, (size_t)t->hcap * 4, t->st);
+  k_clear_marks_all<<<grid_for(t->num_nodes), 256, 0, t->st>>>(t->nd, t->srank.p, t->num_nodes); ++lod::g_launches;
+  if (t->hslots.p) {
+    cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), t->st);
+    if (t->wmask.p) cudaMemsetAsync(t->wmask.p, 0, (size_t)t->wmask.cap * 8, t->st);
   }
   long long words = (t->ncap + 31) / 32 + 1;
   cudaMemsetAsync(t->bitmap.p, 0, (size_t)words * 4, t->st);
@@ -338,6 +360,14 @@ int lod_tree_create(const LodParams *params, LodTree **out) {
   t->dev = p.device;
   cudaSetDevice(t->dev);
   CK(cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking));
+  {
+    // keep freed scratch cached in the stream-ordered pool (growth without syncs)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, t->dev) == cudaSuccess) {
+      unsigned long long thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   for (auto &e : t->ev) CK(cudaEventCreate(&e));
   Geo &g = t->geo;
   for (int k = 0; k < 3; ++k) g.bmin0[k] = p.bmin[k];
@@ -381,13 +411,14 @@ int lod_tree_destroy(LodTree *t) {
   f(t->nd.parent); f(t->nd.octant); f(t->nd.level); f(t->nd.children); f(t->nd.inner);
   f(t->nd.final_); f(t->nd.count); f(t->nd.pending); f(t->nd.chunk_head); f(t->nd.chunk_tail);
   f(t->nd.chunk_count); f(t->nd.grid_off); f(t->nd.bmin);
-  f(t->pool.next); f(t->pool.payload_off); f(t->pool.occupied); f(t->pool.owner); f(t->pool.free_stack);
+  f(t->pool.next); f(t->pool.payload_off); f(t->pool.occupied); f(t->pool.owner); f(t->pool.cidx);
+  f(t->pool.free_stack);
   f(t->d_ctrl);
   if (t->h_ctrl) cudaFreeHost(t->h_ctrl);
   t->touched.release(); t->split_list.release(); t->node_b.release(); t->node_all.release();
   t->bitmap.release(); t->word_prefix.release(); t->scnt.release(); t->schk.release();
-  t->spill_off.release(); t->chunk_off.release(); t->spill.release(); t->hkeys.release();
-  t->hused.release(); t->wins.release(); t->hvals.release(); t->wcount.release(); t->wbase.release();
+  t->spill_off.release(); t->chunk_off.release(); t->spill.release(); t->hslots.release(); t->hslots2.release();
+  t->hused.release(); t->wins.release(); t->wmask.release(); t->srank.release(); t->wcount.release(); t->wbase.release();
   t->bnode.release(); t->bcell.release(); t->brgba.release(); t->keys.release(); t->keys_b.release();
   t->vals_a.release(); t->vals_b.release(); t->hist.release(); t->flags.release(); t->hpos.release();
   t->scan_u32.release(); t->seg_node.release(); t->wl.release(); t->seg_start.release();
@@ -441,10 +472,9 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   const long long launches0 = lod::g_launches;
   t->d2h_bytes = 0;
   S.h2d_bytes = (flags & LOD_FLAG_DEVICE_INPUT) ? 0 : 16 * n;
-  int evi = 0;
+  float count_ms = 0.f;
   auto mark = [&](int phase) {
     if (prof) cudaEventRecord(t->ev[1 + phase], st);
-    (void)evi;
   };
   CK(cudaEventRecord(t->ev[0], st));
   // ---- inputs
@@ -460,22 +490,47 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   }
   CK(cudaEventRecord(t->ev[11], st));  // inputs resident
   k_cycle_begin<<<1, 1, 0, st>>>(t->d_ctrl); ++lod::g_launches;
-  // ---- expansion (update.py:273-296)
+  // ---- expansion (update.py:273-296) with the voxel claims folded in
   RK(t->node_b.ensure(n, st));
   PointSrc src{nullptr, 0, bx, bc, n};
   int32_t *node_of = t->node_b.p;
   long long n_all = n, n_s = 0;
   int first = 1, iters = 0;
   long long splits_cycle = 0;
+  // claim table: sized from the batch and the previous cycle's claims, grown
+  // (rehashed) between iterations when the next pass could overfill it; a
+  // table that still fills up falls back to a separate claim pass
+  {
+    const long long want = std::max<long long>(3 * (t->prev_used + n) / 2, 1 << 20);
+    const unsigned long long H = next_pow2((unsigned long long)want);
+    if ((long long)H > t->hslots.cap) {
+      RK(t->hslots.ensure((long long)H, st));
+      CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
+    }
+    t->hcap = H;
+    RK(t->hused.ensure((long long)H, st));
+  }
+  Hash hs{t->hslots.p, t->hcap - 1, t->hused.p, t->hcap};
+  uint32_t *grid32 = reinterpret_cast<uint32_t *>(t->arena);
   for (;;) {
     ++iters;
-    if (!first) k_reset_touched<<<1, 1, 0, st>>>(t->d_ctrl); ++lod::g_launches;
-    k_count<<<grid_for(n_all), 256, 0, st>>>(t->nd, t->geo, src, node_of, n_all, first, t->touched.p,
+    if (!first) {
+      k_reset_touched<<<1, 1, 0, st>>>(t->d_ctrl);
+      ++lod::g_launches;
+    }
+    if (prof) cudaEventRecord(t->ev[12], st);
+    k_count<<<grid_for(n_all), 256, 0, st>>>(t->nd, t->geo, src, node_of, n_all, first, grid32, hs, t->touched.p,
                                             t->d_ctrl); ++lod::g_launches;
+    if (prof) cudaEventRecord(t->ev[13], st);
     k_decide<<<1, kDecideBlock, 0, st>>>(t->nd, t->geo, t->touched.p, t->bitmap.p, t->word_prefix.p,
-                                         t->split_list.p, t->scnt.p, t->schk.p, t->spill_off.p,
+                                         t->split_list.p, t->srank.p, t->scnt.p, t->schk.p, t->spill_off.p,
                                          t->chunk_off.p, t->d_ctrl, spill_cap, t->arena_cap); ++lod::g_launches;
     RK(sync_ctrl(t));
+    if (prof) {
+      float x = 0.f;
+      cudaEventElapsedTime(&x, t->ev[12], t->ev[13]);
+      count_ms += x;
+    }
     const Ctrl &h = *t->h_ctrl;
     if (h.error) return abort_cycle(t, h.error);
     const long long ns = h.n_splits;
@@ -487,10 +542,12 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       if (!first) return abort_cycle(t, LOD_E_ARG);  // only iteration 1 can spill (update.py:9-11)
       RK(t->spill.ensure(h.spill_total, st));
       RK(t->node_all.ensure(h.spill_total + n, st));
+      k_exec_chunks<<<grid_for(h.allocated_total * 32), 256, 0, st>>>(
+          t->pool, t->geo, t->arena, h.allocated_total, t->srank.p, t->spill_off.p, t->chunk_off.p, t->spill.p,
+          t->node_all.p, t->d_ctrl); ++lod::g_launches;
     }
-    k_execute<<<(unsigned)ns, kExecBlock, 0, st>>>(t->nd, t->pool, t->geo, t->arena, t->split_list.p,
-                                                 t->spill_off.p, t->chunk_off.p, t->spill.p,
-                                                 t->node_all.p, t->d_ctrl); ++lod::g_launches;
+    k_exec_nodes<<<grid_for(8 * ns), 256, 0, st>>>(t->nd, t->geo, t->split_list.p, t->srank.p, ns,
+                                                   t->d_ctrl); ++lod::g_launches;
     t->num_nodes = h.num_nodes;
     if (first) {
       n_s = h.spill_total;
@@ -503,50 +560,72 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       n_all = n_s + n;
       first = 0;
     }
-  }
-  mark(0);
-  const Ctrl h1 = *t->h_ctrl;
-  t->num_nodes = h1.num_nodes;
-  const long long num_nodes = h1.num_nodes;
-  // ---- sampling (update.py:298-315)
-  const int D = (int)std::max<long long>(h1.max_level, 1);
-  const long long bound = n_all * D;
-  const long long claim_cap = std::min<long long>(bound, backlog_cap + 1);
-  {
-    unsigned long long H = next_pow2((unsigned long long)std::max<long long>(2 * claim_cap, 1024));
-    if (H > t->hcap) {
-      t->hkeys.release();
-      t->hvals.release();
-      RK(t->hkeys.ensure((long long)H, st));
-      RK(t->hvals.ensure((long long)H, st));
-      CK(cudaMemsetAsync(t->hkeys.p, 0xFF, (size_t)H * 8, st));
-      CK(cudaMemsetAsync(t->hvals.p, 0xFF, (size_t)H * 4, st));
+    // the next pass claims at most one cell per re-descending point
+    if ((long long)h.n_used + n_all > (long long)(3 * t->hcap / 4)) {
+      const unsigned long long H = next_pow2((unsigned long long)(2 * ((long long)h.n_used + n_all)));
+      if (lod_debug()) fprintf(stderr, "[lod] claim table grow %llu -> %llu (rehash %llu)\n", t->hcap, H, h.n_used);
+      RK(t->hslots2.ensure((long long)H, st));
+      CK(cudaMemsetAsync(t->hslots2.p, 0xFF, (size_t)t->hslots2.cap * sizeof(HSlot), st));
+      RK(t->hused.ensure((long long)H, st, (long long)h.n_used));
+      Hash nh{t->hslots2.p, H - 1, t->hused.p, H};
+      k_rehash<<<grid_for(std::max<long long>((long long)h.n_used, 1)), 256, 0, st>>>(t->hslots.p, nh, t->d_ctrl);
+      ++lod::g_launches;
+      // the old table goes back to empty for later cycles
+      CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
+      std::swap(t->hslots, t->hslots2);
       t->hcap = H;
+      hs = nh;
     }
   }
-  RK(t->hused.ensure(claim_cap + 1, st));
+  mark(0);
+  Ctrl h1 = *t->h_ctrl;
+  t->num_nodes = h1.num_nodes;
+  const long long num_nodes = h1.num_nodes;
+  // ---- resolve the claims (update.py:298-315)
+  const int D = (int)std::max<long long>(h1.max_level, 1);
   RK(t->wcount.ensure(n_all, st));
   RK(t->wbase.ensure(n_all, st));
-  RK(t->wins.ensure(bound, st));
+  RK(t->wins.ensure(n_all * D, st));
+  {
+    long long oldm = t->wmask.cap;
+    RK(t->wmask.ensure(n_all, st, oldm));
+    if (t->wmask.cap > oldm) CK(cudaMemsetAsync(t->wmask.p + oldm, 0, (size_t)(t->wmask.cap - oldm) * 8, st));
+  }
   RK(t->scan_u32.ensure(scan_scratch_elems(std::max<long long>(n_all, 1)), st));
-  Hash hs{t->hkeys.p, t->hvals.p, t->hcap - 1, t->hused.p, (unsigned long long)claim_cap + 1};
-  // a cheap upper bound for what follows: arena as 32-bit words for grids
-  uint32_t *grid32 = reinterpret_cast<uint32_t *>(t->arena);
-  k_claim<<<grid_for(n_all), 256, 0, st>>>(t->nd, t->geo, src, grid32, n_all, hs, t->d_ctrl); ++lod::g_launches;
-  k_win<<<grid_for(n_all), 256, 0, st>>>(t->nd, t->geo, src, grid32, n_all, hs, t->wcount.p, t->wins.p, D); ++lod::g_launches;
+  if (h1.hash_overflow) {
+    if (lod_debug()) fprintf(stderr, "[lod] claim table overflow (H=%llu, used>=%llu): fallback pass\n", t->hcap, h1.n_used);
+    // fallback: clean table sized by the reference's backlog bound, full claim pass
+    const long long bound = std::min<long long>(n_all * D, backlog_cap + 1);
+    const unsigned long long H = next_pow2((unsigned long long)std::max<long long>(2 * bound, 1 << 20));
+    if ((long long)H > t->hslots.cap) RK(t->hslots.ensure((long long)H, st));
+    CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
+    t->hcap = H;
+    RK(t->hused.ensure(bound + 1, st));
+    hs = Hash{t->hslots.p, t->hcap - 1, t->hused.p, (unsigned long long)bound + 1};
+    CK(cudaMemsetAsync(&t->d_ctrl->n_used, 0, 8, st));
+    CK(cudaMemsetAsync(&t->d_ctrl->hash_overflow, 0, 4, st));
+    k_claim<<<grid_for(n_all), 256, 0, st>>>(t->nd, t->geo, src, grid32, n_all, hs, t->d_ctrl); ++lod::g_launches;
+    RK(sync_ctrl(t));
+    h1 = *t->h_ctrl;
+  }
+  if ((long long)h1.n_used > backlog_cap) return abort_cycle(t, LOD_E_BACKLOG_OVERFLOW);  // update.py:311-312
+  if (h1.hash_overflow) return abort_cycle(t, LOD_E_NOMEM);
+  const long long n_v = (long long)h1.n_used;
+  t->prev_used = n_v;
+  if (n_v > 0) {
+    k_resolve<<<grid_for(n_v), 256, 0, st>>>(t->nd, hs, grid32, n_s, D, t->wins.p, t->wmask.p, t->d_ctrl);
+    ++lod::g_launches;
+  }
   mark(1);
-  exclusive_scan<uint32_t>(t->wcount.p, t->wbase.p, n_all, &t->d_ctrl->n_v, t->scan_u32.p, st);
-  RK(sync_ctrl(t));
-  const Ctrl h2 = *t->h_ctrl;
-  if (h2.hash_overflow || (long long)h2.n_used > backlog_cap || (long long)h2.n_v > backlog_cap)
-    return abort_cycle(t, LOD_E_BACKLOG_OVERFLOW);  // update.py:311-312
-  const long long n_v = h2.n_v;
   RK(t->bnode.ensure(std::max<long long>(n_v, 1), st));
   RK(t->bcell.ensure(std::max<long long>(n_v, 1), st));
   RK(t->brgba.ensure(std::max<long long>(n_v, 1), st));
-  if (n_v > 0)
-    k_emit<<<grid_for(n_all), 256, 0, st>>>(n_all, t->wcount.p, t->wbase.p, t->wins.p, D, src, t->bnode.p,
+  if (n_v > 0) {
+    k_wcount<<<grid_for(n_all), 256, 0, st>>>(t->wmask.p, n_all, t->wcount.p); ++lod::g_launches;
+    exclusive_scan<uint32_t>(t->wcount.p, t->wbase.p, n_all, &t->d_ctrl->n_v, t->scan_u32.p, st);
+    k_emit<<<grid_for(n_all), 256, 0, st>>>(n_all, t->wmask.p, t->wbase.p, t->wins.p, D, src, t->bnode.p,
                                            t->bcell.p, t->brgba.p); ++lod::g_launches;
+  }
   mark(2);
   // ---- sort: every new sample by node id, stable (slot order)
   const long long n_items = n_all + n_v;
@@ -577,7 +656,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   RK(t->scan_u64x2.ensure(scan_scratch_elems(Kb), st));
   const long long acq_bound = n_items / C + Kb + 1;
   RK(t->wl.ensure(acq_bound + Kb + 1, st));
-  RK(ensure_chunks(t, h2.allocated_total + acq_bound + 1, h2.allocated_total));
+  RK(ensure_chunks(t, h1.allocated_total + acq_bound + 1, h1.allocated_total));
   k_seg_flags<<<grid_for(n_items), 256, 0, st>>>(skeys, n_items, t->flags.p); ++lod::g_launches;
   exclusive_scan<uint32_t>(t->flags.p, t->hpos.p, n_items, &t->d_ctrl->n_keys, t->scan_u32.p, st);
   k_seg_list<<<grid_for(n_items), 256, 0, st>>>(skeys, n_items, t->hpos.p, t->seg_node.p, t->seg_start.p,
@@ -598,7 +677,6 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   mark(5);
   // ---- cleanup (update.py:375-380)
   k_epilogue<<<grid_for(Kb), 256, 0, st>>>(t->nd, t->seg_node.p, t->seg_start.p, t->d_ctrl); ++lod::g_launches;
-  k_hash_clear<<<grid_for(std::max<long long>(n_v, 1)), 256, 0, st>>>(hs, t->d_ctrl); ++lod::g_launches;
   mark(6);
   CK(cudaEventRecord(t->ev[10], st));
   RK(sync_ctrl(t));
@@ -614,17 +692,25 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   float ms = 0.f;
   cudaEventElapsedTime(&ms, t->ev[11], t->ev[10]);
   S.device_ms = ms;
+  if (lod_debug())
+    fprintf(stderr, "[lod] batch n=%lld n_s=%lld n_v=%lld iters=%d splits=%lld nodes=%lld %.3f ms\n", (long long)n,
+            n_s, n_v, iters, splits_cycle, (long long)S.num_nodes, ms);
   if (prof) {
+    // phases: count, split, resolve, backlog, sort, alloc, store, epilogue, h2d, total
     float h2d = 0.f;
     cudaEventElapsedTime(&h2d, t->ev[0], t->ev[11]);
-    S.phase_ms[7] = h2d;
     cudaEvent_t prev = t->ev[11];
+    float seg[7];
     for (int k = 0; k < 7; ++k) {
-      float x = 0.f;
-      cudaEventElapsedTime(&x, prev, t->ev[1 + k]);
-      S.phase_ms[k] = x;
+      seg[k] = 0.f;
+      cudaEventElapsedTime(&seg[k], prev, t->ev[1 + k]);
       prev = t->ev[1 + k];
     }
+    S.phase_ms[0] = count_ms;
+    S.phase_ms[1] = seg[0] - count_ms;
+    for (int k = 1; k < 7; ++k) S.phase_ms[1 + k] = seg[k];
+    S.phase_ms[8] = h2d;
+    S.phase_ms[9] = ms;
   }
   return LOD_OK;
 }

@@ -73,6 +73,9 @@ struct NodeCols {
   int32_t *chunk_count;
   long long *grid_off;
   double *bmin;  // [ncap * 3]
+  // device-only descent record: {first child id (children are 8 consecutive
+  // ids) or -1 for a leaf, grid offset / 64}; 8 bytes per node, L1-resident
+  int2 *desc;
 };
 
 struct PoolCols {
@@ -88,6 +91,8 @@ struct Geo {
   double bmin0[3];
   double size0;
   double size_by_level[64];  // size * 0.5 ** k (octree.py:167); levels <= 62
+  double inv_by_level[64];   // 1 / size_by_level[k], exact when pow2
+  int pow2;                  // root size is a power of two: x / s == x * (1/s) exactly
   int g;                     // grid_res
   long long grid_bytes;
   long long T;               // leaf_threshold
@@ -139,21 +144,41 @@ __device__ __forceinline__ int octant_step(double x, double y, double z, double 
   return o;
 }
 
-// Occupancy cell (_kernels.py:107-122): floor(g * (x - bx) / s), clamped.
-__device__ __forceinline__ long long cell_axis(double gd, double x, double bx, double s, int g) {
-  long long c = f2i64(floor(gd * (x - bx) / s));
-  if (c < 0) c = 0;
-  else if (c > g - 1) c = g - 1;
-  return c;
+// Same step also tracking 1/s (exact doubling; only meaningful when pow2).
+__device__ __forceinline__ int octant_step(double x, double y, double z, double &bx, double &by, double &bz,
+                                           double &s, double &inv_s) {
+  inv_s = inv_s * 2.0;
+  return octant_step(x, y, z, bx, by, bz, s);
 }
 
+// Clamp of np.int64(np.floor(v)) to [0, g-1] (_kernels.py:107-121) with the
+// x86 conversion semantics: NaN and |v| >= 2^63 become INT64_MIN, i.e. cell 0.
+__device__ __forceinline__ int clamp_cell(double v, int g) {
+  const double f = floor(v);
+  if (!(f < 9223372036854775808.0)) return 0;  // NaN, +inf, >= 2^63 -> INT64_MIN -> 0
+  if (f < 0.0) return 0;
+  if (f > (double)(g - 1)) return g - 1;
+  return (int)f;
+}
+
+// Occupancy cell (_kernels.py:107-122): floor(g * (x - bx) / s) per axis,
+// clamped, cx + g*cy + g*g*cz.  `inv_s` = 1/s is used only when the root size
+// is a power of two: then s = 2^-k exactly and (g*(x-bx)) / s == (g*(x-bx)) * 2^k
+// bit for bit, saving three IEEE divisions per probe.
 __device__ __forceinline__ long long cell_of(const Geo &geo, double x, double y, double z,
-                                             double bx, double by, double bz, double s) {
+                                             double bx, double by, double bz, double s, double inv_s) {
   const double gd = (double)geo.g;
-  long long cx = cell_axis(gd, x, bx, s, geo.g);
-  long long cy = cell_axis(gd, y, by, s, geo.g);
-  long long cz = cell_axis(gd, z, bz, s, geo.g);
-  return cx + (long long)geo.g * cy + (long long)geo.g * geo.g * cz;
+  int cx, cy, cz;
+  if (geo.pow2) {
+    cx = clamp_cell(gd * (x - bx) * inv_s, geo.g);
+    cy = clamp_cell(gd * (y - by) * inv_s, geo.g);
+    cz = clamp_cell(gd * (z - bz) * inv_s, geo.g);
+  } else {
+    cx = clamp_cell(gd * (x - bx) / s, geo.g);
+    cy = clamp_cell(gd * (y - by) / s, geo.g);
+    cz = clamp_cell(gd * (z - bz) / s, geo.g);
+  }
+  return (long long)cx + (long long)geo.g * cy + (long long)geo.g * geo.g * cz;
 }
 
 }  // namespace lod

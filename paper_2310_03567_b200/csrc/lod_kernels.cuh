@@ -53,6 +53,7 @@ struct Ctrl {
   // allocation plan
   unsigned int n_keys;        // touched nodes this cycle (segments)
   unsigned int pad1;
+  U64x2 seg_tot;              // (touched nodes, items)
   U64x2 acq_tot;              // (sum need, sum write-list entries)
   long long alloc_F;          // free stack size before allocation
   long long alloc_A;          // allocated_total before allocation
@@ -83,13 +84,15 @@ struct Hash {
   unsigned long long limit;  // capacity of `used` (= table capacity)
 };
 
-// New keys are appended to the cycle's used-slot list through a per-block
-// shared-memory stage, so a pass issues one global atomic per block instead
-// of one per new voxel (a single hot counter otherwise serializes in L2).
-constexpr int kStage = 2048;
+// New keys are appended to the cycle's used-slot list through a per-warp
+// shared-memory stage, so a pass issues one global atomic per warp instead of
+// one per new voxel (a single hot counter otherwise serializes in L2), and
+// no block-wide barrier is needed to flush it.
+constexpr int kStage = 128;  // slots per warp
+constexpr int kStageWarps = 8;
 struct UsedStage {
-  unsigned long long slot[kStage];
-  unsigned int n;
+  unsigned long long slot[kStageWarps][kStage];
+  unsigned int n[kStageWarps];
 };
 
 __device__ __forceinline__ unsigned long long hmix(unsigned long long k) {
@@ -105,10 +108,16 @@ __device__ __forceinline__ unsigned long long claim_key(int nid, long long cell)
   return ((unsigned long long)(uint32_t)nid << 32) | (unsigned long long)cell;
 }
 
+__device__ __forceinline__ void used_init(UsedStage &stg) {
+  if ((threadIdx.x & 31) == 0) stg.n[threadIdx.x >> 5] = 0;
+  __syncwarp();
+}
+
 __device__ __forceinline__ void used_append(const Hash &h, UsedStage &stg, unsigned long long slot, Ctrl *ctrl) {
-  const unsigned k = atomicAdd(&stg.n, 1u);
+  const int w = threadIdx.x >> 5;
+  const unsigned k = atomicAdd(&stg.n[w], 1u);
   if (k < (unsigned)kStage) {
-    stg.slot[k] = slot;
+    stg.slot[w][k] = slot;
   } else {  // stage full: direct append
     const unsigned long long u = atomicAdd(&ctrl->n_used, 1ull);
     if (u < h.limit) h.used[u] = slot;
@@ -116,37 +125,66 @@ __device__ __forceinline__ void used_append(const Hash &h, UsedStage &stg, unsig
   }
 }
 
-// Block epilogue of a claiming pass: flush the staged used slots.
+// Warp epilogue of a claiming pass (all lanes): flush the warp's staged slots.
 __device__ __forceinline__ void used_flush(const Hash &h, UsedStage &stg, Ctrl *ctrl) {
-  __shared__ unsigned long long s_base;
-  __syncthreads();
-  const unsigned n = min(stg.n, (unsigned)kStage);
-  if (threadIdx.x == 0) s_base = n ? atomicAdd(&ctrl->n_used, (unsigned long long)n) : 0ull;
-  __syncthreads();
-  for (unsigned i = threadIdx.x; i < n; i += blockDim.x) {
-    const unsigned long long u = s_base + i;
-    if (u < h.limit) h.used[u] = stg.slot[i];
+  __syncwarp();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned n = min(stg.n[w], (unsigned)kStage);
+  unsigned long long base = 0;
+  if (lane == 0 && n) base = atomicAdd(&ctrl->n_used, (unsigned long long)n);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (unsigned i = lane; i < n; i += 32) {
+    const unsigned long long u = base + i;
+    if (u < h.limit) h.used[u] = stg.slot[w][i];
     else ctrl->hash_overflow = 1;
   }
 }
 
+// 16-byte compare-and-swap of a whole slot (ATOMG.CAS.128): a new key is
+// installed together with its first claimant's index in one atomic.
+__device__ __forceinline__ ulonglong2 cas_slot(HSlot *sl, ulonglong2 cmp, ulonglong2 val) {
+  ulonglong2 old;
+  asm volatile(
+      "{\n\t.reg .b128 d, b, c;\n\t"
+      "mov.b128 b, {%2, %3};\n\t"
+      "mov.b128 c, {%4, %5};\n\t"
+      "atom.global.cas.b128 d, [%6], b, c;\n\t"
+      "mov.b128 {%0, %1}, d;\n\t}"
+      : "=l"(old.x), "=l"(old.y)
+      : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(sl)
+      : "memory");
+  return old;
+}
+
+constexpr unsigned long long kEmptyHi = 0xFFFFFFFFFFFFFFFFULL;  // val = pad = 0xFFFFFFFF
+
+// Min-combine `v` into the claim of `key`.  Lower indices run earlier, so a
+// claimant usually finds a smaller index already there and issues no atomic.
 __device__ __forceinline__ void hash_claim(const Hash &h, UsedStage &stg, unsigned long long key, uint32_t v,
                                            Ctrl *ctrl) {
+#ifdef LOD_EXP_NOCLAIM  // timing experiment only: results are wrong
+  return;
+#endif
+#ifdef LOD_EXP_COUNT  // instrumentation experiment: claims and probes into Ctrl.alloc_F / alloc_A
+  atomicAdd((unsigned long long *)&ctrl->alloc_F, 1ull);
+#endif
   unsigned long long slot = hmix(key) & h.mask;
   for (unsigned long long probe = 0; probe <= h.mask; ++probe) {
+#ifdef LOD_EXP_COUNT
+    atomicAdd((unsigned long long *)&ctrl->alloc_A, 1ull);
+#endif
     HSlot *sl = h.slots + slot;
-    unsigned long long k = __ldcg(&sl->key);
-    if (k == key) {
-      atomicMin(&sl->val, v);
-      return;
-    }
-    if (k == kEmptyKey) {
-      unsigned long long prev = atomicCAS(&sl->key, kEmptyKey, key);
-      if (prev == kEmptyKey || prev == key) {
-        atomicMin(&sl->val, v);
-        if (prev == kEmptyKey) used_append(h, stg, slot, ctrl);
+    ulonglong2 cur = __ldcg(reinterpret_cast<const ulonglong2 *>(sl));
+    if (cur.x == kEmptyKey) {
+      cur = cas_slot(sl, make_ulonglong2(kEmptyKey, kEmptyHi), make_ulonglong2(key, (unsigned long long)v));
+      if (cur.x == kEmptyKey) {
+        used_append(h, stg, slot, ctrl);
         return;
       }
+    }
+    if (cur.x == key) {
+      if ((uint32_t)cur.y > v) atomicMin(&sl->val, v);
+      return;
     }
     slot = (slot + 1) & h.mask;
   }
@@ -158,8 +196,8 @@ __device__ __forceinline__ void hash_claim(const Hash &h, UsedStage &stg, unsign
 __device__ __forceinline__ void probe_cell(const NodeCols &nd, const Geo &geo, const uint32_t *grid32,
                                            const Hash &h, UsedStage &stg, Ctrl *ctrl, int nid, double x,
                                            double y, double z, double bx, double by, double bz, double s,
-                                           uint32_t v) {
-  const long long cell = cell_of(geo, x, y, z, bx, by, bz, s);
+                                           double inv_s, uint32_t v) {
+  const long long cell = cell_of(geo, x, y, z, bx, by, bz, s, inv_s);
   const uint32_t w = __ldg(grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5));
   if (!(w & (1u << (cell & 31)))) hash_claim(h, stg, claim_key(nid, cell), v, ctrl);
 }
@@ -171,8 +209,8 @@ __global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl
   for (long long u = gtid(); u < (long long)nu; u += gstride()) {
     const HSlot o = old_slots[h.used[u]];
     unsigned long long slot = hmix(o.key) & h.mask;
-    while (atomicCAS(&h.slots[slot].key, kEmptyKey, o.key) != kEmptyKey) slot = (slot + 1) & h.mask;
-    h.slots[slot].val = o.val;
+    const ulonglong2 empty = make_ulonglong2(kEmptyKey, kEmptyHi), nv = make_ulonglong2(o.key, o.val);
+    while (cas_slot(h.slots + slot, empty, nv).x != kEmptyKey) slot = (slot + 1) & h.mask;
     h.used[u] = slot;
   }
 }
@@ -186,27 +224,32 @@ __global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl
 // accumulated descent bounds byte for byte, _kernels.py:9-13).
 __global__ void __launch_bounds__(256, 6)
     k_count(NodeCols nd, Geo geo, PointSrc src, int32_t *__restrict__ node_of, long long n, int first,
-            const uint32_t *__restrict__ grid32, Hash h, int32_t *__restrict__ touched, Ctrl *ctrl) {
+            const uint32_t *__restrict__ grid32, Hash h, Ctrl *ctrl) {
   __shared__ UsedStage stg;
-  if (threadIdx.x == 0) stg.n = 0;
-  __syncthreads();
+  used_init(stg);
   for (long long j0 = (long long)blockIdx.x * blockDim.x; j0 < n; j0 += gstride()) {
     long long j = j0 + threadIdx.x;
     int leaf = -1;
     if (j < n) {
       int nid = first ? 0 : node_of[j];
-      if (nd.inner[nid]) {
+      int2 d = __ldg(nd.desc + nid);  // {first child | -1, grid offset / 64}
+      if (d.x >= 0) {
         float xf, yf, zf;
         src.xyz(j, xf, yf, zf);
         const double x = xf, y = yf, z = zf;
         double bx = nd.bmin[3 * nid], by = nd.bmin[3 * nid + 1], bz = nd.bmin[3 * nid + 2];
-        double s = geo.size_by_level[nd.level[nid]];
+        const int lvl0 = nd.level[nid];
+        double s = geo.size_by_level[lvl0], inv_s = geo.inv_by_level[lvl0];
         const uint32_t v = first ? ((uint32_t)j | kBatchTag) : (uint32_t)j;
+        // one dependent load per level, from the compact descent table
         do {
-          probe_cell(nd, geo, grid32, h, stg, ctrl, nid, x, y, z, bx, by, bz, s, v);
-          const int o = octant_step(x, y, z, bx, by, bz, s);
-          nid = nd.children[8 * nid + o];
-        } while (nd.inner[nid]);
+          const long long cell = cell_of(geo, x, y, z, bx, by, bz, s, inv_s);
+          const uint32_t w = __ldg(grid32 + ((unsigned long long)(uint32_t)d.y << 4) + (cell >> 5));
+          const int cur = nid;
+          nid = d.x + octant_step(x, y, z, bx, by, bz, s, inv_s);
+          d = __ldg(nd.desc + nid);
+          if (!(w & (1u << (cell & 31)))) hash_claim(h, stg, claim_key(cur, cell), v, ctrl);
+        } while (d.x >= 0);
         node_of[j] = nid;
         if (!nd.final_[nid]) leaf = nid;
       } else if (first) {
@@ -218,12 +261,31 @@ __global__ void __launch_bounds__(256, 6)
     if (leaf >= 0) {
       unsigned peers = __match_any_sync(act, leaf);
       if (lane_id() == (unsigned)(__ffs(peers) - 1)) {
-        unsigned long long old = atomicAdd(&nd.pending[leaf], (unsigned long long)__popc(peers));
-        if (old == 0) touched[atomicAdd(&ctrl->n_touched, 1u)] = leaf;
+        // fire-and-forget (no returned value to wait on); the touched leaves
+        // are compacted afterwards from pending > 0 (k_touched)
+        atomicAdd(&nd.pending[leaf], (unsigned long long)__popc(peers));
       }
     }
   }
   used_flush(h, stg, ctrl);
+}
+
+// The reference's `touched` list (pending 0 -> 1 transitions, _kernels.py:59-61)
+// as a set: leaves of [from, num_nodes) counted in this pass.  Iteration 1
+// scans every node, later iterations only the children created by the
+// previous split pass (the only leaves their points can reach).
+__global__ void k_touched(NodeCols nd, long long from, int32_t *__restrict__ touched, Ctrl *ctrl) {
+  const long long nn = ctrl->num_nodes;
+  for (long long i0 = from + (long long)blockIdx.x * blockDim.x; i0 < nn; i0 += gstride()) {
+    const long long i = i0 + threadIdx.x;
+    const bool t = i < nn && nd.pending[i] > 0 && !nd.inner[i] && !nd.final_[i];
+    const unsigned m = __ballot_sync(0xffffffffu, t);
+    if (!m) continue;
+    unsigned base = 0;
+    if (lane_id() == 0) base = atomicAdd(&ctrl->n_touched, (unsigned)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (t) touched[base + __popc(m & lanemask_lt())] = (int32_t)i;
+  }
 }
 
 // _split_pass (update.py:226-249): split iff count + pending > T and
@@ -250,13 +312,10 @@ __global__ void __launch_bounds__(kDecideBlock)
   }
   // phase 1: decide
   for (unsigned t = tid; t < nt; t += kDecideBlock) {
-    int nid = touched[t];
-    long long tot = nd.count[nid] + (long long)nd.pending[nid];
-    if (tot > geo.T && nd.level[nid] < geo.max_depth) {
-      atomicOr(&bitmap[nid >> 5], 1u << (nid & 31));
-    } else {
-      nd.final_[nid] = 1;
-    }
+    const int nid = touched[t];
+    const long long tot = nd.count[nid] + (long long)nd.pending[nid];
+    if (tot > geo.T && nd.level[nid] < geo.max_depth) atomicOr(&bitmap[nid >> 5], 1u << (nid & 31));
+    else nd.final_[nid] = 1;
   }
   __syncthreads();
   // phase 2: popcount prefix over bitmap words
@@ -342,11 +401,12 @@ __global__ void __launch_bounds__(kDecideBlock)
     }
   }
   __syncthreads();
-  // phase 6: clear the split bitmap for the next iteration
+  // phase 6: clear the split bitmap and the touched count for the next iteration
   for (unsigned t = tid; t < nt; t += kDecideBlock) {
     int nid = touched[t];
     bitmap[nid >> 5] = 0;
   }
+  if (tid == 0) ctrl->n_touched = 0;
 }
 
 // Octree.split, part 1 (octree.py:231-237, store.py:125-143), in parallel over
@@ -408,6 +468,7 @@ __global__ void k_exec_nodes(NodeCols nd, Geo geo, const int32_t *__restrict__ s
     nd.chunk_tail[c] = LOD_NO_CHUNK;
     nd.chunk_count[c] = 0;
     nd.grid_off[c] = -1;
+    nd.desc[c] = make_int2(-1, 0);
     nd.bmin[3 * c + 0] = nd.bmin[3 * nid + 0] + ((o & 1) ? half : 0.0);
     nd.bmin[3 * c + 1] = nd.bmin[3 * nid + 1] + ((o & 2) ? half : 0.0);
     nd.bmin[3 * c + 2] = nd.bmin[3 * nid + 2] + ((o & 4) ? half : 0.0);
@@ -421,7 +482,9 @@ __global__ void k_exec_nodes(NodeCols nd, Geo geo, const int32_t *__restrict__ s
       nd.chunk_tail[nid] = LOD_NO_CHUNK;
       nd.chunk_count[nid] = 0;
       const unsigned long long gstride_b = ((unsigned long long)geo.grid_bytes + 63ull) / 64ull * 64ull;
-      nd.grid_off[nid] = (long long)(ctrl->plan_grid0 + (unsigned long long)k * gstride_b);
+      const unsigned long long goff = ctrl->plan_grid0 + (unsigned long long)k * gstride_b;
+      nd.grid_off[nid] = (long long)goff;
+      nd.desc[nid] = make_int2((int)(ctrl->plan_num_nodes0 + 8ll * k), (int)(uint32_t)(goff >> 6));
       srank[nid] = -1;
     }
   }
@@ -440,19 +503,18 @@ __global__ void k_shift_nodes(const int32_t *__restrict__ src, int32_t *__restri
 __global__ void k_claim(NodeCols nd, Geo geo, PointSrc src, const uint32_t *__restrict__ grid32, long long n,
                         Hash h, Ctrl *ctrl) {
   __shared__ UsedStage stg;
-  if (threadIdx.x == 0) stg.n = 0;
-  __syncthreads();
+  used_init(stg);
   for (long long j0 = (long long)blockIdx.x * blockDim.x; j0 < n; j0 += gstride()) {
     const long long j = j0 + threadIdx.x;
     if (j >= n) continue;
     float xf, yf, zf;
     src.xyz(j, xf, yf, zf);
     const double x = xf, y = yf, z = zf;
-    double bx = geo.bmin0[0], by = geo.bmin0[1], bz = geo.bmin0[2], s = geo.size0;
+    double bx = geo.bmin0[0], by = geo.bmin0[1], bz = geo.bmin0[2], s = geo.size0, inv_s = geo.inv_by_level[0];
     int nid = 0;
     while (nd.inner[nid]) {
-      probe_cell(nd, geo, grid32, h, stg, ctrl, nid, x, y, z, bx, by, bz, s, (uint32_t)j);
-      const int o = octant_step(x, y, z, bx, by, bz, s);
+      probe_cell(nd, geo, grid32, h, stg, ctrl, nid, x, y, z, bx, by, bz, s, inv_s, (uint32_t)j);
+      const int o = octant_step(x, y, z, bx, by, bz, s, inv_s);
       nid = nd.children[8 * nid + o];
     }
   }
@@ -470,8 +532,7 @@ __global__ void k_resolve(NodeCols nd, Hash h, uint32_t *grid32, long long n_s, 
     HSlot *sl = h.slots + h.used[u];
     const unsigned long long key = sl->key;
     const uint32_t v = sl->val;
-    sl->key = kEmptyKey;
-    sl->val = 0xFFFFFFFFu;
+    *reinterpret_cast<ulonglong2 *>(sl) = make_ulonglong2(kEmptyKey, kEmptyHi);
     const int nid = (int)(key >> 32);
     const long long cell = (long long)(key & 0xFFFFFFFFu);
     const long long j = (v & kBatchTag) ? n_s + (long long)(v & ~kBatchTag) : (long long)v;
@@ -511,46 +572,43 @@ __global__ void k_emit(long long n, unsigned long long *__restrict__ wmask, cons
 
 // ---------------------------------------------------------------- sort + alloc
 
-// Items: points j in [0, n_all) keyed by their leaf, then backlog entries keyed
-// by their node.  Leaves and inner nodes are disjoint, so one stable sort by
-// node id yields every node's new samples in reference slot order.
-__global__ void k_keys(const int32_t *__restrict__ node_all, long long n_all, const int32_t *__restrict__ bnode,
-                       long long n_v, uint32_t *__restrict__ keys) {
-  const long long n = n_all + n_v;
-  for (long long i = gtid(); i < n; i += gstride()) keys[i] = (uint32_t)(i < n_all ? node_all[i] : bnode[i - n_all]);
-}
-
-__global__ void k_seg_flags(const uint32_t *__restrict__ skeys, long long n, uint32_t *__restrict__ flag) {
-  for (long long p = gtid(); p < n; p += gstride()) flag[p] = (p == 0 || skeys[p] != skeys[p - 1]) ? 1u : 0u;
-}
-
-__global__ void k_seg_list(const uint32_t *__restrict__ skeys, long long n, const uint32_t *__restrict__ hpos,
-                           int32_t *__restrict__ seg_node, long long *__restrict__ seg_start, const Ctrl *ctrl) {
-  for (long long p = gtid(); p < n; p += gstride()) {
-    if (p == 0 || skeys[p] != skeys[p - 1]) {
-      uint32_t d = hpos[p];
-      seg_node[d] = (int32_t)skeys[p];
-      seg_start[d] = p;
-    }
+// Touched nodes of the cycle = nodes with new samples (k_radix_prep's per-node
+// item counts), in ascending id.  Leaves and inner nodes are disjoint, so the
+// stable sort by node id lays every node's new samples out contiguously, in
+// reference slot order, starting at the exclusive prefix of the counts.
+__global__ void k_seg_pairs(const uint32_t *__restrict__ nodecnt, long long num_nodes, U64x2 *__restrict__ pairs) {
+  for (long long i = gtid(); i < num_nodes; i += gstride()) {
+    const uint32_t c = nodecnt[i];
+    pairs[i] = u64x2(c ? 1ull : 0ull, (unsigned long long)c);
   }
-  if (gtid() == 0) seg_start[ctrl->n_keys] = n;
 }
 
 __device__ __forceinline__ long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
 
-// collect_allocs (_kernels.py:253-277): need = ceil((count+pending)/C) -
-// chunk_count per touched node; here in ascending node id (chunk ids are not
-// observable; the acquisition count and arena growth are identical).
-__global__ void k_plan(NodeCols nd, Geo geo, const int32_t *__restrict__ seg_node,
-                       const long long *__restrict__ seg_start, const Ctrl *ctrl, U64x2 *__restrict__ plan) {
-  const long long K = (long long)ctrl->n_keys;
-  for (long long d = gtid(); d < K; d += gstride()) {
-    const int n = seg_node[d];
-    const long long len = seg_start[d + 1] - seg_start[d];
-    const long long cnt = nd.count[n];
+// Segment list + collect_allocs (_kernels.py:253-277): per touched node its
+// dense id, segment start and chunk need = ceil((count+pending)/C) -
+// chunk_count -- in ascending node id (chunk ids are not observable; the
+// acquisition count and the arena growth are the reference's).
+__global__ void k_seg_list(NodeCols nd, Geo geo, const uint32_t *__restrict__ nodecnt, long long num_nodes,
+                           const U64x2 *__restrict__ pairs_ex, int32_t *__restrict__ seg_node,
+                           long long *__restrict__ seg_start, int32_t *__restrict__ dense, U64x2 *__restrict__ plan,
+                           Ctrl *ctrl) {
+  for (long long i = gtid(); i < num_nodes; i += gstride()) {
+    const long long len = nodecnt[i];
+    if (!len) continue;
+    const long long d = (long long)pairs_ex[i].a;
+    seg_node[d] = (int32_t)i;
+    seg_start[d] = (long long)pairs_ex[i].b;
+    dense[i] = (int32_t)d;
+    const long long cnt = nd.count[i];
     const long long need = ceil_div(cnt + len, geo.C) - ceil_div(cnt, geo.C);
     const long long partial = (cnt % geo.C) != 0;
     plan[d] = u64x2((unsigned long long)need, (unsigned long long)(need + partial));
+  }
+  if (gtid() == 0) {
+    const U64x2 tot = ctrl->seg_tot;
+    seg_start[tot.a] = (long long)tot.b;
+    ctrl->n_keys = (unsigned)tot.a;
   }
 }
 
@@ -654,16 +712,14 @@ __global__ void k_alloc_chunks(NodeCols nd, PoolCols pool, Geo geo, const int32_
 // bmin + (c + 0.5) * (size_by_level[level] / g) in f64, then rounded to f32.
 __global__ void k_store(NodeCols nd, PoolCols pool, Geo geo, uint8_t *__restrict__ arena,
                         const uint32_t *__restrict__ skeys, const uint32_t *__restrict__ svals,
-                        const uint32_t *__restrict__ hpos, const long long *__restrict__ seg_start,
+                        const int32_t *__restrict__ dense, const long long *__restrict__ seg_start,
                         const U64x2 *__restrict__ plan, const U64x2 *__restrict__ plan_ex,
                         const int32_t *__restrict__ wl, long long n_items, long long n_all, PointSrc src,
                         const uint32_t *__restrict__ bcell, const uint32_t *__restrict__ brgba, const Ctrl *ctrl) {
   if (ctrl->error) return;
   for (long long p = gtid(); p < n_items; p += gstride()) {
-    const uint32_t key = skeys[p];
-    const int n = (int)key;
-    const bool head = (p == 0) || skeys[p - 1] != key;
-    const long long d = (long long)hpos[p] + (head ? 0 : -1);
+    const int n = (int)skeys[p];
+    const long long d = dense[n];
     const long long rank = p - seg_start[d];
     const long long cnt = nd.count[n];
     const long long slot = cnt + rank;

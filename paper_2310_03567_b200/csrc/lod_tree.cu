@@ -37,6 +37,7 @@ template <typename T>
 struct DBuf {
   T *p = nullptr;
   long long cap = 0;
+  bool plain = false;  // cudaMalloc instead of the stream-ordered pool (atomic-heavy buffers)
   // Grow to hold n elements; keep the first `keep` elements when growing.
   int ensure(long long n, cudaStream_t st, long long keep = 0) {
     if (n <= cap) return 0;
@@ -45,13 +46,19 @@ struct DBuf {
       fprintf(stderr, "[lod] grow buffer %lld -> %lld elems (%.1f MB)\n", cap, nc, nc * sizeof(T) / 1e6);
     T *q = nullptr;
     // stream-ordered: growth never synchronizes the device
-    if (cudaMallocAsync(&q, (size_t)nc * sizeof(T), st) != cudaSuccess) {
+    cudaError_t e = plain ? cudaMalloc(&q, (size_t)nc * sizeof(T)) : cudaMallocAsync(&q, (size_t)nc * sizeof(T), st);
+    if (e != cudaSuccess) {
       cudaGetLastError();
       return LOD_E_NOMEM;
     }
     if (p) {
       if (keep > 0) cudaMemcpyAsync(q, p, (size_t)std::min(keep, cap) * sizeof(T), cudaMemcpyDeviceToDevice, st);
-      cudaFreeAsync(p, st);
+      if (plain) {
+        cudaStreamSynchronize(st);
+        cudaFree(p);
+      } else {
+        cudaFreeAsync(p, st);
+      }
     }
     p = q;
     cap = nc;
@@ -95,6 +102,7 @@ __global__ void k_init_root(NodeCols nd, double b0, double b1, double b2) {
   nd.bmin[0] = b0;
   nd.bmin[1] = b1;
   nd.bmin[2] = b2;
+  nd.desc[0] = make_int2(-1, 0);
 }
 
 __global__ void k_cycle_begin(Ctrl *c) {
@@ -157,7 +165,7 @@ struct LodTree {
   Ctrl *h_ctrl = nullptr;
   // expansion scratch
   DBuf<int32_t> touched, split_list, node_b, node_all;
-  DBuf<uint32_t> bitmap, word_prefix;
+  DBuf<uint32_t> bitmap, word_prefix, tbits;
   DBuf<long long> scnt, schk, spill_off, chunk_off;
   DBuf<float4> spill;
   // sampling scratch
@@ -170,8 +178,8 @@ struct LodTree {
   DBuf<int32_t> bnode;
   DBuf<uint32_t> bcell, brgba;
   // sort / alloc scratch
-  DBuf<uint32_t> keys, keys_b, vals_a, vals_b, hist, flags, hpos, scan_u32;
-  DBuf<int32_t> seg_node, wl;
+  DBuf<uint32_t> keys, keys_b, vals_a, vals_b, hist, ghist, nodecnt, scan_u32;
+  DBuf<int32_t> seg_node, wl, dense;
   DBuf<long long> seg_start;
   DBuf<U64x2> plan, plan_ex, scan_u64x2;
   // inputs / outputs
@@ -250,12 +258,16 @@ static int ensure_nodes(LodTree *t, long long want, long long live) {
   RK(grow_col(t->nd.chunk_count, t->ncap, nc, live, st));
   RK(grow_col(t->nd.grid_off, t->ncap, nc, live, st));
   RK(grow_col(t->nd.bmin, t->ncap * 3, nc * 3, live * 3, st));
+  RK(grow_col(t->nd.desc, t->ncap, nc, live, st));
   // node-indexed scratch
   long long words = (nc + 31) / 32 + 1;
   long long oldw = t->bitmap.cap;
   RK(t->bitmap.ensure(words, st, oldw));
   if (t->bitmap.cap > oldw) CK(cudaMemsetAsync(t->bitmap.p + oldw, 0, (size_t)(t->bitmap.cap - oldw) * 4, st));
   RK(t->word_prefix.ensure(words, st));
+  long long oldt = t->tbits.cap;
+  RK(t->tbits.ensure(words, st, oldt));
+  if (t->tbits.cap > oldt) CK(cudaMemsetAsync(t->tbits.p + oldt, 0, (size_t)(t->tbits.cap - oldt) * 4, st));
   // the split plan of the running iteration survives the growth (k_execute reads it)
   RK(t->touched.ensure(nc, st));
   RK(t->split_list.ensure(nc, st, t->split_list.cap));
@@ -311,6 +323,7 @@ static int abort_cycle(LodTree *t, int code) {
   }
   long long words = (t->ncap + 31) / 32 + 1;
   cudaMemsetAsync(t->bitmap.p, 0, (size_t)words * 4, t->st);
+  cudaMemsetAsync(t->tbits.p, 0, (size_t)t->tbits.cap * 4, t->st);
   cudaStreamSynchronize(t->st);
   // counters: the device ctrl keeps whatever was applied before the failure
   sync_ctrl(t);
@@ -357,6 +370,9 @@ int lod_tree_create(const LodParams *params, LodTree **out) {
   if (lod_device_count(&ndev) != LOD_OK || p.device >= ndev) return LOD_E_NO_DEVICE;
   LodTree *t = new LodTree();
   t->p = p;
+  if (getenv("LOD_PLAIN_HASH")) {
+    t->hslots.plain = t->hslots2.plain = true;
+  }
   t->dev = p.device;
   cudaSetDevice(t->dev);
   CK(cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking));
@@ -373,6 +389,14 @@ int lod_tree_create(const LodParams *params, LodTree **out) {
   for (int k = 0; k < 3; ++k) g.bmin0[k] = p.bmin[k];
   g.size0 = p.size;
   for (int k = 0; k < 64; ++k) g.size_by_level[k] = p.size * std::pow(0.5, (double)k);
+  {
+    // a power-of-two root size makes every node size a power of two: then the
+    // cell formula's division is an exact multiplication by 1/s
+    int e = 0;
+    const double m = std::frexp(p.size, &e);
+    g.pow2 = (m == 0.5 && p.size >= 0x1p-900 && p.size <= 0x1p900) ? 1 : 0;
+    for (int k = 0; k < 64; ++k) g.inv_by_level[k] = g.pow2 ? 1.0 / g.size_by_level[k] : 0.0;
+  }
   g.g = (int)p.grid_res;
   g.grid_bytes = p.grid_res * p.grid_res * p.grid_res / 8;
   g.T = p.leaf_threshold;
@@ -410,17 +434,18 @@ int lod_tree_destroy(LodTree *t) {
   f(t->arena);
   f(t->nd.parent); f(t->nd.octant); f(t->nd.level); f(t->nd.children); f(t->nd.inner);
   f(t->nd.final_); f(t->nd.count); f(t->nd.pending); f(t->nd.chunk_head); f(t->nd.chunk_tail);
-  f(t->nd.chunk_count); f(t->nd.grid_off); f(t->nd.bmin);
+  f(t->nd.chunk_count); f(t->nd.grid_off); f(t->nd.bmin); f(t->nd.desc);
   f(t->pool.next); f(t->pool.payload_off); f(t->pool.occupied); f(t->pool.owner); f(t->pool.cidx);
   f(t->pool.free_stack);
   f(t->d_ctrl);
   if (t->h_ctrl) cudaFreeHost(t->h_ctrl);
   t->touched.release(); t->split_list.release(); t->node_b.release(); t->node_all.release();
-  t->bitmap.release(); t->word_prefix.release(); t->scnt.release(); t->schk.release();
+  t->bitmap.release(); t->word_prefix.release(); t->tbits.release(); t->scnt.release(); t->schk.release();
   t->spill_off.release(); t->chunk_off.release(); t->spill.release(); t->hslots.release(); t->hslots2.release();
   t->hused.release(); t->wins.release(); t->wmask.release(); t->srank.release(); t->wcount.release(); t->wbase.release();
   t->bnode.release(); t->bcell.release(); t->brgba.release(); t->keys.release(); t->keys_b.release();
-  t->vals_a.release(); t->vals_b.release(); t->hist.release(); t->flags.release(); t->hpos.release();
+  t->vals_a.release(); t->vals_b.release(); t->hist.release(); t->ghist.release(); t->nodecnt.release();
+  t->dense.release();
   t->scan_u32.release(); t->seg_node.release(); t->wl.release(); t->seg_start.release();
   t->plan.release(); t->plan_ex.release(); t->scan_u64x2.release(); t->in_xyz.release();
   t->in_rgba.release(); t->gbuf.release(); t->gnodes.release(); t->goff.release(); t->gstart.release();
@@ -497,6 +522,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   long long n_all = n, n_s = 0;
   int first = 1, iters = 0;
   long long splits_cycle = 0;
+  long long touch_from = 0;  // leaves a count pass can reach: all (iteration 1), new children (later)
   // claim table: sized from the batch and the previous cycle's claims, grown
   // (rehashed) between iterations when the next pass could overfill it; a
   // table that still fills up falls back to a separate claim pass
@@ -514,13 +540,11 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   uint32_t *grid32 = reinterpret_cast<uint32_t *>(t->arena);
   for (;;) {
     ++iters;
-    if (!first) {
-      k_reset_touched<<<1, 1, 0, st>>>(t->d_ctrl);
-      ++lod::g_launches;
-    }
     if (prof) cudaEventRecord(t->ev[12], st);
-    k_count<<<grid_for(n_all), 256, 0, st>>>(t->nd, t->geo, src, node_of, n_all, first, grid32, hs, t->touched.p,
-                                            t->d_ctrl); ++lod::g_launches;
+    k_count<<<grid_for(n_all), 256, 0, st>>>(t->nd, t->geo, src, node_of, n_all, first, grid32, hs, t->d_ctrl);
+    ++lod::g_launches;
+    k_touched<<<grid_for(t->num_nodes - touch_from), 256, 0, st>>>(t->nd, touch_from, t->touched.p, t->d_ctrl);
+    ++lod::g_launches;
     if (prof) cudaEventRecord(t->ev[13], st);
     k_decide<<<1, kDecideBlock, 0, st>>>(t->nd, t->geo, t->touched.p, t->bitmap.p, t->word_prefix.p,
                                          t->split_list.p, t->srank.p, t->scnt.p, t->schk.p, t->spill_off.p,
@@ -548,6 +572,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     }
     k_exec_nodes<<<grid_for(8 * ns), 256, 0, st>>>(t->nd, t->geo, t->split_list.p, t->srank.p, ns,
                                                    t->d_ctrl); ++lod::g_launches;
+    touch_from = h.plan_num_nodes0;
     t->num_nodes = h.num_nodes;
     if (first) {
       n_s = h.spill_total;
@@ -579,6 +604,11 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   }
   mark(0);
   Ctrl h1 = *t->h_ctrl;
+#ifdef LOD_EXP_COUNT
+  fprintf(stderr, "[lod] claims=%lld probes=%lld n_used=%llu hcap=%llu n=%lld n_s=%lld\n", h1.alloc_F, h1.alloc_A,
+          h1.n_used, t->hcap, (long long)n, n_s);
+  cudaMemsetAsync(&t->d_ctrl->alloc_F, 0, 16, st);
+#endif
   t->num_nodes = h1.num_nodes;
   const long long num_nodes = h1.num_nodes;
   // ---- resolve the claims (update.py:298-315)
@@ -629,40 +659,48 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   mark(2);
   // ---- sort: every new sample by node id, stable (slot order)
   const long long n_items = n_all + n_v;
+  const int passes = radix_passes((uint32_t)(num_nodes - 1));
   RK(t->keys.ensure(n_items, st));
   RK(t->keys_b.ensure(n_items, st));
   RK(t->vals_a.ensure(n_items, st));
   RK(t->vals_b.ensure(n_items, st));
-  RK(t->flags.ensure(n_items, st));
-  RK(t->hpos.ensure(n_items, st));
-  RK(t->hist.ensure(radix_hist_elems(n_items), st));
-  RK(t->scan_u32.ensure(scan_scratch_elems(std::max<long long>(n_items, radix_hist_elems(n_items))), st));
-  k_keys<<<grid_for(n_items), 256, 0, st>>>(node_of, n_all, t->bnode.p, n_v, t->keys.p); ++lod::g_launches;
+  RK(t->hist.ensure(std::max<long long>(radix_lb_elems(n_items), kMaxPasses * kRadixDigits), st));
+  RK(t->ghist.ensure(kMaxPasses * kRadixDigits, st));
+  RK(t->nodecnt.ensure(num_nodes, st));
+  CK(cudaMemsetAsync(t->ghist.p, 0, kMaxPasses * kRadixDigits * 4, st));
+  CK(cudaMemsetAsync(t->nodecnt.p, 0, (size_t)num_nodes * 4, st));
+  k_radix_prep<<<std::min<unsigned>(grid_for(n_items), 148), kRadixBlock, 0, st>>>(node_of, n_all, t->bnode.p, n_v, num_nodes, t->keys.p,
+                                                          t->nodecnt.p);
+  ++lod::g_launches;
+  k_radix_ghist<<<std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st>>>(t->nodecnt.p, num_nodes, passes,
+                                                                             t->ghist.p);
+  ++lod::g_launches;
   RadixScratch rs;
   rs.keys_b = t->keys_b.p;
   rs.vals_a = t->vals_a.p;
   rs.vals_b = t->vals_b.p;
-  rs.hist = t->hist.p;
-  rs.scan_tmp = t->scan_u32.p;
+  rs.ghist = t->ghist.p;
+  rs.lb = t->hist.p;
   uint32_t *skeys = nullptr, *svals = nullptr;
-  stable_multisplit(t->keys.p, n_items, (uint32_t)(num_nodes - 1), rs, st, &skeys, &svals);
+  stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals);
   mark(3);
-  // ---- allocation (update.py:317-331)
+  // ---- allocation (update.py:317-331): touched nodes = nodes with new samples, ascending id
   const long long Kb = num_nodes + 1;  // bound on touched nodes
   RK(t->seg_node.ensure(Kb, st));
   RK(t->seg_start.ensure(Kb + 1, st));
+  RK(t->dense.ensure(Kb, st));
   RK(t->plan.ensure(Kb, st));
   RK(t->plan_ex.ensure(Kb, st));
   RK(t->scan_u64x2.ensure(scan_scratch_elems(Kb), st));
   const long long acq_bound = n_items / C + Kb + 1;
   RK(t->wl.ensure(acq_bound + Kb + 1, st));
   RK(ensure_chunks(t, h1.allocated_total + acq_bound + 1, h1.allocated_total));
-  k_seg_flags<<<grid_for(n_items), 256, 0, st>>>(skeys, n_items, t->flags.p); ++lod::g_launches;
-  exclusive_scan<uint32_t>(t->flags.p, t->hpos.p, n_items, &t->d_ctrl->n_keys, t->scan_u32.p, st);
-  k_seg_list<<<grid_for(n_items), 256, 0, st>>>(skeys, n_items, t->hpos.p, t->seg_node.p, t->seg_start.p,
-                                               t->d_ctrl); ++lod::g_launches;
+  k_seg_pairs<<<grid_for(num_nodes), 256, 0, st>>>(t->nodecnt.p, num_nodes, t->plan_ex.p); ++lod::g_launches;
+  exclusive_scan<U64x2>(t->plan_ex.p, t->plan_ex.p, num_nodes, &t->d_ctrl->seg_tot, t->scan_u64x2.p, st);
   CK(cudaMemsetAsync(t->plan.p, 0, (size_t)Kb * sizeof(U64x2), st));
-  k_plan<<<grid_for(Kb), 256, 0, st>>>(t->nd, t->geo, t->seg_node.p, t->seg_start.p, t->d_ctrl, t->plan.p); ++lod::g_launches;
+  k_seg_list<<<grid_for(num_nodes), 256, 0, st>>>(t->nd, t->geo, t->nodecnt.p, num_nodes, t->plan_ex.p,
+                                                  t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->d_ctrl);
+  ++lod::g_launches;
   exclusive_scan<U64x2>(t->plan.p, t->plan_ex.p, Kb, &t->d_ctrl->acq_tot, t->scan_u64x2.p, st);
   k_alloc_begin<<<1, 1, 0, st>>>(t->d_ctrl, t->geo, t->arena_cap); ++lod::g_launches;
   k_alloc_nodes<<<grid_for(Kb), 256, 0, st>>>(t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p, t->plan.p,
@@ -671,7 +709,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
                                                       t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl); ++lod::g_launches;
   mark(4);
   // ---- store (update.py:357-373)
-  k_store<<<grid_for(n_items), 256, 0, st>>>(t->nd, t->pool, t->geo, t->arena, skeys, svals, t->hpos.p,
+  k_store<<<grid_for(n_items), 256, 0, st>>>(t->nd, t->pool, t->geo, t->arena, skeys, svals, t->dense.p,
                                              t->seg_start.p, t->plan.p, t->plan_ex.p, t->wl.p, n_items, n_all,
                                              src, t->bcell.p, t->brgba.p, t->d_ctrl); ++lod::g_launches;
   mark(5);

@@ -1,17 +1,23 @@
-// radix.cuh -- stable multisplit of an ordered item list by a small dense key.
+// radix.cuh -- stable multisplit of an ordered item list by node id.
 //
 // The reference appends records to each node in global ingestion order
 // (store_points/store_voxels, _kernels.py:155-250: slot = count[node]++ in
 // all-array / backlog order).  On the GPU that order is recovered with an LSD
-// radix sort over dense node keys: 8-bit digits, one pass per key byte, each
-// pass a tile histogram -> digit-major exclusive scan -> stable tile scatter.
+// radix sort over node ids, 8-bit digits, in the onesweep form: one upfront
+// pass builds the key array and the per-node item counts (which define the
+// node segments and, summed by digit, every pass's digit totals), then ONE
+// kernel per digit pass ranks its tile, publishes its per-digit counts and
+// resolves its global offsets with a decoupled look-back over earlier tiles.
 // Stability inside a tile comes from warp-ordered rounds: each warp owns a
 // contiguous 512-item range, ranks lanes with __match_any_sync, and keeps a
 // per-warp digit histogram in shared memory; warps are combined in order.
+// The tile is then reordered by digit in shared memory so the global writes
+// go out as contiguous digit runs.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "lod_common.cuh"
 #include "scan.cuh"
 
 namespace lod {
@@ -20,83 +26,174 @@ constexpr int kRadixBits = 8;
 constexpr int kRadixDigits = 1 << kRadixBits;
 constexpr int kRadixBlock = 256;  // 8 warps
 constexpr int kRadixWarps = kRadixBlock / 32;
-constexpr int kRadixRounds = 16;  // per warp: 16 rounds x 32 lanes
-constexpr long long kRadixTile = (long long)kRadixBlock * kRadixRounds;
+constexpr int kRadixRounds = 12;  // per warp: 12 rounds x 32 lanes (tile staged in 40 KB smem)
+constexpr int kRadixTile = kRadixBlock * kRadixRounds;
+constexpr int kMaxPasses = 4;
+constexpr int kNodeHistSmem = 10240;  // node counts kept in shared memory up to this many nodes
 
+// look-back words: [31:30] status (0 empty, 1 aggregate, 2 inclusive prefix), [29:0] count
+constexpr uint32_t kLbAgg = 1u << 30, kLbPre = 2u << 30, kLbMask = (1u << 30) - 1;
+
+// Items: points j in [0, n_all) keyed by their leaf, then backlog entries keyed
+// by their node.  Writes the key array and the per-node item counts (= each
+// node's new samples this cycle; hot leaves are aggregated per warp first).
 __global__ void __launch_bounds__(kRadixBlock)
-    k_radix_hist(const uint32_t *__restrict__ keys, long long n, int shift, long long ntiles,
-                 uint32_t *__restrict__ hist) {
-  __shared__ uint32_t h[kRadixDigits];
-  for (int d = threadIdx.x; d < kRadixDigits; d += kRadixBlock) h[d] = 0;
+    k_radix_prep(const int32_t *__restrict__ node_all, long long n_all, const int32_t *__restrict__ bnode,
+                 long long n_v, long long num_nodes, uint32_t *__restrict__ keys, uint32_t *__restrict__ nodecnt) {
+  __shared__ uint32_t nc[kNodeHistSmem];
+  const bool smem_nodes = num_nodes <= kNodeHistSmem;
+  if (smem_nodes)
+    for (long long i = threadIdx.x; i < num_nodes; i += kRadixBlock) nc[i] = 0;
   __syncthreads();
-  long long base = (long long)blockIdx.x * kRadixTile;
-  for (int i = threadIdx.x; i < kRadixTile; i += kRadixBlock) {
-    long long idx = base + i;
-    if (idx < n) atomicAdd(&h[(__ldg(keys + idx) >> shift) & (kRadixDigits - 1)], 1u);
+  const long long n = n_all + n_v;
+  for (long long i0 = (long long)blockIdx.x * kRadixBlock; i0 < n; i0 += gstride()) {
+    const long long i = i0 + threadIdx.x;
+    uint32_t key = 0xFFFFFFFFu;
+    if (i < n) {
+      key = (uint32_t)(i < n_all ? node_all[i] : bnode[i - n_all]);
+      keys[i] = key;
+    }
+    const unsigned act = __ballot_sync(0xffffffffu, i < n);
+    if (i < n) {
+      const unsigned peers = __match_any_sync(act, key);
+      if (lane_id() == (unsigned)(__ffs(peers) - 1)) {
+        if (smem_nodes) atomicAdd(&nc[key], (uint32_t)__popc(peers));
+        else atomicAdd(&nodecnt[key], (uint32_t)__popc(peers));
+      }
+    }
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < kRadixDigits; d += kRadixBlock)
-    hist[(long long)d * ntiles + blockIdx.x] = h[d];
+  if (smem_nodes)
+    for (long long i = threadIdx.x; i < num_nodes; i += kRadixBlock)
+      if (nc[i]) atomicAdd(nodecnt + i, nc[i]);
 }
 
-// vals_in == nullptr means the identity permutation (item index).
-__global__ void __launch_bounds__(kRadixBlock)
-    k_radix_scatter(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
-                    long long n, int shift, long long ntiles, const uint32_t *__restrict__ gofs,
-                    uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out) {
-  __shared__ uint32_t wh[kRadixWarps][kRadixDigits];
+// Digit totals of every pass from the per-node counts (keys are node ids).
+__global__ void k_radix_ghist(const uint32_t *__restrict__ nodecnt, long long num_nodes, int passes,
+                              uint32_t *__restrict__ ghist) {
+  __shared__ uint32_t h[kMaxPasses * kRadixDigits];
+  for (int i = threadIdx.x; i < kMaxPasses * kRadixDigits; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (long long n = gtid(); n < num_nodes; n += gstride()) {
+    const uint32_t c = nodecnt[n];
+    if (c)
+      for (int p = 0; p < passes; ++p) atomicAdd(&h[p * kRadixDigits + ((n >> (p * kRadixBits)) & 0xFF)], c);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * kRadixDigits; i += blockDim.x)
+    if (h[i]) atomicAdd(ghist + i, h[i]);
+}
+
+// One LSD pass.  vals_in == nullptr means the identity permutation.
+// `lb` holds ntiles * 256 look-back words + 1 tile ticket, zeroed before the pass.
+__global__ void __launch_bounds__(kRadixBlock, 4)
+    k_onesweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in, long long n, int shift,
+               const uint32_t *__restrict__ ghist_pass, uint32_t *lb, long long ntiles,
+               uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out) {
+  __shared__ uint32_t wh[kRadixWarps][kRadixDigits];  // per-warp digit counts -> warp offsets
+  __shared__ uint32_t dstart[kRadixDigits];           // tile-local digit start
+  __shared__ uint32_t gbase[kRadixDigits];            // global position of the tile's digit run
+  __shared__ uint32_t sk[kRadixTile], sv[kRadixTile];
+  __shared__ uint16_t sloc[kRadixTile];
+  __shared__ uint32_t sh[kRadixBlock / 32 + 1];
+  __shared__ uint32_t s_tile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(lb + ntiles * kRadixDigits, 1u);  // launch-order tile ids
   for (int d = lane; d < kRadixDigits; d += 32) wh[warp][d] = 0;
-  __syncwarp();
-  const long long wbase = (long long)blockIdx.x * kRadixTile + (long long)warp * (32 * kRadixRounds);
-  uint32_t key[kRadixRounds], val[kRadixRounds], loc[kRadixRounds];
+  __syncthreads();
+  const long long tile = s_tile;
+  const long long t0 = tile * kRadixTile;
+  const int wofs = warp * (32 * kRadixRounds);
   const unsigned lt = lanemask_lt();
-#pragma unroll
+  // 1) warp-ordered ranking; keys/values/ranks staged in input order
   for (int r = 0; r < kRadixRounds; ++r) {
-    long long idx = wbase + r * 32 + lane;
-    bool ok = idx < n;
-    key[r] = ok ? __ldg(keys_in + idx) : 0u;
-    val[r] = ok ? (vals_in ? __ldg(vals_in + idx) : (uint32_t)idx) : 0u;
-    int d = ok ? (int)((key[r] >> shift) & (kRadixDigits - 1)) : kRadixDigits + 1;
-    unsigned peers = __match_any_sync(0xffffffffu, d);
-    uint32_t b = ok ? wh[warp][d] : 0u;
-    loc[r] = b + __popc(peers & lt);
+    const int li = wofs + r * 32 + lane;
+    const long long idx = t0 + li;
+    const bool ok = idx < n;
+    const uint32_t key = ok ? __ldg(keys_in + idx) : 0u;
+    const int d = ok ? (int)((key >> shift) & (kRadixDigits - 1)) : kRadixDigits + 1;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t b = ok ? wh[warp][d] : 0u;
+    sk[li] = key;
+    sv[li] = ok ? (vals_in ? __ldg(vals_in + idx) : (uint32_t)idx) : 0u;
+    sloc[li] = (uint16_t)(b + __popc(peers & lt));
     __syncwarp();
     if (ok && lane == __ffs(peers) - 1) wh[warp][d] = b + __popc(peers);
     __syncwarp();
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < kRadixDigits; d += kRadixBlock) {
-    uint32_t run = gofs[(long long)d * ntiles + blockIdx.x];
+  // 2) per digit: warp offsets, tile-local digit start, decoupled look-back
+  {
+    const int d = threadIdx.x;
+    uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < kRadixWarps; ++w) {
-      uint32_t t = wh[w][d];
+      const uint32_t c = wh[w][d];
       wh[w][d] = run;
-      run += t;
+      run += c;
+    }
+    uint32_t tot;
+    dstart[d] = block_exclusive_scan<uint32_t, kRadixBlock>(run, sh, tot);
+    uint32_t *mine = lb + tile * kRadixDigits + d;
+    uint32_t excl = 0;
+    if (tile == 0) {
+      atomicExch(mine, kLbPre | run);
+    } else {
+      atomicExch(mine, kLbAgg | run);
+      long long t = tile - 1;
+      while (true) {
+        const uint32_t v = *((volatile uint32_t *)(lb + t * kRadixDigits + d));
+        if ((v & ~kLbMask) == 0) continue;  // predecessor not published yet
+        excl += v & kLbMask;
+        if ((v & ~kLbMask) == kLbPre) break;
+        --t;
+      }
+      atomicExch(mine, kLbPre | (excl + run));
+    }
+    // digit base of this pass (exclusive scan of the totals) + earlier tiles
+    const uint32_t gex = block_exclusive_scan<uint32_t, kRadixBlock>(ghist_pass[d], sh, tot);
+    gbase[d] = gex + excl;
+  }
+  __syncthreads();
+  // 3) reorder the tile by digit in shared memory
+  uint32_t rk[kRadixRounds], rv[kRadixRounds], rp[kRadixRounds];
+#pragma unroll
+  for (int r = 0; r < kRadixRounds; ++r) {
+    const int li = wofs + r * 32 + lane;
+    const uint32_t key = sk[li];
+    const int d = (int)((key >> shift) & (kRadixDigits - 1));
+    rk[r] = key;
+    rv[r] = sv[li];
+    rp[r] = dstart[d] + wh[warp][d] + sloc[li];
+  }
+  __syncthreads();
+  const long long valid = min((long long)kRadixTile, n - t0);
+#pragma unroll
+  for (int r = 0; r < kRadixRounds; ++r) {
+    if ((long long)(wofs + r * 32 + lane) < valid) {
+      sk[rp[r]] = rk[r];
+      sv[rp[r]] = rv[r];
     }
   }
   __syncthreads();
-#pragma unroll
-  for (int r = 0; r < kRadixRounds; ++r) {
-    long long idx = wbase + r * 32 + lane;
-    if (idx < n) {
-      int d = (int)((key[r] >> shift) & (kRadixDigits - 1));
-      uint32_t pos = wh[warp][d] + loc[r];
-      keys_out[pos] = key[r];
-      vals_out[pos] = val[r];
-    }
+  // 4) contiguous digit runs out to global memory
+  for (int p = threadIdx.x; p < valid; p += kRadixBlock) {
+    const uint32_t key = sk[p];
+    const int d = (int)((key >> shift) & (kRadixDigits - 1));
+    const uint32_t pos = gbase[d] + (uint32_t)p - dstart[d];
+    keys_out[pos] = key;
+    vals_out[pos] = sv[p];
   }
 }
 
 struct RadixScratch {
   uint32_t *keys_b = nullptr, *vals_a = nullptr, *vals_b = nullptr;
-  uint32_t *hist = nullptr, *scan_tmp = nullptr;
+  uint32_t *ghist = nullptr;  // kMaxPasses * 256
+  uint32_t *lb = nullptr;     // ntiles * 256 + 1 per pass (reused)
 };
 
-inline long long radix_hist_elems(long long n) {
-  long long ntiles = (n + kRadixTile - 1) / kRadixTile;
-  return ntiles * kRadixDigits;
-}
+inline long long radix_tiles(long long n) { return (n + kRadixTile - 1) / kRadixTile; }
+inline long long radix_lb_elems(long long n) { return radix_tiles(n) * kRadixDigits + 1; }
 
 inline int radix_passes(uint32_t max_key) {
   int bits = 0;
@@ -105,24 +202,22 @@ inline int radix_passes(uint32_t max_key) {
   return p < 1 ? 1 : p;
 }
 
-// Stable sort of (keys, item index) by key.  On return *keys_res / *vals_res
-// point at the sorted keys / original item indices (inside keys or scratch).
-inline void stable_multisplit(uint32_t *keys, long long n, uint32_t max_key, RadixScratch &s,
-                              cudaStream_t st, uint32_t **keys_res, uint32_t **vals_res) {
-  int passes = radix_passes(max_key);
-  long long ntiles = (n + kRadixTile - 1) / kRadixTile;
+// Stable sort of (keys, item index) by key (keys/ghist from k_radix_prep +
+// k_radix_ghist).  On return *keys_res / *vals_res point at the sorted keys /
+// original item indices.
+inline void stable_multisplit(uint32_t *keys, long long n, int passes, RadixScratch &s, cudaStream_t st,
+                              uint32_t **keys_res, uint32_t **vals_res) {
+  const long long ntiles = radix_tiles(n);
   uint32_t *kin = keys, *kout = s.keys_b;
   const uint32_t *vin = nullptr;
   uint32_t *vout = s.vals_a;
   for (int p = 0; p < passes; ++p) {
-    int shift = p * kRadixBits;
     if (n > 0) {
-      k_radix_hist<<<(unsigned)ntiles, kRadixBlock, 0, st>>>(kin, n, shift, ntiles, s.hist); ++lod::g_launches;
-      exclusive_scan<uint32_t>(s.hist, s.hist, ntiles * kRadixDigits, nullptr, s.scan_tmp, st);
-      k_radix_scatter<<<(unsigned)ntiles, kRadixBlock, 0, st>>>(kin, vin, n, shift, ntiles, s.hist,
-                                                                kout, vout); ++lod::g_launches;
+      cudaMemsetAsync(s.lb, 0, (size_t)(ntiles * kRadixDigits + 1) * 4, st);
+      k_onesweep<<<(unsigned)ntiles, kRadixBlock, 0, st>>>(kin, vin, n, p * kRadixBits, s.ghist + p * kRadixDigits,
+                                                           s.lb, ntiles, kout, vout);
+      ++lod::g_launches;
     }
-    // ping-pong
     uint32_t *kt = kin;
     kin = kout;
     kout = kt;

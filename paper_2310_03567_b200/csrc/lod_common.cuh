@@ -17,6 +17,30 @@ namespace lod {
 // kernels launched by this thread (reported per call as LodBatchStats.launches)
 inline thread_local long long g_launches = 0;
 
+// Programmatic dependent launch (sm_90+): every update kernel is launched with
+// programmatic stream serialization, so the next kernel's launch overlaps the
+// tail of the current one; each kernel waits for its predecessor's memory
+// before its first dependent access.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ++g_launches;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 constexpr int kWarp = 32;
 
 __device__ __forceinline__ long long f2i64(double v) {

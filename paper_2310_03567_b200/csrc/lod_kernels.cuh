@@ -63,6 +63,8 @@ struct Ctrl {
 
 __device__ __forceinline__ void set_error(Ctrl *c, int code) { atomicCAS(&c->error, 0, code); }
 
+constexpr int kMaxPassesHist = 4 * 256;  // radix digit totals (radix.cuh kMaxPasses * kRadixDigits)
+
 // ---------------------------------------------------------------- claim hash
 
 // Open-addressing table of (node, cell) -> min all-array index, 16-byte slots
@@ -204,7 +206,7 @@ __device__ __forceinline__ void probe_cell(const NodeCols &nd, const Geo &geo, c
 
 // Grow the claim table between expansion iterations: re-insert every key
 // claimed so far (keys are unique, values carried) into the new table.
-__global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl *ctrl) {
+__global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl *ctrl) { lod::pdl_wait();
   const unsigned long long nu = ctrl->n_used;
   for (long long u = gtid(); u < (long long)nu; u += gstride()) {
     const HSlot o = old_slots[h.used[u]];
@@ -224,7 +226,7 @@ __global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl
 // accumulated descent bounds byte for byte, _kernels.py:9-13).
 __global__ void __launch_bounds__(256, 6)
     k_count(NodeCols nd, Geo geo, PointSrc src, int32_t *__restrict__ node_of, long long n, int first,
-            const uint32_t *__restrict__ grid32, Hash h, Ctrl *ctrl) {
+            const uint32_t *__restrict__ grid32, Hash h, Ctrl *ctrl) { lod::pdl_wait();
   __shared__ UsedStage stg;
   used_init(stg);
   for (long long j0 = (long long)blockIdx.x * blockDim.x; j0 < n; j0 += gstride()) {
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(256, 6)
 // as a set: leaves of [from, num_nodes) counted in this pass.  Iteration 1
 // scans every node, later iterations only the children created by the
 // previous split pass (the only leaves their points can reach).
-__global__ void k_touched(NodeCols nd, long long from, int32_t *__restrict__ touched, Ctrl *ctrl) {
+__global__ void k_touched(NodeCols nd, long long from, int32_t *__restrict__ touched, Ctrl *ctrl) { lod::pdl_wait();
   const long long nn = ctrl->num_nodes;
   for (long long i0 = from + (long long)blockIdx.x * blockDim.x; i0 < nn; i0 += gstride()) {
     const long long i = i0 + threadIdx.x;
@@ -298,7 +300,7 @@ constexpr int kDecideBlock = 1024;
 __global__ void __launch_bounds__(kDecideBlock)
     k_decide(NodeCols nd, Geo geo, const int32_t *__restrict__ touched, uint32_t *bitmap, uint32_t *word_prefix,
              int32_t *split_list, int32_t *srank, long long *scnt, long long *schk, long long *spill_off,
-             long long *chunk_off, Ctrl *ctrl, long long spill_cap, unsigned long long arena_cap) {
+             long long *chunk_off, Ctrl *ctrl, long long spill_cap, unsigned long long arena_cap) { lod::pdl_wait();
   __shared__ uint32_t sh32[kDecideBlock / 32 + 1];
   __shared__ U64x2 sh64[kDecideBlock / 32 + 1];
   __shared__ unsigned int s_maxlvl;
@@ -416,7 +418,7 @@ __global__ void __launch_bounds__(kDecideBlock)
 __global__ void k_exec_chunks(PoolCols pool, Geo geo, const uint8_t *__restrict__ arena, long long nchunks,
                               const int32_t *__restrict__ srank, const long long *__restrict__ spill_off,
                               const long long *__restrict__ chunk_off, float4 *spill_buf, int32_t *spill_node_of,
-                              const Ctrl *ctrl) {
+                              const Ctrl *ctrl) { lod::pdl_wait();
   const long long warp = gtid() >> 5, nwarps = gstride() >> 5;
   const int lane = threadIdx.x & 31;
   for (long long cid = warp; cid < nchunks; cid += nwarps) {
@@ -447,7 +449,7 @@ __global__ void k_exec_chunks(PoolCols pool, Geo geo, const uint8_t *__restrict_
 // grid (arena regions are zeroed and never reused) and gets 8 children in
 // octant order with bmin = base + half (f64).  One thread per (split, octant).
 __global__ void k_exec_nodes(NodeCols nd, Geo geo, const int32_t *__restrict__ split_list, int32_t *srank,
-                             long long ns, const Ctrl *ctrl) {
+                             long long ns, const Ctrl *ctrl) { lod::pdl_wait();
   for (long long t = gtid(); t < ns * 8; t += gstride()) {
     const long long k = t >> 3;
     const int o = (int)(t & 7);
@@ -492,7 +494,7 @@ __global__ void k_exec_nodes(NodeCols nd, Geo geo, const int32_t *__restrict__ s
 
 // Move the batch part of the per-point node cache behind the spill segment:
 // all = [spill || batch] (update.py:281-286).
-__global__ void k_shift_nodes(const int32_t *__restrict__ src, int32_t *__restrict__ dst, long long n) {
+__global__ void k_shift_nodes(const int32_t *__restrict__ src, int32_t *__restrict__ dst, long long n) { lod::pdl_wait();
   for (long long i = gtid(); i < n; i += gstride()) dst[i] = src[i];
 }
 
@@ -501,7 +503,7 @@ __global__ void k_shift_nodes(const int32_t *__restrict__ src, int32_t *__restri
 // Fallback claim pass (only when the cycle's claim table overflowed): a full
 // descent of every point over the final topology with all-array indices.
 __global__ void k_claim(NodeCols nd, Geo geo, PointSrc src, const uint32_t *__restrict__ grid32, long long n,
-                        Hash h, Ctrl *ctrl) {
+                        Hash h, Ctrl *ctrl) { lod::pdl_wait();
   __shared__ UsedStage stg;
   used_init(stg);
   for (long long j0 = (long long)blockIdx.x * blockDim.x; j0 < n; j0 += gstride()) {
@@ -525,7 +527,7 @@ __global__ void k_claim(NodeCols nd, Geo geo, PointSrc src, const uint32_t *__re
 // bit, record the win at the node's level for the winner, and free the slot.
 __global__ void k_resolve(NodeCols nd, Hash h, uint32_t *grid32, long long n_s, int D,
                           unsigned long long *__restrict__ wins, unsigned long long *__restrict__ wmask,
-                          const Ctrl *ctrl) {
+                          const Ctrl *ctrl) { lod::pdl_wait();
   unsigned long long nu = ctrl->n_used;
   if (nu > h.limit) nu = h.limit;
   for (long long u = gtid(); u < (long long)nu; u += gstride()) {
@@ -543,7 +545,7 @@ __global__ void k_resolve(NodeCols nd, Hash h, uint32_t *grid32, long long n_s, 
   }
 }
 
-__global__ void k_wcount(const unsigned long long *__restrict__ wmask, long long n, uint32_t *__restrict__ wcount) {
+__global__ void k_wcount(const unsigned long long *__restrict__ wmask, long long n, uint32_t *__restrict__ wcount) { lod::pdl_wait();
   for (long long j = gtid(); j < n; j += gstride()) wcount[j] = (uint32_t)__popcll(wmask[j]);
 }
 
@@ -551,7 +553,7 @@ __global__ void k_wcount(const unsigned long long *__restrict__ wmask, long long
 // path order = ascending level, _kernels.py:100-151): entry b = wbase[j] + k.
 __global__ void k_emit(long long n, unsigned long long *__restrict__ wmask, const uint32_t *__restrict__ wbase,
                        const unsigned long long *__restrict__ wins, int D, PointSrc src,
-                       int32_t *__restrict__ bnode, uint32_t *__restrict__ bcell, uint32_t *__restrict__ brgba) {
+                       int32_t *__restrict__ bnode, uint32_t *__restrict__ bcell, uint32_t *__restrict__ brgba) { lod::pdl_wait();
   for (long long j = gtid(); j < n; j += gstride()) {
     unsigned long long m = wmask[j];
     if (!m) continue;
@@ -576,7 +578,7 @@ __global__ void k_emit(long long n, unsigned long long *__restrict__ wmask, cons
 // item counts), in ascending id.  Leaves and inner nodes are disjoint, so the
 // stable sort by node id lays every node's new samples out contiguously, in
 // reference slot order, starting at the exclusive prefix of the counts.
-__global__ void k_seg_pairs(const uint32_t *__restrict__ nodecnt, long long num_nodes, U64x2 *__restrict__ pairs) {
+__global__ void k_seg_pairs(const uint32_t *__restrict__ nodecnt, long long num_nodes, U64x2 *__restrict__ pairs) { lod::pdl_wait();
   for (long long i = gtid(); i < num_nodes; i += gstride()) {
     const uint32_t c = nodecnt[i];
     pairs[i] = u64x2(c ? 1ull : 0ull, (unsigned long long)c);
@@ -589,13 +591,19 @@ __device__ __forceinline__ long long ceil_div(long long a, long long b) { return
 // dense id, segment start and chunk need = ceil((count+pending)/C) -
 // chunk_count -- in ascending node id (chunk ids are not observable; the
 // acquisition count and the arena growth are the reference's).
-__global__ void k_seg_list(NodeCols nd, Geo geo, const uint32_t *__restrict__ nodecnt, long long num_nodes,
+__global__ void k_seg_list(NodeCols nd, Geo geo, uint32_t *__restrict__ nodecnt, long long num_nodes,
                            const U64x2 *__restrict__ pairs_ex, int32_t *__restrict__ seg_node,
                            long long *__restrict__ seg_start, int32_t *__restrict__ dense, U64x2 *__restrict__ plan,
-                           Ctrl *ctrl) {
+                           Ctrl *ctrl, uint32_t *__restrict__ ghist) { lod::pdl_wait();
+  const long long K = (long long)ctrl->seg_tot.a;
+  // this kernel is the last reader of the node counts and digit totals: leave
+  // them zeroed for the next cycle; zero the plan tail the scan reads past K
+  for (long long i = gtid(); i < kMaxPassesHist; i += gstride()) ghist[i] = 0;
+  for (long long i = K + gtid(); i <= num_nodes; i += gstride()) plan[i] = u64x2(0, 0);
   for (long long i = gtid(); i < num_nodes; i += gstride()) {
     const long long len = nodecnt[i];
     if (!len) continue;
+    nodecnt[i] = 0;
     const long long d = (long long)pairs_ex[i].a;
     seg_node[d] = (int32_t)i;
     seg_start[d] = (long long)pairs_ex[i].b;
@@ -614,7 +622,7 @@ __global__ void k_seg_list(NodeCols nd, Geo geo, const uint32_t *__restrict__ no
 
 // ChunkPool.acquire in bulk (store.py:110-123): acquisitions pop the LIFO free
 // stack first, then cut fresh C*16-byte payloads from the arena (16-aligned).
-__global__ void k_alloc_begin(Ctrl *ctrl, Geo geo, unsigned long long arena_cap) {
+__global__ void k_alloc_begin(Ctrl *ctrl, Geo geo, unsigned long long arena_cap) { lod::pdl_wait();
   const long long M = (long long)ctrl->acq_tot.a;
   const long long F = ctrl->free_count;
   const long long A = ctrl->allocated_total;
@@ -643,7 +651,7 @@ __device__ __forceinline__ int acq_cid(const PoolCols &pool, const Ctrl *ctrl, l
 // node's write list.
 __global__ void k_alloc_nodes(NodeCols nd, PoolCols pool, Geo geo, const int32_t *__restrict__ seg_node,
                               const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
-                              const U64x2 *__restrict__ plan_ex, int32_t *__restrict__ wl, const Ctrl *ctrl) {
+                              const U64x2 *__restrict__ plan_ex, int32_t *__restrict__ wl, const Ctrl *ctrl) { lod::pdl_wait();
   if (ctrl->error) return;
   const long long K = (long long)ctrl->n_keys;
   for (long long d = gtid(); d < K; d += gstride()) {
@@ -673,7 +681,7 @@ __global__ void k_alloc_nodes(NodeCols nd, PoolCols pool, Geo geo, const int32_t
 // position and final occupancy, write-list slot.
 __global__ void k_alloc_chunks(NodeCols nd, PoolCols pool, Geo geo, const int32_t *__restrict__ seg_node,
                                const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
-                               const U64x2 *__restrict__ plan_ex, int32_t *__restrict__ wl, const Ctrl *ctrl) {
+                               const U64x2 *__restrict__ plan_ex, int32_t *__restrict__ wl, const Ctrl *ctrl) { lod::pdl_wait();
   if (ctrl->error) return;
   const long long M = (long long)ctrl->acq_tot.a;
   const long long K = (long long)ctrl->n_keys;
@@ -715,7 +723,7 @@ __global__ void k_store(NodeCols nd, PoolCols pool, Geo geo, uint8_t *__restrict
                         const int32_t *__restrict__ dense, const long long *__restrict__ seg_start,
                         const U64x2 *__restrict__ plan, const U64x2 *__restrict__ plan_ex,
                         const int32_t *__restrict__ wl, long long n_items, long long n_all, PointSrc src,
-                        const uint32_t *__restrict__ bcell, const uint32_t *__restrict__ brgba, const Ctrl *ctrl) {
+                        const uint32_t *__restrict__ bcell, const uint32_t *__restrict__ brgba, const Ctrl *ctrl) { lod::pdl_wait();
   if (ctrl->error) return;
   for (long long p = gtid(); p < n_items; p += gstride()) {
     const int n = (int)skeys[p];
@@ -748,7 +756,7 @@ __global__ void k_store(NodeCols nd, PoolCols pool, Geo geo, uint8_t *__restrict
 
 // clear_marks (_kernels.py:280-287) + count advance: pending drains into count.
 __global__ void k_epilogue(NodeCols nd, const int32_t *__restrict__ seg_node, const long long *__restrict__ seg_start,
-                           const Ctrl *ctrl) {
+                           const Ctrl *ctrl) { lod::pdl_wait();
   if (ctrl->error) return;
   const long long K = (long long)ctrl->n_keys;
   for (long long d = gtid(); d < K; d += gstride()) {
@@ -760,7 +768,7 @@ __global__ void k_epilogue(NodeCols nd, const int32_t *__restrict__ seg_node, co
 }
 
 // Safety net after a fatal error: pending/final of every node back to zero.
-__global__ void k_clear_marks_all(NodeCols nd, int32_t *srank, long long n) {
+__global__ void k_clear_marks_all(NodeCols nd, int32_t *srank, long long n) { lod::pdl_wait();
   for (long long i = gtid(); i < n; i += gstride()) {
     nd.pending[i] = 0;
     nd.final_[i] = 0;

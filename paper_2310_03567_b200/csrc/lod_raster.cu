@@ -56,7 +56,7 @@ __device__ __forceinline__ void splat(const Cam &cam, long long w, long long h, 
 }
 
 __global__ void k_raster_points(const float *__restrict__ xyz, const uint32_t *__restrict__ rgba, long long n,
-                                Cam cam, unsigned long long *fb, long long w, long long h) {
+                                Cam cam, unsigned long long *fb, long long w, long long h) { lod::pdl_wait();
   for (long long i = gtid(); i < n; i += gstride())
     splat(cam, w, h, (double)__ldg(xyz + 3 * i), (double)__ldg(xyz + 3 * i + 1), (double)__ldg(xyz + 3 * i + 2),
           __ldg(rgba + i), fb);
@@ -66,7 +66,7 @@ __global__ void k_raster_points(const float *__restrict__ xyz, const uint32_t *_
 // list (samples_drawn counts every listed occurrence, _kernels.py:307-317).
 __global__ void k_raster_chunks(PoolCols pool, const uint8_t *__restrict__ arena, long long nchunks,
                                 const uint32_t *__restrict__ visflag, Cam cam, unsigned long long *fb,
-                                long long w, long long h, unsigned long long *samples) {
+                                long long w, long long h, unsigned long long *samples) { lod::pdl_wait();
   const long long warp = gtid() >> 5, nwarps = gstride() >> 5;
   const int lane = threadIdx.x & 31;
   unsigned long long drawn = 0;
@@ -86,14 +86,14 @@ __global__ void k_raster_chunks(PoolCols pool, const uint8_t *__restrict__ arena
   if (lane == 0 && drawn) atomicAdd(samples, drawn);
 }
 
-__global__ void k_set_vis(const int32_t *__restrict__ vis, long long n, uint32_t *visflag, int add) {
+__global__ void k_set_vis(const int32_t *__restrict__ vis, long long n, uint32_t *visflag, int add) { lod::pdl_wait();
   for (long long i = gtid(); i < n; i += gstride()) {
     if (add) atomicAdd(visflag + vis[i], 1u);
     else visflag[vis[i]] = 0;
   }
 }
 
-__global__ void k_fill_u64(unsigned long long *p, long long n, unsigned long long v) {
+__global__ void k_fill_u64(unsigned long long *p, long long n, unsigned long long v) { lod::pdl_wait();
   for (long long i = gtid(); i < n; i += gstride()) p[i] = v;
 }
 
@@ -155,10 +155,10 @@ int lod_rasterize(LodTree *t, const int32_t *vis, int64_t nvis, const double *ca
   uint32_t *vf = lod_tree_visflag(t);
   const long long nchunks = lod_tree_allocated(t);
   if (nvis) {
-    k_set_vis<<<grid_for(nvis), 256, 0, st>>>(dvis, nvis, vf, 1); ++lod::g_launches;
-    k_raster_chunks<<<grid_for(nchunks * 32), 256, 0, st>>>(lod_tree_pool(t), lod_tree_arena(t), nchunks, vf, c,
-                                                             dfb, width, height, cnt); ++lod::g_launches;
-    k_set_vis<<<grid_for(nvis), 256, 0, st>>>(dvis, nvis, vf, 0); ++lod::g_launches;
+    lod::launch(k_set_vis, grid_for(nvis), 256, 0, st, dvis, nvis, vf, 1);
+    lod::launch(k_raster_chunks, grid_for(nchunks * 32), 256, 0, st, lod_tree_pool(t), lod_tree_arena(t), nchunks, vf, c,
+                                                             dfb, width, height, cnt);
+    lod::launch(k_set_vis, grid_for(nvis), 256, 0, st, dvis, nvis, vf, 0);
   }
   unsigned long long drawn = 0;
   CK(cudaMemcpyAsync(&drawn, cnt, 8, cudaMemcpyDeviceToHost, st));
@@ -211,7 +211,7 @@ int lod_raster_points(int32_t device, const float *xyz, const uint32_t *rgba, in
     dfb = s.fb;
     CK(cudaMemcpyAsync(dfb, fb, npx * 8, cudaMemcpyHostToDevice, s.st));
   }
-  if (n > 0) k_raster_points<<<grid_for(n), 256, 0, s.st>>>(dx, dc, n, c, dfb, width, height); ++lod::g_launches;
+  if (n > 0) lod::launch(k_raster_points, grid_for(n), 256, 0, s.st, dx, dc, n, c, dfb, width, height);
   if (!(flags & LOD_FLAG_DEVICE_FB)) CK(cudaMemcpyAsync(fb, dfb, npx * 8, cudaMemcpyDeviceToHost, s.st));
   CK(cudaStreamSynchronize(s.st));
   return LOD_OK;
@@ -244,7 +244,7 @@ int lod_host_alloc(uint64_t bytes, void **ptr) {
 int lod_host_free(void *ptr) { return cuda_rc(cudaFreeHost(ptr)); }
 int lod_fb_fill(int32_t device, uint64_t *fb_dev, int64_t n, uint64_t value) {
   cudaSetDevice(device);
-  k_fill_u64<<<grid_for(n), 256>>>(reinterpret_cast<unsigned long long *>(fb_dev), n, value); ++lod::g_launches;
+  lod::launch(k_fill_u64, grid_for(n), 256, 0, 0, reinterpret_cast<unsigned long long *>(fb_dev), n, value);
   return cuda_rc(cudaDeviceSynchronize());
 }
 int lod_l2_flush(int32_t device) {

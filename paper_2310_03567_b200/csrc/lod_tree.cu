@@ -86,7 +86,7 @@ inline unsigned long long next_pow2(unsigned long long v) {
 
 }  // namespace
 
-__global__ void k_init_root(NodeCols nd, double b0, double b1, double b2) {
+__global__ void k_init_root(NodeCols nd, double b0, double b1, double b2) { lod::pdl_wait();
   nd.parent[0] = LOD_NO_NODE;
   nd.octant[0] = 0;
   nd.level[0] = 0;
@@ -105,7 +105,7 @@ __global__ void k_init_root(NodeCols nd, double b0, double b1, double b2) {
   nd.desc[0] = make_int2(-1, 0);
 }
 
-__global__ void k_cycle_begin(Ctrl *c) {
+__global__ void k_cycle_begin(Ctrl *c) { lod::pdl_wait();
   c->n_touched = 0;
   c->n_splits = 0;
   c->error = 0;
@@ -118,13 +118,13 @@ __global__ void k_cycle_begin(Ctrl *c) {
   c->acq_tot = u64x2(0, 0);
 }
 
-__global__ void k_reset_touched(Ctrl *c) { c->n_touched = 0; }
+__global__ void k_reset_touched(Ctrl *c) { lod::pdl_wait(); c->n_touched = 0; }
 
 // Walk one node's chunk list into a packed record buffer (gather_samples,
 // octree.py:298-326).  One CTA per listed node.
 __global__ void k_gather_nodes(NodeCols nd, PoolCols pool, Geo geo, const uint8_t *__restrict__ arena,
                                const int32_t *__restrict__ nodes, const long long *__restrict__ starts,
-                               const long long *__restrict__ out_off, float4 *__restrict__ out) {
+                               const long long *__restrict__ out_off, float4 *__restrict__ out) { lod::pdl_wait();
   __shared__ int s_cid, s_occ;
   __shared__ long long s_poff;
   const int nid = nodes[blockIdx.x];
@@ -316,7 +316,7 @@ static void fill_stats(LodTree *t, LodBatchStats *s) {
 // After a fatal error: drop per-cycle marks and the claim table so the
 // structure stays walkable (the reference leaves partial state, errors.py:1-5).
 static int abort_cycle(LodTree *t, int code) {
-  k_clear_marks_all<<<grid_for(t->num_nodes), 256, 0, t->st>>>(t->nd, t->srank.p, t->num_nodes); ++lod::g_launches;
+  lod::launch(k_clear_marks_all, grid_for(t->num_nodes), 256, 0, t->st, t->nd, t->srank.p, t->num_nodes);
   if (t->hslots.p) {
     cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), t->st);
     if (t->wmask.p) cudaMemsetAsync(t->wmask.p, 0, (size_t)t->wmask.cap * 8, t->st);
@@ -415,7 +415,7 @@ int lod_tree_create(const LodParams *params, LodTree **out) {
   CK(cudaMallocHost(&t->h_ctrl, sizeof(Ctrl)));
   CK(cudaMemsetAsync(t->d_ctrl, 0, sizeof(Ctrl), t->st));
   memset(t->h_ctrl, 0, sizeof(Ctrl));
-  k_init_root<<<1, 1, 0, t->st>>>(t->nd, p.bmin[0], p.bmin[1], p.bmin[2]); ++lod::g_launches;
+  lod::launch(k_init_root, 1, 1, 0, t->st, t->nd, p.bmin[0], p.bmin[1], p.bmin[2]);
   Ctrl c0{};
   c0.num_nodes = 1;
   CK(cudaMemcpyAsync(t->d_ctrl, &c0, sizeof(Ctrl), cudaMemcpyHostToDevice, t->st));
@@ -514,7 +514,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     bc = t->in_rgba.p;
   }
   CK(cudaEventRecord(t->ev[11], st));  // inputs resident
-  k_cycle_begin<<<1, 1, 0, st>>>(t->d_ctrl); ++lod::g_launches;
+  lod::launch(k_cycle_begin, 1, 1, 0, st, t->d_ctrl);
   // ---- expansion (update.py:273-296) with the voxel claims folded in
   RK(t->node_b.ensure(n, st));
   PointSrc src{nullptr, 0, bx, bc, n};
@@ -541,14 +541,12 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   for (;;) {
     ++iters;
     if (prof) cudaEventRecord(t->ev[12], st);
-    k_count<<<grid_for(n_all), 256, 0, st>>>(t->nd, t->geo, src, node_of, n_all, first, grid32, hs, t->d_ctrl);
-    ++lod::g_launches;
-    k_touched<<<grid_for(t->num_nodes - touch_from), 256, 0, st>>>(t->nd, touch_from, t->touched.p, t->d_ctrl);
-    ++lod::g_launches;
+    lod::launch(k_count, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, node_of, n_all, first, grid32, hs, t->d_ctrl);
+    lod::launch(k_touched, grid_for(t->num_nodes - touch_from), 256, 0, st, t->nd, touch_from, t->touched.p, t->d_ctrl);
     if (prof) cudaEventRecord(t->ev[13], st);
-    k_decide<<<1, kDecideBlock, 0, st>>>(t->nd, t->geo, t->touched.p, t->bitmap.p, t->word_prefix.p,
+    lod::launch(k_decide, 1, kDecideBlock, 0, st, t->nd, t->geo, t->touched.p, t->bitmap.p, t->word_prefix.p,
                                          t->split_list.p, t->srank.p, t->scnt.p, t->schk.p, t->spill_off.p,
-                                         t->chunk_off.p, t->d_ctrl, spill_cap, t->arena_cap); ++lod::g_launches;
+                                         t->chunk_off.p, t->d_ctrl, spill_cap, t->arena_cap);
     RK(sync_ctrl(t));
     if (prof) {
       float x = 0.f;
@@ -566,18 +564,18 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       if (!first) return abort_cycle(t, LOD_E_ARG);  // only iteration 1 can spill (update.py:9-11)
       RK(t->spill.ensure(h.spill_total, st));
       RK(t->node_all.ensure(h.spill_total + n, st));
-      k_exec_chunks<<<grid_for(h.allocated_total * 32), 256, 0, st>>>(
+      lod::launch(k_exec_chunks, grid_for(h.allocated_total * 32), 256, 0, st, 
           t->pool, t->geo, t->arena, h.allocated_total, t->srank.p, t->spill_off.p, t->chunk_off.p, t->spill.p,
-          t->node_all.p, t->d_ctrl); ++lod::g_launches;
+          t->node_all.p, t->d_ctrl);
     }
-    k_exec_nodes<<<grid_for(8 * ns), 256, 0, st>>>(t->nd, t->geo, t->split_list.p, t->srank.p, ns,
-                                                   t->d_ctrl); ++lod::g_launches;
+    lod::launch(k_exec_nodes, grid_for(8 * ns), 256, 0, st, t->nd, t->geo, t->split_list.p, t->srank.p, ns,
+                                                   t->d_ctrl);
     touch_from = h.plan_num_nodes0;
     t->num_nodes = h.num_nodes;
     if (first) {
       n_s = h.spill_total;
       if (n_s > 0) {
-        k_shift_nodes<<<grid_for(n), 256, 0, st>>>(t->node_b.p, t->node_all.p + n_s, n); ++lod::g_launches;
+        lod::launch(k_shift_nodes, grid_for(n), 256, 0, st, t->node_b.p, t->node_all.p + n_s, n);
         node_of = t->node_all.p;
         src.spill = t->spill.p;
         src.ns = n_s;
@@ -593,8 +591,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       CK(cudaMemsetAsync(t->hslots2.p, 0xFF, (size_t)t->hslots2.cap * sizeof(HSlot), st));
       RK(t->hused.ensure((long long)H, st, (long long)h.n_used));
       Hash nh{t->hslots2.p, H - 1, t->hused.p, H};
-      k_rehash<<<grid_for(std::max<long long>((long long)h.n_used, 1)), 256, 0, st>>>(t->hslots.p, nh, t->d_ctrl);
-      ++lod::g_launches;
+      lod::launch(k_rehash, grid_for(std::max<long long>((long long)h.n_used, 1)), 256, 0, st, t->hslots.p, nh, t->d_ctrl);
       // the old table goes back to empty for later cycles
       CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
       std::swap(t->hslots, t->hslots2);
@@ -634,7 +631,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     hs = Hash{t->hslots.p, t->hcap - 1, t->hused.p, (unsigned long long)bound + 1};
     CK(cudaMemsetAsync(&t->d_ctrl->n_used, 0, 8, st));
     CK(cudaMemsetAsync(&t->d_ctrl->hash_overflow, 0, 4, st));
-    k_claim<<<grid_for(n_all), 256, 0, st>>>(t->nd, t->geo, src, grid32, n_all, hs, t->d_ctrl); ++lod::g_launches;
+    lod::launch(k_claim, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, grid32, n_all, hs, t->d_ctrl);
     RK(sync_ctrl(t));
     h1 = *t->h_ctrl;
   }
@@ -643,18 +640,17 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   const long long n_v = (long long)h1.n_used;
   t->prev_used = n_v;
   if (n_v > 0) {
-    k_resolve<<<grid_for(n_v), 256, 0, st>>>(t->nd, hs, grid32, n_s, D, t->wins.p, t->wmask.p, t->d_ctrl);
-    ++lod::g_launches;
+    lod::launch(k_resolve, grid_for(n_v), 256, 0, st, t->nd, hs, grid32, n_s, D, t->wins.p, t->wmask.p, t->d_ctrl);
   }
   mark(1);
   RK(t->bnode.ensure(std::max<long long>(n_v, 1), st));
   RK(t->bcell.ensure(std::max<long long>(n_v, 1), st));
   RK(t->brgba.ensure(std::max<long long>(n_v, 1), st));
   if (n_v > 0) {
-    k_wcount<<<grid_for(n_all), 256, 0, st>>>(t->wmask.p, n_all, t->wcount.p); ++lod::g_launches;
+    lod::launch(k_wcount, grid_for(n_all), 256, 0, st, t->wmask.p, n_all, t->wcount.p);
     exclusive_scan<uint32_t>(t->wcount.p, t->wbase.p, n_all, &t->d_ctrl->n_v, t->scan_u32.p, st);
-    k_emit<<<grid_for(n_all), 256, 0, st>>>(n_all, t->wmask.p, t->wbase.p, t->wins.p, D, src, t->bnode.p,
-                                           t->bcell.p, t->brgba.p); ++lod::g_launches;
+    lod::launch(k_emit, grid_for(n_all), 256, 0, st, n_all, t->wmask.p, t->wbase.p, t->wins.p, D, src, t->bnode.p,
+                                           t->bcell.p, t->brgba.p);
   }
   mark(2);
   // ---- sort: every new sample by node id, stable (slot order)
@@ -664,23 +660,27 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   RK(t->keys_b.ensure(n_items, st));
   RK(t->vals_a.ensure(n_items, st));
   RK(t->vals_b.ensure(n_items, st));
-  RK(t->hist.ensure(std::max<long long>(radix_lb_elems(n_items), kMaxPasses * kRadixDigits), st));
-  RK(t->ghist.ensure(kMaxPasses * kRadixDigits, st));
-  RK(t->nodecnt.ensure(num_nodes, st));
-  CK(cudaMemsetAsync(t->ghist.p, 0, kMaxPasses * kRadixDigits * 4, st));
-  CK(cudaMemsetAsync(t->nodecnt.p, 0, (size_t)num_nodes * 4, st));
-  k_radix_prep<<<std::min<unsigned>(grid_for(n_items), 148), kRadixBlock, 0, st>>>(node_of, n_all, t->bnode.p, n_v, num_nodes, t->keys.p,
-                                                          t->nodecnt.p);
-  ++lod::g_launches;
-  k_radix_ghist<<<std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st>>>(t->nodecnt.p, num_nodes, passes,
-                                                                             t->ghist.p);
-  ++lod::g_launches;
+  RK(t->hist.ensure(2 * radix_lb_elems(n_items), st));
+  {
+    long long oldg = t->ghist.cap, oldn = t->nodecnt.cap;
+    RK(t->ghist.ensure(kMaxPasses * kRadixDigits, st));
+    RK(t->nodecnt.ensure(num_nodes, st, oldn));
+    // zero once when (re)allocated; afterwards k_seg_list leaves them zeroed
+    if (t->ghist.cap > oldg) CK(cudaMemsetAsync(t->ghist.p, 0, (size_t)t->ghist.cap * 4, st));
+    if (t->nodecnt.cap > oldn) CK(cudaMemsetAsync(t->nodecnt.p + oldn, 0, (size_t)(t->nodecnt.cap - oldn) * 4, st));
+  }
+  const long long lbw = radix_lb_elems(n_items);
+  lod::launch(k_radix_prep, std::min<unsigned>(grid_for(n_items), 148), kRadixBlock, 0, st, node_of, n_all, t->bnode.p,
+              n_v, num_nodes, t->keys.p, t->nodecnt.p, t->hist.p, lbw);
+  lod::launch(k_radix_ghist, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p, num_nodes, passes,
+              t->ghist.p);
   RadixScratch rs;
   rs.keys_b = t->keys_b.p;
   rs.vals_a = t->vals_a.p;
   rs.vals_b = t->vals_b.p;
   rs.ghist = t->ghist.p;
-  rs.lb = t->hist.p;
+  rs.lb[0] = t->hist.p;
+  rs.lb[1] = t->hist.p + lbw;
   uint32_t *skeys = nullptr, *svals = nullptr;
   stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals);
   mark(3);
@@ -695,26 +695,24 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   const long long acq_bound = n_items / C + Kb + 1;
   RK(t->wl.ensure(acq_bound + Kb + 1, st));
   RK(ensure_chunks(t, h1.allocated_total + acq_bound + 1, h1.allocated_total));
-  k_seg_pairs<<<grid_for(num_nodes), 256, 0, st>>>(t->nodecnt.p, num_nodes, t->plan_ex.p); ++lod::g_launches;
+  lod::launch(k_seg_pairs, grid_for(num_nodes), 256, 0, st, t->nodecnt.p, num_nodes, t->plan_ex.p);
   exclusive_scan<U64x2>(t->plan_ex.p, t->plan_ex.p, num_nodes, &t->d_ctrl->seg_tot, t->scan_u64x2.p, st);
-  CK(cudaMemsetAsync(t->plan.p, 0, (size_t)Kb * sizeof(U64x2), st));
-  k_seg_list<<<grid_for(num_nodes), 256, 0, st>>>(t->nd, t->geo, t->nodecnt.p, num_nodes, t->plan_ex.p,
-                                                  t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->d_ctrl);
-  ++lod::g_launches;
+  lod::launch(k_seg_list, grid_for(num_nodes), 256, 0, st, t->nd, t->geo, t->nodecnt.p, num_nodes, t->plan_ex.p,
+                                                  t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->d_ctrl, t->ghist.p);
   exclusive_scan<U64x2>(t->plan.p, t->plan_ex.p, Kb, &t->d_ctrl->acq_tot, t->scan_u64x2.p, st);
-  k_alloc_begin<<<1, 1, 0, st>>>(t->d_ctrl, t->geo, t->arena_cap); ++lod::g_launches;
-  k_alloc_nodes<<<grid_for(Kb), 256, 0, st>>>(t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p, t->plan.p,
-                                              t->plan_ex.p, t->wl.p, t->d_ctrl); ++lod::g_launches;
-  k_alloc_chunks<<<grid_for(acq_bound), 256, 0, st>>>(t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p,
-                                                      t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl); ++lod::g_launches;
+  lod::launch(k_alloc_begin, 1, 1, 0, st, t->d_ctrl, t->geo, t->arena_cap);
+  lod::launch(k_alloc_nodes, grid_for(Kb), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p, t->plan.p,
+                                              t->plan_ex.p, t->wl.p, t->d_ctrl);
+  lod::launch(k_alloc_chunks, grid_for(acq_bound), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p,
+                                                      t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl);
   mark(4);
   // ---- store (update.py:357-373)
-  k_store<<<grid_for(n_items), 256, 0, st>>>(t->nd, t->pool, t->geo, t->arena, skeys, svals, t->dense.p,
+  lod::launch(k_store, grid_for(n_items), 256, 0, st, t->nd, t->pool, t->geo, t->arena, skeys, svals, t->dense.p,
                                              t->seg_start.p, t->plan.p, t->plan_ex.p, t->wl.p, n_items, n_all,
-                                             src, t->bcell.p, t->brgba.p, t->d_ctrl); ++lod::g_launches;
+                                             src, t->bcell.p, t->brgba.p, t->d_ctrl);
   mark(5);
   // ---- cleanup (update.py:375-380)
-  k_epilogue<<<grid_for(Kb), 256, 0, st>>>(t->nd, t->seg_node.p, t->seg_start.p, t->d_ctrl); ++lod::g_launches;
+  lod::launch(k_epilogue, grid_for(Kb), 256, 0, st, t->nd, t->seg_node.p, t->seg_start.p, t->d_ctrl);
   mark(6);
   CK(cudaEventRecord(t->ev[10], st));
   RK(sync_ctrl(t));
@@ -809,8 +807,8 @@ static int gather_impl(LodTree *t, const std::vector<int32_t> &nodes, const std:
   CK(cudaMemcpyAsync(t->goff.p, offs.data(), m * 8, cudaMemcpyHostToDevice, st));
   for (long long b = 0; b < m; b += 65535) {
     long long cnt = std::min<long long>(65535, m - b);
-    k_gather_nodes<<<(unsigned)cnt, 256, 0, st>>>(t->nd, t->pool, t->geo, t->arena, t->gnodes.p + b,
-                                                  t->gstart.p + b, t->goff.p + b, t->gbuf.p); ++lod::g_launches;
+    lod::launch(k_gather_nodes, (unsigned)cnt, 256, 0, st, t->nd, t->pool, t->geo, t->arena, t->gnodes.p + b,
+                                                  t->gstart.p + b, t->goff.p + b, t->gbuf.p);
   }
   CK(cudaMemcpyAsync(host_out, t->gbuf.p, total * 16, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));

@@ -39,8 +39,10 @@ constexpr uint32_t kLbAgg = 1u << 30, kLbPre = 2u << 30, kLbMask = (1u << 30) - 
 // node's new samples this cycle; hot leaves are aggregated per warp first).
 __global__ void __launch_bounds__(kRadixBlock)
     k_radix_prep(const int32_t *__restrict__ node_all, long long n_all, const int32_t *__restrict__ bnode,
-                 long long n_v, long long num_nodes, uint32_t *__restrict__ keys, uint32_t *__restrict__ nodecnt) {
+                 long long n_v, long long num_nodes, uint32_t *__restrict__ keys, uint32_t *__restrict__ nodecnt,
+                 uint32_t *__restrict__ lb0, long long lb_words) { lod::pdl_wait();
   __shared__ uint32_t nc[kNodeHistSmem];
+  for (long long i = gtid(); i < lb_words; i += gstride()) lb0[i] = 0;  // look-back words of pass 0
   const bool smem_nodes = num_nodes <= kNodeHistSmem;
   if (smem_nodes)
     for (long long i = threadIdx.x; i < num_nodes; i += kRadixBlock) nc[i] = 0;
@@ -70,7 +72,7 @@ __global__ void __launch_bounds__(kRadixBlock)
 
 // Digit totals of every pass from the per-node counts (keys are node ids).
 __global__ void k_radix_ghist(const uint32_t *__restrict__ nodecnt, long long num_nodes, int passes,
-                              uint32_t *__restrict__ ghist) {
+                              uint32_t *__restrict__ ghist) { lod::pdl_wait();
   __shared__ uint32_t h[kMaxPasses * kRadixDigits];
   for (int i = threadIdx.x; i < kMaxPasses * kRadixDigits; i += blockDim.x) h[i] = 0;
   __syncthreads();
@@ -89,7 +91,12 @@ __global__ void k_radix_ghist(const uint32_t *__restrict__ nodecnt, long long nu
 __global__ void __launch_bounds__(kRadixBlock, 4)
     k_onesweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in, long long n, int shift,
                const uint32_t *__restrict__ ghist_pass, uint32_t *lb, long long ntiles,
-               uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out) {
+               uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint32_t *lb_next) { lod::pdl_wait();
+  // zero the next pass's look-back words (one per thread, + the ticket)
+  if (lb_next) {
+    lb_next[(long long)blockIdx.x * kRadixDigits + threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) lb_next[ntiles * kRadixDigits] = 0;
+  }
   __shared__ uint32_t wh[kRadixWarps][kRadixDigits];  // per-warp digit counts -> warp offsets
   __shared__ uint32_t dstart[kRadixDigits];           // tile-local digit start
   __shared__ uint32_t gbase[kRadixDigits];            // global position of the tile's digit run
@@ -188,8 +195,8 @@ __global__ void __launch_bounds__(kRadixBlock, 4)
 
 struct RadixScratch {
   uint32_t *keys_b = nullptr, *vals_a = nullptr, *vals_b = nullptr;
-  uint32_t *ghist = nullptr;  // kMaxPasses * 256
-  uint32_t *lb = nullptr;     // ntiles * 256 + 1 per pass (reused)
+  uint32_t *ghist = nullptr;         // kMaxPasses * 256
+  uint32_t *lb[2] = {nullptr, nullptr};  // ntiles * 256 + 1 each, alternating per pass
 };
 
 inline long long radix_tiles(long long n) { return (n + kRadixTile - 1) / kRadixTile; }
@@ -213,10 +220,10 @@ inline void stable_multisplit(uint32_t *keys, long long n, int passes, RadixScra
   uint32_t *vout = s.vals_a;
   for (int p = 0; p < passes; ++p) {
     if (n > 0) {
-      cudaMemsetAsync(s.lb, 0, (size_t)(ntiles * kRadixDigits + 1) * 4, st);
-      k_onesweep<<<(unsigned)ntiles, kRadixBlock, 0, st>>>(kin, vin, n, p * kRadixBits, s.ghist + p * kRadixDigits,
-                                                           s.lb, ntiles, kout, vout);
-      ++lod::g_launches;
+      // look-back buffer p&1 was zeroed by k_radix_prep (p = 0) or by pass p-1
+      lod::launch(k_onesweep, (unsigned)ntiles, kRadixBlock, 0, st, kin, vin, n, p * kRadixBits,
+                  s.ghist + p * kRadixDigits, s.lb[p & 1], ntiles, kout, vout,
+                  p + 1 < passes ? s.lb[(p + 1) & 1] : (uint32_t *)nullptr);
     }
     uint32_t *kt = kin;
     kin = kout;

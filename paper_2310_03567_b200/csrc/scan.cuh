@@ -78,7 +78,7 @@ constexpr long long kScanTile = (long long)kScanBlock * kScanItems;
 // Per-tile reduction.
 template <typename T>
 __global__ void __launch_bounds__(kScanBlock) k_scan_reduce(const T *__restrict__ in, long long n,
-                                                            T *__restrict__ partial) {
+                                                            T *__restrict__ partial) { lod::pdl_wait();
   __shared__ T sh[kScanBlock / 32 + 1];
   long long base = (long long)blockIdx.x * kScanTile + (long long)threadIdx.x * kScanItems;
   T acc = T();
@@ -95,7 +95,7 @@ template <typename T>
 __global__ void __launch_bounds__(kScanBlock) k_scan_tiles(const T *__restrict__ in, long long n,
                                                            T *__restrict__ out,
                                                            const T *__restrict__ tile_off,
-                                                           T *__restrict__ total_out) {
+                                                           T *__restrict__ total_out) { lod::pdl_wait();
   __shared__ T sh[kScanBlock / 32 + 1];
   long long base = (long long)blockIdx.x * kScanTile + (long long)threadIdx.x * kScanItems;
   T v[kScanItems];
@@ -139,15 +139,15 @@ void exclusive_scan(const T *in, T *out, long long n, T *total_out, T *scratch, 
     return;
   }
   if (n <= kScanTile) {
-    k_scan_tiles<T><<<1, kScanBlock, 0, st>>>(in, n, out, nullptr, total_out); ++lod::g_launches;
+    lod::launch(k_scan_tiles<T>, 1, kScanBlock, 0, st, in, n, out, nullptr, total_out);
     return;
   }
   long long tiles = (n + kScanTile - 1) / kScanTile;
   T *partial = scratch;
   T *partial_scan = scratch + tiles;
-  k_scan_reduce<T><<<(unsigned)tiles, kScanBlock, 0, st>>>(in, n, partial); ++lod::g_launches;
+  lod::launch(k_scan_reduce<T>, (unsigned)tiles, kScanBlock, 0, st, in, n, partial);
   exclusive_scan<T>(partial, partial_scan, tiles, nullptr, scratch + 2 * tiles, st);
-  k_scan_tiles<T><<<(unsigned)tiles, kScanBlock, 0, st>>>(in, n, out, partial_scan, total_out); ++lod::g_launches;
+  lod::launch(k_scan_tiles<T>, (unsigned)tiles, kScanBlock, 0, st, in, n, out, partial_scan, total_out);
 }
 
 }  // namespace lod

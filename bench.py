@@ -140,29 +140,97 @@ def new_tree(device: int, arena_bytes: int):
     return tree, state
 
 
+def run_multi(args, rank, world, local_rank):
+    """N > 1: every step is a global batch of N x 1M points arriving striped
+    (1M per rank); points are routed to the owners of their octant prefixes
+    with one NCCL all-to-all and inserted into the owner's tree
+    (paper_2310_03567_b200/multigpu.py).  Warm-up batches run the single-tree
+    protocol on rank 0 until the top is inner, then rank 0's tree is
+    broadcast.  Weak scaling: per-GPU input is fixed at 1M points per step."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2310_03567_b200 import multigpu, partition
+
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    kind = CONFIGS[args.config][0]
+    sample = [gen_stripe(kind, s, 0) for s in range(2)]
+    plan = partition.plan_owners(sample, world)  # deterministic: same on every rank
+    tree, state = new_tree(local_rank, int(args.arena_gib * (1 << 30)))
+    ins = multigpu.PartitionedInserter(tree, state, plan, rank, world)
+    step = 0
+    while step < args.warmup or not ins.partitioned:
+        x, c = gen_stripe(kind, step, rank)
+        ins.insert(torch.from_numpy(x).cuda(), torch.from_numpy(c.view(np.int32)).cuda())
+        step += 1
+    stripes = [gen_stripe(kind, step + k, rank) for k in range(args.steps)]
+    dev_b = [(torch.from_numpy(x).cuda(), torch.from_numpy(c.view(np.int32)).cuda()) for x, c in stripes]
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    with ClockSampler(local_rank) as clocks:
+        e0.record()
+        for x, c in dev_b:
+            ins.insert(x, c)
+            launches += int(state._bstats.launches)
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    v = torch.tensor([ms, float(sum(len(c) for _, c in stripes))], device="cuda", dtype=torch.float64)
+    allv = [torch.zeros_like(v) for _ in range(world)]
+    dist.all_gather(allv, v)
+    t_max = max(float(a[0]) for a in allv)
+    pts = sum(float(a[1]) for a in allv)
+    line = None
+    if rank == 0:
+        value = pts / (t_max * 1e-3) / 1e6
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "Mpts/s", "n_gpus": world, "steps": args.steps,
+            "warmup": step, "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic",
+            "config": {"workload": CONFIGS[args.config][1] + f"; global batch {world} x 1M striped over ranks",
+                       "batch_points": BATCH * world, "tree": PARAMS,
+                       "parallelism": f"octant-prefix partition depth {plan.depth} x{world}, NCCL all-to-all routing",
+                       "imbalance_max_over_mean": round(partition.imbalance(plan), 3),
+                       "l2": "inputs larger than L2: distinct 16 MB stripes per step"},
+            "e2e": None, "gpu_launches": launches, "clocks": clocks.summary(),
+        }
+    dist.destroy_process_group()
+    return line
+
+
+def gen_stripe(kind: str, step: int, rank: int):
+    """Rank `rank`'s 1M-point stripe of global batch `step` (seeded per stripe)."""
+    from paper_2310_03567_b200 import synth
+
+    seed = 1000 + step * 64 + rank
+    if kind == "mesh":
+        return synth.gen_mesh(BATCH, seed, synth.mesh_scene())
+    return synth.GENERATORS[kind](BATCH, seed)
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
-    from paper_2310_03567_b200 import insert_batch, partition
+    from paper_2310_03567_b200 import insert_batch
 
+    if world > 1:
+        return run_multi(args, rank, world, local_rank)
     torch.cuda.set_device(local_rank)
     dev = local_rank
     dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     kind = CONFIGS[args.config][0]
     total = args.warmup + args.steps
     batches = gen_batches(kind, total)
     if args.presort:  # experiment only: z-ordered input batches (changes the workload)
         batches = [morton_sorted(x, c) for x, c in batches]
-    if world > 1:
-        # octant-prefix partition of every batch; this rank keeps its subtrees' points
-        plan = partition.plan_owners(batches[: max(1, args.warmup)], world)
-        batches = [partition.take(plan, x, c, rank) for x, c in batches]
     n_points = [len(c) for _, c in batches]
-    arena_bytes = int(args.arena_gib * (1 << 30)) // max(world, 1) if world > 1 else int(args.arena_gib * (1 << 30))
+    arena_bytes = int(args.arena_gib * (1 << 30))
     # device-resident inputs (value) and pinned host inputs (e2e)
     dev_b = [(torch.from_numpy(x).cuda(), torch.from_numpy(c.view(np.int32)).cuda()) for x, c in batches]
     pin_b = []

@@ -132,6 +132,15 @@ int lod_dump_records(LodTree *tree, int64_t num_nodes, int64_t *offsets, void *r
 /* Raw arena bytes [off, off+size) (Octree.grid, octree.py:275-279). */
 int lod_read_arena(LodTree *tree, uint64_t off, uint64_t size, void *dst);
 
+/* Whole-tree state as one contiguous DEVICE byte buffer (node table, chunk
+ * pool, free stack, used arena bytes, counters), for replicating a tree to
+ * other ranks (e.g. an NCCL broadcast before octant-prefix partitioning).
+ * lod_tree_pack_size -> bytes; lod_tree_pack writes them to `dev_buf`;
+ * lod_tree_unpack replaces `tree`'s state (same params, arena large enough). */
+int lod_tree_pack_size(LodTree *tree, uint64_t *bytes);
+int lod_tree_pack(LodTree *tree, void *dev_buf, uint64_t bytes);
+int lod_tree_unpack(LodTree *tree, const void *dev_buf, uint64_t bytes);
+
 /* _kernels.rasterize_nodes via render.rasterize (_kernels.py:290-339,
  * render.py:213-225): splat every sample of the listed nodes into the packed
  * u64 framebuffer (float32 depth bits << 32 | rgba, atomicMin).  cam is the

@@ -113,6 +113,9 @@ SIGNATURES = {
     "lod_host_free": (ctypes.c_int, [_P]),
     "lod_fb_fill": (ctypes.c_int, [ctypes.c_int32, _P, _I64, ctypes.c_uint64]),
     "lod_l2_flush": (ctypes.c_int, [ctypes.c_int32]),
+    "lod_tree_pack_size": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
+    "lod_tree_pack": (ctypes.c_int, [_P, _P, ctypes.c_uint64]),
+    "lod_tree_unpack": (ctypes.c_int, [_P, _P, ctypes.c_uint64]),
 }
 
 _lib = None

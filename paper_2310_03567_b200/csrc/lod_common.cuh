@@ -74,6 +74,14 @@ __device__ __forceinline__ unsigned long long warp_agg_add_u64(unsigned long lon
   return base;
 }
 
+// Read-only load that is not allocated in L1: for random single-use words
+// (occupancy grids) that would otherwise evict the L1-resident node table.
+__device__ __forceinline__ uint32_t ld_nol1(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
 // Grid-stride helpers.
 __device__ __forceinline__ long long gtid() {
   return (long long)blockIdx.x * blockDim.x + threadIdx.x;

@@ -224,7 +224,10 @@ __global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl
 // point from the root; later iterations re-descend only points whose cached
 // node became inner, starting at that node (its stored bmin equals the
 // accumulated descent bounds byte for byte, _kernels.py:9-13).
-__global__ void __launch_bounds__(256, 6)
+#ifndef LOD_COUNT_MINB
+#define LOD_COUNT_MINB 5  // blocks per SM: 51 registers
+#endif
+__global__ void __launch_bounds__(256, LOD_COUNT_MINB)
     k_count(NodeCols nd, Geo geo, PointSrc src, int32_t *__restrict__ node_of, long long n, int first,
             const uint32_t *__restrict__ grid32, Hash h, Ctrl *ctrl) { lod::pdl_wait();
   __shared__ UsedStage stg;
@@ -243,10 +246,11 @@ __global__ void __launch_bounds__(256, 6)
         const int lvl0 = nd.level[nid];
         double s = geo.size_by_level[lvl0], inv_s = geo.inv_by_level[lvl0];
         const uint32_t v = first ? ((uint32_t)j | kBatchTag) : (uint32_t)j;
-        // one dependent load per level, from the compact descent table
+        // one dependent load per level, from the compact (L1-resident)
+        // descent table; grid words bypass L1 so they do not evict it
         do {
           const long long cell = cell_of(geo, x, y, z, bx, by, bz, s, inv_s);
-          const uint32_t w = __ldg(grid32 + ((unsigned long long)(uint32_t)d.y << 4) + (cell >> 5));
+          const uint32_t w = ld_nol1(grid32 + ((unsigned long long)(uint32_t)d.y << 4) + (cell >> 5));
           const int cur = nid;
           nid = d.x + octant_step(x, y, z, bx, by, bz, s, inv_s);
           d = __ldg(nd.desc + nid);

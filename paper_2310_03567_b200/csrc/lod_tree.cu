@@ -501,6 +501,16 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   auto mark = [&](int phase) {
     if (prof) cudaEventRecord(t->ev[1 + phase], st);
   };
+  // LOD_DEBUG=2: host timeline of the call (microseconds since entry)
+  const bool tl = getenv("LOD_DEBUG") && atoi(getenv("LOD_DEBUG")) >= 2;
+  const auto t_entry = std::chrono::steady_clock::now();
+  char tlbuf[2048];
+  int tlpos = 0;
+  auto tp = [&](const char *what) {
+    if (!tl || tlpos > 1900) return;
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_entry).count();
+    tlpos += snprintf(tlbuf + tlpos, sizeof(tlbuf) - tlpos, " %s=%.0f", what, us);
+  };
   CK(cudaEventRecord(t->ev[0], st));
   // ---- inputs
   const float *bx = xyz;
@@ -547,7 +557,9 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     lod::launch(k_decide, 1, kDecideBlock, 0, st, t->nd, t->geo, t->touched.p, t->bitmap.p, t->word_prefix.p,
                                          t->split_list.p, t->srank.p, t->scnt.p, t->schk.p, t->spill_off.p,
                                          t->chunk_off.p, t->d_ctrl, spill_cap, t->arena_cap);
+    tp("pre_sync");
     RK(sync_ctrl(t));
+    tp("sync");
     if (prof) {
       float x = 0.f;
       cudaEventElapsedTime(&x, t->ev[12], t->ev[13]);
@@ -600,6 +612,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     }
   }
   mark(0);
+  tp("expand_done");
   Ctrl h1 = *t->h_ctrl;
 #ifdef LOD_EXP_COUNT
   fprintf(stderr, "[lod] claims=%lld probes=%lld n_used=%llu hcap=%llu n=%lld n_s=%lld\n", h1.alloc_F, h1.alloc_A,
@@ -643,6 +656,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     lod::launch(k_resolve, grid_for(n_v), 256, 0, st, t->nd, hs, grid32, n_s, D, t->wins.p, t->wmask.p, t->d_ctrl);
   }
   mark(1);
+  tp("resolve_launched");
   RK(t->bnode.ensure(std::max<long long>(n_v, 1), st));
   RK(t->bcell.ensure(std::max<long long>(n_v, 1), st));
   RK(t->brgba.ensure(std::max<long long>(n_v, 1), st));
@@ -684,6 +698,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   uint32_t *skeys = nullptr, *svals = nullptr;
   stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals);
   mark(3);
+  tp("sort_launched");
   // ---- allocation (update.py:317-331): touched nodes = nodes with new samples, ascending id
   const long long Kb = num_nodes + 1;  // bound on touched nodes
   RK(t->seg_node.ensure(Kb, st));
@@ -715,7 +730,10 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   lod::launch(k_epilogue, grid_for(Kb), 256, 0, st, t->nd, t->seg_node.p, t->seg_start.p, t->d_ctrl);
   mark(6);
   CK(cudaEventRecord(t->ev[10], st));
+  tp("all_launched");
   RK(sync_ctrl(t));
+  tp("final_sync");
+  if (tl) fprintf(stderr, "[lod] timeline%s\n", tlbuf);
   const Ctrl &h3 = *t->h_ctrl;
   if (h3.error) return abort_cycle(t, h3.error);
   S.n_spill = n_s;
@@ -892,3 +910,116 @@ int lod_tree_ensure_fb(LodTree *t, long long n, unsigned long long **p) {
   return rc;
 }
 unsigned long long *lod_tree_counter(LodTree *t) { return t->counter.p; }
+
+// ---------------------------------------------------------------- replication
+
+namespace {
+struct PackHeader {
+  unsigned long long magic;
+  long long num_nodes, allocated_total, free_count;
+  unsigned long long arena_off;
+  Ctrl ctrl;
+};
+constexpr unsigned long long kPackMagic = 0x4C4F4442323030ULL;  // "LODB200"
+
+struct PackLayout {
+  size_t off[32];
+  size_t total;
+};
+
+// Byte layout of a packed tree: header, 14 node columns [0, n), 6 pool columns
+// [0, allocated_total), the free stack [0, free_count), arena [0, arena_off).
+PackLayout pack_layout(const Ctrl &c) {
+  PackLayout L{};
+  const size_t n = (size_t)c.num_nodes, a = (size_t)c.allocated_total, f = (size_t)c.free_count;
+  const size_t sizes[] = {sizeof(PackHeader),
+                          n * 4, n * 1, n * 4, n * 32, n * 1, n * 1, n * 8, n * 8, n * 4, n * 4, n * 4, n * 8,
+                          n * 24, n * 8,
+                          a * 4, a * 8, a * 4, a * 4, a * 4,
+                          f * 4,
+                          (size_t)c.arena_off};
+  size_t o = 0;
+  int k = 0;
+  for (size_t s : sizes) {
+    L.off[k++] = o;
+    o += (s + 255) / 256 * 256;
+  }
+  L.off[k] = o;
+  L.total = o;
+  return L;
+}
+}  // namespace
+
+extern "C" {
+
+int lod_tree_pack_size(LodTree *t, uint64_t *bytes) {
+  if (!t || !bytes) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  RK(sync_ctrl(t));
+  *bytes = pack_layout(*t->h_ctrl).total;
+  return LOD_OK;
+}
+
+int lod_tree_pack(LodTree *t, void *dev_buf, uint64_t bytes) {
+  if (!t || !dev_buf) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  RK(sync_ctrl(t));
+  const Ctrl c = *t->h_ctrl;
+  const PackLayout L = pack_layout(c);
+  if (bytes < L.total) return LOD_E_ARG;
+  uint8_t *b = static_cast<uint8_t *>(dev_buf);
+  PackHeader hd{kPackMagic, c.num_nodes, c.allocated_total, c.free_count, c.arena_off, c};
+  cudaStream_t st = t->st;
+  CK(cudaMemcpyAsync(b + L.off[0], &hd, sizeof(hd), cudaMemcpyHostToDevice, st));
+  const size_t n = (size_t)c.num_nodes, a = (size_t)c.allocated_total, f = (size_t)c.free_count;
+  const void *src[] = {t->nd.parent, t->nd.octant, t->nd.level, t->nd.children, t->nd.inner, t->nd.final_,
+                       t->nd.count, t->nd.pending, t->nd.chunk_head, t->nd.chunk_tail, t->nd.chunk_count,
+                       t->nd.grid_off, t->nd.bmin, t->nd.desc, t->pool.next, t->pool.payload_off,
+                       t->pool.occupied, t->pool.owner, t->pool.cidx, t->pool.free_stack, t->arena};
+  const size_t sz[] = {n * 4, n, n * 4, n * 32, n, n, n * 8, n * 8, n * 4, n * 4, n * 4, n * 8, n * 24, n * 8,
+                       a * 4, a * 8, a * 4, a * 4, a * 4, f * 4, (size_t)c.arena_off};
+  for (int k = 0; k < 21; ++k)
+    if (sz[k]) CK(cudaMemcpyAsync(b + L.off[k + 1], src[k], sz[k], cudaMemcpyDeviceToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  return LOD_OK;
+}
+
+int lod_tree_unpack(LodTree *t, const void *dev_buf, uint64_t bytes) {
+  if (!t || !dev_buf || bytes < sizeof(PackHeader)) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  cudaStream_t st = t->st;
+  const uint8_t *b = static_cast<const uint8_t *>(dev_buf);
+  PackHeader hd;
+  CK(cudaMemcpy(&hd, b, sizeof(hd), cudaMemcpyDeviceToHost));
+  if (hd.magic != kPackMagic) return LOD_E_ARG;
+  const Ctrl c = hd.ctrl;
+  const PackLayout L = pack_layout(c);
+  if (bytes < L.total || c.arena_off > t->arena_cap) return LOD_E_ARG;
+  RK(ensure_nodes(t, std::max<long long>(c.num_nodes, 1), 0));
+  RK(ensure_chunks(t, std::max<long long>(c.allocated_total + 1, 1), 0));
+  const size_t n = (size_t)c.num_nodes, a = (size_t)c.allocated_total, f = (size_t)c.free_count;
+  void *dst[] = {t->nd.parent, t->nd.octant, t->nd.level, t->nd.children, t->nd.inner, t->nd.final_,
+                 t->nd.count, t->nd.pending, t->nd.chunk_head, t->nd.chunk_tail, t->nd.chunk_count,
+                 t->nd.grid_off, t->nd.bmin, t->nd.desc, t->pool.next, t->pool.payload_off,
+                 t->pool.occupied, t->pool.owner, t->pool.cidx, t->pool.free_stack, t->arena};
+  const size_t sz[] = {n * 4, n, n * 4, n * 32, n, n, n * 8, n * 8, n * 4, n * 4, n * 4, n * 8, n * 24, n * 8,
+                       a * 4, a * 8, a * 4, a * 4, a * 4, f * 4, (size_t)c.arena_off};
+  for (int k = 0; k < 21; ++k)
+    if (sz[k]) CK(cudaMemcpyAsync(dst[k], b + L.off[k + 1], sz[k], cudaMemcpyDeviceToDevice, st));
+  // the rest of the arena must stay zeroed (regions are handed out zeroed)
+  if (t->arena_cap > c.arena_off) CK(cudaMemsetAsync(t->arena + c.arena_off, 0, t->arena_cap - c.arena_off, st));
+  Ctrl nc{};
+  nc.num_nodes = c.num_nodes;
+  nc.splits_total = c.splits_total;
+  nc.max_level = c.max_level;
+  nc.arena_off = c.arena_off;
+  nc.allocated_total = c.allocated_total;
+  nc.free_count = c.free_count;
+  nc.released_total = c.released_total;
+  CK(cudaMemcpyAsync(t->d_ctrl, &nc, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+  RK(sync_ctrl(t));
+  t->num_nodes = c.num_nodes;
+  return LOD_OK;
+}
+
+}  // extern "C"

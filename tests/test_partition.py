@@ -112,3 +112,52 @@ def test_gloo_all_to_all_routing_preserves_global_order():
         p.join(timeout=120)
     assert all(p.exitcode == 0 for p in procs)
     assert dict(out) == {0: True, 1: True}
+
+
+def _route_worker(rank, world, port, out):
+    """multigpu.route + composite_min with CPU tensors over gloo (the NCCL path's logic)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2310_03567_b200 import multigpu
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    xyz, _ = synth.gen_surface(12_000, 9)
+    rgba = np.arange(len(xyz), dtype=np.uint32)  # colour = global index
+    plan = partition.plan_owners([(xyz, rgba)], world)
+    n = len(rgba)
+    st = slice(rank * n // world, (rank + 1) * n // world)
+    gx, gc = multigpu.route(torch.from_numpy(xyz[st].copy()), torch.from_numpy(rgba[st].view(np.int32).copy()),
+                            plan, world)
+    want_x, want_c = partition.take(plan, xyz, rgba, rank)
+    ok = np.array_equal(gx.numpy(), want_x) and np.array_equal(gc.numpy().view(np.uint32), want_c)
+    # framebuffer min-composite with the all-ones sentinel
+    rng = np.random.default_rng(rank)
+    fb = np.full(64, np.uint64(0xFFFFFFFFFFFFFFFF))
+    hit = rng.choice(64, 20, replace=False)
+    fb[hit] = rng.integers(0, 1 << 62, 20).astype(np.uint64)
+    comp = multigpu.composite_min(torch.from_numpy(fb.view(np.int64).copy())).numpy().view(np.uint64)
+    allfb = [torch.zeros(64, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(allfb, torch.from_numpy(fb.view(np.int64).copy()))
+    want_fb = np.minimum.reduce([a.numpy().view(np.uint64) for a in allfb])
+    out[rank] = bool(ok and np.array_equal(comp, want_fb))
+    dist.destroy_process_group()
+
+
+def test_gloo_route_and_composite():
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    procs = [ctx.Process(target=_route_worker, args=(r, 2, port, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    assert all(p.exitcode == 0 for p in procs)
+    assert dict(out) == {0: True, 1: True}

@@ -78,6 +78,18 @@ typedef struct {
     int64_t *stamp;
     int64_t touched_cap, vtouched_cap, leaf_cap, alloc_cap, scratch_nodes;
     int64_t pass_no;
+    /* BatchDelta capture (update.py:183-194, 333-355), on when collect_delta */
+    int delta_on;
+    int32_t *d_splits;            /* split nodes in split order */
+    int64_t d_nsplits, d_splits_cap;
+    int32_t *d_vnode;             /* per voxel group: node, start, count (ascending node) */
+    int64_t *d_vstart, *d_vcount;
+    int32_t *d_vcell;             /* voxel cells / colours, stable by node (claim order) */
+    uint32_t *d_vrgba;
+    int64_t d_nvgroups, d_nvox;
+    int32_t *d_pnode;             /* per touched leaf: node, pre-store count, new points */
+    int64_t *d_pstart, *d_pcount;
+    int64_t d_npts;
 } OrcTree;
 
 /* x86 cvttsd2si: out-of-range / NaN -> INT64_MIN (numba np.int64(float)). */
@@ -242,6 +254,8 @@ void orc_tree_destroy(OrcTree *t) {
     free(t->spill_xyz); free(t->spill_rgba); free(t->bnode); free(t->bcell); free(t->brgba);
     free(t->touched); free(t->vtouched); free(t->leaf_ids); free(t->alloc_node);
     free(t->alloc_need); free(t->cursor); free(t->stamp);
+    free(t->d_splits); free(t->d_vnode); free(t->d_vstart); free(t->d_vcount); free(t->d_vcell);
+    free(t->d_vrgba); free(t->d_pnode); free(t->d_pstart); free(t->d_pcount);
     free(t);
 }
 
@@ -401,6 +415,13 @@ static int split_pass(OrcTree *t, int32_t *ids, int64_t n, int64_t *n_splits) {
         if (t->count[nid] + t->pending[nid] > t->p.leaf_threshold && t->level[nid] < t->p.max_depth) {
             rc = split_node(t, nid);
             if (!rc) *n_splits += 1;
+            if (!rc && t->delta_on) { /* events.append(("split", nid)), update.py:240-245 */
+                if (t->d_nsplits == t->d_splits_cap) {
+                    t->d_splits_cap = t->d_splits_cap ? 2 * t->d_splits_cap : 64;
+                    t->d_splits = (int32_t *)xrealloc(t->d_splits, sizeof(int32_t) * t->d_splits_cap);
+                }
+                t->d_splits[t->d_nsplits++] = (int32_t)nid;
+            }
         } else {
             t->final_[nid] = 1;
         }
@@ -543,11 +564,60 @@ static void node_scratch(OrcTree *t) { /* UpdateState._node_scratch, update.py:2
     t->scratch_nodes = n;
 }
 
-/* update.insert_batch, update.py:252-393 (collect_delta not restated). */
+/* BatchDelta voxels / points (update.py:333-355), captured before the store
+ * passes advance the counts: voxels grouped by node with a stable sort of the
+ * backlog (claim order inside a node), points as (leaf, count, pending) over
+ * the sorted touched leaves that are still leaves and received points. */
+static void build_delta(OrcTree *t, int64_t blen, int64_t leaf_touch_end) {
+    int64_t nn = t->num_nodes;
+    int64_t *cnt = (int64_t *)calloc((size_t)nn + 1, sizeof(int64_t));
+    for (int64_t i = 0; i < blen; ++i) cnt[t->bnode[i] + 1] += 1;
+    t->d_nvgroups = 0;
+    for (int64_t k = 0; k < nn; ++k) t->d_nvgroups += cnt[k + 1] > 0;
+    t->d_vnode = (int32_t *)xrealloc(t->d_vnode, sizeof(int32_t) * (size_t)t->d_nvgroups);
+    t->d_vstart = (int64_t *)xrealloc(t->d_vstart, sizeof(int64_t) * (size_t)t->d_nvgroups);
+    t->d_vcount = (int64_t *)xrealloc(t->d_vcount, sizeof(int64_t) * (size_t)t->d_nvgroups);
+    int64_t g = 0;
+    for (int64_t k = 0; k < nn; ++k) {
+        if (cnt[k + 1]) { t->d_vnode[g] = (int32_t)k; t->d_vcount[g] = cnt[k + 1]; g++; }
+        cnt[k + 1] += cnt[k];
+    }
+    for (int64_t q = 0; q < g; ++q) t->d_vstart[q] = cnt[t->d_vnode[q]];
+    t->d_vcell = (int32_t *)xrealloc(t->d_vcell, sizeof(int32_t) * (size_t)blen);
+    t->d_vrgba = (uint32_t *)xrealloc(t->d_vrgba, sizeof(uint32_t) * (size_t)blen);
+    for (int64_t i = 0; i < blen; ++i) {
+        int64_t pos = cnt[t->bnode[i]]++;
+        t->d_vcell[pos] = t->bcell[i];
+        t->d_vrgba[pos] = t->brgba[i];
+    }
+    t->d_nvox = blen;
+    free(cnt);
+    int32_t *ids = (int32_t *)malloc(sizeof(int32_t) * (size_t)(leaf_touch_end ? leaf_touch_end : 1));
+    memcpy(ids, t->touched, sizeof(int32_t) * (size_t)leaf_touch_end);
+    qsort(ids, (size_t)leaf_touch_end, sizeof(int32_t), cmp_i32);
+    t->d_pnode = (int32_t *)xrealloc(t->d_pnode, sizeof(int32_t) * (size_t)leaf_touch_end);
+    t->d_pstart = (int64_t *)xrealloc(t->d_pstart, sizeof(int64_t) * (size_t)leaf_touch_end);
+    t->d_pcount = (int64_t *)xrealloc(t->d_pcount, sizeof(int64_t) * (size_t)leaf_touch_end);
+    t->d_npts = 0;
+    for (int64_t k = 0; k < leaf_touch_end; ++k) {
+        int32_t nid = ids[k];
+        if (!t->inner[nid] && t->pending[nid] > 0) {
+            t->d_pnode[t->d_npts] = nid;
+            t->d_pstart[t->d_npts] = t->count[nid];
+            t->d_pcount[t->d_npts] = t->pending[nid];
+            t->d_npts++;
+        }
+    }
+    free(ids);
+}
+
+/* update.insert_batch, update.py:252-393; with t->delta_on the BatchDelta of
+ * the cycle is captured (update.py:333-355) and read with orc_delta_view. */
 int orc_insert_batch(OrcTree *t, const float *xyz, const uint32_t *rgba, int64_t n_batch,
                      OrcBatchStats *st) {
     memset(st, 0, sizeof(*st));
     st->n_batch = n_batch;
+    t->d_nsplits = t->d_nvgroups = t->d_nvox = t->d_npts = 0;
     if (n_batch == 0) return 0; /* update.py:266-268 */
     int rc;
     Src s = {NULL, NULL, 0, xyz, rgba, n_batch};
@@ -604,6 +674,7 @@ int orc_insert_batch(OrcTree *t, const float *xyz, const uint32_t *rgba, int64_t
             }
         }
     }
+    if (t->delta_on) build_delta(t, blen, leaf_touch_end);
     /* store, update.py:358-373 */
     t->pass_no += 1;
     store_points(t, &s);
@@ -703,4 +774,23 @@ void orc_view(const OrcTree *t, OrcView *v) {
     v->pending = t->pending; v->grid_off = t->grid_off; v->bmin = t->bmin; v->next = t->next;
     v->occupied = t->occupied; v->free_list = t->free_; v->payload_off = t->payload_off;
     v->arena = t->arena;
+}
+
+/* ---- BatchDelta export (collect_delta=True) ------------------------------ */
+
+typedef struct {
+    int64_t n_splits, n_voxel_groups, n_voxels, n_point_groups;
+    int32_t *splits, *vnode, *vcell, *pnode;
+    int64_t *vstart, *vcount, *pstart, *pcount;
+    uint32_t *vrgba;
+} OrcDeltaView;
+
+void orc_set_delta(OrcTree *t, int on) { t->delta_on = on; }
+
+void orc_delta_view(const OrcTree *t, OrcDeltaView *v) {
+    v->n_splits = t->d_nsplits; v->n_voxel_groups = t->d_nvgroups; v->n_voxels = t->d_nvox;
+    v->n_point_groups = t->d_npts;
+    v->splits = t->d_splits; v->vnode = t->d_vnode; v->vcell = t->d_vcell; v->pnode = t->d_pnode;
+    v->vstart = t->d_vstart; v->vcount = t->d_vcount; v->pstart = t->d_pstart; v->pcount = t->d_pcount;
+    v->vrgba = t->d_vrgba;
 }

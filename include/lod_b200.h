@@ -41,7 +41,8 @@ enum {
 enum {
     LOD_FLAG_DEVICE_INPUT = 1, /* xyz / rgba are device pointers (resident in HBM)          */
     LOD_FLAG_DEVICE_FB = 2,    /* framebuffer pointer is a device pointer                   */
-    LOD_FLAG_PROFILE = 4       /* record per-phase CUDA-event times into LodBatchStats      */
+    LOD_FLAG_PROFILE = 4,      /* record per-phase CUDA-event times into LodBatchStats      */
+    LOD_FLAG_DELTA = 8         /* capture the cycle's BatchDelta (collect_delta=True)       */
 };
 
 typedef struct LodTree LodTree;
@@ -128,6 +129,22 @@ int lod_gather(LodTree *tree, int64_t nid, int64_t start, float *xyz, uint32_t *
 /* Every node's samples, packed in node-id order: offsets (num_nodes+1) are the
  * prefix sums of count; records are 16-byte (x,y,z,rgba). */
 int lod_dump_records(LodTree *tree, int64_t num_nodes, int64_t *offsets, void *records);
+
+/* BatchDelta of the last lod_insert_batch made with LOD_FLAG_DELTA -- replaces
+ * insert_batch(collect_delta=True) (update.py:183-194, 333-355), the producer
+ * of the streaming service (service.py:228-243, 299):
+ *   splits        split nodes in split order (each split's 8 "create" events
+ *                 are its children, ids children[8*nid+o], octant o);
+ *   voxel groups  ascending node id: node, [vstart, vstart+vcount) into
+ *                 vcells / vrgba (claim order inside a node);
+ *   point groups  ascending node id: leaf, pre-store count (gather start), new points.
+ * lod_delta_info gives the sizes; lod_read_delta copies to host (NULL skips). */
+typedef struct {
+    int64_t n_splits, n_voxel_groups, n_voxels, n_point_groups;
+} LodDeltaInfo;
+int lod_delta_info(LodTree *tree, LodDeltaInfo *info);
+int lod_read_delta(LodTree *tree, int32_t *splits, int32_t *vnode, int64_t *vstart, int64_t *vcount,
+                   uint32_t *vcells, uint32_t *vrgba, int32_t *pnode, int64_t *pstart, int64_t *pcount);
 
 /* Raw arena bytes [off, off+size) (Octree.grid, octree.py:275-279). */
 int lod_read_arena(LodTree *tree, uint64_t off, uint64_t size, void *dst);

@@ -10,7 +10,7 @@ no CPU fallback: without the library or a CUDA device the entry points raise.
 from .errors import BacklogOverflow, OutOfArena, SpillOverflow
 from .octree import CubeBounds, Octree, cubify
 from .store import Arena, ChunkPool
-from .update import UpdateConfig, UpdateState, insert_batch, run_frame_updates
+from .update import BatchDelta, UpdateConfig, UpdateState, insert_batch, run_frame_updates
 
 __version__ = "0.1.0"
 
@@ -19,6 +19,7 @@ __all__ = [
     "ChunkPool",
     "CubeBounds",
     "Octree",
+    "BatchDelta",
     "UpdateConfig",
     "UpdateState",
     "cubify",

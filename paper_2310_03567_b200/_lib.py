@@ -28,6 +28,7 @@ LOD_E_NO_DEVICE = 7
 LOD_FLAG_DEVICE_INPUT = 1
 LOD_FLAG_DEVICE_FB = 2
 LOD_FLAG_PROFILE = 4
+LOD_FLAG_DELTA = 8
 LOD_NPHASE = 10
 PHASES = ("count", "split", "resolve", "backlog", "sort", "alloc", "store", "epilogue", "h2d", "total")
 
@@ -86,6 +87,11 @@ class LodTreeInfo(ctypes.Structure):
     ]
 
 
+class LodDeltaInfo(ctypes.Structure):
+    _fields_ = [("n_splits", ctypes.c_int64), ("n_voxel_groups", ctypes.c_int64), ("n_voxels", ctypes.c_int64),
+                ("n_point_groups", ctypes.c_int64)]
+
+
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 
@@ -102,6 +108,8 @@ SIGNATURES = {
     "lod_read_pool": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _I64]),
     "lod_gather": (ctypes.c_int, [_P, _I64, _I64, _P, _P]),
     "lod_dump_records": (ctypes.c_int, [_P, _I64, _P, _P]),
+    "lod_delta_info": (ctypes.c_int, [_P, ctypes.POINTER(LodDeltaInfo)]),
+    "lod_read_delta": (ctypes.c_int, [_P] + [_P] * 9),
     "lod_read_arena": (ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     "lod_rasterize": (ctypes.c_int, [_P, _P, _I64, _P, _P, _I64, _I64, ctypes.c_int, ctypes.POINTER(_I64)]),
     "lod_raster_points": (ctypes.c_int, [ctypes.c_int32, _P, _P, _I64, _P, _P, _I64, _I64, ctypes.c_int]),

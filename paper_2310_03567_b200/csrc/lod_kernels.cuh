@@ -59,6 +59,9 @@ struct Ctrl {
   long long alloc_A;          // allocated_total before allocation
   unsigned long long chunk_base;
   long long n_items;
+  // BatchDelta capture (LOD_FLAG_DELTA)
+  unsigned int d_nvg;         // voxel groups (inner nodes with new voxels)
+  unsigned int d_npg;         // point groups (leaves with new points)
 };
 
 __device__ __forceinline__ void set_error(Ctrl *c, int code) { atomicCAS(&c->error, 0, code); }
@@ -768,6 +771,80 @@ __global__ void k_epilogue(NodeCols nd, const int32_t *__restrict__ seg_node, co
     nd.count[n] += seg_start[d + 1] - seg_start[d];
     nd.pending[n] = 0;
     nd.final_[n] = 0;
+  }
+}
+
+// ---------------------------------------------------------------- BatchDelta
+
+// collect_delta (update.py:333-355), from the cycle's segment table before the
+// epilogue advances the counts: every touched segment is either an inner node
+// (its items are new voxels, in claim order) or a leaf (new points).  One CTA
+// scans the segments in ascending node id into the voxel-group list (node,
+// offset into the delta voxel arrays, count) and the point-group list (node,
+// pre-store count, count); vbase[d] is segment d's delta voxel offset.
+constexpr int kDeltaBlock = 1024;
+__global__ void __launch_bounds__(kDeltaBlock)
+    k_delta_segs(NodeCols nd, const int32_t *__restrict__ seg_node, const long long *__restrict__ seg_start,
+                 int32_t *__restrict__ vnode, long long *__restrict__ vstart, long long *__restrict__ vcount,
+                 int32_t *__restrict__ pnode, long long *__restrict__ pstart, long long *__restrict__ pcount,
+                 long long *__restrict__ vbase, Ctrl *ctrl) { lod::pdl_wait();
+  __shared__ U64x2 sh[kDeltaBlock / 32 + 1];
+  if (ctrl->error) return;
+  const long long K = (long long)ctrl->n_keys;
+  U64x2 carry = u64x2(0, 0);
+  for (long long base = 0; base < K; base += kDeltaBlock) {
+    const long long d = base + threadIdx.x;
+    int n = -1;
+    bool inner = false;
+    long long len = 0;
+    if (d < K) {
+      n = seg_node[d];
+      inner = nd.inner[n] != 0;
+      len = seg_start[d + 1] - seg_start[d];
+    }
+    // a: group counters (voxel groups low word, point groups high word); b: voxels
+    const U64x2 v = u64x2(d < K ? (inner ? 1ull : (1ull << 32)) : 0ull, inner ? (unsigned long long)len : 0ull);
+    U64x2 tot;
+    U64x2 ex = block_exclusive_scan<U64x2, kDeltaBlock>(v, sh, tot);
+    ex = ex + carry;
+    if (d < K) {
+      if (inner) {
+        const long long g = (long long)(ex.a & 0xFFFFFFFFull);
+        vnode[g] = n;
+        vstart[g] = (long long)ex.b;
+        vcount[g] = len;
+        vbase[d] = (long long)ex.b;
+      } else {
+        const long long g = (long long)(ex.a >> 32);
+        pnode[g] = n;
+        pstart[g] = nd.count[n];
+        pcount[g] = len;
+      }
+    }
+    carry = carry + tot;
+  }
+  if (threadIdx.x == 0) {
+    ctrl->d_nvg = (unsigned)(carry.a & 0xFFFFFFFFull);
+    ctrl->d_npg = (unsigned)(carry.a >> 32);
+  }
+}
+
+// Delta voxel payload: every voxel item of the sorted order (node-major,
+// ascending claim index inside a node = the reference's stable argsort of the
+// backlog by node) copies its (cell, rgba) to its group's slot.
+__global__ void k_delta_vox(const uint32_t *__restrict__ skeys, const uint32_t *__restrict__ svals,
+                            const int32_t *__restrict__ dense, const long long *__restrict__ seg_start,
+                            const long long *__restrict__ vbase, long long n_items, long long n_all,
+                            const uint32_t *__restrict__ bcell, const uint32_t *__restrict__ brgba,
+                            uint32_t *__restrict__ dcell, uint32_t *__restrict__ drgba, const Ctrl *ctrl) { lod::pdl_wait();
+  if (ctrl->error) return;
+  for (long long p = gtid(); p < n_items; p += gstride()) {
+    const long long i = svals[p];
+    if (i < n_all) continue;
+    const long long d = dense[skeys[p]];
+    const long long pos = vbase[d] + (p - seg_start[d]);
+    dcell[pos] = bcell[i - n_all];
+    drgba[pos] = brgba[i - n_all];
   }
 }
 

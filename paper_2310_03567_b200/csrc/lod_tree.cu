@@ -192,6 +192,11 @@ struct LodTree {
   DBuf<int32_t> vislist;
   DBuf<unsigned long long> fb;
   DBuf<unsigned long long> counter;
+  // BatchDelta of the last call with LOD_FLAG_DELTA (lod_read_delta)
+  DBuf<int32_t> dsplits, dvnode, dpnode;
+  DBuf<long long> dvstart, dvcount, dpstart, dpcount, dvbase;
+  DBuf<uint32_t> dvcell, dvrgba;
+  long long d_nsplits = 0, d_nvg = 0, d_npg = 0, d_nv = 0;
   cudaEvent_t ev[14] = {};  // 12, 13: per-iteration k_count brackets
   // host copies of counters (authoritative after every call)
   long long num_nodes = 1;
@@ -382,6 +387,24 @@ int lod_tree_create(const LodParams *params, LodTree **out) {
     if (cudaDeviceGetDefaultMemPool(&pool, t->dev) == cudaSuccess) {
       unsigned long long thr = ~0ull;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      // Back the pool with physical memory once per device (LOD_POOL_RESERVE_MIB,
+      // default 6 GiB, at most 1/8 of free HBM): scratch growth during a split
+      // burst is then a pool sub-allocation instead of a page-table mapping
+      // inside the update (measured: 20-27 ms first-touch stalls on 5.8M-point spills).
+      static bool warmed[64] = {};
+      if (t->dev < 64 && !warmed[t->dev]) {
+        warmed[t->dev] = true;
+        const char *e = getenv("LOD_POOL_RESERVE_MIB");
+        unsigned long long want = (e ? strtoull(e, nullptr, 10) : 6144ull) << 20;
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) want = std::min<unsigned long long>(want, fr / 8);
+        void *q = nullptr;
+        if (want && cudaMallocAsync(&q, want, t->st) == cudaSuccess) {
+          cudaFreeAsync(q, t->st);
+          cudaStreamSynchronize(t->st);
+        }
+        cudaGetLastError();
+      }
     }
   }
   for (auto &e : t->ev) CK(cudaEventCreate(&e));
@@ -486,6 +509,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   cudaSetDevice(t->dev);
   cudaStream_t st = t->st;
   const bool prof = (flags & LOD_FLAG_PROFILE) != 0;
+  const bool delta = (flags & LOD_FLAG_DELTA) != 0;
+  t->d_nsplits = t->d_nvg = t->d_npg = t->d_nv = 0;
   const long long backlog_cap = limits ? limits->backlog_capacity : 10000000LL;
   const long long spill_cap = limits ? limits->spill_capacity : 100000000LL;
   if (n == 0) {  // update.py:266-268
@@ -570,6 +595,11 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     const long long ns = h.n_splits;
     if (ns == 0) break;
     splits_cycle += ns;
+    if (delta) {  // events.append(("split", nid)) in split order (update.py:240-245)
+      RK(t->dsplits.ensure(t->d_nsplits + ns, st, t->d_nsplits));
+      CK(cudaMemcpyAsync(t->dsplits.p + t->d_nsplits, t->split_list.p, (size_t)ns * 4, cudaMemcpyDeviceToDevice, st));
+      t->d_nsplits += ns;
+    }
     // capacity for the new children and the spill segment
     RK(ensure_nodes(t, h.num_nodes, h.plan_num_nodes0));
     if (h.spill_add > 0) {
@@ -725,6 +755,22 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   lod::launch(k_store, grid_for(n_items), 256, 0, st, t->nd, t->pool, t->geo, t->arena, skeys, svals, t->dense.p,
                                              t->seg_start.p, t->plan.p, t->plan_ex.p, t->wl.p, n_items, n_all,
                                              src, t->bcell.p, t->brgba.p, t->d_ctrl);
+  if (delta) {  // ---- BatchDelta (update.py:333-355), before the counts advance
+    RK(t->dvnode.ensure(Kb, st));
+    RK(t->dvstart.ensure(Kb, st));
+    RK(t->dvcount.ensure(Kb, st));
+    RK(t->dpnode.ensure(Kb, st));
+    RK(t->dpstart.ensure(Kb, st));
+    RK(t->dpcount.ensure(Kb, st));
+    RK(t->dvbase.ensure(Kb, st));
+    RK(t->dvcell.ensure(std::max<long long>(n_v, 1), st));
+    RK(t->dvrgba.ensure(std::max<long long>(n_v, 1), st));
+    lod::launch(k_delta_segs, 1, kDeltaBlock, 0, st, t->nd, t->seg_node.p, t->seg_start.p, t->dvnode.p, t->dvstart.p,
+                t->dvcount.p, t->dpnode.p, t->dpstart.p, t->dpcount.p, t->dvbase.p, t->d_ctrl);
+    if (n_v > 0)
+      lod::launch(k_delta_vox, grid_for(n_items), 256, 0, st, skeys, svals, t->dense.p, t->seg_start.p, t->dvbase.p,
+                  n_items, n_all, t->bcell.p, t->brgba.p, t->dvcell.p, t->dvrgba.p, t->d_ctrl);
+  }
   mark(5);
   // ---- cleanup (update.py:375-380)
   lod::launch(k_epilogue, grid_for(Kb), 256, 0, st, t->nd, t->seg_node.p, t->seg_start.p, t->d_ctrl);
@@ -736,6 +782,11 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   if (tl) fprintf(stderr, "[lod] timeline%s\n", tlbuf);
   const Ctrl &h3 = *t->h_ctrl;
   if (h3.error) return abort_cycle(t, h3.error);
+  if (delta) {
+    t->d_nvg = h3.d_nvg;
+    t->d_npg = h3.d_npg;
+    t->d_nv = n_v;
+  }
   S.n_spill = n_s;
   S.launches = lod::g_launches - launches0;
   S.d2h_bytes = t->d2h_bytes;
@@ -886,6 +937,40 @@ int lod_read_arena(LodTree *t, uint64_t off, uint64_t size, void *dst) {
 }
 
 }  // extern "C"
+
+int lod_delta_info(LodTree *t, LodDeltaInfo *info) {
+  if (!t || !info) return LOD_E_ARG;
+  info->n_splits = t->d_nsplits;
+  info->n_voxel_groups = t->d_nvg;
+  info->n_voxels = t->d_nv;
+  info->n_point_groups = t->d_npg;
+  return LOD_OK;
+}
+
+int lod_read_delta(LodTree *t, int32_t *splits, int32_t *vnode, int64_t *vstart, int64_t *vcount, uint32_t *vcells,
+                   uint32_t *vrgba, int32_t *pnode, int64_t *pstart, int64_t *pcount) {
+  if (!t) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  cudaStream_t st = t->st;
+  auto cp = [&](void *dst, const void *src, long long bytes) -> int {
+    if (bytes <= 0 || !dst) return LOD_OK;
+    if (!src) return LOD_E_ARG;
+    t->d2h_bytes += bytes;
+    CK(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, st));
+    return LOD_OK;
+  };
+  RK(cp(splits, t->dsplits.p, t->d_nsplits * 4));
+  RK(cp(vnode, t->dvnode.p, t->d_nvg * 4));
+  RK(cp(vstart, t->dvstart.p, t->d_nvg * 8));
+  RK(cp(vcount, t->dvcount.p, t->d_nvg * 8));
+  RK(cp(vcells, t->dvcell.p, t->d_nv * 4));
+  RK(cp(vrgba, t->dvrgba.p, t->d_nv * 4));
+  RK(cp(pnode, t->dpnode.p, t->d_npg * 4));
+  RK(cp(pstart, t->dpstart.p, t->d_npg * 8));
+  RK(cp(pcount, t->dpcount.p, t->d_npg * 8));
+  CK(cudaStreamSynchronize(st));
+  return LOD_OK;
+}
 
 // accessors for lod_raster.cu
 cudaStream_t lod_tree_stream(LodTree *t) { return t->st; }

@@ -117,6 +117,11 @@ class VoxelBacklog:
 
 @dataclass
 class BatchDelta:
+    """What one cycle changed, in stream emission order (update.py:183-194):
+    ``structure`` interleaves ("split", node) and ("create", node, parent,
+    octant, level) events in split order; ``voxels`` lists (node, cells u32,
+    rgba u32) and ``points`` (node, start, count) in ascending node id."""
+
     structure: list[tuple] = field(default_factory=list)
     voxels: list[tuple[int, np.ndarray, np.ndarray]] = field(default_factory=list)
     points: list[tuple[int, int, int]] = field(default_factory=list)
@@ -167,17 +172,16 @@ def insert_batch(
     (numpy arrays, copied H2D; or CUDA tensors already resident in HBM).  The
     whole batch is always consumed.
     """
-    if collect_delta:
-        raise NotImplementedError("collect_delta (service stream deltas) is not built yet (SURVEY 8(f) row 3)")
     t0 = time.perf_counter()
     n_batch = len(rgba)
-    if n_batch == 0:
-        return None
+    if n_batch == 0:  # update.py:266-268
+        return BatchDelta() if collect_delta else None
     xyz_b, dev_x = _as_input(xyz, np.float32, (3,))
     rgba_b, dev_c = _as_input(rgba, np.uint32, ())
     if dev_x != dev_c:
         raise ValueError("xyz and rgba must both be host arrays or both be device tensors")
-    flags = (_lib.LOD_FLAG_DEVICE_INPUT if dev_x else 0) | (_lib.LOD_FLAG_PROFILE if profile else 0)
+    flags = ((_lib.LOD_FLAG_DEVICE_INPUT if dev_x else 0) | (_lib.LOD_FLAG_PROFILE if profile else 0)
+             | (_lib.LOD_FLAG_DELTA if collect_delta else 0))
     lim = state._limits
     lim.backlog_capacity = state.config.backlog_capacity
     lim.spill_capacity = state.config.spill_capacity
@@ -202,10 +206,39 @@ def insert_batch(
         state.last = bs.as_dict()
     else:
         state.last = None
+    delta = _read_delta(tree) if collect_delta else None
     dt = time.perf_counter() - t0
     st.update_seconds += dt
     st.max_batch_ms = max(st.max_batch_ms, dt * 1e3)
-    return None
+    return delta
+
+
+def _read_delta(tree: Octree) -> BatchDelta:
+    """The cycle's BatchDelta, assembled on the device (k_delta_segs /
+    k_delta_vox) and copied out once (lod_read_delta); the "create" events are
+    each split's 8 children in octant order (update.py:240-245)."""
+    info = _lib.LodDeltaInfo()
+    _lib.check(tree._L.lod_delta_info(tree.handle, ctypes.byref(info)), "delta_info")
+    ns, nvg, nv, npg = info.n_splits, info.n_voxel_groups, info.n_voxels, info.n_point_groups
+    splits = np.empty(ns, np.int32)
+    vnode, vstart, vcount = np.empty(nvg, np.int32), np.empty(nvg, np.int64), np.empty(nvg, np.int64)
+    cells, cols = np.empty(nv, np.uint32), np.empty(nv, np.uint32)
+    pnode, pstart, pcount = np.empty(npg, np.int32), np.empty(npg, np.int64), np.empty(npg, np.int64)
+    p = _lib.ptr
+    _lib.check(tree._L.lod_read_delta(tree.handle, p(splits), p(vnode), p(vstart), p(vcount), p(cells), p(cols),
+                                      p(pnode), p(pstart), p(pcount)), "read_delta")
+    d = BatchDelta()
+    if ns:
+        children, level = tree.children, tree.level
+        for nid in splits.tolist():
+            d.structure.append(("split", nid))
+            for o in range(8):
+                kid = int(children[nid, o])
+                d.structure.append(("create", kid, nid, o, int(level[kid])))
+    d.voxels = [(int(a), cells[s:s + c], cols[s:s + c]) for a, s, c in zip(vnode.tolist(), vstart.tolist(),
+                                                                        vcount.tolist())]
+    d.points = list(zip(pnode.tolist(), pstart.tolist(), pcount.tolist()))
+    return d
 
 
 def run_frame_updates(tree, batches, state: UpdateState, on_delta=None) -> int:

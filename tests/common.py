@@ -17,7 +17,7 @@ CHUNK_ID_COLS = ("chunk_head", "chunk_tail", "next", "occupied", "payload_off", 
 
 
 def golden_names() -> list[str]:
-    return sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and f != "raster.npz")
+    return sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and f not in ("raster.npz", "deltas.npz"))
 
 
 def load_golden(name: str) -> dict:
@@ -35,6 +35,58 @@ def load_golden(name: str) -> dict:
 def load_raster() -> dict:
     z = np.load(os.path.join(GOLDEN, "raster.npz"))
     return {k: z[k] for k in z.files}
+
+
+DELTA_KEYS = ("events", "vgroups", "vcells", "vrgba", "points", "ev_off", "vg_off", "vc_off", "pt_off")
+
+
+def delta_names() -> list[str]:
+    z = np.load(os.path.join(GOLDEN, "deltas.npz"))
+    return sorted({k.split("__")[0] for k in z.files})
+
+
+def load_deltas(name: str) -> dict:
+    """The reference's BatchDelta of every batch of a scenario (make_golden.make_deltas)."""
+    z = np.load(os.path.join(GOLDEN, "deltas.npz"))
+    return {k: z[f"{name}__{k}"] for k in DELTA_KEYS}
+
+
+def flatten_deltas(deltas) -> dict:
+    """[(structure, voxels, points)] or [BatchDelta] -> the deltas.npz layout."""
+    ev, vg, cells, cols, pts = [], [], [], [], []
+    off = {"ev": [0], "vg": [0], "vc": [0], "pt": [0]}
+    nvc = 0
+    for d in deltas:
+        structure, voxels, points = (d.structure, d.voxels, d.points) if hasattr(d, "structure") else d
+        for e in structure:
+            ev.append([0, e[1], -1, -1, -1] if e[0] == "split" else [1, e[1], e[2], e[3], e[4]])
+        for node, c, r in voxels:
+            assert np.asarray(c).dtype == np.uint32 and np.asarray(r).dtype == np.uint32
+            vg.append([node, len(c)])
+            cells.append(np.asarray(c, np.uint32))
+            cols.append(np.asarray(r, np.uint32))
+            nvc += len(c)
+        for node, start, count in points:
+            pts.append([node, start, count])
+        off["ev"].append(len(ev))
+        off["vg"].append(len(vg))
+        off["vc"].append(nvc)
+        off["pt"].append(len(pts))
+    out = {
+        "events": np.array(ev, np.int64).reshape(-1, 5),
+        "vgroups": np.array(vg, np.int64).reshape(-1, 2),
+        "vcells": np.concatenate(cells) if cells else np.empty(0, np.uint32),
+        "vrgba": np.concatenate(cols) if cols else np.empty(0, np.uint32),
+        "points": np.array(pts, np.int64).reshape(-1, 3),
+    }
+    for k, v in off.items():
+        out[k + "_off"] = np.array(v, np.int64)
+    return out
+
+
+def assert_same_deltas(got: dict, want: dict, what: str = "") -> None:
+    for k in DELTA_KEYS:
+        assert np.array_equal(np.asarray(got[k]), np.asarray(want[k])), f"{what}: delta {k} differs"
 
 
 def dense_fb(idx, val, n):

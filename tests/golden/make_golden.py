@@ -205,8 +205,70 @@ def sparse_fb(cells):
     return idx.astype(np.int64), cells[idx]
 
 
+DELTA_SCENARIOS = ("canonical", "canonical_1by1", "ten_points_spill", "depth_cap", "chunks_c50", "surface_253",
+                   "uniform_g16_c7", "skew_g8", "surface_g32_big_batches", "rebuild_bs333")
+
+
+def flatten_deltas(deltas) -> dict:
+    """BatchDelta list -> flat arrays: structure rows (kind 0 = split, 1 =
+    create; node, parent, octant, level), voxel groups (node, count) with the
+    concatenated cells / colours, point ranges (node, start, count); *_off
+    give each batch's rows."""
+    ev, vg, cells, cols, pts = [], [], [], [], []
+    off = {"ev": [0], "vg": [0], "vc": [0], "pt": [0]}
+    for d in deltas:
+        for e in d.structure:
+            ev.append([0, e[1], -1, -1, -1] if e[0] == "split" else [1, e[1], e[2], e[3], e[4]])
+        for node, c, r in d.voxels:
+            vg.append([node, len(c)])
+            cells.append(np.asarray(c, np.uint32))
+            cols.append(np.asarray(r, np.uint32))
+        for node, start, count in d.points:
+            pts.append([node, start, count])
+        off["ev"].append(len(ev))
+        off["vg"].append(len(vg))
+        off["vc"].append(sum(len(c) for c in cells))
+        off["pt"].append(len(pts))
+    out = {
+        "events": np.array(ev, np.int64).reshape(-1, 5),
+        "vgroups": np.array(vg, np.int64).reshape(-1, 2),
+        "vcells": np.concatenate(cells) if cells else np.empty(0, np.uint32),
+        "vrgba": np.concatenate(cols) if cols else np.empty(0, np.uint32),
+        "points": np.array(pts, np.int64).reshape(-1, 3),
+    }
+    for k, v in off.items():
+        out[k + "_off"] = np.array(v, np.int64)
+    return out
+
+
+def make_deltas(mods) -> None:
+    """deltas.npz: the reference's BatchDelta (insert_batch(collect_delta=True),
+    update.py:333-355) for every batch of the DELTA_SCENARIOS."""
+    octree, render, store, update, errors = mods
+    blob = {}
+    for name, params, batches in scenarios():
+        if name not in DELTA_SCENARIOS:
+            continue
+        arena = store.Arena(params["arena_bytes"])
+        pool = store.ChunkPool(arena, params["chunk_capacity"])
+        tree = octree.Octree(octree.CubeBounds(tuple(params["bmin"]), params["size"]), arena, pool,
+                             grid_res=params["grid_res"], leaf_threshold=params["leaf_threshold"],
+                             max_depth=params["max_depth"])
+        st = update.UpdateState(update.UpdateConfig(backlog_capacity=params["backlog_capacity"],
+                                                    spill_capacity=params["spill_capacity"]))
+        deltas = [update.insert_batch(tree, x, c, st, collect_delta=True) for x, c in batches]
+        for k, v in flatten_deltas(deltas).items():
+            blob[f"{name}__{k}"] = v
+    np.savez_compressed(os.path.join(HERE, "deltas.npz"), **blob)
+    print("deltas.npz:", ", ".join(DELTA_SCENARIOS))
+
+
 def main():
     mods = _import_ref()
+    if "--only-deltas" in sys.argv:
+        make_deltas(mods)
+        return
+    make_deltas(mods)
     octree, render, store, update, errors = mods
     manifest = {}
     for name, params, batches in scenarios():

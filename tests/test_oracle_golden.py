@@ -9,8 +9,8 @@ import pytest
 
 import oracle
 from oracle import rebuild
-from common import (assert_same_state, dense_fb, golden_names, load_golden, load_raster, oracle_state,
-                    run_oracle)
+from common import (assert_same_deltas, assert_same_state, delta_names, dense_fb, flatten_deltas, golden_names,
+                    load_deltas, load_golden, load_raster, oracle_state, run_oracle)
 
 
 @pytest.mark.parametrize("name", golden_names())
@@ -71,3 +71,16 @@ def test_oracle_matches_topdown_rebuild(name):
         occupied_cells = staticmethod(t.occupied_cells)
 
     rebuild.assert_matches_reference(View(), ref)
+
+
+@pytest.mark.parametrize("name", delta_names())
+def test_oracle_delta_matches_reference_fixture(name):
+    """BatchDelta restatement (update.py:333-355) vs the reference's own deltas."""
+    g = load_golden(name)
+    p = g["params"]
+    t = oracle.OracleTree(p["bmin"], p["size"], grid_res=p["grid_res"], leaf_threshold=p["leaf_threshold"],
+                          max_depth=p["max_depth"], chunk_capacity=p["chunk_capacity"],
+                          arena_bytes=p["arena_bytes"], backlog_capacity=p["backlog_capacity"],
+                          spill_capacity=p["spill_capacity"])
+    deltas = [t.insert_batch(x, c, collect_delta=True)["delta"] for x, c in g["batches"]]
+    assert_same_deltas(flatten_deltas(deltas), load_deltas(name), name)

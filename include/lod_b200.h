@@ -165,6 +165,21 @@ int lod_tree_unpack(LodTree *tree, const void *dev_buf, uint64_t bytes);
 int lod_rasterize(LodTree *tree, const int32_t *vis, int64_t nvis, const double *cam,
                   uint64_t *fb, int64_t width, int64_t height, int flags, int64_t *samples);
 
+/* render.select_visible (render.py:177-200) on the device: the depth-first,
+ * octant-ordered cut of nodes to draw.  planes = frustum_planes(camera)
+ * (6 x (normal, d), render.py:127-148, computed by the caller like the
+ * reference), cam = Camera.packed().  `selected` (host, capacity >= num_nodes)
+ * receives the node ids in the reference's visit order; *n_selected their count. */
+int lod_select_visible(LodTree *tree, const double *planes, const double *cam, double threshold,
+                       int32_t *selected, int64_t capacity, int64_t *n_selected);
+
+/* render.rasterize (render.py:213-225) in one call: device selection as in
+ * lod_select_visible, then the chunk splat of lod_rasterize into fb (host
+ * pointer, or device with LOD_FLAG_DEVICE_FB).  `selected` may be NULL. */
+int lod_render(LodTree *tree, const double *planes, const double *cam, double threshold, uint64_t *fb,
+               int64_t width, int64_t height, int flags, int32_t *selected, int64_t capacity,
+               int64_t *n_selected, int64_t *samples);
+
 /* _kernels.rasterize_points via render.brute_force_render (_kernels.py:342-372,
  * render.py:228-239).  device selects the GPU when no tree is involved. */
 int lod_raster_points(int32_t device, const float *xyz, const uint32_t *rgba, int64_t n,

@@ -112,6 +112,9 @@ SIGNATURES = {
     "lod_read_delta": (ctypes.c_int, [_P] + [_P] * 9),
     "lod_read_arena": (ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     "lod_rasterize": (ctypes.c_int, [_P, _P, _I64, _P, _P, _I64, _I64, ctypes.c_int, ctypes.POINTER(_I64)]),
+    "lod_select_visible": (ctypes.c_int, [_P, _P, _P, ctypes.c_double, _P, _I64, ctypes.POINTER(_I64)]),
+    "lod_render": (ctypes.c_int, [_P, _P, _P, ctypes.c_double, _P, _I64, _I64, ctypes.c_int, _P, _I64,
+                                  ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "lod_raster_points": (ctypes.c_int, [ctypes.c_int32, _P, _P, _I64, _P, _P, _I64, _I64, ctypes.c_int]),
     "lod_device_alloc": (ctypes.c_int, [ctypes.c_int32, ctypes.c_uint64, ctypes.POINTER(_P)]),
     "lod_device_free": (ctypes.c_int, [_P]),

@@ -14,6 +14,7 @@
 
 #include "../../include/lod_b200.h"
 #include "lod_common.cuh"
+#include "scan.cuh"
 
 using namespace lod;
 
@@ -28,6 +29,9 @@ uint32_t *lod_tree_visflag(LodTree *t);
 int lod_tree_ensure_vislist(LodTree *t, long long n, int32_t **p);
 int lod_tree_ensure_fb(LodTree *t, long long n, unsigned long long **p);
 unsigned long long *lod_tree_counter(LodTree *t);
+NodeCols lod_tree_nodes(LodTree *t);
+Geo lod_tree_geo(LodTree *t);
+int lod_tree_ensure_sel(LodTree *t, long long n, int32_t **a, int32_t **b);
 
 namespace {
 
@@ -91,6 +95,126 @@ __global__ void k_set_vis(const int32_t *__restrict__ vis, long long n, uint32_t
     if (add) atomicAdd(visflag + vis[i], 1u);
     else visflag[vis[i]] = 0;
   }
+}
+
+// ---------------------------------------------------------------- selection
+
+// select_visible (render.py:177-200) on the device.  The reference walks a
+// stack depth-first (octant order) and emits every node where the walk stops:
+// outside the frustum -> dropped, inner and projecting larger than the pixel
+// threshold -> refined into its 8 children, else -> drawn.  Here one CTA keeps
+// the whole cut as an ordered list and refines it level by level: every
+// pending entry is replaced in place by 0 (culled), 1 (drawn, final) or 8
+// (its children, pending) entries, with a block scan placing them.  Replacing
+// an entry by its children in octant order keeps the list in depth-first
+// order, so the final list is the reference's visit order.  The plane and
+// projection arithmetic is the reference's per corner, in f64 without FMA
+// (frustum_intersects render.py:151-157, screen_size render.py:160-174).
+struct SelParams {
+  double planes[24];  // frustum_planes(camera): (normal, d) x 6, host-computed like the reference
+  double cam[18];     // Camera.packed()
+  double threshold;
+};
+
+__device__ __forceinline__ int sel_decide(const NodeCols &nd, const Geo &geo, const SelParams &sp, int nid) {
+  const double s = geo.size_by_level[nd.level[nid]];
+  const double b0 = nd.bmin[3 * nid], b1 = nd.bmin[3 * nid + 1], b2 = nd.bmin[3 * nid + 2];
+  double cx[8], cy[8], cz[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {  // CubeBounds.corners(): corner i at octant offset i
+    cx[i] = b0 + ((i & 1) ? s : 0.0);
+    cy[i] = b1 + ((i & 2) ? s : 0.0);
+    cz[i] = b2 + ((i & 4) ? s : 0.0);
+  }
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const double *pl = sp.planes + 4 * k;
+    bool all_out = true;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) all_out &= (cx[i] * pl[0] + cy[i] * pl[1] + cz[i] * pl[2] + pl[3] < 0.0);
+    if (all_out) return 0;
+  }
+  if (!nd.inner[nid]) return 1;
+  const double *c = sp.cam;
+  double sxmin = 0, sxmax = 0, symin = 0, symax = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const double dx = cx[i] - c[0], dy = cy[i] - c[1], dz = cz[i] - c[2];
+    const double zv = dx * c[9] + dy * c[10] + dz * c[11];
+    if (zv <= c[14]) return ((double)INFINITY > sp.threshold) ? 8 : 1;  // screen_size = inf
+    const double sx = ((dx * c[3] + dy * c[4] + dz * c[5]) / (zv * c[12] * c[13]) + 1.0) * 0.5 * c[16];
+    const double sy = (1.0 - (dx * c[6] + dy * c[7] + dz * c[8]) / (zv * c[12])) * 0.5 * c[17];
+    if (i == 0) {
+      sxmin = sxmax = sx;
+      symin = symax = sy;
+    } else {
+      sxmin = fmin(sxmin, sx);
+      sxmax = fmax(sxmax, sx);
+      symin = fmin(symin, sy);
+      symax = fmax(symax, sy);
+    }
+  }
+  const double size = fmax(sxmax - sxmin, symax - symin);
+  return size > sp.threshold ? 8 : 1;
+}
+
+constexpr int kSelBlock = 1024;
+// Entries: nid >= 0 pending, -(nid + 1) final.  Result: the final list of
+// node ids in *out_list (one of the two buffers), its length in *nsel; with
+// `mark`, every selected node's visflag is set for the chunk rasterizer.
+__global__ void __launch_bounds__(kSelBlock)
+    k_select(NodeCols nd, Geo geo, SelParams sp, int32_t *bufA, int32_t *bufB, int32_t *sel_out,
+             unsigned long long *nsel, uint32_t *visflag, int mark) { lod::pdl_wait();
+  __shared__ uint32_t sh[kSelBlock / 32 + 1];
+  __shared__ int s_expanded;
+  int32_t *cur = bufA, *nxt = bufB;
+  long long n = 1;
+  if (!nd.inner[0] && nd.count[0] == 0) n = 0;  // a tree holding nothing selects nothing
+  if (threadIdx.x == 0) cur[0] = 0;
+  __syncthreads();
+  for (;;) {
+    if (threadIdx.x == 0) s_expanded = 0;
+    __syncthreads();
+    long long carry = 0;
+    for (long long base = 0; base < n; base += kSelBlock) {
+      const long long i = base + threadIdx.x;
+      int item = 0, k = 0;
+      if (i < n) {
+        item = cur[i];
+        k = item < 0 ? 1 : sel_decide(nd, geo, sp, item);
+      }
+      uint32_t tot;
+      const uint32_t ex = block_exclusive_scan<uint32_t, kSelBlock>((uint32_t)k, sh, tot);
+      const long long o = carry + ex;
+      if (k == 1) {
+        nxt[o] = item < 0 ? item : -(item + 1);
+      } else if (k == 8) {
+        s_expanded = 1;
+        const int c0 = nd.desc[item].x;  // children are 8 consecutive ids, octant order
+#pragma unroll
+        for (int q = 0; q < 8; ++q) nxt[o + q] = c0 + q;
+      }
+      carry += tot;
+    }
+    __syncthreads();
+    n = carry;
+    int32_t *t = cur;
+    cur = nxt;
+    nxt = t;
+    if (!s_expanded) break;
+  }
+  for (long long i = threadIdx.x; i < n; i += kSelBlock) {
+    const int nid = -cur[i] - 1;
+    sel_out[i] = nid;
+    if (mark) visflag[nid] = 1;
+  }
+  if (threadIdx.x == 0) *nsel = (unsigned long long)n;
+}
+
+__global__ void k_clear_vis(const int32_t *__restrict__ sel, const unsigned long long *__restrict__ nsel,
+                            uint32_t *visflag) { lod::pdl_wait();
+  const long long n = (long long)*nsel;
+  for (long long i = gtid(); i < n; i += gstride()) visflag[sel[i]] = 0;
 }
 
 __global__ void k_fill_u64(unsigned long long *p, long long n, unsigned long long v) { lod::pdl_wait();
@@ -166,6 +290,66 @@ int lod_rasterize(LodTree *t, const int32_t *vis, int64_t nvis, const double *ca
   CK(cudaStreamSynchronize(st));
   if (samples) *samples = (int64_t)drawn;
   return LOD_OK;
+}
+
+// select_visible on the device (+ optional splat of the selection): one
+// selection kernel, one flat chunk pass, one D2H of (count, list, framebuffer).
+static int render_impl(LodTree *t, const double *planes, const double *cam, double threshold, uint64_t *fb,
+                       int64_t width, int64_t height, int flags, int32_t *selected, int64_t capacity,
+                       int64_t *n_selected, int64_t *samples) {
+  if (!t || !planes || !cam || (fb && (width <= 0 || height <= 0))) return LOD_E_ARG;
+  const long long nn = lod_tree_num_nodes(t);
+  if (selected && capacity < nn) return LOD_E_ARG;
+  cudaSetDevice(lod_tree_device(t));
+  cudaStream_t st = lod_tree_stream(t);
+  SelParams sp;
+  memcpy(sp.planes, planes, sizeof(sp.planes));
+  memcpy(sp.cam, cam, sizeof(sp.cam));
+  sp.threshold = threshold;
+  int32_t *la = nullptr, *lb = nullptr;
+  int rc = lod_tree_ensure_sel(t, nn, &la, &lb);
+  if (rc) return rc;
+  unsigned long long *cnt = lod_tree_counter(t);  // [0] samples, [1] selected
+  CK(cudaMemsetAsync(cnt, 0, 16, st));
+  uint32_t *vf = lod_tree_visflag(t);
+  int32_t *sel = la;  // k_select decodes the final list into la[0, n) (same index as it reads)
+  unsigned long long *dfb = reinterpret_cast<unsigned long long *>(fb);
+  const long long npx = fb ? width * height : 0;
+  if (fb && !(flags & LOD_FLAG_DEVICE_FB)) {
+    rc = lod_tree_ensure_fb(t, npx, &dfb);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(dfb, fb, npx * 8, cudaMemcpyHostToDevice, st));
+  }
+  lod::launch(k_select, 1, kSelBlock, 0, st, lod_tree_nodes(t), lod_tree_geo(t), sp, la, lb, sel, cnt + 1, vf,
+              fb ? 1 : 0);
+  if (fb) {
+    Cam c;
+    memcpy(c.c, cam, sizeof(c.c));
+    const long long nchunks = lod_tree_allocated(t);
+    lod::launch(k_raster_chunks, grid_for(nchunks * 32), 256, 0, st, lod_tree_pool(t), lod_tree_arena(t), nchunks, vf,
+                c, dfb, width, height, cnt);
+    lod::launch(k_clear_vis, grid_for(nn), 256, 0, st, sel, cnt + 1, vf);
+  }
+  unsigned long long h[2] = {0, 0};
+  CK(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, st));
+  if (fb && !(flags & LOD_FLAG_DEVICE_FB)) CK(cudaMemcpyAsync(fb, dfb, npx * 8, cudaMemcpyDeviceToHost, st));
+  if (selected) CK(cudaMemcpyAsync(selected, sel, nn * 4, cudaMemcpyDeviceToHost, st));  // list <= num_nodes
+  CK(cudaStreamSynchronize(st));
+  if (n_selected) *n_selected = (int64_t)h[1];
+  if (samples) *samples = (int64_t)h[0];
+  return LOD_OK;
+}
+
+int lod_select_visible(LodTree *t, const double *planes, const double *cam, double threshold, int32_t *selected,
+                       int64_t capacity, int64_t *n_selected) {
+  return render_impl(t, planes, cam, threshold, nullptr, 0, 0, 0, selected, capacity, n_selected, nullptr);
+}
+
+int lod_render(LodTree *t, const double *planes, const double *cam, double threshold, uint64_t *fb, int64_t width,
+               int64_t height, int flags, int32_t *selected, int64_t capacity, int64_t *n_selected,
+               int64_t *samples) {
+  if (!fb) return LOD_E_ARG;
+  return render_impl(t, planes, cam, threshold, fb, width, height, flags, selected, capacity, n_selected, samples);
 }
 
 int lod_raster_points(int32_t device, const float *xyz, const uint32_t *rgba, int64_t n, const double *cam,

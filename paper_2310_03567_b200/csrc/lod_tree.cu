@@ -995,6 +995,16 @@ int lod_tree_ensure_fb(LodTree *t, long long n, unsigned long long **p) {
   return rc;
 }
 unsigned long long *lod_tree_counter(LodTree *t) { return t->counter.p; }
+NodeCols lod_tree_nodes(LodTree *t) { return t->nd; }
+Geo lod_tree_geo(LodTree *t) { return t->geo; }
+// two ping-pong selection lists of num_nodes entries each (the cut never
+// holds a node twice, so num_nodes bounds every list)
+int lod_tree_ensure_sel(LodTree *t, long long n, int32_t **a, int32_t **b) {
+  int rc = t->vislist.ensure(std::max<long long>(2 * n, 2), t->st);
+  *a = t->vislist.p;
+  *b = t->vislist.p + std::max<long long>(n, 1);
+  return rc;
+}
 
 // ---------------------------------------------------------------- replication
 

@@ -121,3 +121,71 @@ def test_full_refinement_equals_brute_force_many_scenes(gpu):
         ofb = np.full(256 * 256, np.uint64(0xFFFFFFFFFFFFFFFF))
         oracle.rasterize_points(xyz, rgba, cam.packed(), ofb)
         assert np.array_equal(ofb, fb.cells)
+
+
+def _cols(tree):
+    return {k: getattr(tree, k) for k in ("inner", "count", "children", "bmin", "level")}
+
+
+def _random_cameras(rng, k):
+    from paper_2310_03567_b200.render import Camera
+
+    cams = []
+    for _ in range(k):
+        target = rng.uniform(0.2, 0.8, 3)
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        pos = target + d * rng.uniform(0.15, 2.5)
+        cams.append(Camera(tuple(pos), tuple(target), fov_deg=float(rng.uniform(40, 100)), near=0.01,
+                           far=float(rng.uniform(2.0, 50.0)), width=int(rng.integers(200, 1400)),
+                           height=int(rng.integers(150, 1000))))
+    return cams
+
+
+def test_device_selection_matches_host_restatement(gpu):
+    """select_visible on the GPU vs the reference's stack walk (oracle/select.py)
+    on a terrain tree, 24 random cameras x 4 thresholds; a differing node must be
+    a float-order tie (decision margin < 1e-9), which none of these cameras hit."""
+    from oracle import select as osel
+    from paper_2310_03567_b200 import insert_batch, synth
+    from paper_2310_03567_b200.render import rasterize, select_visible
+
+    import oracle
+
+    params = dict(bmin=(0.0, 0.0, 0.0), size=1.0, arena_bytes=1 << 30, chunk_capacity=500, grid_res=32,
+                  leaf_threshold=2000, max_depth=14, backlog_capacity=10_000_000, spill_capacity=100_000_000)
+    tree, state = make_product(params)
+    ot = oracle.OracleTree(grid_res=32, leaf_threshold=2000, max_depth=14, chunk_capacity=500, arena_bytes=1 << 30)
+    for i in range(4):
+        xyz, rgba = synth.gen_surface(100_000, 50 + i)
+        insert_batch(tree, xyz, rgba, state)
+        ot.insert_batch(xyz, rgba)
+    cols = _cols(tree)
+    rng = np.random.default_rng(7)
+    for cam in _random_cameras(rng, 24):
+        for thr in (-1.0, 32.0, 128.0, 700.0):
+            want = osel.select_visible(cols, 1.0, cam, thr)
+            got = select_visible(tree, cam, thr)
+            if got != want:
+                diff = sorted(set(got) ^ set(want))
+                m = osel.decision_margins(cols, 1.0, cam, thr, diff)
+                assert all(min(v) < 1e-9 for v in m.values()), (thr, m)
+                continue
+            fb, rep = rasterize(tree, cam, threshold=thr)
+            assert rep.selected == want
+            from paper_2310_03567_b200.render import Framebuffer
+
+            ofb = Framebuffer(cam.width, cam.height)
+            assert rep.samples_drawn == ot.rasterize_nodes(want, cam.packed(), ofb.cells)
+            assert np.array_equal(fb.cells, ofb.cells)
+
+
+def test_empty_tree_selects_nothing(gpu):
+    from paper_2310_03567_b200.render import Camera, rasterize, select_visible
+
+    tree, _ = make_product(dict(bmin=(0.0, 0.0, 0.0), size=1.0, arena_bytes=1 << 20, chunk_capacity=10,
+                                grid_res=4, leaf_threshold=10, max_depth=4, backlog_capacity=10, spill_capacity=10))
+    cam = Camera(**FRONT)
+    assert select_visible(tree, cam) == []
+    fb, rep = rasterize(tree, cam)
+    assert rep.selected == [] and rep.samples_drawn == 0

@@ -10,8 +10,11 @@ T=50,000, C=1,000, G=128, max depth 20); W + K batches = the stream prefix.
 * ``value``: Mpts/s = K * 1M / (device time of the K timed steps), inputs
   already resident in HBM (CUDA tensors), timed with CUDA events bracketed by
   barrier + synchronize, max over ranks.
-* ``e2e``: the same metric through the public API with the batch in pinned
-  host memory -- H2D copy + update + result read-back inside the timed region.
+* ``e2e``: the same metric through the public API a user streams with: the
+  reference's frame loop (``run_frame_updates`` over a queue of host batches
+  in pinned memory, 10 ms budget, cli._build) -- every batch's H2D copy (the
+  ingest feed stages batch k+1 while batch k updates) + update + control-block
+  read-backs inside the timed region.
 * ``roofline``: the dominant phase of the update (per-phase CUDA events on the
   tree stream in a profiled replay), algorithmic bytes / time vs measured HBM.
 * ``cpu_baseline``: the C oracle (a 1-thread port of the reference's
@@ -26,6 +29,8 @@ stream; ``value`` = all ranks' points / max-over-ranks time ("scaling": "weak").
 from __future__ import annotations
 
 import argparse
+import collections
+import dataclasses
 import json
 import os
 import statistics
@@ -217,7 +222,7 @@ def gen_stripe(kind: str, step: int, rank: int):
 def run_ours(args, rank, world, local_rank):
     import torch
 
-    from paper_2310_03567_b200 import insert_batch
+    from paper_2310_03567_b200 import insert_batch, run_frame_updates
 
     if world > 1:
         return run_multi(args, rank, world, local_rank)
@@ -245,28 +250,36 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def timed_stream(inputs, profile=False):
+    def timed_stream(inputs, profile=False, frames=False):
+        """Device-resident batches one insert_batch per step, or (frames=True)
+        host batches through the frame loop a user runs (cli._build:
+        run_frame_updates over a queue, 10 ms budget, ingest feed overlapped)."""
         tree, state = new_tree(dev, arena_bytes)
         per, launches, phases = [], 0, []
         h2d = d2h = 0
         for i in range(args.warmup):
             insert_batch(tree, *inputs[i], state)
         barrier()
+        s0 = dataclasses.replace(state.stats)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for i in range(args.warmup, total):
-            insert_batch(tree, *inputs[i], state, profile=profile)
-            b = state._bstats
-            per.append(float(b.device_ms))
-            launches += int(b.launches)
-            h2d += int(b.h2d_bytes)
-            d2h += int(b.d2h_bytes)
-            if profile:
-                ph = dict(state.last["phase_ms"])
-                ph["_counts"] = (int(b.n_batch), int(b.n_spill), int(b.n_voxels))
-                phases.append(ph)
+        if frames:
+            q = collections.deque(inputs[args.warmup:total])
+            while q:
+                run_frame_updates(tree, q, state)
+        else:
+            for i in range(args.warmup, total):
+                insert_batch(tree, *inputs[i], state, profile=profile)
+                b = state._bstats
+                per.append(float(b.device_ms))
+                if profile:
+                    ph = dict(state.last["phase_ms"])
+                    ph["_counts"] = (int(b.n_batch), int(b.n_spill), int(b.n_voxels))
+                    phases.append(ph)
         e1.record()
         barrier()
+        st = state.stats
+        launches, h2d, d2h = st.launches - s0.launches, st.h2d_bytes - s0.h2d_bytes, st.d2h_bytes - s0.d2h_bytes
         ms = e0.elapsed_time(e1)
         info = dict(nodes=tree.num_nodes, points=tree.total_points() if args.steps <= 200 else None,
                     voxels_created=state.stats.voxels_created, arena=tree.arena.offset)
@@ -275,7 +288,7 @@ def run_ours(args, rank, world, local_rank):
 
     with ClockSampler(dev) as clocks:
         ms, per, launches, _, info, _ = timed_stream(dev_b)
-    ms_e2e, per_e2e, _, _, _, (h2d, d2h) = timed_stream(pin_b)
+    ms_e2e, per_e2e, _, _, _, (h2d, d2h) = timed_stream(pin_b, frames=True)
     # profiled replay: per-phase CUDA events on the tree stream + per-batch B_alg inputs
     _, per_prof, _, phases, _, _ = timed_stream(dev_b, profile=True)
 

@@ -110,6 +110,17 @@ int lod_tree_info(LodTree *tree, LodTreeInfo *info);
 int lod_insert_batch(LodTree *tree, const float *xyz, const uint32_t *rgba, int64_t n,
                      const LodLimits *limits, int flags, LodBatchStats *stats);
 
+/* Ingest feed (the reference's BatchSource queue feeding
+ * run_frame_updates, io.py:340-413, update.py:396-417): start the H2D copy of
+ * a batch in PAGE-LOCKED host memory on the tree's copy stream, double-
+ * buffered, so it overlaps the update running ahead of it.  A later
+ * lod_insert_batch with the same (xyz, rgba, n) consumes the staged copy
+ * instead of copying.  Pageable memory is ignored (the insert copies it).
+ * The caller keeps the host arrays unchanged until that insert, or until
+ * lod_prefetch_drain (waits for outstanding copies, drops unused stages). */
+int lod_prefetch_batch(LodTree *tree, const float *xyz, const uint32_t *rgba, int64_t n);
+int lod_prefetch_drain(LodTree *tree);
+
 /* D2H mirror of the node table columns (octree.py:169-182), rows [0, n).
  * Any pointer may be NULL to skip that column. children is (n,8), bmin (n,3). */
 int lod_read_nodes(LodTree *tree, int64_t n, int32_t *parent, uint8_t *octant, int32_t *level,

@@ -104,6 +104,8 @@ SIGNATURES = {
     "lod_tree_info": (ctypes.c_int, [_P, ctypes.POINTER(LodTreeInfo)]),
     "lod_insert_batch": (ctypes.c_int, [_P, _P, _P, _I64, ctypes.POINTER(LodLimits), ctypes.c_int,
                                         ctypes.POINTER(LodBatchStats)]),
+    "lod_prefetch_batch": (ctypes.c_int, [_P, _P, _P, _I64]),
+    "lod_prefetch_drain": (ctypes.c_int, [_P]),
     "lod_read_nodes": (ctypes.c_int, [_P, _I64] + [_P] * 13),
     "lod_read_pool": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _I64]),
     "lod_gather": (ctypes.c_int, [_P, _I64, _I64, _P, _P]),

@@ -197,6 +197,18 @@ struct LodTree {
   DBuf<long long> dvstart, dvcount, dpstart, dpcount, dvbase;
   DBuf<uint32_t> dvcell, dvrgba;
   long long d_nsplits = 0, d_nvg = 0, d_npg = 0, d_nv = 0;
+  // ingest feed: batches staged H2D on a copy stream ahead of their insert
+  // (lod_prefetch_batch), double-buffered
+  cudaStream_t cst = nullptr;
+  struct Stage {
+    DBuf<float> xyz;
+    DBuf<uint32_t> rgba;
+    const void *hx = nullptr, *hc = nullptr;
+    long long n = 0;
+    bool valid = false;
+    cudaEvent_t ready = nullptr;
+  } stage[2];
+  int stage_next = 0;
   cudaEvent_t ev[14] = {};  // 12, 13: per-iteration k_count brackets
   // host copies of counters (authoritative after every call)
   long long num_nodes = 1;
@@ -473,6 +485,15 @@ int lod_tree_destroy(LodTree *t) {
   t->plan.release(); t->plan_ex.release(); t->scan_u64x2.release(); t->in_xyz.release();
   t->in_rgba.release(); t->gbuf.release(); t->gnodes.release(); t->goff.release(); t->gstart.release();
   t->visflag.release(); t->vislist.release(); t->fb.release(); t->counter.release();
+  t->dsplits.release(); t->dvnode.release(); t->dpnode.release(); t->dvstart.release(); t->dvcount.release();
+  t->dpstart.release(); t->dpcount.release(); t->dvbase.release(); t->dvcell.release(); t->dvrgba.release();
+  if (t->cst) cudaStreamSynchronize(t->cst);
+  for (auto &sg : t->stage) {
+    sg.xyz.release();
+    sg.rgba.release();
+    if (sg.ready) cudaEventDestroy(sg.ready);
+  }
+  if (t->cst) cudaStreamDestroy(t->cst);
   for (auto &e : t->ev) if (e) cudaEventDestroy(e);
   cudaStreamDestroy(t->st);
   delete t;
@@ -540,7 +561,17 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   // ---- inputs
   const float *bx = xyz;
   const uint32_t *bc = rgba;
+  LodTree::Stage *staged = nullptr;
   if (!(flags & LOD_FLAG_DEVICE_INPUT)) {
+    for (auto &sg : t->stage)
+      if (sg.valid && sg.hx == xyz && sg.hc == rgba && sg.n == n) staged = &sg;
+  }
+  if (staged) {  // prefetched on the copy stream: wait for it, no copy here
+    CK(cudaStreamWaitEvent(st, staged->ready, 0));
+    staged->valid = false;
+    bx = staged->xyz.p;
+    bc = staged->rgba.p;
+  } else if (!(flags & LOD_FLAG_DEVICE_INPUT)) {
     RK(t->in_xyz.ensure(3 * n, st));
     RK(t->in_rgba.ensure(n, st));
     CK(cudaMemcpyAsync(t->in_xyz.p, xyz, (size_t)n * 12, cudaMemcpyHostToDevice, st));
@@ -937,6 +968,49 @@ int lod_read_arena(LodTree *t, uint64_t off, uint64_t size, void *dst) {
 }
 
 }  // extern "C"
+
+int lod_prefetch_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t n) {
+  if (!t || n < 0 || (n > 0 && (!xyz || !rgba))) return LOD_E_ARG;
+  if (n == 0) return LOD_OK;
+  // only page-locked host memory can be copied asynchronously; anything else
+  // is left to lod_insert_batch's own copy
+  cudaPointerAttributes ax{}, ac{};
+  if (cudaPointerGetAttributes(&ax, xyz) != cudaSuccess || cudaPointerGetAttributes(&ac, rgba) != cudaSuccess) {
+    cudaGetLastError();
+    return LOD_OK;
+  }
+  if (ax.type != cudaMemoryTypeHost || ac.type != cudaMemoryTypeHost) return LOD_OK;
+  cudaSetDevice(t->dev);
+  if (!t->cst) {
+    CK(cudaStreamCreateWithFlags(&t->cst, cudaStreamNonBlocking));
+    for (auto &sg : t->stage) CK(cudaEventCreateWithFlags(&sg.ready, cudaEventDisableTiming));
+  }
+  for (auto &sg : t->stage)
+    if (sg.valid && sg.hx == xyz && sg.hc == rgba && sg.n == n) return LOD_OK;  // already staged
+  LodTree::Stage &sg = t->stage[t->stage_next];
+  t->stage_next ^= 1;
+  // the slot's previous batch was consumed by a completed insert (every
+  // lod_insert_batch returns after its update finished), or is superseded
+  RK(sg.xyz.ensure(3 * n, t->cst));
+  RK(sg.rgba.ensure(n, t->cst));
+  CK(cudaMemcpyAsync(sg.xyz.p, xyz, (size_t)n * 12, cudaMemcpyHostToDevice, t->cst));
+  CK(cudaMemcpyAsync(sg.rgba.p, rgba, (size_t)n * 4, cudaMemcpyHostToDevice, t->cst));
+  CK(cudaEventRecord(sg.ready, t->cst));
+  sg.hx = xyz;
+  sg.hc = rgba;
+  sg.n = n;
+  sg.valid = true;
+  return LOD_OK;
+}
+
+int lod_prefetch_drain(LodTree *t) {
+  if (!t) return LOD_E_ARG;
+  if (!t->cst) return LOD_OK;
+  cudaSetDevice(t->dev);
+  CK(cudaStreamSynchronize(t->cst));
+  for (auto &sg : t->stage) sg.valid = false;
+  return LOD_OK;
+}
 
 int lod_delta_info(LodTree *t, LodDeltaInfo *info) {
   if (!t || !info) return LOD_E_ARG;

@@ -60,6 +60,9 @@ class UpdateStats:
     backlog_high_water: int = 0
     spill_high_water: int = 0
     device_seconds: float = 0.0  # CUDA-event time of the update kernels (B200 extra)
+    launches: int = 0  # kernels launched by the updates (B200 extra)
+    h2d_bytes: int = 0  # host->device bytes copied by the updates (B200 extra)
+    d2h_bytes: int = 0  # device->host bytes read back by the updates (B200 extra)
 
     def throughput_mps(self) -> float:
         """Million points ingested per update-second (update.py:82-86)."""
@@ -202,6 +205,9 @@ def insert_batch(
     st.splits = int(bs.splits_total)
     st.nodes = int(bs.num_nodes)
     st.device_seconds += float(bs.device_ms) * 1e-3
+    st.launches += int(bs.launches)
+    st.h2d_bytes += int(bs.h2d_bytes)
+    st.d2h_bytes += int(bs.d2h_bytes)
     if profile:
         state.last = bs.as_dict()
     else:
@@ -241,16 +247,43 @@ def _read_delta(tree: Octree) -> BatchDelta:
     return d
 
 
+def _prefetch(tree: Octree, batch) -> bool:
+    """Stage a queued host batch H2D on the tree's copy stream (the ingest
+    feed, lod_prefetch_batch) when its arrays are used in place by
+    insert_batch (C-contiguous float32 (n,3) / uint32); page-locked memory
+    overlaps with the running update, anything else is left to the insert."""
+    xyz, rgba = batch
+    if not (isinstance(xyz, np.ndarray) and isinstance(rgba, np.ndarray)):
+        return False
+    if (xyz.dtype != np.float32 or rgba.dtype != np.uint32 or not xyz.flags.c_contiguous
+            or not rgba.flags.c_contiguous or xyz.ndim != 2 or xyz.shape[1] != 3 or len(rgba) != len(xyz)
+            or len(rgba) == 0):
+        return False
+    _lib.check(tree._L.lod_prefetch_batch(tree.handle, _lib.ptr(xyz), _lib.ptr(rgba), len(rgba)), "prefetch")
+    return True
+
+
 def run_frame_updates(tree, batches, state: UpdateState, on_delta=None) -> int:
-    """Drain queued batches for one frame within the budget (update.py:396-417)."""
+    """Drain queued batches for one frame within the budget (update.py:396-417).
+
+    The budget is checked between batches, as in the reference.  While batch
+    k updates, batch k+1's H2D copy is already running on the copy stream
+    (pinned host batches), so the queue streams at the update rate."""
     state.clock.restart()
     processed = 0
-    while batches and (processed == 0 or not state.clock.exceeded()):
-        xyz, rgba = batches.popleft()
-        delta = insert_batch(tree, xyz, rgba, state, collect_delta=on_delta is not None)
-        if on_delta is not None:
-            on_delta(delta)
-        processed += 1
+    staged = False
+    try:
+        while batches and (processed == 0 or not state.clock.exceeded()):
+            xyz, rgba = batches.popleft()
+            if batches:
+                staged = _prefetch(tree, batches[0]) or staged
+            delta = insert_batch(tree, xyz, rgba, state, collect_delta=on_delta is not None)
+            if on_delta is not None:
+                on_delta(delta)
+            processed += 1
+    finally:
+        if staged:  # the caller owns the queued arrays again
+            tree._L.lod_prefetch_drain(tree.handle)
     if processed:
         st = state.stats
         st.frames += 1

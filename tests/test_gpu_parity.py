@@ -166,3 +166,35 @@ def test_conservation_and_placement(gpu):
                 (lx[:, 2] >= cx[2]).astype(np.int8) << 2)
             assert (o == int(tree.octant[nid])).all()
             nid = par
+
+
+def test_frame_loop_with_pinned_ingest_feed_matches_oracle(gpu):
+    """run_frame_updates over page-locked batches (the staged H2D feed,
+    lod_prefetch_batch) settles the same tree as the oracle; frames follow
+    the reference's budget rule."""
+    from collections import deque
+
+    import torch
+
+    from paper_2310_03567_b200 import run_frame_updates
+
+    params = _params(arena_bytes=1 << 30, grid_res=64, leaf_threshold=3000, max_depth=16, chunk_capacity=500)
+    xyz, rgba = _cloud(400_000, 11, "surface")
+    bs = 40_000
+    batches = [(xyz[i:i + bs], rgba[i:i + bs]) for i in range(0, len(rgba), bs)]
+    pinned = []
+    for x, c in batches:
+        px = torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
+        pc = torch.from_numpy(np.ascontiguousarray(c).view(np.int32)).pin_memory().numpy().view(np.uint32)
+        pinned.append((px, pc))
+    ot, _, oper = run_oracle(params, batches)
+    tree, state = make_product(params)
+    q = deque(pinned)
+    frames = 0
+    while q:
+        assert run_frame_updates(tree, q, state) >= 1
+        frames += 1
+    assert state.stats.frames == frames and state.stats.batches == len(batches)
+    assert state.stats.h2d_bytes == 16 * len(rgba)
+    assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label="frame_loop")
+    _hygiene(tree, state)

@@ -530,52 +530,50 @@ __global__ void k_claim(NodeCols nd, Geo geo, PointSrc src, const uint32_t *__re
   used_flush(h, stg, ctrl);
 }
 
-// Every distinct claimed (node, cell): the min index is the winner.  Set the
-// bit, record the win at the node's level for the winner, and free the slot.
-__global__ void k_resolve(NodeCols nd, Hash h, uint32_t *grid32, long long n_s, int D,
-                          unsigned long long *__restrict__ wins, unsigned long long *__restrict__ wmask,
-                          const Ctrl *ctrl) { lod::pdl_wait();
-  unsigned long long nu = ctrl->n_used;
-  if (nu > h.limit) nu = h.limit;
-  for (long long u = gtid(); u < (long long)nu; u += gstride()) {
-    HSlot *sl = h.slots + h.used[u];
-    const unsigned long long key = sl->key;
-    const uint32_t v = sl->val;
-    *reinterpret_cast<ulonglong2 *>(sl) = make_ulonglong2(kEmptyKey, kEmptyHi);
-    const int nid = (int)(key >> 32);
-    const long long cell = (long long)(key & 0xFFFFFFFFu);
-    const long long j = (v & kBatchTag) ? n_s + (long long)(v & ~kBatchTag) : (long long)v;
-    const int lvl = nd.level[nid];
+// Every distinct claimed (node, cell): the min index is the winner.  Two
+// sequential sweeps of the claim table (every sector read once, coalesced;
+// a table larger than L2 costs a streaming read, not a DRAM round trip per
+// voxel, and no list or cursor is needed):
+//   k_resolve: set the cell's bit and take a rank among the winner's wins
+//     (atomicAdd on the per-point win count), kept in the slot's pad word;
+//   k_scatter (after the exclusive scan wbase of the win counts): write the
+//     backlog entry at wbase[j] + rank and free the slot.
+// The backlog order inside a node is ascending winner index (sample_and_route
+// appends per point, _kernels.py:100-151, and a point wins at most one cell
+// per node), so a point's own wins -- all at different nodes -- may take any
+// order: the stable node sort separates them.
+__device__ __forceinline__ long long claim_index(uint32_t v, long long n_s) {
+  return (v & kBatchTag) ? n_s + (long long)(v & ~kBatchTag) : (long long)v;
+}
+
+__global__ void __launch_bounds__(256)
+    k_resolve(NodeCols nd, Hash h, uint32_t *grid32, long long n_s, uint32_t *__restrict__ wcount) { lod::pdl_wait();
+  const long long H = (long long)h.mask + 1;
+  for (long long sidx = gtid(); sidx < H; sidx += gstride()) {
+    HSlot *sl = h.slots + sidx;
+    const ulonglong2 kv = __ldcg(reinterpret_cast<const ulonglong2 *>(sl));
+    if (kv.x == kEmptyKey) continue;
+    const int nid = (int)(kv.x >> 32);
+    const uint32_t cell = (uint32_t)(kv.x & 0xFFFFFFFFu);
     atomicOr(grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5), 1u << (cell & 31));
-    wins[j * D + lvl] = key;
-    atomicOr(wmask + j, 1ull << lvl);
+    sl->pad = atomicAdd(wcount + claim_index((uint32_t)kv.y, n_s), 1u);
   }
 }
 
-__global__ void k_wcount(const unsigned long long *__restrict__ wmask, long long n, uint32_t *__restrict__ wcount) { lod::pdl_wait();
-  for (long long j = gtid(); j < n; j += gstride()) wcount[j] = (uint32_t)__popcll(wmask[j]);
-}
-
-// Backlog in the reference's order (sample_and_route appends per point, in
-// path order = ascending level, _kernels.py:100-151): entry b = wbase[j] + k.
-__global__ void k_emit(long long n, unsigned long long *__restrict__ wmask, const uint32_t *__restrict__ wbase,
-                       const unsigned long long *__restrict__ wins, int D, PointSrc src,
-                       int32_t *__restrict__ bnode, uint32_t *__restrict__ bcell, uint32_t *__restrict__ brgba) { lod::pdl_wait();
-  for (long long j = gtid(); j < n; j += gstride()) {
-    unsigned long long m = wmask[j];
-    if (!m) continue;
-    wmask[j] = 0;
-    uint32_t b = wbase[j];
-    const uint32_t col = src.rgba(j);
-    while (m) {
-      const int lvl = __ffsll((long long)m) - 1;
-      m &= m - 1;
-      const unsigned long long key = wins[j * D + lvl];
-      bnode[b] = (int32_t)(key >> 32);
-      bcell[b] = (uint32_t)(key & 0xFFFFFFFFu);
-      brgba[b] = col;
-      ++b;
-    }
+__global__ void __launch_bounds__(256)
+    k_scatter(Hash h, long long n_s, const uint32_t *__restrict__ wbase, PointSrc src, int32_t *__restrict__ bnode,
+              uint32_t *__restrict__ bcell, uint32_t *__restrict__ brgba) { lod::pdl_wait();
+  const long long H = (long long)h.mask + 1;
+  for (long long sidx = gtid(); sidx < H; sidx += gstride()) {
+    HSlot *sl = h.slots + sidx;
+    const ulonglong2 kv = __ldcg(reinterpret_cast<const ulonglong2 *>(sl));
+    if (kv.x == kEmptyKey) continue;
+    *reinterpret_cast<ulonglong2 *>(sl) = make_ulonglong2(kEmptyKey, kEmptyHi);
+    const long long j = claim_index((uint32_t)kv.y, n_s);
+    const uint32_t b = __ldg(wbase + j) + (uint32_t)(kv.y >> 32);
+    bnode[b] = (int32_t)(kv.x >> 32);
+    bcell[b] = (uint32_t)(kv.x & 0xFFFFFFFFu);
+    brgba[b] = src.rgba(j);
   }
 }
 

@@ -171,8 +171,8 @@ struct LodTree {
   // sampling scratch
   DBuf<int32_t> srank;  // split rank per node (-1 when not splitting)
   DBuf<HSlot> hslots, hslots2;  // claim table (`hcap` slots in use) + growth spare
-  DBuf<unsigned long long> hused, wins, wmask;
-  DBuf<uint32_t> wcount, wbase;
+  DBuf<unsigned long long> hused;
+  DBuf<uint32_t> wcount, wbase;  // per-point win counts (zero between cycles) / their exclusive scan
   unsigned long long hcap = 0;
   long long prev_used = 0;  // claims of the previous cycle (sizes the table)
   DBuf<int32_t> bnode;
@@ -336,7 +336,7 @@ static int abort_cycle(LodTree *t, int code) {
   lod::launch(k_clear_marks_all, grid_for(t->num_nodes), 256, 0, t->st, t->nd, t->srank.p, t->num_nodes);
   if (t->hslots.p) {
     cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), t->st);
-    if (t->wmask.p) cudaMemsetAsync(t->wmask.p, 0, (size_t)t->wmask.cap * 8, t->st);
+    if (t->wcount.p) cudaMemsetAsync(t->wcount.p, 0, (size_t)t->wcount.cap * 4, t->st);
   }
   long long words = (t->ncap + 31) / 32 + 1;
   cudaMemsetAsync(t->bitmap.p, 0, (size_t)words * 4, t->st);
@@ -477,7 +477,7 @@ int lod_tree_destroy(LodTree *t) {
   t->touched.release(); t->split_list.release(); t->node_b.release(); t->node_all.release();
   t->bitmap.release(); t->word_prefix.release(); t->tbits.release(); t->scnt.release(); t->schk.release();
   t->spill_off.release(); t->chunk_off.release(); t->spill.release(); t->hslots.release(); t->hslots2.release();
-  t->hused.release(); t->wins.release(); t->wmask.release(); t->srank.release(); t->wcount.release(); t->wbase.release();
+  t->hused.release(); t->srank.release(); t->wcount.release(); t->wbase.release();
   t->bnode.release(); t->bcell.release(); t->brgba.release(); t->keys.release(); t->keys_b.release();
   t->vals_a.release(); t->vals_b.release(); t->hist.release(); t->ghist.release(); t->nodecnt.release();
   t->dense.release();
@@ -684,14 +684,12 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   const long long num_nodes = h1.num_nodes;
   // ---- resolve the claims (update.py:298-315)
   const int D = (int)std::max<long long>(h1.max_level, 1);
-  RK(t->wcount.ensure(n_all, st));
-  RK(t->wbase.ensure(n_all, st));
-  RK(t->wins.ensure(n_all * D, st));
   {
-    long long oldm = t->wmask.cap;
-    RK(t->wmask.ensure(n_all, st, oldm));
-    if (t->wmask.cap > oldm) CK(cudaMemsetAsync(t->wmask.p + oldm, 0, (size_t)(t->wmask.cap - oldm) * 8, st));
+    long long oldw = t->wcount.cap;  // zero when (re)allocated; k_radix_prep re-zeroes it every cycle
+    RK(t->wcount.ensure(n_all, st));
+    if (t->wcount.cap > oldw) CK(cudaMemsetAsync(t->wcount.p, 0, (size_t)t->wcount.cap * 4, st));
   }
+  RK(t->wbase.ensure(n_all, st));
   RK(t->scan_u32.ensure(scan_scratch_elems(std::max<long long>(n_all, 1)), st));
   if (h1.hash_overflow) {
     if (lod_debug()) fprintf(stderr, "[lod] claim table overflow (H=%llu, used>=%llu): fallback pass\n", t->hcap, h1.n_used);
@@ -713,19 +711,16 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   if (h1.hash_overflow) return abort_cycle(t, LOD_E_NOMEM);
   const long long n_v = (long long)h1.n_used;
   t->prev_used = n_v;
-  if (n_v > 0) {
-    lod::launch(k_resolve, grid_for(n_v), 256, 0, st, t->nd, hs, grid32, n_s, D, t->wins.p, t->wmask.p, t->d_ctrl);
-  }
+  if (n_v > 0) lod::launch(k_resolve, grid_for((long long)t->hcap), 256, 0, st, t->nd, hs, grid32, n_s, t->wcount.p);
   mark(1);
   tp("resolve_launched");
   RK(t->bnode.ensure(std::max<long long>(n_v, 1), st));
   RK(t->bcell.ensure(std::max<long long>(n_v, 1), st));
   RK(t->brgba.ensure(std::max<long long>(n_v, 1), st));
   if (n_v > 0) {
-    lod::launch(k_wcount, grid_for(n_all), 256, 0, st, t->wmask.p, n_all, t->wcount.p);
     exclusive_scan<uint32_t>(t->wcount.p, t->wbase.p, n_all, &t->d_ctrl->n_v, t->scan_u32.p, st);
-    lod::launch(k_emit, grid_for(n_all), 256, 0, st, n_all, t->wmask.p, t->wbase.p, t->wins.p, D, src, t->bnode.p,
-                                           t->bcell.p, t->brgba.p);
+    lod::launch(k_scatter, grid_for((long long)t->hcap), 256, 0, st, hs, n_s, t->wbase.p, src, t->bnode.p, t->bcell.p,
+                t->brgba.p);
   }
   mark(2);
   // ---- sort: every new sample by node id, stable (slot order)
@@ -745,8 +740,9 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     if (t->nodecnt.cap > oldn) CK(cudaMemsetAsync(t->nodecnt.p + oldn, 0, (size_t)(t->nodecnt.cap - oldn) * 4, st));
   }
   const long long lbw = radix_lb_elems(n_items);
-  lod::launch(k_radix_prep, std::min<unsigned>(grid_for(n_items), 148), kRadixBlock, 0, st, node_of, n_all, t->bnode.p,
-              n_v, num_nodes, t->keys.p, t->nodecnt.p, t->hist.p, lbw);
+  lod::launch(k_radix_prep, std::min<unsigned>(grid_for(n_items, kRadixBlock * kPrepItems), 148 * kPrepBlocksPerSM),
+              kRadixBlock, 0, st, node_of, n_all, t->bnode.p, n_v, num_nodes, t->keys.p, t->nodecnt.p, t->hist.p, lbw,
+              t->wcount.p);
   lod::launch(k_radix_ghist, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p, num_nodes, passes,
               t->ghist.p);
   RadixScratch rs;

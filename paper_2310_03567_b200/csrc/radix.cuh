@@ -36,11 +36,15 @@ constexpr uint32_t kLbAgg = 1u << 30, kLbPre = 2u << 30, kLbMask = (1u << 30) - 
 
 // Items: points j in [0, n_all) keyed by their leaf, then backlog entries keyed
 // by their node.  Writes the key array and the per-node item counts (= each
-// node's new samples this cycle; hot leaves are aggregated per warp first).
-__global__ void __launch_bounds__(kRadixBlock)
+// node's new samples this cycle; hot leaves are aggregated per warp first),
+// and re-zeroes the per-point win counts for the next cycle.  4 items per
+// thread per round (independent loads in flight), 4 CTAs per SM.
+constexpr int kPrepItems = 4;
+constexpr int kPrepBlocksPerSM = 4;
+__global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
     k_radix_prep(const int32_t *__restrict__ node_all, long long n_all, const int32_t *__restrict__ bnode,
                  long long n_v, long long num_nodes, uint32_t *__restrict__ keys, uint32_t *__restrict__ nodecnt,
-                 uint32_t *__restrict__ lb0, long long lb_words) { lod::pdl_wait();
+                 uint32_t *__restrict__ lb0, long long lb_words, uint32_t *__restrict__ wcount) { lod::pdl_wait();
   __shared__ uint32_t nc[kNodeHistSmem];
   for (long long i = gtid(); i < lb_words; i += gstride()) lb0[i] = 0;  // look-back words of pass 0
   const bool smem_nodes = num_nodes <= kNodeHistSmem;
@@ -48,19 +52,30 @@ __global__ void __launch_bounds__(kRadixBlock)
     for (long long i = threadIdx.x; i < num_nodes; i += kRadixBlock) nc[i] = 0;
   __syncthreads();
   const long long n = n_all + n_v;
-  for (long long i0 = (long long)blockIdx.x * kRadixBlock; i0 < n; i0 += gstride()) {
-    const long long i = i0 + threadIdx.x;
-    uint32_t key = 0xFFFFFFFFu;
-    if (i < n) {
-      key = (uint32_t)(i < n_all ? node_all[i] : bnode[i - n_all]);
-      keys[i] = key;
+  constexpr long long kSpan = (long long)kRadixBlock * kPrepItems;
+  for (long long i0 = (long long)blockIdx.x * kSpan; i0 < n; i0 += (long long)gridDim.x * kSpan) {
+    uint32_t key[kPrepItems];
+#pragma unroll
+    for (int q = 0; q < kPrepItems; ++q) {
+      const long long i = i0 + q * kRadixBlock + threadIdx.x;
+      key[q] = 0xFFFFFFFFu;
+      if (i < n) key[q] = (uint32_t)(i < n_all ? __ldg(node_all + i) : __ldg(bnode + (i - n_all)));
     }
-    const unsigned act = __ballot_sync(0xffffffffu, i < n);
-    if (i < n) {
-      const unsigned peers = __match_any_sync(act, key);
-      if (lane_id() == (unsigned)(__ffs(peers) - 1)) {
-        if (smem_nodes) atomicAdd(&nc[key], (uint32_t)__popc(peers));
-        else atomicAdd(&nodecnt[key], (uint32_t)__popc(peers));
+#pragma unroll
+    for (int q = 0; q < kPrepItems; ++q) {
+      const long long i = i0 + q * kRadixBlock + threadIdx.x;
+      const bool ok = i < n;
+      if (ok) {
+        keys[i] = key[q];
+        if (i < n_all) wcount[i] = 0;
+      }
+      const unsigned act = __ballot_sync(0xffffffffu, ok);
+      if (ok) {
+        const unsigned peers = __match_any_sync(act, key[q]);
+        if (lane_id() == (unsigned)(__ffs(peers) - 1)) {
+          if (smem_nodes) atomicAdd(&nc[key[q]], (uint32_t)__popc(peers));
+          else atomicAdd(&nodecnt[key[q]], (uint32_t)__popc(peers));
+        }
       }
     }
   }

@@ -196,6 +196,17 @@ int lod_render(LodTree *tree, const double *planes, const double *cam, double th
 int lod_raster_points(int32_t device, const float *xyz, const uint32_t *rgba, int64_t n,
                       const double *cam, uint64_t *fb, int64_t width, int64_t height, int flags);
 
+/* io.morton_key / io.morton_sort (io.py:419-446) on the device: keys_out gets
+ * the 64-bit Morton keys in INPUT order (`bits` 1..21 per axis, x at bit 0,
+ * then y, z; scale = (1 << bits) / size computed by the caller like the
+ * reference); xyz_out / rgba_out get the stable reorder of the points by key.
+ * Any output may be NULL (no sort runs when both record outputs are NULL);
+ * rgba may be NULL when rgba_out is.  Host pointers, or device pointers with
+ * LOD_FLAG_DEVICE_INPUT. */
+int lod_morton_sort(int32_t device, const double *bmin, double scale, int32_t bits, const float *xyz,
+                    const uint32_t *rgba, int64_t n, float *xyz_out, uint32_t *rgba_out, uint64_t *keys_out,
+                    int flags);
+
 /* Device-side helpers for benchmarking the resident path (inputs in HBM). */
 int lod_device_alloc(int32_t device, uint64_t bytes, void **ptr);
 int lod_device_free(void *ptr);

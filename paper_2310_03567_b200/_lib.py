@@ -118,6 +118,8 @@ SIGNATURES = {
     "lod_render": (ctypes.c_int, [_P, _P, _P, ctypes.c_double, _P, _I64, _I64, ctypes.c_int, _P, _I64,
                                   ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "lod_raster_points": (ctypes.c_int, [ctypes.c_int32, _P, _P, _I64, _P, _P, _I64, _I64, ctypes.c_int]),
+    "lod_morton_sort": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_double, ctypes.c_int32, _P, _P, _I64, _P, _P,
+                                       _P, ctypes.c_int]),
     "lod_device_alloc": (ctypes.c_int, [ctypes.c_int32, ctypes.c_uint64, ctypes.POINTER(_P)]),
     "lod_device_free": (ctypes.c_int, [_P]),
     "lod_memcpy_h2d": (ctypes.c_int, [_P, _P, ctypes.c_uint64]),

@@ -41,7 +41,7 @@ constexpr uint32_t kLbAgg = 1u << 30, kLbPre = 2u << 30, kLbMask = (1u << 30) - 
 // thread per round (independent loads in flight), 4 CTAs per SM.
 constexpr int kPrepItems = 4;
 constexpr int kPrepBlocksPerSM = 4;
-__global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
+static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
     k_radix_prep(const int32_t *__restrict__ node_all, long long n_all, const int32_t *__restrict__ bnode,
                  long long n_v, long long num_nodes, uint32_t *__restrict__ keys, uint32_t *__restrict__ nodecnt,
                  uint32_t *__restrict__ lb0, long long lb_words, uint32_t *__restrict__ wcount) { lod::pdl_wait();
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
 }
 
 // Digit totals of every pass from the per-node counts (keys are node ids).
-__global__ void k_radix_ghist(const uint32_t *__restrict__ nodecnt, long long num_nodes, int passes,
+static __global__ void k_radix_ghist(const uint32_t *__restrict__ nodecnt, long long num_nodes, int passes,
                               uint32_t *__restrict__ ghist) { lod::pdl_wait();
   __shared__ uint32_t h[kMaxPasses * kRadixDigits];
   for (int i = threadIdx.x; i < kMaxPasses * kRadixDigits; i += blockDim.x) h[i] = 0;
@@ -103,7 +103,7 @@ __global__ void k_radix_ghist(const uint32_t *__restrict__ nodecnt, long long nu
 
 // One LSD pass.  vals_in == nullptr means the identity permutation.
 // `lb` holds ntiles * 256 look-back words + 1 tile ticket, zeroed before the pass.
-__global__ void __launch_bounds__(kRadixBlock, 4)
+static __global__ void __launch_bounds__(kRadixBlock, 4)
     k_onesweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in, long long n, int shift,
                const uint32_t *__restrict__ ghist_pass, uint32_t *lb, long long ntiles,
                uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint32_t *lb_next) { lod::pdl_wait();
@@ -208,6 +208,23 @@ __global__ void __launch_bounds__(kRadixBlock, 4)
   }
 }
 
+// Digit histograms of `passes` 8-bit digits starting at bit `shift0` over
+// arbitrary u32 keys (the upsweep of a general sort; k_radix_ghist derives
+// them from node counts instead).  ghist[p * 256 + d] must be zero on entry.
+static __global__ void k_digit_hist(const uint32_t *__restrict__ keys, long long n, int shift0, int passes,
+                                   uint32_t *__restrict__ ghist) { lod::pdl_wait();
+  __shared__ uint32_t h[kMaxPasses * kRadixDigits];
+  for (int i = threadIdx.x; i < kMaxPasses * kRadixDigits; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (long long i = gtid(); i < n; i += gstride()) {
+    const uint32_t k = __ldg(keys + i);
+    for (int p = 0; p < passes; ++p) atomicAdd(&h[p * kRadixDigits + ((k >> (shift0 + p * kRadixBits)) & 0xFF)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * kRadixDigits; i += blockDim.x)
+    if (h[i]) atomicAdd(ghist + i, h[i]);
+}
+
 struct RadixScratch {
   uint32_t *keys_b = nullptr, *vals_a = nullptr, *vals_b = nullptr;
   uint32_t *ghist = nullptr;         // kMaxPasses * 256
@@ -228,15 +245,16 @@ inline int radix_passes(uint32_t max_key) {
 // k_radix_ghist).  On return *keys_res / *vals_res point at the sorted keys /
 // original item indices.
 inline void stable_multisplit(uint32_t *keys, long long n, int passes, RadixScratch &s, cudaStream_t st,
-                              uint32_t **keys_res, uint32_t **vals_res) {
+                              uint32_t **keys_res, uint32_t **vals_res, const uint32_t *vals0 = nullptr,
+                              int shift0 = 0) {
   const long long ntiles = radix_tiles(n);
   uint32_t *kin = keys, *kout = s.keys_b;
-  const uint32_t *vin = nullptr;
+  const uint32_t *vin = vals0;
   uint32_t *vout = s.vals_a;
   for (int p = 0; p < passes; ++p) {
     if (n > 0) {
       // look-back buffer p&1 was zeroed by k_radix_prep (p = 0) or by pass p-1
-      lod::launch(k_onesweep, (unsigned)ntiles, kRadixBlock, 0, st, kin, vin, n, p * kRadixBits,
+      lod::launch(k_onesweep, (unsigned)ntiles, kRadixBlock, 0, st, kin, vin, n, shift0 + p * kRadixBits,
                   s.ghist + p * kRadixDigits, s.lb[p & 1], ntiles, kout, vout,
                   p + 1 < passes ? s.lb[(p + 1) & 1] : (uint32_t *)nullptr);
     }

@@ -17,7 +17,7 @@ CHUNK_ID_COLS = ("chunk_head", "chunk_tail", "next", "occupied", "payload_off", 
 
 
 def golden_names() -> list[str]:
-    return sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and f not in ("raster.npz", "deltas.npz"))
+    return sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and f not in ("raster.npz", "deltas.npz", "morton.npz"))
 
 
 def load_golden(name: str) -> dict:

@@ -263,12 +263,47 @@ def make_deltas(mods) -> None:
     print("deltas.npz:", ", ".join(DELTA_SCENARIOS))
 
 
+def make_morton() -> None:
+    """morton.npz: the reference's morton_key / morton_sort (io.py:419-446) on
+    clouds with duplicates, boundary and out-of-cube coordinates, several bit
+    widths and an offset non-unit root."""
+    sys.path.insert(0, REF)
+    from lodstream import io as lio
+    from lodstream.octree import CubeBounds
+
+    out = {}
+    rng = np.random.default_rng(41)
+    xyz, rgba = cloud(6000, seed=42)
+    dup = xyz[rng.integers(0, len(xyz), 600)]
+    edge = np.array([[0.0, 0.0, 0.0], [1.0, 1.0, 1.0], [0.5, 0.5, 0.5], [-0.25, 0.5, 1.75], [0.999999, 0.0, 0.5],
+                     [np.nextafter(np.float32(1), np.float32(0))] * 3], np.float32)
+    x = np.concatenate([xyz, dup, edge]).astype(np.float32)
+    c = np.concatenate([rgba, rgba[:600], np.arange(len(edge), dtype=np.uint32)]).astype(np.uint32)
+    out["xyz"], out["rgba"] = x, c
+    unit = CubeBounds((0.0, 0.0, 0.0), 1.0)
+    for bits in (1, 2, 5, 10, 11, 16, 21):
+        out[f"keys_b{bits}"] = lio.morton_key(x, unit, bits=bits)
+    sx, sr = lio.morton_sort(x, c, unit)
+    out["sorted_xyz"], out["sorted_rgba"] = sx, sr
+    off = CubeBounds((-3.0, 2.5, 10.0), 6.5)
+    xo = (x.astype(np.float64) * 6.5 + np.array([-3.0, 2.5, 10.0])).astype(np.float32)
+    out["off_xyz"] = xo
+    out["off_keys"] = lio.morton_key(xo, off)
+    out["off_sorted_rgba"] = lio.morton_sort(xo, c, off)[1]
+    np.savez_compressed(os.path.join(HERE, "morton.npz"), **out)
+    print("morton.npz:", len(x), "points")
+
+
 def main():
     mods = _import_ref()
     if "--only-deltas" in sys.argv:
         make_deltas(mods)
         return
+    if "--only-morton" in sys.argv:
+        make_morton()
+        return
     make_deltas(mods)
+    make_morton()
     octree, render, store, update, errors = mods
     manifest = {}
     for name, params, batches in scenarios():

@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import oracle
+from common import GOLDEN as GOLDEN_DIR
 from oracle import rebuild
 from common import (assert_same_deltas, assert_same_state, delta_names, dense_fb, flatten_deltas, golden_names,
                     load_deltas, load_golden, load_raster, oracle_state, run_oracle)
@@ -84,3 +85,27 @@ def test_oracle_delta_matches_reference_fixture(name):
                           spill_capacity=p["spill_capacity"])
     deltas = [t.insert_batch(x, c, collect_delta=True)["delta"] for x, c in g["batches"]]
     assert_same_deltas(flatten_deltas(deltas), load_deltas(name), name)
+
+
+def test_oracle_morton_matches_reference_fixture():
+    """io.py:419-446 restatement (oracle/morton.py) vs the reference's own keys and orders."""
+    from oracle import morton
+
+    z = np.load(GOLDEN_DIR + "/morton.npz")
+    x, c = z["xyz"], z["rgba"]
+    for bits in (1, 2, 5, 10, 11, 16, 21):
+        assert np.array_equal(morton.morton_key(x, (0.0, 0.0, 0.0), 1.0, bits), z[f"keys_b{bits}"]), bits
+    order = morton.morton_order(x, (0.0, 0.0, 0.0), 1.0)
+    assert np.array_equal(x[order], z["sorted_xyz"]) and np.array_equal(c[order], z["sorted_rgba"])
+    assert np.array_equal(morton.morton_key(z["off_xyz"], (-3.0, 2.5, 10.0), 6.5), z["off_keys"])
+    assert np.array_equal(c[morton.morton_order(z["off_xyz"], (-3.0, 2.5, 10.0), 6.5)], z["off_sorted_rgba"])
+
+
+def test_oracle_morton_known_answers():
+    """test_io.py:231-275 known answers."""
+    from oracle import morton
+
+    pts = np.array([[0.1, 0.1, 0.1], [0.6, 0.6, 0.6], [0.6, 0.1, 0.1]], np.float32)
+    assert morton.morton_key(pts, (0, 0, 0), 1.0, bits=1).tolist() == [0, 7, 1]
+    for p, k in (([0.6, 0.1, 0.1], 8), ([0.1, 0.6, 0.1], 16), ([0.1, 0.1, 0.6], 32)):
+        assert morton.morton_key(np.array([p], np.float32), (0, 0, 0), 1.0, bits=2).tolist() == [k]

@@ -250,7 +250,7 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def timed_stream(inputs, profile=False, frames=False):
+    def timed_stream(inputs, profile=False, frames=False, keep=None):
         """Device-resident batches one insert_batch per step, or (frames=True)
         host batches through the frame loop a user runs (cli._build:
         run_frame_updates over a queue, 10 ms budget, ingest feed overlapped)."""
@@ -283,14 +283,20 @@ def run_ours(args, rank, world, local_rank):
         ms = e0.elapsed_time(e1)
         info = dict(nodes=tree.num_nodes, points=tree.total_points() if args.steps <= 200 else None,
                     voxels_created=state.stats.voxels_created, arena=tree.arena.offset)
-        tree.close()
+        if keep is not None:
+            keep.extend([tree, state])
+        else:
+            tree.close()
         return ms, per, launches, phases, info, (h2d, d2h)
 
     with ClockSampler(dev) as clocks:
         ms, per, launches, _, info, _ = timed_stream(dev_b)
     ms_e2e, per_e2e, _, _, _, (h2d, d2h) = timed_stream(pin_b, frames=True)
     # profiled replay: per-phase CUDA events on the tree stream + per-batch B_alg inputs
-    _, per_prof, _, phases, _, _ = timed_stream(dev_b, profile=True)
+    kept = []
+    _, per_prof, _, phases, _, _ = timed_stream(dev_b, profile=True, keep=kept)
+    rows = secondary_rows(args, kept[0], kept[1], dev_b, dev) if not args.no_rows else None
+    kept[0].close()
 
     timed_pts = sum(n_points[args.warmup:])
     t_max = ms
@@ -338,10 +344,88 @@ def run_ours(args, rank, world, local_rank):
         "phase_ms": phase_summary,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
+        "rows": rows,
     }
     if dist is not None:
         dist.destroy_process_group()
     return line
+
+
+def secondary_rows(args, tree, state, dev_b, dev) -> dict:
+    """The SURVEY 8(f) rows on the settled stream tree (device timings, wall
+    clock around synchronous calls, best of a few):
+
+    * render: ``rasterize`` = device selection + splat (lod_render, device
+      framebuffer) at the bench camera of cli.py:325-328 (1024 x 768), and
+      ``select_visible`` alone;
+    * delta: insert_batch(collect_delta=True) vs plain on further batches;
+    * morton: device Morton sort of 16M resident points (lod_morton_sort).
+    """
+    import ctypes
+
+    import torch
+
+    from paper_2310_03567_b200 import _lib, insert_batch, synth
+    from paper_2310_03567_b200.render import Camera, frustum_planes, select_visible
+
+    out = {}
+    cam = Camera((0.5, 0.5, -1.5), (0.5, 0.5, 0.5), fov_deg=60.0, near=0.05, far=100.0, width=1024, height=768)
+    planes = np.ascontiguousarray(frustum_planes(cam), np.float64)
+    cpk = np.ascontiguousarray(cam.packed(), np.float64)
+    fb = torch.full((cam.width * cam.height,), -1, dtype=torch.int64, device=f"cuda:{dev}")
+    sel = np.empty(tree.num_nodes, np.int32)
+    n, drawn = ctypes.c_int64(0), ctypes.c_int64(0)
+
+    def render_once():
+        fb.fill_(-1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _lib.check(tree._L.lod_render(tree.handle, _lib.ptr(planes), _lib.ptr(cpk), 128.0, _lib.ptr(fb), cam.width,
+                                      cam.height, _lib.LOD_FLAG_DEVICE_FB, _lib.ptr(sel), len(sel), ctypes.byref(n),
+                                      ctypes.byref(drawn)), "render")
+        return time.perf_counter() - t0
+
+    render_once()
+    t_r = min(render_once() for _ in range(10))
+    t0 = time.perf_counter()
+    for _ in range(10):
+        select_visible(tree, cam, 128.0)
+    t_s = (time.perf_counter() - t0) / 10
+    out["render"] = {"camera": "cli.py:325-328 bench camera, 1024x768, threshold 128", "ms": round(t_r * 1e3, 3),
+                     "select_ms": round(t_s * 1e3, 3), "nodes_selected": int(n.value),
+                     "samples_drawn": int(drawn.value),
+                     "msamples_per_s": round(drawn.value / t_r / 1e6, 1)}
+    # delta capture overhead on further batches
+    extra = [synth.gen_surface(BATCH, 9000 + i) for i in range(6)]
+    ex = [(torch.from_numpy(x).cuda(), torch.from_numpy(c.view(np.int32)).cuda()) for x, c in extra]
+    tp, td = [], []
+    for i, (x, c) in enumerate(ex):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        insert_batch(tree, x, c, state, collect_delta=bool(i % 2))
+        (td if i % 2 else tp).append(time.perf_counter() - t0)
+    out["delta"] = {"plain_ms": round(min(tp) * 1e3, 3), "collect_delta_ms": round(min(td) * 1e3, 3),
+                    "note": "wall ms per 1M-point insert incl. delta assembly + D2H, same tree, alternating"}
+    # Morton sort of 16M device-resident points
+    mx = torch.cat([b[0] for b in dev_b[:16]])
+    mc = torch.cat([b[1] for b in dev_b[:16]])
+    mo_x, mo_c = torch.empty_like(mx), torch.empty_like(mc)
+    bmin = np.zeros(3, np.float64)
+    L = _lib.load()
+
+    def morton_once():
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _lib.check(L.lod_morton_sort(dev, _lib.ptr(bmin), float(1 << 21), 21, _lib.ptr(mx), _lib.ptr(mc),
+                                     mc.numel(), _lib.ptr(mo_x), _lib.ptr(mo_c), None, _lib.LOD_FLAG_DEVICE_INPUT),
+                   "morton")
+        return time.perf_counter() - t0
+
+    morton_once()
+    t_m = min(morton_once() for _ in range(5))
+    out["morton_sort"] = {"points": int(mc.numel()), "ms": round(t_m * 1e3, 3),
+                          "mpts_per_s": round(mc.numel() / t_m / 1e6, 1)}
+    return out
 
 
 def phase_bytes(phase: str, n_b: int, n_s: int, n_v: int) -> int | None:
@@ -456,6 +540,7 @@ def main():
     ap.add_argument("--arena-gib", type=float, default=8.0)
     ap.add_argument("--cpu-batches", type=int, default=12)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-rows", action="store_true", help="skip the render / delta / Morton rows")
     ap.add_argument("--presort", action="store_true", help="experiment: z-order each batch on the host")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -5,6 +5,7 @@
 // lodstream.update.insert_batch (update.py:252-393); see lod_kernels.cuh for
 // the per-pass kernels and DESIGN.md for the data layout.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <chrono>
@@ -162,7 +163,11 @@ struct LodTree {
   long long ccap = 0;
   PoolCols pool{};
   Ctrl *d_ctrl = nullptr;
-  Ctrl *h_ctrl = nullptr;
+  Ctrl *h_ctrl = nullptr;       // pinned + mapped: k_publish writes it directly
+  Ctrl *h_ctrl_dev = nullptr;   // device alias of h_ctrl
+  unsigned *h_seq = nullptr;    // pinned + mapped publication counter
+  unsigned *h_seq_dev = nullptr;
+  unsigned seq = 0;
   // expansion scratch
   DBuf<int32_t> touched, split_list, node_b, node_all;
   DBuf<uint32_t> bitmap, word_prefix, tbits;
@@ -234,10 +239,47 @@ static int cuda_rc(cudaError_t e) {
     if (rc__) return rc__;                   \
   } while (0)
 
+// Host view of the control block after all work queued so far: one warp
+// copies it into mapped pinned memory and then bumps a publication counter,
+// which the host polls -- no copy-engine round trip and no stream-sync wake-up
+// on the critical path of the expansion loop.  A stream error while polling
+// (or LOD_SYNC_MEMCPY=1) falls back to copy + synchronize.
+__global__ void k_publish(const Ctrl *__restrict__ d, Ctrl *h, volatile unsigned *seq_out, unsigned seq) {
+  lod::pdl_wait();
+  constexpr int kWords = (int)(sizeof(Ctrl) / 8);
+  static_assert(sizeof(Ctrl) % 8 == 0, "Ctrl is copied in 8-byte words");
+  const unsigned long long *src = reinterpret_cast<const unsigned long long *>(d);
+  volatile unsigned long long *dst = reinterpret_cast<volatile unsigned long long *>(h);
+  for (int k = threadIdx.x; k < kWords; k += 32) dst[k] = src[k];
+  __threadfence_system();
+  __syncwarp();
+  if (threadIdx.x == 0) *seq_out = seq;
+}
+
 static int sync_ctrl(LodTree *t) {
+  static const bool memcpy_sync = getenv("LOD_SYNC_MEMCPY") != nullptr;
+  if (memcpy_sync || !t->h_seq_dev) {
+    t->d2h_bytes += (long long)sizeof(Ctrl);
+    CK(cudaMemcpyAsync(t->h_ctrl, t->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, t->st));
+    CK(cudaStreamSynchronize(t->st));
+    return LOD_OK;
+  }
+  const unsigned want = ++t->seq;
   t->d2h_bytes += (long long)sizeof(Ctrl);
-  CK(cudaMemcpyAsync(t->h_ctrl, t->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, t->st));
-  CK(cudaStreamSynchronize(t->st));
+  lod::launch(k_publish, 1, 32, 0, t->st, t->d_ctrl, t->h_ctrl_dev, t->h_seq_dev, want);
+  volatile unsigned *flag = t->h_seq;
+  for (unsigned spins = 0; *flag != want; ++spins) {
+    if ((spins & 1023) == 1023) {
+      const cudaError_t e = cudaStreamQuery(t->st);
+      if (e != cudaSuccess && e != cudaErrorNotReady) return cuda_rc(e);
+      if (e == cudaSuccess && *flag != want) {  // stream drained without the flag: should not happen
+        CK(cudaMemcpyAsync(t->h_ctrl, t->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, t->st));
+        CK(cudaStreamSynchronize(t->st));
+        return LOD_OK;
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
   return LOD_OK;
 }
 
@@ -447,7 +489,11 @@ int lod_tree_create(const LodParams *params, LodTree **out) {
   RK(ensure_nodes(t, 1024, 0));
   RK(ensure_chunks(t, 1024, 0));
   CK(cudaMalloc(&t->d_ctrl, sizeof(Ctrl)));
-  CK(cudaMallocHost(&t->h_ctrl, sizeof(Ctrl)));
+  CK(cudaHostAlloc(&t->h_ctrl, sizeof(Ctrl), cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer(&t->h_ctrl_dev, t->h_ctrl, 0));
+  CK(cudaHostAlloc(&t->h_seq, sizeof(unsigned), cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer(&t->h_seq_dev, t->h_seq, 0));
+  *t->h_seq = 0;
   CK(cudaMemsetAsync(t->d_ctrl, 0, sizeof(Ctrl), t->st));
   memset(t->h_ctrl, 0, sizeof(Ctrl));
   lod::launch(k_init_root, 1, 1, 0, t->st, t->nd, p.bmin[0], p.bmin[1], p.bmin[2]);
@@ -474,6 +520,7 @@ int lod_tree_destroy(LodTree *t) {
   f(t->pool.free_stack);
   f(t->d_ctrl);
   if (t->h_ctrl) cudaFreeHost(t->h_ctrl);
+  if (t->h_seq) cudaFreeHost(t->h_seq);
   t->touched.release(); t->split_list.release(); t->node_b.release(); t->node_all.release();
   t->bitmap.release(); t->word_prefix.release(); t->tbits.release(); t->scnt.release(); t->schk.release();
   t->spill_off.release(); t->chunk_off.release(); t->spill.release(); t->hslots.release(); t->hslots2.release();

@@ -1,7 +1,7 @@
 // lod_kernels.cuh -- device kernels of one update cycle (insert_batch).
 //
 // Order of a cycle (reference: update.py:1-27, 252-393):
-//   expand   k_count (+ voxel claims) -> k_decide -> [sync] -> k_exec_chunks/k_exec_nodes   (repeat)
+//   expand   k_count (+ voxel claims, touched list) -> k_decide -> [sync] -> k_exec_chunks/k_exec_nodes (repeat)
 //   resolve  k_resolve (winners set bits, per-point wins) -> k_wcount -> scan -> k_emit
 //   sort     k_keys -> stable_multisplit by node id
 //   alloc    k_seg_* (touched nodes, ascending id) -> scan(need) -> k_alloc_*
@@ -232,7 +232,7 @@ __global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl
 #endif
 __global__ void __launch_bounds__(256, LOD_COUNT_MINB)
     k_count(NodeCols nd, Geo geo, PointSrc src, int32_t *__restrict__ node_of, long long n, int first,
-            const uint32_t *__restrict__ grid32, Hash h, Ctrl *ctrl) { lod::pdl_wait();
+            const uint32_t *__restrict__ grid32, Hash h, int32_t *__restrict__ touched, Ctrl *ctrl) { lod::pdl_wait();
   __shared__ UsedStage stg;
   used_init(stg);
   for (long long j0 = (long long)blockIdx.x * blockDim.x; j0 < n; j0 += gstride()) {
@@ -270,31 +270,15 @@ __global__ void __launch_bounds__(256, LOD_COUNT_MINB)
     if (leaf >= 0) {
       unsigned peers = __match_any_sync(act, leaf);
       if (lane_id() == (unsigned)(__ffs(peers) - 1)) {
-        // fire-and-forget (no returned value to wait on); the touched leaves
-        // are compacted afterwards from pending > 0 (k_touched)
-        atomicAdd(&nd.pending[leaf], (unsigned long long)__popc(peers));
+        // the leaf's first count of the cycle appends it to the touched list
+        // (pending 0 -> 1, _kernels.py:59-61; order is irrelevant, k_decide
+        // ranks by id)
+        const unsigned long long old = atomicAdd(&nd.pending[leaf], (unsigned long long)__popc(peers));
+        if (old == 0) touched[atomicAdd(&ctrl->n_touched, 1u)] = leaf;
       }
     }
   }
   used_flush(h, stg, ctrl);
-}
-
-// The reference's `touched` list (pending 0 -> 1 transitions, _kernels.py:59-61)
-// as a set: leaves of [from, num_nodes) counted in this pass.  Iteration 1
-// scans every node, later iterations only the children created by the
-// previous split pass (the only leaves their points can reach).
-__global__ void k_touched(NodeCols nd, long long from, int32_t *__restrict__ touched, Ctrl *ctrl) { lod::pdl_wait();
-  const long long nn = ctrl->num_nodes;
-  for (long long i0 = from + (long long)blockIdx.x * blockDim.x; i0 < nn; i0 += gstride()) {
-    const long long i = i0 + threadIdx.x;
-    const bool t = i < nn && nd.pending[i] > 0 && !nd.inner[i] && !nd.final_[i];
-    const unsigned m = __ballot_sync(0xffffffffu, t);
-    if (!m) continue;
-    unsigned base = 0;
-    if (lane_id() == 0) base = atomicAdd(&ctrl->n_touched, (unsigned)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (t) touched[base + __popc(m & lanemask_lt())] = (int32_t)i;
-  }
 }
 
 // _split_pass (update.py:226-249): split iff count + pending > T and

@@ -119,7 +119,6 @@ __global__ void k_cycle_begin(Ctrl *c) { lod::pdl_wait();
   c->acq_tot = u64x2(0, 0);
 }
 
-__global__ void k_reset_touched(Ctrl *c) { lod::pdl_wait(); c->n_touched = 0; }
 
 // Walk one node's chunk list into a packed record buffer (gather_samples,
 // octree.py:298-326).  One CTA per listed node.
@@ -635,7 +634,6 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   long long n_all = n, n_s = 0;
   int first = 1, iters = 0;
   long long splits_cycle = 0;
-  long long touch_from = 0;  // leaves a count pass can reach: all (iteration 1), new children (later)
   // claim table: sized from the batch and the previous cycle's claims, grown
   // (rehashed) between iterations when the next pass could overfill it; a
   // table that still fills up falls back to a separate claim pass
@@ -654,8 +652,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   for (;;) {
     ++iters;
     if (prof) cudaEventRecord(t->ev[12], st);
-    lod::launch(k_count, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, node_of, n_all, first, grid32, hs, t->d_ctrl);
-    lod::launch(k_touched, grid_for(t->num_nodes - touch_from), 256, 0, st, t->nd, touch_from, t->touched.p, t->d_ctrl);
+    lod::launch(k_count, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, node_of, n_all, first, grid32, hs,
+                t->touched.p, t->d_ctrl);
     if (prof) cudaEventRecord(t->ev[13], st);
     lod::launch(k_decide, 1, kDecideBlock, 0, st, t->nd, t->geo, t->touched.p, t->bitmap.p, t->word_prefix.p,
                                          t->split_list.p, t->srank.p, t->scnt.p, t->schk.p, t->spill_off.p,
@@ -690,7 +688,6 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     }
     lod::launch(k_exec_nodes, grid_for(8 * ns), 256, 0, st, t->nd, t->geo, t->split_list.p, t->srank.p, ns,
                                                    t->d_ctrl);
-    touch_from = h.plan_num_nodes0;
     t->num_nodes = h.num_nodes;
     if (first) {
       n_s = h.spill_total;

@@ -171,25 +171,37 @@ def run_multi(args, rank, world, local_rank):
         step += 1
     stripes = [gen_stripe(kind, step + k, rank) for k in range(args.steps)]
     dev_b = [(torch.from_numpy(x).cuda(), torch.from_numpy(c.view(np.int32)).cuda()) for x, c in stripes]
+    pin_b = [(torch.from_numpy(x).pin_memory(), torch.from_numpy(c.view(np.int32)).pin_memory())
+             for x, c in (gen_stripe(kind, step + args.steps + k, rank) for k in range(args.steps))]
     torch.cuda.synchronize()
-    dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches = 0
-    with ClockSampler(local_rank) as clocks:
+
+    def timed(inputs, host):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches = h2d = 0
         e0.record()
-        for x, c in dev_b:
+        for x, c in inputs:
+            if host:  # the stripe arrives in host memory: H2D inside the timed region
+                x, c = x.cuda(non_blocking=True), c.cuda(non_blocking=True)
+                h2d += 16 * c.numel()
             ins.insert(x, c)
             launches += int(state._bstats.launches)
         e1.record()
         torch.cuda.synchronize()
         dist.barrier()
         torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    v = torch.tensor([ms, float(sum(len(c) for _, c in stripes))], device="cuda", dtype=torch.float64)
+        return e0.elapsed_time(e1), launches, h2d
+
+    with ClockSampler(local_rank) as clocks:
+        ms, launches, _ = timed(dev_b, False)
+    # e2e: the next stripes of the stream from pinned host memory
+    ms_e2e, _, h2d = timed(pin_b, True)
+    v = torch.tensor([ms, float(sum(len(c) for _, c in stripes)), ms_e2e], device="cuda", dtype=torch.float64)
     allv = [torch.zeros_like(v) for _ in range(world)]
     dist.all_gather(allv, v)
     t_max = max(float(a[0]) for a in allv)
+    t_e2e = max(float(a[2]) for a in allv)
     pts = sum(float(a[1]) for a in allv)
     line = None
     if rank == 0:
@@ -203,7 +215,11 @@ def run_multi(args, rank, world, local_rank):
                        "parallelism": f"octant-prefix partition depth {plan.depth} x{world}, NCCL all-to-all routing",
                        "imbalance_max_over_mean": round(partition.imbalance(plan), 3),
                        "l2": "inputs larger than L2: distinct 16 MB stripes per step"},
-            "e2e": None, "gpu_launches": launches, "clocks": clocks.summary(),
+            "e2e": {"value": round(pts / (t_e2e * 1e-3) / 1e6, 2), "unit": "Mpts/s",
+                    "h2d_bytes_per_step": h2d // max(args.steps, 1), "d2h_bytes_per_step": None,
+                    "note": "the next K stripes of the stream, each H2D from pinned host memory + routing + "
+                            "insert, max over ranks"},
+            "gpu_launches": launches, "clocks": clocks.summary(),
         }
     dist.destroy_process_group()
     return line

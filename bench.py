@@ -449,16 +449,16 @@ def phase_bytes(phase: str, n_b: int, n_s: int, n_v: int) -> int | None:
 
     count:   every point's 16-byte record read once + its 4-byte leaf id written
     resolve: per new voxel: claim slot read+clear (32), grid word RMW (8), win (8), mask RMW (16)
-    sort:    per item and radix pass: key read (hist) + key/value read + write (20), 2 passes
-    store:   records read 16 n_all, written 16 (n_all + n_v)  (= B_alg of the whole update)
+    sort:    radix pass 1 (key read, key + item write: 12 per item), pass 2 (key + item read: 8)
+             + the store its last pass performs (source records read 16 n_all, written 16 per item)
     total:   B_alg = 32 n_b + 32 n_s + 16 n_v
     """
     n_all = n_b + n_s
+    n_items = n_all + n_v
     return {
         "count": 20 * n_all,
         "resolve": 64 * n_v,
-        "sort": 2 * 20 * (n_all + n_v),
-        "store": 32 * n_all + 16 * n_v,
+        "sort": 20 * n_items + 16 * n_all + 16 * n_items,
         "total": 32 * n_b + 32 * n_s + 16 * n_v,
     }.get(phase)
 
@@ -474,8 +474,7 @@ def roofline_from_phases(phases: list[dict], peak: float) -> tuple[dict, dict]:
     dom = max((k for k in names if phase_bytes(k, 1, 1, 1) is not None), key=lambda k: tot[k])
     gbs = {k: round(byts[k] / (tot[k] * 1e-3) / 1e9, 1) for k in byts if byts[k] and tot[k] > 0}
     roof = {
-        "bound": "hbm", "kernel": {"count": "k_count", "store": "k_store", "sort": "k_radix_*",
-                                   "resolve": "k_resolve"}[dom],
+        "bound": "hbm", "kernel": {"count": "k_count", "sort": "k_onesweep", "resolve": "k_resolve"}[dom],
         "achieved": gbs.get(dom), "unit": "GB/s", "traffic": None,
         "kernel_share_of_step": round(tot[dom] / tot["total"], 3) if tot["total"] else None,
         "whole_update": {"achieved": gbs.get("total"), "frac": round(gbs.get("total", 0) / peak, 4)},

@@ -82,8 +82,8 @@ typedef struct {
     int64_t h2d_bytes, d2h_bytes;  /* host<->device traffic of this call                      */
     float device_ms;               /* CUDA-event time of the whole update on the tree stream  */
     float phase_ms[LOD_NPHASE];    /* with LOD_FLAG_PROFILE: count (k_count only), split,
-                                      resolve, backlog, sort, alloc, store, epilogue, h2d,
-                                      total                                                   */
+                                      resolve, backlog, alloc, sort (+ store), delta,
+                                      epilogue, h2d, total                                    */
 } LodBatchStats;
 
 /* Counters of the live tree (Octree / ChunkPool / Arena scalar attributes). */

@@ -30,7 +30,7 @@ LOD_FLAG_DEVICE_FB = 2
 LOD_FLAG_PROFILE = 4
 LOD_FLAG_DELTA = 8
 LOD_NPHASE = 10
-PHASES = ("count", "split", "resolve", "backlog", "sort", "alloc", "store", "epilogue", "h2d", "total")
+PHASES = ("count", "split", "resolve", "backlog", "alloc", "sort", "delta", "epilogue", "h2d", "total")
 
 
 class NativeUnavailable(RuntimeError):

@@ -585,9 +585,9 @@ __global__ void k_seg_list(NodeCols nd, Geo geo, uint32_t *__restrict__ nodecnt,
                            long long *__restrict__ seg_start, int32_t *__restrict__ dense, U64x2 *__restrict__ plan,
                            Ctrl *ctrl, uint32_t *__restrict__ ghist) { lod::pdl_wait();
   const long long K = (long long)ctrl->seg_tot.a;
-  // this kernel is the last reader of the node counts and digit totals: leave
-  // them zeroed for the next cycle; zero the plan tail the scan reads past K
-  for (long long i = gtid(); i < kMaxPassesHist; i += gstride()) ghist[i] = 0;
+  // this kernel is the last reader of the node counts: leave them zeroed for
+  // the next cycle; zero the plan tail the scan reads past K
+  (void)ghist;
   for (long long i = K + gtid(); i <= num_nodes; i += gstride()) plan[i] = u64x2(0, 0);
   for (long long i = gtid(); i < num_nodes; i += gstride()) {
     const long long len = nodecnt[i];
@@ -707,23 +707,33 @@ __global__ void k_alloc_chunks(NodeCols nd, PoolCols pool, Geo geo, const int32_
 // node's segment is its slot count[node] + rank; records are 16-byte
 // (f32 x,y,z | u32 rgba, store.py:14-16); voxel centres are
 // bmin + (c + 0.5) * (size_by_level[level] / g) in f64, then rounded to f32.
-__global__ void k_store(NodeCols nd, PoolCols pool, Geo geo, uint8_t *__restrict__ arena,
-                        const uint32_t *__restrict__ skeys, const uint32_t *__restrict__ svals,
-                        const int32_t *__restrict__ dense, const long long *__restrict__ seg_start,
-                        const U64x2 *__restrict__ plan, const U64x2 *__restrict__ plan_ex,
-                        const int32_t *__restrict__ wl, long long n_items, long long n_all, PointSrc src,
-                        const uint32_t *__restrict__ bcell, const uint32_t *__restrict__ brgba, const Ctrl *ctrl) { lod::pdl_wait();
-  if (ctrl->error) return;
-  for (long long p = gtid(); p < n_items; p += gstride()) {
-    const int n = (int)skeys[p];
+// Used as the sink of the sort's last radix pass (the allocation runs before
+// the sort: it needs only the per-node counts), so sorted keys / item ids are
+// never written back; k_store is the same body over materialised arrays.
+struct StoreSink {
+  NodeCols nd;
+  PoolCols pool;
+  Geo geo;
+  uint8_t *arena;
+  const int32_t *dense;
+  const long long *seg_start;
+  const U64x2 *plan_ex;
+  const int32_t *wl;
+  long long n_all;
+  PointSrc src;
+  const uint32_t *bcell, *brgba;
+  const Ctrl *ctrl;
+  __device__ __forceinline__ void operator()(uint32_t p, uint32_t key, uint32_t item) const {
+    if (ctrl->error) return;
+    const int n = (int)key;
     const long long d = dense[n];
-    const long long rank = p - seg_start[d];
+    const long long rank = (long long)p - seg_start[d];
     const long long cnt = nd.count[n];
     const long long slot = cnt + rank;
     const long long rel = slot / geo.C - cnt / geo.C;
     const int cid = wl[(long long)plan_ex[d].b + rel];
     const long long off = slot % geo.C;
-    const long long i = svals[p];
+    const long long i = item;
     float4 rec;
     if (i < n_all) {
       rec = src.record(i);
@@ -741,11 +751,18 @@ __global__ void k_store(NodeCols nd, PoolCols pool, Geo geo, uint8_t *__restrict
     float4 *dst = reinterpret_cast<float4 *>(arena + pool.payload_off[cid]) + off;
     *dst = rec;
   }
+};
+
+__global__ void k_store(StoreSink sink, const uint32_t *__restrict__ skeys, const uint32_t *__restrict__ svals,
+                        long long n_items) { lod::pdl_wait();
+  for (long long p = gtid(); p < n_items; p += gstride()) sink((uint32_t)p, skeys[p], svals[p]);
 }
 
 // clear_marks (_kernels.py:280-287) + count advance: pending drains into count.
 __global__ void k_epilogue(NodeCols nd, const int32_t *__restrict__ seg_node, const long long *__restrict__ seg_start,
-                           const Ctrl *ctrl) { lod::pdl_wait();
+                           const Ctrl *ctrl, uint32_t *__restrict__ ghist) { lod::pdl_wait();
+  // the sort is the last reader of the digit totals: zeroed for the next cycle
+  for (long long i = gtid(); i < kMaxPassesHist; i += gstride()) ghist[i] = 0;
   if (ctrl->error) return;
   const long long K = (long long)ctrl->n_keys;
   for (long long d = gtid(); d < K; d += gstride()) {

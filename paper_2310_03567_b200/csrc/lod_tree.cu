@@ -789,18 +789,9 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
               t->wcount.p);
   lod::launch(k_radix_ghist, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p, num_nodes, passes,
               t->ghist.p);
-  RadixScratch rs;
-  rs.keys_b = t->keys_b.p;
-  rs.vals_a = t->vals_a.p;
-  rs.vals_b = t->vals_b.p;
-  rs.ghist = t->ghist.p;
-  rs.lb[0] = t->hist.p;
-  rs.lb[1] = t->hist.p + lbw;
-  uint32_t *skeys = nullptr, *svals = nullptr;
-  stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals);
-  mark(3);
-  tp("sort_launched");
-  // ---- allocation (update.py:317-331): touched nodes = nodes with new samples, ascending id
+  // ---- allocation (update.py:317-331): touched nodes = nodes with new samples, ascending id.
+  // It needs only the per-node counts, so it runs before the sort, whose last
+  // pass then writes every record straight into its chunk slot.
   const long long Kb = num_nodes + 1;  // bound on touched nodes
   RK(t->seg_node.ensure(Kb, st));
   RK(t->seg_start.ensure(Kb + 1, st));
@@ -814,18 +805,34 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   lod::launch(k_seg_pairs, grid_for(num_nodes), 256, 0, st, t->nodecnt.p, num_nodes, t->plan_ex.p);
   exclusive_scan<U64x2>(t->plan_ex.p, t->plan_ex.p, num_nodes, &t->d_ctrl->seg_tot, t->scan_u64x2.p, st);
   lod::launch(k_seg_list, grid_for(num_nodes), 256, 0, st, t->nd, t->geo, t->nodecnt.p, num_nodes, t->plan_ex.p,
-                                                  t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->d_ctrl, t->ghist.p);
+              t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->d_ctrl, t->ghist.p);
   exclusive_scan<U64x2>(t->plan.p, t->plan_ex.p, Kb, &t->d_ctrl->acq_tot, t->scan_u64x2.p, st);
   lod::launch(k_alloc_begin, 1, 1, 0, st, t->d_ctrl, t->geo, t->arena_cap);
-  lod::launch(k_alloc_nodes, grid_for(Kb), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p, t->plan.p,
-                                              t->plan_ex.p, t->wl.p, t->d_ctrl);
-  lod::launch(k_alloc_chunks, grid_for(acq_bound), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p,
-                                                      t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl);
+  lod::launch(k_alloc_nodes, grid_for(Kb), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p,
+              t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl);
+  lod::launch(k_alloc_chunks, grid_for(acq_bound), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p,
+              t->seg_start.p, t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl);
+  mark(3);
+  tp("alloc_launched");
+  // ---- sort + store (update.py:357-373): stable by node id = slot order
+  RadixScratch rs;
+  rs.keys_b = t->keys_b.p;
+  rs.vals_a = t->vals_a.p;
+  rs.vals_b = t->vals_b.p;
+  rs.ghist = t->ghist.p;
+  rs.lb[0] = t->hist.p;
+  rs.lb[1] = t->hist.p + lbw;
+  const StoreSink sink{t->nd,      t->pool,      t->geo, t->arena, t->dense.p, t->seg_start.p, t->plan_ex.p,
+                       t->wl.p,    n_all,        src,    t->bcell.p, t->brgba.p, t->d_ctrl};
+  uint32_t *skeys = nullptr, *svals = nullptr;
+  if (delta) {  // the delta reads the sorted order: materialise it, then store
+    stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals);
+    lod::launch(k_store, grid_for(n_items), 256, 0, st, sink, skeys, svals, n_items);
+  } else {
+    stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals, nullptr, 0, &sink);
+  }
   mark(4);
-  // ---- store (update.py:357-373)
-  lod::launch(k_store, grid_for(n_items), 256, 0, st, t->nd, t->pool, t->geo, t->arena, skeys, svals, t->dense.p,
-                                             t->seg_start.p, t->plan.p, t->plan_ex.p, t->wl.p, n_items, n_all,
-                                             src, t->bcell.p, t->brgba.p, t->d_ctrl);
+  tp("sort_launched");
   if (delta) {  // ---- BatchDelta (update.py:333-355), before the counts advance
     RK(t->dvnode.ensure(Kb, st));
     RK(t->dvstart.ensure(Kb, st));
@@ -844,7 +851,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   }
   mark(5);
   // ---- cleanup (update.py:375-380)
-  lod::launch(k_epilogue, grid_for(Kb), 256, 0, st, t->nd, t->seg_node.p, t->seg_start.p, t->d_ctrl);
+  lod::launch(k_epilogue, grid_for(Kb), 256, 0, st, t->nd, t->seg_node.p, t->seg_start.p, t->d_ctrl, t->ghist.p);
   mark(6);
   CK(cudaEventRecord(t->ev[10], st));
   tp("all_launched");
@@ -872,7 +879,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     fprintf(stderr, "[lod] batch n=%lld n_s=%lld n_v=%lld iters=%d splits=%lld nodes=%lld %.3f ms\n", (long long)n,
             n_s, n_v, iters, splits_cycle, (long long)S.num_nodes, ms);
   if (prof) {
-    // phases: count, split, resolve, backlog, sort, alloc, store, epilogue, h2d, total
+    // phases: count, split, resolve, backlog, alloc, sort (+ store), delta, epilogue, h2d, total
     float h2d = 0.f;
     cudaEventElapsedTime(&h2d, t->ev[0], t->ev[11]);
     cudaEvent_t prev = t->ev[11];

@@ -101,12 +101,23 @@ static __global__ void k_radix_ghist(const uint32_t *__restrict__ nodecnt, long 
     if (h[i]) atomicAdd(ghist + i, h[i]);
 }
 
+// Where a pass writes its sorted items: the next pass's key / value arrays, or
+// (the last pass of the update's sort) straight into the consumer (Sink).
+struct KVSink {
+  uint32_t *keys_out, *vals_out;
+  __device__ __forceinline__ void operator()(uint32_t pos, uint32_t key, uint32_t val) const {
+    keys_out[pos] = key;
+    vals_out[pos] = val;
+  }
+};
+
 // One LSD pass.  vals_in == nullptr means the identity permutation.
 // `lb` holds ntiles * 256 look-back words + 1 tile ticket, zeroed before the pass.
+template <class Sink>
 static __global__ void __launch_bounds__(kRadixBlock, 4)
     k_onesweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in, long long n, int shift,
-               const uint32_t *__restrict__ ghist_pass, uint32_t *lb, long long ntiles,
-               uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint32_t *lb_next) { lod::pdl_wait();
+               const uint32_t *__restrict__ ghist_pass, uint32_t *lb, long long ntiles, Sink sink,
+               uint32_t *lb_next) { lod::pdl_wait();
   // zero the next pass's look-back words (one per thread, + the ticket)
   if (lb_next) {
     lb_next[(long long)blockIdx.x * kRadixDigits + threadIdx.x] = 0;
@@ -202,9 +213,7 @@ static __global__ void __launch_bounds__(kRadixBlock, 4)
   for (int p = threadIdx.x; p < valid; p += kRadixBlock) {
     const uint32_t key = sk[p];
     const int d = (int)((key >> shift) & (kRadixDigits - 1));
-    const uint32_t pos = gbase[d] + (uint32_t)p - dstart[d];
-    keys_out[pos] = key;
-    vals_out[pos] = sv[p];
+    sink(gbase[d] + (uint32_t)p - dstart[d], key, sv[p]);
   }
 }
 
@@ -243,10 +252,13 @@ inline int radix_passes(uint32_t max_key) {
 
 // Stable sort of (keys, item index) by key (keys/ghist from k_radix_prep +
 // k_radix_ghist).  On return *keys_res / *vals_res point at the sorted keys /
-// original item indices.
+// original item indices -- unless `last` is given: then the last pass hands
+// every item's final position to that sink instead of writing the arrays
+// (*keys_res / *vals_res are then null).
+template <class LastSink = KVSink>
 inline void stable_multisplit(uint32_t *keys, long long n, int passes, RadixScratch &s, cudaStream_t st,
                               uint32_t **keys_res, uint32_t **vals_res, const uint32_t *vals0 = nullptr,
-                              int shift0 = 0) {
+                              int shift0 = 0, const LastSink *last = nullptr) {
   const long long ntiles = radix_tiles(n);
   uint32_t *kin = keys, *kout = s.keys_b;
   const uint32_t *vin = vals0;
@@ -254,9 +266,13 @@ inline void stable_multisplit(uint32_t *keys, long long n, int passes, RadixScra
   for (int p = 0; p < passes; ++p) {
     if (n > 0) {
       // look-back buffer p&1 was zeroed by k_radix_prep (p = 0) or by pass p-1
-      lod::launch(k_onesweep, (unsigned)ntiles, kRadixBlock, 0, st, kin, vin, n, shift0 + p * kRadixBits,
-                  s.ghist + p * kRadixDigits, s.lb[p & 1], ntiles, kout, vout,
-                  p + 1 < passes ? s.lb[(p + 1) & 1] : (uint32_t *)nullptr);
+      uint32_t *lbn = p + 1 < passes ? s.lb[(p + 1) & 1] : (uint32_t *)nullptr;
+      if (last && p + 1 == passes)
+        lod::launch(k_onesweep<LastSink>, (unsigned)ntiles, kRadixBlock, 0, st, kin, vin, n, shift0 + p * kRadixBits,
+                    s.ghist + p * kRadixDigits, s.lb[p & 1], ntiles, *last, lbn);
+      else
+        lod::launch(k_onesweep<KVSink>, (unsigned)ntiles, kRadixBlock, 0, st, kin, vin, n, shift0 + p * kRadixBits,
+                    s.ghist + p * kRadixDigits, s.lb[p & 1], ntiles, KVSink{kout, vout}, lbn);
     }
     uint32_t *kt = kin;
     kin = kout;
@@ -264,8 +280,8 @@ inline void stable_multisplit(uint32_t *keys, long long n, int passes, RadixScra
     vin = vout;
     vout = (vout == s.vals_a) ? s.vals_b : s.vals_a;
   }
-  *keys_res = kin;
-  *vals_res = const_cast<uint32_t *>(vin);
+  *keys_res = last ? nullptr : kin;
+  *vals_res = last ? nullptr : const_cast<uint32_t *>(vin);
 }
 
 }  // namespace lod

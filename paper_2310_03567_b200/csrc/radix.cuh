@@ -126,29 +126,49 @@ static __global__ void __launch_bounds__(kRadixBlock, 4)
   __shared__ uint32_t wh[kRadixWarps][kRadixDigits];  // per-warp digit counts -> warp offsets
   __shared__ uint32_t dstart[kRadixDigits];           // tile-local digit start
   __shared__ uint32_t gbase[kRadixDigits];            // global position of the tile's digit run
-  __shared__ uint32_t sk[kRadixTile], sv[kRadixTile];
+  __shared__ alignas(16) uint32_t sk[kRadixTile];
+  __shared__ alignas(16) uint32_t sv[kRadixTile];
   __shared__ uint16_t sloc[kRadixTile];
   __shared__ uint32_t sh[kRadixBlock / 32 + 1];
   __shared__ uint32_t s_tile;
+  __shared__ unsigned long long s_bar;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = atomicAdd(lb + ntiles * kRadixDigits, 1u);  // launch-order tile ids
+  if (threadIdx.x == 0) {
+    s_tile = atomicAdd(lb + ntiles * kRadixDigits, 1u);  // launch-order tile ids
+    mbar_init(&s_bar, 1);
+  }
   for (int d = lane; d < kRadixDigits; d += 32) wh[warp][d] = 0;
   __syncthreads();
   const long long tile = s_tile;
   const long long t0 = tile * kRadixTile;
   const int wofs = warp * (32 * kRadixRounds);
   const unsigned lt = lanemask_lt();
-  // 1) warp-ordered ranking; keys/values/ranks staged in input order
+  const long long valid = min((long long)kRadixTile, n - t0);
+  // 0) stage the tile (keys, and item ids unless identity) in shared memory with
+  //    TMA bulk copies; the ragged tail (< 4 items) is loaded directly
+  const int nbulk = (int)(valid & ~3ll);
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&s_bar, (unsigned)nbulk * 4u * (vals_in ? 2u : 1u));
+    if (nbulk) {
+      bulk_g2s(sk, keys_in + t0, (unsigned)nbulk * 4u, &s_bar);
+      if (vals_in) bulk_g2s(sv, vals_in + t0, (unsigned)nbulk * 4u, &s_bar);
+    }
+  }
+  if (threadIdx.x < valid - nbulk) {
+    sk[nbulk + threadIdx.x] = __ldg(keys_in + t0 + nbulk + threadIdx.x);
+    if (vals_in) sv[nbulk + threadIdx.x] = __ldg(vals_in + t0 + nbulk + threadIdx.x);
+  }
+  mbar_wait(&s_bar, 0);
+  __syncthreads();
+  // 1) warp-ordered ranking over the staged tile (input order)
   for (int r = 0; r < kRadixRounds; ++r) {
     const int li = wofs + r * 32 + lane;
-    const long long idx = t0 + li;
-    const bool ok = idx < n;
-    const uint32_t key = ok ? __ldg(keys_in + idx) : 0u;
+    const bool ok = li < valid;
+    const uint32_t key = ok ? sk[li] : 0u;
     const int d = ok ? (int)((key >> shift) & (kRadixDigits - 1)) : kRadixDigits + 1;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const uint32_t b = ok ? wh[warp][d] : 0u;
-    sk[li] = key;
-    sv[li] = ok ? (vals_in ? __ldg(vals_in + idx) : (uint32_t)idx) : 0u;
+    if (!vals_in) sv[li] = (uint32_t)(t0 + li);
     sloc[li] = (uint16_t)(b + __popc(peers & lt));
     __syncwarp();
     if (ok && lane == __ffs(peers) - 1) wh[warp][d] = b + __popc(peers);
@@ -200,7 +220,6 @@ static __global__ void __launch_bounds__(kRadixBlock, 4)
     rp[r] = dstart[d] + wh[warp][d] + sloc[li];
   }
   __syncthreads();
-  const long long valid = min((long long)kRadixTile, n - t0);
 #pragma unroll
   for (int r = 0; r < kRadixRounds; ++r) {
     if ((long long)(wofs + r * 32 + lane) < valid) {

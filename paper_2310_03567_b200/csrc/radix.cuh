@@ -193,13 +193,27 @@ static __global__ void __launch_bounds__(kRadixBlock, 4)
       atomicExch(mine, kLbPre | run);
     } else {
       atomicExch(mine, kLbAgg | run);
+      // look back 8 predecessors per round trip (independent loads), consuming
+      // aggregates in order until an inclusive prefix; an unpublished tile
+      // ends the round and is re-read in the next one
+      constexpr int kLook = 8;
       long long t = tile - 1;
-      while (true) {
-        const uint32_t v = *((volatile uint32_t *)(lb + t * kRadixDigits + d));
-        if ((v & ~kLbMask) == 0) continue;  // predecessor not published yet
-        excl += v & kLbMask;
-        if ((v & ~kLbMask) == kLbPre) break;
-        --t;
+      bool done = false;
+      while (!done) {
+        uint32_t v[kLook];
+#pragma unroll
+        for (int q = 0; q < kLook; ++q)
+          v[q] = t - q >= 0 ? *((volatile uint32_t *)(lb + (t - q) * kRadixDigits + d)) : (2u << 30);  // kLbPre
+        int q = 0;
+        for (; q < kLook; ++q) {
+          if ((v[q] & ~kLbMask) == 0) break;  // predecessor not published yet
+          excl += v[q] & kLbMask;
+          if ((v[q] & ~kLbMask) == kLbPre) {
+            done = true;
+            break;
+          }
+        }
+        t -= q;
       }
       atomicExch(mine, kLbPre | (excl + run));
     }

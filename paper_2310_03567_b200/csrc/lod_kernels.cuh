@@ -60,6 +60,8 @@ struct Ctrl {
   unsigned long long chunk_base;
   long long n_items;
   // BatchDelta capture (LOD_FLAG_DELTA)
+  int spec_abort;             // k_decide: a speculatively launched post-expansion pipeline must not run
+  int pad2;
   unsigned int d_nvg;         // voxel groups (inner nodes with new voxels)
   unsigned int d_npg;         // point groups (leaves with new points)
 };
@@ -291,7 +293,8 @@ constexpr int kDecideBlock = 1024;
 __global__ void __launch_bounds__(kDecideBlock)
     k_decide(NodeCols nd, Geo geo, const int32_t *__restrict__ touched, uint32_t *bitmap, uint32_t *word_prefix,
              int32_t *split_list, int32_t *srank, long long *scnt, long long *schk, long long *spill_off,
-             long long *chunk_off, Ctrl *ctrl, long long spill_cap, unsigned long long arena_cap) { lod::pdl_wait();
+             long long *chunk_off, Ctrl *ctrl, long long spill_cap, unsigned long long arena_cap,
+             long long backlog_cap) { lod::pdl_wait();
   __shared__ uint32_t sh32[kDecideBlock / 32 + 1];
   __shared__ U64x2 sh64[kDecideBlock / 32 + 1];
   __shared__ unsigned int s_maxlvl;
@@ -383,6 +386,10 @@ __global__ void __launch_bounds__(kDecideBlock)
     ctrl->plan_spill0 = spill0;
     ctrl->plan_grid0 = g0;
     ctrl->iter_max_level = s_maxlvl;
+    // a post-expansion pipeline launched behind this decision runs only if the
+    // expansion settled here and the claims fit (else the host takes over)
+    ctrl->spec_abort = (ctrl->error != 0 || ns > 0 || ctrl->hash_overflow != 0 ||
+                        (long long)ctrl->n_used > backlog_cap) ? 1 : 0;
     if (ctrl->error == 0 && ns > 0) {
       ctrl->num_nodes = nn + 8ll * ns;
       ctrl->splits_total += ns;
@@ -531,7 +538,9 @@ __device__ __forceinline__ long long claim_index(uint32_t v, long long n_s) {
 }
 
 __global__ void __launch_bounds__(256)
-    k_resolve(NodeCols nd, Hash h, uint32_t *grid32, long long n_s, uint32_t *__restrict__ wcount) { lod::pdl_wait();
+    k_resolve(NodeCols nd, Hash h, uint32_t *grid32, long long n_s, uint32_t *__restrict__ wcount,
+              const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
   const long long H = (long long)h.mask + 1;
   for (long long sidx = gtid(); sidx < H; sidx += gstride()) {
     HSlot *sl = h.slots + sidx;
@@ -546,7 +555,8 @@ __global__ void __launch_bounds__(256)
 
 __global__ void __launch_bounds__(256)
     k_scatter(Hash h, long long n_s, const uint32_t *__restrict__ wbase, PointSrc src, int32_t *__restrict__ bnode,
-              uint32_t *__restrict__ bcell, uint32_t *__restrict__ brgba) { lod::pdl_wait();
+              uint32_t *__restrict__ bcell, uint32_t *__restrict__ brgba, const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
   const long long H = (long long)h.mask + 1;
   for (long long sidx = gtid(); sidx < H; sidx += gstride()) {
     HSlot *sl = h.slots + sidx;
@@ -567,7 +577,9 @@ __global__ void __launch_bounds__(256)
 // item counts), in ascending id.  Leaves and inner nodes are disjoint, so the
 // stable sort by node id lays every node's new samples out contiguously, in
 // reference slot order, starting at the exclusive prefix of the counts.
-__global__ void k_seg_pairs(const uint32_t *__restrict__ nodecnt, long long num_nodes, U64x2 *__restrict__ pairs) { lod::pdl_wait();
+__global__ void k_seg_pairs(const uint32_t *__restrict__ nodecnt, long long num_nodes, U64x2 *__restrict__ pairs,
+                            const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
   for (long long i = gtid(); i < num_nodes; i += gstride()) {
     const uint32_t c = nodecnt[i];
     pairs[i] = u64x2(c ? 1ull : 0ull, (unsigned long long)c);
@@ -583,7 +595,8 @@ __device__ __forceinline__ long long ceil_div(long long a, long long b) { return
 __global__ void k_seg_list(NodeCols nd, Geo geo, uint32_t *__restrict__ nodecnt, long long num_nodes,
                            const U64x2 *__restrict__ pairs_ex, int32_t *__restrict__ seg_node,
                            long long *__restrict__ seg_start, int32_t *__restrict__ dense, U64x2 *__restrict__ plan,
-                           Ctrl *ctrl, uint32_t *__restrict__ ghist) { lod::pdl_wait();
+                           Ctrl *ctrl, uint32_t *__restrict__ ghist, const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
   const long long K = (long long)ctrl->seg_tot.a;
   // this kernel is the last reader of the node counts: leave them zeroed for
   // the next cycle; zero the plan tail the scan reads past K
@@ -611,7 +624,8 @@ __global__ void k_seg_list(NodeCols nd, Geo geo, uint32_t *__restrict__ nodecnt,
 
 // ChunkPool.acquire in bulk (store.py:110-123): acquisitions pop the LIFO free
 // stack first, then cut fresh C*16-byte payloads from the arena (16-aligned).
-__global__ void k_alloc_begin(Ctrl *ctrl, Geo geo, unsigned long long arena_cap) { lod::pdl_wait();
+__global__ void k_alloc_begin(Ctrl *ctrl, Geo geo, unsigned long long arena_cap, const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
   const long long M = (long long)ctrl->acq_tot.a;
   const long long F = ctrl->free_count;
   const long long A = ctrl->allocated_total;
@@ -640,7 +654,9 @@ __device__ __forceinline__ int acq_cid(const PoolCols &pool, const Ctrl *ctrl, l
 // node's write list.
 __global__ void k_alloc_nodes(NodeCols nd, PoolCols pool, Geo geo, const int32_t *__restrict__ seg_node,
                               const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
-                              const U64x2 *__restrict__ plan_ex, int32_t *__restrict__ wl, const Ctrl *ctrl) { lod::pdl_wait();
+                              const U64x2 *__restrict__ plan_ex, int32_t *__restrict__ wl, const Ctrl *ctrl,
+                              const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
   if (ctrl->error) return;
   const long long K = (long long)ctrl->n_keys;
   for (long long d = gtid(); d < K; d += gstride()) {
@@ -670,7 +686,9 @@ __global__ void k_alloc_nodes(NodeCols nd, PoolCols pool, Geo geo, const int32_t
 // position and final occupancy, write-list slot.
 __global__ void k_alloc_chunks(NodeCols nd, PoolCols pool, Geo geo, const int32_t *__restrict__ seg_node,
                                const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
-                               const U64x2 *__restrict__ plan_ex, int32_t *__restrict__ wl, const Ctrl *ctrl) { lod::pdl_wait();
+                               const U64x2 *__restrict__ plan_ex, int32_t *__restrict__ wl, const Ctrl *ctrl,
+                               const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
   if (ctrl->error) return;
   const long long M = (long long)ctrl->acq_tot.a;
   const long long K = (long long)ctrl->n_keys;
@@ -754,13 +772,16 @@ struct StoreSink {
 };
 
 __global__ void k_store(StoreSink sink, const uint32_t *__restrict__ skeys, const uint32_t *__restrict__ svals,
-                        long long n_items) { lod::pdl_wait();
+                        const long long *__restrict__ n_items_dev, const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
+  const long long n_items = *n_items_dev;
   for (long long p = gtid(); p < n_items; p += gstride()) sink((uint32_t)p, skeys[p], svals[p]);
 }
 
 // clear_marks (_kernels.py:280-287) + count advance: pending drains into count.
 __global__ void k_epilogue(NodeCols nd, const int32_t *__restrict__ seg_node, const long long *__restrict__ seg_start,
-                           const Ctrl *ctrl, uint32_t *__restrict__ ghist) { lod::pdl_wait();
+                           const Ctrl *ctrl, uint32_t *__restrict__ ghist, const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
   // the sort is the last reader of the digit totals: zeroed for the next cycle
   for (long long i = gtid(); i < kMaxPassesHist; i += gstride()) ghist[i] = 0;
   if (ctrl->error) return;
@@ -786,7 +807,8 @@ __global__ void __launch_bounds__(kDeltaBlock)
     k_delta_segs(NodeCols nd, const int32_t *__restrict__ seg_node, const long long *__restrict__ seg_start,
                  int32_t *__restrict__ vnode, long long *__restrict__ vstart, long long *__restrict__ vcount,
                  int32_t *__restrict__ pnode, long long *__restrict__ pstart, long long *__restrict__ pcount,
-                 long long *__restrict__ vbase, Ctrl *ctrl) { lod::pdl_wait();
+                 long long *__restrict__ vbase, Ctrl *ctrl, const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
   __shared__ U64x2 sh[kDeltaBlock / 32 + 1];
   if (ctrl->error) return;
   const long long K = (long long)ctrl->n_keys;
@@ -833,10 +855,13 @@ __global__ void __launch_bounds__(kDeltaBlock)
 // backlog by node) copies its (cell, rgba) to its group's slot.
 __global__ void k_delta_vox(const uint32_t *__restrict__ skeys, const uint32_t *__restrict__ svals,
                             const int32_t *__restrict__ dense, const long long *__restrict__ seg_start,
-                            const long long *__restrict__ vbase, long long n_items, long long n_all,
+                            const long long *__restrict__ vbase, long long n_all,
                             const uint32_t *__restrict__ bcell, const uint32_t *__restrict__ brgba,
-                            uint32_t *__restrict__ dcell, uint32_t *__restrict__ drgba, const Ctrl *ctrl) { lod::pdl_wait();
+                            uint32_t *__restrict__ dcell, uint32_t *__restrict__ drgba, const Ctrl *ctrl,
+                            const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
   if (ctrl->error) return;
+  const long long n_items = ctrl->n_items;
   for (long long p = gtid(); p < n_items; p += gstride()) {
     const long long i = svals[p];
     if (i < n_all) continue;

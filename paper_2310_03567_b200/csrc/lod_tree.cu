@@ -179,6 +179,8 @@ struct LodTree {
   DBuf<uint32_t> wcount, wbase;  // per-point win counts (zero between cycles) / their exclusive scan
   unsigned long long hcap = 0;
   long long prev_used = 0;  // claims of the previous cycle (sizes the table)
+  int last_iters = 0;       // expansion iterations of the previous cycle (speculation policy)
+  long long spec_hits = 0;  // cycles whose pipeline ran speculatively
   DBuf<int32_t> bnode;
   DBuf<uint32_t> bcell, brgba;
   // sort / alloc scratch
@@ -649,6 +651,129 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   }
   Hash hs{t->hslots.p, t->hcap - 1, t->hused.p, t->hcap};
   uint32_t *grid32 = reinterpret_cast<uint32_t *>(t->arena);
+  // ---- post-expansion pipeline: resolve -> backlog -> alloc -> sort+store ->
+  // [delta] -> epilogue.  Launched either after the expansion settled (guard
+  // null, nv = the claim count), or speculatively behind an expansion
+  // iteration's k_decide (guard = Ctrl.spec_abort, nv = an upper bound): every
+  // kernel then returns at once unless that decide settled the expansion, and
+  // counts that only the device knows yet (new voxels) are read on the device.
+  bool pipeline_launched = false;
+  auto pipeline = [&](const int *guard, long long nv) -> int {
+    const long long num_nodes = t->num_nodes;
+    {
+      long long oldw = t->wcount.cap;  // zero when (re)allocated; k_radix_prep re-zeroes it every cycle
+      RK(t->wcount.ensure(n_all, st));
+      if (t->wcount.cap > oldw) CK(cudaMemsetAsync(t->wcount.p, 0, (size_t)t->wcount.cap * 4, st));
+    }
+    RK(t->wbase.ensure(n_all, st));
+    RK(t->scan_u32.ensure(scan_scratch_elems(std::max<long long>(n_all, 1)), st));
+    if (nv > 0) lod::launch(k_resolve, grid_for((long long)t->hcap), 256, 0, st, t->nd, hs, grid32, n_s, t->wcount.p, guard);
+    mark(1);
+    tp("resolve_launched");
+    RK(t->bnode.ensure(std::max<long long>(nv, 1), st));
+    RK(t->bcell.ensure(std::max<long long>(nv, 1), st));
+    RK(t->brgba.ensure(std::max<long long>(nv, 1), st));
+    if (nv > 0) {
+      exclusive_scan<uint32_t>(t->wcount.p, t->wbase.p, n_all, &t->d_ctrl->n_v, t->scan_u32.p, st, guard);
+      lod::launch(k_scatter, grid_for((long long)t->hcap), 256, 0, st, hs, n_s, t->wbase.p, src, t->bnode.p, t->bcell.p,
+                  t->brgba.p, guard);
+    }
+    mark(2);
+    // ---- sort: every new sample by node id, stable (slot order)
+    const long long n_items = n_all + nv;  // exact, or an upper bound (the device count is Ctrl.n_items)
+    const int passes = radix_passes((uint32_t)(num_nodes - 1));
+    RK(t->keys.ensure(n_items, st));
+    RK(t->keys_b.ensure(n_items, st));
+    RK(t->vals_a.ensure(n_items, st));
+    RK(t->vals_b.ensure(n_items, st));
+    RK(t->hist.ensure(2 * radix_lb_elems(n_items), st));
+    {
+      long long oldg = t->ghist.cap, oldn = t->nodecnt.cap;
+      RK(t->ghist.ensure(kMaxPasses * kRadixDigits, st));
+      RK(t->nodecnt.ensure(num_nodes, st, oldn));
+      // zero once when (re)allocated; afterwards k_seg_list / k_epilogue leave them zeroed
+      if (t->ghist.cap > oldg) CK(cudaMemsetAsync(t->ghist.p, 0, (size_t)t->ghist.cap * 4, st));
+      if (t->nodecnt.cap > oldn) CK(cudaMemsetAsync(t->nodecnt.p + oldn, 0, (size_t)(t->nodecnt.cap - oldn) * 4, st));
+    }
+    const long long lbw = radix_lb_elems(n_items);
+    long long *n_items_dev = &t->d_ctrl->n_items;
+    lod::launch(k_radix_prep, std::min<unsigned>(grid_for(n_items, kRadixBlock * kPrepItems), 148 * kPrepBlocksPerSM),
+                kRadixBlock, 0, st, node_of, n_all, t->bnode.p, num_nodes, t->keys.p, t->nodecnt.p, t->hist.p, lbw,
+                t->wcount.p, &t->d_ctrl->n_used, n_items_dev, guard);
+    lod::launch(k_radix_ghist, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p, num_nodes,
+                passes, t->ghist.p, guard);
+    // ---- allocation (update.py:317-331): touched nodes = nodes with new samples, ascending id.
+    // It needs only the per-node counts, so it runs before the sort, whose last
+    // pass then writes every record straight into its chunk slot.
+    const long long Kb = num_nodes + 1;  // bound on touched nodes
+    RK(t->seg_node.ensure(Kb, st));
+    RK(t->seg_start.ensure(Kb + 1, st));
+    RK(t->dense.ensure(Kb, st));
+    RK(t->plan.ensure(Kb, st));
+    RK(t->plan_ex.ensure(Kb, st));
+    RK(t->scan_u64x2.ensure(scan_scratch_elems(Kb), st));
+    const long long acq_bound = n_items / C + Kb + 1;
+    RK(t->wl.ensure(acq_bound + Kb + 1, st));
+    const long long alloc0 = t->h_ctrl->allocated_total;
+    RK(ensure_chunks(t, alloc0 + acq_bound + 1, alloc0));
+    lod::launch(k_seg_pairs, grid_for(num_nodes), 256, 0, st, t->nodecnt.p, num_nodes, t->plan_ex.p, guard);
+    exclusive_scan<U64x2>(t->plan_ex.p, t->plan_ex.p, num_nodes, &t->d_ctrl->seg_tot, t->scan_u64x2.p, st, guard);
+    lod::launch(k_seg_list, grid_for(num_nodes), 256, 0, st, t->nd, t->geo, t->nodecnt.p, num_nodes, t->plan_ex.p,
+                t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->d_ctrl, t->ghist.p, guard);
+    exclusive_scan<U64x2>(t->plan.p, t->plan_ex.p, Kb, &t->d_ctrl->acq_tot, t->scan_u64x2.p, st, guard);
+    lod::launch(k_alloc_begin, 1, 1, 0, st, t->d_ctrl, t->geo, t->arena_cap, guard);
+    lod::launch(k_alloc_nodes, grid_for(Kb), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p,
+                t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl, guard);
+    lod::launch(k_alloc_chunks, grid_for(acq_bound), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p,
+                t->seg_start.p, t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl, guard);
+    mark(3);
+    tp("alloc_launched");
+    // ---- sort + store (update.py:357-373): stable by node id = slot order
+    RadixScratch rs;
+    rs.keys_b = t->keys_b.p;
+    rs.vals_a = t->vals_a.p;
+    rs.vals_b = t->vals_b.p;
+    rs.ghist = t->ghist.p;
+    rs.lb[0] = t->hist.p;
+    rs.lb[1] = t->hist.p + lbw;
+    const StoreSink sink{t->nd,   t->pool, t->geo, t->arena,   t->dense.p, t->seg_start.p, t->plan_ex.p,
+                         t->wl.p, n_all,   src,    t->bcell.p, t->brgba.p, t->d_ctrl};
+    uint32_t *skeys = nullptr, *svals = nullptr;
+    if (delta) {  // the delta reads the sorted order: materialise it, then store
+      stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals, nullptr, 0, (const KVSink *)nullptr,
+                        n_items_dev, guard);
+      lod::launch(k_store, grid_for(n_items), 256, 0, st, sink, skeys, svals, (const long long *)n_items_dev, guard);
+    } else {
+      stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals, nullptr, 0, &sink, n_items_dev, guard);
+    }
+    mark(4);
+    tp("sort_launched");
+    if (delta) {  // ---- BatchDelta (update.py:333-355), before the counts advance
+      RK(t->dvnode.ensure(Kb, st));
+      RK(t->dvstart.ensure(Kb, st));
+      RK(t->dvcount.ensure(Kb, st));
+      RK(t->dpnode.ensure(Kb, st));
+      RK(t->dpstart.ensure(Kb, st));
+      RK(t->dpcount.ensure(Kb, st));
+      RK(t->dvbase.ensure(Kb, st));
+      RK(t->dvcell.ensure(std::max<long long>(nv, 1), st));
+      RK(t->dvrgba.ensure(std::max<long long>(nv, 1), st));
+      lod::launch(k_delta_segs, 1, kDeltaBlock, 0, st, t->nd, t->seg_node.p, t->seg_start.p, t->dvnode.p,
+                  t->dvstart.p, t->dvcount.p, t->dpnode.p, t->dpstart.p, t->dpcount.p, t->dvbase.p, t->d_ctrl, guard);
+      if (nv > 0)
+        lod::launch(k_delta_vox, grid_for(n_items), 256, 0, st, skeys, svals, t->dense.p, t->seg_start.p,
+                    t->dvbase.p, n_all, t->bcell.p, t->brgba.p, t->dvcell.p, t->dvrgba.p, t->d_ctrl, guard);
+    }
+    mark(5);
+    // ---- cleanup (update.py:375-380)
+    lod::launch(k_epilogue, grid_for(Kb), 256, 0, st, t->nd, t->seg_node.p, t->seg_start.p, t->d_ctrl, t->ghist.p,
+                guard);
+    return LOD_OK;
+  };
+  // speculate on "this iteration settles the expansion" from the second
+  // iteration on (the first usually splits), or from the first when the last
+  // cycle needed a single one; never while profiling (phase events)
+  const bool may_speculate = !prof && !getenv("LOD_NO_SPEC");
   for (;;) {
     ++iters;
     if (prof) cudaEventRecord(t->ev[12], st);
@@ -657,7 +782,14 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     if (prof) cudaEventRecord(t->ev[13], st);
     lod::launch(k_decide, 1, kDecideBlock, 0, st, t->nd, t->geo, t->touched.p, t->bitmap.p, t->word_prefix.p,
                                          t->split_list.p, t->srank.p, t->scnt.p, t->schk.p, t->spill_off.p,
-                                         t->chunk_off.p, t->d_ctrl, spill_cap, t->arena_cap);
+                                         t->chunk_off.p, t->d_ctrl, spill_cap, t->arena_cap, backlog_cap);
+    if (may_speculate && (iters >= 2 || t->last_iters == 1)) {
+      // the pipeline's host-side sizes: nodes as of now (no further split if
+      // it runs), new voxels bounded by the claim table's capacity
+      RK(pipeline(&t->d_ctrl->spec_abort, (long long)t->hcap));
+      CK(cudaEventRecord(t->ev[10], st));
+      pipeline_launched = true;
+    }
     tp("pre_sync");
     RK(sync_ctrl(t));
     tp("sync");
@@ -669,7 +801,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     const Ctrl &h = *t->h_ctrl;
     if (h.error) return abort_cycle(t, h.error);
     const long long ns = h.n_splits;
-    if (ns == 0) break;
+    if (ns == 0) break;  // settled (a speculative pipeline ran iff spec_abort == 0)
+    pipeline_launched = false;  // the speculative pipeline (if any) stood down
     splits_cycle += ns;
     if (delta) {  // events.append(("split", nid)) in split order (update.py:240-245)
       RK(t->dsplits.ensure(t->d_nsplits + ns, st, t->d_nsplits));
@@ -725,141 +858,45 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   cudaMemsetAsync(&t->d_ctrl->alloc_F, 0, 16, st);
 #endif
   t->num_nodes = h1.num_nodes;
-  const long long num_nodes = h1.num_nodes;
-  // ---- resolve the claims (update.py:298-315)
-  const int D = (int)std::max<long long>(h1.max_level, 1);
-  {
-    long long oldw = t->wcount.cap;  // zero when (re)allocated; k_radix_prep re-zeroes it every cycle
-    RK(t->wcount.ensure(n_all, st));
-    if (t->wcount.cap > oldw) CK(cudaMemsetAsync(t->wcount.p, 0, (size_t)t->wcount.cap * 4, st));
-  }
-  RK(t->wbase.ensure(n_all, st));
-  RK(t->scan_u32.ensure(scan_scratch_elems(std::max<long long>(n_all, 1)), st));
-  if (h1.hash_overflow) {
-    if (lod_debug()) fprintf(stderr, "[lod] claim table overflow (H=%llu, used>=%llu): fallback pass\n", t->hcap, h1.n_used);
-    // fallback: clean table sized by the reference's backlog bound, full claim pass
-    const long long bound = std::min<long long>(n_all * D, backlog_cap + 1);
-    const unsigned long long H = next_pow2((unsigned long long)std::max<long long>(2 * bound, 1 << 20));
-    if ((long long)H > t->hslots.cap) RK(t->hslots.ensure((long long)H, st));
-    CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
-    t->hcap = H;
-    RK(t->hused.ensure(bound + 1, st));
-    hs = Hash{t->hslots.p, t->hcap - 1, t->hused.p, (unsigned long long)bound + 1};
-    CK(cudaMemsetAsync(&t->d_ctrl->n_used, 0, 8, st));
-    CK(cudaMemsetAsync(&t->d_ctrl->hash_overflow, 0, 4, st));
-    lod::launch(k_claim, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, grid32, n_all, hs, t->d_ctrl);
+  // a pipeline launched behind the settling decide has already run (the sync
+  // waited for it) unless the claims overflowed, which the host handles here
+  if (pipeline_launched && h1.spec_abort) pipeline_launched = false;
+  t->spec_hits += pipeline_launched ? 1 : 0;
+  if (!pipeline_launched) {
+    // ---- resolve the claims (update.py:298-315)
+    const int D = (int)std::max<long long>(h1.max_level, 1);
+    if (h1.hash_overflow) {
+      if (lod_debug())
+        fprintf(stderr, "[lod] claim table overflow (H=%llu, used>=%llu): fallback pass\n", t->hcap, h1.n_used);
+      // fallback: clean table sized by the reference's backlog bound, full claim pass
+      const long long bound = std::min<long long>(n_all * D, backlog_cap + 1);
+      const unsigned long long H = next_pow2((unsigned long long)std::max<long long>(2 * bound, 1 << 20));
+      if ((long long)H > t->hslots.cap) RK(t->hslots.ensure((long long)H, st));
+      CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
+      t->hcap = H;
+      RK(t->hused.ensure(bound + 1, st));
+      hs = Hash{t->hslots.p, t->hcap - 1, t->hused.p, (unsigned long long)bound + 1};
+      CK(cudaMemsetAsync(&t->d_ctrl->n_used, 0, 8, st));
+      CK(cudaMemsetAsync(&t->d_ctrl->hash_overflow, 0, 4, st));
+      lod::launch(k_claim, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, grid32, n_all, hs, t->d_ctrl);
+      RK(sync_ctrl(t));
+      h1 = *t->h_ctrl;
+    }
+    if ((long long)h1.n_used > backlog_cap) return abort_cycle(t, LOD_E_BACKLOG_OVERFLOW);  // update.py:311-312
+    if (h1.hash_overflow) return abort_cycle(t, LOD_E_NOMEM);
+    RK(pipeline(nullptr, (long long)h1.n_used));
+    mark(6);
+    CK(cudaEventRecord(t->ev[10], st));
+    tp("all_launched");
     RK(sync_ctrl(t));
-    h1 = *t->h_ctrl;
+    tp("final_sync");
   }
-  if ((long long)h1.n_used > backlog_cap) return abort_cycle(t, LOD_E_BACKLOG_OVERFLOW);  // update.py:311-312
-  if (h1.hash_overflow) return abort_cycle(t, LOD_E_NOMEM);
-  const long long n_v = (long long)h1.n_used;
-  t->prev_used = n_v;
-  if (n_v > 0) lod::launch(k_resolve, grid_for((long long)t->hcap), 256, 0, st, t->nd, hs, grid32, n_s, t->wcount.p);
-  mark(1);
-  tp("resolve_launched");
-  RK(t->bnode.ensure(std::max<long long>(n_v, 1), st));
-  RK(t->bcell.ensure(std::max<long long>(n_v, 1), st));
-  RK(t->brgba.ensure(std::max<long long>(n_v, 1), st));
-  if (n_v > 0) {
-    exclusive_scan<uint32_t>(t->wcount.p, t->wbase.p, n_all, &t->d_ctrl->n_v, t->scan_u32.p, st);
-    lod::launch(k_scatter, grid_for((long long)t->hcap), 256, 0, st, hs, n_s, t->wbase.p, src, t->bnode.p, t->bcell.p,
-                t->brgba.p);
-  }
-  mark(2);
-  // ---- sort: every new sample by node id, stable (slot order)
-  const long long n_items = n_all + n_v;
-  const int passes = radix_passes((uint32_t)(num_nodes - 1));
-  RK(t->keys.ensure(n_items, st));
-  RK(t->keys_b.ensure(n_items, st));
-  RK(t->vals_a.ensure(n_items, st));
-  RK(t->vals_b.ensure(n_items, st));
-  RK(t->hist.ensure(2 * radix_lb_elems(n_items), st));
-  {
-    long long oldg = t->ghist.cap, oldn = t->nodecnt.cap;
-    RK(t->ghist.ensure(kMaxPasses * kRadixDigits, st));
-    RK(t->nodecnt.ensure(num_nodes, st, oldn));
-    // zero once when (re)allocated; afterwards k_seg_list leaves them zeroed
-    if (t->ghist.cap > oldg) CK(cudaMemsetAsync(t->ghist.p, 0, (size_t)t->ghist.cap * 4, st));
-    if (t->nodecnt.cap > oldn) CK(cudaMemsetAsync(t->nodecnt.p + oldn, 0, (size_t)(t->nodecnt.cap - oldn) * 4, st));
-  }
-  const long long lbw = radix_lb_elems(n_items);
-  lod::launch(k_radix_prep, std::min<unsigned>(grid_for(n_items, kRadixBlock * kPrepItems), 148 * kPrepBlocksPerSM),
-              kRadixBlock, 0, st, node_of, n_all, t->bnode.p, n_v, num_nodes, t->keys.p, t->nodecnt.p, t->hist.p, lbw,
-              t->wcount.p);
-  lod::launch(k_radix_ghist, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p, num_nodes, passes,
-              t->ghist.p);
-  // ---- allocation (update.py:317-331): touched nodes = nodes with new samples, ascending id.
-  // It needs only the per-node counts, so it runs before the sort, whose last
-  // pass then writes every record straight into its chunk slot.
-  const long long Kb = num_nodes + 1;  // bound on touched nodes
-  RK(t->seg_node.ensure(Kb, st));
-  RK(t->seg_start.ensure(Kb + 1, st));
-  RK(t->dense.ensure(Kb, st));
-  RK(t->plan.ensure(Kb, st));
-  RK(t->plan_ex.ensure(Kb, st));
-  RK(t->scan_u64x2.ensure(scan_scratch_elems(Kb), st));
-  const long long acq_bound = n_items / C + Kb + 1;
-  RK(t->wl.ensure(acq_bound + Kb + 1, st));
-  RK(ensure_chunks(t, h1.allocated_total + acq_bound + 1, h1.allocated_total));
-  lod::launch(k_seg_pairs, grid_for(num_nodes), 256, 0, st, t->nodecnt.p, num_nodes, t->plan_ex.p);
-  exclusive_scan<U64x2>(t->plan_ex.p, t->plan_ex.p, num_nodes, &t->d_ctrl->seg_tot, t->scan_u64x2.p, st);
-  lod::launch(k_seg_list, grid_for(num_nodes), 256, 0, st, t->nd, t->geo, t->nodecnt.p, num_nodes, t->plan_ex.p,
-              t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->d_ctrl, t->ghist.p);
-  exclusive_scan<U64x2>(t->plan.p, t->plan_ex.p, Kb, &t->d_ctrl->acq_tot, t->scan_u64x2.p, st);
-  lod::launch(k_alloc_begin, 1, 1, 0, st, t->d_ctrl, t->geo, t->arena_cap);
-  lod::launch(k_alloc_nodes, grid_for(Kb), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p,
-              t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl);
-  lod::launch(k_alloc_chunks, grid_for(acq_bound), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p,
-              t->seg_start.p, t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl);
-  mark(3);
-  tp("alloc_launched");
-  // ---- sort + store (update.py:357-373): stable by node id = slot order
-  RadixScratch rs;
-  rs.keys_b = t->keys_b.p;
-  rs.vals_a = t->vals_a.p;
-  rs.vals_b = t->vals_b.p;
-  rs.ghist = t->ghist.p;
-  rs.lb[0] = t->hist.p;
-  rs.lb[1] = t->hist.p + lbw;
-  const StoreSink sink{t->nd,      t->pool,      t->geo, t->arena, t->dense.p, t->seg_start.p, t->plan_ex.p,
-                       t->wl.p,    n_all,        src,    t->bcell.p, t->brgba.p, t->d_ctrl};
-  uint32_t *skeys = nullptr, *svals = nullptr;
-  if (delta) {  // the delta reads the sorted order: materialise it, then store
-    stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals);
-    lod::launch(k_store, grid_for(n_items), 256, 0, st, sink, skeys, svals, n_items);
-  } else {
-    stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals, nullptr, 0, &sink);
-  }
-  mark(4);
-  tp("sort_launched");
-  if (delta) {  // ---- BatchDelta (update.py:333-355), before the counts advance
-    RK(t->dvnode.ensure(Kb, st));
-    RK(t->dvstart.ensure(Kb, st));
-    RK(t->dvcount.ensure(Kb, st));
-    RK(t->dpnode.ensure(Kb, st));
-    RK(t->dpstart.ensure(Kb, st));
-    RK(t->dpcount.ensure(Kb, st));
-    RK(t->dvbase.ensure(Kb, st));
-    RK(t->dvcell.ensure(std::max<long long>(n_v, 1), st));
-    RK(t->dvrgba.ensure(std::max<long long>(n_v, 1), st));
-    lod::launch(k_delta_segs, 1, kDeltaBlock, 0, st, t->nd, t->seg_node.p, t->seg_start.p, t->dvnode.p, t->dvstart.p,
-                t->dvcount.p, t->dpnode.p, t->dpstart.p, t->dpcount.p, t->dvbase.p, t->d_ctrl);
-    if (n_v > 0)
-      lod::launch(k_delta_vox, grid_for(n_items), 256, 0, st, skeys, svals, t->dense.p, t->seg_start.p, t->dvbase.p,
-                  n_items, n_all, t->bcell.p, t->brgba.p, t->dvcell.p, t->dvrgba.p, t->d_ctrl);
-  }
-  mark(5);
-  // ---- cleanup (update.py:375-380)
-  lod::launch(k_epilogue, grid_for(Kb), 256, 0, st, t->nd, t->seg_node.p, t->seg_start.p, t->d_ctrl, t->ghist.p);
-  mark(6);
-  CK(cudaEventRecord(t->ev[10], st));
-  tp("all_launched");
-  RK(sync_ctrl(t));
-  tp("final_sync");
   if (tl) fprintf(stderr, "[lod] timeline%s\n", tlbuf);
+  t->last_iters = iters;
   const Ctrl &h3 = *t->h_ctrl;
   if (h3.error) return abort_cycle(t, h3.error);
+  const long long n_v = (long long)h3.n_used;
+  t->prev_used = n_v;
   if (delta) {
     t->d_nvg = h3.d_nvg;
     t->d_npg = h3.d_npg;

@@ -43,9 +43,14 @@ constexpr int kPrepItems = 4;
 constexpr int kPrepBlocksPerSM = 4;
 static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
     k_radix_prep(const int32_t *__restrict__ node_all, long long n_all, const int32_t *__restrict__ bnode,
-                 long long n_v, long long num_nodes, uint32_t *__restrict__ keys, uint32_t *__restrict__ nodecnt,
-                 uint32_t *__restrict__ lb0, long long lb_words, uint32_t *__restrict__ wcount) { lod::pdl_wait();
+                 long long num_nodes, uint32_t *__restrict__ keys, uint32_t *__restrict__ nodecnt,
+                 uint32_t *__restrict__ lb0, long long lb_words, uint32_t *__restrict__ wcount,
+                 const unsigned long long *__restrict__ n_v_dev, long long *__restrict__ n_items_out,
+                 const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
   __shared__ uint32_t nc[kNodeHistSmem];
+  const long long n_v = (long long)*n_v_dev;  // new voxels (device count: launches may precede the host's view)
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_items_out = n_all + n_v;
   for (long long i = gtid(); i < lb_words; i += gstride()) lb0[i] = 0;  // look-back words of pass 0
   const bool smem_nodes = num_nodes <= kNodeHistSmem;
   if (smem_nodes)
@@ -87,7 +92,8 @@ static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
 
 // Digit totals of every pass from the per-node counts (keys are node ids).
 static __global__ void k_radix_ghist(const uint32_t *__restrict__ nodecnt, long long num_nodes, int passes,
-                              uint32_t *__restrict__ ghist) { lod::pdl_wait();
+                              uint32_t *__restrict__ ghist, const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
   __shared__ uint32_t h[kMaxPasses * kRadixDigits];
   for (int i = threadIdx.x; i < kMaxPasses * kRadixDigits; i += blockDim.x) h[i] = 0;
   __syncthreads();
@@ -115,9 +121,13 @@ struct KVSink {
 // `lb` holds ntiles * 256 look-back words + 1 tile ticket, zeroed before the pass.
 template <class Sink>
 static __global__ void __launch_bounds__(kRadixBlock, 4)
-    k_onesweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in, long long n, int shift,
-               const uint32_t *__restrict__ ghist_pass, uint32_t *lb, long long ntiles, Sink sink,
-               uint32_t *lb_next) { lod::pdl_wait();
+    k_onesweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in, long long n_max,
+               const long long *__restrict__ n_dev, int shift, const uint32_t *__restrict__ ghist_pass, uint32_t *lb,
+               long long ntiles, Sink sink, uint32_t *lb_next, const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
+  // item count: n_max, or the device count when launched for an upper bound
+  // (tiles past it take their ticket and leave)
+  const long long n = n_dev ? *n_dev : n_max;
   // zero the next pass's look-back words (one per thread, + the ticket)
   if (lb_next) {
     lb_next[(long long)blockIdx.x * kRadixDigits + threadIdx.x] = 0;
@@ -141,6 +151,7 @@ static __global__ void __launch_bounds__(kRadixBlock, 4)
   __syncthreads();
   const long long tile = s_tile;
   const long long t0 = tile * kRadixTile;
+  if (t0 >= n) return;
   const int wofs = warp * (32 * kRadixRounds);
   const unsigned lt = lanemask_lt();
   const long long valid = min((long long)kRadixTile, n - t0);
@@ -284,14 +295,16 @@ inline int radix_passes(uint32_t max_key) {
 }
 
 // Stable sort of (keys, item index) by key (keys/ghist from k_radix_prep +
-// k_radix_ghist).  On return *keys_res / *vals_res point at the sorted keys /
+// k_radix_ghist).  n is the item count, or an upper bound when n_dev holds
+// the count on the device.  On return *keys_res / *vals_res point at the sorted keys /
 // original item indices -- unless `last` is given: then the last pass hands
 // every item's final position to that sink instead of writing the arrays
 // (*keys_res / *vals_res are then null).
 template <class LastSink = KVSink>
 inline void stable_multisplit(uint32_t *keys, long long n, int passes, RadixScratch &s, cudaStream_t st,
                               uint32_t **keys_res, uint32_t **vals_res, const uint32_t *vals0 = nullptr,
-                              int shift0 = 0, const LastSink *last = nullptr) {
+                              int shift0 = 0, const LastSink *last = nullptr, const long long *n_dev = nullptr,
+                              const int *guard = nullptr) {
   const long long ntiles = radix_tiles(n);
   uint32_t *kin = keys, *kout = s.keys_b;
   const uint32_t *vin = vals0;
@@ -301,11 +314,12 @@ inline void stable_multisplit(uint32_t *keys, long long n, int passes, RadixScra
       // look-back buffer p&1 was zeroed by k_radix_prep (p = 0) or by pass p-1
       uint32_t *lbn = p + 1 < passes ? s.lb[(p + 1) & 1] : (uint32_t *)nullptr;
       if (last && p + 1 == passes)
-        lod::launch(k_onesweep<LastSink>, (unsigned)ntiles, kRadixBlock, 0, st, kin, vin, n, shift0 + p * kRadixBits,
-                    s.ghist + p * kRadixDigits, s.lb[p & 1], ntiles, *last, lbn);
+        lod::launch(k_onesweep<LastSink>, (unsigned)ntiles, kRadixBlock, 0, st, kin, vin, n, n_dev,
+                    shift0 + p * kRadixBits, s.ghist + p * kRadixDigits, s.lb[p & 1], ntiles, *last, lbn, guard);
       else
-        lod::launch(k_onesweep<KVSink>, (unsigned)ntiles, kRadixBlock, 0, st, kin, vin, n, shift0 + p * kRadixBits,
-                    s.ghist + p * kRadixDigits, s.lb[p & 1], ntiles, KVSink{kout, vout}, lbn);
+        lod::launch(k_onesweep<KVSink>, (unsigned)ntiles, kRadixBlock, 0, st, kin, vin, n, n_dev,
+                    shift0 + p * kRadixBits, s.ghist + p * kRadixDigits, s.lb[p & 1], ntiles, KVSink{kout, vout}, lbn,
+                    guard);
     }
     uint32_t *kt = kin;
     kin = kout;

@@ -78,7 +78,8 @@ constexpr long long kScanTile = (long long)kScanBlock * kScanItems;
 // Per-tile reduction.
 template <typename T>
 __global__ void __launch_bounds__(kScanBlock) k_scan_reduce(const T *__restrict__ in, long long n,
-                                                            T *__restrict__ partial) { lod::pdl_wait();
+                                                            T *__restrict__ partial, const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
   __shared__ T sh[kScanBlock / 32 + 1];
   long long base = (long long)blockIdx.x * kScanTile + (long long)threadIdx.x * kScanItems;
   T acc = T();
@@ -95,7 +96,8 @@ template <typename T>
 __global__ void __launch_bounds__(kScanBlock) k_scan_tiles(const T *__restrict__ in, long long n,
                                                            T *__restrict__ out,
                                                            const T *__restrict__ tile_off,
-                                                           T *__restrict__ total_out) { lod::pdl_wait();
+                                                           T *__restrict__ total_out, const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
   __shared__ T sh[kScanBlock / 32 + 1];
   long long base = (long long)blockIdx.x * kScanTile + (long long)threadIdx.x * kScanItems;
   T v[kScanItems];
@@ -131,23 +133,25 @@ inline long long scan_scratch_elems(long long n) {
 }
 
 // out[i] = sum(in[0..i)); *total_out (device) = sum(in).  `in` may alias `out`.
-// `scratch` must hold scan_scratch_elems(n) elements.
+// `scratch` must hold scan_scratch_elems(n) elements.  With a guard, every
+// kernel returns at once while *guard != 0 (speculative launches).
 template <typename T>
-void exclusive_scan(const T *in, T *out, long long n, T *total_out, T *scratch, cudaStream_t st) {
+void exclusive_scan(const T *in, T *out, long long n, T *total_out, T *scratch, cudaStream_t st,
+                    const int *guard = nullptr) {
   if (n <= 0) {
-    if (total_out) cudaMemsetAsync(total_out, 0, sizeof(T), st);
+    if (total_out && !guard) cudaMemsetAsync(total_out, 0, sizeof(T), st);
     return;
   }
   if (n <= kScanTile) {
-    lod::launch(k_scan_tiles<T>, 1, kScanBlock, 0, st, in, n, out, nullptr, total_out);
+    lod::launch(k_scan_tiles<T>, 1, kScanBlock, 0, st, in, n, out, nullptr, total_out, guard);
     return;
   }
   long long tiles = (n + kScanTile - 1) / kScanTile;
   T *partial = scratch;
   T *partial_scan = scratch + tiles;
-  lod::launch(k_scan_reduce<T>, (unsigned)tiles, kScanBlock, 0, st, in, n, partial);
-  exclusive_scan<T>(partial, partial_scan, tiles, nullptr, scratch + 2 * tiles, st);
-  lod::launch(k_scan_tiles<T>, (unsigned)tiles, kScanBlock, 0, st, in, n, out, partial_scan, total_out);
+  lod::launch(k_scan_reduce<T>, (unsigned)tiles, kScanBlock, 0, st, in, n, partial, guard);
+  exclusive_scan<T>(partial, partial_scan, tiles, nullptr, scratch + 2 * tiles, st, guard);
+  lod::launch(k_scan_tiles<T>, (unsigned)tiles, kScanBlock, 0, st, in, n, out, partial_scan, total_out, guard);
 }
 
 }  // namespace lod

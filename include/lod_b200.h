@@ -112,8 +112,9 @@ int lod_insert_batch(LodTree *tree, const float *xyz, const uint32_t *rgba, int6
 
 /* Ingest feed (the reference's BatchSource queue feeding
  * run_frame_updates, io.py:340-413, update.py:396-417): start the H2D copy of
- * a batch in PAGE-LOCKED host memory on the tree's copy stream, double-
- * buffered, so it overlaps the update running ahead of it.  A later
+ * a batch in PAGE-LOCKED host memory on the tree's copy stream (a ring of 3
+ * staging slots: up to two batches in flight ahead of the one updating), so
+ * it overlaps the updates running ahead of it.  A later
  * lod_insert_batch with the same (xyz, rgba, n) consumes the staged copy
  * instead of copying.  Pageable memory is ignored (the insert copies it).
  * The caller keeps the host arrays unchanged until that insert, or until

@@ -204,7 +204,7 @@ struct LodTree {
   DBuf<uint32_t> dvcell, dvrgba;
   long long d_nsplits = 0, d_nvg = 0, d_npg = 0, d_nv = 0;
   // ingest feed: batches staged H2D on a copy stream ahead of their insert
-  // (lod_prefetch_batch), double-buffered
+  // (lod_prefetch_batch), a ring of kStages slots
   cudaStream_t cst = nullptr;
   struct Stage {
     DBuf<float> xyz;
@@ -213,7 +213,7 @@ struct LodTree {
     long long n = 0;
     bool valid = false;
     cudaEvent_t ready = nullptr;
-  } stage[2];
+  } stage[3];
   int stage_next = 0;
   cudaEvent_t ev[14] = {};  // 12, 13: per-iteration k_count brackets
   // host copies of counters (authoritative after every call)
@@ -1072,7 +1072,7 @@ int lod_prefetch_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64
   for (auto &sg : t->stage)
     if (sg.valid && sg.hx == xyz && sg.hc == rgba && sg.n == n) return LOD_OK;  // already staged
   LodTree::Stage &sg = t->stage[t->stage_next];
-  t->stage_next ^= 1;
+  t->stage_next = (t->stage_next + 1) % 3;
   // the slot's previous batch was consumed by a completed insert (every
   // lod_insert_batch returns after its update finished), or is superseded
   RK(sg.xyz.ensure(3 * n, t->cst));

@@ -267,16 +267,19 @@ def run_frame_updates(tree, batches, state: UpdateState, on_delta=None) -> int:
     """Drain queued batches for one frame within the budget (update.py:396-417).
 
     The budget is checked between batches, as in the reference.  While batch
-    k updates, batch k+1's H2D copy is already running on the copy stream
-    (pinned host batches), so the queue streams at the update rate."""
+    k updates, the H2D copies of batches k+1 and k+2 run on the copy stream
+    (pinned host batches), so the queue streams at the update rate or the
+    PCIe rate, whichever is lower."""
     state.clock.restart()
     processed = 0
     staged = False
     try:
         while batches and (processed == 0 or not state.clock.exceeded()):
             xyz, rgba = batches.popleft()
-            if batches:
-                staged = _prefetch(tree, batches[0]) or staged
+            # keep the next two queued batches copying (3 staging slots: the
+            # one being consumed + two in flight)
+            for ahead in range(min(2, len(batches))):
+                staged = _prefetch(tree, batches[ahead]) or staged
             delta = insert_batch(tree, xyz, rgba, state, collect_delta=on_delta is not None)
             if on_delta is not None:
                 on_delta(delta)

@@ -184,10 +184,11 @@ struct LodTree {
   DBuf<int32_t> bnode;
   DBuf<uint32_t> bcell, brgba;
   // sort / alloc scratch
-  DBuf<uint32_t> keys, keys_b, vals_a, vals_b, hist, ghist, nodecnt, scan_u32;
+  DBuf<uint32_t> keys, keys_b, vals_a, vals_b, hist, ghist, nodecnt;
   DBuf<int32_t> seg_node, wl, dense;
   DBuf<long long> seg_start;
-  DBuf<U64x2> plan, plan_ex, scan_u64x2;
+  DBuf<U64x2> plan, plan_ex;
+  ScanLB lb32, lb64;  // single-pass scan state (u32 win counts; U64x2 segment / need pairs)
   // inputs / outputs
   DBuf<float> in_xyz;
   DBuf<uint32_t> in_rgba;
@@ -362,6 +363,38 @@ static int ensure_chunks(LodTree *t, long long want, long long live) {
   return LOD_OK;
 }
 
+// Look-back state of the single-pass scan for up to `tiles` tiles of T.
+template <typename T>
+static int ensure_scan_lb(ScanLB &lb, long long n) {
+  const long long tiles = std::max<long long>((n + kScanTile - 1) / kScanTile, 1);
+  if (tiles <= lb.cap_tiles) return LOD_OK;
+  const long long c = std::max<long long>(tiles, 2 * lb.cap_tiles);
+  cudaDeviceSynchronize();  // rare (growth); no launch may still use the old arrays
+  if (lb.status) cudaFree(lb.status);
+  if (lb.agg) cudaFree(lb.agg);
+  if (lb.incl) cudaFree(lb.incl);
+  if (!lb.ticket) {
+    CK(cudaMalloc(&lb.ticket, 8));
+    CK(cudaMemset(lb.ticket, 0, 8));
+    lb.tickets = 0;
+  }
+  CK(cudaMalloc(&lb.status, (size_t)c * 4));
+  CK(cudaMemset(lb.status, 0, (size_t)c * 4));
+  CK(cudaMalloc(&lb.agg, (size_t)c * sizeof(T)));
+  CK(cudaMalloc(&lb.incl, (size_t)c * sizeof(T)));
+  lb.epoch = 0;
+  lb.cap_tiles = c;
+  return LOD_OK;
+}
+
+static void release_scan_lb(ScanLB &lb) {
+  if (lb.status) cudaFree(lb.status);
+  if (lb.agg) cudaFree(lb.agg);
+  if (lb.incl) cudaFree(lb.incl);
+  if (lb.ticket) cudaFree(lb.ticket);
+  lb = ScanLB{};
+}
+
 static void fill_stats(LodTree *t, LodBatchStats *s) {
   const Ctrl &c = *t->h_ctrl;
   s->num_nodes = c.num_nodes;
@@ -529,10 +562,12 @@ int lod_tree_destroy(LodTree *t) {
   t->bnode.release(); t->bcell.release(); t->brgba.release(); t->keys.release(); t->keys_b.release();
   t->vals_a.release(); t->vals_b.release(); t->hist.release(); t->ghist.release(); t->nodecnt.release();
   t->dense.release();
-  t->scan_u32.release(); t->seg_node.release(); t->wl.release(); t->seg_start.release();
-  t->plan.release(); t->plan_ex.release(); t->scan_u64x2.release(); t->in_xyz.release();
+  t->seg_node.release(); t->wl.release(); t->seg_start.release();
+  t->plan.release(); t->plan_ex.release(); t->in_xyz.release();
   t->in_rgba.release(); t->gbuf.release(); t->gnodes.release(); t->goff.release(); t->gstart.release();
   t->visflag.release(); t->vislist.release(); t->fb.release(); t->counter.release();
+  release_scan_lb(t->lb32);
+  release_scan_lb(t->lb64);
   t->dsplits.release(); t->dvnode.release(); t->dpnode.release(); t->dvstart.release(); t->dvcount.release();
   t->dpstart.release(); t->dpcount.release(); t->dvbase.release(); t->dvcell.release(); t->dvrgba.release();
   if (t->cst) cudaStreamSynchronize(t->cst);
@@ -666,7 +701,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       if (t->wcount.cap > oldw) CK(cudaMemsetAsync(t->wcount.p, 0, (size_t)t->wcount.cap * 4, st));
     }
     RK(t->wbase.ensure(n_all, st));
-    RK(t->scan_u32.ensure(scan_scratch_elems(std::max<long long>(n_all, 1)), st));
+    RK(ensure_scan_lb<uint32_t>(t->lb32, n_all));
     if (nv > 0) lod::launch(k_resolve, grid_for((long long)t->hcap), 256, 0, st, t->nd, hs, grid32, n_s, t->wcount.p, guard);
     mark(1);
     tp("resolve_launched");
@@ -674,7 +709,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     RK(t->bcell.ensure(std::max<long long>(nv, 1), st));
     RK(t->brgba.ensure(std::max<long long>(nv, 1), st));
     if (nv > 0) {
-      exclusive_scan<uint32_t>(t->wcount.p, t->wbase.p, n_all, &t->d_ctrl->n_v, t->scan_u32.p, st, guard);
+      exclusive_scan_lb<uint32_t>(t->wcount.p, t->wbase.p, n_all, &t->d_ctrl->n_v, t->lb32, st, guard);
       lod::launch(k_scatter, grid_for((long long)t->hcap), 256, 0, st, hs, n_s, t->wbase.p, src, t->bnode.p, t->bcell.p,
                   t->brgba.p, guard);
     }
@@ -711,16 +746,16 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     RK(t->dense.ensure(Kb, st));
     RK(t->plan.ensure(Kb, st));
     RK(t->plan_ex.ensure(Kb, st));
-    RK(t->scan_u64x2.ensure(scan_scratch_elems(Kb), st));
+    RK(ensure_scan_lb<U64x2>(t->lb64, Kb));
     const long long acq_bound = n_items / C + Kb + 1;
     RK(t->wl.ensure(acq_bound + Kb + 1, st));
     const long long alloc0 = t->h_ctrl->allocated_total;
     RK(ensure_chunks(t, alloc0 + acq_bound + 1, alloc0));
     lod::launch(k_seg_pairs, grid_for(num_nodes), 256, 0, st, t->nodecnt.p, num_nodes, t->plan_ex.p, guard);
-    exclusive_scan<U64x2>(t->plan_ex.p, t->plan_ex.p, num_nodes, &t->d_ctrl->seg_tot, t->scan_u64x2.p, st, guard);
+    exclusive_scan_lb<U64x2>(t->plan_ex.p, t->plan_ex.p, num_nodes, &t->d_ctrl->seg_tot, t->lb64, st, guard);
     lod::launch(k_seg_list, grid_for(num_nodes), 256, 0, st, t->nd, t->geo, t->nodecnt.p, num_nodes, t->plan_ex.p,
                 t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->d_ctrl, t->ghist.p, guard);
-    exclusive_scan<U64x2>(t->plan.p, t->plan_ex.p, Kb, &t->d_ctrl->acq_tot, t->scan_u64x2.p, st, guard);
+    exclusive_scan_lb<U64x2>(t->plan.p, t->plan_ex.p, Kb, &t->d_ctrl->acq_tot, t->lb64, st, guard);
     lod::launch(k_alloc_begin, 1, 1, 0, st, t->d_ctrl, t->geo, t->arena_cap, guard);
     lod::launch(k_alloc_nodes, grid_for(Kb), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p,
                 t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl, guard);

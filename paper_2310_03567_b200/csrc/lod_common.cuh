@@ -189,6 +189,16 @@ struct PointSrc {
   }
 };
 
+// Per-point node cache over the same all-array index space: spilled points'
+// entries live in their own array (written by the spill gather), batch points'
+// in another, so the batch part never has to move behind the spill.
+struct NodeOf {
+  int32_t *spill;
+  int32_t *batch;
+  long long ns;
+  __device__ __forceinline__ int32_t &operator[](long long j) const { return j < ns ? spill[j] : batch[j - ns]; }
+};
+
 // One descent step (count_points / sample_and_route, _kernels.py:44-56):
 // bit set when x >= bx + h, then bx += h; upper children own the split plane.
 __device__ __forceinline__ int octant_step(double x, double y, double z, double &bx, double &by,

@@ -233,7 +233,7 @@ __global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl
 #define LOD_COUNT_MINB 5  // blocks per SM: 51 registers
 #endif
 __global__ void __launch_bounds__(256, LOD_COUNT_MINB)
-    k_count(NodeCols nd, Geo geo, PointSrc src, int32_t *__restrict__ node_of, long long n, int first,
+    k_count(NodeCols nd, Geo geo, PointSrc src, NodeOf node_of, long long n, int first,
             const uint32_t *__restrict__ grid32, Hash h, int32_t *__restrict__ touched, Ctrl *ctrl) { lod::pdl_wait();
   __shared__ UsedStage stg;
   used_init(stg);
@@ -488,12 +488,6 @@ __global__ void k_exec_nodes(NodeCols nd, Geo geo, const int32_t *__restrict__ s
       srank[nid] = -1;
     }
   }
-}
-
-// Move the batch part of the per-point node cache behind the spill segment:
-// all = [spill || batch] (update.py:281-286).
-__global__ void k_shift_nodes(const int32_t *__restrict__ src, int32_t *__restrict__ dst, long long n) { lod::pdl_wait();
-  for (long long i = gtid(); i < n; i += gstride()) dst[i] = src[i];
 }
 
 // ---------------------------------------------------------------- sampling

@@ -168,7 +168,7 @@ struct LodTree {
   unsigned *h_seq_dev = nullptr;
   unsigned seq = 0;
   // expansion scratch
-  DBuf<int32_t> touched, split_list, node_b, node_all;
+  DBuf<int32_t> touched, split_list, node_b, node_all;  // node_b: batch points' node cache; node_all: spilled points'
   DBuf<uint32_t> bitmap, word_prefix, tbits;
   DBuf<long long> scnt, schk, spill_off, chunk_off;
   DBuf<float4> spill;
@@ -667,7 +667,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   // ---- expansion (update.py:273-296) with the voxel claims folded in
   RK(t->node_b.ensure(n, st));
   PointSrc src{nullptr, 0, bx, bc, n};
-  int32_t *node_of = t->node_b.p;
+  NodeOf node_of{nullptr, t->node_b.p, 0};
   long long n_all = n, n_s = 0;
   int first = 1, iters = 0;
   long long splits_cycle = 0;
@@ -849,7 +849,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     if (h.spill_add > 0) {
       if (!first) return abort_cycle(t, LOD_E_ARG);  // only iteration 1 can spill (update.py:9-11)
       RK(t->spill.ensure(h.spill_total, st));
-      RK(t->node_all.ensure(h.spill_total + n, st));
+      RK(t->node_all.ensure(h.spill_total, st));
       lod::launch(k_exec_chunks, grid_for(h.allocated_total * 32), 256, 0, st, 
           t->pool, t->geo, t->arena, h.allocated_total, t->srank.p, t->spill_off.p, t->chunk_off.p, t->spill.p,
           t->node_all.p, t->d_ctrl);
@@ -860,8 +860,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     if (first) {
       n_s = h.spill_total;
       if (n_s > 0) {
-        lod::launch(k_shift_nodes, grid_for(n), 256, 0, st, t->node_b.p, t->node_all.p + n_s, n);
-        node_of = t->node_all.p;
+        node_of.spill = t->node_all.p;
+        node_of.ns = n_s;
         src.spill = t->spill.p;
         src.ns = n_s;
       }

@@ -519,9 +519,11 @@ __global__ void k_claim(NodeCols nd, Geo geo, PointSrc src, const uint32_t *__re
 // sequential sweeps of the claim table (every sector read once, coalesced;
 // a table larger than L2 costs a streaming read, not a DRAM round trip per
 // voxel, and no list or cursor is needed):
-//   k_resolve: set the cell's bit and take a rank among the winner's wins
-//     (atomicAdd on the per-point win count), kept in the slot's pad word;
-//   k_scatter (after the exclusive scan wbase of the win counts): write the
+//   k_resolve: set the cell's bit and count the win for its winner
+//     (fire-and-forget atomics: nothing waits on them);
+//   k_scatter (after the exclusive scan wbase of the win counts): take a rank
+//     among the winner's wins by counting its count back down (atomicSub --
+//     which also leaves the counts zeroed for the next cycle), write the
 //     backlog entry at wbase[j] + rank and free the slot.
 // The backlog order inside a node is ascending winner index (sample_and_route
 // appends per point, _kernels.py:100-151, and a point wins at most one cell
@@ -537,19 +539,19 @@ __global__ void __launch_bounds__(256)
   if (guard && *guard) return;
   const long long H = (long long)h.mask + 1;
   for (long long sidx = gtid(); sidx < H; sidx += gstride()) {
-    HSlot *sl = h.slots + sidx;
-    const ulonglong2 kv = __ldcg(reinterpret_cast<const ulonglong2 *>(sl));
+    const ulonglong2 kv = __ldcg(reinterpret_cast<const ulonglong2 *>(h.slots + sidx));
     if (kv.x == kEmptyKey) continue;
     const int nid = (int)(kv.x >> 32);
     const uint32_t cell = (uint32_t)(kv.x & 0xFFFFFFFFu);
     atomicOr(grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5), 1u << (cell & 31));
-    sl->pad = atomicAdd(wcount + claim_index((uint32_t)kv.y, n_s), 1u);
+    atomicAdd(wcount + claim_index((uint32_t)kv.y, n_s), 1u);
   }
 }
 
 __global__ void __launch_bounds__(256)
-    k_scatter(Hash h, long long n_s, const uint32_t *__restrict__ wbase, PointSrc src, int32_t *__restrict__ bnode,
-              uint32_t *__restrict__ bcell, uint32_t *__restrict__ brgba, const int *guard) { lod::pdl_wait();
+    k_scatter(Hash h, long long n_s, const uint32_t *__restrict__ wbase, uint32_t *__restrict__ wcount, PointSrc src,
+              int32_t *__restrict__ bnode, uint32_t *__restrict__ bcell, uint32_t *__restrict__ brgba,
+              const int *guard) { lod::pdl_wait();
   if (guard && *guard) return;
   const long long H = (long long)h.mask + 1;
   for (long long sidx = gtid(); sidx < H; sidx += gstride()) {
@@ -558,7 +560,7 @@ __global__ void __launch_bounds__(256)
     if (kv.x == kEmptyKey) continue;
     *reinterpret_cast<ulonglong2 *>(sl) = make_ulonglong2(kEmptyKey, kEmptyHi);
     const long long j = claim_index((uint32_t)kv.y, n_s);
-    const uint32_t b = __ldg(wbase + j) + (uint32_t)(kv.y >> 32);
+    const uint32_t b = __ldg(wbase + j) + atomicSub(wcount + j, 1u) - 1u;
     bnode[b] = (int32_t)(kv.x >> 32);
     bcell[b] = (uint32_t)(kv.x & 0xFFFFFFFFu);
     brgba[b] = src.rgba(j);

@@ -696,7 +696,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   auto pipeline = [&](const int *guard, long long nv) -> int {
     const long long num_nodes = t->num_nodes;
     {
-      long long oldw = t->wcount.cap;  // zero when (re)allocated; k_radix_prep re-zeroes it every cycle
+      long long oldw = t->wcount.cap;  // zero when (re)allocated; k_scatter counts every entry back to zero
       RK(t->wcount.ensure(n_all, st));
       if (t->wcount.cap > oldw) CK(cudaMemsetAsync(t->wcount.p, 0, (size_t)t->wcount.cap * 4, st));
     }
@@ -710,8 +710,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     RK(t->brgba.ensure(std::max<long long>(nv, 1), st));
     if (nv > 0) {
       exclusive_scan_lb<uint32_t>(t->wcount.p, t->wbase.p, n_all, &t->d_ctrl->n_v, t->lb32, st, guard);
-      lod::launch(k_scatter, grid_for((long long)t->hcap), 256, 0, st, hs, n_s, t->wbase.p, src, t->bnode.p, t->bcell.p,
-                  t->brgba.p, guard);
+      lod::launch(k_scatter, grid_for((long long)t->hcap), 256, 0, st, hs, n_s, t->wbase.p, t->wcount.p, src,
+                  t->bnode.p, t->bcell.p, t->brgba.p, guard);
     }
     mark(2);
     // ---- sort: every new sample by node id, stable (slot order)
@@ -734,7 +734,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     long long *n_items_dev = &t->d_ctrl->n_items;
     lod::launch(k_radix_prep, std::min<unsigned>(grid_for(n_items, kRadixBlock * kPrepItems), 148 * kPrepBlocksPerSM),
                 kRadixBlock, 0, st, node_of, n_all, t->bnode.p, num_nodes, t->keys.p, t->nodecnt.p, t->hist.p, lbw,
-                t->wcount.p, &t->d_ctrl->n_used, n_items_dev, guard);
+                &t->d_ctrl->n_used, n_items_dev, guard);
     lod::launch(k_radix_ghist, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p, num_nodes,
                 passes, t->ghist.p, guard);
     // ---- allocation (update.py:317-331): touched nodes = nodes with new samples, ascending id.

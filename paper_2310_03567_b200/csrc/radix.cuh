@@ -36,16 +36,14 @@ constexpr uint32_t kLbAgg = 1u << 30, kLbPre = 2u << 30, kLbMask = (1u << 30) - 
 
 // Items: points j in [0, n_all) keyed by their leaf, then backlog entries keyed
 // by their node.  Writes the key array and the per-node item counts (= each
-// node's new samples this cycle; hot leaves are aggregated per warp first),
-// and re-zeroes the per-point win counts for the next cycle.  4 items per
-// thread per round (independent loads in flight), 4 CTAs per SM.
+// node's new samples this cycle; hot leaves are aggregated per warp first).
+// 4 items per thread per round (independent loads in flight), 4 CTAs per SM.
 constexpr int kPrepItems = 4;
 constexpr int kPrepBlocksPerSM = 4;
 static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
     k_radix_prep(NodeOf node_of, long long n_all, const int32_t *__restrict__ bnode,
                  long long num_nodes, uint32_t *__restrict__ keys, uint32_t *__restrict__ nodecnt,
-                 uint32_t *__restrict__ lb0, long long lb_words, uint32_t *__restrict__ wcount,
-                 const unsigned long long *__restrict__ n_v_dev, long long *__restrict__ n_items_out,
+                 uint32_t *__restrict__ lb0, long long lb_words, const unsigned long long *__restrict__ n_v_dev, long long *__restrict__ n_items_out,
                  const int *guard) { lod::pdl_wait();
   if (guard && *guard) return;
   __shared__ uint32_t nc[kNodeHistSmem];
@@ -70,10 +68,7 @@ static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
     for (int q = 0; q < kPrepItems; ++q) {
       const long long i = i0 + q * kRadixBlock + threadIdx.x;
       const bool ok = i < n;
-      if (ok) {
-        keys[i] = key[q];
-        if (i < n_all) wcount[i] = 0;
-      }
+      if (ok) keys[i] = key[q];
       const unsigned act = __ballot_sync(0xffffffffu, ok);
       if (ok) {
         const unsigned peers = __match_any_sync(act, key[q]);

@@ -572,15 +572,8 @@ __global__ void __launch_bounds__(256)
 // Touched nodes of the cycle = nodes with new samples (k_radix_prep's per-node
 // item counts), in ascending id.  Leaves and inner nodes are disjoint, so the
 // stable sort by node id lays every node's new samples out contiguously, in
-// reference slot order, starting at the exclusive prefix of the counts.
-__global__ void k_seg_pairs(const uint32_t *__restrict__ nodecnt, long long num_nodes, U64x2 *__restrict__ pairs,
-                            const int *guard) { lod::pdl_wait();
-  if (guard && *guard) return;
-  for (long long i = gtid(); i < num_nodes; i += gstride()) {
-    const uint32_t c = nodecnt[i];
-    pairs[i] = u64x2(c ? 1ull : 0ull, (unsigned long long)c);
-  }
-}
+// reference slot order, starting at the exclusive prefix of the counts (the
+// (flag, count) pairs are written by k_radix_ghist).
 
 __device__ __forceinline__ long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
 
@@ -615,30 +608,12 @@ __global__ void k_seg_list(NodeCols nd, Geo geo, uint32_t *__restrict__ nodecnt,
     const U64x2 tot = ctrl->seg_tot;
     seg_start[tot.a] = (long long)tot.b;
     ctrl->n_keys = (unsigned)tot.a;
+    // acquisition snapshot (ChunkPool.acquire, store.py:110-123): the free
+    // stack pops first, then fresh payloads are cut 16-aligned from the arena
+    ctrl->alloc_F = ctrl->free_count;
+    ctrl->alloc_A = ctrl->allocated_total;
+    ctrl->chunk_base = (ctrl->arena_off + 15ull) / 16ull * 16ull;
   }
-}
-
-// ChunkPool.acquire in bulk (store.py:110-123): acquisitions pop the LIFO free
-// stack first, then cut fresh C*16-byte payloads from the arena (16-aligned).
-__global__ void k_alloc_begin(Ctrl *ctrl, Geo geo, unsigned long long arena_cap, const int *guard) { lod::pdl_wait();
-  if (guard && *guard) return;
-  const long long M = (long long)ctrl->acq_tot.a;
-  const long long F = ctrl->free_count;
-  const long long A = ctrl->allocated_total;
-  ctrl->alloc_F = F;
-  ctrl->alloc_A = A;
-  const long long fresh = M > F ? M - F : 0;
-  const unsigned long long pay = (unsigned long long)geo.C * 16ull;
-  unsigned long long base = ctrl->arena_off;
-  if (fresh > 0) base = (base + 15ull) / 16ull * 16ull;
-  ctrl->chunk_base = base;
-  if (fresh > 0 && base + (unsigned long long)fresh * pay > arena_cap) {
-    set_error(ctrl, 1 /*LOD_E_OUT_OF_ARENA*/);
-    return;
-  }
-  if (fresh > 0) ctrl->arena_off = base + (unsigned long long)fresh * pay;
-  ctrl->free_count = F - (M < F ? M : F);
-  ctrl->allocated_total = A + fresh;
 }
 
 __device__ __forceinline__ int acq_cid(const PoolCols &pool, const Ctrl *ctrl, long long a) {
@@ -648,12 +623,30 @@ __device__ __forceinline__ int acq_cid(const PoolCols &pool, const Ctrl *ctrl, l
 // Per touched node: link the new run after the old tail (Octree.append_chunk,
 // octree.py:328-337) and put the partially filled tail at the head of the
 // node's write list.
+// The bulk acquisition's bookkeeping (every thread derives the same fresh
+// count; OutOfArena at the first fresh payload past capacity, store.py:60-69)
+// is done here too: thread 0 advances the arena / free-stack / pool counters.
 __global__ void k_alloc_nodes(NodeCols nd, PoolCols pool, Geo geo, const int32_t *__restrict__ seg_node,
                               const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
-                              const U64x2 *__restrict__ plan_ex, int32_t *__restrict__ wl, const Ctrl *ctrl,
-                              const int *guard) { lod::pdl_wait();
+                              const U64x2 *__restrict__ plan_ex, int32_t *__restrict__ wl, Ctrl *ctrl,
+                              unsigned long long arena_cap, const int *guard) { lod::pdl_wait();
   if (guard && *guard) return;
   if (ctrl->error) return;
+  {
+    const long long M = (long long)ctrl->acq_tot.a;
+    const long long F = ctrl->alloc_F, A = ctrl->alloc_A;
+    const long long fresh = M > F ? M - F : 0;
+    const unsigned long long end = ctrl->chunk_base + (unsigned long long)fresh * (unsigned long long)geo.C * 16ull;
+    if (fresh > 0 && end > arena_cap) {
+      if (gtid() == 0) set_error(ctrl, 1 /*LOD_E_OUT_OF_ARENA*/);
+      return;
+    }
+    if (gtid() == 0) {
+      if (fresh > 0) ctrl->arena_off = end;
+      ctrl->free_count = F - (M < F ? M : F);
+      ctrl->allocated_total = A + fresh;
+    }
+  }
   const long long K = (long long)ctrl->n_keys;
   for (long long d = gtid(); d < K; d += gstride()) {
     const int n = seg_node[d];

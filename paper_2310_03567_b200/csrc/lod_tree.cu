@@ -730,16 +730,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       if (t->ghist.cap > oldg) CK(cudaMemsetAsync(t->ghist.p, 0, (size_t)t->ghist.cap * 4, st));
       if (t->nodecnt.cap > oldn) CK(cudaMemsetAsync(t->nodecnt.p + oldn, 0, (size_t)(t->nodecnt.cap - oldn) * 4, st));
     }
-    const long long lbw = radix_lb_elems(n_items);
-    long long *n_items_dev = &t->d_ctrl->n_items;
-    lod::launch(k_radix_prep, std::min<unsigned>(grid_for(n_items, kRadixBlock * kPrepItems), 148 * kPrepBlocksPerSM),
-                kRadixBlock, 0, st, node_of, n_all, t->bnode.p, num_nodes, t->keys.p, t->nodecnt.p, t->hist.p, lbw,
-                &t->d_ctrl->n_used, n_items_dev, guard);
-    lod::launch(k_radix_ghist, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p, num_nodes,
-                passes, t->ghist.p, guard);
-    // ---- allocation (update.py:317-331): touched nodes = nodes with new samples, ascending id.
-    // It needs only the per-node counts, so it runs before the sort, whose last
-    // pass then writes every record straight into its chunk slot.
+    // allocation scratch (segments, chunk needs, write lists, pool rows)
     const long long Kb = num_nodes + 1;  // bound on touched nodes
     RK(t->seg_node.ensure(Kb, st));
     RK(t->seg_start.ensure(Kb + 1, st));
@@ -751,14 +742,22 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     RK(t->wl.ensure(acq_bound + Kb + 1, st));
     const long long alloc0 = t->h_ctrl->allocated_total;
     RK(ensure_chunks(t, alloc0 + acq_bound + 1, alloc0));
-    lod::launch(k_seg_pairs, grid_for(num_nodes), 256, 0, st, t->nodecnt.p, num_nodes, t->plan_ex.p, guard);
+    const long long lbw = radix_lb_elems(n_items);
+    long long *n_items_dev = &t->d_ctrl->n_items;
+    lod::launch(k_radix_prep, std::min<unsigned>(grid_for(n_items, kRadixBlock * kPrepItems), 148 * kPrepBlocksPerSM),
+                kRadixBlock, 0, st, node_of, n_all, t->bnode.p, num_nodes, t->keys.p, t->nodecnt.p, t->hist.p, lbw,
+                &t->d_ctrl->n_used, n_items_dev, guard);
+    lod::launch(k_radix_ghist, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p, num_nodes,
+                passes, t->ghist.p, t->plan_ex.p, guard);
+    // ---- allocation (update.py:317-331): touched nodes = nodes with new samples, ascending id.
+    // It needs only the per-node counts, so it runs before the sort, whose last
+    // pass then writes every record straight into its chunk slot.
     exclusive_scan_lb<U64x2>(t->plan_ex.p, t->plan_ex.p, num_nodes, &t->d_ctrl->seg_tot, t->lb64, st, guard);
     lod::launch(k_seg_list, grid_for(num_nodes), 256, 0, st, t->nd, t->geo, t->nodecnt.p, num_nodes, t->plan_ex.p,
                 t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->d_ctrl, t->ghist.p, guard);
     exclusive_scan_lb<U64x2>(t->plan.p, t->plan_ex.p, Kb, &t->d_ctrl->acq_tot, t->lb64, st, guard);
-    lod::launch(k_alloc_begin, 1, 1, 0, st, t->d_ctrl, t->geo, t->arena_cap, guard);
     lod::launch(k_alloc_nodes, grid_for(Kb), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p,
-                t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl, guard);
+                t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl, t->arena_cap, guard);
     lod::launch(k_alloc_chunks, grid_for(acq_bound), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p,
                 t->seg_start.p, t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl, guard);
     mark(3);

@@ -14,7 +14,7 @@ import numpy as np
 from .errors import BacklogOverflow, OutOfArena, SpillOverflow
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lodb200.so")
+LIB_PATH = os.environ.get("LOD_B200_LIB") or os.path.join(_HERE, "_lodb200.so")  # override: A/B experiments
 
 LOD_OK = 0
 LOD_E_OUT_OF_ARENA = 1

@@ -675,7 +675,10 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   // (rehashed) between iterations when the next pass could overfill it; a
   // table that still fills up falls back to a separate claim pass
   {
-    const long long want = std::max<long long>(3 * (t->prev_used + n) / 2, 1 << 20);
+#ifndef LOD_HASH_FACTOR_X4
+#define LOD_HASH_FACTOR_X4 6  // table slots ~ 1.5 x (previous cycle's claims + batch), next power of two
+#endif
+    const long long want = std::max<long long>(LOD_HASH_FACTOR_X4 * (t->prev_used + n) / 4, 1 << 20);
     const unsigned long long H = next_pow2((unsigned long long)want);
     if ((long long)H > t->hslots.cap) {
       RK(t->hslots.ensure((long long)H, st));

@@ -26,7 +26,13 @@ constexpr int kRadixBits = 8;
 constexpr int kRadixDigits = 1 << kRadixBits;
 constexpr int kRadixBlock = 256;  // 8 warps
 constexpr int kRadixWarps = kRadixBlock / 32;
-constexpr int kRadixRounds = 12;  // per warp: 12 rounds x 32 lanes (tile staged in 40 KB smem)
+#ifndef LOD_RADIX_ROUNDS
+#define LOD_RADIX_ROUNDS 8  // measured: 8 > 6, 12 > 4 (update bench, same box)
+#endif
+#ifndef LOD_RADIX_MINB
+#define LOD_RADIX_MINB 4
+#endif
+constexpr int kRadixRounds = LOD_RADIX_ROUNDS;  // per warp: 8 rounds x 32 lanes (2048-item tile, ~27 KB smem)
 constexpr int kRadixTile = kRadixBlock * kRadixRounds;
 constexpr int kMaxPasses = 4;
 constexpr int kNodeHistSmem = 10240;  // node counts kept in shared memory up to this many nodes
@@ -117,7 +123,7 @@ struct KVSink {
 // One LSD pass.  vals_in == nullptr means the identity permutation.
 // `lb` holds ntiles * 256 look-back words + 1 tile ticket, zeroed before the pass.
 template <class Sink>
-static __global__ void __launch_bounds__(kRadixBlock, 4)
+static __global__ void __launch_bounds__(kRadixBlock, LOD_RADIX_MINB)
     k_onesweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in, long long n_max,
                const long long *__restrict__ n_dev, int shift, const uint32_t *__restrict__ ghist_pass, uint32_t *lb,
                long long ntiles, Sink sink, uint32_t *lb_next, const int *guard) { lod::pdl_wait();

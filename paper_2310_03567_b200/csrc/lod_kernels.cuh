@@ -230,7 +230,7 @@ __global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl
 // node became inner, starting at that node (its stored bmin equals the
 // accumulated descent bounds byte for byte, _kernels.py:9-13).
 #ifndef LOD_COUNT_MINB
-#define LOD_COUNT_MINB 5  // blocks per SM: 51 registers
+#define LOD_COUNT_MINB 6  // blocks per SM (40 registers; same-box A/B: 6 > 5 > 4, 8)
 #endif
 __global__ void __launch_bounds__(256, LOD_COUNT_MINB)
     k_count(NodeCols nd, Geo geo, PointSrc src, NodeOf node_of, long long n, int first,

@@ -399,6 +399,19 @@ static void release_scan_lb(ScanLB &lb) {
 
 static int issue_stage(LodTree *t, LodTree::Stage &sg);
 
+// Issue the queued batches' deferred H2D copies behind the work queued so far.
+static int issue_pending(LodTree *t) {
+  if (!t->cst) return LOD_OK;
+  bool any = false;
+  for (auto &sg : t->stage) any |= sg.valid && sg.pending;
+  if (!any) return LOD_OK;
+  CK(cudaEventRecord(t->ev_counted, t->st));
+  CK(cudaStreamWaitEvent(t->cst, t->ev_counted, 0));
+  for (auto &sg : t->stage)
+    if (sg.valid && sg.pending) RK(issue_stage(t, sg));
+  return LOD_OK;
+}
+
 static void fill_stats(LodTree *t, LodBatchStats *s) {
   const Ctrl &c = *t->h_ctrl;
   s->num_nodes = c.num_nodes;
@@ -822,16 +835,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     if (prof) cudaEventRecord(t->ev[12], st);
     lod::launch(k_count, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, node_of, n_all, first, grid32, hs,
                 t->touched.p, t->d_ctrl);
-    if (first && t->cst) {  // queued batches' copies start once this count pass is done
-      bool any = false;
-      for (auto &sg : t->stage) any |= sg.valid && sg.pending;
-      if (any) {
-        CK(cudaEventRecord(t->ev_counted, st));
-        CK(cudaStreamWaitEvent(t->cst, t->ev_counted, 0));
-        for (auto &sg : t->stage)
-          if (sg.valid && sg.pending) RK(issue_stage(t, sg));
-      }
-    }
+    if (first) RK(issue_pending(t));  // queued batches' copies start once this count pass is done
     if (prof) cudaEventRecord(t->ev[13], st);
     lod::launch(k_decide, 1, kDecideBlock, 0, st, t->nd, t->geo, t->touched.p, t->bitmap.p, t->word_prefix.p,
                                          t->split_list.p, t->srank.p, t->scnt.p, t->schk.p, t->spill_off.p,

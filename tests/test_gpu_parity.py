@@ -104,11 +104,14 @@ def test_config1_one_million_uniform(gpu):
 
 
 def test_terrain_stream_matches_oracle(gpu):
-    """Config 2 shape (gen_surface 1M batches, paper parameters), a 4-batch prefix."""
+    """Config 2 exactly as bench.py streams it (gen_surface 1M batches, seeds
+    1000+i, paper parameters): a 60-batch prefix, through the spill bursts of
+    batches 12-13 (3.4M points) and 51 (5.8M points)."""
     from paper_2310_03567_b200 import synth
 
-    params = _params(arena_bytes=2 << 30, grid_res=128, leaf_threshold=50_000, max_depth=20, chunk_capacity=1000)
-    batches = [synth.gen_surface(1_000_000, 100 + i) for i in range(4)]
+    params = _params(arena_bytes=4 << 30, grid_res=128, leaf_threshold=50_000, max_depth=20, chunk_capacity=1000,
+                     backlog_capacity=64_000_000)
+    batches = [synth.gen_surface(1_000_000, 1000 + i) for i in range(60)]
     ot, _, oper = run_oracle(params, batches)
     tree, state, err, per = run_product(params, batches)
     assert err == ""

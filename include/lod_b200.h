@@ -42,7 +42,9 @@ enum {
     LOD_FLAG_DEVICE_INPUT = 1, /* xyz / rgba are device pointers (resident in HBM)          */
     LOD_FLAG_DEVICE_FB = 2,    /* framebuffer pointer is a device pointer                   */
     LOD_FLAG_PROFILE = 4,      /* record per-phase CUDA-event times into LodBatchStats      */
-    LOD_FLAG_DELTA = 8         /* capture the cycle's BatchDelta (collect_delta=True)       */
+    LOD_FLAG_DELTA = 8,        /* capture the cycle's BatchDelta (collect_delta=True)       */
+    LOD_FLAG_PACKED = 16       /* xyz points at n 16-byte records (f32 x,y,z | u32 rgba);
+                                  rgba is ignored (may be NULL)                              */
 };
 
 typedef struct LodTree LodTree;
@@ -207,6 +209,18 @@ int lod_raster_points(int32_t device, const float *xyz, const uint32_t *rgba, in
 int lod_morton_sort(int32_t device, const double *bmin, double scale, int32_t bits, const float *xyz,
                     const uint32_t *rgba, int64_t n, float *xyz_out, uint32_t *rgba_out, uint64_t *keys_out,
                     int flags);
+
+/* Multi-GPU routing, local half: bucket a stripe of points by
+ * owner rank -- owner_of_prefix[octant path over `depth` levels], the path
+ * computed with the reference's float64 descent rule -- keeping input order
+ * inside each bucket, as packed 16-byte records in out_records (bucket r at
+ * starts[r], counts[r] records).  xyz / rgba / out_records / counts / starts
+ * are DEVICE pointers; owner_of_prefix is a host array of 8^depth ranks;
+ * `stream` is the cudaStream_t to order the work on (NULL = legacy default).
+ * Asynchronous: counts / starts are valid once the stream reaches them. */
+int lod_route_bucket(int32_t device, const double *bmin, double size, int32_t depth, const int32_t *owner_of_prefix,
+                     int32_t world, const float *xyz, const uint32_t *rgba, int64_t n, void *out_records,
+                     int64_t *counts, int64_t *starts, void *stream);
 
 /* Device-side helpers for benchmarking the resident path (inputs in HBM). */
 int lod_device_alloc(int32_t device, uint64_t bytes, void **ptr);

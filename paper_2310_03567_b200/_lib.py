@@ -29,6 +29,7 @@ LOD_FLAG_DEVICE_INPUT = 1
 LOD_FLAG_DEVICE_FB = 2
 LOD_FLAG_PROFILE = 4
 LOD_FLAG_DELTA = 8
+LOD_FLAG_PACKED = 16
 LOD_NPHASE = 10
 PHASES = ("count", "split", "resolve", "backlog", "alloc", "sort", "delta", "epilogue", "h2d", "total")
 
@@ -120,6 +121,8 @@ SIGNATURES = {
     "lod_raster_points": (ctypes.c_int, [ctypes.c_int32, _P, _P, _I64, _P, _P, _I64, _I64, ctypes.c_int]),
     "lod_morton_sort": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_double, ctypes.c_int32, _P, _P, _I64, _P, _P,
                                        _P, ctypes.c_int]),
+    "lod_route_bucket": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_double, ctypes.c_int32, _P, ctypes.c_int32, _P, _P,
+                                        _I64, _P, _P, _P, _P]),
     "lod_device_alloc": (ctypes.c_int, [ctypes.c_int32, ctypes.c_uint64, ctypes.POINTER(_P)]),
     "lod_device_free": (ctypes.c_int, [_P]),
     "lod_memcpy_h2d": (ctypes.c_int, [_P, _P, ctypes.c_uint64]),

@@ -20,7 +20,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lodb200.so")
-SOURCES = ["lod_tree.cu", "lod_raster.cu", "lod_morton.cu"]
+SOURCES = ["lod_tree.cu", "lod_raster.cu", "lod_morton.cu", "lod_route.cu"]
 HEADERS = ["lod_common.cuh", "lod_kernels.cuh", "radix.cuh", "scan.cuh"]
 
 

@@ -159,17 +159,19 @@ struct Geo {
 };
 
 // One point source over the reference's all-array [spill || batch]
-// (update.py:281-286): spill points are 16-byte records, batch points come
-// straight from the caller's xyz (n,3) f32 + rgba (n,) u32 arrays.
+// (update.py:281-286): spill points are 16-byte records; batch points come
+// from the caller's xyz (n,3) f32 + rgba (n,) u32 arrays, or from 16-byte
+// records when the batch arrives packed (brec; e.g. routed from other ranks).
 struct PointSrc {
   const float4 *spill;
   long long ns;
   const float *bxyz;
   const uint32_t *brgba;
   long long nb;
+  const float4 *brec;  // packed batch records, or null
   __device__ __forceinline__ void xyz(long long j, float &x, float &y, float &z) const {
-    if (j < ns) {
-      float4 r = __ldg(spill + j);
+    if (j < ns || brec) {
+      const float4 r = j < ns ? __ldg(spill + j) : __ldg(brec + (j - ns));
       x = r.x; y = r.y; z = r.z;
     } else {
       const float *p = bxyz + 3 * (j - ns);
@@ -178,6 +180,7 @@ struct PointSrc {
   }
   __device__ __forceinline__ float4 record(long long j) const {
     if (j < ns) return __ldg(spill + j);
+    if (brec) return __ldg(brec + (j - ns));
     const float *p = bxyz + 3 * (j - ns);
     float4 r;
     r.x = __ldg(p); r.y = __ldg(p + 1); r.z = __ldg(p + 2);
@@ -185,7 +188,8 @@ struct PointSrc {
     return r;
   }
   __device__ __forceinline__ uint32_t rgba(long long j) const {
-    return j < ns ? __float_as_uint(__ldg(spill + j).w) : __ldg(brgba + (j - ns));
+    if (j < ns) return __float_as_uint(__ldg(spill + j).w);
+    return brec ? __float_as_uint(__ldg(brec + (j - ns)).w) : __ldg(brgba + (j - ns));
   }
 };
 

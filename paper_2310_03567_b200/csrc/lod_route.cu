@@ -1,0 +1,222 @@
+// lod_route.cu -- multi-GPU point routing, local half.
+//
+// Every rank holds a stripe of each global batch in global order.  Before the
+// all-to-all, its points are bucketed by owner rank -- the rank that owns the
+// point's depth-L octant prefix, computed with the reference's exact float64
+// descent rule (x >= bx + h per axis, _kernels.py:44-56) -- keeping input
+// order inside every bucket, and packed into 16-byte records
+// (f32 x, y, z | u32 rgba, store.py:14-16) ready to send.  Three launches:
+//   k_route_count   owner per point (kept as a byte), per-tile bucket counts;
+//   k_route_scan    per-bucket exclusive scans over the tiles + bucket starts;
+//   k_route_scatter warp-ordered stable ranks inside each tile, 16-byte writes.
+// The bucket sizes stay on the device for the caller (the split sizes of the
+// collective); no host round trip happens here.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/lod_b200.h"
+#include "lod_common.cuh"
+#include "scan.cuh"
+
+using namespace lod;
+
+namespace {
+
+constexpr int kRouteBlock = 256;
+constexpr int kRouteRounds = 8;  // per warp: 8 x 32 consecutive points
+constexpr int kRouteTile = kRouteBlock * kRouteRounds;
+constexpr int kRouteMaxWorld = 64;
+
+struct RouteGeo {
+  double bmin[3];
+  double size;
+  int depth;
+  int world;
+};
+
+__device__ __forceinline__ int owner_of(const RouteGeo &g, const int32_t *__restrict__ table, float xf, float yf,
+                                        float zf) {
+  const double x = xf, y = yf, z = zf;
+  double bx = g.bmin[0], by = g.bmin[1], bz = g.bmin[2], s = g.size;
+  int key = 0;
+  for (int l = 0; l < g.depth; ++l) key = key * 8 + octant_step(x, y, z, bx, by, bz, s);
+  return __ldg(table + key);
+}
+
+__global__ void __launch_bounds__(kRouteBlock)
+    k_route_count(const float *__restrict__ xyz, long long n, RouteGeo g, const int32_t *__restrict__ table,
+                  uint8_t *__restrict__ owner, uint32_t *__restrict__ tile_counts) { lod::pdl_wait();
+  __shared__ uint32_t cnt[kRouteMaxWorld];
+  for (int d = threadIdx.x; d < g.world; d += kRouteBlock) cnt[d] = 0;
+  __syncthreads();
+  const long long t0 = (long long)blockIdx.x * kRouteTile;
+  for (int r = 0; r < kRouteRounds; ++r) {
+    const long long i = t0 + r * kRouteBlock + threadIdx.x;
+    if (i < n) {
+      const int o = owner_of(g, table, __ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1), __ldg(xyz + 3 * i + 2));
+      owner[i] = (uint8_t)o;
+      atomicAdd(&cnt[o], 1u);
+    }
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < g.world; d += kRouteBlock) tile_counts[(long long)blockIdx.x * g.world + d] = cnt[d];
+}
+
+// One CTA: per bucket, the exclusive scan of its tile counts (in place), the
+// bucket totals and the bucket starts (exclusive scan of the totals).
+__global__ void __launch_bounds__(1024)
+    k_route_scan(uint32_t *__restrict__ tile_counts, long long ntiles, int world, long long *__restrict__ counts,
+                 long long *__restrict__ starts) { lod::pdl_wait();
+  __shared__ uint32_t sh[1024 / 32 + 1];
+  __shared__ long long s_tot[kRouteMaxWorld];
+  for (int d = 0; d < world; ++d) {
+    uint32_t carry = 0;
+    for (long long base = 0; base < ntiles; base += 1024) {
+      const long long t = base + threadIdx.x;
+      const uint32_t v = t < ntiles ? tile_counts[t * world + d] : 0u;
+      uint32_t tot;
+      const uint32_t ex = block_exclusive_scan<uint32_t, 1024>(v, sh, tot);
+      if (t < ntiles) tile_counts[t * world + d] = carry + ex;
+      carry += tot;
+    }
+    if (threadIdx.x == 0) s_tot[d] = carry;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long run = 0;
+    for (int d = 0; d < world; ++d) {
+      starts[d] = run;
+      counts[d] = s_tot[d];
+      run += s_tot[d];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kRouteBlock)
+    k_route_scatter(const float *__restrict__ xyz, const uint32_t *__restrict__ rgba, long long n, int world,
+                    const uint8_t *__restrict__ owner, const uint32_t *__restrict__ tile_off,
+                    const long long *__restrict__ starts, float4 *__restrict__ out) { lod::pdl_wait();
+  __shared__ uint32_t wtot[kRouteBlock / 32][kRouteMaxWorld];  // per-warp bucket totals -> warp offsets
+  __shared__ uint16_t lrank[kRouteTile];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = lanemask_lt();
+  const long long t0 = (long long)blockIdx.x * kRouteTile;
+  const int wofs = warp * 32 * kRouteRounds;  // each warp ranks a contiguous run of the tile
+  // lane d keeps the warp's running count of bucket d (and d + 32)
+  uint32_t run0 = 0, run1 = 0;
+  for (int r = 0; r < kRouteRounds; ++r) {
+    const int li = wofs + r * 32 + lane;
+    const long long i = t0 + li;
+    const int o = i < n ? owner[i] : kRouteMaxWorld;  // out-of-range lanes form their own group
+    const unsigned peers = __match_any_sync(0xffffffffu, o);
+    const uint32_t b0 = __shfl_sync(0xffffffffu, run0, o & 31);  // both shuffles in every lane (converged)
+    const uint32_t b1 = __shfl_sync(0xffffffffu, run1, o & 31);
+    const uint32_t before = o < 32 ? b0 : b1;
+    if (i < n) lrank[li] = (uint16_t)(before + __popc(peers & lt));
+    for (int d = 0; d < world; ++d) {  // world <= 64 ballots per round
+      const unsigned m = __ballot_sync(0xffffffffu, o == d);
+      if (lane == (d & 31)) {
+        if (d < 32) run0 += __popc(m);
+        else run1 += __popc(m);
+      }
+    }
+  }
+  if (lane < world) wtot[warp][lane] = run0;
+  if (lane + 32 < world) wtot[warp][lane + 32] = run1;
+  __syncthreads();
+  for (int d = threadIdx.x; d < world; d += kRouteBlock) {
+    uint32_t acc = 0;
+    for (int w = 0; w < kRouteBlock / 32; ++w) {
+      const uint32_t c = wtot[w][d];
+      wtot[w][d] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+  for (int r = 0; r < kRouteRounds; ++r) {
+    const int li = wofs + r * 32 + lane;
+    const long long i = t0 + li;
+    if (i >= n) continue;
+    const int o = owner[i];
+    const long long pos = starts[o] + tile_off[(long long)blockIdx.x * world + o] + wtot[warp][o] + lrank[li];
+    out[pos] = make_float4(__ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1), __ldg(xyz + 3 * i + 2),
+                           __uint_as_float(__ldg(rgba + i)));
+  }
+}
+
+inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+int cuda_rc(cudaError_t e) {
+  if (e == cudaSuccess) return LOD_OK;
+  fprintf(stderr, "[lod_b200] CUDA error: %s\n", cudaGetErrorString(e));
+  return LOD_E_CUDA;
+}
+#define CK(expr)               \
+  do {                         \
+    int rc__ = cuda_rc(expr);  \
+    if (rc__) return rc__;     \
+  } while (0)
+
+struct RouteScratch {
+  uint8_t *owner = nullptr;
+  uint32_t *tiles = nullptr;
+  int32_t *table = nullptr;
+  long long cap = 0, tcap = 0, table_cap = 0;
+};
+std::mutex g_mu;
+RouteScratch g_rs[64];
+
+}  // namespace
+
+extern "C" {
+
+int lod_route_bucket(int32_t device, const double *bmin, double size, int32_t depth, const int32_t *owner_of_prefix,
+                     int32_t world, const float *xyz, const uint32_t *rgba, int64_t n, void *out_records,
+                     int64_t *counts, int64_t *starts, void *stream) {
+  if (!bmin || !owner_of_prefix || depth < 0 || depth > 8 || world < 1 || world > kRouteMaxWorld || n < 0 ||
+      (n > 0 && (!xyz || !rgba || !out_records)) || !counts || !starts || device < 0 || device >= 64)
+    return LOD_E_ARG;
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaSetDevice(device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  RouteScratch &s = g_rs[device];
+  const long long ntiles = std::max<long long>((n + kRouteTile - 1) / kRouteTile, 1);
+  if (n > s.cap) {
+    if (s.owner) cudaFree(s.owner);
+    s.cap = std::max<long long>(n, 2 * s.cap);
+    CK(cudaMalloc(&s.owner, (size_t)s.cap));
+  }
+  if (ntiles * world > s.tcap) {
+    if (s.tiles) cudaFree(s.tiles);
+    s.tcap = std::max<long long>(ntiles * world, 2 * s.tcap);
+    CK(cudaMalloc(&s.tiles, (size_t)s.tcap * 4));
+  }
+  const long long tsize = 1LL << (3 * depth);
+  if (tsize > s.table_cap) {
+    if (s.table) cudaFree(s.table);
+    s.table_cap = tsize;
+    CK(cudaMalloc(&s.table, (size_t)tsize * 4));
+  }
+  for (long long k = 0; k < tsize; ++k)
+    if (owner_of_prefix[k] < 0 || owner_of_prefix[k] >= world) return LOD_E_ARG;
+  CK(cudaMemcpyAsync(s.table, owner_of_prefix, (size_t)tsize * 4, cudaMemcpyHostToDevice, st));
+  RouteGeo g;
+  memcpy(g.bmin, bmin, sizeof(g.bmin));
+  g.size = size;
+  g.depth = depth;
+  g.world = world;
+  if (n > 0)
+    lod::launch(k_route_count, cdiv(n, kRouteTile), kRouteBlock, 0, st, xyz, (long long)n, g, s.table, s.owner,
+                s.tiles);
+  else
+    CK(cudaMemsetAsync(s.tiles, 0, (size_t)world * 4, st));
+  lod::launch(k_route_scan, 1, 1024, 0, st, s.tiles, ntiles, (int)world, (long long *)counts, (long long *)starts);
+  if (n > 0)
+    lod::launch(k_route_scatter, cdiv(n, kRouteTile), kRouteBlock, 0, st, xyz, rgba, (long long)n, (int)world,
+                s.owner, s.tiles, (const long long *)starts, reinterpret_cast<float4 *>(out_records));
+  return cuda_rc(cudaGetLastError());
+}
+
+}  // extern "C"

@@ -191,6 +191,7 @@ struct LodTree {
   ScanLB lb32, lb64;  // single-pass scan state (u32 win counts; U64x2 segment / need pairs)
   // inputs / outputs
   DBuf<float> in_xyz;
+  DBuf<float4> in_rec;  // packed host input (LOD_FLAG_PACKED)
   DBuf<uint32_t> in_rgba;
   DBuf<float4> gbuf;
   DBuf<int32_t> gnodes;
@@ -581,7 +582,7 @@ int lod_tree_destroy(LodTree *t) {
   t->dense.release();
   t->seg_node.release(); t->wl.release(); t->seg_start.release();
   t->plan.release(); t->plan_ex.release(); t->in_xyz.release();
-  t->in_rgba.release(); t->gbuf.release(); t->gnodes.release(); t->goff.release(); t->gstart.release();
+  t->in_rgba.release(); t->in_rec.release(); t->gbuf.release(); t->gnodes.release(); t->goff.release(); t->gstart.release();
   t->visflag.release(); t->vislist.release(); t->fb.release(); t->counter.release();
   release_scan_lb(t->lb32);
   release_scan_lb(t->lb64);
@@ -623,7 +624,8 @@ int lod_tree_info(LodTree *t, LodTreeInfo *info) {
 
 int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t n,
                      const LodLimits *limits, int flags, LodBatchStats *stats) {
-  if (!t || n < 0 || (n > 0 && (!xyz || !rgba))) return LOD_E_ARG;
+  const bool packed = (flags & LOD_FLAG_PACKED) != 0;
+  if (!t || n < 0 || (n > 0 && (!xyz || (!rgba && !packed)))) return LOD_E_ARG;
   LodBatchStats local{};
   LodBatchStats &S = stats ? *stats : local;
   memset(&S, 0, sizeof(S));
@@ -662,8 +664,17 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   // ---- inputs
   const float *bx = xyz;
   const uint32_t *bc = rgba;
+  const float4 *brec = nullptr;  // packed 16-byte input records
   LodTree::Stage *staged = nullptr;
-  if (!(flags & LOD_FLAG_DEVICE_INPUT)) {
+  if (packed) {
+    if (flags & LOD_FLAG_DEVICE_INPUT) {
+      brec = reinterpret_cast<const float4 *>(xyz);
+    } else {
+      RK(t->in_rec.ensure(n, st));
+      CK(cudaMemcpyAsync(t->in_rec.p, xyz, (size_t)n * 16, cudaMemcpyHostToDevice, st));
+      brec = t->in_rec.p;
+    }
+  } else if (!(flags & LOD_FLAG_DEVICE_INPUT)) {
     for (auto &sg : t->stage)
       if (sg.valid && sg.hx == xyz && sg.hc == rgba && sg.n == n) staged = &sg;
   }
@@ -673,7 +684,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     staged->valid = false;
     bx = staged->xyz.p;
     bc = staged->rgba.p;
-  } else if (!(flags & LOD_FLAG_DEVICE_INPUT)) {
+  } else if (!packed && !(flags & LOD_FLAG_DEVICE_INPUT)) {
     RK(t->in_xyz.ensure(3 * n, st));
     RK(t->in_rgba.ensure(n, st));
     CK(cudaMemcpyAsync(t->in_xyz.p, xyz, (size_t)n * 12, cudaMemcpyHostToDevice, st));
@@ -685,7 +696,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   lod::launch(k_cycle_begin, 1, 1, 0, st, t->d_ctrl);
   // ---- expansion (update.py:273-296) with the voxel claims folded in
   RK(t->node_b.ensure(n, st));
-  PointSrc src{nullptr, 0, bx, bc, n};
+  PointSrc src{nullptr, 0, bx, bc, n, brec};
   NodeOf node_of{nullptr, t->node_b.p, 0};
   long long n_all = n, n_s = 0;
   int first = 1, iters = 0;

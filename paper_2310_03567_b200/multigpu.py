@@ -82,22 +82,52 @@ def owners_device(xyz, plan: partition.Plan, bmin=(0.0, 0.0, 0.0), size: float =
     return owner[key]
 
 
+def bucket(xyz, rgba, plan: partition.Plan, world: int, bmin=(0.0, 0.0, 0.0), size: float = 1.0):
+    """Stable bucketing of one stripe by owner rank into packed 16-byte records
+    (CUDA tensors in; lod_route_bucket: owner prefix + per-tile counts, scans,
+    warp-ordered stable scatter).  Returns (records (n, 4) int32, counts (world,)
+    int64, starts (world,) int64), all on the device."""
+    import torch
+
+    dev = xyz.device
+    n = int(rgba.shape[0])
+    out = torch.empty((n, 4), dtype=torch.int32, device=dev)
+    counts = torch.empty(world, dtype=torch.int64, device=dev)
+    starts = torch.empty(world, dtype=torch.int64, device=dev)
+    table = np.ascontiguousarray(plan.owner, np.int32)
+    b = np.ascontiguousarray(bmin, np.float64)
+    x = xyz.contiguous()
+    c = rgba.contiguous()
+    L = _lib.load()
+    _lib.check(L.lod_route_bucket(dev.index, _lib.ptr(b), float(size), int(plan.depth), _lib.ptr(table), int(world),
+                                  _lib.ptr(x), _lib.ptr(c), n, _lib.ptr(out), _lib.ptr(counts), _lib.ptr(starts),
+                                  torch.cuda.current_stream(dev).cuda_stream), "route_bucket")
+    return out, counts, starts
+
+
 def route(xyz, rgba, plan: partition.Plan, world: int, group=None):
-    """All-to-all routing of one stripe (CUDA tensors, global order) to the
-    owners of its points; returns this rank's points in global order."""
+    """All-to-all routing of one stripe (global order) to the owners of its
+    points; returns this rank's points as packed 16-byte records (n, 4) int32
+    in global order (receivers concatenate by source rank).
+
+    CUDA tensors are bucketed by the lod_route_bucket kernels; CPU tensors
+    (the gloo test path) by the same rule in torch."""
     import torch
     import torch.distributed as dist
 
-    own = owners_device(xyz, plan)
-    order = torch.sort(own, stable=True).indices  # bucket by owner, keep order
-    rec = torch.cat([xyz.contiguous().view(torch.int32), rgba.view(torch.int32).reshape(-1, 1)], dim=1)[order]
-    send_counts = torch.bincount(own, minlength=world).to(torch.int64)
+    if xyz.is_cuda:
+        rec, send_counts, _ = bucket(xyz, rgba, plan, world)
+    else:
+        own = owners_device(xyz, plan)
+        order = torch.sort(own, stable=True).indices  # bucket by owner, keep order
+        rec = torch.cat([xyz.contiguous().view(torch.int32), rgba.view(torch.int32).reshape(-1, 1)], dim=1)[order]
+        send_counts = torch.bincount(own, minlength=world).to(torch.int64)
     recv_counts = torch.empty_like(send_counts)
     dist.all_to_all_single(recv_counts, send_counts, group=group)
     rc, sc = recv_counts.tolist(), send_counts.tolist()
     out = torch.empty((sum(rc), 4), dtype=torch.int32, device=xyz.device)
     dist.all_to_all_single(out, rec.contiguous(), rc, sc, group=group)
-    return out[:, :3].contiguous().view(torch.float32), out[:, 3].contiguous()
+    return out
 
 
 def composite_min(fb_cells_dev, group=None):
@@ -125,13 +155,15 @@ class PartitionedInserter:
         import torch
         import torch.distributed as dist
 
-        from .update import insert_batch
+        from .update import insert_batch, insert_records
 
         if self.partitioned:
-            if self.world > 1:
-                xyz, rgba = route(xyz, rgba, self.plan, self.world, self.group)
-            insert_batch(self.tree, xyz, rgba, self.state)
-            return int(rgba.shape[0])
+            if self.world == 1:
+                insert_batch(self.tree, xyz, rgba, self.state)
+                return int(rgba.shape[0])
+            rec = route(xyz, rgba, self.plan, self.world, self.group)
+            insert_records(self.tree, rec, self.state)
+            return int(rec.shape[0])
         # warm-up: gather stripes to rank 0 (rank order = global order)
         n = torch.tensor([rgba.shape[0]], dtype=torch.int64, device=xyz.device)
         sizes = [torch.zeros_like(n) for _ in range(self.world)]
@@ -145,8 +177,7 @@ class PartitionedInserter:
         got = 0
         if self.rank == 0:
             allrec = torch.cat([b[: int(s.item())] for b, s in zip(bufs, sizes)])
-            insert_batch(self.tree, allrec[:, :3].contiguous().view(torch.float32), allrec[:, 3].contiguous(),
-                         self.state)
+            insert_records(self.tree, allrec, self.state)
             got = int(allrec.shape[0])
         flag = torch.tensor([1 if (self.rank == 0 and top_is_inner(self.tree, self.plan.depth)) else 0],
                             device=xyz.device)

@@ -28,6 +28,7 @@ __all__ = [
     "VoxelBacklog",
     "chunks_needed",
     "insert_batch",
+    "insert_records",
     "run_frame_updates",
 ]
 
@@ -193,6 +194,50 @@ def insert_batch(
                                   ctypes.byref(lim), flags, ctypes.byref(bs))
     tree._invalidate()
     _lib.check(rc, "insert_batch")
+    _account(state, bs, n_batch, profile)
+    st = state.stats
+    delta = _read_delta(tree) if collect_delta else None
+    dt = time.perf_counter() - t0
+    st.update_seconds += dt
+    st.max_batch_ms = max(st.max_batch_ms, dt * 1e3)
+    return delta
+
+
+def insert_records(tree: Octree, records, state: UpdateState, collect_delta: bool = False) -> BatchDelta | None:
+    """insert_batch for a batch already packed as 16-byte records
+    (f32 x, y, z | u32 rgba; store.py:14-16) -- e.g. the points routed to this
+    rank by multigpu.route.  ``records`` is a CUDA tensor (n, 4) of 4-byte
+    elements, or a numpy array of the same shape."""
+    t0 = time.perf_counter()
+    n_batch = int(records.shape[0])
+    if n_batch == 0:
+        return BatchDelta() if collect_delta else None
+    if hasattr(records, "is_cuda") and records.is_cuda:
+        if records.element_size() != 4 or records.dim() != 2 or records.shape[1] != 4:
+            raise TypeError("records must be an (n, 4) tensor of 4-byte elements")
+        rec, flags = records.contiguous(), _lib.LOD_FLAG_DEVICE_INPUT
+    else:
+        rec, flags = np.ascontiguousarray(records).reshape(-1, 4), 0
+        if rec.dtype.itemsize != 4:
+            raise TypeError("records must be (n, 4) of 4-byte elements")
+    flags |= _lib.LOD_FLAG_PACKED | (_lib.LOD_FLAG_DELTA if collect_delta else 0)
+    lim = state._limits
+    lim.backlog_capacity = state.config.backlog_capacity
+    lim.spill_capacity = state.config.spill_capacity
+    bs = state._bstats
+    rc = tree._L.lod_insert_batch(tree.handle, _lib.ptr(rec), None, n_batch, ctypes.byref(lim), flags, ctypes.byref(bs))
+    tree._invalidate()
+    _lib.check(rc, "insert_records")
+    _account(state, bs, n_batch, profile=False)
+    delta = _read_delta(tree) if collect_delta else None
+    dt = time.perf_counter() - t0
+    state.stats.update_seconds += dt
+    state.stats.max_batch_ms = max(state.stats.max_batch_ms, dt * 1e3)
+    return delta
+
+
+def _account(state: UpdateState, bs, n_batch: int, profile: bool) -> None:
+    """UpdateStats bookkeeping of one cycle (update.py:382-392)."""
     st = state.stats
     n_v, n_s = int(bs.n_voxels), int(bs.n_spill)
     st.batches += 1
@@ -208,15 +253,7 @@ def insert_batch(
     st.launches += int(bs.launches)
     st.h2d_bytes += int(bs.h2d_bytes)
     st.d2h_bytes += int(bs.d2h_bytes)
-    if profile:
-        state.last = bs.as_dict()
-    else:
-        state.last = None
-    delta = _read_delta(tree) if collect_delta else None
-    dt = time.perf_counter() - t0
-    st.update_seconds += dt
-    st.max_batch_ms = max(st.max_batch_ms, dt * 1e3)
-    return delta
+    state.last = bs.as_dict() if profile else None
 
 
 def _read_delta(tree: Octree) -> BatchDelta:

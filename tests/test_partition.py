@@ -128,10 +128,10 @@ def _route_worker(rank, world, port, out):
     plan = partition.plan_owners([(xyz, rgba)], world)
     n = len(rgba)
     st = slice(rank * n // world, (rank + 1) * n // world)
-    gx, gc = multigpu.route(torch.from_numpy(xyz[st].copy()), torch.from_numpy(rgba[st].view(np.int32).copy()),
-                            plan, world)
+    rec = multigpu.route(torch.from_numpy(xyz[st].copy()), torch.from_numpy(rgba[st].view(np.int32).copy()),
+                         plan, world).numpy()
     want_x, want_c = partition.take(plan, xyz, rgba, rank)
-    ok = np.array_equal(gx.numpy(), want_x) and np.array_equal(gc.numpy().view(np.uint32), want_c)
+    ok = np.array_equal(rec[:, :3].copy().view(np.float32), want_x) and np.array_equal(rec[:, 3].view(np.uint32), want_c)
     # framebuffer min-composite with the all-ones sentinel
     rng = np.random.default_rng(rank)
     fb = np.full(64, np.uint64(0xFFFFFFFFFFFFFFFF))

@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(256)
 
 __global__ void __launch_bounds__(256)
     k_scatter(Hash h, long long n_s, const uint32_t *__restrict__ wbase, uint32_t *__restrict__ wcount, PointSrc src,
-              int32_t *__restrict__ bnode, uint32_t *__restrict__ bcell, uint32_t *__restrict__ brgba,
+              uint4 *__restrict__ backlog,
               const int *guard) { lod::pdl_wait();
   if (guard && *guard) return;
   const long long H = (long long)h.mask + 1;
@@ -561,9 +561,7 @@ __global__ void __launch_bounds__(256)
     *reinterpret_cast<ulonglong2 *>(sl) = make_ulonglong2(kEmptyKey, kEmptyHi);
     const long long j = claim_index((uint32_t)kv.y, n_s);
     const uint32_t b = __ldg(wbase + j) + atomicSub(wcount + j, 1u) - 1u;
-    bnode[b] = (int32_t)(kv.x >> 32);
-    bcell[b] = (uint32_t)(kv.x & 0xFFFFFFFFu);
-    brgba[b] = src.rgba(j);
+    backlog[b] = make_uint4((uint32_t)(kv.x >> 32), (uint32_t)(kv.x & 0xFFFFFFFFu), src.rgba(j), 0u);
   }
 }
 
@@ -728,7 +726,7 @@ struct StoreSink {
   const int32_t *wl;
   long long n_all;
   PointSrc src;
-  const uint32_t *bcell, *brgba;
+  const uint4 *backlog;  // new voxels in backlog order: {node, cell, rgba, 0}
   const Ctrl *ctrl;
   __device__ __forceinline__ void operator()(uint32_t p, uint32_t key, uint32_t item) const {
     if (ctrl->error) return;
@@ -746,14 +744,15 @@ struct StoreSink {
       rec = src.record(i);
     } else {
       const long long b = i - n_all;
-      const long long cell = bcell[b];
+      const uint4 bl = backlog[b];
+      const long long cell = bl.y;
       const long long g = geo.g;
       const long long cx = cell % g, cy = (cell / g) % g, cz = cell / (g * g);
       const double step = geo.size_by_level[nd.level[n]] / (double)g;
       const double x = nd.bmin[3 * n] + ((double)cx + 0.5) * step;
       const double y = nd.bmin[3 * n + 1] + ((double)cy + 0.5) * step;
       const double z = nd.bmin[3 * n + 2] + ((double)cz + 0.5) * step;
-      rec = make_float4(__double2float_rn(x), __double2float_rn(y), __double2float_rn(z), __uint_as_float(brgba[b]));
+      rec = make_float4(__double2float_rn(x), __double2float_rn(y), __double2float_rn(z), __uint_as_float(bl.z));
     }
     float4 *dst = reinterpret_cast<float4 *>(arena + pool.payload_off[cid]) + off;
     *dst = rec;
@@ -845,7 +844,7 @@ __global__ void __launch_bounds__(kDeltaBlock)
 __global__ void k_delta_vox(const uint32_t *__restrict__ skeys, const uint32_t *__restrict__ svals,
                             const int32_t *__restrict__ dense, const long long *__restrict__ seg_start,
                             const long long *__restrict__ vbase, long long n_all,
-                            const uint32_t *__restrict__ bcell, const uint32_t *__restrict__ brgba,
+                            const uint4 *__restrict__ backlog,
                             uint32_t *__restrict__ dcell, uint32_t *__restrict__ drgba, const Ctrl *ctrl,
                             const int *guard) { lod::pdl_wait();
   if (guard && *guard) return;
@@ -856,8 +855,9 @@ __global__ void k_delta_vox(const uint32_t *__restrict__ skeys, const uint32_t *
     if (i < n_all) continue;
     const long long d = dense[skeys[p]];
     const long long pos = vbase[d] + (p - seg_start[d]);
-    dcell[pos] = bcell[i - n_all];
-    drgba[pos] = brgba[i - n_all];
+    const uint4 bl = backlog[i - n_all];
+    dcell[pos] = bl.y;
+    drgba[pos] = bl.z;
   }
 }
 

@@ -181,8 +181,7 @@ struct LodTree {
   long long prev_used = 0;  // claims of the previous cycle (sizes the table)
   int last_iters = 0;       // expansion iterations of the previous cycle (speculation policy)
   long long spec_hits = 0;  // cycles whose pipeline ran speculatively
-  DBuf<int32_t> bnode;
-  DBuf<uint32_t> bcell, brgba;
+  DBuf<uint4> backlog;  // the cycle's new voxels in backlog order: {node, cell, rgba, 0}
   // sort / alloc scratch
   DBuf<uint32_t> keys, keys_b, vals_a, vals_b, hist, ghist, nodecnt;
   DBuf<int32_t> seg_node, wl, dense;
@@ -577,7 +576,7 @@ int lod_tree_destroy(LodTree *t) {
   t->bitmap.release(); t->word_prefix.release(); t->tbits.release(); t->scnt.release(); t->schk.release();
   t->spill_off.release(); t->chunk_off.release(); t->spill.release(); t->hslots.release(); t->hslots2.release();
   t->hused.release(); t->srank.release(); t->wcount.release(); t->wbase.release();
-  t->bnode.release(); t->bcell.release(); t->brgba.release(); t->keys.release(); t->keys_b.release();
+  t->backlog.release(); t->keys.release(); t->keys_b.release();
   t->vals_a.release(); t->vals_b.release(); t->hist.release(); t->ghist.release(); t->nodecnt.release();
   t->dense.release();
   t->seg_node.release(); t->wl.release(); t->seg_start.release();
@@ -738,13 +737,11 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     if (nv > 0) lod::launch(k_resolve, grid_for((long long)t->hcap), 256, 0, st, t->nd, hs, grid32, n_s, t->wcount.p, guard);
     mark(1);
     tp("resolve_launched");
-    RK(t->bnode.ensure(std::max<long long>(nv, 1), st));
-    RK(t->bcell.ensure(std::max<long long>(nv, 1), st));
-    RK(t->brgba.ensure(std::max<long long>(nv, 1), st));
+    RK(t->backlog.ensure(std::max<long long>(nv, 1), st));
     if (nv > 0) {
       exclusive_scan_lb<uint32_t>(t->wcount.p, t->wbase.p, n_all, &t->d_ctrl->n_v, t->lb32, st, guard);
       lod::launch(k_scatter, grid_for((long long)t->hcap), 256, 0, st, hs, n_s, t->wbase.p, t->wcount.p, src,
-                  t->bnode.p, t->bcell.p, t->brgba.p, guard);
+                  t->backlog.p, guard);
     }
     mark(2);
     // ---- sort: every new sample by node id, stable (slot order)
@@ -778,7 +775,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     const long long lbw = radix_lb_elems(n_items);
     long long *n_items_dev = &t->d_ctrl->n_items;
     lod::launch(k_radix_prep, std::min<unsigned>(grid_for(n_items, kRadixBlock * kPrepItems), 148 * kPrepBlocksPerSM),
-                kRadixBlock, 0, st, node_of, n_all, t->bnode.p, num_nodes, t->keys.p, t->nodecnt.p, t->hist.p, lbw,
+                kRadixBlock, 0, st, node_of, n_all, t->backlog.p, num_nodes, t->keys.p, t->nodecnt.p, t->hist.p, lbw,
                 &t->d_ctrl->n_used, n_items_dev, guard);
     lod::launch(k_radix_ghist, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p, num_nodes,
                 passes, t->ghist.p, t->plan_ex.p, guard);
@@ -804,7 +801,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     rs.lb[0] = t->hist.p;
     rs.lb[1] = t->hist.p + lbw;
     const StoreSink sink{t->nd,   t->pool, t->geo, t->arena,   t->dense.p, t->seg_start.p, t->plan_ex.p,
-                         t->wl.p, n_all,   src,    t->bcell.p, t->brgba.p, t->d_ctrl};
+                         t->wl.p, n_all,   src,    t->backlog.p, t->d_ctrl};
     uint32_t *skeys = nullptr, *svals = nullptr;
     if (delta) {  // the delta reads the sorted order: materialise it, then store
       stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals, nullptr, 0, (const KVSink *)nullptr,
@@ -829,7 +826,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
                   t->dvstart.p, t->dvcount.p, t->dpnode.p, t->dpstart.p, t->dpcount.p, t->dvbase.p, t->d_ctrl, guard);
       if (nv > 0)
         lod::launch(k_delta_vox, grid_for(n_items), 256, 0, st, skeys, svals, t->dense.p, t->seg_start.p,
-                    t->dvbase.p, n_all, t->bcell.p, t->brgba.p, t->dvcell.p, t->dvrgba.p, t->d_ctrl, guard);
+                    t->dvbase.p, n_all, t->backlog.p, t->dvcell.p, t->dvrgba.p, t->d_ctrl, guard);
     }
     mark(5);
     // ---- cleanup (update.py:375-380)

@@ -47,7 +47,7 @@ constexpr uint32_t kLbAgg = 1u << 30, kLbPre = 2u << 30, kLbMask = (1u << 30) - 
 constexpr int kPrepItems = 4;
 constexpr int kPrepBlocksPerSM = 4;
 static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
-    k_radix_prep(NodeOf node_of, long long n_all, const int32_t *__restrict__ bnode,
+    k_radix_prep(NodeOf node_of, long long n_all, const uint4 *__restrict__ backlog,
                  long long num_nodes, uint32_t *__restrict__ keys, uint32_t *__restrict__ nodecnt,
                  uint32_t *__restrict__ lb0, long long lb_words, const unsigned long long *__restrict__ n_v_dev, long long *__restrict__ n_items_out,
                  const int *guard) { lod::pdl_wait();
@@ -68,7 +68,7 @@ static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
     for (int q = 0; q < kPrepItems; ++q) {
       const long long i = i0 + q * kRadixBlock + threadIdx.x;
       key[q] = 0xFFFFFFFFu;
-      if (i < n) key[q] = (uint32_t)(i < n_all ? node_of[i] : __ldg(bnode + (i - n_all)));
+      if (i < n) key[q] = (uint32_t)(i < n_all ? node_of[i] : __ldg(&backlog[i - n_all].x));
     }
 #pragma unroll
     for (int q = 0; q < kPrepItems; ++q) {

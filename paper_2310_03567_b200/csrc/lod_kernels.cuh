@@ -73,13 +73,15 @@ constexpr int kMaxPassesHist = 4 * 256;  // radix digit totals (radix.cuh kMaxPa
 // ---------------------------------------------------------------- claim hash
 
 // Open-addressing table of (node, cell) -> min all-array index, 16-byte slots
-// so key and value share one sector.  Iteration-1 claims (at nodes inner at
-// cycle start) carry batch index | 2^31 because the spill length is not known
-// yet; all claims at one node live in one index space, so min order is exact.
+// so key and value share one sector.  The value word is (index << 32 | rgba):
+// a 64-bit min keeps the lowest claimant together with its colour, so the
+// backlog never gathers the winner's colour back from the point arrays.
+// Iteration-1 claims (at nodes inner at cycle start) carry batch index | 2^31
+// because the spill length is not known yet; all claims at one node live in
+// one index space, so min order is exact.
 struct HSlot {
   unsigned long long key;
-  uint32_t val;
-  uint32_t pad;
+  unsigned long long claim;  // claimant index << 32 | its rgba
 };
 constexpr unsigned long long kEmptyKey = 0xFFFFFFFFFFFFFFFFULL;
 constexpr uint32_t kBatchTag = 0x80000000u;
@@ -163,12 +165,12 @@ __device__ __forceinline__ ulonglong2 cas_slot(HSlot *sl, ulonglong2 cmp, ulongl
   return old;
 }
 
-constexpr unsigned long long kEmptyHi = 0xFFFFFFFFFFFFFFFFULL;  // val = pad = 0xFFFFFFFF
+constexpr unsigned long long kEmptyHi = 0xFFFFFFFFFFFFFFFFULL;  // claim = all ones (index 0xFFFFFFFF)
 
 // Min-combine `v` into the claim of `key`.  Lower indices run earlier, so a
 // claimant usually finds a smaller index already there and issues no atomic.
 __device__ __forceinline__ void hash_claim(const Hash &h, UsedStage &stg, unsigned long long key, uint32_t v,
-                                           Ctrl *ctrl) {
+                                           uint32_t rgba, Ctrl *ctrl) {
 #ifdef LOD_EXP_NOCLAIM  // timing experiment only: results are wrong
   return;
 #endif
@@ -181,16 +183,17 @@ __device__ __forceinline__ void hash_claim(const Hash &h, UsedStage &stg, unsign
     atomicAdd((unsigned long long *)&ctrl->alloc_A, 1ull);
 #endif
     HSlot *sl = h.slots + slot;
+    const unsigned long long mine = ((unsigned long long)v << 32) | rgba;
     ulonglong2 cur = __ldcg(reinterpret_cast<const ulonglong2 *>(sl));
     if (cur.x == kEmptyKey) {
-      cur = cas_slot(sl, make_ulonglong2(kEmptyKey, kEmptyHi), make_ulonglong2(key, (unsigned long long)v));
+      cur = cas_slot(sl, make_ulonglong2(kEmptyKey, kEmptyHi), make_ulonglong2(key, mine));
       if (cur.x == kEmptyKey) {
         used_append(h, stg, slot, ctrl);
         return;
       }
     }
     if (cur.x == key) {
-      if ((uint32_t)cur.y > v) atomicMin(&sl->val, v);
+      if ((uint32_t)(cur.y >> 32) > v) atomicMin(&sl->claim, mine);
       return;
     }
     slot = (slot + 1) & h.mask;
@@ -203,10 +206,10 @@ __device__ __forceinline__ void hash_claim(const Hash &h, UsedStage &stg, unsign
 __device__ __forceinline__ void probe_cell(const NodeCols &nd, const Geo &geo, const uint32_t *grid32,
                                            const Hash &h, UsedStage &stg, Ctrl *ctrl, int nid, double x,
                                            double y, double z, double bx, double by, double bz, double s,
-                                           double inv_s, uint32_t v) {
+                                           double inv_s, uint32_t v, uint32_t rgba) {
   const long long cell = cell_of(geo, x, y, z, bx, by, bz, s, inv_s);
   const uint32_t w = __ldg(grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5));
-  if (!(w & (1u << (cell & 31)))) hash_claim(h, stg, claim_key(nid, cell), v, ctrl);
+  if (!(w & (1u << (cell & 31)))) hash_claim(h, stg, claim_key(nid, cell), v, rgba, ctrl);
 }
 
 // Grow the claim table between expansion iterations: re-insert every key
@@ -216,7 +219,7 @@ __global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl
   for (long long u = gtid(); u < (long long)nu; u += gstride()) {
     const HSlot o = old_slots[h.used[u]];
     unsigned long long slot = hmix(o.key) & h.mask;
-    const ulonglong2 empty = make_ulonglong2(kEmptyKey, kEmptyHi), nv = make_ulonglong2(o.key, o.val);
+    const ulonglong2 empty = make_ulonglong2(kEmptyKey, kEmptyHi), nv = make_ulonglong2(o.key, o.claim);
     while (cas_slot(h.slots + slot, empty, nv).x != kEmptyKey) slot = (slot + 1) & h.mask;
     h.used[u] = slot;
   }
@@ -251,6 +254,7 @@ __global__ void __launch_bounds__(256, LOD_COUNT_MINB)
         const int lvl0 = nd.level[nid];
         double s = geo.size_by_level[lvl0], inv_s = geo.inv_by_level[lvl0];
         const uint32_t v = first ? ((uint32_t)j | kBatchTag) : (uint32_t)j;
+        const uint32_t col = src.rgba(j);
         // one dependent load per level, from the compact (L1-resident)
         // descent table; grid words bypass L1 so they do not evict it
         do {
@@ -259,7 +263,7 @@ __global__ void __launch_bounds__(256, LOD_COUNT_MINB)
           const int cur = nid;
           nid = d.x + octant_step(x, y, z, bx, by, bz, s, inv_s);
           d = __ldg(nd.desc + nid);
-          if (!(w & (1u << (cell & 31)))) hash_claim(h, stg, claim_key(cur, cell), v, ctrl);
+          if (!(w & (1u << (cell & 31)))) hash_claim(h, stg, claim_key(cur, cell), v, col, ctrl);
         } while (d.x >= 0);
         node_of[j] = nid;
         if (!nd.final_[nid]) leaf = nid;
@@ -507,7 +511,7 @@ __global__ void k_claim(NodeCols nd, Geo geo, PointSrc src, const uint32_t *__re
     double bx = geo.bmin0[0], by = geo.bmin0[1], bz = geo.bmin0[2], s = geo.size0, inv_s = geo.inv_by_level[0];
     int nid = 0;
     while (nd.inner[nid]) {
-      probe_cell(nd, geo, grid32, h, stg, ctrl, nid, x, y, z, bx, by, bz, s, inv_s, (uint32_t)j);
+      probe_cell(nd, geo, grid32, h, stg, ctrl, nid, x, y, z, bx, by, bz, s, inv_s, (uint32_t)j, src.rgba(j));
       const int o = octant_step(x, y, z, bx, by, bz, s, inv_s);
       nid = nd.children[8 * nid + o];
     }
@@ -544,7 +548,7 @@ __global__ void __launch_bounds__(256)
     const int nid = (int)(kv.x >> 32);
     const uint32_t cell = (uint32_t)(kv.x & 0xFFFFFFFFu);
     atomicOr(grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5), 1u << (cell & 31));
-    atomicAdd(wcount + claim_index((uint32_t)kv.y, n_s), 1u);
+    atomicAdd(wcount + claim_index((uint32_t)(kv.y >> 32), n_s), 1u);
   }
 }
 
@@ -559,9 +563,9 @@ __global__ void __launch_bounds__(256)
     const ulonglong2 kv = __ldcg(reinterpret_cast<const ulonglong2 *>(sl));
     if (kv.x == kEmptyKey) continue;
     *reinterpret_cast<ulonglong2 *>(sl) = make_ulonglong2(kEmptyKey, kEmptyHi);
-    const long long j = claim_index((uint32_t)kv.y, n_s);
+    const long long j = claim_index((uint32_t)(kv.y >> 32), n_s);
     const uint32_t b = __ldg(wbase + j) + atomicSub(wcount + j, 1u) - 1u;
-    backlog[b] = make_uint4((uint32_t)(kv.x >> 32), (uint32_t)(kv.x & 0xFFFFFFFFu), src.rgba(j), 0u);
+    backlog[b] = make_uint4((uint32_t)(kv.x >> 32), (uint32_t)(kv.x & 0xFFFFFFFFu), (uint32_t)kv.y, 0u);
   }
 }
 

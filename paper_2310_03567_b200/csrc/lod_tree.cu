@@ -38,7 +38,6 @@ template <typename T>
 struct DBuf {
   T *p = nullptr;
   long long cap = 0;
-  bool plain = false;  // cudaMalloc instead of the stream-ordered pool (atomic-heavy buffers)
   // Grow to hold n elements; keep the first `keep` elements when growing.
   int ensure(long long n, cudaStream_t st, long long keep = 0) {
     if (n <= cap) return 0;
@@ -47,19 +46,14 @@ struct DBuf {
       fprintf(stderr, "[lod] grow buffer %lld -> %lld elems (%.1f MB)\n", cap, nc, nc * sizeof(T) / 1e6);
     T *q = nullptr;
     // stream-ordered: growth never synchronizes the device
-    cudaError_t e = plain ? cudaMalloc(&q, (size_t)nc * sizeof(T)) : cudaMallocAsync(&q, (size_t)nc * sizeof(T), st);
+    cudaError_t e = cudaMallocAsync(&q, (size_t)nc * sizeof(T), st);
     if (e != cudaSuccess) {
       cudaGetLastError();
       return LOD_E_NOMEM;
     }
     if (p) {
       if (keep > 0) cudaMemcpyAsync(q, p, (size_t)std::min(keep, cap) * sizeof(T), cudaMemcpyDeviceToDevice, st);
-      if (plain) {
-        cudaStreamSynchronize(st);
-        cudaFree(p);
-      } else {
-        cudaFreeAsync(p, st);
-      }
+      cudaFreeAsync(p, st);
     }
     p = q;
     cap = nc;
@@ -480,9 +474,6 @@ int lod_tree_create(const LodParams *params, LodTree **out) {
   if (lod_device_count(&ndev) != LOD_OK || p.device >= ndev) return LOD_E_NO_DEVICE;
   LodTree *t = new LodTree();
   t->p = p;
-  if (getenv("LOD_PLAIN_HASH")) {
-    t->hslots.plain = t->hslots2.plain = true;
-  }
   t->dev = p.device;
   cudaSetDevice(t->dev);
   CK(cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking));
@@ -837,7 +828,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   // speculate on "this iteration settles the expansion" from the second
   // iteration on (the first usually splits), or from the first when the last
   // cycle needed a single one; never while profiling (phase events)
-  const bool may_speculate = !prof && !getenv("LOD_NO_SPEC");
+  static const bool no_spec = getenv("LOD_NO_SPEC") != nullptr;
+  const bool may_speculate = !prof && !no_spec;
   for (;;) {
     ++iters;
     if (prof) cudaEventRecord(t->ev[12], st);

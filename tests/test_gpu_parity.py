@@ -218,3 +218,26 @@ def test_skew_stream_burst_matches_oracle(gpu):
     assert per == oper
     assert max(p[4] for p in per) > 5_000_000  # the spill burst happened
     assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label="skew_burst")
+
+
+def test_frame_budget_semantics(gpu):
+    """run_frame_updates (update.py:396-417): at least one batch per call even
+    over budget, the budget checked between batches, frames counted."""
+    from collections import deque
+
+    from paper_2310_03567_b200 import run_frame_updates
+
+    params = _params(grid_res=16, leaf_threshold=200, chunk_capacity=64)
+    xyz, rgba = _cloud(20_000, 12, "uniform")
+    batches = [(xyz[i:i + 1000], rgba[i:i + 1000]) for i in range(0, 20_000, 1000)]
+    tree, state = make_product(params)
+    state.clock.budget_ms = 0.0
+    q = deque(batches[:5])
+    assert [run_frame_updates(tree, q, state) for _ in range(5)] == [1, 1, 1, 1, 1]
+    assert not q and state.stats.frames == 5 and state.stats.batches == 5
+    assert run_frame_updates(tree, q, state) == 0 and state.stats.frames == 5  # empty queue: no frame
+    state.clock.budget_ms = 1e9
+    q = deque(batches[5:])
+    assert run_frame_updates(tree, q, state) == 15 and state.stats.frames == 6
+    ot, _, _ = run_oracle(params, batches)
+    assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label="budget")

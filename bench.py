@@ -157,8 +157,16 @@ def run_multi(args, rank, world, local_rank):
 
     from paper_2310_03567_b200 import multigpu, partition
 
+    # one process per GPU over NCCL; LOD_DIST_BACKEND=gloo (with ranks sharing
+    # GPUs, local_rank modulo the visible devices) exercises this whole path on
+    # a single-GPU box
+    backend = os.environ.get("LOD_DIST_BACKEND", "nccl")
+    local_rank = local_rank % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        dist.init_process_group(backend)
     kind = CONFIGS[args.config][0]
     sample = [gen_stripe(kind, s, 0) for s in range(2)]
     plan = partition.plan_owners(sample, world)  # deterministic: same on every rank
@@ -180,6 +188,7 @@ def run_multi(args, rank, world, local_rank):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         launches = h2d = 0
+        d2h0 = state.stats.d2h_bytes
         e0.record()
         for x, c in inputs:
             if host:  # the stripe arrives in host memory: H2D inside the timed region
@@ -191,6 +200,7 @@ def run_multi(args, rank, world, local_rank):
         torch.cuda.synchronize()
         dist.barrier()
         torch.cuda.synchronize()
+        timed.d2h = state.stats.d2h_bytes - d2h0
         return e0.elapsed_time(e1), launches, h2d
 
     with ClockSampler(local_rank) as clocks:
@@ -212,11 +222,13 @@ def run_multi(args, rank, world, local_rank):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic",
             "config": {"workload": CONFIGS[args.config][1] + f"; global batch {world} x 1M striped over ranks",
                        "batch_points": BATCH * world, "tree": PARAMS,
-                       "parallelism": f"octant-prefix partition depth {plan.depth} x{world}, NCCL all-to-all routing",
+                       "parallelism": f"octant-prefix partition depth {plan.depth} x{world}, "
+                                      f"{backend.upper()} all-to-all routing",
                        "imbalance_max_over_mean": round(partition.imbalance(plan), 3),
                        "l2": "inputs larger than L2: distinct 16 MB stripes per step"},
             "e2e": {"value": round(pts / (t_e2e * 1e-3) / 1e6, 2), "unit": "Mpts/s",
-                    "h2d_bytes_per_step": h2d // max(args.steps, 1), "d2h_bytes_per_step": None,
+                    "h2d_bytes_per_step": h2d // max(args.steps, 1),
+                    "d2h_bytes_per_step": timed.d2h // max(args.steps, 1),
                     "note": "the next K stripes of the stream, each H2D from pinned host memory + routing + "
                             "insert, max over ranks"},
             "gpu_launches": launches, "clocks": clocks.summary(),

@@ -122,10 +122,22 @@ def route(xyz, rgba, plan: partition.Plan, world: int, group=None):
         order = torch.sort(own, stable=True).indices  # bucket by owner, keep order
         rec = torch.cat([xyz.contiguous().view(torch.int32), rgba.view(torch.int32).reshape(-1, 1)], dim=1)[order]
         send_counts = torch.bincount(own, minlength=world).to(torch.int64)
+    if xyz.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo has no CUDA all-to-all: the exchange goes through host copies
+        # (single-box validation of this path; NCCL moves device memory)
+        out = _all_to_all_records(rec.cpu(), send_counts.cpu(), group)
+        return out.to(xyz.device)
+    return _all_to_all_records(rec, send_counts, group)
+
+
+def _all_to_all_records(rec, send_counts, group):
+    import torch
+    import torch.distributed as dist
+
     recv_counts = torch.empty_like(send_counts)
     dist.all_to_all_single(recv_counts, send_counts, group=group)
     rc, sc = recv_counts.tolist(), send_counts.tolist()
-    out = torch.empty((sum(rc), 4), dtype=torch.int32, device=xyz.device)
+    out = torch.empty((sum(rc), 4), dtype=torch.int32, device=rec.device)
     dist.all_to_all_single(out, rec.contiguous(), rc, sc, group=group)
     return out
 

@@ -61,7 +61,7 @@ struct Ctrl {
   long long n_items;
   // BatchDelta capture (LOD_FLAG_DELTA)
   int spec_abort;             // k_decide: a speculatively launched post-expansion pipeline must not run
-  int pad2;
+  unsigned int n_xchunks;     // chunks of the iteration's splitting nodes (k_split_chunk_list)
   unsigned int d_nvg;         // voxel groups (inner nodes with new voxels)
   unsigned int d_npg;         // point groups (leaves with new points)
 };
@@ -394,6 +394,7 @@ __global__ void __launch_bounds__(kDecideBlock)
     // expansion settled here and the claims fit (else the host takes over)
     ctrl->spec_abort = (ctrl->error != 0 || ns > 0 || ctrl->hash_overflow != 0 ||
                         (long long)ctrl->n_used > backlog_cap) ? 1 : 0;
+    ctrl->n_xchunks = 0;
     if (ctrl->error == 0 && ns > 0) {
       ctrl->num_nodes = nn + 8ll * ns;
       ctrl->splits_total += ns;
@@ -417,17 +418,41 @@ __global__ void __launch_bounds__(kDecideBlock)
 // the chunk table: every chunk owned by a splitting node copies its records to
 // the node's spill segment (chunk position cidx = storage order) and pushes
 // itself onto the free stack at its walk-order slot.  One warp per chunk.
-__global__ void k_exec_chunks(PoolCols pool, Geo geo, const uint8_t *__restrict__ arena, long long nchunks,
-                              const int32_t *__restrict__ srank, const long long *__restrict__ spill_off,
-                              const long long *__restrict__ chunk_off, float4 *spill_buf, int32_t *spill_node_of,
-                              const Ctrl *ctrl) { lod::pdl_wait();
+// The chunks owned by splitting nodes, listed in one coalesced pass over the
+// pool (a large tree holds millions of chunks; a split touches a few
+// thousand): thread per chunk, warp-aggregated appends, order irrelevant.
+__global__ void k_split_chunk_list(PoolCols pool, long long nchunks, const int32_t *__restrict__ srank,
+                                   int32_t *__restrict__ list, Ctrl *ctrl) { lod::pdl_wait();
+  for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < nchunks; i0 += gstride()) {
+    const long long cid = i0 + threadIdx.x;
+    bool hit = false;
+    if (cid < nchunks) {
+      const int owner = pool.owner[cid];
+      hit = owner >= 0 && srank[owner] >= 0;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (!m) continue;
+    unsigned base = 0;
+    if (lane_id() == 0) base = atomicAdd(&ctrl->n_xchunks, (unsigned)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (hit) list[base + __popc(m & lanemask_lt())] = (int32_t)cid;
+  }
+}
+
+// One warp per listed chunk: copy its records to the node's spill segment
+// (chunk position cidx = storage order) and push the chunk onto the free
+// stack at its walk-order slot.
+__global__ void k_exec_chunks(PoolCols pool, Geo geo, const uint8_t *__restrict__ arena,
+                              const int32_t *__restrict__ list, const int32_t *__restrict__ srank,
+                              const long long *__restrict__ spill_off, const long long *__restrict__ chunk_off,
+                              float4 *spill_buf, int32_t *spill_node_of, const Ctrl *ctrl) { lod::pdl_wait();
   const long long warp = gtid() >> 5, nwarps = gstride() >> 5;
   const int lane = threadIdx.x & 31;
-  for (long long cid = warp; cid < nchunks; cid += nwarps) {
+  const long long nlist = (long long)ctrl->n_xchunks;
+  for (long long li = warp; li < nlist; li += nwarps) {
+    const int cid = list[li];
     const int owner = pool.owner[cid];
-    if (owner < 0) continue;
     const int r = srank[owner];
-    if (r < 0) continue;
     const int ci = pool.cidx[cid];
     const int occ = pool.occupied[cid];
     const long long sp = ctrl->plan_spill0 + spill_off[r] + (long long)ci * geo.C;

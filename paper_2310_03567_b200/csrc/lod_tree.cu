@@ -162,7 +162,7 @@ struct LodTree {
   unsigned *h_seq_dev = nullptr;
   unsigned seq = 0;
   // expansion scratch
-  DBuf<int32_t> touched, split_list, node_b, node_all;  // node_b: batch points' node cache; node_all: spilled points'
+  DBuf<int32_t> touched, split_list, node_b, node_all, xlist;  // xlist: chunks of splitting nodes  // node_b: batch points' node cache; node_all: spilled points'
   DBuf<uint32_t> bitmap, word_prefix, tbits;
   DBuf<long long> scnt, schk, spill_off, chunk_off;
   DBuf<float4> spill;
@@ -563,7 +563,7 @@ int lod_tree_destroy(LodTree *t) {
   f(t->d_ctrl);
   if (t->h_ctrl) cudaFreeHost(t->h_ctrl);
   if (t->h_seq) cudaFreeHost(t->h_seq);
-  t->touched.release(); t->split_list.release(); t->node_b.release(); t->node_all.release();
+  t->touched.release(); t->xlist.release(); t->split_list.release(); t->node_b.release(); t->node_all.release();
   t->bitmap.release(); t->word_prefix.release(); t->tbits.release(); t->scnt.release(); t->schk.release();
   t->spill_off.release(); t->chunk_off.release(); t->spill.release(); t->hslots.release(); t->hslots2.release();
   t->hused.release(); t->srank.release(); t->wcount.release(); t->wbase.release();
@@ -872,9 +872,11 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       if (!first) return abort_cycle(t, LOD_E_ARG);  // only iteration 1 can spill (update.py:9-11)
       RK(t->spill.ensure(h.spill_total, st));
       RK(t->node_all.ensure(h.spill_total, st));
-      lod::launch(k_exec_chunks, grid_for(h.allocated_total * 32), 256, 0, st, 
-          t->pool, t->geo, t->arena, h.allocated_total, t->srank.p, t->spill_off.p, t->chunk_off.p, t->spill.p,
-          t->node_all.p, t->d_ctrl);
+      RK(t->xlist.ensure(std::max<long long>(h.allocated_total, 1), st));
+      lod::launch(k_split_chunk_list, grid_for(h.allocated_total), 256, 0, st, t->pool, h.allocated_total, t->srank.p,
+                  t->xlist.p, t->d_ctrl);
+      lod::launch(k_exec_chunks, grid_for(h.allocated_total * 32), 256, 0, st, t->pool, t->geo, t->arena, t->xlist.p,
+                  t->srank.p, t->spill_off.p, t->chunk_off.p, t->spill.p, t->node_all.p, t->d_ctrl);
     }
     lod::launch(k_exec_nodes, grid_for(8 * ns), 256, 0, st, t->nd, t->geo, t->split_list.p, t->srank.p, ns,
                                                    t->d_ctrl);

@@ -1,0 +1,56 @@
+"""Long single-GPU stream (config 2/3 scale): N x 1M batches into one tree,
+device time per batch from the library's CUDA events; batches are generated on
+the host one at a time (not timed).
+
+    python tools/long_stream.py --config terrain --batches 1000 --arena-gib 64
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import torch
+
+    from bench import CONFIGS, new_tree
+    from paper_2310_03567_b200 import insert_batch, synth
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="terrain")
+    ap.add_argument("--batches", type=int, default=1000)
+    ap.add_argument("--arena-gib", type=float, default=64)
+    ap.add_argument("--window", type=int, default=100)
+    a = ap.parse_args()
+    kind = CONFIGS[a.config][0]
+    gen = synth.GENERATORS[kind]
+    scene = synth.mesh_scene() if kind == "mesh" else None
+    tree, state = new_tree(0, int(a.arena_gib * (1 << 30)))
+    dev_ms, out = [], []
+    t0 = time.time()
+    for i in range(a.batches):
+        x, c = gen(1_000_000, 1000 + i, scene) if scene is not None else gen(1_000_000, 1000 + i)
+        xd, cd = torch.from_numpy(x).cuda(), torch.from_numpy(c.view(np.int32)).cuda()
+        insert_batch(tree, xd, cd, state)
+        dev_ms.append(float(state._bstats.device_ms))
+        if (i + 1) % a.window == 0:
+            w = dev_ms[-a.window:]
+            row = dict(batches=i + 1, window_mpts_s=round(a.window * 1e3 / sum(w), 1),
+                       window_p50_ms=round(float(np.median(w)), 3), window_max_ms=round(max(w), 3),
+                       nodes=int(state._bstats.num_nodes), arena_gb=round(state._bstats.arena_offset / 1e9, 2),
+                       wall_s=round(time.time() - t0, 1))
+            out.append(row)
+            print(json.dumps(row), flush=True)
+    total = dict(config=a.config, batches=a.batches, points=a.batches * 1_000_000,
+                 device_mpts_s=round(a.batches * 1e3 / sum(dev_ms), 1), nodes=int(state._bstats.num_nodes),
+                 arena_gb=round(state._bstats.arena_offset / 1e9, 2), voxels=state.stats.voxels_created)
+    print(json.dumps(total), flush=True)
+
+
+if __name__ == "__main__":
+    main()

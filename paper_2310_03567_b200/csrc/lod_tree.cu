@@ -765,9 +765,21 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     RK(ensure_chunks(t, alloc0 + acq_bound + 1, alloc0));
     const long long lbw = radix_lb_elems(n_items);
     long long *n_items_dev = &t->d_ctrl->n_items;
-    lod::launch(k_radix_prep, std::min<unsigned>(grid_for(n_items, kRadixBlock * kPrepItems), 148 * kPrepBlocksPerSM),
-                kRadixBlock, 0, st, node_of, n_all, t->backlog.p, num_nodes, t->keys.p, t->nodecnt.p, t->hist.p, lbw,
-                &t->d_ctrl->n_used, n_items_dev, guard);
+    {
+      // node counts in per-CTA shared memory (16-bit counters) up to
+      // kNodeHistSmemMax nodes, as long as no CTA can see 65535 items
+      const unsigned grid = std::min<unsigned>(grid_for(n_items, kRadixBlock * kPrepItems), 148 * kPrepBlocksPerSM);
+      long long nc_words = (num_nodes + 1) / 2;
+      if (num_nodes > kNodeHistSmemMax || n_items > (long long)grid * 65535) nc_words = 0;
+      static bool smem_attr[64] = {};  // per device
+      if (t->dev < 64 && !smem_attr[t->dev]) {
+        CK(cudaFuncSetAttribute(k_radix_prep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(kNodeHistSmemMax / 2 * 4)));
+        smem_attr[t->dev] = true;
+      }
+      lod::launch(k_radix_prep, grid, kRadixBlock, (size_t)nc_words * 4, st, node_of, n_all, t->backlog.p, nc_words,
+                  t->keys.p, t->nodecnt.p, t->hist.p, lbw, &t->d_ctrl->n_used, n_items_dev, guard);
+    }
     lod::launch(k_radix_ghist, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p, num_nodes,
                 passes, t->ghist.p, t->plan_ex.p, guard);
     // ---- allocation (update.py:317-331): touched nodes = nodes with new samples, ascending id.

@@ -35,7 +35,10 @@ constexpr int kRadixWarps = kRadixBlock / 32;
 constexpr int kRadixRounds = LOD_RADIX_ROUNDS;  // per warp: 8 rounds x 32 lanes (2048-item tile, ~27 KB smem)
 constexpr int kRadixTile = kRadixBlock * kRadixRounds;
 constexpr int kMaxPasses = 4;
-constexpr int kNodeHistSmem = 10240;  // node counts kept in shared memory up to this many nodes
+// Per-CTA node histograms live in dynamic shared memory as 16-bit counters
+// (two per word) for trees of up to kNodeHistSmemMax nodes (192 KB); a CTA
+// never counts more than 65535 items of one node (checked by the launcher).
+constexpr long long kNodeHistSmemMax = 98304;
 
 // look-back words: [31:30] status (0 empty, 1 aggregate, 2 inclusive prefix), [29:0] count
 constexpr uint32_t kLbAgg = 1u << 30, kLbPre = 2u << 30, kLbMask = (1u << 30) - 1;
@@ -48,17 +51,16 @@ constexpr int kPrepItems = 4;
 constexpr int kPrepBlocksPerSM = 4;
 static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
     k_radix_prep(NodeOf node_of, long long n_all, const uint4 *__restrict__ backlog,
-                 long long num_nodes, uint32_t *__restrict__ keys, uint32_t *__restrict__ nodecnt,
+                 long long nc_words, uint32_t *__restrict__ keys, uint32_t *__restrict__ nodecnt,
                  uint32_t *__restrict__ lb0, long long lb_words, const unsigned long long *__restrict__ n_v_dev, long long *__restrict__ n_items_out,
                  const int *guard) { lod::pdl_wait();
   if (guard && *guard) return;
-  __shared__ uint32_t nc[kNodeHistSmem];
+  extern __shared__ uint32_t nc2[];  // nc_words words: node 2w in the low half, 2w+1 in the high half
   const long long n_v = (long long)*n_v_dev;  // new voxels (device count: launches may precede the host's view)
   if (blockIdx.x == 0 && threadIdx.x == 0) *n_items_out = n_all + n_v;
   for (long long i = gtid(); i < lb_words; i += gstride()) lb0[i] = 0;  // look-back words of pass 0
-  const bool smem_nodes = num_nodes <= kNodeHistSmem;
-  if (smem_nodes)
-    for (long long i = threadIdx.x; i < num_nodes; i += kRadixBlock) nc[i] = 0;
+  const bool smem_nodes = nc_words > 0;
+  for (long long w = threadIdx.x; w < nc_words; w += kRadixBlock) nc2[w] = 0;
   __syncthreads();
   const long long n = n_all + n_v;
   constexpr long long kSpan = (long long)kRadixBlock * kPrepItems;
@@ -79,16 +81,18 @@ static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
       if (ok) {
         const unsigned peers = __match_any_sync(act, key[q]);
         if (lane_id() == (unsigned)(__ffs(peers) - 1)) {
-          if (smem_nodes) atomicAdd(&nc[key[q]], (uint32_t)__popc(peers));
+          if (smem_nodes) atomicAdd(&nc2[key[q] >> 1], (uint32_t)__popc(peers) << (16 * (key[q] & 1)));
           else atomicAdd(&nodecnt[key[q]], (uint32_t)__popc(peers));
         }
       }
     }
   }
   __syncthreads();
-  if (smem_nodes)
-    for (long long i = threadIdx.x; i < num_nodes; i += kRadixBlock)
-      if (nc[i]) atomicAdd(nodecnt + i, nc[i]);
+  for (long long w = threadIdx.x; w < nc_words; w += kRadixBlock) {
+    const uint32_t v = nc2[w];
+    if (v & 0xFFFFu) atomicAdd(nodecnt + 2 * w, v & 0xFFFFu);
+    if (v >> 16) atomicAdd(nodecnt + 2 * w + 1, v >> 16);
+  }
 }
 
 // Digit totals of every pass from the per-node counts (keys are node ids).

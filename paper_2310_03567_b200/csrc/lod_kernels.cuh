@@ -288,37 +288,41 @@ __global__ void __launch_bounds__(256, LOD_COUNT_MINB)
 }
 
 // _split_pass (update.py:226-249): split iff count + pending > T and
-// level < max_depth, else mark final.  Splits are ranked by ascending node id
-// (bitmap popcount prefix), so child ids num_nodes + 8*rank match the
-// reference's sorted-id split order (octree.py:249-261).  Also plans the
-// spill segments (ascending id, stored order), free-stack pushes (walk order)
-// and grid offsets, and detects SpillOverflow / OutOfArena in reference order.
-constexpr int kDecideBlock = 1024;
-__global__ void __launch_bounds__(kDecideBlock)
-    k_decide(NodeCols nd, Geo geo, const int32_t *__restrict__ touched, uint32_t *bitmap, uint32_t *word_prefix,
-             int32_t *split_list, int32_t *srank, long long *scnt, long long *schk, long long *spill_off,
-             long long *chunk_off, Ctrl *ctrl, long long spill_cap, unsigned long long arena_cap,
-             long long backlog_cap) { lod::pdl_wait();
-  __shared__ uint32_t sh32[kDecideBlock / 32 + 1];
-  __shared__ U64x2 sh64[kDecideBlock / 32 + 1];
-  __shared__ unsigned int s_maxlvl;
-  __shared__ long long s_err_spill;
-  const int tid = threadIdx.x;
+// level < max_depth, else mark final.  k_decide_mark tests every touched leaf
+// (grid-wide: a large tree touches tens of thousands per batch) and flags the
+// splits in a bitmap over node ids; k_decide (1 CTA) ranks them by ascending
+// node id (popcount prefix over the bitmap words), so child ids
+// num_nodes + 8*rank match the reference's sorted-id split order
+// (octree.py:249-261), and plans the spill segments (ascending id, stored
+// order), free-stack pushes (walk order) and grid offsets, detecting
+// SpillOverflow / OutOfArena in reference order.
+__global__ void k_decide_mark(NodeCols nd, Geo geo, const int32_t *__restrict__ touched, uint32_t *bitmap,
+                              const Ctrl *ctrl) { lod::pdl_wait();
   const unsigned nt = ctrl->n_touched;
-  const long long nn = ctrl->num_nodes;
-  if (tid == 0) {
-    s_maxlvl = 0;
-    s_err_spill = -1;
-  }
-  // phase 1: decide
-  for (unsigned t = tid; t < nt; t += kDecideBlock) {
+  for (long long t = gtid(); t < nt; t += gstride()) {
     const int nid = touched[t];
     const long long tot = nd.count[nid] + (long long)nd.pending[nid];
     if (tot > geo.T && nd.level[nid] < geo.max_depth) atomicOr(&bitmap[nid >> 5], 1u << (nid & 31));
     else nd.final_[nid] = 1;
   }
-  __syncthreads();
-  // phase 2: popcount prefix over bitmap words
+}
+
+constexpr int kDecideBlock = 1024;
+__global__ void __launch_bounds__(kDecideBlock)
+    k_decide(NodeCols nd, Geo geo, uint32_t *bitmap, int32_t *split_list, int32_t *srank, long long *scnt,
+             long long *schk, long long *spill_off, long long *chunk_off, Ctrl *ctrl, long long spill_cap,
+             unsigned long long arena_cap, long long backlog_cap) { lod::pdl_wait();
+  __shared__ uint32_t sh32[kDecideBlock / 32 + 1];
+  __shared__ U64x2 sh64[kDecideBlock / 32 + 1];
+  __shared__ unsigned int s_maxlvl;
+  __shared__ long long s_err_spill;
+  const int tid = threadIdx.x;
+  const long long nn = ctrl->num_nodes;
+  if (tid == 0) {
+    s_maxlvl = 0;
+    s_err_spill = -1;
+  }
+  // phase 2: popcount prefix over the bitmap words (contiguous word ranges per thread)
   const long long W = (nn + 31) / 32;
   const long long per = (W + kDecideBlock - 1) / kDecideBlock;
   const long long w0 = tid * per, w1 = min(W, w0 + per);
@@ -326,24 +330,23 @@ __global__ void __launch_bounds__(kDecideBlock)
   for (long long w = w0; w < w1; ++w) local += __popc(__ldcg(bitmap + w));
   uint32_t total;
   uint32_t run = block_exclusive_scan<uint32_t, kDecideBlock>(local, sh32, total);
-  for (long long w = w0; w < w1; ++w) {
-    word_prefix[w] = run;
-    run += __popc(__ldcg(bitmap + w));
-  }
-  __syncthreads();
   const unsigned ns = total;
-  // phase 3: rank splits, gather their counts
-  for (unsigned t = tid; t < nt; t += kDecideBlock) {
-    int nid = touched[t];
-    uint32_t wv = __ldcg(bitmap + (nid >> 5));
-    uint32_t bit = 1u << (nid & 31);
-    if (wv & bit) {
-      uint32_t rank = word_prefix[nid >> 5] + __popc(wv & (bit - 1));
-      split_list[rank] = nid;
-      srank[nid] = (int32_t)rank;
-      scnt[rank] = nd.count[nid];
-      schk[rank] = nd.chunk_count[nid];
+  // phase 3: the splits in id order out of the words (rank = running prefix),
+  // their counts; the words are cleared for the next iteration
+  for (long long w = w0; w < w1; ++w) {
+    uint32_t wv = __ldcg(bitmap + w);
+    if (!wv) continue;
+    bitmap[w] = 0;
+    while (wv) {
+      const int b = __ffs(wv) - 1;
+      wv &= wv - 1;
+      const int nid = (int)(w * 32 + b);
+      split_list[run] = nid;
+      srank[nid] = (int32_t)run;
+      scnt[run] = nd.count[nid];
+      schk[run] = nd.chunk_count[nid];
       atomicMax(&s_maxlvl, (unsigned)(nd.level[nid] + 1));
+      ++run;
     }
   }
   __syncthreads();
@@ -405,13 +408,7 @@ __global__ void __launch_bounds__(kDecideBlock)
       ctrl->arena_off = g0 + (unsigned long long)(ns - 1) * gstride_b + gb;
     }
   }
-  __syncthreads();
-  // phase 6: clear the split bitmap and the touched count for the next iteration
-  for (unsigned t = tid; t < nt; t += kDecideBlock) {
-    int nid = touched[t];
-    bitmap[nid >> 5] = 0;
-  }
-  if (tid == 0) ctrl->n_touched = 0;
+  if (tid == 0) ctrl->n_touched = 0;  // phase 6: the touched list restarts next iteration
 }
 
 // Octree.split, part 1 (octree.py:231-237, store.py:125-143), in parallel over

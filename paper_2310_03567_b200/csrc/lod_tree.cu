@@ -163,7 +163,7 @@ struct LodTree {
   unsigned seq = 0;
   // expansion scratch
   DBuf<int32_t> touched, split_list, node_b, node_all, xlist;  // xlist: chunks of splitting nodes  // node_b: batch points' node cache; node_all: spilled points'
-  DBuf<uint32_t> bitmap, word_prefix, tbits;
+  DBuf<uint32_t> bitmap;  // split flags over node ids (k_decide_mark -> k_decide)
   DBuf<long long> scnt, schk, spill_off, chunk_off;
   DBuf<float4> spill;
   // sampling scratch
@@ -321,10 +321,6 @@ static int ensure_nodes(LodTree *t, long long want, long long live) {
   long long oldw = t->bitmap.cap;
   RK(t->bitmap.ensure(words, st, oldw));
   if (t->bitmap.cap > oldw) CK(cudaMemsetAsync(t->bitmap.p + oldw, 0, (size_t)(t->bitmap.cap - oldw) * 4, st));
-  RK(t->word_prefix.ensure(words, st));
-  long long oldt = t->tbits.cap;
-  RK(t->tbits.ensure(words, st, oldt));
-  if (t->tbits.cap > oldt) CK(cudaMemsetAsync(t->tbits.p + oldt, 0, (size_t)(t->tbits.cap - oldt) * 4, st));
   // the split plan of the running iteration survives the growth (k_execute reads it)
   RK(t->touched.ensure(nc, st));
   RK(t->split_list.ensure(nc, st, t->split_list.cap));
@@ -427,7 +423,8 @@ static int abort_cycle(LodTree *t, int code) {
   }
   long long words = (t->ncap + 31) / 32 + 1;
   cudaMemsetAsync(t->bitmap.p, 0, (size_t)words * 4, t->st);
-  cudaMemsetAsync(t->tbits.p, 0, (size_t)t->tbits.cap * 4, t->st);
+  if (t->ghist.p) cudaMemsetAsync(t->ghist.p, 0, (size_t)t->ghist.cap * 4, t->st);
+  if (t->nodecnt.p) cudaMemsetAsync(t->nodecnt.p, 0, (size_t)t->nodecnt.cap * 4, t->st);
   cudaStreamSynchronize(t->st);
   // counters: the device ctrl keeps whatever was applied before the failure
   sync_ctrl(t);
@@ -564,7 +561,7 @@ int lod_tree_destroy(LodTree *t) {
   if (t->h_ctrl) cudaFreeHost(t->h_ctrl);
   if (t->h_seq) cudaFreeHost(t->h_seq);
   t->touched.release(); t->xlist.release(); t->split_list.release(); t->node_b.release(); t->node_all.release();
-  t->bitmap.release(); t->word_prefix.release(); t->tbits.release(); t->scnt.release(); t->schk.release();
+  t->bitmap.release(); t->scnt.release(); t->schk.release();
   t->spill_off.release(); t->chunk_off.release(); t->spill.release(); t->hslots.release(); t->hslots2.release();
   t->hused.release(); t->srank.release(); t->wcount.release(); t->wbase.release();
   t->backlog.release(); t->keys.release(); t->keys_b.release();
@@ -849,9 +846,11 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
                 t->touched.p, t->d_ctrl);
     if (first) RK(issue_pending(t));  // queued batches' copies start once this count pass is done
     if (prof) cudaEventRecord(t->ev[13], st);
-    lod::launch(k_decide, 1, kDecideBlock, 0, st, t->nd, t->geo, t->touched.p, t->bitmap.p, t->word_prefix.p,
-                                         t->split_list.p, t->srank.p, t->scnt.p, t->schk.p, t->spill_off.p,
-                                         t->chunk_off.p, t->d_ctrl, spill_cap, t->arena_cap, backlog_cap);
+    lod::launch(k_decide_mark, grid_for(t->num_nodes), 256, 0, st, t->nd, t->geo, t->touched.p, t->bitmap.p,
+                t->d_ctrl);
+    lod::launch(k_decide, 1, kDecideBlock, 0, st, t->nd, t->geo, t->bitmap.p, t->split_list.p, t->srank.p,
+                t->scnt.p, t->schk.p, t->spill_off.p, t->chunk_off.p, t->d_ctrl, spill_cap, t->arena_cap,
+                backlog_cap);
     if (may_speculate && (iters >= 2 || t->last_iters == 1)) {
       // the pipeline's host-side sizes: nodes as of now (no further split if
       // it runs), new voxels bounded by the claim table's capacity

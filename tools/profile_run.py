@@ -21,10 +21,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="surface")
     ap.add_argument("--profiled", type=int, default=1)
+    ap.add_argument("--arena-gib", type=float, default=8.0)
     a = ap.parse_args()
     batches = gen_batches(a.config, a.warmup + a.profiled)
     dev = [(torch.from_numpy(x).cuda(), torch.from_numpy(c.view(np.int32)).cuda()) for x, c in batches]
-    tree, state = new_tree(0, 8 << 30)
+    tree, state = new_tree(0, int(a.arena_gib * (1 << 30)))
     for i in range(a.warmup):
         insert_batch(tree, *dev[i], state)
     torch.cuda.synchronize()

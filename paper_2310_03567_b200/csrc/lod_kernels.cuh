@@ -88,7 +88,7 @@ constexpr uint32_t kBatchTag = 0x80000000u;
 
 struct Hash {
   HSlot *slots;
-  unsigned long long mask;   // capacity - 1 (power of two)
+  unsigned long long cap;    // slots (any size: the hash is range-reduced by a multiply-high)
   unsigned long long *used;  // slots inserted this cycle
   unsigned long long limit;  // capacity of `used` (= table capacity)
 };
@@ -111,6 +111,15 @@ __device__ __forceinline__ unsigned long long hmix(unsigned long long k) {
   k *= 0xc4ceb9fe1a85ec53ULL;
   k ^= k >> 33;
   return k;
+}
+
+// Home slot: the 64-bit mix range-reduced to [0, cap) by a multiply-high (no
+// power-of-two table: the sweeps read exactly the slots the load needs).
+__device__ __forceinline__ unsigned long long home_slot(const Hash &h, unsigned long long key) {
+  return __umul64hi(hmix(key), h.cap);
+}
+__device__ __forceinline__ unsigned long long next_slot(const Hash &h, unsigned long long s) {
+  return s + 1 == h.cap ? 0ull : s + 1;
 }
 
 __device__ __forceinline__ unsigned long long claim_key(int nid, long long cell) {
@@ -177,8 +186,8 @@ __device__ __forceinline__ void hash_claim(const Hash &h, UsedStage &stg, unsign
 #ifdef LOD_EXP_COUNT  // instrumentation experiment: claims and probes into Ctrl.alloc_F / alloc_A
   atomicAdd((unsigned long long *)&ctrl->alloc_F, 1ull);
 #endif
-  unsigned long long slot = hmix(key) & h.mask;
-  for (unsigned long long probe = 0; probe <= h.mask; ++probe) {
+  unsigned long long slot = home_slot(h, key);
+  for (unsigned long long probe = 0; probe < h.cap; ++probe) {
 #ifdef LOD_EXP_COUNT
     atomicAdd((unsigned long long *)&ctrl->alloc_A, 1ull);
 #endif
@@ -196,7 +205,7 @@ __device__ __forceinline__ void hash_claim(const Hash &h, UsedStage &stg, unsign
       if ((uint32_t)(cur.y >> 32) > v) atomicMin(&sl->claim, mine);
       return;
     }
-    slot = (slot + 1) & h.mask;
+    slot = next_slot(h, slot);
   }
   ctrl->hash_overflow = 1;  // table full
 }
@@ -218,9 +227,9 @@ __global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl
   const unsigned long long nu = ctrl->n_used;
   for (long long u = gtid(); u < (long long)nu; u += gstride()) {
     const HSlot o = old_slots[h.used[u]];
-    unsigned long long slot = hmix(o.key) & h.mask;
+    unsigned long long slot = home_slot(h, o.key);
     const ulonglong2 empty = make_ulonglong2(kEmptyKey, kEmptyHi), nv = make_ulonglong2(o.key, o.claim);
-    while (cas_slot(h.slots + slot, empty, nv).x != kEmptyKey) slot = (slot + 1) & h.mask;
+    while (cas_slot(h.slots + slot, empty, nv).x != kEmptyKey) slot = next_slot(h, slot);
     h.used[u] = slot;
   }
 }
@@ -563,7 +572,7 @@ __global__ void __launch_bounds__(256)
     k_resolve(NodeCols nd, Hash h, uint32_t *grid32, long long n_s, uint32_t *__restrict__ wcount,
               const int *guard) { lod::pdl_wait();
   if (guard && *guard) return;
-  const long long H = (long long)h.mask + 1;
+  const long long H = (long long)h.cap;
   for (long long sidx = gtid(); sidx < H; sidx += gstride()) {
     const ulonglong2 kv = __ldcg(reinterpret_cast<const ulonglong2 *>(h.slots + sidx));
     if (kv.x == kEmptyKey) continue;
@@ -579,7 +588,7 @@ __global__ void __launch_bounds__(256)
               uint4 *__restrict__ backlog,
               const int *guard) { lod::pdl_wait();
   if (guard && *guard) return;
-  const long long H = (long long)h.mask + 1;
+  const long long H = (long long)h.cap;
   for (long long sidx = gtid(); sidx < H; sidx += gstride()) {
     HSlot *sl = h.slots + sidx;
     const ulonglong2 kv = __ldcg(reinterpret_cast<const ulonglong2 *>(sl));

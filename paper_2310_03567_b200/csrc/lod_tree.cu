@@ -73,11 +73,9 @@ inline unsigned grid_for(long long n, int block = 256) {
   return (unsigned)std::min(b, cap);
 }
 
-inline unsigned long long next_pow2(unsigned long long v) {
-  unsigned long long p = 1;
-  while (p < v) p <<= 1;
-  return p;
-}
+// Claim-table sizes: rounded up to a multiple of 64 Ki slots.
+inline unsigned long long round_slots(unsigned long long v) { return (v + 65535ull) / 65536ull * 65536ull; }
+
 
 }  // namespace
 
@@ -696,7 +694,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
 #define LOD_HASH_FACTOR_X4 6  // table slots ~ 1.5 x (previous cycle's claims + batch), next power of two
 #endif
     const long long want = std::max<long long>(LOD_HASH_FACTOR_X4 * (t->prev_used + n) / 4, 1 << 20);
-    const unsigned long long H = next_pow2((unsigned long long)want);
+    const unsigned long long H = round_slots((unsigned long long)want);
     if ((long long)H > t->hslots.cap) {
       RK(t->hslots.ensure((long long)H, st));
       CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
@@ -704,7 +702,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     t->hcap = H;
     RK(t->hused.ensure((long long)H, st));
   }
-  Hash hs{t->hslots.p, t->hcap - 1, t->hused.p, t->hcap};
+  Hash hs{t->hslots.p, t->hcap, t->hused.p, t->hcap};
   uint32_t *grid32 = reinterpret_cast<uint32_t *>(t->arena);
   // ---- post-expansion pipeline: resolve -> backlog -> alloc -> sort+store ->
   // [delta] -> epilogue.  Launched either after the expansion settled (guard
@@ -905,12 +903,12 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     }
     // the next pass claims at most one cell per re-descending point
     if ((long long)h.n_used + n_all > (long long)(3 * t->hcap / 4)) {
-      const unsigned long long H = next_pow2((unsigned long long)(2 * ((long long)h.n_used + n_all)));
+      const unsigned long long H = round_slots((unsigned long long)(2 * ((long long)h.n_used + n_all)));
       if (lod_debug()) fprintf(stderr, "[lod] claim table grow %llu -> %llu (rehash %llu)\n", t->hcap, H, h.n_used);
       RK(t->hslots2.ensure((long long)H, st));
       CK(cudaMemsetAsync(t->hslots2.p, 0xFF, (size_t)t->hslots2.cap * sizeof(HSlot), st));
       RK(t->hused.ensure((long long)H, st, (long long)h.n_used));
-      Hash nh{t->hslots2.p, H - 1, t->hused.p, H};
+      Hash nh{t->hslots2.p, H, t->hused.p, H};
       lod::launch(k_rehash, grid_for(std::max<long long>((long long)h.n_used, 1)), 256, 0, st, t->hslots.p, nh, t->d_ctrl);
       // the old table goes back to empty for later cycles
       CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
@@ -940,12 +938,12 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
         fprintf(stderr, "[lod] claim table overflow (H=%llu, used>=%llu): fallback pass\n", t->hcap, h1.n_used);
       // fallback: clean table sized by the reference's backlog bound, full claim pass
       const long long bound = std::min<long long>(n_all * D, backlog_cap + 1);
-      const unsigned long long H = next_pow2((unsigned long long)std::max<long long>(2 * bound, 1 << 20));
+      const unsigned long long H = round_slots((unsigned long long)std::max<long long>(2 * bound, 1 << 20));
       if ((long long)H > t->hslots.cap) RK(t->hslots.ensure((long long)H, st));
       CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
       t->hcap = H;
       RK(t->hused.ensure(bound + 1, st));
-      hs = Hash{t->hslots.p, t->hcap - 1, t->hused.p, (unsigned long long)bound + 1};
+      hs = Hash{t->hslots.p, t->hcap, t->hused.p, (unsigned long long)bound + 1};
       CK(cudaMemsetAsync(&t->d_ctrl->n_used, 0, 8, st));
       CK(cudaMemsetAsync(&t->d_ctrl->hash_overflow, 0, 4, st));
       lod::launch(k_claim, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, grid32, n_all, hs, t->d_ctrl);

@@ -45,6 +45,7 @@ enum {
     LOD_FLAG_DELTA = 8,        /* capture the cycle's BatchDelta (collect_delta=True)       */
     LOD_FLAG_PACKED = 16       /* xyz points at n 16-byte records (f32 x,y,z | u32 rgba);
                                   rgba is ignored (may be NULL)                              */
+    , LOD_FLAG_INPUT_STREAM = 32 /* order the device inputs after LodLimits.input_stream      */
 };
 
 typedef struct LodTree LodTree;
@@ -69,6 +70,12 @@ typedef struct {
 typedef struct {
     int64_t backlog_capacity;
     int64_t spill_capacity;
+    /* With LOD_FLAG_INPUT_STREAM: the CUDA stream (cudaStream_t; 0 = the legacy
+     * default stream) that produces the device inputs.  The tree's own stream
+     * waits for the work queued on it so far (an event, no host sync), so a
+     * batch written by a copy, kernel or collective on the caller's stream is
+     * read only once it is complete. */
+    void *input_stream;
 } LodLimits;
 
 enum { LOD_NPHASE = 10 };

@@ -30,6 +30,7 @@ LOD_FLAG_DEVICE_FB = 2
 LOD_FLAG_PROFILE = 4
 LOD_FLAG_DELTA = 8
 LOD_FLAG_PACKED = 16
+LOD_FLAG_INPUT_STREAM = 32
 LOD_NPHASE = 10
 PHASES = ("count", "split", "resolve", "backlog", "alloc", "sort", "delta", "epilogue", "h2d", "total")
 
@@ -57,7 +58,8 @@ class LodParams(ctypes.Structure):
 
 
 class LodLimits(ctypes.Structure):
-    _fields_ = [("backlog_capacity", ctypes.c_int64), ("spill_capacity", ctypes.c_int64)]
+    _fields_ = [("backlog_capacity", ctypes.c_int64), ("spill_capacity", ctypes.c_int64),
+                ("input_stream", ctypes.c_void_p)]
 
 
 class LodBatchStats(ctypes.Structure):

@@ -209,6 +209,7 @@ struct LodTree {
     cudaEvent_t ready = nullptr;
   } stage[3];
   cudaEvent_t ev_counted = nullptr;  // the running cycle's first count pass is done
+  cudaEvent_t ev_input = nullptr;    // the caller's input stream (LOD_FLAG_INPUT_STREAM)
   int stage_next = 0;
   cudaEvent_t ev[14] = {};  // 12, 13: per-iteration k_count brackets
   // host copies of counters (authoritative after every call)
@@ -575,6 +576,7 @@ int lod_tree_destroy(LodTree *t) {
   t->dpstart.release(); t->dpcount.release(); t->dvbase.release(); t->dvcell.release(); t->dvrgba.release();
   if (t->cst) cudaStreamSynchronize(t->cst);
   if (t->ev_counted) cudaEventDestroy(t->ev_counted);
+  if (t->ev_input) cudaEventDestroy(t->ev_input);
   for (auto &sg : t->stage) {
     sg.xyz.release();
     sg.rgba.release();
@@ -645,6 +647,11 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_entry).count();
     tlpos += snprintf(tlbuf + tlpos, sizeof(tlbuf) - tlpos, " %s=%.0f", what, us);
   };
+  if ((flags & LOD_FLAG_INPUT_STREAM) && limits) {  // device inputs produced on the caller's stream
+    if (!t->ev_input) CK(cudaEventCreateWithFlags(&t->ev_input, cudaEventDisableTiming));
+    CK(cudaEventRecord(t->ev_input, reinterpret_cast<cudaStream_t>(limits->input_stream)));
+    CK(cudaStreamWaitEvent(st, t->ev_input, 0));
+  }
   CK(cudaEventRecord(t->ev[0], st));
   // ---- inputs
   const float *bx = xyz;

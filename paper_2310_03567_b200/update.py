@@ -186,9 +186,9 @@ def insert_batch(
         raise ValueError("xyz and rgba must both be host arrays or both be device tensors")
     flags = ((_lib.LOD_FLAG_DEVICE_INPUT if dev_x else 0) | (_lib.LOD_FLAG_PROFILE if profile else 0)
              | (_lib.LOD_FLAG_DELTA if collect_delta else 0))
-    lim = state._limits
-    lim.backlog_capacity = state.config.backlog_capacity
-    lim.spill_capacity = state.config.spill_capacity
+    lim = _limits(tree, state, xyz_b if dev_x else None)
+    if dev_x:
+        flags |= _lib.LOD_FLAG_INPUT_STREAM
     bs = state._bstats
     rc = tree._L.lod_insert_batch(tree.handle, _lib.ptr(xyz_b), _lib.ptr(rgba_b), n_batch,
                                   ctypes.byref(lim), flags, ctypes.byref(bs))
@@ -215,15 +215,13 @@ def insert_records(tree: Octree, records, state: UpdateState, collect_delta: boo
     if hasattr(records, "is_cuda") and records.is_cuda:
         if records.element_size() != 4 or records.dim() != 2 or records.shape[1] != 4:
             raise TypeError("records must be an (n, 4) tensor of 4-byte elements")
-        rec, flags = records.contiguous(), _lib.LOD_FLAG_DEVICE_INPUT
+        rec, flags = records.contiguous(), _lib.LOD_FLAG_DEVICE_INPUT | _lib.LOD_FLAG_INPUT_STREAM
     else:
         rec, flags = np.ascontiguousarray(records).reshape(-1, 4), 0
         if rec.dtype.itemsize != 4:
             raise TypeError("records must be (n, 4) of 4-byte elements")
     flags |= _lib.LOD_FLAG_PACKED | (_lib.LOD_FLAG_DELTA if collect_delta else 0)
-    lim = state._limits
-    lim.backlog_capacity = state.config.backlog_capacity
-    lim.spill_capacity = state.config.spill_capacity
+    lim = _limits(tree, state, rec if flags & _lib.LOD_FLAG_DEVICE_INPUT else None)
     bs = state._bstats
     rc = tree._L.lod_insert_batch(tree.handle, _lib.ptr(rec), None, n_batch, ctypes.byref(lim), flags, ctypes.byref(bs))
     tree._invalidate()
@@ -234,6 +232,23 @@ def insert_records(tree: Octree, records, state: UpdateState, collect_delta: boo
     state.stats.update_seconds += dt
     state.stats.max_batch_ms = max(state.stats.max_batch_ms, dt * 1e3)
     return delta
+
+
+def _limits(tree: Octree, state: UpdateState, dev_tensor):
+    """LodLimits of one call.  Device inputs are ordered after the work queued
+    so far on torch's current stream of their device (the copy, kernel or
+    collective that produced them), without a host sync."""
+    lim = state._limits
+    lim.backlog_capacity = state.config.backlog_capacity
+    lim.spill_capacity = state.config.spill_capacity
+    lim.input_stream = None
+    if dev_tensor is not None:
+        import torch
+
+        if dev_tensor.device.index != tree.device:
+            raise ValueError(f"input on {dev_tensor.device}, tree on cuda:{tree.device}")
+        lim.input_stream = torch.cuda.current_stream(dev_tensor.device).cuda_stream
+    return lim
 
 
 def _account(state: UpdateState, bs, n_batch: int, profile: bool) -> None:

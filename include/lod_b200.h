@@ -89,7 +89,10 @@ typedef struct {
     uint64_t arena_offset;
     int64_t launches;              /* kernels this call launched                              */
     int64_t h2d_bytes, d2h_bytes;  /* host<->device traffic of this call                      */
-    float device_ms;               /* CUDA-event time of the whole update on the tree stream  */
+    float device_ms;               /* CUDA-event time of the whole update on the tree stream,
+                                      -1 when the call returned before its tail (sort + store +
+                                      cleanup) ran: reported by the next call or lod_tree_wait */
+    float device_ms_prev;          /* the previous call's device_ms if it was -1, else -1     */
     float phase_ms[LOD_NPHASE];    /* with LOD_FLAG_PROFILE: count (k_count only), split,
                                       resolve, backlog, alloc, sort (+ store), delta,
                                       epilogue, h2d, total                                    */
@@ -118,6 +121,12 @@ int lod_tree_info(LodTree *tree, LodTreeInfo *info);
  * ChunkPool.acquire/release (store.py:110-143). */
 int lod_insert_batch(LodTree *tree, const float *xyz, const uint32_t *rgba, int64_t n,
                      const LodLimits *limits, int flags, LodBatchStats *stats);
+
+/* Wait until the tree's stream is idle (the last insert's tail included);
+ * `last_device_ms` (may be NULL) receives that insert's device_ms when the
+ * call returned early (else -1).  Every other entry point that reads the
+ * tree is already ordered behind the tail. */
+int lod_tree_wait(LodTree *tree, float *last_device_ms);
 
 /* Ingest feed (the reference's BatchSource queue feeding
  * run_frame_updates, io.py:340-413, update.py:396-417): start the H2D copy of

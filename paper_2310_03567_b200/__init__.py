@@ -10,7 +10,7 @@ no CPU fallback: without the library or a CUDA device the entry points raise.
 from .errors import BacklogOverflow, OutOfArena, SpillOverflow
 from .octree import CubeBounds, Octree, cubify
 from .store import Arena, ChunkPool
-from .update import BatchDelta, UpdateConfig, UpdateState, insert_batch, run_frame_updates
+from .update import BatchDelta, UpdateConfig, UpdateState, insert_batch, run_frame_updates, wait_settled
 
 __version__ = "0.1.0"
 
@@ -25,6 +25,7 @@ __all__ = [
     "cubify",
     "insert_batch",
     "run_frame_updates",
+    "wait_settled",
     "OutOfArena",
     "SpillOverflow",
     "BacklogOverflow",

@@ -70,7 +70,8 @@ class LodBatchStats(ctypes.Structure):
         ("allocated_total", ctypes.c_int64), ("free_count", ctypes.c_int64),
         ("released_total", ctypes.c_int64), ("arena_offset", ctypes.c_uint64),
         ("launches", ctypes.c_int64), ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
-        ("device_ms", ctypes.c_float), ("phase_ms", ctypes.c_float * LOD_NPHASE),
+        ("device_ms", ctypes.c_float), ("device_ms_prev", ctypes.c_float),
+        ("phase_ms", ctypes.c_float * LOD_NPHASE),
     ]
 
     def as_dict(self) -> dict:
@@ -109,6 +110,7 @@ SIGNATURES = {
                                         ctypes.POINTER(LodBatchStats)]),
     "lod_prefetch_batch": (ctypes.c_int, [_P, _P, _P, _I64]),
     "lod_prefetch_drain": (ctypes.c_int, [_P]),
+    "lod_tree_wait": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_float)]),
     "lod_read_nodes": (ctypes.c_int, [_P, _I64] + [_P] * 13),
     "lod_read_pool": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _I64]),
     "lod_gather": (ctypes.c_int, [_P, _I64, _I64, _P, _P]),

@@ -211,7 +211,10 @@ struct LodTree {
   cudaEvent_t ev_counted = nullptr;  // the running cycle's first count pass is done
   cudaEvent_t ev_input = nullptr;    // the caller's input stream (LOD_FLAG_INPUT_STREAM)
   int stage_next = 0;
-  cudaEvent_t ev[14] = {};  // 12, 13: per-iteration k_count brackets
+  cudaEvent_t ev[16] = {};  // 12, 13: per-iteration k_count brackets; 10/11 and 14/15: the two
+                            // (inputs resident, settled) pairs, alternating between calls
+  int ev_slot = 0;          // pair of the last call
+  bool tail_pending = false;  // the last call returned before its sort + store finished
   // host copies of counters (authoritative after every call)
   long long num_nodes = 1;
   long long d2h_bytes = 0;  // control-block readbacks since the last reset
@@ -253,17 +256,37 @@ __global__ void k_publish(const Ctrl *__restrict__ d, Ctrl *h, volatile unsigned
   if (threadIdx.x == 0) *seq_out = seq;
 }
 
-static int sync_ctrl(LodTree *t) {
+static unsigned publish_ctrl(LodTree *t);
+static int wait_ctrl(LodTree *t, unsigned want);
+
+// Control-block reads through mapped pinned memory (k_publish), unless
+// LOD_SYNC_MEMCPY asks for a copy + stream sync.
+static bool mapped_sync(const LodTree *t) {
   static const bool memcpy_sync = getenv("LOD_SYNC_MEMCPY") != nullptr;
-  if (memcpy_sync || !t->h_seq_dev) {
+  return !memcpy_sync && t->h_seq_dev;
+}
+
+static int sync_ctrl(LodTree *t) {
+  if (!mapped_sync(t)) {
     t->d2h_bytes += (long long)sizeof(Ctrl);
     CK(cudaMemcpyAsync(t->h_ctrl, t->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, t->st));
     CK(cudaStreamSynchronize(t->st));
     return LOD_OK;
   }
+  return wait_ctrl(t, publish_ctrl(t));
+}
+
+// Queue a publication of the control block on the tree stream (no wait).
+static unsigned publish_ctrl(LodTree *t) {
   const unsigned want = ++t->seq;
   t->d2h_bytes += (long long)sizeof(Ctrl);
   lod::launch(k_publish, 1, 32, 0, t->st, t->d_ctrl, t->h_ctrl_dev, t->h_seq_dev, want);
+  return want;
+}
+
+// Wait until publication `want` reached the host (the stream work queued
+// before it is done; work queued after it may still run).
+static int wait_ctrl(LodTree *t, unsigned want) {
   volatile unsigned *flag = t->h_seq;
   for (unsigned spins = 0; *flag != want; ++spins) {
     if ((spins & 1023) == 1023) {
@@ -375,6 +398,9 @@ static int ensure_scan_lb(ScanLB &lb, long long n) {
   CK(cudaMalloc(&lb.incl, (size_t)c * sizeof(T)));
   lb.epoch = 0;
   lb.cap_tiles = c;
+  // the memsets ran on the legacy stream, which the (non-blocking) tree
+  // streams do not wait for
+  CK(cudaDeviceSynchronize());
   return LOD_OK;
 }
 
@@ -629,6 +655,24 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     return LOD_OK;
   }
   if (n >= (1LL << 31)) return LOD_E_ARG;
+  // device-time events: this call's pair, the previous call's kept for its
+  // report when that call returned before its tail ran
+  const bool prev_pending = t->tail_pending;
+  const int prev_slot = t->ev_slot, es = t->ev_slot ^ 1;
+  t->ev_slot = es;
+  t->tail_pending = false;
+  cudaEvent_t EB = es ? t->ev[14] : t->ev[11], EE = es ? t->ev[15] : t->ev[10];
+  // Early return: once allocation has run, nothing later in the cycle can fail
+  // or change what the call reports, so the host returns after the control
+  // block published behind k_alloc_chunks while the sort + store + cleanup
+  // still run on the tree stream (every later call and reader is ordered
+  // behind them on that stream; device inputs are released to the caller's
+  // stream by an event).  Not with a delta or phase profile (both read the
+  // tail's results), nor for device inputs without a stream to order.
+  static const bool no_early = getenv("LOD_NO_EARLY") != nullptr;  // A/B switch
+  const bool early = !no_early && !prof && !delta && mapped_sync(t) &&
+                     (!(flags & LOD_FLAG_DEVICE_INPUT) || ((flags & LOD_FLAG_INPUT_STREAM) && limits));
+  unsigned mid_seq = 0;
   const long long C = t->geo.C;
   const long long launches0 = lod::g_launches;
   t->d2h_bytes = 0;
@@ -684,7 +728,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     bx = t->in_xyz.p;
     bc = t->in_rgba.p;
   }
-  CK(cudaEventRecord(t->ev[11], st));  // inputs resident
+  CK(cudaEventRecord(EB, st));  // inputs resident
   lod::launch(k_cycle_begin, 1, 1, 0, st, t->d_ctrl);
   // ---- expansion (update.py:273-296) with the voxel claims folded in
   RK(t->node_b.ensure(n, st));
@@ -795,6 +839,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
                 t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl, t->arena_cap, guard);
     lod::launch(k_alloc_chunks, grid_for(acq_bound), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p,
                 t->seg_start.p, t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl, guard);
+    if (early) mid_seq = publish_ctrl(t);
     mark(3);
     tp("alloc_launched");
     // ---- sort + store (update.py:357-373): stable by node id = slot order
@@ -860,11 +905,12 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       // the pipeline's host-side sizes: nodes as of now (no further split if
       // it runs), new voxels bounded by the claim table's capacity
       RK(pipeline(&t->d_ctrl->spec_abort, (long long)t->hcap));
-      CK(cudaEventRecord(t->ev[10], st));
+      CK(cudaEventRecord(EE, st));
       pipeline_launched = true;
     }
     tp("pre_sync");
-    RK(sync_ctrl(t));
+    if (pipeline_launched && early) RK(wait_ctrl(t, mid_seq));
+    else RK(sync_ctrl(t));
     tp("sync");
     if (prof) {
       float x = 0.f;
@@ -961,9 +1007,10 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     if (h1.hash_overflow) return abort_cycle(t, LOD_E_NOMEM);
     RK(pipeline(nullptr, (long long)h1.n_used));
     mark(6);
-    CK(cudaEventRecord(t->ev[10], st));
+    CK(cudaEventRecord(EE, st));
     tp("all_launched");
-    RK(sync_ctrl(t));
+    if (early) RK(wait_ctrl(t, mid_seq));
+    else RK(sync_ctrl(t));
     tp("final_sync");
   }
   if (tl) fprintf(stderr, "[lod] timeline%s\n", tlbuf);
@@ -984,17 +1031,29 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   S.n_splits = splits_cycle;
   S.iterations = iters;
   fill_stats(t, &S);
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, t->ev[11], t->ev[10]);
+  float ms = -1.f;
+  if (early) {  // the tail is still running: its time is reported by the next call / lod_tree_wait
+    t->tail_pending = true;
+    if (flags & LOD_FLAG_DEVICE_INPUT)  // the store re-reads the batch: the caller's stream waits
+      CK(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(limits->input_stream), EE, 0));
+  } else {
+    cudaEventElapsedTime(&ms, EB, EE);
+  }
   S.device_ms = ms;
+  S.device_ms_prev = -1.f;
+  if (prev_pending) {  // queued before this call's last publication: complete by now
+    cudaEvent_t pb = prev_slot ? t->ev[14] : t->ev[11], pe = prev_slot ? t->ev[15] : t->ev[10];
+    if (cudaEventQuery(pe) == cudaSuccess) cudaEventElapsedTime(&S.device_ms_prev, pb, pe);
+    else cudaGetLastError();
+  }
   if (lod_debug())
     fprintf(stderr, "[lod] batch n=%lld n_s=%lld n_v=%lld iters=%d splits=%lld nodes=%lld %.3f ms\n", (long long)n,
             n_s, n_v, iters, splits_cycle, (long long)S.num_nodes, ms);
   if (prof) {
     // phases: count, split, resolve, backlog, alloc, sort (+ store), delta, epilogue, h2d, total
     float h2d = 0.f;
-    cudaEventElapsedTime(&h2d, t->ev[0], t->ev[11]);
-    cudaEvent_t prev = t->ev[11];
+    cudaEventElapsedTime(&h2d, t->ev[0], EB);
+    cudaEvent_t prev = EB;
     float seg[7];
     for (int k = 0; k < 7; ++k) {
       seg[k] = 0.f;
@@ -1007,6 +1066,19 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     S.phase_ms[8] = h2d;
     S.phase_ms[9] = ms;
   }
+  return LOD_OK;
+}
+
+int lod_tree_wait(LodTree *t, float *last_device_ms) {
+  if (!t) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  CK(cudaStreamSynchronize(t->st));
+  float ms = -1.f;
+  if (t->tail_pending) {
+    cudaEventElapsedTime(&ms, t->ev_slot ? t->ev[14] : t->ev[11], t->ev_slot ? t->ev[15] : t->ev[10]);
+    t->tail_pending = false;
+  }
+  if (last_device_ms) *last_device_ms = ms;
   return LOD_OK;
 }
 
@@ -1149,8 +1221,13 @@ int lod_prefetch_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64
     if (sg.valid && sg.hx == xyz && sg.hc == rgba && sg.n == n) return LOD_OK;  // already staged
   LodTree::Stage &sg = t->stage[t->stage_next];
   t->stage_next = (t->stage_next + 1) % 3;
-  // the slot's previous batch was consumed by a completed insert (every
-  // lod_insert_batch returns after its update finished), or is superseded
+  // the slot's previous batch was consumed by an earlier insert (or is
+  // superseded); that insert's tail may still read it on the tree stream, so
+  // a growing slot frees its old buffers only behind the tree stream
+  if (3 * n > sg.xyz.cap || n > sg.rgba.cap) {
+    CK(cudaEventRecord(t->ev_counted, t->st));
+    CK(cudaStreamWaitEvent(t->cst, t->ev_counted, 0));
+  }
   RK(sg.xyz.ensure(3 * n, t->cst));
   RK(sg.rgba.ensure(n, t->cst));
   // The copy itself is issued by the next lod_insert_batch behind its first

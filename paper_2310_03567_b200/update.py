@@ -264,11 +264,30 @@ def _account(state: UpdateState, bs, n_batch: int, profile: bool) -> None:
     st.voxels_created += n_v
     st.splits = int(bs.splits_total)
     st.nodes = int(bs.num_nodes)
-    st.device_seconds += float(bs.device_ms) * 1e-3
+    # device time: this call's, or (when it returned before its tail ran) the
+    # previous early call's, reported now; wait_settled collects the last one
+    for ms in (bs.device_ms, bs.device_ms_prev):
+        if ms >= 0:
+            st.device_seconds += float(ms) * 1e-3
     st.launches += int(bs.launches)
     st.h2d_bytes += int(bs.h2d_bytes)
     st.d2h_bytes += int(bs.d2h_bytes)
     state.last = bs.as_dict() if profile else None
+
+
+def wait_settled(tree: Octree, state: UpdateState | None = None) -> float:
+    """Block until the tree's last update has fully run on the device.
+
+    insert_batch returns once the cycle's outcome is final (allocation done,
+    errors raised); the sort + store + cleanup of its last pass may still run
+    on the tree's stream, ahead of every later call on the tree.  Returns that
+    update's device ms (-1 if none was outstanding) and adds it to
+    ``state.stats.device_seconds``."""
+    ms = ctypes.c_float(-1.0)
+    _lib.check(tree._L.lod_tree_wait(tree.handle, ctypes.byref(ms)), "tree_wait")
+    if state is not None and ms.value >= 0:
+        state.stats.device_seconds += ms.value * 1e-3
+    return float(ms.value)
 
 
 def _read_delta(tree: Octree) -> BatchDelta:

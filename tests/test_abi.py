@@ -53,7 +53,7 @@ def test_struct_layouts_match_header():
 
     assert ctypes.sizeof(_lib.LodParams) == 3 * 8 + 8 + 4 * 8 + 8 + 4 + 4
     assert ctypes.sizeof(_lib.LodLimits) == 24
-    assert ctypes.sizeof(_lib.LodBatchStats) == 15 * 8 + 4 + 4 * _lib.LOD_NPHASE + 4  # tail padding
+    assert ctypes.sizeof(_lib.LodBatchStats) == 15 * 8 + 4 + 4 + 4 * _lib.LOD_NPHASE
     assert ctypes.sizeof(_lib.LodTreeInfo) == 12 * 8
 
 

@@ -67,3 +67,58 @@ def test_input_on_other_device_rejected(gpu):
     x, c = synth.gen_uniform(1000, 1)
     with pytest.raises(ValueError):
         insert_batch(t, torch.from_numpy(x).to("cuda:1"), torch.from_numpy(c.view(np.int32)).to("cuda:1"), s)
+
+
+@pytest.mark.parametrize("packed", [False, True])
+def test_inputs_reused_right_after_insert(gpu, packed):
+    """insert returns before the last pass's store has re-read the batch: the
+    caller's stream is made to wait, so overwriting the input at once is safe."""
+    import torch
+
+    from paper_2310_03567_b200 import insert_batch, synth
+    from paper_2310_03567_b200.update import insert_records
+
+    want_t, want_s = make_product(PARAMS)
+    got_t, got_s = make_product(PARAMS)
+    for i in range(4):
+        x, c = synth.gen_surface(60_000, 90 + i)
+        rec = np.concatenate([x.view(np.int32), c.view(np.int32).reshape(-1, 1)], axis=1)
+        insert_batch(want_t, x, c, want_s)
+        if packed:
+            drec = torch.from_numpy(rec).cuda()
+            insert_records(got_t, drec, got_s)
+            drec.fill_(0x7FC00000)  # NaN coordinates
+        else:
+            dx, dc = torch.from_numpy(x).cuda(), torch.from_numpy(c.view(np.int32)).cuda()
+            insert_batch(got_t, dx, dc, got_s)
+            dx.fill_(float("nan"))
+            dc.fill_(0)
+    torch.cuda.synchronize()
+    assert_same_state(product_state(got_t), product_state(want_t), chunk_ids=True,
+                      label="packed" if packed else "xyz+rgba")
+
+
+def test_device_time_reported_after_early_return(gpu):
+    """Early-returning calls report device_ms = -1; the next call (device_ms_prev)
+    or wait_settled reports it, and UpdateStats.device_seconds gets every batch."""
+    from paper_2310_03567_b200 import insert_batch, synth, wait_settled
+
+    t, s = make_product(PARAMS)
+    got = []
+    for i in range(5):
+        x, c = synth.gen_surface(60_000, 110 + i)
+        insert_batch(t, x, c, s)
+        b = s._bstats
+        got.append((float(b.device_ms), float(b.device_ms_prev)))
+    last = wait_settled(t, s)
+    assert all(d < 0 for d, _ in got)  # host input, no delta / profile: every call returned early
+    assert got[0][1] < 0 and all(p > 0 for _, p in got[1:])
+    assert last > 0 and wait_settled(t, s) < 0  # nothing outstanding the second time
+    total = sum(p for _, p in got[1:]) + last
+    assert s.stats.device_seconds == pytest.approx(total * 1e-3, rel=1e-4)
+    # profile / delta calls are synchronous: their own time, and the pending one
+    x, c = synth.gen_surface(60_000, 120)
+    insert_batch(t, x, c, s)
+    insert_batch(t, *synth.gen_surface(60_000, 121), s, profile=True)
+    assert s._bstats.device_ms > 0 and s._bstats.device_ms_prev > 0
+    assert wait_settled(t, s) < 0

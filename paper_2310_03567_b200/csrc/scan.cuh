@@ -86,6 +86,9 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T *sh, T &total) {
   return out;
 }
 
+#ifndef LOD_SCAN_VEC
+#define LOD_SCAN_VEC 1
+#endif
 constexpr int kScanBlock = 512;
 constexpr int kScanItems = 8;
 constexpr long long kScanTile = (long long)kScanBlock * kScanItems;
@@ -131,11 +134,22 @@ __global__ void __launch_bounds__(kScanBlock)
   const long long base = tile * kScanTile + (long long)threadIdx.x * kScanItems;
   T v[kScanItems];
   T acc = T();
+  // u32 items of a full tile: two 16-byte loads per thread
+  constexpr bool kVec = LOD_SCAN_VEC && sizeof(T) == 4 && kScanItems == 8;
+  const bool vec = kVec && base + kScanItems <= n;
+  if constexpr (kVec) if (vec) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(in + base);
+    const uint4 a = p[0], b = p[1];
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    v[i] = base + i < n ? in[base + i] : T();
-    acc = acc + v[i];
+    for (int i = 0; i < kScanItems; ++i) v[i] = *reinterpret_cast<const T *>(&w[i]);
   }
+  if (!vec) {
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) v[i] = base + i < n ? in[base + i] : T();
+  }
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) acc = acc + v[i];
   T total;
   T run = block_exclusive_scan<T, kScanBlock>(acc, sh, total);
   if (threadIdx.x < 32) {  // warp 0 publishes and looks back, 32 predecessors per round trip
@@ -187,6 +201,18 @@ __global__ void __launch_bounds__(kScanBlock)
   }
   __syncthreads();
   run = run + s_excl;
+  if constexpr (kVec) if (vec) {
+    uint32_t w[8];
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      w[i] = *reinterpret_cast<const uint32_t *>(&run);
+      run = run + v[i];
+    }
+    uint4 *q = reinterpret_cast<uint4 *>(out + base);
+    q[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    q[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
     if (base + i < n) out[base + i] = run;

@@ -399,7 +399,7 @@ def secondary_rows(args, tree, state, dev_b, dev) -> dict:
 
     import torch
 
-    from paper_2310_03567_b200 import _lib, insert_batch, synth
+    from paper_2310_03567_b200 import _lib, insert_batch, synth, wait_settled
     from paper_2310_03567_b200.render import Camera, frustum_planes, select_visible
 
     out = {}

@@ -506,21 +506,27 @@ int lod_tree_create(const LodParams *params, LodTree **out) {
       unsigned long long thr = ~0ull;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
       // Back the pool with physical memory once per device (LOD_POOL_RESERVE_MIB,
-      // default 6 GiB, at most 1/8 of free HBM): scratch growth during a split
+      // default 16 GiB, at most 1/8 of free HBM): scratch growth during a split
       // burst is then a pool sub-allocation instead of a page-table mapping
-      // inside the update (measured: 20-27 ms first-touch stalls on 5.8M-point spills).
+      // inside the update (measured: 20-27 ms first-touch stalls on 5.8M-point
+      // spills; the skew stream's 20-43M-point split waves need ~10 GiB of
+      // scratch: 6 -> 16 GiB took its bench from 1202 to 1362 M points/s).
       static bool warmed[64] = {};
       if (t->dev < 64 && !warmed[t->dev]) {
         warmed[t->dev] = true;
         const char *e = getenv("LOD_POOL_RESERVE_MIB");
-        unsigned long long want = (e ? strtoull(e, nullptr, 10) : 6144ull) << 20;
+        unsigned long long want = (e ? strtoull(e, nullptr, 10) : 16384ull) << 20;
         size_t fr = 0, tot = 0;
         if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) want = std::min<unsigned long long>(want, fr / 8);
         void *q = nullptr;
+        const auto w0 = std::chrono::steady_clock::now();
         if (want && cudaMallocAsync(&q, want, t->st) == cudaSuccess) {
           cudaFreeAsync(q, t->st);
           cudaStreamSynchronize(t->st);
         }
+        if (lod_debug())
+          fprintf(stderr, "[lod] pool reserve %.1f GiB in %.1f ms\n", want / 1073741824.0,
+                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count());
         cudaGetLastError();
       }
     }
@@ -888,6 +894,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   // iteration on (the first usually splits), or from the first when the last
   // cycle needed a single one; never while profiling (phase events)
   static const bool no_spec = getenv("LOD_NO_SPEC") != nullptr;
+  long long spec_used = 0;  // claims after the last synced iteration
   const bool may_speculate = !prof && !no_spec;
   for (;;) {
     ++iters;
@@ -898,13 +905,19 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     if (prof) cudaEventRecord(t->ev[13], st);
     lod::launch(k_decide_mark, grid_for(t->num_nodes), 256, 0, st, t->nd, t->geo, t->touched.p, t->bitmap.p,
                 t->d_ctrl);
+    // a speculative pipeline's host-side sizes: nodes as of now (no further
+    // split if it runs); new voxels at most the claims so far + one per
+    // re-descending point (known after an iteration), else the claim table's
+    // capacity -- k_decide stands the pipeline down past that bound (or past
+    // backlog_capacity; the host path then decides)
+    const bool speculate = may_speculate && (iters >= 2 || t->last_iters == 1);
+    const long long nv_bound = iters >= 2 ? std::min<long long>((long long)t->hcap, spec_used + n_all)
+                                          : (long long)t->hcap;
     lod::launch(k_decide, 1, kDecideBlock, 0, st, t->nd, t->geo, t->bitmap.p, t->split_list.p, t->srank.p,
                 t->scnt.p, t->schk.p, t->spill_off.p, t->chunk_off.p, t->d_ctrl, spill_cap, t->arena_cap,
-                backlog_cap);
-    if (may_speculate && (iters >= 2 || t->last_iters == 1)) {
-      // the pipeline's host-side sizes: nodes as of now (no further split if
-      // it runs), new voxels bounded by the claim table's capacity
-      RK(pipeline(&t->d_ctrl->spec_abort, (long long)t->hcap));
+                std::min<long long>(backlog_cap, nv_bound));
+    if (speculate) {
+      RK(pipeline(&t->d_ctrl->spec_abort, nv_bound));
       CK(cudaEventRecord(EE, st));
       pipeline_launched = true;
     }
@@ -918,6 +931,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       count_ms += x;
     }
     const Ctrl &h = *t->h_ctrl;
+    spec_used = (long long)h.n_used;
     if (h.error) return abort_cycle(t, h.error);
     const long long ns = h.n_splits;
     if (ns == 0) break;  // settled (a speculative pipeline ran iff spec_abort == 0)

@@ -499,7 +499,34 @@ def roofline_from_phases(phases: list[dict], peak: float) -> tuple[dict, dict]:
         "whole_update": {"achieved": gbs.get("total"), "frac": round(gbs.get("total", 0) / peak, 4)},
         "phase_gbs": gbs,
     }
+    # the count phase is bound by L2 atomics, not bytes: one 128-bit CAS install
+    # per new voxel (claims are ~1.04x the new voxels), against the measured
+    # random-install rate of tools/cas_bench.cu (profiles/r01_cas_roofline.txt)
+    cas = cas_peak()
+    if cas and tot.get("count"):
+        n_v = sum(p["_counts"][2] for p in phases)
+        rate = n_v / (tot["count"] * 1e-3) / 1e9
+        roof["atomics"] = {"bound": "l2_atomics", "kernel": "k_count", "achieved": round(rate, 2),
+                           "unit": "G installs/s", "peak": round(cas[0], 2), "frac": round(rate / cas[0], 3),
+                           "peak_source": cas[1]}
     return roof, {"median_ms": med, "mean_ms": {k: round(tot[k] / len(phases), 4) for k in tot}}
+
+
+def cas_peak():
+    """Best measured 128-bit CAS install rate (G/s) from the committed
+    microbenchmark output, or None."""
+    import re
+
+    path = os.path.join(ROOT, "profiles", "r01_cas_roofline.txt")
+    try:
+        best = 0.0
+        for line in open(path):
+            m = re.search(r"([0-9.]+)M installs\s+cas128\s+([0-9.]+) us", line)
+            if m:
+                best = max(best, float(m.group(1)) * 1e6 / (float(m.group(2)) * 1e-6) / 1e9)
+        return (best, "tools/cas_bench.cu, profiles/r01_cas_roofline.txt") if best else None
+    except OSError:
+        return None
 
 
 def load_traffic(kernel: str | None):

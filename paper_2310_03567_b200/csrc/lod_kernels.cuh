@@ -64,6 +64,8 @@ struct Ctrl {
   unsigned int n_xchunks;     // chunks of the iteration's splitting nodes (k_split_chunk_list)
   unsigned int d_nvg;         // voxel groups (inner nodes with new voxels)
   unsigned int d_npg;         // point groups (leaves with new points)
+  long long redescend;        // k_decide: points in the splitting nodes (stored + pending) -- the only
+                              // points the next count pass re-descends, each claiming at most one cell
 };
 
 __device__ __forceinline__ void set_error(Ctrl *c, int code) { atomicCAS(&c->error, 0, code); }
@@ -325,11 +327,13 @@ __global__ void __launch_bounds__(kDecideBlock)
   __shared__ U64x2 sh64[kDecideBlock / 32 + 1];
   __shared__ unsigned int s_maxlvl;
   __shared__ long long s_err_spill;
+  __shared__ unsigned long long s_pend;  // pending points of the splitting nodes
   const int tid = threadIdx.x;
   const long long nn = ctrl->num_nodes;
   if (tid == 0) {
     s_maxlvl = 0;
     s_err_spill = -1;
+    s_pend = 0;
   }
   // phase 2: popcount prefix over the bitmap words (contiguous word ranges per thread)
   const long long W = (nn + 31) / 32;
@@ -354,6 +358,7 @@ __global__ void __launch_bounds__(kDecideBlock)
       srank[nid] = (int32_t)run;
       scnt[run] = nd.count[nid];
       schk[run] = nd.chunk_count[nid];
+      atomicAdd(&s_pend, (unsigned long long)nd.pending[nid]);
       atomicMax(&s_maxlvl, (unsigned)(nd.level[nid] + 1));
       ++run;
     }
@@ -397,6 +402,7 @@ __global__ void __launch_bounds__(kDecideBlock)
     else if (err_ooa >= 0) set_error(ctrl, 1 /*LOD_E_OUT_OF_ARENA*/);
     ctrl->n_splits = ns;
     ctrl->spill_add = (long long)carry.a;
+    ctrl->redescend = (long long)carry.a + (long long)s_pend;
     ctrl->plan_num_nodes0 = nn;
     ctrl->plan_free0 = ctrl->free_count;
     ctrl->plan_spill0 = spill0;

@@ -820,9 +820,17 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     {
       // node counts in per-CTA shared memory (16-bit counters) up to
       // kNodeHistSmemMax nodes, as long as no CTA can see 65535 items
-      const unsigned grid = std::min<unsigned>(grid_for(n_items, kRadixBlock * kPrepItems), 148 * kPrepBlocksPerSM);
+      // kNodeHistSmemMax nodes, as long as no CTA can see 65535 items; one
+      // wave: as many CTAs per SM as their histograms fit (228 KB per SM)
       long long nc_words = (num_nodes + 1) / 2;
-      if (num_nodes > kNodeHistSmemMax || n_items > (long long)grid * 65535) nc_words = 0;
+      int bps = LOD_PREP_BPS;
+      if (num_nodes <= kNodeHistSmemMax)
+        bps = (int)std::max<long long>(1, std::min<long long>(LOD_PREP_BPS, 233472 / (nc_words * 4 + 1024)));
+      unsigned grid = std::min<unsigned>(grid_for(n_items, kRadixBlock * kPrepItems), 148 * bps);
+      if (num_nodes > kNodeHistSmemMax || n_items > (long long)grid * 65535) {
+        nc_words = 0;
+        grid = std::min<unsigned>(grid_for(n_items, kRadixBlock * kPrepItems), 148 * kPrepBlocksPerSM);
+      }
       static bool smem_attr[64] = {};  // per device
       if (t->dev < 64 && !smem_attr[t->dev]) {
         CK(cudaFuncSetAttribute(k_radix_prep, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -894,7 +902,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   // iteration on (the first usually splits), or from the first when the last
   // cycle needed a single one; never while profiling (phase events)
   static const bool no_spec = getenv("LOD_NO_SPEC") != nullptr;
-  long long spec_used = 0;  // claims after the last synced iteration
+  long long spec_used = 0;    // claims after the last synced iteration
+  long long spec_redesc = 0;  // points the next count pass re-descends (each claims at most one cell)
   const bool may_speculate = !prof && !no_spec;
   for (;;) {
     ++iters;
@@ -911,7 +920,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     // capacity -- k_decide stands the pipeline down past that bound (or past
     // backlog_capacity; the host path then decides)
     const bool speculate = may_speculate && (iters >= 2 || t->last_iters == 1);
-    const long long nv_bound = iters >= 2 ? std::min<long long>((long long)t->hcap, spec_used + n_all)
+    const long long nv_bound = iters >= 2 ? std::min<long long>((long long)t->hcap, spec_used + spec_redesc)
                                           : (long long)t->hcap;
     lod::launch(k_decide, 1, kDecideBlock, 0, st, t->nd, t->geo, t->bitmap.p, t->split_list.p, t->srank.p,
                 t->scnt.p, t->schk.p, t->spill_off.p, t->chunk_off.p, t->d_ctrl, spill_cap, t->arena_cap,
@@ -932,6 +941,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     }
     const Ctrl &h = *t->h_ctrl;
     spec_used = (long long)h.n_used;
+    spec_redesc = h.redescend;
     if (h.error) return abort_cycle(t, h.error);
     const long long ns = h.n_splits;
     if (ns == 0) break;  // settled (a speculative pipeline ran iff spec_abort == 0)
@@ -968,9 +978,10 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       n_all = n_s + n;
       first = 0;
     }
-    // the next pass claims at most one cell per re-descending point
-    if ((long long)h.n_used + n_all > (long long)(3 * t->hcap / 4)) {
-      const unsigned long long H = round_slots((unsigned long long)(2 * ((long long)h.n_used + n_all)));
+    // the next pass claims at most one cell per re-descending point (the
+    // points of the nodes that just split)
+    if ((long long)h.n_used + h.redescend > (long long)(3 * t->hcap / 4)) {
+      const unsigned long long H = round_slots((unsigned long long)(2 * ((long long)h.n_used + h.redescend)));
       if (lod_debug()) fprintf(stderr, "[lod] claim table grow %llu -> %llu (rehash %llu)\n", t->hcap, H, h.n_used);
       RK(t->hslots2.ensure((long long)H, st));
       CK(cudaMemsetAsync(t->hslots2.p, 0xFF, (size_t)t->hslots2.cap * sizeof(HSlot), st));

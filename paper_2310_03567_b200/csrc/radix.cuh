@@ -49,6 +49,9 @@ constexpr uint32_t kLbAgg = 1u << 30, kLbPre = 2u << 30, kLbMask = (1u << 30) - 
 // 4 items per thread per round (independent loads in flight), 4 CTAs per SM.
 constexpr int kPrepItems = 4;
 constexpr int kPrepBlocksPerSM = 4;
+#ifndef LOD_PREP_BPS
+#define LOD_PREP_BPS 2  // CTAs per SM with shared-memory node histograms (capped by what fits)
+#endif
 static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
     k_radix_prep(NodeOf node_of, long long n_all, const uint4 *__restrict__ backlog,
                  long long nc_words, uint32_t *__restrict__ keys, uint32_t *__restrict__ nodecnt,

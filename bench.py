@@ -148,7 +148,8 @@ def new_tree(device: int, arena_bytes: int):
 def run_multi(args, rank, world, local_rank):
     """N > 1: every step is a global batch of N x 1M points arriving striped
     (1M per rank); points are routed to the owners of their octant prefixes
-    with one NCCL all-to-all and inserted into the owner's tree
+    by the fused bucket scatter into the owners' peer-memory windows
+    (multigpu.PeerRouter) and inserted into the owner's tree
     (paper_2310_03567_b200/multigpu.py).  Warm-up batches run the single-tree
     protocol on rank 0 until the top is inner, then rank 0's tree is
     broadcast.  Weak scaling: per-GPU input is fixed at 1M points per step."""
@@ -223,7 +224,8 @@ def run_multi(args, rank, world, local_rank):
             "config": {"workload": CONFIGS[args.config][1] + f"; global batch {world} x 1M striped over ranks",
                        "batch_points": BATCH * world, "tree": PARAMS,
                        "parallelism": f"octant-prefix partition depth {plan.depth} x{world}, "
-                                      f"{backend.upper()} all-to-all routing",
+                                      f"peer-memory routing (bucket scatter into CUDA IPC windows), "
+                                      f"{backend.upper()} barriers",
                        "imbalance_max_over_mean": round(partition.imbalance(plan), 3),
                        "l2": "inputs larger than L2: distinct 16 MB stripes per step"},
             "e2e": {"value": round(pts / (t_e2e * 1e-3) / 1e6, 2), "unit": "Mpts/s",
@@ -233,6 +235,7 @@ def run_multi(args, rank, world, local_rank):
                             "insert, max over ranks"},
             "gpu_launches": launches, "clocks": clocks.summary(),
         }
+    ins.close()
     dist.destroy_process_group()
     return line
 

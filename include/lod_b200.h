@@ -238,6 +238,38 @@ int lod_route_bucket(int32_t device, const double *bmin, double size, int32_t de
                      int32_t world, const float *xyz, const uint32_t *rgba, int64_t n, void *out_records,
                      int64_t *counts, int64_t *starts, void *stream);
 
+/* Multi-GPU routing and composite over peer memory (the fused
+ * replacement for the all-to-all and the all-reduce): each rank owns one
+ * receive window -- an IPC-shareable device allocation (NVLink peer memory
+ * between GPUs) laid out as the int64 count matrix [source][owner] in the
+ * first LOD_WINDOW_HEADER_BYTES, then two halves of `half_records` 16-byte
+ * records -- and maps every peer's window (`windows[r]` = rank r's window as
+ * seen by this process, its own included).  Per batch:
+ *   lod_route_peers_begin   owners + bucket sizes of this rank's stripe, the
+ *                           sizes stored as row `rank` of every peer's matrix;
+ *   (host: stream sync + barrier; every rank reads the full matrix)
+ *   lod_route_peers_finish  the stable bucket scatter, each record written
+ *                           straight into its owner's window half `half`
+ *                           behind the lower source ranks' records;
+ *   (host: stream sync + barrier; the owner inserts its half, global order).
+ * lod_composite_min_peers: the depth-min of all ranks' framebuffers (`fbs`,
+ * mapped windows of npix u64 each) over this rank's pixel slice, written back
+ * into every framebuffer; after all ranks ran it (stream sync + barrier)
+ * every framebuffer holds the composite.  Handles are
+ * LOD_IPC_HANDLE_BYTES-byte cudaIpcMemHandle_t blobs. */
+#define LOD_IPC_HANDLE_BYTES 64
+#define LOD_WINDOW_HEADER_BYTES (64 * 64 * 8)
+int lod_ipc_alloc(int32_t device, uint64_t bytes, void **ptr, void *handle); /* zeroed; free: lod_device_free */
+int lod_ipc_open(int32_t device, const void *handle, void **ptr);
+int lod_ipc_close(void *ptr);
+int lod_route_peers_begin(int32_t device, const double *bmin, double size, int32_t depth,
+                          const int32_t *owner_of_prefix, int32_t world, int32_t rank, const float *xyz, int64_t n,
+                          void *const *windows, void *stream);
+int lod_route_peers_finish(int32_t device, int32_t world, int32_t rank, const float *xyz, const uint32_t *rgba,
+                           int64_t n, void *const *windows, int32_t half, int64_t half_records, void *stream);
+int lod_composite_min_peers(int32_t device, int32_t world, int32_t rank, void *const *fbs, int64_t npix,
+                            void *stream);
+
 /* Device-side helpers for benchmarking the resident path (inputs in HBM). */
 int lod_device_alloc(int32_t device, uint64_t bytes, void **ptr);
 int lod_device_free(void *ptr);

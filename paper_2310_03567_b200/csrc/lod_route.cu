@@ -29,6 +29,17 @@ constexpr int kRouteRounds = 8;  // per warp: 8 x 32 consecutive points
 constexpr int kRouteTile = kRouteBlock * kRouteRounds;
 constexpr int kRouteMaxWorld = 64;
 
+// A rank's receive window (one cudaMalloc, shared with the other ranks over
+// CUDA IPC; NVLink peer memory between GPUs): the int64 count matrix
+// [source rank][owner rank] in the first kWindowHeader bytes, then two halves
+// of 16-byte records (batches alternate halves, so a sender's next batch never
+// lands on records the owner's previous insert may still read).
+constexpr size_t kWindowHeader = LOD_WINDOW_HEADER_BYTES;
+static_assert(kWindowHeader == (size_t)kRouteMaxWorld * kRouteMaxWorld * 8, "window header");
+struct PeerWindows {
+  char *p[kRouteMaxWorld];  // p[r] = rank r's window as mapped in this process (own window: local)
+};
+
 struct RouteGeo {
   double bmin[3];
   double size;
@@ -94,12 +105,37 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+// Where bucket o of this rank's stripe goes: the local packed buffer at
+// starts[o] (lod_route_bucket), or -- the fused peer-memory route -- straight
+// into owner o's receive window over NVLink, behind the records of the lower
+// source ranks (offset = sum over s < rank of the window count matrix's
+// column o, identical on every rank after the count exchange).
+struct LocalDest {
+  const long long *starts;
+  float4 *out;
+  __device__ float4 *base(int o) const { return out + starts[o]; }
+};
+struct PeerDest {
+  PeerWindows win;
+  int rank, world, half;
+  long long half_records;
+  __device__ float4 *base(int o) const {
+    const long long *m = reinterpret_cast<const long long *>(win.p[rank]);  // my copy of the matrix
+    long long off = 0;
+    for (int s = 0; s < rank; ++s) off += m[s * world + o];
+    return reinterpret_cast<float4 *>(win.p[o] + kWindowHeader) + (long long)half * half_records + off;
+  }
+};
+
+template <typename Dest>
 __global__ void __launch_bounds__(kRouteBlock)
     k_route_scatter(const float *__restrict__ xyz, const uint32_t *__restrict__ rgba, long long n, int world,
-                    const uint8_t *__restrict__ owner, const uint32_t *__restrict__ tile_off,
-                    const long long *__restrict__ starts, float4 *__restrict__ out) { lod::pdl_wait();
+                    const uint8_t *__restrict__ owner, const uint32_t *__restrict__ tile_off, Dest dest) {
+  lod::pdl_wait();
   __shared__ uint32_t wtot[kRouteBlock / 32][kRouteMaxWorld];  // per-warp bucket totals -> warp offsets
   __shared__ uint16_t lrank[kRouteTile];
+  __shared__ float4 *s_base[kRouteMaxWorld];
+  for (int d = threadIdx.x; d < world; d += kRouteBlock) s_base[d] = dest.base(d);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = lanemask_lt();
   const long long t0 = (long long)blockIdx.x * kRouteTile;
@@ -140,10 +176,55 @@ __global__ void __launch_bounds__(kRouteBlock)
     const long long i = t0 + li;
     if (i >= n) continue;
     const int o = owner[i];
-    const long long pos = starts[o] + tile_off[(long long)blockIdx.x * world + o] + wtot[warp][o] + lrank[li];
-    out[pos] = make_float4(__ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1), __ldg(xyz + 3 * i + 2),
+    const long long pos = tile_off[(long long)blockIdx.x * world + o] + wtot[warp][o] + lrank[li];
+    s_base[o][pos] = make_float4(__ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1), __ldg(xyz + 3 * i + 2),
                            __uint_as_float(__ldg(rgba + i)));
   }
+}
+
+// The count exchange: this rank's bucket sizes become row `rank` of every
+// peer's count matrix (world x world remote 8-byte stores).
+__global__ void k_route_publish(const long long *__restrict__ counts, int rank, int world, PeerWindows win) {
+  lod::pdl_wait();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < world * world) {
+    const int peer = t / world, o = t % world;
+    reinterpret_cast<long long *>(win.p[peer])[rank * world + o] = counts[o];
+  }
+  __threadfence_system();
+}
+
+// Depth-min composite over peer memory, reduce-scatter and all-gather fused:
+// rank r owns pixel slice r; for each of its pixels it reads every rank's
+// framebuffer, takes the unsigned 64-bit min (the all-ones sentinel is the
+// largest value, so it needs no mapping) and writes the result back into every
+// rank's framebuffer.  Slices are disjoint, so the ranks' kernels never touch
+// the same word.  Two pixels per thread (16-byte loads/stores).
+__global__ void __launch_bounds__(256)
+    k_composite_min(PeerWindows fb, int world, long long lo, long long hi) {
+  lod::pdl_wait();
+  const long long stride = (long long)gridDim.x * blockDim.x * 2;
+  for (long long i = lo + ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 2; i < hi; i += stride) {
+    if (i + 1 < hi && (i & 1) == 0) {
+      ulonglong2 m = make_ulonglong2(~0ull, ~0ull);
+      for (int r = 0; r < world; ++r) {
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(fb.p[r] + i * 8);
+        m.x = v.x < m.x ? v.x : m.x;
+        m.y = v.y < m.y ? v.y : m.y;
+      }
+      for (int r = 0; r < world; ++r) *reinterpret_cast<ulonglong2 *>(fb.p[r] + i * 8) = m;
+    } else {
+      for (long long j = i; j < i + 2 && j < hi; ++j) {
+        unsigned long long m = ~0ull;
+        for (int r = 0; r < world; ++r) {
+          const unsigned long long v = reinterpret_cast<const unsigned long long *>(fb.p[r])[j];
+          m = v < m ? v : m;
+        }
+        for (int r = 0; r < world; ++r) reinterpret_cast<unsigned long long *>(fb.p[r])[j] = m;
+      }
+    }
+  }
+  __threadfence_system();
 }
 
 inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
@@ -163,25 +244,16 @@ struct RouteScratch {
   uint8_t *owner = nullptr;
   uint32_t *tiles = nullptr;
   int32_t *table = nullptr;
+  long long *counts = nullptr, *starts = nullptr;  // device, for the peer route
   long long cap = 0, tcap = 0, table_cap = 0;
 };
 std::mutex g_mu;
 RouteScratch g_rs[64];
 
-}  // namespace
-
-extern "C" {
-
-int lod_route_bucket(int32_t device, const double *bmin, double size, int32_t depth, const int32_t *owner_of_prefix,
-                     int32_t world, const float *xyz, const uint32_t *rgba, int64_t n, void *out_records,
-                     int64_t *counts, int64_t *starts, void *stream) {
-  if (!bmin || !owner_of_prefix || depth < 0 || depth > 8 || world < 1 || world > kRouteMaxWorld || n < 0 ||
-      (n > 0 && (!xyz || !rgba || !out_records)) || !counts || !starts || device < 0 || device >= 64)
-    return LOD_E_ARG;
-  std::lock_guard<std::mutex> lk(g_mu);
-  cudaSetDevice(device);
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  RouteScratch &s = g_rs[device];
+// Owners, per-tile bucket counts and their scans (the first two launches of
+// both routes); counts / starts are device arrays of `world` entries.
+int route_prepare(RouteScratch &s, const double *bmin, double size, int depth, const int32_t *owner_of_prefix,
+                  int world, const float *xyz, long long n, long long *counts, long long *starts, cudaStream_t st) {
   const long long ntiles = std::max<long long>((n + kRouteTile - 1) / kRouteTile, 1);
   if (n > s.cap) {
     if (s.owner) cudaFree(s.owner);
@@ -208,14 +280,129 @@ int lod_route_bucket(int32_t device, const double *bmin, double size, int32_t de
   g.depth = depth;
   g.world = world;
   if (n > 0)
-    lod::launch(k_route_count, cdiv(n, kRouteTile), kRouteBlock, 0, st, xyz, (long long)n, g, s.table, s.owner,
-                s.tiles);
+    lod::launch(k_route_count, cdiv(n, kRouteTile), kRouteBlock, 0, st, xyz, n, g, s.table, s.owner, s.tiles);
   else
     CK(cudaMemsetAsync(s.tiles, 0, (size_t)world * 4, st));
-  lod::launch(k_route_scan, 1, 1024, 0, st, s.tiles, ntiles, (int)world, (long long *)counts, (long long *)starts);
+  lod::launch(k_route_scan, 1, 1024, 0, st, s.tiles, ntiles, world, counts, starts);
+  return LOD_OK;
+}
+
+bool windows_ok(void *const *w, int world) {
+  if (!w) return false;
+  for (int r = 0; r < world; ++r)
+    if (!w[r]) return false;
+  return true;
+}
+
+PeerWindows pack_windows(void *const *w, int world) {
+  PeerWindows pw{};
+  for (int r = 0; r < world; ++r) pw.p[r] = static_cast<char *>(w[r]);
+  return pw;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lod_route_bucket(int32_t device, const double *bmin, double size, int32_t depth, const int32_t *owner_of_prefix,
+                     int32_t world, const float *xyz, const uint32_t *rgba, int64_t n, void *out_records,
+                     int64_t *counts, int64_t *starts, void *stream) {
+  if (!bmin || !owner_of_prefix || depth < 0 || depth > 8 || world < 1 || world > kRouteMaxWorld || n < 0 ||
+      (n > 0 && (!xyz || !rgba || !out_records)) || !counts || !starts || device < 0 || device >= 64)
+    return LOD_E_ARG;
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaSetDevice(device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  RouteScratch &s = g_rs[device];
+  int rc = route_prepare(s, bmin, size, depth, owner_of_prefix, world, xyz, n, (long long *)counts,
+                         (long long *)starts, st);
+  if (rc) return rc;
   if (n > 0)
-    lod::launch(k_route_scatter, cdiv(n, kRouteTile), kRouteBlock, 0, st, xyz, rgba, (long long)n, (int)world,
-                s.owner, s.tiles, (const long long *)starts, reinterpret_cast<float4 *>(out_records));
+    lod::launch(k_route_scatter<LocalDest>, cdiv(n, kRouteTile), kRouteBlock, 0, st, xyz, rgba, (long long)n,
+                (int)world, s.owner, s.tiles,
+                LocalDest{(const long long *)starts, reinterpret_cast<float4 *>(out_records)});
+  return cuda_rc(cudaGetLastError());
+}
+
+int lod_ipc_alloc(int32_t device, uint64_t bytes, void **ptr, void *handle) {
+  if (!ptr || !handle || device < 0) return LOD_E_ARG;
+  cudaSetDevice(device);
+  if (cudaMalloc(ptr, bytes ? bytes : 1) != cudaSuccess) {
+    cudaGetLastError();
+    return LOD_E_NOMEM;
+  }
+  CK(cudaMemset(*ptr, 0, bytes ? bytes : 1));
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, *ptr));
+  static_assert(sizeof(h) == LOD_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle, &h, sizeof(h));
+  return cuda_rc(cudaDeviceSynchronize());
+}
+
+int lod_ipc_open(int32_t device, const void *handle, void **ptr) {
+  if (!ptr || !handle || device < 0) return LOD_E_ARG;
+  cudaSetDevice(device);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return cuda_rc(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+}
+
+int lod_ipc_close(void *ptr) { return cuda_rc(cudaIpcCloseMemHandle(ptr)); }
+
+int lod_route_peers_begin(int32_t device, const double *bmin, double size, int32_t depth,
+                          const int32_t *owner_of_prefix, int32_t world, int32_t rank, const float *xyz, int64_t n,
+                          void *const *windows, void *stream) {
+  if (!bmin || !owner_of_prefix || depth < 0 || depth > 8 || world < 1 || world > kRouteMaxWorld || rank < 0 ||
+      rank >= world || n < 0 || (n > 0 && !xyz) || !windows_ok(windows, world) || device < 0 || device >= 64)
+    return LOD_E_ARG;
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaSetDevice(device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  RouteScratch &s = g_rs[device];
+  if (!s.counts) {
+    CK(cudaMalloc(&s.counts, 2 * kRouteMaxWorld * sizeof(long long)));
+    s.starts = s.counts + kRouteMaxWorld;
+  }
+  int rc = route_prepare(s, bmin, size, depth, owner_of_prefix, world, xyz, n, s.counts, s.starts, st);
+  if (rc) return rc;
+  lod::launch(k_route_publish, cdiv(world * world, 256), 256, 0, st, (const long long *)s.counts, (int)rank,
+              (int)world, pack_windows(windows, world));
+  return cuda_rc(cudaGetLastError());
+}
+
+int lod_route_peers_finish(int32_t device, int32_t world, int32_t rank, const float *xyz, const uint32_t *rgba,
+                           int64_t n, void *const *windows, int32_t half, int64_t half_records, void *stream) {
+  if (world < 1 || world > kRouteMaxWorld || rank < 0 || rank >= world || n < 0 || (n > 0 && (!xyz || !rgba)) ||
+      !windows_ok(windows, world) || half < 0 || half > 1 || half_records < 0 || device < 0 || device >= 64)
+    return LOD_E_ARG;
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaSetDevice(device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  RouteScratch &s = g_rs[device];
+  if (n > s.cap) return LOD_E_ARG;  // begin() sized the scratch for this stripe
+  if (n > 0)
+    lod::launch(k_route_scatter<PeerDest>, cdiv(n, kRouteTile), kRouteBlock, 0, st, xyz, rgba, (long long)n,
+                (int)world, s.owner, s.tiles,
+                PeerDest{pack_windows(windows, world), (int)rank, (int)world, (int)half, (long long)half_records});
+  return cuda_rc(cudaGetLastError());
+}
+
+int lod_composite_min_peers(int32_t device, int32_t world, int32_t rank, void *const *fbs, int64_t npix,
+                            void *stream) {
+  if (world < 1 || world > kRouteMaxWorld || rank < 0 || rank >= world || npix < 0 || !windows_ok(fbs, world) ||
+      device < 0)
+    return LOD_E_ARG;
+  cudaSetDevice(device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // slice boundaries even, so the 16-byte accesses stay aligned
+  const long long per = ((npix + world - 1) / world + 1) & ~1LL;
+  const long long lo = std::min<long long>(npix, per * rank), hi = std::min<long long>(npix, lo + per);
+  if (hi > lo) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const unsigned grid = std::min<long long>(cdiv(hi - lo, 512), 4LL * sms);
+    lod::launch(k_composite_min, grid, 256, 0, st, pack_windows(fbs, world), (int)world, lo, hi);
+  }
   return cuda_rc(cudaGetLastError());
 }
 

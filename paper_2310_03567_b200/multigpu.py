@@ -10,16 +10,25 @@ One process per GPU (torch.distributed, NCCL).  Protocol per global batch
   every rank unpacks it, so all ranks share the same top and every prefix
   subtree starts from the single-GPU state.
 * **partitioned** -- each rank computes the owner of its stripe's points from
-  their depth-L octant prefix (exact float64 descent rule on the device),
-  buckets them stably by owner, and one ``all_to_all_single`` routes 16-byte
-  records to their owners; receivers concatenate by source rank, which is
-  global order, and insert into their tree.  Below the top, each prefix
+  their depth-L octant prefix (exact float64 descent rule on the device) and
+  buckets them stably by owner; the bucket scatter writes every 16-byte record
+  straight into its owner's receive window over peer memory (``PeerRouter``:
+  CUDA IPC windows, NVLink between GPUs; no send buffer, no NCCL all-to-all)
+  behind the records of the lower source ranks, so each owner's window holds
+  its points in global order, and the owner inserts them into its tree.  Below the top, each prefix
   subtree therefore evolves exactly as in the single-GPU run; top-node cells
   never straddle prefix boundaries (G a multiple of 2^(L-level)), so their
   claims stay rank-local (checked by the GPU tests on the merged trees).
-* **render** -- every rank rasterizes its tree; framebuffers are combined with
-  one ``all_reduce(MIN)`` (the all-ones sentinel is mapped to INT64_MAX for the
-  signed reduction and back).
+* **render** -- every rank rasterizes its tree into its framebuffer window;
+  ``PeerFramebuffers.composite`` min-reduces each rank's pixel slice across
+  all windows and writes it back into every window (reduce-scatter and
+  all-gather fused in one kernel over peer memory).  ``composite_min`` is the
+  same composite as one ``all_reduce(MIN)`` for CPU tensors (gloo tests).
+
+The peer-memory steps are ordered by host barriers (stream sync + barrier of
+the process group) -- two per routed batch, two per composite -- never by
+device-side spin waits, so ranks that share one GPU (the single-GPU test box:
+``LOD_DIST_BACKEND=gloo``) cannot deadlock on each other's kernels.
 """
 from __future__ import annotations
 
@@ -154,6 +163,214 @@ def composite_min(fb_cells_dev, group=None):
     return torch.where(x == INT64_MAX, torch.full_like(x, -1), x)
 
 
+class _DeviceArray:
+    """Zero-copy torch view of raw device memory (``__cuda_array_interface__``)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 2, "strides": None}
+
+
+def _device_view(ptr: int, shape, dtype, device: int):
+    import torch
+
+    typestr = {torch.int32: "<i4", torch.int64: "<i8"}[dtype]
+    return torch.as_tensor(_DeviceArray(ptr, shape, typestr), device=f"cuda:{device}")
+
+
+class PeerWindows:
+    """One IPC-shareable device allocation per rank, mapped by every rank
+    (``lod_ipc_alloc`` / ``lod_ipc_open``: NVLink peer memory between GPUs).
+    ``ptrs[r]`` is rank r's window as seen by this process.  Collective:
+    every rank of the group constructs and closes it together."""
+
+    def __init__(self, device: int, rank: int, world: int, nbytes: int, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        self.device, self.rank, self.world, self.group, self.nbytes = device, rank, world, group, int(nbytes)
+        L = self._L = _lib.load()
+        own = ctypes.c_void_p()
+        h = ctypes.create_string_buffer(_lib.LOD_IPC_HANDLE_BYTES)
+        _lib.check(L.lod_ipc_alloc(device, self.nbytes, ctypes.byref(own), h), "lod_ipc_alloc")
+        self.own = int(own.value)
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(h.raw), group=group)
+        self.ptrs = (ctypes.c_void_p * world)()
+        self._opened = []
+        for r in range(world):
+            if r == rank:
+                self.ptrs[r] = self.own
+                continue
+            p = ctypes.c_void_p()
+            hb = ctypes.create_string_buffer(handles[r], _lib.LOD_IPC_HANDLE_BYTES)
+            _lib.check(L.lod_ipc_open(device, hb, ctypes.byref(p)), "lod_ipc_open")
+            self.ptrs[r] = p.value
+            self._opened.append(int(p.value))
+
+    def close(self) -> None:
+        import torch
+        import torch.distributed as dist
+
+        if self.own is None:
+            return
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)  # nobody writes into a window that is about to go
+        for p in self._opened:
+            _lib.check(self._L.lod_ipc_close(p), "lod_ipc_close")
+        dist.barrier(group=self.group)
+        _lib.check(self._L.lod_device_free(self.own), "lod_device_free")
+        self.own, self._opened = None, []
+
+
+def _sync_barrier(device: int, group) -> None:
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.current_stream(device).synchronize()
+    dist.barrier(group=group)
+
+
+class PeerRouter:
+    """Routing of striped batches to the owners of their octant prefixes over
+    peer memory (``lod_route_peers_begin`` / ``_finish``): the bucket sizes
+    are exchanged through every window's count matrix, then the stable bucket
+    scatter stores each record directly in its owner's window.  Windows hold
+    two halves of ``half_records`` records (batches alternate halves) and grow
+    collectively -- every rank reads the same full count matrix, so all ranks
+    take the same decision."""
+
+    def __init__(self, device: int, rank: int, world: int, plan: partition.Plan, half_records: int = 1 << 20,
+                 group=None, bmin=(0.0, 0.0, 0.0), size: float = 1.0):
+        self.device, self.rank, self.world, self.group, self.plan = device, rank, world, group, plan
+        self.table = np.ascontiguousarray(plan.owner, np.int32)
+        self.bmin, self.size = np.ascontiguousarray(bmin, np.float64), float(size)
+        self.half_records = int(half_records)
+        self.win = PeerWindows(device, rank, world, self._bytes(self.half_records), group)
+        self.k = 0
+        self.matrix = np.zeros((world, world), np.int64)
+
+    @staticmethod
+    def _bytes(half_records: int) -> int:
+        return _lib.LOD_WINDOW_HEADER_BYTES + 2 * 16 * half_records
+
+    def _begin(self, x, n: int, stream: int) -> None:
+        import ctypes
+
+        _lib.check(self.win._L.lod_route_peers_begin(
+            self.device, _lib.ptr(self.bmin), self.size, int(self.plan.depth), _lib.ptr(self.table), self.world,
+            self.rank, _lib.ptr(x), n, self.win.ptrs, ctypes.c_void_p(stream)), "lod_route_peers_begin")
+        _sync_barrier(self.device, self.group)
+        _lib.check(self.win._L.lod_memcpy_d2h(_lib.ptr(self.matrix), self.win.own, self.matrix.nbytes),
+                   "count matrix")
+
+    def route(self, xyz, rgba):
+        """This rank's stripe (CUDA tensors) in; this rank's points of the
+        global batch out, as an (n, 4) int32 view of its window in global order
+        (valid until the batch after next is routed)."""
+        import ctypes
+
+        import torch
+
+        x, c = xyz.contiguous(), rgba.contiguous()
+        n = int(c.shape[0])
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self._begin(x, n, stream)
+        need = int(self.matrix.sum(axis=0).max())
+        if need > self.half_records:  # identical decision on every rank
+            self.win.close()
+            self.half_records = max(need, 2 * self.half_records)
+            self.win = PeerWindows(self.device, self.rank, self.world, self._bytes(self.half_records), self.group)
+            self._begin(x, n, stream)
+        half = self.k & 1
+        _lib.check(self.win._L.lod_route_peers_finish(
+            self.device, self.world, self.rank, _lib.ptr(x), _lib.ptr(c), n, self.win.ptrs, half,
+            self.half_records, ctypes.c_void_p(stream)), "lod_route_peers_finish")
+        _sync_barrier(self.device, self.group)
+        self.k += 1
+        mine = int(self.matrix[:, self.rank].sum())
+        base = self.win.own + _lib.LOD_WINDOW_HEADER_BYTES + half * 16 * self.half_records
+        return _device_view(base, (mine, 4), torch.int32, self.device)
+
+    def close(self) -> None:
+        self.win.close()
+
+
+class PeerFramebuffers:
+    """Per-rank framebuffer windows and the fused depth-min composite
+    (``lod_composite_min_peers``)."""
+
+    def __init__(self, device: int, rank: int, world: int, width: int, height: int, group=None):
+        self.device, self.rank, self.world, self.group = device, rank, world, group
+        self.width, self.height = int(width), int(height)
+        self.npix = self.width * self.height
+        self.win = PeerWindows(device, rank, world, 8 * self.npix, group)
+
+    def render(self, tree, camera, plan: partition.Plan, threshold: float = 128.0) -> int:
+        """Clear this rank's framebuffer and splat its share of the cut into
+        it: the device selection (render.select_visible) restricted to the
+        replicated top and the prefixes this rank owns (its copies of other
+        prefixes are frozen at the hand-off), drawn by ``lod_rasterize`` into
+        the window.  Returns the samples drawn."""
+        import ctypes
+
+        from . import render as R
+
+        L = self.win._L
+        _lib.check(L.lod_fb_fill(self.device, self.win.own, self.npix, int(SENTINEL_U64)), "fb fill")
+        vis = np.asarray(owned_cut(tree, R.select_visible(tree, camera, threshold), plan, self.rank), np.int32)
+        cam = np.ascontiguousarray(camera.packed(), np.float64)
+        drawn = ctypes.c_int64(0)
+        _lib.check(L.lod_rasterize(tree.handle, _lib.ptr(vis), len(vis), _lib.ptr(cam),
+                                   ctypes.c_void_p(self.win.own), self.width, self.height, _lib.LOD_FLAG_DEVICE_FB,
+                                   ctypes.byref(drawn)), "lod_rasterize")
+        return int(drawn.value)
+
+    def composite(self):
+        """Depth-min of all ranks' framebuffers (collective); returns it as a
+        host Framebuffer (every rank's window holds the same composite)."""
+        import ctypes
+
+        import torch
+
+        from .render import Framebuffer
+
+        _sync_barrier(self.device, self.group)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(self.win._L.lod_composite_min_peers(self.device, self.world, self.rank, self.win.ptrs, self.npix,
+                                                       ctypes.c_void_p(stream)), "lod_composite_min_peers")
+        _sync_barrier(self.device, self.group)
+        fb = Framebuffer(self.width, self.height)
+        _lib.check(self.win._L.lod_memcpy_d2h(_lib.ptr(fb.cells), self.win.own, 8 * self.npix), "fb read")
+        return fb
+
+    def close(self) -> None:
+        self.win.close()
+
+
+def owned_cut(tree, selected, plan: partition.Plan, rank: int) -> list[int]:
+    """The nodes of a selection this rank draws: the replicated top (level <
+    plan.depth) and the nodes under the prefixes it owns."""
+    par, octs, lvl = tree.parent, tree.octant, tree.level
+    keep = []
+    for nid in selected:
+        if lvl[nid] < plan.depth:
+            keep.append(nid)
+            continue
+        a = nid
+        while lvl[a] > plan.depth:
+            a = par[a]
+        prefix, k = 0, 1
+        while lvl[a] > 0:  # octants of the depth-`plan.depth` ancestor's path, deepest first
+            prefix += int(octs[a]) * k
+            k *= 8
+            a = par[a]
+        if int(plan.owner[prefix]) == rank:
+            keep.append(nid)
+    return keep
+
+
 class PartitionedInserter:
     """Drives one rank of the warm-up / hand-off / partitioned protocol."""
 
@@ -161,6 +378,7 @@ class PartitionedInserter:
         self.tree, self.state, self.plan = tree, state, plan
         self.rank, self.world, self.group = rank, world, group
         self.partitioned = world == 1
+        self.router = None  # PeerRouter, created at the hand-off
 
     def insert(self, xyz, rgba) -> int:
         """Insert this rank's stripe of one global batch; returns points inserted here."""
@@ -173,7 +391,13 @@ class PartitionedInserter:
             if self.world == 1:
                 insert_batch(self.tree, xyz, rgba, self.state)
                 return int(rgba.shape[0])
-            rec = route(xyz, rgba, self.plan, self.world, self.group)
+            if xyz.is_cuda:
+                if self.router is None:
+                    self.router = PeerRouter(self.tree.device, self.rank, self.world, self.plan,
+                                             half_records=2 * int(rgba.shape[0]), group=self.group)
+                rec = self.router.route(xyz, rgba)
+            else:
+                rec = route(xyz, rgba, self.plan, self.world, self.group)
             insert_records(self.tree, rec, self.state)
             return int(rec.shape[0])
         # warm-up: gather stripes to rank 0 (rank order = global order)
@@ -197,6 +421,12 @@ class PartitionedInserter:
         if int(flag.item()):
             self.hand_off()
         return got
+
+    def close(self) -> None:
+        """Release the peer windows (collective)."""
+        if self.router is not None:
+            self.router.close()
+            self.router = None
 
     def hand_off(self) -> None:
         import torch

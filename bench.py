@@ -395,6 +395,7 @@ def secondary_rows(args, tree, state, dev_b, dev) -> dict:
     * render: ``rasterize`` = device selection + splat (lod_render, device
       framebuffer) at the bench camera of cli.py:325-328 (1024 x 768), and
       ``select_visible`` alone;
+    * frame: config 3's loop, insert + render per frame (public API);
     * delta: insert_batch(collect_delta=True) vs plain on further batches;
     * morton: device Morton sort of 16M resident points (lod_morton_sort).
     """
@@ -432,6 +433,37 @@ def secondary_rows(args, tree, state, dev_b, dev) -> dict:
                      "select_ms": round(t_s * 1e3, 3), "nodes_selected": int(n.value),
                      "samples_drawn": int(drawn.value),
                      "msamples_per_s": round(drawn.value / t_r / 1e6, 1)}
+    # config 3's frame loop: insert one 1M batch + render the bench camera per
+    # frame through the public API (render.rasterize: device selection +
+    # splat, host framebuffer), on a fresh tree over the same stream
+    from paper_2310_03567_b200.render import rasterize
+
+    ftree, fstate = new_tree(dev, int(args.arena_gib * (1 << 30)))
+    for i in range(args.warmup):
+        insert_batch(ftree, *dev_b[i], fstate)
+    rasterize(ftree, cam)
+    torch.cuda.synchronize()
+    fr, rr, pts = [], [], 0
+    for i in range(args.warmup, len(dev_b)):
+        t0 = time.perf_counter()
+        insert_batch(ftree, *dev_b[i], fstate)
+        t1 = time.perf_counter()
+        _, rep = rasterize(ftree, cam)
+        t2 = time.perf_counter()
+        fr.append(t2 - t0)
+        rr.append(t2 - t1)
+        pts += int(dev_b[i][1].numel())
+    ftree.close()
+    fr_s = sorted(fr)
+    out["frame"] = {"note": "per frame: insert_batch (device-resident 1M batch) + rasterize (bench camera, "
+                            "1024x768, threshold 128, host framebuffer); wall clock, the render's sync "
+                            "settles the insert",
+                    "frames": len(fr), "mpts_per_s": round(pts / sum(fr) / 1e6, 1),
+                    "ms_per_frame": {"avg": round(statistics.mean(fr) * 1e3, 3),
+                                     "p50": round(fr_s[len(fr_s) // 2] * 1e3, 3),
+                                     "p99": round(fr_s[min(len(fr_s) - 1, int(0.99 * len(fr_s)))] * 1e3, 3)},
+                    "render_ms_avg": round(statistics.mean(rr) * 1e3, 3),
+                    "samples_drawn_last": int(rep.samples_drawn)}
     # delta capture overhead on further batches
     extra = [synth.gen_surface(BATCH, 9000 + i) for i in range(6)]
     ex = [(torch.from_numpy(x).cuda(), torch.from_numpy(c.view(np.int32)).cuda()) for x, c in extra]

@@ -46,6 +46,8 @@ enum {
     LOD_FLAG_PACKED = 16       /* xyz points at n 16-byte records (f32 x,y,z | u32 rgba);
                                   rgba is ignored (may be NULL)                              */
     , LOD_FLAG_INPUT_STREAM = 32 /* order the device inputs after LodLimits.input_stream      */
+    , LOD_FLAG_FB_CLEAR = 64   /* host framebuffer is all sentinel (a fresh Framebuffer): the
+                                  device target is filled instead of uploaded             */
 };
 
 typedef struct LodTree LodTree;

@@ -31,6 +31,7 @@ LOD_FLAG_PROFILE = 4
 LOD_FLAG_DELTA = 8
 LOD_FLAG_PACKED = 16
 LOD_FLAG_INPUT_STREAM = 32
+LOD_FLAG_FB_CLEAR = 64
 LOD_NPHASE = 10
 LOD_IPC_HANDLE_BYTES = 64
 LOD_WINDOW_HEADER_BYTES = 64 * 64 * 8

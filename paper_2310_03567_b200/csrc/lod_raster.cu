@@ -268,7 +268,10 @@ int lod_rasterize(LodTree *t, const int32_t *vis, int64_t nvis, const double *ca
   if (!(flags & LOD_FLAG_DEVICE_FB)) {
     int rc = lod_tree_ensure_fb(t, npx, &dfb);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(dfb, fb, npx * 8, cudaMemcpyHostToDevice, st));
+    if (flags & LOD_FLAG_FB_CLEAR)  // the host target is all sentinel: fill, do not upload
+      lod::launch(k_fill_u64, grid_for(npx), 256, 0, st, dfb, npx, ~0ull);
+    else
+      CK(cudaMemcpyAsync(dfb, fb, npx * 8, cudaMemcpyHostToDevice, st));
   }
   int32_t *dvis = nullptr;
   int rc = lod_tree_ensure_vislist(t, nvis, &dvis);
@@ -318,7 +321,10 @@ static int render_impl(LodTree *t, const double *planes, const double *cam, doub
   if (fb && !(flags & LOD_FLAG_DEVICE_FB)) {
     rc = lod_tree_ensure_fb(t, npx, &dfb);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(dfb, fb, npx * 8, cudaMemcpyHostToDevice, st));
+    if (flags & LOD_FLAG_FB_CLEAR)  // the host target is all sentinel: fill, do not upload
+      lod::launch(k_fill_u64, grid_for(npx), 256, 0, st, dfb, npx, ~0ull);
+    else
+      CK(cudaMemcpyAsync(dfb, fb, npx * 8, cudaMemcpyHostToDevice, st));
   }
   lod::launch(k_select, 1, kSelBlock, 0, st, lod_tree_nodes(t), lod_tree_geo(t), sp, la, lb, sel, cnt + 1, vf,
               fb ? 1 : 0);
@@ -393,7 +399,10 @@ int lod_raster_points(int32_t device, const float *xyz, const uint32_t *rgba, in
       s.fcap = npx;
     }
     dfb = s.fb;
-    CK(cudaMemcpyAsync(dfb, fb, npx * 8, cudaMemcpyHostToDevice, s.st));
+    if (flags & LOD_FLAG_FB_CLEAR)
+      lod::launch(k_fill_u64, grid_for(npx), 256, 0, s.st, dfb, npx, ~0ull);
+    else
+      CK(cudaMemcpyAsync(dfb, fb, npx * 8, cudaMemcpyHostToDevice, s.st));
   }
   if (n > 0) lod::launch(k_raster_points, grid_for(n), 256, 0, s.st, dx, dc, n, c, dfb, width, height);
   if (!(flags & LOD_FLAG_DEVICE_FB)) CK(cudaMemcpyAsync(fb, dfb, npx * 8, cudaMemcpyDeviceToHost, s.st));

@@ -189,3 +189,42 @@ def test_empty_tree_selects_nothing(gpu):
     assert select_visible(tree, cam) == []
     fb, rep = rasterize(tree, cam)
     assert rep.selected == [] and rep.samples_drawn == 0
+
+
+def test_render_onto_existing_framebuffer_and_pinned_targets(gpu):
+    """A fresh target (pinned, device-filled: LOD_FLAG_FB_CLEAR) and a caller's
+    framebuffer splatted on top of its contents agree: drawing onto existing
+    cells is their depth-min with a fresh render; pooled targets are reused
+    without leaking old contents."""
+    import gc
+
+    from paper_2310_03567_b200 import insert_batch, synth
+    from paper_2310_03567_b200.render import Camera, Framebuffer, brute_force_render, rasterize, rasterize_nodes
+
+    P = dict(bmin=(0.0, 0.0, 0.0), size=1.0, arena_bytes=256 << 20, chunk_capacity=256, grid_res=32,
+             leaf_threshold=2000, max_depth=12, backlog_capacity=10_000_000, spill_capacity=100_000_000)
+    tree, state = make_product(P)
+    for i in range(3):
+        insert_batch(tree, *synth.gen_surface(30_000, 70 + i), state)
+    cam = Camera((0.5, 0.4, -1.5), (0.5, 0.5, 0.5), fov_deg=60.0, near=0.05, far=100.0, width=320, height=240)
+    xa, ca = synth.gen_uniform(20_000, 5)
+    a = brute_force_render(xa, ca, cam).cells.copy()
+    fresh, rep = rasterize(tree, cam, threshold=64.0)
+    want = np.minimum(a, fresh.cells)
+    host = Framebuffer(cam.width, cam.height)
+    host.cells[:] = a
+    got, rep2 = rasterize(tree, cam, threshold=64.0, fb=host)
+    assert got is host and np.array_equal(host.cells, want)
+    assert rep2.samples_drawn == rep.samples_drawn
+    nodes_fb, _ = rasterize_nodes(tree, rep.selected, cam)
+    assert np.array_equal(nodes_fb.cells, fresh.cells)
+    # pooled pinned targets: a recycled buffer starts from the sentinel again
+    ref = fresh.cells.copy()
+    del fresh, nodes_fb
+    gc.collect()
+    for _ in range(3):
+        again, _ = rasterize(tree, cam, threshold=64.0)
+        assert np.array_equal(again.cells, ref)
+    empty = Camera((0.5, 0.5, 3.0), (0.5, 0.5, 10.0), fov_deg=30.0, near=0.05, far=1.0, width=320, height=240)
+    blank, rep3 = rasterize(tree, empty, threshold=64.0)
+    assert rep3.samples_drawn == 0 and bool((blank.cells == np.uint64(0xFFFFFFFFFFFFFFFF)).all())

@@ -220,3 +220,39 @@ def ptr(a) -> ctypes.c_void_p:
     if isinstance(a, int):
         return ctypes.c_void_p(a)
     raise TypeError(f"cannot take a pointer of {type(a)!r}")
+
+
+# -- page-locked host arrays ---------------------------------------------------
+# Results the device writes out wholesale (framebuffers, BatchDelta columns)
+# land in page-locked memory, so the D2H is a DMA at link speed instead of a
+# staged pageable copy.  Buffers come from a per-size-class pool (powers of
+# two) and return to it when the last numpy view of them dies.
+_PINNED_FREE: dict[int, list[int]] = {}
+_PINNED_KEEP = 4
+
+
+def _pinned_release(nbytes: int, addr: int) -> None:
+    free = _PINNED_FREE.setdefault(nbytes, [])
+    if len(free) < _PINNED_KEEP:
+        free.append(addr)
+    else:
+        load().lod_host_free(ctypes.c_void_p(addr))
+
+
+def pinned_empty(n: int, dtype) -> np.ndarray:
+    """An uninitialised page-locked numpy array of n elements."""
+    import weakref
+
+    dt = np.dtype(dtype)
+    need = max(int(n) * dt.itemsize, 1)
+    nbytes = 1 << (need - 1).bit_length()
+    free = _PINNED_FREE.get(nbytes)
+    if free:
+        addr = free.pop()
+    else:
+        p = ctypes.c_void_p()
+        check(load().lod_host_alloc(nbytes, ctypes.byref(p)), "pinned host buffer")
+        addr = int(p.value)
+    buf = (ctypes.c_uint8 * nbytes).from_address(addr)
+    weakref.finalize(buf, _pinned_release, nbytes, addr)
+    return np.frombuffer(buf, dt, count=int(n))

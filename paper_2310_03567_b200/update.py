@@ -299,19 +299,25 @@ def _read_delta(tree: Octree) -> BatchDelta:
     ns, nvg, nv, npg = info.n_splits, info.n_voxel_groups, info.n_voxels, info.n_point_groups
     splits = np.empty(ns, np.int32)
     vnode, vstart, vcount = np.empty(nvg, np.int32), np.empty(nvg, np.int64), np.empty(nvg, np.int64)
-    cells, cols = np.empty(nv, np.uint32), np.empty(nv, np.uint32)
+    cells, cols = _lib.pinned_empty(nv, np.uint32), _lib.pinned_empty(nv, np.uint32)  # the bulk: DMA'd
     pnode, pstart, pcount = np.empty(npg, np.int32), np.empty(npg, np.int64), np.empty(npg, np.int64)
     p = _lib.ptr
     _lib.check(tree._L.lod_read_delta(tree.handle, p(splits), p(vnode), p(vstart), p(vcount), p(cells), p(cols),
                                       p(pnode), p(pstart), p(pcount)), "read_delta")
     d = BatchDelta()
     if ns:
-        children, level = tree.children, tree.level
-        for nid in splits.tolist():
+        # every split appends its 8 children in split order (octree.py:249-261),
+        # so the i-th split's children are n0 + 8 i + o; only the level column
+        # is read back (not the whole node table)
+        n1 = tree.num_nodes
+        n0 = n1 - 8 * ns
+        level = np.empty(n1, np.int32)
+        _lib.check(tree._L.lod_read_nodes(tree.handle, n1, None, None, p(level), *([None] * 10)), "read levels")
+        for i, nid in enumerate(splits.tolist()):
             d.structure.append(("split", nid))
+            lv = int(level[nid]) + 1
             for o in range(8):
-                kid = int(children[nid, o])
-                d.structure.append(("create", kid, nid, o, int(level[kid])))
+                d.structure.append(("create", n0 + 8 * i + o, nid, o, lv))
     d.voxels = [(int(a), cells[s:s + c], cols[s:s + c]) for a, s, c in zip(vnode.tolist(), vstart.tolist(),
                                                                         vcount.tolist())]
     d.points = list(zip(pnode.tolist(), pstart.tolist(), pcount.tolist()))

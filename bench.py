@@ -224,8 +224,10 @@ def run_multi(args, rank, world, local_rank):
             "config": {"workload": CONFIGS[args.config][1] + f"; global batch {world} x 1M striped over ranks",
                        "batch_points": BATCH * world, "tree": PARAMS,
                        "parallelism": f"octant-prefix partition depth {plan.depth} x{world}, "
-                                      f"peer-memory routing (bucket scatter into CUDA IPC windows), "
-                                      f"{backend.upper()} barriers",
+                                      + (f"{backend.upper()} all-to-all routing (peer windows unavailable: "
+                                         f"{ins.no_peers})" if ins.no_peers else
+                                         f"peer-memory routing (bucket scatter into CUDA IPC windows), "
+                                         f"{backend.upper()} barriers"),
                        "imbalance_max_over_mean": round(partition.imbalance(plan), 3),
                        "l2": "inputs larger than L2: distinct 16 MB stripes per step"},
             "e2e": {"value": round(pts / (t_e2e * 1e-3) / 1e6, 2), "unit": "Mpts/s",

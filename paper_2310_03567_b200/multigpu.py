@@ -178,6 +178,11 @@ def _device_view(ptr: int, shape, dtype, device: int):
     return torch.as_tensor(_DeviceArray(ptr, shape, typestr), device=f"cuda:{device}")
 
 
+class PeerUnavailable(RuntimeError):
+    """Some rank cannot map another rank's window (no CUDA IPC / P2P path
+    between the GPUs); raised on every rank together."""
+
+
 class PeerWindows:
     """One IPC-shareable device allocation per rank, mapped by every rank
     (``lod_ipc_alloc`` / ``lod_ipc_open``: NVLink peer memory between GPUs).
@@ -199,15 +204,29 @@ class PeerWindows:
         dist.all_gather_object(handles, bytes(h.raw), group=group)
         self.ptrs = (ctypes.c_void_p * world)()
         self._opened = []
+        err = ""
         for r in range(world):
             if r == rank:
                 self.ptrs[r] = self.own
                 continue
             p = ctypes.c_void_p()
             hb = ctypes.create_string_buffer(handles[r], _lib.LOD_IPC_HANDLE_BYTES)
-            _lib.check(L.lod_ipc_open(device, hb, ctypes.byref(p)), "lod_ipc_open")
+            rc = L.lod_ipc_open(device, hb, ctypes.byref(p))
+            if rc != _lib.LOD_OK:
+                err = f"rank {rank} cannot map rank {r}'s window: {L.lod_strerror(rc).decode()}"
+                break
             self.ptrs[r] = p.value
             self._opened.append(int(p.value))
+        errs = [None] * world
+        dist.all_gather_object(errs, err, group=group)  # every rank takes the same decision
+        bad = [e for e in errs if e]
+        if bad:
+            for q in self._opened:
+                L.lod_ipc_close(ctypes.c_void_p(q))
+            dist.barrier(group=group)
+            L.lod_device_free(ctypes.c_void_p(self.own))
+            self.own, self._opened = None, []
+            raise PeerUnavailable(bad[0])
 
     def close(self) -> None:
         import torch
@@ -378,7 +397,8 @@ class PartitionedInserter:
         self.tree, self.state, self.plan = tree, state, plan
         self.rank, self.world, self.group = rank, world, group
         self.partitioned = world == 1
-        self.router = None  # PeerRouter, created at the hand-off
+        self.router = None  # PeerRouter, created at the first partitioned batch
+        self.no_peers = ""  # why the peer route is unavailable (then: NCCL all-to-all)
 
     def insert(self, xyz, rgba) -> int:
         """Insert this rank's stripe of one global batch; returns points inserted here."""
@@ -391,10 +411,13 @@ class PartitionedInserter:
             if self.world == 1:
                 insert_batch(self.tree, xyz, rgba, self.state)
                 return int(rgba.shape[0])
-            if xyz.is_cuda:
-                if self.router is None:
+            if xyz.is_cuda and self.router is None and not self.no_peers:
+                try:
                     self.router = PeerRouter(self.tree.device, self.rank, self.world, self.plan,
                                              half_records=2 * int(rgba.shape[0]), group=self.group)
+                except PeerUnavailable as e:  # GPUs without a peer path: route with the collective
+                    self.no_peers = str(e)
+            if self.router is not None:
                 rec = self.router.route(xyz, rgba)
             else:
                 rec = route(xyz, rgba, self.plan, self.world, self.group)

@@ -161,3 +161,45 @@ def test_gloo_route_and_composite():
         p.join(timeout=180)
     assert all(p.exitcode == 0 for p in procs)
     assert dict(out) == {0: True, 1: True}
+
+
+def test_owned_cut_keeps_top_and_owned_prefixes():
+    """multigpu.owned_cut on a synthetic node table: a full tree to depth 3
+    (ids in creation order, octant order); a node is kept iff it is above
+    the partition depth or the owner of its depth-L octant prefix is the rank."""
+    from types import SimpleNamespace
+
+    from paper_2310_03567_b200 import multigpu
+
+    parent, octant, level, paths = [-1], [0], [0], [()]
+    frontier = [0]
+    for _ in range(3):
+        nxt = []
+        for nid in frontier:
+            for o in range(8):
+                parent.append(nid)
+                octant.append(o)
+                level.append(level[nid] + 1)
+                paths.append(paths[nid] + (o,))
+                nxt.append(len(parent) - 1)
+        frontier = nxt
+    tree = SimpleNamespace(parent=np.array(parent, np.int32), octant=np.array(octant, np.uint8),
+                           level=np.array(level, np.int32))
+    rng = np.random.default_rng(4)
+    for depth, world in ((1, 2), (2, 4), (2, 8)):
+        plan = partition.Plan(depth=depth, owner=rng.integers(0, world, 8 ** depth).astype(np.int32),
+                              load=np.zeros(world))
+        sel = list(rng.permutation(len(parent)))
+        kept = [set(multigpu.owned_cut(tree, sel, plan, r)) for r in range(world)]
+        for nid in sel:
+            p = paths[nid]
+            if len(p) < depth:
+                assert all(nid in k for k in kept)
+                continue
+            key = 0
+            for o in p[:depth]:
+                key = key * 8 + o
+            owners = [r for r in range(world) if nid in kept[r]]
+            assert owners == [int(plan.owner[key])], (nid, p)
+        # order of the selection is preserved
+        assert multigpu.owned_cut(tree, sel, plan, 0) == [n for n in sel if n in kept[0]]

@@ -346,10 +346,21 @@ def run_frame_updates(tree, batches, state: UpdateState, on_delta=None) -> int:
     The budget is checked between batches, as in the reference.  While batch
     k updates, the H2D copies of batches k+1 and k+2 run on the copy stream
     (pinned host batches), so the queue streams at the update rate or the
-    PCIe rate, whichever is lower."""
+    PCIe rate, whichever is lower.  Staged copies of batches still queued at
+    the end of a frame are kept for the next frame (the tree holds references
+    to those arrays, so they stay alive): if the next call finds the same
+    array objects at the head of the queue, their copies are used, otherwise
+    every staged copy is dropped first.  As with any asynchronous copy, a
+    queued batch must not be modified in place while it is queued."""
     state.clock.restart()
     processed = 0
-    staged = False
+    kept = getattr(tree, "_staged_heads", None)
+    if kept:
+        tree._staged_heads = None
+        if not (len(batches) >= len(kept) and all(batches[i] is kept[i] for i in range(len(kept)))):
+            tree._L.lod_prefetch_drain(tree.handle)
+    staged = bool(kept)
+    ok = False
     try:
         while batches and (processed == 0 or not state.clock.exceeded()):
             xyz, rgba = batches.popleft()
@@ -361,9 +372,13 @@ def run_frame_updates(tree, batches, state: UpdateState, on_delta=None) -> int:
             if on_delta is not None:
                 on_delta(delta)
             processed += 1
+        ok = True
     finally:
-        if staged:  # the caller owns the queued arrays again
-            tree._L.lod_prefetch_drain(tree.handle)
+        if staged:
+            if ok:  # the still-queued batches staged last keep their copies
+                tree._staged_heads = [batches[i] for i in range(min(2, len(batches)))]
+            else:  # an error ends the frame: the caller owns the queued arrays again
+                tree._L.lod_prefetch_drain(tree.handle)
     if processed:
         st = state.stats
         st.frames += 1

@@ -241,3 +241,42 @@ def test_frame_budget_semantics(gpu):
     assert run_frame_updates(tree, q, state) == 15 and state.stats.frames == 6
     ot, _, _ = run_oracle(params, batches)
     assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label="budget")
+
+
+def test_frame_loop_keeps_staged_copies_across_frames(gpu):
+    """One batch per frame (budget 0): the two queued batches staged at the end
+    of a frame are used by the next frames; replacing the queue's head between
+    frames drops the staged copies (the new head's own data is inserted)."""
+    from collections import deque
+
+    import torch
+
+    from paper_2310_03567_b200 import UpdateConfig, UpdateState, run_frame_updates
+
+    params = _params(arena_bytes=1 << 30, grid_res=64, leaf_threshold=3000, max_depth=16, chunk_capacity=500)
+    xyz, rgba = _cloud(360_000, 12, "surface")
+    bs = 30_000
+
+    def pin(x, c):
+        px = torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
+        pc = torch.from_numpy(np.ascontiguousarray(c).view(np.int32)).pin_memory().numpy().view(np.uint32)
+        return px, pc
+
+    batches = [pin(xyz[i:i + bs], rgba[i:i + bs]) for i in range(0, len(rgba), bs)]
+    sub_x, sub_c = _cloud(bs, 99, "uniform")
+    substitute = pin(sub_x, sub_c)
+    tree, _ = make_product(params)
+    state = UpdateState(UpdateConfig(budget_ms=0.0, backlog_capacity=params["backlog_capacity"],
+                                     spill_capacity=params["spill_capacity"]))
+    q = deque(batches)
+    inserted = []
+    frame = 0
+    while q:
+        if frame == 4:  # the staged head is replaced by a different batch of the same size
+            q[0] = substitute
+        inserted.append(q[0])
+        assert run_frame_updates(tree, q, state) == 1
+        frame += 1
+    ot, _, _ = run_oracle(params, [(np.asarray(x), np.asarray(c)) for x, c in inserted])
+    assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label="frames_staged")
+    _hygiene(tree, state)

@@ -13,9 +13,10 @@ from paper_2310_03567_b200 import _lib, insert_batch, synth, update, wait_settle
 from bench import new_tree  # noqa: E402
 
 tree, state = new_tree(0, 8 << 30)
-bs = [synth.gen_surface(1_000_000, 1000 + i) for i in range(40)]
+NW = int(os.environ.get("NW", 30))
+bs = [synth.gen_surface(1_000_000, 1000 + i) for i in range(NW + 10)]
 db = [(torch.from_numpy(x).cuda(), torch.from_numpy(c.view(np.int32)).cuda()) for x, c in bs]
-for i in range(30):
+for i in range(NW):
     insert_batch(tree, *db[i], state)
 wait_settled(tree, state)
 orig = update._read_delta
@@ -34,7 +35,7 @@ def timed_read(t):
 
 
 update._read_delta = timed_read
-for i in range(30, 40):
+for i in range(NW, NW + 10):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     insert_batch(tree, *db[i], state, collect_delta=bool(i % 2))

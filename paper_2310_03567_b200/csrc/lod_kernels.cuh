@@ -66,6 +66,7 @@ struct Ctrl {
   unsigned int d_npg;         // point groups (leaves with new points)
   long long redescend;        // k_decide: points in the splitting nodes (stored + pending) -- the only
                               // points the next count pass re-descends, each claiming at most one cell
+  long long n_wins;           // k_resolve_list: entries of the win list (burst path)
 };
 
 __device__ __forceinline__ void set_error(Ctrl *c, int code) { atomicCAS(&c->error, 0, code); }

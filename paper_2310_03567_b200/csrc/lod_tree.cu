@@ -107,6 +107,7 @@ __global__ void k_cycle_begin(Ctrl *c) { lod::pdl_wait();
   c->n_used = 0;
   c->hash_overflow = 0;
   c->n_v = 0;
+  c->n_wins = 0;
   c->n_keys = 0;
   c->acq_tot = u64x2(0, 0);
 }
@@ -174,6 +175,7 @@ struct LodTree {
   int last_iters = 0;       // expansion iterations of the previous cycle (speculation policy)
   long long spec_hits = 0;  // cycles whose pipeline ran speculatively
   DBuf<uint4> backlog;  // the cycle's new voxels in backlog order: {node, cell, rgba, 0}
+  DBuf<uint4> wins;     // burst path: k_resolve_list's win list {winner, node, cell, rgba}
   // sort / alloc scratch
   DBuf<uint32_t> keys, keys_b, vals_a, vals_b, hist, ghist, nodecnt;
   DBuf<int32_t> seg_node, wl, dense;
@@ -218,6 +220,77 @@ struct LodTree {
   // host copies of counters (authoritative after every call)
   long long num_nodes = 1;
   long long d2h_bytes = 0;  // control-block readbacks since the last reset
+};
+
+// ---------------------------------------------------------------- burst resolve
+// A split wave re-descends tens of millions of spilled points in one cycle
+// (density-skew stream: 20-43M), and as many new voxels are claimed.  The
+// regular resolve then does two random atomics per voxel on per-point win
+// counters far larger than L2 (plus a random backlog write); instead the
+// burst path lists every occupied slot once, {winner, node, cell, rgba},
+// with the winner as a sort key, and orders the list by winner with the
+// stable LSD radix passes -- ascending winner index is exactly the backlog
+// order (a point's wins lie at different nodes, so their mutual order is
+// irrelevant after the node sort).  The last pass writes the backlog.
+constexpr int kResolveItems = 8;  // slots per thread per round: one list reservation per 2048 slots
+__global__ void __launch_bounds__(256)
+    k_resolve_list(NodeCols nd, Hash h, uint32_t *grid32, long long n_s, uint4 *__restrict__ wins,
+                   uint32_t *__restrict__ wkey, int passes, uint32_t *__restrict__ ghist, Ctrl *ctrl,
+                   const int *guard) { lod::pdl_wait();
+  __shared__ uint32_t sh[256 / 32 + 1];
+  __shared__ unsigned long long s_base;
+  __shared__ uint32_t hist[kMaxPasses * kRadixDigits];
+  if (guard && *guard) return;
+  for (int i = threadIdx.x; i < kMaxPasses * kRadixDigits; i += blockDim.x) hist[i] = 0;
+  const long long H = (long long)h.cap;
+  constexpr long long kRound = 256LL * kResolveItems;
+  for (long long r0 = (long long)blockIdx.x * kRound; r0 < H; r0 += (long long)gridDim.x * kRound) {
+    ulonglong2 kv[kResolveItems];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kResolveItems; ++k) {
+      const long long sidx = r0 + k * 256 + threadIdx.x;
+      kv[k] = make_ulonglong2(kEmptyKey, kEmptyHi);
+      if (sidx < H) kv[k] = __ldcg(reinterpret_cast<const ulonglong2 *>(h.slots + sidx));
+      cnt += kv[k].x != kEmptyKey;
+    }
+    uint32_t tot;
+    const uint32_t off = block_exclusive_scan<uint32_t, 256>(cnt, sh, tot);
+    if (tot == 0) continue;  // block-uniform
+    if (threadIdx.x == 0) s_base = atomicAdd(reinterpret_cast<unsigned long long *>(&ctrl->n_wins),
+                                             (unsigned long long)tot);
+    __syncthreads();
+    unsigned long long pos = s_base + off;
+    __syncthreads();  // s_base is rewritten next round
+#pragma unroll
+    for (int k = 0; k < kResolveItems; ++k) {
+      if (kv[k].x == kEmptyKey) continue;
+      const long long sidx = r0 + k * 256 + threadIdx.x;
+      *reinterpret_cast<ulonglong2 *>(h.slots + sidx) = make_ulonglong2(kEmptyKey, kEmptyHi);  // next cycle
+      const int nid = (int)(kv[k].x >> 32);
+      const uint32_t cell = (uint32_t)(kv[k].x & 0xFFFFFFFFu);
+      const uint32_t j = (uint32_t)claim_index((uint32_t)(kv[k].y >> 32), n_s);
+      atomicOr(grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5), 1u << (cell & 31));
+      wins[pos] = make_uint4(j, (uint32_t)nid, cell, (uint32_t)kv[k].y);
+      wkey[pos] = j;
+      ++pos;
+      for (int p = 0; p < passes; ++p) atomicAdd(&hist[p * kRadixDigits + ((j >> (p * kRadixBits)) & 0xFF)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * kRadixDigits; i += blockDim.x)
+    if (hist[i]) atomicAdd(ghist + i, hist[i]);
+}
+
+// The win sort's last pass: the entry at sorted position `pos` becomes
+// backlog entry `pos` {node, cell, rgba}.
+struct WinSink {
+  const uint4 *wins;
+  uint4 *backlog;
+  __device__ __forceinline__ void operator()(uint32_t pos, uint32_t, uint32_t val) const {
+    const uint4 e = wins[val];
+    backlog[pos] = make_uint4(e.y, e.z, e.w, 0u);
+  }
 };
 
 // ---------------------------------------------------------------- helpers
@@ -595,7 +668,7 @@ int lod_tree_destroy(LodTree *t) {
   t->bitmap.release(); t->scnt.release(); t->schk.release();
   t->spill_off.release(); t->chunk_off.release(); t->spill.release(); t->hslots.release(); t->hslots2.release();
   t->hused.release(); t->srank.release(); t->wcount.release(); t->wbase.release();
-  t->backlog.release(); t->keys.release(); t->keys_b.release();
+  t->backlog.release(); t->wins.release(); t->keys.release(); t->keys_b.release();
   t->vals_a.release(); t->vals_b.release(); t->hist.release(); t->ghist.release(); t->nodecnt.release();
   t->dense.release();
   t->seg_node.release(); t->wl.release(); t->seg_start.release();
@@ -770,24 +843,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   bool pipeline_launched = false;
   auto pipeline = [&](const int *guard, long long nv) -> int {
     const long long num_nodes = t->num_nodes;
-    {
-      long long oldw = t->wcount.cap;  // zero when (re)allocated; k_scatter counts every entry back to zero
-      RK(t->wcount.ensure(n_all, st));
-      if (t->wcount.cap > oldw) CK(cudaMemsetAsync(t->wcount.p, 0, (size_t)t->wcount.cap * 4, st));
-    }
-    RK(t->wbase.ensure(n_all, st));
-    RK(ensure_scan_lb<uint32_t>(t->lb32, n_all));
-    if (nv > 0) lod::launch(k_resolve, grid_for((long long)t->hcap), 256, 0, st, t->nd, hs, grid32, n_s, t->wcount.p, guard);
-    mark(1);
-    tp("resolve_launched");
-    RK(t->backlog.ensure(std::max<long long>(nv, 1), st));
-    if (nv > 0) {
-      exclusive_scan_lb<uint32_t>(t->wcount.p, t->wbase.p, n_all, &t->d_ctrl->n_v, t->lb32, st, guard);
-      lod::launch(k_scatter, grid_for((long long)t->hcap), 256, 0, st, hs, n_s, t->wbase.p, t->wcount.p, src,
-                  t->backlog.p, guard);
-    }
-    mark(2);
-    // ---- sort: every new sample by node id, stable (slot order)
+    // sort scratch first: the burst resolve sorts its win list with it
     const long long n_items = n_all + nv;  // exact, or an upper bound (the device count is Ctrl.n_items)
     const int passes = radix_passes((uint32_t)(num_nodes - 1));
     RK(t->keys.ensure(n_items, st));
@@ -803,6 +859,47 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       if (t->ghist.cap > oldg) CK(cudaMemsetAsync(t->ghist.p, 0, (size_t)t->ghist.cap * 4, st));
       if (t->nodecnt.cap > oldn) CK(cudaMemsetAsync(t->nodecnt.p + oldn, 0, (size_t)(t->nodecnt.cap - oldn) * 4, st));
     }
+    RK(t->backlog.ensure(std::max<long long>(nv, 1), st));
+    static const long long winsort_min = getenv("LOD_WINSORT_MIN") ? atoll(getenv("LOD_WINSORT_MIN")) : (4LL << 20);
+    if (nv > 0 && nv >= winsort_min) {  // ---- burst resolve: win list sorted by winner
+      RK(t->wins.ensure(nv, st));
+      const int wpasses = radix_passes((uint32_t)std::max<long long>(n_all - 1, 1));
+      const long long lbw_w = radix_lb_elems(nv);
+      CK(cudaMemsetAsync(t->hist.p, 0, (size_t)lbw_w * 4, st));  // pass 0's look-back words
+      lod::launch(k_resolve_list, grid_for((long long)t->hcap), 256, 0, st, t->nd, hs, grid32, n_s, t->wins.p,
+                  t->keys.p, wpasses, t->ghist.p, t->d_ctrl, guard);
+      mark(1);
+      tp("resolve_launched");
+      RadixScratch rw;
+      rw.keys_b = t->keys_b.p;
+      rw.vals_a = t->vals_a.p;
+      rw.vals_b = t->vals_b.p;
+      rw.ghist = t->ghist.p;
+      rw.lb[0] = t->hist.p;
+      rw.lb[1] = t->hist.p + lbw_w;
+      const WinSink ws{t->wins.p, t->backlog.p};
+      uint32_t *wk = nullptr, *wv = nullptr;
+      stable_multisplit(t->keys.p, nv, wpasses, rw, st, &wk, &wv, nullptr, 0, &ws, &t->d_ctrl->n_wins, guard);
+      CK(cudaMemsetAsync(t->ghist.p, 0, (size_t)kMaxPasses * kRadixDigits * 4, st));  // the node sort's totals
+    } else {
+      {
+        long long oldw = t->wcount.cap;  // zero when (re)allocated; k_scatter counts every entry back to zero
+        RK(t->wcount.ensure(n_all, st));
+        if (t->wcount.cap > oldw) CK(cudaMemsetAsync(t->wcount.p, 0, (size_t)t->wcount.cap * 4, st));
+      }
+      RK(t->wbase.ensure(n_all, st));
+      RK(ensure_scan_lb<uint32_t>(t->lb32, n_all));
+      if (nv > 0) lod::launch(k_resolve, grid_for((long long)t->hcap), 256, 0, st, t->nd, hs, grid32, n_s, t->wcount.p, guard);
+      mark(1);
+      tp("resolve_launched");
+      if (nv > 0) {
+        exclusive_scan_lb<uint32_t>(t->wcount.p, t->wbase.p, n_all, &t->d_ctrl->n_v, t->lb32, st, guard);
+        lod::launch(k_scatter, grid_for((long long)t->hcap), 256, 0, st, hs, n_s, t->wbase.p, t->wcount.p, src,
+                    t->backlog.p, guard);
+      }
+    }
+    mark(2);
+    // ---- sort: every new sample by node id, stable (slot order)
     // allocation scratch (segments, chunk needs, write lists, pool rows)
     const long long Kb = num_nodes + 1;  // bound on touched nodes
     RK(t->seg_node.ensure(Kb, st));

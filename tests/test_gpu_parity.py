@@ -280,3 +280,20 @@ def test_frame_loop_keeps_staged_copies_across_frames(gpu):
     ot, _, _ = run_oracle(params, [(np.asarray(x), np.asarray(c)) for x, c in inserted])
     assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label="frames_staged")
     _hygiene(tree, state)
+
+
+def test_burst_resolve_path_forced_matches_reference(gpu):
+    """The burst resolve (win list ordered by the radix passes, normally from
+    4M new voxels per cycle) forced on every cycle (LOD_WINSORT_MIN=0, read
+    once per process): the reference fixtures and oracle cases still match."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, LOD_WINSORT_MIN="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_parity.py"), "-k", "reference_fixture or test_matches_oracle"],
+                       env=env, capture_output=True, text=True, timeout=900, cwd=os.path.dirname(here))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout

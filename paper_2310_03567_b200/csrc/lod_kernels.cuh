@@ -1,7 +1,7 @@
 // lod_kernels.cuh -- device kernels of one update cycle (insert_batch).
 //
 // Order of a cycle (reference: update.py:1-27, 252-393):
-//   expand   k_count (+ voxel claims, touched list) -> k_decide -> [sync] -> k_exec_chunks/k_exec_nodes (repeat)
+//   expand   k_count (+ voxel claims, pending counts) -> k_decide -> [sync] -> k_exec_chunks/k_exec_nodes (repeat)
 //   resolve  k_resolve (winners set bits, per-point wins) -> k_wcount -> scan -> k_emit
 //   sort     k_keys -> stable_multisplit by node id
 //   alloc    k_seg_* (touched nodes, ascending id) -> scan(need) -> k_alloc_*
@@ -249,7 +249,7 @@ __global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl
 #endif
 __global__ void __launch_bounds__(256, LOD_COUNT_MINB)
     k_count(NodeCols nd, Geo geo, PointSrc src, NodeOf node_of, long long n, int first,
-            const uint32_t *__restrict__ grid32, Hash h, int32_t *__restrict__ touched, Ctrl *ctrl) { lod::pdl_wait();
+            const uint32_t *__restrict__ grid32, Hash h, Ctrl *ctrl) { lod::pdl_wait();
   __shared__ UsedStage stg;
   used_init(stg);
   for (long long j0 = (long long)blockIdx.x * blockDim.x; j0 < n; j0 += gstride()) {
@@ -287,33 +287,32 @@ __global__ void __launch_bounds__(256, LOD_COUNT_MINB)
     unsigned act = __ballot_sync(0xffffffffu, leaf >= 0);
     if (leaf >= 0) {
       unsigned peers = __match_any_sync(act, leaf);
-      if (lane_id() == (unsigned)(__ffs(peers) - 1)) {
-        // the leaf's first count of the cycle appends it to the touched list
-        // (pending 0 -> 1, _kernels.py:59-61; order is irrelevant, k_decide
-        // ranks by id)
-        const unsigned long long old = atomicAdd(&nd.pending[leaf], (unsigned long long)__popc(peers));
-        if (old == 0) touched[atomicAdd(&ctrl->n_touched, 1u)] = leaf;
-      }
+      // fire-and-forget: k_decide_mark finds the touched leaves by their
+      // pending counts (waiting for the old value here stalled the pass)
+      if (lane_id() == (unsigned)(__ffs(peers) - 1)) atomicAdd(&nd.pending[leaf], (unsigned long long)__popc(peers));
     }
   }
   used_flush(h, stg, ctrl);
 }
 
 // _split_pass (update.py:226-249): split iff count + pending > T and
-// level < max_depth, else mark final.  k_decide_mark tests every touched leaf
-// (grid-wide: a large tree touches tens of thousands per batch) and flags the
+// level < max_depth, else mark final.  k_decide_mark tests every leaf touched
+// in this iteration -- a leaf, not final, with pending points (pending 0 -> 1
+// is the reference's touched rule, _kernels.py:59-61; every leaf touched in an
+// earlier iteration is final or split by now) -- over all nodes grid-wide
+// (a large tree touches tens of thousands per batch) and flags the
 // splits in a bitmap over node ids; k_decide (1 CTA) ranks them by ascending
 // node id (popcount prefix over the bitmap words), so child ids
 // num_nodes + 8*rank match the reference's sorted-id split order
 // (octree.py:249-261), and plans the spill segments (ascending id, stored
 // order), free-stack pushes (walk order) and grid offsets, detecting
 // SpillOverflow / OutOfArena in reference order.
-__global__ void k_decide_mark(NodeCols nd, Geo geo, const int32_t *__restrict__ touched, uint32_t *bitmap,
-                              const Ctrl *ctrl) { lod::pdl_wait();
-  const unsigned nt = ctrl->n_touched;
-  for (long long t = gtid(); t < nt; t += gstride()) {
-    const int nid = touched[t];
-    const long long tot = nd.count[nid] + (long long)nd.pending[nid];
+__global__ void k_decide_mark(NodeCols nd, Geo geo, long long num_nodes, uint32_t *bitmap) { lod::pdl_wait();
+  for (long long t = gtid(); t < num_nodes; t += gstride()) {
+    const int nid = (int)t;
+    const unsigned long long pend = nd.pending[nid];
+    if (pend == 0 || nd.inner[nid] || nd.final_[nid]) continue;
+    const long long tot = nd.count[nid] + (long long)pend;
     if (tot > geo.T && nd.level[nid] < geo.max_depth) atomicOr(&bitmap[nid >> 5], 1u << (nid & 31));
     else nd.final_[nid] = 1;
   }

@@ -161,7 +161,7 @@ struct LodTree {
   unsigned *h_seq_dev = nullptr;
   unsigned seq = 0;
   // expansion scratch
-  DBuf<int32_t> touched, split_list, node_b, node_all, xlist;  // xlist: chunks of splitting nodes  // node_b: batch points' node cache; node_all: spilled points'
+  DBuf<int32_t> split_list, node_b, node_all, xlist;  // xlist: chunks of splitting nodes  // node_b: batch points' node cache; node_all: spilled points'
   DBuf<uint32_t> bitmap;  // split flags over node ids (k_decide_mark -> k_decide)
   DBuf<long long> scnt, schk, spill_off, chunk_off;
   DBuf<float4> spill;
@@ -417,7 +417,6 @@ static int ensure_nodes(LodTree *t, long long want, long long live) {
   RK(t->bitmap.ensure(words, st, oldw));
   if (t->bitmap.cap > oldw) CK(cudaMemsetAsync(t->bitmap.p + oldw, 0, (size_t)(t->bitmap.cap - oldw) * 4, st));
   // the split plan of the running iteration survives the growth (k_execute reads it)
-  RK(t->touched.ensure(nc, st));
   RK(t->split_list.ensure(nc, st, t->split_list.cap));
   RK(t->scnt.ensure(nc, st));
   RK(t->schk.ensure(nc, st));
@@ -664,7 +663,7 @@ int lod_tree_destroy(LodTree *t) {
   f(t->d_ctrl);
   if (t->h_ctrl) cudaFreeHost(t->h_ctrl);
   if (t->h_seq) cudaFreeHost(t->h_seq);
-  t->touched.release(); t->xlist.release(); t->split_list.release(); t->node_b.release(); t->node_all.release();
+  t->xlist.release(); t->split_list.release(); t->node_b.release(); t->node_all.release();
   t->bitmap.release(); t->scnt.release(); t->schk.release();
   t->spill_off.release(); t->chunk_off.release(); t->spill.release(); t->hslots.release(); t->hslots2.release();
   t->hused.release(); t->srank.release(); t->wcount.release(); t->wbase.release();
@@ -1006,11 +1005,10 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     ++iters;
     if (prof) cudaEventRecord(t->ev[12], st);
     lod::launch(k_count, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, node_of, n_all, first, grid32, hs,
-                t->touched.p, t->d_ctrl);
+                t->d_ctrl);
     if (first) RK(issue_pending(t));  // queued batches' copies start once this count pass is done
     if (prof) cudaEventRecord(t->ev[13], st);
-    lod::launch(k_decide_mark, grid_for(t->num_nodes), 256, 0, st, t->nd, t->geo, t->touched.p, t->bitmap.p,
-                t->d_ctrl);
+    lod::launch(k_decide_mark, grid_for(t->num_nodes), 256, 0, st, t->nd, t->geo, (long long)t->num_nodes, t->bitmap.p);
     // a speculative pipeline's host-side sizes: nodes as of now (no further
     // split if it runs); new voxels at most the claims so far + one per
     // re-descending point (known after an iteration), else the claim table's

@@ -659,6 +659,13 @@ __device__ __forceinline__ int acq_cid(const PoolCols &pool, const Ctrl *ctrl, l
   return a < ctrl->alloc_F ? pool.free_stack[ctrl->alloc_F - 1 - a] : (int)(ctrl->alloc_A + (a - ctrl->alloc_F));
 }
 
+// What the store needs per touched node, in one 32-byte record indexed by node
+// id (written by k_alloc_nodes): its segment start in the sorted order, its
+// first write-list entry and its stored count before this cycle.
+struct SinkInfo {
+  long long seg_start, wl_start, cnt, pad;
+};
+
 // Per touched node: link the new run after the old tail (Octree.append_chunk,
 // octree.py:328-337) and put the partially filled tail at the head of the
 // node's write list.
@@ -667,8 +674,9 @@ __device__ __forceinline__ int acq_cid(const PoolCols &pool, const Ctrl *ctrl, l
 // is done here too: thread 0 advances the arena / free-stack / pool counters.
 __global__ void k_alloc_nodes(NodeCols nd, PoolCols pool, Geo geo, const int32_t *__restrict__ seg_node,
                               const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
-                              const U64x2 *__restrict__ plan_ex, int32_t *__restrict__ wl, Ctrl *ctrl,
-                              unsigned long long arena_cap, const int *guard) { lod::pdl_wait();
+                              const U64x2 *__restrict__ plan_ex, long long *__restrict__ wlo,
+                              SinkInfo *__restrict__ sinfo, Ctrl *ctrl, unsigned long long arena_cap,
+                              const int *guard) { lod::pdl_wait();
   if (guard && *guard) return;
   if (ctrl->error) return;
   {
@@ -694,8 +702,9 @@ __global__ void k_alloc_nodes(NodeCols nd, PoolCols pool, Geo geo, const int32_t
     const long long need = (long long)plan[d].a;
     const long long A0 = (long long)plan_ex[d].a, W0 = (long long)plan_ex[d].b;
     const int tail = nd.chunk_tail[n];
+    sinfo[n] = SinkInfo{seg_start[d], W0, cnt, 0};
     if (cnt % geo.C) {
-      wl[W0] = tail;
+      wlo[W0] = pool.payload_off[tail];
       const long long ci = cnt / geo.C;  // tail chunk index in the node's list
       const long long rem = cnt + len - ci * geo.C;
       pool.occupied[tail] = (int)(rem < geo.C ? rem : geo.C);
@@ -714,7 +723,7 @@ __global__ void k_alloc_nodes(NodeCols nd, PoolCols pool, Geo geo, const int32_t
 // position and final occupancy, write-list slot.
 __global__ void k_alloc_chunks(NodeCols nd, PoolCols pool, Geo geo, const int32_t *__restrict__ seg_node,
                                const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
-                               const U64x2 *__restrict__ plan_ex, int32_t *__restrict__ wl, const Ctrl *ctrl,
+                               const U64x2 *__restrict__ plan_ex, long long *__restrict__ wlo, const Ctrl *ctrl,
                                const int *guard) { lod::pdl_wait();
   if (guard && *guard) return;
   if (ctrl->error) return;
@@ -735,9 +744,13 @@ __global__ void k_alloc_chunks(NodeCols nd, PoolCols pool, Geo geo, const int32_
     const long long cnt = nd.count[n];
     const long long len = seg_start[d + 1] - seg_start[d];
     const int cid = acq_cid(pool, ctrl, a);
-    if (a >= ctrl->alloc_F)
-      pool.payload_off[cid] =
-          (long long)(ctrl->chunk_base + (unsigned long long)(a - ctrl->alloc_F) * (unsigned long long)geo.C * 16ull);
+    long long poff;
+    if (a >= ctrl->alloc_F) {
+      poff = (long long)(ctrl->chunk_base + (unsigned long long)(a - ctrl->alloc_F) * (unsigned long long)geo.C * 16ull);
+      pool.payload_off[cid] = poff;
+    } else {
+      poff = pool.payload_off[cid];
+    }
     pool.next[cid] = (t + 1 < need) ? acq_cid(pool, ctrl, a + 1) : LOD_NO_CHUNK;
     pool.owner[cid] = n;
     const long long ci = ceil_div(cnt, geo.C) + t;
@@ -745,7 +758,7 @@ __global__ void k_alloc_chunks(NodeCols nd, PoolCols pool, Geo geo, const int32_
     const long long rem = cnt + len - ci * geo.C;
     pool.occupied[cid] = (int)(rem < geo.C ? rem : geo.C);
     const long long partial = (long long)plan[d].b - need;
-    wl[(long long)plan_ex[d].b + partial + t] = cid;
+    wlo[(long long)plan_ex[d].b + partial + t] = poff;  // the store writes by payload offset
   }
 }
 
@@ -761,10 +774,8 @@ struct StoreSink {
   PoolCols pool;
   Geo geo;
   uint8_t *arena;
-  const int32_t *dense;
-  const long long *seg_start;
-  const U64x2 *plan_ex;
-  const int32_t *wl;
+  const SinkInfo *sinfo;
+  const long long *wlo;
   long long n_all;
   PointSrc src;
   const uint4 *backlog;  // new voxels in backlog order: {node, cell, rgba, 0}
@@ -772,12 +783,12 @@ struct StoreSink {
   __device__ __forceinline__ void operator()(uint32_t p, uint32_t key, uint32_t item) const {
     if (ctrl->error) return;
     const int n = (int)key;
-    const long long d = dense[n];
-    const long long rank = (long long)p - seg_start[d];
-    const long long cnt = nd.count[n];
+    const SinkInfo si = sinfo[n];
+    const long long rank = (long long)p - si.seg_start;
+    const long long cnt = si.cnt;
     const long long slot = cnt + rank;
     const long long rel = slot / geo.C - cnt / geo.C;
-    const int cid = wl[(long long)plan_ex[d].b + rel];
+    const long long poff = wlo[si.wl_start + rel];
     const long long off = slot % geo.C;
     const long long i = item;
     float4 rec;
@@ -795,7 +806,7 @@ struct StoreSink {
       const double z = nd.bmin[3 * n + 2] + ((double)cz + 0.5) * step;
       rec = make_float4(__double2float_rn(x), __double2float_rn(y), __double2float_rn(z), __uint_as_float(bl.z));
     }
-    float4 *dst = reinterpret_cast<float4 *>(arena + pool.payload_off[cid]) + off;
+    float4 *dst = reinterpret_cast<float4 *>(arena + poff) + off;
     *dst = rec;
   }
 };

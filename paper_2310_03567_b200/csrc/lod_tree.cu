@@ -178,7 +178,9 @@ struct LodTree {
   DBuf<uint4> wins;     // burst path: k_resolve_list's win list {winner, node, cell, rgba}
   // sort / alloc scratch
   DBuf<uint32_t> keys, keys_b, vals_a, vals_b, hist, ghist, nodecnt;
-  DBuf<int32_t> seg_node, wl, dense;
+  DBuf<int32_t> seg_node, dense;
+  DBuf<long long> wlo;   // write list: payload offsets of every touched node's chunks in slot order
+  DBuf<SinkInfo> sinfo;  // per node id: segment start, write-list start, count (k_alloc_nodes)
   DBuf<long long> seg_start;
   DBuf<U64x2> plan, plan_ex;
   ScanLB lb32, lb64;  // single-pass scan state (u32 win counts; U64x2 segment / need pairs)
@@ -670,7 +672,7 @@ int lod_tree_destroy(LodTree *t) {
   t->backlog.release(); t->wins.release(); t->keys.release(); t->keys_b.release();
   t->vals_a.release(); t->vals_b.release(); t->hist.release(); t->ghist.release(); t->nodecnt.release();
   t->dense.release();
-  t->seg_node.release(); t->wl.release(); t->seg_start.release();
+  t->seg_node.release(); t->wlo.release(); t->sinfo.release(); t->seg_start.release();
   t->plan.release(); t->plan_ex.release(); t->in_xyz.release();
   t->in_rgba.release(); t->in_rec.release(); t->gbuf.release(); t->gnodes.release(); t->goff.release(); t->gstart.release();
   t->visflag.release(); t->vislist.release(); t->fb.release(); t->counter.release();
@@ -908,7 +910,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     RK(t->plan_ex.ensure(Kb, st));
     RK(ensure_scan_lb<U64x2>(t->lb64, Kb));
     const long long acq_bound = n_items / C + Kb + 1;
-    RK(t->wl.ensure(acq_bound + Kb + 1, st));
+    RK(t->wlo.ensure(acq_bound + Kb + 1, st));
+    RK(t->sinfo.ensure(Kb, st));
     const long long alloc0 = t->h_ctrl->allocated_total;
     RK(ensure_chunks(t, alloc0 + acq_bound + 1, alloc0));
     const long long lbw = radix_lb_elems(n_items);
@@ -946,9 +949,9 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
                 t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->d_ctrl, t->ghist.p, guard);
     exclusive_scan_lb<U64x2>(t->plan.p, t->plan_ex.p, Kb, &t->d_ctrl->acq_tot, t->lb64, st, guard);
     lod::launch(k_alloc_nodes, grid_for(Kb), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p,
-                t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl, t->arena_cap, guard);
+                t->plan.p, t->plan_ex.p, t->wlo.p, t->sinfo.p, t->d_ctrl, t->arena_cap, guard);
     lod::launch(k_alloc_chunks, grid_for(acq_bound), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p,
-                t->seg_start.p, t->plan.p, t->plan_ex.p, t->wl.p, t->d_ctrl, guard);
+                t->seg_start.p, t->plan.p, t->plan_ex.p, t->wlo.p, t->d_ctrl, guard);
     if (early) mid_seq = publish_ctrl(t);
     mark(3);
     tp("alloc_launched");
@@ -960,8 +963,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     rs.ghist = t->ghist.p;
     rs.lb[0] = t->hist.p;
     rs.lb[1] = t->hist.p + lbw;
-    const StoreSink sink{t->nd,   t->pool, t->geo, t->arena,   t->dense.p, t->seg_start.p, t->plan_ex.p,
-                         t->wl.p, n_all,   src,    t->backlog.p, t->d_ctrl};
+    const StoreSink sink{t->nd, t->pool, t->geo, t->arena, t->sinfo.p, t->wlo.p, n_all, src, t->backlog.p, t->d_ctrl};
     uint32_t *skeys = nullptr, *svals = nullptr;
     if (delta) {  // the delta reads the sorted order: materialise it, then store
       stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals, nullptr, 0, (const KVSink *)nullptr,

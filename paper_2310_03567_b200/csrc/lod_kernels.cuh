@@ -94,7 +94,16 @@ struct Hash {
   unsigned long long cap;    // slots (any size: the hash is range-reduced by a multiply-high)
   unsigned long long *used;  // slots inserted this cycle
   unsigned long long limit;  // capacity of `used` (= table capacity)
+  unsigned long long tag;    // this cycle's epoch << 56 (0..254)
 };
+
+// Keys carry the cycle's epoch in their top byte ({epoch:8, node:24, cell:32});
+// a slot is occupied iff its epoch is the current one.  Slots of earlier
+// cycles are simply stale -- nothing clears the table between cycles (the
+// clearing writes dirtied ~1.5M random sectors per batch that the next count
+// pass had to write back); it is reset with a memset when the epoch wraps.
+constexpr int kEpochs = 255;  // epoch 255 = the all-ones memset state, never live
+__device__ __forceinline__ bool live(const Hash &h, unsigned long long k) { return (k >> 56) == (h.tag >> 56); }
 
 // New keys are appended to the cycle's used-slot list through a per-warp
 // shared-memory stage, so a pass issues one global atomic per warp instead of
@@ -189,6 +198,7 @@ __device__ __forceinline__ void hash_claim(const Hash &h, UsedStage &stg, unsign
 #ifdef LOD_EXP_COUNT  // instrumentation experiment: claims and probes into Ctrl.alloc_F / alloc_A
   atomicAdd((unsigned long long *)&ctrl->alloc_F, 1ull);
 #endif
+  key |= h.tag;
   unsigned long long slot = home_slot(h, key);
   for (unsigned long long probe = 0; probe < h.cap; ++probe) {
 #ifdef LOD_EXP_COUNT
@@ -197,12 +207,13 @@ __device__ __forceinline__ void hash_claim(const Hash &h, UsedStage &stg, unsign
     HSlot *sl = h.slots + slot;
     const unsigned long long mine = ((unsigned long long)v << 32) | rgba;
     ulonglong2 cur = __ldcg(reinterpret_cast<const ulonglong2 *>(sl));
-    if (cur.x == kEmptyKey) {
-      cur = cas_slot(sl, make_ulonglong2(kEmptyKey, kEmptyHi), make_ulonglong2(key, mine));
-      if (cur.x == kEmptyKey) {
+    while (!live(h, cur.x)) {  // empty or stale: install over exactly what was read
+      const ulonglong2 old = cas_slot(sl, cur, make_ulonglong2(key, mine));
+      if (old.x == cur.x && old.y == cur.y) {
         used_append(h, stg, slot, ctrl);
         return;
       }
+      cur = old;
     }
     if (cur.x == key) {
       if ((uint32_t)(cur.y >> 32) > v) atomicMin(&sl->claim, mine);
@@ -581,8 +592,8 @@ __global__ void __launch_bounds__(256)
   const long long H = (long long)h.cap;
   for (long long sidx = gtid(); sidx < H; sidx += gstride()) {
     const ulonglong2 kv = __ldcg(reinterpret_cast<const ulonglong2 *>(h.slots + sidx));
-    if (kv.x == kEmptyKey) continue;
-    const int nid = (int)(kv.x >> 32);
+    if (!live(h, kv.x)) continue;
+    const int nid = (int)((kv.x >> 32) & 0xFFFFFFu);
     const uint32_t cell = (uint32_t)(kv.x & 0xFFFFFFFFu);
     atomicOr(grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5), 1u << (cell & 31));
     atomicAdd(wcount + claim_index((uint32_t)(kv.y >> 32), n_s), 1u);
@@ -598,11 +609,10 @@ __global__ void __launch_bounds__(256)
   for (long long sidx = gtid(); sidx < H; sidx += gstride()) {
     HSlot *sl = h.slots + sidx;
     const ulonglong2 kv = __ldcg(reinterpret_cast<const ulonglong2 *>(sl));
-    if (kv.x == kEmptyKey) continue;
-    *reinterpret_cast<ulonglong2 *>(sl) = make_ulonglong2(kEmptyKey, kEmptyHi);
+    if (!live(h, kv.x)) continue;  // left in place: stale from the next cycle on
     const long long j = claim_index((uint32_t)(kv.y >> 32), n_s);
     const uint32_t b = __ldg(wbase + j) + atomicSub(wcount + j, 1u) - 1u;
-    backlog[b] = make_uint4((uint32_t)(kv.x >> 32), (uint32_t)(kv.x & 0xFFFFFFFFu), (uint32_t)kv.y, 0u);
+    backlog[b] = make_uint4((uint32_t)((kv.x >> 32) & 0xFFFFFFu), (uint32_t)(kv.x & 0xFFFFFFFFu), (uint32_t)kv.y, 0u);
   }
 }
 

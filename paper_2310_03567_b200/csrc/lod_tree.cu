@@ -167,6 +167,7 @@ struct LodTree {
   DBuf<float4> spill;
   // sampling scratch
   DBuf<int32_t> srank;  // split rank per node (-1 when not splitting)
+  int hepoch = 0;                // claim-key epoch of the running cycle (Hash.tag)
   DBuf<HSlot> hslots, hslots2;  // claim table (`hcap` slots in use) + growth spare
   DBuf<unsigned long long> hused;
   DBuf<uint32_t> wcount, wbase;  // per-point win counts (zero between cycles) / their exclusive scan
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(256)
       const long long sidx = r0 + k * 256 + threadIdx.x;
       kv[k] = make_ulonglong2(kEmptyKey, kEmptyHi);
       if (sidx < H) kv[k] = __ldcg(reinterpret_cast<const ulonglong2 *>(h.slots + sidx));
-      cnt += kv[k].x != kEmptyKey;
+      cnt += live(h, kv[k].x);
     }
     uint32_t tot;
     const uint32_t off = block_exclusive_scan<uint32_t, 256>(cnt, sh, tot);
@@ -266,10 +267,8 @@ __global__ void __launch_bounds__(256)
     __syncthreads();  // s_base is rewritten next round
 #pragma unroll
     for (int k = 0; k < kResolveItems; ++k) {
-      if (kv[k].x == kEmptyKey) continue;
-      const long long sidx = r0 + k * 256 + threadIdx.x;
-      *reinterpret_cast<ulonglong2 *>(h.slots + sidx) = make_ulonglong2(kEmptyKey, kEmptyHi);  // next cycle
-      const int nid = (int)(kv[k].x >> 32);
+      if (!live(h, kv[k].x)) continue;  // stale from the next cycle on: no clearing write
+      const int nid = (int)((kv[k].x >> 32) & 0xFFFFFFu);
       const uint32_t cell = (uint32_t)(kv[k].x & 0xFFFFFFFFu);
       const uint32_t j = (uint32_t)claim_index((uint32_t)(kv[k].y >> 32), n_s);
       atomicOr(grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5), 1u << (cell & 31));
@@ -395,6 +394,7 @@ static int grow_col(T *&ptr, long long old_cap, long long new_cap, long long kee
 // Node table capacity (Octree._grow doubling, octree.py:192-209).
 static int ensure_nodes(LodTree *t, long long want, long long live) {
   if (want <= t->ncap) return LOD_OK;
+  if (want > (1LL << 24)) return LOD_E_NOMEM;  // claim keys hold 24-bit node ids
   long long nc = std::max<long long>(t->ncap, 1024);
   while (nc < want) nc *= 2;
   if (lod_debug()) fprintf(stderr, "[lod] grow node table %lld -> %lld\n", t->ncap, nc);
@@ -833,7 +833,12 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     t->hcap = H;
     RK(t->hused.ensure((long long)H, st));
   }
-  Hash hs{t->hslots.p, t->hcap, t->hused.p, t->hcap};
+  // this cycle's epoch; the table is reset when the epochs wrap
+  t->hepoch = (t->hepoch + 1) % kEpochs;
+  if (t->hepoch == 0 && t->hslots.p)
+    CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
+  const unsigned long long htag = (unsigned long long)t->hepoch << 56;
+  Hash hs{t->hslots.p, t->hcap, t->hused.p, t->hcap, htag};
   uint32_t *grid32 = reinterpret_cast<uint32_t *>(t->arena);
   // ---- post-expansion pipeline: resolve -> backlog -> alloc -> sort+store ->
   // [delta] -> epilogue.  Launched either after the expansion settled (guard
@@ -1083,7 +1088,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       RK(t->hslots2.ensure((long long)H, st));
       CK(cudaMemsetAsync(t->hslots2.p, 0xFF, (size_t)t->hslots2.cap * sizeof(HSlot), st));
       RK(t->hused.ensure((long long)H, st, (long long)h.n_used));
-      Hash nh{t->hslots2.p, H, t->hused.p, H};
+      Hash nh{t->hslots2.p, H, t->hused.p, H, htag};
       lod::launch(k_rehash, grid_for(std::max<long long>((long long)h.n_used, 1)), 256, 0, st, t->hslots.p, nh, t->d_ctrl);
       // the old table goes back to empty for later cycles
       CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
@@ -1118,7 +1123,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
       t->hcap = H;
       RK(t->hused.ensure(bound + 1, st));
-      hs = Hash{t->hslots.p, t->hcap, t->hused.p, (unsigned long long)bound + 1};
+      hs = Hash{t->hslots.p, t->hcap, t->hused.p, (unsigned long long)bound + 1, htag};
       CK(cudaMemsetAsync(&t->d_ctrl->n_used, 0, 8, st));
       CK(cudaMemsetAsync(&t->d_ctrl->hash_overflow, 0, 4, st));
       lod::launch(k_claim, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, grid32, n_all, hs, t->d_ctrl);

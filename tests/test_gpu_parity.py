@@ -297,3 +297,18 @@ def test_burst_resolve_path_forced_matches_reference(gpu):
                        env=env, capture_output=True, text=True, timeout=900, cwd=os.path.dirname(here))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+def test_claim_epoch_wraparound_matches_oracle(gpu):
+    """600 small batches: the claim table's key epochs (255 per cycle of
+    resets, stale slots never cleared) wrap twice; per-batch stats and the
+    final state still match the oracle."""
+    from paper_2310_03567_b200 import synth
+
+    params = _params(arena_bytes=1 << 30, grid_res=32, leaf_threshold=600, max_depth=14, chunk_capacity=128)
+    batches = [synth.gen_surface(1500, 5000 + i) for i in range(600)]
+    ot, _, oper = run_oracle(params, batches)
+    tree, state, err, per = run_product(params, batches)
+    assert err == ""
+    assert per == oper
+    assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label="epoch_wrap")

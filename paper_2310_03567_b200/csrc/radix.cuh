@@ -45,7 +45,7 @@ constexpr uint32_t kLbAgg = 1u << 30, kLbPre = 2u << 30, kLbMask = (1u << 30) - 
 
 // Items: points j in [0, n_all) keyed by their leaf, then backlog entries keyed
 // by their node.  Writes the key array and the per-node item counts (= each
-// node's new samples this cycle; hot leaves are aggregated per warp first).
+// node's new samples this cycle; per-CTA shared-memory counters when they fit).
 // 4 items per thread per round (independent loads in flight), 4 CTAs per SM.
 constexpr int kPrepItems = 4;
 constexpr int kPrepBlocksPerSM = 4;
@@ -80,13 +80,15 @@ static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
       const long long i = i0 + q * kRadixBlock + threadIdx.x;
       const bool ok = i < n;
       if (ok) keys[i] = key[q];
+      if (smem_nodes) {  // shared-memory counters: the atomic units resolve same-node lanes
+        // (per-warp MATCH.ANY aggregation first was 1.7 % slower end to end)
+        if (ok) atomicAdd(&nc2[key[q] >> 1], 1u << (16 * (key[q] & 1)));
+        continue;
+      }
       const unsigned act = __ballot_sync(0xffffffffu, ok);
-      if (ok) {
+      if (ok) {  // global counters: hot nodes are aggregated per warp first
         const unsigned peers = __match_any_sync(act, key[q]);
-        if (lane_id() == (unsigned)(__ffs(peers) - 1)) {
-          if (smem_nodes) atomicAdd(&nc2[key[q] >> 1], (uint32_t)__popc(peers) << (16 * (key[q] & 1)));
-          else atomicAdd(&nodecnt[key[q]], (uint32_t)__popc(peers));
-        }
+        if (lane_id() == (unsigned)(__ffs(peers) - 1)) atomicAdd(&nodecnt[key[q]], (uint32_t)__popc(peers));
       }
     }
   }

@@ -55,6 +55,7 @@ struct Ctrl {
   unsigned int pad1;
   U64x2 seg_tot;              // (touched nodes, items)
   U64x2 acq_tot;              // (sum need, sum write-list entries)
+  U64x2 pack_tot;             // the packed node-plan scan's total (k_radix_ghist layout)
   long long alloc_F;          // free stack size before allocation
   long long alloc_A;          // allocated_total before allocation
   unsigned long long chunk_base;
@@ -630,33 +631,56 @@ __device__ __forceinline__ long long ceil_div(long long a, long long b) { return
 // dense id, segment start and chunk need = ceil((count+pending)/C) -
 // chunk_count -- in ascending node id (chunk ids are not observable; the
 // acquisition count and the arena growth are the reference's).
+// Packed per-node plan (written by k_radix_ghist, scanned once): .a = touched
+// flag << 40 | item count, .b = need << 32 | write-list entries (need +
+// partial tail).  Exclusive sums stay inside their fields (< 2^24 nodes,
+// < 2^40 items, < 2^32 acquisitions per cycle), so one scan yields every
+// touched node's dense id, segment start, acquisition start and write-list
+// start.
+constexpr int kPackShift = 40;
+constexpr unsigned long long kPackLow = (1ull << kPackShift) - 1;
+__device__ __forceinline__ U64x2 node_plan(const NodeCols &nd, const Geo &geo, long long n, uint32_t len) {
+  if (!len) return u64x2(0, 0);
+  const long long cnt = nd.count[n];
+  const long long need = ceil_div(cnt + len, geo.C) - ceil_div(cnt, geo.C);
+  const long long partial = (cnt % geo.C) != 0;
+  return u64x2((1ull << kPackShift) | (unsigned long long)len,
+               ((unsigned long long)need << 32) | (unsigned long long)(need + partial));
+}
+
+struct NodePlanOf {
+  NodeCols nd;
+  Geo geo;
+  __device__ __forceinline__ U64x2 operator()(long long n, uint32_t len) const { return node_plan(nd, geo, n, len); }
+};
+
 __global__ void k_seg_list(NodeCols nd, Geo geo, uint32_t *__restrict__ nodecnt, long long num_nodes,
                            const U64x2 *__restrict__ pairs_ex, int32_t *__restrict__ seg_node,
                            long long *__restrict__ seg_start, int32_t *__restrict__ dense, U64x2 *__restrict__ plan,
-                           Ctrl *ctrl, uint32_t *__restrict__ ghist, const int *guard) { lod::pdl_wait();
+                           U64x2 *__restrict__ plan_ex, Ctrl *ctrl, const int *guard) { lod::pdl_wait();
   if (guard && *guard) return;
-  const long long K = (long long)ctrl->seg_tot.a;
   // this kernel is the last reader of the node counts: leave them zeroed for
-  // the next cycle; zero the plan tail the scan reads past K
-  (void)ghist;
-  for (long long i = K + gtid(); i <= num_nodes; i += gstride()) plan[i] = u64x2(0, 0);
+  // the next cycle
   for (long long i = gtid(); i < num_nodes; i += gstride()) {
-    const long long len = nodecnt[i];
+    const uint32_t len = nodecnt[i];
     if (!len) continue;
     nodecnt[i] = 0;
-    const long long d = (long long)pairs_ex[i].a;
+    const U64x2 ex = pairs_ex[i];
+    const long long d = (long long)(ex.a >> kPackShift);
     seg_node[d] = (int32_t)i;
-    seg_start[d] = (long long)pairs_ex[i].b;
+    seg_start[d] = (long long)(ex.a & kPackLow);
     dense[i] = (int32_t)d;
-    const long long cnt = nd.count[i];
-    const long long need = ceil_div(cnt + len, geo.C) - ceil_div(cnt, geo.C);
-    const long long partial = (cnt % geo.C) != 0;
-    plan[d] = u64x2((unsigned long long)need, (unsigned long long)(need + partial));
+    const U64x2 own = node_plan(nd, geo, i, len);
+    plan[d] = u64x2(own.b >> 32, own.b & 0xFFFFFFFFull);
+    plan_ex[d] = u64x2(ex.b >> 32, ex.b & 0xFFFFFFFFull);
   }
   if (gtid() == 0) {
-    const U64x2 tot = ctrl->seg_tot;
-    seg_start[tot.a] = (long long)tot.b;
-    ctrl->n_keys = (unsigned)tot.a;
+    const U64x2 tot = ctrl->pack_tot;
+    const unsigned long long K = tot.a >> kPackShift;
+    ctrl->seg_tot = u64x2(K, tot.a & kPackLow);
+    ctrl->acq_tot = u64x2(tot.b >> 32, tot.b & 0xFFFFFFFFull);
+    seg_start[K] = (long long)(tot.a & kPackLow);
+    ctrl->n_keys = (unsigned)K;
     // acquisition snapshot (ChunkPool.acquire, store.py:110-123): the free
     // stack pops first, then fresh payloads are cut 16-aligned from the arena
     ctrl->alloc_F = ctrl->free_count;

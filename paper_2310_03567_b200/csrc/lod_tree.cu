@@ -180,6 +180,7 @@ struct LodTree {
   // sort / alloc scratch
   DBuf<uint32_t> keys, keys_b, vals_a, vals_b, hist, ghist, nodecnt;
   DBuf<int32_t> seg_node, dense;
+  DBuf<U64x2> pairs;     // packed per-node plans, scanned in place (k_radix_ghist -> k_seg_list)
   DBuf<long long> wlo;   // write list: payload offsets of every touched node's chunks in slot order
   DBuf<SinkInfo> sinfo;  // per node id: segment start, write-list start, count (k_alloc_nodes)
   DBuf<long long> seg_start;
@@ -672,7 +673,7 @@ int lod_tree_destroy(LodTree *t) {
   t->backlog.release(); t->wins.release(); t->keys.release(); t->keys_b.release();
   t->vals_a.release(); t->vals_b.release(); t->hist.release(); t->ghist.release(); t->nodecnt.release();
   t->dense.release();
-  t->seg_node.release(); t->wlo.release(); t->sinfo.release(); t->seg_start.release();
+  t->seg_node.release(); t->pairs.release(); t->wlo.release(); t->sinfo.release(); t->seg_start.release();
   t->plan.release(); t->plan_ex.release(); t->in_xyz.release();
   t->in_rgba.release(); t->in_rec.release(); t->gbuf.release(); t->gnodes.release(); t->goff.release(); t->gstart.release();
   t->visflag.release(); t->vislist.release(); t->fb.release(); t->counter.release();
@@ -944,15 +945,17 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       lod::launch(k_radix_prep, grid, kRadixBlock, (size_t)nc_words * 4, st, node_of, n_all, t->backlog.p, nc_words,
                   t->keys.p, t->nodecnt.p, t->hist.p, lbw, &t->d_ctrl->n_used, n_items_dev, guard);
     }
-    lod::launch(k_radix_ghist, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p, num_nodes,
-                passes, t->ghist.p, t->plan_ex.p, guard);
+    RK(t->pairs.ensure(Kb, st));
+    lod::launch(k_radix_ghist<NodePlanOf>, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p,
+                num_nodes, passes, t->ghist.p, t->pairs.p, NodePlanOf{t->nd, t->geo}, guard);
     // ---- allocation (update.py:317-331): touched nodes = nodes with new samples, ascending id.
     // It needs only the per-node counts, so it runs before the sort, whose last
     // pass then writes every record straight into its chunk slot.
-    exclusive_scan_lb<U64x2>(t->plan_ex.p, t->plan_ex.p, num_nodes, &t->d_ctrl->seg_tot, t->lb64, st, guard);
-    lod::launch(k_seg_list, grid_for(num_nodes), 256, 0, st, t->nd, t->geo, t->nodecnt.p, num_nodes, t->plan_ex.p,
-                t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->d_ctrl, t->ghist.p, guard);
-    exclusive_scan_lb<U64x2>(t->plan.p, t->plan_ex.p, Kb, &t->d_ctrl->acq_tot, t->lb64, st, guard);
+    // one scan of the packed node plans: dense ids, segment starts, acquisition
+    // and write-list starts (k_seg_list unpacks them per touched node)
+    exclusive_scan_lb<U64x2>(t->pairs.p, t->pairs.p, num_nodes, &t->d_ctrl->pack_tot, t->lb64, st, guard);
+    lod::launch(k_seg_list, grid_for(num_nodes), 256, 0, st, t->nd, t->geo, t->nodecnt.p, num_nodes, t->pairs.p,
+                t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->plan_ex.p, t->d_ctrl, guard);
     lod::launch(k_alloc_nodes, grid_for(Kb), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p,
                 t->plan.p, t->plan_ex.p, t->wlo.p, t->sinfo.p, t->d_ctrl, t->arena_cap, guard);
     lod::launch(k_alloc_chunks, grid_for(acq_bound), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p,

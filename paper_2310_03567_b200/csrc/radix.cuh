@@ -101,16 +101,18 @@ static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
 }
 
 // Digit totals of every pass from the per-node counts (keys are node ids).
-// Also writes each node's (touched flag, count) pair for the segment scan.
+// Also writes each node's plan record for the segment scan (plan_of(n, count)).
+template <class PlanOf>
 static __global__ void k_radix_ghist(const uint32_t *__restrict__ nodecnt, long long num_nodes, int passes,
-                              uint32_t *__restrict__ ghist, U64x2 *__restrict__ pairs, const int *guard) { lod::pdl_wait();
+                              uint32_t *__restrict__ ghist, U64x2 *__restrict__ pairs, PlanOf plan_of,
+                              const int *guard) { lod::pdl_wait();
   if (guard && *guard) return;
   __shared__ uint32_t h[kMaxPasses * kRadixDigits];
   for (int i = threadIdx.x; i < kMaxPasses * kRadixDigits; i += blockDim.x) h[i] = 0;
   __syncthreads();
   for (long long n = gtid(); n < num_nodes; n += gstride()) {
     const uint32_t c = nodecnt[n];
-    pairs[n] = u64x2(c ? 1ull : 0ull, (unsigned long long)c);
+    pairs[n] = plan_of(n, c);
     if (c)
       for (int p = 0; p < passes; ++p) atomicAdd(&h[p * kRadixDigits + ((n >> (p * kRadixBits)) & 0xFF)], c);
   }

@@ -694,7 +694,7 @@ __device__ __forceinline__ int acq_cid(const PoolCols &pool, const Ctrl *ctrl, l
 }
 
 // What the store needs per touched node, in one 32-byte record indexed by node
-// id (written by k_alloc_nodes): its segment start in the sorted order, its
+// id (written by k_alloc's node pass): its segment start in the sorted order, its
 // first write-list entry and its stored count before this cycle.
 struct SinkInfo {
   long long seg_start, wl_start, cnt, pad;
@@ -706,13 +706,13 @@ struct SinkInfo {
 // The bulk acquisition's bookkeeping (every thread derives the same fresh
 // count; OutOfArena at the first fresh payload past capacity, store.py:60-69)
 // is done here too: thread 0 advances the arena / free-stack / pool counters.
-__global__ void k_alloc_nodes(NodeCols nd, PoolCols pool, Geo geo, const int32_t *__restrict__ seg_node,
-                              const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
-                              const U64x2 *__restrict__ plan_ex, long long *__restrict__ wlo,
-                              SinkInfo *__restrict__ sinfo, Ctrl *ctrl, unsigned long long arena_cap,
-                              const int *guard) { lod::pdl_wait();
-  if (guard && *guard) return;
-  if (ctrl->error) return;
+__device__ __forceinline__ bool alloc_nodes_body(NodeCols nd, PoolCols pool, Geo geo,
+                                                 const int32_t *__restrict__ seg_node,
+                                                 const long long *__restrict__ seg_start,
+                                                 const U64x2 *__restrict__ plan, const U64x2 *__restrict__ plan_ex,
+                                                 long long *__restrict__ wlo, SinkInfo *__restrict__ sinfo,
+                                                 Ctrl *ctrl, unsigned long long arena_cap) {
+  if (ctrl->error) return false;
   {
     const long long M = (long long)ctrl->acq_tot.a;
     const long long F = ctrl->alloc_F, A = ctrl->alloc_A;
@@ -720,7 +720,7 @@ __global__ void k_alloc_nodes(NodeCols nd, PoolCols pool, Geo geo, const int32_t
     const unsigned long long end = ctrl->chunk_base + (unsigned long long)fresh * (unsigned long long)geo.C * 16ull;
     if (fresh > 0 && end > arena_cap) {
       if (gtid() == 0) set_error(ctrl, 1 /*LOD_E_OUT_OF_ARENA*/);
-      return;
+      return false;
     }
     if (gtid() == 0) {
       if (fresh > 0) ctrl->arena_off = end;
@@ -751,16 +751,16 @@ __global__ void k_alloc_nodes(NodeCols nd, PoolCols pool, Geo geo, const int32_t
       nd.chunk_count[n] += (int)need;
     }
   }
+  return true;
 }
 
 // Per acquisition: payload offset for fresh chunks, in-run links, owner,
 // position and final occupancy, write-list slot.
-__global__ void k_alloc_chunks(NodeCols nd, PoolCols pool, Geo geo, const int32_t *__restrict__ seg_node,
-                               const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
-                               const U64x2 *__restrict__ plan_ex, long long *__restrict__ wlo, const Ctrl *ctrl,
-                               const int *guard) { lod::pdl_wait();
-  if (guard && *guard) return;
-  if (ctrl->error) return;
+__device__ __forceinline__ void alloc_chunks_body(NodeCols nd, PoolCols pool, Geo geo,
+                                                  const int32_t *__restrict__ seg_node,
+                                                  const long long *__restrict__ seg_start,
+                                                  const U64x2 *__restrict__ plan, const U64x2 *__restrict__ plan_ex,
+                                                  long long *__restrict__ wlo, const Ctrl *ctrl) {
   const long long M = (long long)ctrl->acq_tot.a;
   const long long K = (long long)ctrl->n_keys;
   for (long long a = gtid(); a < M; a += gstride()) {
@@ -794,6 +794,19 @@ __global__ void k_alloc_chunks(NodeCols nd, PoolCols pool, Geo geo, const int32_
     const long long partial = (long long)plan[d].b - need;
     wlo[(long long)plan_ex[d].b + partial + t] = poff;  // the store writes by payload offset
   }
+}
+
+// Both allocation passes in one launch: the node pass (links, tails, the
+// counters) and the acquisition pass only share read-only snapshots
+// (k_seg_list's alloc_F / alloc_A / chunk_base, the plans), and an
+// OutOfArena stops every thread before either writes.
+__global__ void k_alloc(NodeCols nd, PoolCols pool, Geo geo, const int32_t *__restrict__ seg_node,
+                        const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
+                        const U64x2 *__restrict__ plan_ex, long long *__restrict__ wlo, SinkInfo *__restrict__ sinfo,
+                        Ctrl *ctrl, unsigned long long arena_cap, const int *guard) { lod::pdl_wait();
+  if (guard && *guard) return;
+  if (!alloc_nodes_body(nd, pool, geo, seg_node, seg_start, plan, plan_ex, wlo, sinfo, ctrl, arena_cap)) return;
+  alloc_chunks_body(nd, pool, geo, seg_node, seg_start, plan, plan_ex, wlo, ctrl);
 }
 
 // store_points / store_voxels (_kernels.py:155-250): sorted position p of a

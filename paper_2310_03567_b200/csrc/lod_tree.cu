@@ -182,7 +182,7 @@ struct LodTree {
   DBuf<int32_t> seg_node, dense;
   DBuf<U64x2> pairs;     // packed per-node plans, scanned in place (k_radix_ghist -> k_seg_list)
   DBuf<long long> wlo;   // write list: payload offsets of every touched node's chunks in slot order
-  DBuf<SinkInfo> sinfo;  // per node id: segment start, write-list start, count (k_alloc_nodes)
+  DBuf<SinkInfo> sinfo;  // per node id: segment start, write-list start, count (k_alloc)
   DBuf<long long> seg_start;
   DBuf<U64x2> plan, plan_ex;
   ScanLB lb32, lb64;  // single-pass scan state (u32 win counts; U64x2 segment / need pairs)
@@ -745,7 +745,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   cudaEvent_t EB = es ? t->ev[14] : t->ev[11], EE = es ? t->ev[15] : t->ev[10];
   // Early return: once allocation has run, nothing later in the cycle can fail
   // or change what the call reports, so the host returns after the control
-  // block published behind k_alloc_chunks while the sort + store + cleanup
+  // block published behind k_alloc while the sort + store + cleanup
   // still run on the tree stream (every later call and reader is ordered
   // behind them on that stream; device inputs are released to the caller's
   // stream by an event).  Not with a delta or phase profile (both read the
@@ -956,10 +956,9 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     exclusive_scan_lb<U64x2>(t->pairs.p, t->pairs.p, num_nodes, &t->d_ctrl->pack_tot, t->lb64, st, guard);
     lod::launch(k_seg_list, grid_for(num_nodes), 256, 0, st, t->nd, t->geo, t->nodecnt.p, num_nodes, t->pairs.p,
                 t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->plan_ex.p, t->d_ctrl, guard);
-    lod::launch(k_alloc_nodes, grid_for(Kb), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p, t->seg_start.p,
-                t->plan.p, t->plan_ex.p, t->wlo.p, t->sinfo.p, t->d_ctrl, t->arena_cap, guard);
-    lod::launch(k_alloc_chunks, grid_for(acq_bound), 256, 0, st, t->nd, t->pool, t->geo, t->seg_node.p,
-                t->seg_start.p, t->plan.p, t->plan_ex.p, t->wlo.p, t->d_ctrl, guard);
+    lod::launch(k_alloc, std::max(grid_for(Kb), grid_for(acq_bound)), 256, 0, st, t->nd, t->pool, t->geo,
+                t->seg_node.p, t->seg_start.p, t->plan.p, t->plan_ex.p, t->wlo.p, t->sinfo.p, t->d_ctrl,
+                t->arena_cap, guard);
     if (early) mid_seq = publish_ctrl(t);
     mark(3);
     tp("alloc_launched");

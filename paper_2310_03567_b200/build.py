@@ -39,7 +39,6 @@ def flags() -> list[str]:
         "-Xptxas", "-v" if os.environ.get("LOD_PTXAS_VERBOSE") else "-O3",
         "--expt-relaxed-constexpr",
         "-I", os.path.join(HERE, "..", "include"),
-        *os.environ.get("LOD_NVCC_EXTRA", "").split(),  # experiments only (e.g. -DLOD_EXP_NOCLAIM)
     ]
 
 

@@ -193,18 +193,9 @@ constexpr unsigned long long kEmptyHi = 0xFFFFFFFFFFFFFFFFULL;  // claim = all o
 // claimant usually finds a smaller index already there and issues no atomic.
 __device__ __forceinline__ void hash_claim(const Hash &h, UsedStage &stg, unsigned long long key, uint32_t v,
                                            uint32_t rgba, Ctrl *ctrl) {
-#ifdef LOD_EXP_NOCLAIM  // timing experiment only: results are wrong
-  return;
-#endif
-#ifdef LOD_EXP_COUNT  // instrumentation experiment: claims and probes into Ctrl.alloc_F / alloc_A
-  atomicAdd((unsigned long long *)&ctrl->alloc_F, 1ull);
-#endif
   key |= h.tag;
   unsigned long long slot = home_slot(h, key);
   for (unsigned long long probe = 0; probe < h.cap; ++probe) {
-#ifdef LOD_EXP_COUNT
-    atomicAdd((unsigned long long *)&ctrl->alloc_A, 1ull);
-#endif
     HSlot *sl = h.slots + slot;
     const unsigned long long mine = ((unsigned long long)v << 32) | rgba;
     ulonglong2 cur = __ldcg(reinterpret_cast<const ulonglong2 *>(sl));

@@ -166,15 +166,13 @@ __global__ void __launch_bounds__(kSelBlock)
     k_select(NodeCols nd, Geo geo, SelParams sp, int32_t *bufA, int32_t *bufB, int32_t *sel_out,
              unsigned long long *nsel, uint32_t *visflag, int mark) { lod::pdl_wait();
   __shared__ uint32_t sh[kSelBlock / 32 + 1];
-  __shared__ int s_expanded;
   int32_t *cur = bufA, *nxt = bufB;
   long long n = 1;
   if (!nd.inner[0] && nd.count[0] == 0) n = 0;  // a tree holding nothing selects nothing
   if (threadIdx.x == 0) cur[0] = 0;
   __syncthreads();
   for (;;) {
-    if (threadIdx.x == 0) s_expanded = 0;
-    __syncthreads();
+    int expanded = 0;  // this thread refined an entry in this round
     long long carry = 0;
     for (long long base = 0; base < n; base += kSelBlock) {
       const long long i = base + threadIdx.x;
@@ -189,19 +187,21 @@ __global__ void __launch_bounds__(kSelBlock)
       if (k == 1) {
         nxt[o] = item < 0 ? item : -(item + 1);
       } else if (k == 8) {
-        s_expanded = 1;
+        expanded = 1;
         const int c0 = nd.desc[item].x;  // children are 8 consecutive ids, octant order
 #pragma unroll
         for (int q = 0; q < 8; ++q) nxt[o + q] = c0 + q;
       }
       carry += tot;
     }
-    __syncthreads();
+    // block-wide OR of the flags doubles as the barrier that publishes `nxt`
+    // (a shared flag reset by one thread raced with the other warps' reads)
+    const int more = __syncthreads_or(expanded);
     n = carry;
     int32_t *t = cur;
     cur = nxt;
     nxt = t;
-    if (!s_expanded) break;
+    if (!more) break;
   }
   for (long long i = threadIdx.x; i < n; i += kSelBlock) {
     const int nid = -cur[i] - 1;

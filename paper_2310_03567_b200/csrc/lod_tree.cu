@@ -796,7 +796,9 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       if (sg.valid && sg.hx == xyz && sg.hc == rgba && sg.n == n) staged = &sg;
   }
   if (staged) {  // prefetched on the copy stream: wait for it, no copy here
-    if (staged->pending) RK(issue_stage(t, *staged));
+    // a copy not issued yet goes behind the work queued so far on the tree
+    // stream: an earlier early-returning insert's tail may still read this slot
+    if (staged->pending) RK(issue_pending(t));
     CK(cudaStreamWaitEvent(st, staged->ready, 0));
     staged->valid = false;
     bx = staged->xyz.p;
@@ -1102,11 +1104,6 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   mark(0);
   tp("expand_done");
   Ctrl h1 = *t->h_ctrl;
-#ifdef LOD_EXP_COUNT
-  fprintf(stderr, "[lod] claims=%lld probes=%lld n_used=%llu hcap=%llu n=%lld n_s=%lld\n", h1.alloc_F, h1.alloc_A,
-          h1.n_used, t->hcap, (long long)n, n_s);
-  cudaMemsetAsync(&t->d_ctrl->alloc_F, 0, 16, st);
-#endif
   t->num_nodes = h1.num_nodes;
   // a pipeline launched behind the settling decide has already run (the sync
   // waited for it) unless the claims overflowed, which the host handles here
@@ -1462,8 +1459,18 @@ struct PackHeader {
   unsigned long long magic;
   long long num_nodes, allocated_total, free_count;
   unsigned long long arena_off;
+  // the source tree's geometry: a pack unpacks only into an identically
+  // configured tree (node ids, grid offsets and chunk payloads depend on it)
+  double bmin[3], size;
+  long long grid_res, leaf_threshold, max_depth, chunk_capacity;
   Ctrl ctrl;
 };
+
+bool same_geometry(const PackHeader &h, const LodParams &p) {
+  return h.bmin[0] == p.bmin[0] && h.bmin[1] == p.bmin[1] && h.bmin[2] == p.bmin[2] && h.size == p.size &&
+         h.grid_res == p.grid_res && h.leaf_threshold == p.leaf_threshold && h.max_depth == p.max_depth &&
+         h.chunk_capacity == p.chunk_capacity;
+}
 constexpr unsigned long long kPackMagic = 0x4C4F4442323030ULL;  // "LODB200"
 
 struct PackLayout {
@@ -1512,7 +1519,19 @@ int lod_tree_pack(LodTree *t, void *dev_buf, uint64_t bytes) {
   const PackLayout L = pack_layout(c);
   if (bytes < L.total) return LOD_E_ARG;
   uint8_t *b = static_cast<uint8_t *>(dev_buf);
-  PackHeader hd{kPackMagic, c.num_nodes, c.allocated_total, c.free_count, c.arena_off, c};
+  PackHeader hd{};
+  hd.magic = kPackMagic;
+  hd.num_nodes = c.num_nodes;
+  hd.allocated_total = c.allocated_total;
+  hd.free_count = c.free_count;
+  hd.arena_off = c.arena_off;
+  for (int k = 0; k < 3; ++k) hd.bmin[k] = t->p.bmin[k];
+  hd.size = t->p.size;
+  hd.grid_res = t->p.grid_res;
+  hd.leaf_threshold = t->p.leaf_threshold;
+  hd.max_depth = t->p.max_depth;
+  hd.chunk_capacity = t->p.chunk_capacity;
+  hd.ctrl = c;
   cudaStream_t st = t->st;
   CK(cudaMemcpyAsync(b + L.off[0], &hd, sizeof(hd), cudaMemcpyHostToDevice, st));
   const size_t n = (size_t)c.num_nodes, a = (size_t)c.allocated_total, f = (size_t)c.free_count;
@@ -1535,7 +1554,7 @@ int lod_tree_unpack(LodTree *t, const void *dev_buf, uint64_t bytes) {
   const uint8_t *b = static_cast<const uint8_t *>(dev_buf);
   PackHeader hd;
   CK(cudaMemcpy(&hd, b, sizeof(hd), cudaMemcpyDeviceToHost));
-  if (hd.magic != kPackMagic) return LOD_E_ARG;
+  if (hd.magic != kPackMagic || !same_geometry(hd, t->p)) return LOD_E_ARG;
   const Ctrl c = hd.ctrl;
   const PackLayout L = pack_layout(c);
   if (bytes < L.total || c.arena_off > t->arena_cap) return LOD_E_ARG;

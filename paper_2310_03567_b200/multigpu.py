@@ -114,10 +114,12 @@ def bucket(xyz, rgba, plan: partition.Plan, world: int, bmin=(0.0, 0.0, 0.0), si
     return out, counts, starts
 
 
-def route(xyz, rgba, plan: partition.Plan, world: int, group=None):
+def route(xyz, rgba, plan: partition.Plan, world: int, group=None, bmin=(0.0, 0.0, 0.0), size: float = 1.0):
     """All-to-all routing of one stripe (global order) to the owners of its
     points; returns this rank's points as packed 16-byte records (n, 4) int32
-    in global order (receivers concatenate by source rank).
+    in global order (receivers concatenate by source rank).  ``bmin`` / ``size``
+    are the tree's root cube (``tree.bounds``): the octant prefix is computed
+    against it, like ``partition.plan_owners`` must be.
 
     CUDA tensors are bucketed by the lod_route_bucket kernels; CPU tensors
     (the gloo test path) by the same rule in torch."""
@@ -125,9 +127,9 @@ def route(xyz, rgba, plan: partition.Plan, world: int, group=None):
     import torch.distributed as dist
 
     if xyz.is_cuda:
-        rec, send_counts, _ = bucket(xyz, rgba, plan, world)
+        rec, send_counts, _ = bucket(xyz, rgba, plan, world, bmin, size)
     else:
-        own = owners_device(xyz, plan)
+        own = owners_device(xyz, plan, bmin, size)
         order = torch.sort(own, stable=True).indices  # bucket by owner, keep order
         rec = torch.cat([xyz.contiguous().view(torch.int32), rgba.view(torch.int32).reshape(-1, 1)], dim=1)[order]
         send_counts = torch.bincount(own, minlength=world).to(torch.int64)
@@ -390,12 +392,30 @@ def owned_cut(tree, selected, plan: partition.Plan, rank: int) -> list[int]:
     return keep
 
 
+def check_plan(tree, plan: partition.Plan) -> None:
+    """The partition invariants the protocol relies on: the plan covers every
+    depth-L prefix, and no cell of a replicated top node straddles a prefix
+    boundary (the split planes down to depth L coincide with cell faces iff
+    grid_res is a multiple of 2^L), so top-node claims stay rank-local."""
+    if len(plan.owner) != 8 ** plan.depth:
+        raise ValueError(f"plan has {len(plan.owner)} owners for depth {plan.depth}")
+    if tree.grid_res % (1 << plan.depth):
+        raise ValueError(f"grid_res {tree.grid_res} is not a multiple of 2^{plan.depth}: top-node cells would "
+                         "straddle prefix boundaries")
+
+
 class PartitionedInserter:
-    """Drives one rank of the warm-up / hand-off / partitioned protocol."""
+    """Drives one rank of the warm-up / hand-off / partitioned protocol.
+    Owners are computed against ``tree.bounds`` (the root cube); ``plan``
+    must have been made with the same bounds (``partition.plan_owners(...,
+    bmin=tree.bounds.min, size=tree.bounds.size)``)."""
 
     def __init__(self, tree, state, plan: partition.Plan, rank: int, world: int, group=None):
+        check_plan(tree, plan)
         self.tree, self.state, self.plan = tree, state, plan
         self.rank, self.world, self.group = rank, world, group
+        self.bmin = tuple(float(v) for v in tree.bounds.min)
+        self.size = float(tree.bounds.size)
         self.partitioned = world == 1
         self.router = None  # PeerRouter, created at the first partitioned batch
         self.no_peers = ""  # why the peer route is unavailable (then: NCCL all-to-all)
@@ -414,13 +434,14 @@ class PartitionedInserter:
             if xyz.is_cuda and self.router is None and not self.no_peers:
                 try:
                     self.router = PeerRouter(self.tree.device, self.rank, self.world, self.plan,
-                                             half_records=2 * int(rgba.shape[0]), group=self.group)
+                                             half_records=2 * int(rgba.shape[0]), group=self.group,
+                                             bmin=self.bmin, size=self.size)
                 except PeerUnavailable as e:  # GPUs without a peer path: route with the collective
                     self.no_peers = str(e)
             if self.router is not None:
                 rec = self.router.route(xyz, rgba)
             else:
-                rec = route(xyz, rgba, self.plan, self.world, self.group)
+                rec = route(xyz, rgba, self.plan, self.world, self.group, self.bmin, self.size)
             insert_records(self.tree, rec, self.state)
             return int(rec.shape[0])
         # warm-up: gather stripes to rank 0 (rank order = global order)

@@ -184,6 +184,12 @@ def insert_batch(
     rgba_b, dev_c = _as_input(rgba, np.uint32, ())
     if dev_x != dev_c:
         raise ValueError("xyz and rgba must both be host arrays or both be device tensors")
+    # the C ABI copies / reads exactly 12 n + 4 n bytes: shapes must agree
+    nx = xyz_b.numel() if dev_x else xyz_b.size
+    nc = rgba_b.numel() if dev_c else rgba_b.size
+    if nx != 3 * n_batch or nc != n_batch or (dev_x and tuple(xyz_b.shape) not in ((n_batch, 3), (3 * n_batch,))):
+        raise ValueError(f"xyz must be ({n_batch}, 3) and rgba ({n_batch},); got {tuple(xyz_b.shape)} and "
+                         f"{tuple(rgba_b.shape)}")
     flags = ((_lib.LOD_FLAG_DEVICE_INPUT if dev_x else 0) | (_lib.LOD_FLAG_PROFILE if profile else 0)
              | (_lib.LOD_FLAG_DELTA if collect_delta else 0))
     lim = _limits(tree, state, xyz_b if dev_x else None)
@@ -217,9 +223,10 @@ def insert_records(tree: Octree, records, state: UpdateState, collect_delta: boo
             raise TypeError("records must be an (n, 4) tensor of 4-byte elements")
         rec, flags = records.contiguous(), _lib.LOD_FLAG_DEVICE_INPUT | _lib.LOD_FLAG_INPUT_STREAM
     else:
-        rec, flags = np.ascontiguousarray(records).reshape(-1, 4), 0
-        if rec.dtype.itemsize != 4:
-            raise TypeError("records must be (n, 4) of 4-byte elements")
+        rec = np.ascontiguousarray(records)
+        if rec.ndim != 2 or rec.shape[1] != 4 or rec.dtype.itemsize != 4:
+            raise TypeError("records must be an (n, 4) array of 4-byte elements")
+        flags = 0
     flags |= _lib.LOD_FLAG_PACKED | (_lib.LOD_FLAG_DELTA if collect_delta else 0)
     lim = _limits(tree, state, rec if flags & _lib.LOD_FLAG_DEVICE_INPUT else None)
     bs = state._bstats

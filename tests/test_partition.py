@@ -114,8 +114,13 @@ def test_gloo_all_to_all_routing_preserves_global_order():
     assert dict(out) == {0: True, 1: True}
 
 
+OFFSET_ROOT = ((-3.0, 2.5, 10.0), 6.5)  # a cubified, non-unit, non-power-of-two root
+
+
 def _route_worker(rank, world, port, out):
-    """multigpu.route + composite_min with CPU tensors over gloo (the NCCL path's logic)."""
+    """multigpu.route + composite_min with CPU tensors over gloo (the NCCL path's
+    logic), for the unit cube and for an offset non-unit root (the owners must
+    be computed against the tree's bounds, not the unit cube)."""
     import torch
     import torch.distributed as dist
 
@@ -123,15 +128,20 @@ def _route_worker(rank, world, port, out):
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    xyz, _ = synth.gen_surface(12_000, 9)
-    rgba = np.arange(len(xyz), dtype=np.uint32)  # colour = global index
-    plan = partition.plan_owners([(xyz, rgba)], world)
-    n = len(rgba)
-    st = slice(rank * n // world, (rank + 1) * n // world)
-    rec = multigpu.route(torch.from_numpy(xyz[st].copy()), torch.from_numpy(rgba[st].view(np.int32).copy()),
-                         plan, world).numpy()
-    want_x, want_c = partition.take(plan, xyz, rgba, rank)
-    ok = np.array_equal(rec[:, :3].copy().view(np.float32), want_x) and np.array_equal(rec[:, 3].view(np.uint32), want_c)
+    ok = True
+    for bmin, size in (((0.0, 0.0, 0.0), 1.0), OFFSET_ROOT):
+        xyz, _ = synth.gen_surface(12_000, 9)
+        xyz = (xyz.astype(np.float64) * size + np.asarray(bmin)).astype(np.float32)
+        rgba = np.arange(len(xyz), dtype=np.uint32)  # colour = global index
+        plan = partition.plan_owners([(xyz, rgba)], world, bmin=bmin, size=size)
+        assert len(np.unique(plan.owner[partition.prefix_of(xyz, plan.depth, bmin, size)])) == world
+        n = len(rgba)
+        st = slice(rank * n // world, (rank + 1) * n // world)
+        rec = multigpu.route(torch.from_numpy(xyz[st].copy()), torch.from_numpy(rgba[st].view(np.int32).copy()),
+                             plan, world, bmin=bmin, size=size).numpy()
+        want_x, want_c = partition.take(plan, xyz, rgba, rank, bmin, size)
+        ok = ok and np.array_equal(rec[:, :3].copy().view(np.float32), want_x) and np.array_equal(
+            rec[:, 3].view(np.uint32), want_c)
     # framebuffer min-composite with the all-ones sentinel
     rng = np.random.default_rng(rank)
     fb = np.full(64, np.uint64(0xFFFFFFFFFFFFFFFF))

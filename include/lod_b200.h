@@ -124,6 +124,25 @@ int lod_tree_info(LodTree *tree, LodTreeInfo *info);
 int lod_insert_batch(LodTree *tree, const float *xyz, const uint32_t *rgba, int64_t n,
                      const LodLimits *limits, int flags, LodBatchStats *stats);
 
+/* Counts of the cycles whose insert returned before the device ran them:
+ * batches of at most 256 host points run as ONE kernel per cycle, and when no
+ * error is possible for the batch (its worst case bounded from n, the leaf
+ * threshold and the depth cannot overflow the backlog, the spill buffer or
+ * the arena) lod_insert_batch returns once the kernel is queued, reporting
+ * iterations = -1 and n_voxels = n_spill = n_splits = -1.  lod_tree_settle
+ * waits for the tree's stream (those cycles and an early-returning insert's
+ * tail included) and reports what the queued cycles did since the last
+ * settle; every other entry point that reads the tree is ordered behind them. */
+typedef struct {
+    int64_t calls;                          /* queued cycles folded by this call          */
+    int64_t n_voxels, n_voxels_max;         /* their new voxels: sum, largest cycle        */
+    int64_t n_spill_max, n_splits;          /* largest spill, sum of splits                */
+    int64_t num_nodes, splits_total, max_level;  /* the tree after them                    */
+    float device_ms;                        /* device time of those cycles + the last tail */
+    int32_t error;                          /* LOD_OK (a queued cycle cannot fail)         */
+} LodSettleStats;
+int lod_tree_settle(LodTree *tree, LodSettleStats *out);
+
 /* Wait until the tree's stream is idle (the last insert's tail included);
  * `last_device_ms` (may be NULL) receives that insert's device_ms when the
  * call returned early (else -1).  Every other entry point that reads the

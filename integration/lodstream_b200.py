@@ -70,7 +70,13 @@ class LodDeltaInfo(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int64) for k in ("n_splits", "n_voxel_groups", "n_voxels", "n_point_groups")]
 
 
-STRUCTS = (LodParams, LodLimits, LodBatchStats, LodTreeInfo, LodDeltaInfo)
+class LodSettleStats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int64) for k in ("calls", "n_voxels", "n_voxels_max", "n_spill_max", "n_splits",
+                                              "num_nodes", "splits_total", "max_level")] + [
+        ("device_ms", ctypes.c_float), ("error", ctypes.c_int32)]
+
+
+STRUCTS = (LodParams, LodLimits, LodBatchStats, LodTreeInfo, LodDeltaInfo, LodSettleStats)
 
 _P, _I64 = ctypes.c_void_p, ctypes.c_int64
 _SIGS = {
@@ -81,6 +87,7 @@ _SIGS = {
     "lod_insert_batch": (ctypes.c_int, [_P, _P, _P, _I64, ctypes.POINTER(LodLimits), ctypes.c_int,
                                         ctypes.POINTER(LodBatchStats)]),
     "lod_tree_wait": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_float)]),
+    "lod_tree_settle": (ctypes.c_int, [_P, ctypes.POINTER(LodSettleStats)]),
     "lod_prefetch_batch": (ctypes.c_int, [_P, _P, _P, _I64]),
     "lod_prefetch_drain": (ctypes.c_int, [_P]),
     "lod_read_nodes": (ctypes.c_int, [_P, _I64] + [_P] * 13),
@@ -169,6 +176,16 @@ def insert_batch_device(h, xyz_ptr: int, rgba_ptr: int, n: int, stream: int, bac
                                   FLAG_DEVICE_INPUT | FLAG_INPUT_STREAM, ctypes.byref(st)),
            "lod_insert_batch", errors_module)
     return st
+
+
+def settle(h) -> LodSettleStats:
+    """Wait for every queued cycle of the tree (tiny batches return once their
+    one-kernel cycle is queued, with n_voxels = -1) and get what those cycles
+    did: fold calls / n_voxels / n_voxels_max / n_spill_max / n_splits into
+    UpdateStats (update.py:382-392)."""
+    out = LodSettleStats()
+    _check(lib().lod_tree_settle(h, ctypes.byref(out)), "lod_tree_settle")
+    return out
 
 
 def wait(h) -> float:

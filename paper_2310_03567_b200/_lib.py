@@ -94,6 +94,13 @@ class LodTreeInfo(ctypes.Structure):
     ]
 
 
+class LodSettleStats(ctypes.Structure):
+    _fields_ = [("calls", ctypes.c_int64), ("n_voxels", ctypes.c_int64), ("n_voxels_max", ctypes.c_int64),
+                ("n_spill_max", ctypes.c_int64), ("n_splits", ctypes.c_int64), ("num_nodes", ctypes.c_int64),
+                ("splits_total", ctypes.c_int64), ("max_level", ctypes.c_int64), ("device_ms", ctypes.c_float),
+                ("error", ctypes.c_int32)]
+
+
 class LodDeltaInfo(ctypes.Structure):
     _fields_ = [("n_splits", ctypes.c_int64), ("n_voxel_groups", ctypes.c_int64), ("n_voxels", ctypes.c_int64),
                 ("n_point_groups", ctypes.c_int64)]
@@ -114,6 +121,7 @@ SIGNATURES = {
     "lod_prefetch_batch": (ctypes.c_int, [_P, _P, _P, _I64]),
     "lod_prefetch_drain": (ctypes.c_int, [_P]),
     "lod_tree_wait": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_float)]),
+    "lod_tree_settle": (ctypes.c_int, [_P, ctypes.POINTER(LodSettleStats)]),
     "lod_read_nodes": (ctypes.c_int, [_P, _I64] + [_P] * 13),
     "lod_read_pool": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _I64]),
     "lod_gather": (ctypes.c_int, [_P, _I64, _I64, _P, _P]),

@@ -17,6 +17,7 @@
 #include "../../include/lod_b200.h"
 #include "lod_common.cuh"
 #include "lod_kernels.cuh"
+#include "lod_small.cuh"
 #include "radix.cuh"
 #include "scan.cuh"
 
@@ -224,7 +225,26 @@ struct LodTree {
   // host copies of counters (authoritative after every call)
   long long num_nodes = 1;
   long long d2h_bytes = 0;  // control-block readbacks since the last reset
+  // small-batch path (lod_small.cuh): one launch per cycle
+  DBuf<float4> sm_brec, sm_srec;
+  DBuf<int32_t> sm_node_b, sm_node_s, sm_tl, sm_cand, sm_splits, sm_touched;
+  DBuf<long long> sm_nnew, sm_cur, sm_wls, sm_pl, sm_wl, sm_sp;  // nnew / cur / wls: per node
+  DBuf<uint4> sm_backlog;
+  float4 *sm_ring = nullptr, *sm_ring_dev = nullptr;  // mapped pinned batch slots
+  SmallResult *sm_res = nullptr, *sm_res_dev = nullptr;  // mapped per-call result
+  unsigned *sm_done = nullptr, *sm_done_dev = nullptr;    // mapped completion counter
+  SmallAccum *sm_acc = nullptr;                           // device: totals of queued cycles
+  unsigned sm_seq = 0;
+  long long sm_queued = 0;  // asynchronous small cycles since the host copies were exact
+  long long sm_unfolded = 0;  // asynchronous small cycles not yet reported by lod_tree_settle
+  // upper bounds of the counters while asynchronous small cycles are queued
+  // (exact whenever sm_queued == 0)
+  long long ub_nodes = 1, ub_alloc = 0;
+  unsigned long long ub_arena = 0;
+  long long ingested = 0;  // points inserted so far (bounds the spill of a cycle)
 };
+
+static constexpr int kSmallRing = 512;  // batch slots of kSmallMaxBatch records each
 
 // ---------------------------------------------------------------- burst resolve
 // A split wave re-descends tens of millions of spilled points in one cycle
@@ -378,6 +398,24 @@ static int wait_ctrl(LodTree *t, unsigned want) {
   return LOD_OK;
 }
 
+// The counters as the host last saw them become exact again (after queued
+// asynchronous small cycles: one publication behind everything queued).
+static void exact_bounds(LodTree *t) {
+  const Ctrl &c = *t->h_ctrl;
+  t->num_nodes = c.num_nodes;
+  t->ub_nodes = c.num_nodes;
+  t->ub_alloc = c.allocated_total;
+  t->ub_arena = c.arena_off;
+  t->sm_queued = 0;
+}
+
+static int refresh(LodTree *t) {
+  if (t->sm_queued == 0) return LOD_OK;
+  RK(sync_ctrl(t));
+  exact_bounds(t);
+  return LOD_OK;
+}
+
 template <typename T>
 static int grow_col(T *&ptr, long long old_cap, long long new_cap, long long keep, cudaStream_t st) {
   T *q = nullptr;
@@ -431,6 +469,11 @@ static int ensure_nodes(LodTree *t, long long want, long long live) {
   long long oldv = t->visflag.cap;
   RK(t->visflag.ensure(nc, st, oldv));
   if (t->visflag.cap > oldv) CK(cudaMemsetAsync(t->visflag.p + oldv, 0, (size_t)(t->visflag.cap - oldv) * 4, st));
+  long long oldnn = t->sm_nnew.cap;  // zero between cycles
+  RK(t->sm_nnew.ensure(nc, st, oldnn));
+  if (t->sm_nnew.cap > oldnn) CK(cudaMemsetAsync(t->sm_nnew.p + oldnn, 0, (size_t)(t->sm_nnew.cap - oldnn) * 8, st));
+  RK(t->sm_cur.ensure(nc, st));
+  RK(t->sm_wls.ensure(nc, st));
   t->ncap = nc;
   return LOD_OK;
 }
@@ -528,8 +571,179 @@ static int abort_cycle(LodTree *t, int code) {
   cudaStreamSynchronize(t->st);
   // counters: the device ctrl keeps whatever was applied before the failure
   sync_ctrl(t);
-  t->num_nodes = t->h_ctrl->num_nodes;
+  exact_bounds(t);
   return code;
+}
+
+// ---------------------------------------------------------------- small batches
+
+// Spin until a mapped counter reaches `want` (a stream error ends the wait).
+static int wait_mapped(LodTree *t, volatile unsigned *flag, unsigned want) {
+  for (unsigned spins = 0; (int)(*flag - want) < 0; ++spins) {
+    if ((spins & 1023) == 1023) {
+      const cudaError_t e = cudaStreamQuery(t->st);
+      if (e != cudaSuccess && e != cudaErrorNotReady) return cuda_rc(e);
+      if (e == cudaSuccess && (int)(*flag - want) < 0) return LOD_E_CUDA;  // drained without the write
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  return LOD_OK;
+}
+
+// One update cycle of a tiny host batch in one launch (k_small_cycle).  The
+// worst case of the cycle is bounded from n alone: a leaf below max depth
+// holds <= T points, so the spill is <= n*T, a path crosses <= max_depth
+// inner nodes, every split needs > T points.  When that worst case cannot
+// overflow the backlog, the spill buffer or the arena, the call returns as
+// soon as the kernel is queued (its counters are folded in by
+// lod_tree_settle; host copies are refreshed by the next reader); otherwise
+// it waits for the kernel's result and reports errors like the pipeline.
+// *handled = false: not eligible, the caller runs the pipeline.
+static int small_insert(LodTree *t, const float *xyz, const uint32_t *rgba, long long n, long long backlog_cap,
+                        long long spill_cap, LodBatchStats &S, bool *handled) {
+  *handled = false;
+  const Geo &g = t->geo;
+  const long long T = std::max<long long>(g.T, 0), D = std::max<long long>(g.max_depth, 1), C = g.C;
+  if (n * T > kSmallAllMax && t->ingested > kSmallAllMax) return LOD_OK;
+  const long long spill_max = std::min<long long>(n * T, t->ingested);
+  const long long all_max = n + spill_max;
+  if (all_max > kSmallAllMax) return LOD_OK;
+  const long long s_max = n + D * (all_max / (T + 1));
+  const long long nv_max = all_max * D;
+  const long long touched_max = std::min<long long>(all_max + nv_max, (n + 8 * s_max) + (n * D + s_max));
+  const long long chunks_max = (all_max + nv_max) / C + touched_max + 1;
+  const unsigned long long gs = ((unsigned long long)g.grid_bytes + 63ull) / 64ull * 64ull;
+  const unsigned long long arena_max =
+      (unsigned long long)s_max * gs + 80ull + (unsigned long long)chunks_max * (unsigned long long)C * 16ull;
+  *handled = true;
+  cudaStream_t st = t->st;
+  // capacities for the worst case (stream-ordered growth; exact counters first)
+  if (t->sm_queued && (t->ub_nodes + 8 * s_max + 1 > t->ncap || t->ub_alloc + chunks_max + 1 > t->ccap ||
+                       t->ub_arena + arena_max > t->arena_cap || t->sm_queued >= 4096))
+    RK(refresh(t));
+  RK(ensure_nodes(t, t->ub_nodes + 8 * s_max + 1, t->ub_nodes));
+  RK(ensure_chunks(t, t->ub_alloc + chunks_max + 1, t->ub_alloc));
+  const bool async_call = nv_max <= backlog_cap && spill_max <= spill_cap && t->ub_arena + arena_max <= t->arena_cap;
+  RK(t->sm_brec.ensure(kSmallMaxBatch, st));
+  RK(t->sm_node_b.ensure(kSmallMaxBatch, st));
+  RK(t->sm_srec.ensure(spill_max + 1, st));
+  RK(t->sm_node_s.ensure(spill_max + 1, st));
+  RK(t->sm_tl.ensure(all_max, st));
+  RK(t->sm_cand.ensure(all_max, st));
+  RK(t->sm_splits.ensure(all_max, st));
+  RK(t->sm_sp.ensure(4 * all_max, st));
+  RK(t->sm_touched.ensure(touched_max, st));
+  RK(t->sm_pl.ensure(3 * touched_max, st));
+  RK(t->sm_wl.ensure(chunks_max + touched_max, st));
+  RK(t->sm_backlog.ensure(nv_max, st));
+  if (!t->sm_ring) {
+    CK(cudaHostAlloc(&t->sm_ring, (size_t)kSmallRing * kSmallMaxBatch * sizeof(float4), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(&t->sm_ring_dev, t->sm_ring, 0));
+    CK(cudaHostAlloc(&t->sm_res, sizeof(SmallResult), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(&t->sm_res_dev, t->sm_res, 0));
+    CK(cudaHostAlloc(&t->sm_done, sizeof(unsigned), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(&t->sm_done_dev, t->sm_done, 0));
+    memset(t->sm_res, 0, sizeof(SmallResult));
+    *t->sm_done = t->sm_seq;
+    CK(cudaMalloc(&t->sm_acc, sizeof(SmallAccum)));
+    CK(cudaMemsetAsync(t->sm_acc, 0, sizeof(SmallAccum), st));
+  }
+  const unsigned seq = t->sm_seq + 1;
+  // the slot was last used kSmallRing cycles ago: that cycle must be done
+  RK(wait_mapped(t, t->sm_done, seq - kSmallRing));
+  const size_t off = (size_t)(seq % kSmallRing) * kSmallMaxBatch;
+  float4 *slot = t->sm_ring + off;
+  for (long long i = 0; i < n; ++i) {
+    float4 r;
+    r.x = xyz[3 * i];
+    r.y = xyz[3 * i + 1];
+    r.z = xyz[3 * i + 2];
+    uint32_t c = rgba[i];
+    memcpy(&r.w, &c, 4);
+    slot[i] = r;
+  }
+  SmallArgs a;
+  a.nd = t->nd;
+  a.pool = t->pool;
+  a.geo = t->geo;
+  a.arena = t->arena;
+  a.ctrl = t->d_ctrl;
+  a.in = t->sm_ring_dev + off;
+  a.n = (int)n;
+  a.brec = t->sm_brec.p;
+  a.srec = t->sm_srec.p;
+  a.node_b = t->sm_node_b.p;
+  a.node_s = t->sm_node_s.p;
+  a.srank = t->srank.p;
+  a.nnew = t->sm_nnew.p;
+  a.cur = t->sm_cur.p;
+  a.wls = t->sm_wls.p;
+  a.backlog = t->sm_backlog.p;
+  a.tl = t->sm_tl.p;
+  a.cand = t->sm_cand.p;
+  a.splits = t->sm_splits.p;
+  a.touched = t->sm_touched.p;
+  a.pl = t->sm_pl.p;
+  a.wl = t->sm_wl.p;
+  a.sp = t->sm_sp.p;
+  a.all_cap = std::min<long long>({t->sm_tl.cap, t->sm_cand.cap, t->sm_splits.cap, t->sm_sp.cap / 4,
+                                   t->sm_srec.cap + n, t->sm_node_s.cap + n});
+  a.vox_cap = t->sm_backlog.cap;
+  a.touched_cap = std::min<long long>(t->sm_touched.cap, t->sm_pl.cap / 3);
+  a.split_cap = std::min<long long>(t->sm_cand.cap, t->sm_splits.cap);
+  a.wl_cap = t->sm_wl.cap;
+  a.ncap = t->ncap;
+  a.ccap = t->ccap;
+  a.spill_cap = spill_cap;
+  a.backlog_cap = backlog_cap;
+  a.arena_cap = t->arena_cap;
+  a.res = t->sm_res_dev;
+  a.done = t->sm_done_dev;
+  a.acc = t->sm_acc;
+  a.seq = seq;
+  a.async_call = async_call ? 1 : 0;
+  t->sm_seq = seq;
+  CK(lod::launch(k_small_cycle, 1, kSmallBlock, 0, st, a));
+  t->ingested += n;
+  S.launches = 1;
+  S.h2d_bytes = 16 * n;  // read by the kernel from mapped host memory
+  if (async_call) {  // no error is possible: return now
+    t->ub_nodes += 8 * s_max;
+    t->ub_alloc += chunks_max;
+    t->ub_arena += arena_max;
+    ++t->sm_queued;
+    ++t->sm_unfolded;
+    S.iterations = -1;  // queued: lod_tree_settle reports the counts
+    S.device_ms = -1.f;
+    S.device_ms_prev = -1.f;
+    S.n_spill = S.n_voxels = S.n_splits = -1;
+    S.num_nodes = t->ub_nodes;  // upper bounds
+    S.allocated_total = t->ub_alloc;
+    S.arena_offset = t->ub_arena;
+    return LOD_OK;
+  }
+  volatile SmallResult *r = t->sm_res;
+  RK(wait_mapped(t, &r->seq, seq));
+  S.n_spill = r->n_spill;
+  S.n_voxels = r->n_voxels;
+  S.n_splits = r->n_splits;
+  S.iterations = r->iterations;
+  S.num_nodes = r->num_nodes;
+  S.splits_total = r->splits_total;
+  S.max_level = r->max_level;
+  S.allocated_total = r->allocated_total;
+  S.free_count = r->free_count;
+  S.released_total = r->released_total;
+  S.arena_offset = r->arena_off;
+  S.device_ms = (float)(r->device_ns * 1e-6);
+  S.device_ms_prev = -1.f;
+  t->num_nodes = r->num_nodes;
+  t->ub_nodes = r->num_nodes;
+  t->ub_alloc = r->allocated_total;
+  t->ub_arena = r->arena_off;
+  t->sm_queued = 0;
+  t->prev_used = r->n_voxels;
+  return r->error;
 }
 
 // ---------------------------------------------------------------- C ABI
@@ -665,6 +879,14 @@ int lod_tree_destroy(LodTree *t) {
   f(t->pool.free_stack);
   f(t->d_ctrl);
   if (t->h_ctrl) cudaFreeHost(t->h_ctrl);
+  if (t->sm_ring) cudaFreeHost(t->sm_ring);
+  if (t->sm_res) cudaFreeHost(t->sm_res);
+  if (t->sm_done) cudaFreeHost(t->sm_done);
+  f(t->sm_acc);
+  t->sm_brec.release(); t->sm_srec.release(); t->sm_node_b.release(); t->sm_node_s.release();
+  t->sm_tl.release(); t->sm_cand.release(); t->sm_splits.release(); t->sm_touched.release();
+  t->sm_nnew.release(); t->sm_cur.release(); t->sm_wls.release(); t->sm_pl.release(); t->sm_wl.release();
+  t->sm_sp.release(); t->sm_backlog.release();
   if (t->h_seq) cudaFreeHost(t->h_seq);
   t->xlist.release(); t->split_list.release(); t->node_b.release(); t->node_all.release();
   t->bitmap.release(); t->scnt.release(); t->schk.release();
@@ -700,6 +922,7 @@ int lod_tree_info(LodTree *t, LodTreeInfo *info) {
   if (!t || !info) return LOD_E_ARG;
   cudaSetDevice(t->dev);
   RK(sync_ctrl(t));
+  exact_bounds(t);  // between calls the published counters are exact
   const Ctrl &c = *t->h_ctrl;
   info->num_nodes = c.num_nodes;
   info->node_capacity = t->ncap;
@@ -736,6 +959,20 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     return LOD_OK;
   }
   if (n >= (1LL << 31)) return LOD_E_ARG;
+  static const bool no_small = getenv("LOD_NO_SMALL") != nullptr;  // A/B switch: pipeline for every batch
+  if (!no_small && n <= kSmallMaxBatch &&
+      !(flags & (LOD_FLAG_DEVICE_INPUT | LOD_FLAG_PACKED | LOD_FLAG_DELTA | LOD_FLAG_PROFILE))) {
+    bool handled = false;
+    const int rc = small_insert(t, xyz, rgba, n, backlog_cap, spill_cap, S, &handled);
+    if (handled) {
+      if (rc) {  // the structure stays walkable (partial state, errors.py:1-5)
+        RK(sync_ctrl(t));
+        exact_bounds(t);
+      }
+      return rc;
+    }
+  }
+  RK(refresh(t));  // the pipeline sizes its launches from exact host copies
   // device-time events: this call's pair, the previous call's kept for its
   // report when that call returned before its tail ran
   const bool prev_pending = t->tail_pending;
@@ -1157,6 +1394,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   S.n_splits = splits_cycle;
   S.iterations = iters;
   fill_stats(t, &S);
+  exact_bounds(t);  // the counters published behind k_alloc are final
+  t->ingested += n;
   float ms = -1.f;
   if (early) {  // the tail is still running: its time is reported by the next call / lod_tree_wait
     t->tail_pending = true;
@@ -1195,10 +1434,45 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   return LOD_OK;
 }
 
+int lod_tree_settle(LodTree *t, LodSettleStats *out) {
+  if (!t || !out) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  memset(out, 0, sizeof(*out));
+  CK(cudaStreamSynchronize(t->st));
+  float ms = 0.f;
+  if (t->tail_pending) {
+    float x = 0.f;
+    cudaEventElapsedTime(&x, t->ev_slot ? t->ev[14] : t->ev[11], t->ev_slot ? t->ev[15] : t->ev[10]);
+    ms += x;
+    t->tail_pending = false;
+  }
+  if (t->sm_acc && t->sm_unfolded) {
+    SmallAccum acc;
+    CK(cudaMemcpy(&acc, t->sm_acc, sizeof(acc), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(t->sm_acc, 0, sizeof(acc)));
+    out->calls = acc.calls;
+    out->n_voxels = acc.nv_sum;
+    out->n_voxels_max = acc.nv_max;
+    out->n_spill_max = acc.ns_max;
+    out->n_splits = acc.splits_sum;
+    out->error = acc.error;
+    ms += (float)(acc.device_ns * 1e-6);
+  }
+  t->sm_unfolded = 0;
+  RK(sync_ctrl(t));
+  exact_bounds(t);
+  out->num_nodes = t->h_ctrl->num_nodes;
+  out->splits_total = t->h_ctrl->splits_total;
+  out->max_level = t->h_ctrl->max_level;
+  out->device_ms = ms;
+  return out->error;
+}
+
 int lod_tree_wait(LodTree *t, float *last_device_ms) {
   if (!t) return LOD_E_ARG;
   cudaSetDevice(t->dev);
   CK(cudaStreamSynchronize(t->st));
+  RK(refresh(t));
   float ms = -1.f;
   if (t->tail_pending) {
     cudaEventElapsedTime(&ms, t->ev_slot ? t->ev[14] : t->ev[11], t->ev_slot ? t->ev[15] : t->ev[10]);
@@ -1273,6 +1547,7 @@ static int gather_impl(LodTree *t, const std::vector<int32_t> &nodes, const std:
 }
 
 int lod_gather(LodTree *t, int64_t nid, int64_t start, float *xyz, uint32_t *rgba) {
+  if (t) RK(refresh(t));
   if (!t || nid < 0 || nid >= t->num_nodes || start < 0) return LOD_E_ARG;
   cudaSetDevice(t->dev);
   long long cnt = 0;
@@ -1294,6 +1569,7 @@ int lod_gather(LodTree *t, int64_t nid, int64_t start, float *xyz, uint32_t *rgb
 }
 
 int lod_dump_records(LodTree *t, int64_t num_nodes, int64_t *offsets, void *records) {
+  if (t) RK(refresh(t));
   if (!t || num_nodes < 0 || num_nodes > t->num_nodes || !offsets) return LOD_E_ARG;
   cudaSetDevice(t->dev);
   std::vector<long long> cnt((size_t)num_nodes);
@@ -1428,7 +1704,10 @@ long long lod_tree_allocated(LodTree *t) {
   cudaStreamSynchronize(t->st);
   return t->h_ctrl->allocated_total;
 }
-long long lod_tree_num_nodes(LodTree *t) { return t->num_nodes; }
+long long lod_tree_num_nodes(LodTree *t) {
+  refresh(t);
+  return t->num_nodes;
+}
 uint32_t *lod_tree_visflag(LodTree *t) { return t->visflag.p; }
 int lod_tree_ensure_vislist(LodTree *t, long long n, int32_t **p) {
   int rc = t->vislist.ensure(std::max<long long>(n, 1), t->st);
@@ -1550,6 +1829,7 @@ int lod_tree_pack(LodTree *t, void *dev_buf, uint64_t bytes) {
 int lod_tree_unpack(LodTree *t, const void *dev_buf, uint64_t bytes) {
   if (!t || !dev_buf || bytes < sizeof(PackHeader)) return LOD_E_ARG;
   cudaSetDevice(t->dev);
+  RK(refresh(t));
   cudaStream_t st = t->st;
   const uint8_t *b = static_cast<const uint8_t *>(dev_buf);
   PackHeader hd;
@@ -1581,7 +1861,8 @@ int lod_tree_unpack(LodTree *t, const void *dev_buf, uint64_t bytes) {
   nc.released_total = c.released_total;
   CK(cudaMemcpyAsync(t->d_ctrl, &nc, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
   RK(sync_ctrl(t));
-  t->num_nodes = c.num_nodes;
+  exact_bounds(t);
+  t->ingested = 1LL << 40;  // unknown: the spill of a cycle is then bounded by n * T alone
   return LOD_OK;
 }
 

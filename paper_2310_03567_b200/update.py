@@ -132,17 +132,56 @@ class BatchDelta:
 
 
 class UpdateState:
-    """Per-tree transient state and statistics (update.py:197-223)."""
+    """Per-tree transient state and statistics (update.py:197-223).
+
+    Cycles the device has not run yet (a tiny batch's one-kernel cycle queued
+    by an insert that could not fail, or an early-returning insert's tail) are
+    folded into ``stats`` on the first read: the read waits for them
+    (lod_tree_settle), adds their counts, and adds the wait to
+    ``update_seconds`` -- so ``update_seconds`` is the wall time until the
+    tree was settled, as in the reference, whose insert_batch returns settled."""
 
     def __init__(self, config: UpdateConfig | None = None) -> None:
         self.config = config or UpdateConfig()
         self.spill = SpillBuffer(self.config.spill_capacity)
         self.backlog = VoxelBacklog(self.config.backlog_capacity)
-        self.stats = UpdateStats()
+        self._stats = UpdateStats()
         self.clock = BudgetClock(self.config.budget_ms)
         self.last: dict | None = None  # LodBatchStats of the last call
         self._limits = _lib.LodLimits()
         self._bstats = _lib.LodBatchStats()
+        self._unsettled: dict[int, Octree] = {}  # trees with work the device has not run yet
+
+    @property
+    def stats(self) -> UpdateStats:
+        if self._unsettled:
+            self.settle()
+        return self._stats
+
+    @stats.setter
+    def stats(self, value: UpdateStats) -> None:
+        self._stats = value
+
+    def settle(self) -> None:
+        """Wait for every queued cycle of this state's trees and fold their counts in."""
+        st = self._stats
+        for tree in list(self._unsettled.values()):
+            t0 = time.perf_counter()
+            out = _lib.LodSettleStats()
+            rc = tree._L.lod_tree_settle(tree.handle, ctypes.byref(out))
+            tree._invalidate()
+            st.update_seconds += time.perf_counter() - t0
+            st.device_seconds += float(out.device_ms) * 1e-3
+            if out.calls:
+                st.voxels_created += int(out.n_voxels)
+                self.backlog.high_water = max(self.backlog.high_water, int(out.n_voxels_max))
+                self.spill.high_water = max(self.spill.high_water, int(out.n_spill_max))
+                st.backlog_high_water = self.backlog.high_water
+                st.spill_high_water = self.spill.high_water
+            st.splits = int(out.splits_total)
+            st.nodes = int(out.num_nodes)
+            _lib.check(rc, "settle")
+        self._unsettled.clear()
 
 
 def _as_input(a, dtype, shape_tail):
@@ -180,6 +219,9 @@ def insert_batch(
     n_batch = len(rgba)
     if n_batch == 0:  # update.py:266-268
         return BatchDelta() if collect_delta else None
+    if (n_batch <= _SMALL and not collect_delta and not profile and type(xyz) is np.ndarray
+            and type(rgba) is np.ndarray):
+        return _insert_small(tree, xyz, rgba, n_batch, state, t0)
     xyz_b, dev_x = _as_input(xyz, np.float32, (3,))
     rgba_b, dev_c = _as_input(rgba, np.uint32, ())
     if dev_x != dev_c:
@@ -201,12 +243,56 @@ def insert_batch(
     tree._invalidate()
     _lib.check(rc, "insert_batch")
     _account(state, bs, n_batch, profile)
-    st = state.stats
+    if bs.device_ms < 0:  # returned before its tail ran
+        state._unsettled[id(tree)] = tree
+    st = state._stats
     delta = _read_delta(tree) if collect_delta else None
     dt = time.perf_counter() - t0
     st.update_seconds += dt
     st.max_batch_ms = max(st.max_batch_ms, dt * 1e3)
     return delta
+
+
+_SMALL = 256  # kSmallMaxBatch: host batches up to this size run as one kernel per cycle
+
+
+def _insert_small(tree: Octree, xyz: np.ndarray, rgba: np.ndarray, n_batch: int, state: UpdateState,
+                  t0: float) -> None:
+    """insert_batch for a tiny host batch: the library runs the whole cycle as
+    one kernel (lod_small.cuh) and, when no error is possible for the batch,
+    returns as soon as it is queued (bs.iterations == -1); its counts reach
+    ``state.stats`` when the state settles."""
+    if xyz.dtype != np.float32 or not xyz.flags.c_contiguous:
+        xyz = np.ascontiguousarray(xyz, np.float32)
+    if rgba.dtype != np.uint32 or not rgba.flags.c_contiguous:
+        rgba = np.ascontiguousarray(rgba, np.uint32)
+    if xyz.size != 3 * n_batch or rgba.size != n_batch:
+        raise ValueError(f"xyz must be ({n_batch}, 3) and rgba ({n_batch},); got {xyz.shape} and {rgba.shape}")
+    lim = state._limits
+    lim.backlog_capacity = state.config.backlog_capacity
+    lim.spill_capacity = state.config.spill_capacity
+    lim.input_stream = None
+    bs = state._bstats
+    rc = tree._L.lod_insert_batch(tree._h, xyz.ctypes.data, rgba.ctypes.data, n_batch, ctypes.byref(lim), 0,
+                                  ctypes.byref(bs))
+    tree._gen += 1
+    if tree._cache:
+        tree._cache.clear()
+    _lib.check(rc, "insert_batch")
+    st = state._stats
+    if bs.iterations < 0:  # queued: counts folded in when the state settles
+        st.batches += 1
+        st.points += n_batch
+        st.launches += 1
+        st.h2d_bytes += 16 * n_batch
+        state._unsettled[id(tree)] = tree
+    else:
+        _account(state, bs, n_batch, False)
+    dt = time.perf_counter() - t0
+    st.update_seconds += dt
+    if dt * 1e3 > st.max_batch_ms:
+        st.max_batch_ms = dt * 1e3
+    return None
 
 
 def insert_records(tree: Octree, records, state: UpdateState, collect_delta: bool = False) -> BatchDelta | None:
@@ -236,8 +322,10 @@ def insert_records(tree: Octree, records, state: UpdateState, collect_delta: boo
     _account(state, bs, n_batch, profile=False)
     delta = _read_delta(tree) if collect_delta else None
     dt = time.perf_counter() - t0
-    state.stats.update_seconds += dt
-    state.stats.max_batch_ms = max(state.stats.max_batch_ms, dt * 1e3)
+    if bs.device_ms < 0:
+        state._unsettled[id(tree)] = tree
+    state._stats.update_seconds += dt
+    state._stats.max_batch_ms = max(state._stats.max_batch_ms, dt * 1e3)
     return delta
 
 
@@ -260,7 +348,7 @@ def _limits(tree: Octree, state: UpdateState, dev_tensor):
 
 def _account(state: UpdateState, bs, n_batch: int, profile: bool) -> None:
     """UpdateStats bookkeeping of one cycle (update.py:382-392)."""
-    st = state.stats
+    st = state._stats
     n_v, n_s = int(bs.n_voxels), int(bs.n_spill)
     st.batches += 1
     st.points += n_batch
@@ -283,18 +371,25 @@ def _account(state: UpdateState, bs, n_batch: int, profile: bool) -> None:
 
 
 def wait_settled(tree: Octree, state: UpdateState | None = None) -> float:
-    """Block until the tree's last update has fully run on the device.
+    """Block until the tree's updates have fully run on the device.
 
     insert_batch returns once the cycle's outcome is final (allocation done,
     errors raised); the sort + store + cleanup of its last pass may still run
-    on the tree's stream, ahead of every later call on the tree.  Returns that
-    update's device ms (-1 if none was outstanding) and adds it to
-    ``state.stats.device_seconds``."""
-    ms = ctypes.c_float(-1.0)
-    _lib.check(tree._L.lod_tree_wait(tree.handle, ctypes.byref(ms)), "tree_wait")
-    if state is not None and ms.value >= 0:
-        state.stats.device_seconds += ms.value * 1e-3
-    return float(ms.value)
+    on the tree's stream, ahead of every later call on the tree, and a tiny
+    batch's one-kernel cycle may still be queued.  Returns the device ms of
+    the work that was outstanding (-1 if none) and, with ``state``, folds its
+    counts and the wall wait into ``state.stats``."""
+    if state is not None:
+        state._unsettled[id(tree)] = tree
+        before = state._stats.device_seconds
+        state.settle()
+        ms = (state._stats.device_seconds - before) * 1e3
+        return ms if ms > 0 else -1.0
+    out = _lib.LodSettleStats()
+    rc = tree._L.lod_tree_settle(tree.handle, ctypes.byref(out))
+    tree._invalidate()
+    _lib.check(rc, "settle")
+    return float(out.device_ms) if out.device_ms > 0 else -1.0
 
 
 def _read_delta(tree: Octree) -> BatchDelta:
@@ -387,7 +482,7 @@ def run_frame_updates(tree, batches, state: UpdateState, on_delta=None) -> int:
             else:  # an error ends the frame: the caller owns the queued arrays again
                 tree._L.lod_prefetch_drain(tree.handle)
     if processed:
-        st = state.stats
+        st = state._stats  # no settle: the frame's last tail keeps running behind the caller
         st.frames += 1
         dt = state.clock.elapsed_ms()
         st.frame_ms_total += dt

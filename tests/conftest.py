@@ -34,3 +34,7 @@ def gpu():
 
     _lib.require_device(0)
     return 0
+
+
+# the staged reference suite runs in its own pytest process (test_ref_suite.py)
+collect_ignore_glob = ["ref_suite/*"]

@@ -41,7 +41,7 @@ def _bindings():
 
     return {
         "facade": {c.__name__: c for c in (_lib.LodParams, _lib.LodLimits, _lib.LodBatchStats, _lib.LodTreeInfo,
-                                           _lib.LodDeltaInfo)},
+                                           _lib.LodDeltaInfo, _lib.LodSettleStats)},
         "integration": {c.__name__: c for c in ref_side.STRUCTS},
     }
 
@@ -49,7 +49,8 @@ def _bindings():
 @pytest.mark.parametrize("which", ["facade", "integration"])
 def test_struct_layouts_match_header(tmp_path, which):
     structs = _bindings()[which]
-    assert set(structs) == {"LodParams", "LodLimits", "LodBatchStats", "LodTreeInfo", "LodDeltaInfo"}
+    assert set(structs) == {"LodParams", "LodLimits", "LodBatchStats", "LodTreeInfo", "LodDeltaInfo",
+                            "LodSettleStats"}
     c = _c_layout(tmp_path, {name: [f for f, _ in cls._fields_] for name, cls in structs.items()})
     for name, cls in structs.items():
         assert ctypes.sizeof(cls) == c[name]["__size__"], (which, name, ctypes.sizeof(cls), c[name]["__size__"])

@@ -60,14 +60,40 @@ def rank_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def gen_batches(kind: str, count: int, seed0: int = 1000):
+def _gen_one(args):
     from paper_2310_03567_b200 import synth
 
-    gen = synth.GENERATORS[kind]
+    kind, seed = args
     if kind == "mesh":
-        scene = synth.mesh_scene()
-        return [gen(BATCH, seed0 + i, scene) for i in range(count)]
-    return [gen(BATCH, seed0 + i) for i in range(count)]
+        return synth.gen_mesh(BATCH, seed, synth.mesh_scene())
+    return synth.GENERATORS[kind](BATCH, seed)
+
+
+def gen_batches(kind: str, count: int, seed0: int = 1000):
+    """Batches seed0 .. seed0+count-1 of the stream (deterministic per seed);
+    generated on a process pool when there are many (the full 100-batch
+    stream in a few seconds)."""
+    jobs = [(kind, seed0 + i) for i in range(count)]
+    if count <= 8:
+        return [_gen_one(j) for j in jobs]
+    import concurrent.futures as cf
+    import multiprocessing as mp
+
+    workers = max(1, min(16, (os.cpu_count() or 2) - 1))
+    with cf.ProcessPoolExecutor(workers, mp_context=mp.get_context("fork")) as ex:
+        return list(ex.map(_gen_one, jobs, chunksize=2))
+
+
+FULL_STREAM = 100  # BASELINE config 2: 100 x 1M-point batches
+
+
+def bench_config(args) -> dict:
+    """The `config` both arms print (identical dicts: the driver compares them)."""
+    w, k = args.warmup, args.steps
+    return {"workload": f"{CONFIGS[args.config][1]}; timed: stream batches {w}..{w + k - 1} ({k} x 1M points) "
+                        f"after {w} untimed warm-up batches (the tree holds {w + k}M points at the end)",
+            "batch_points": BATCH, "tree": PARAMS, "timed_batches": [w, w + k],
+            "l2": "inputs larger than L2: every step inserts a distinct 16 MB batch"}
 
 
 def morton_sorted(xyz, rgba, bits: int = 10):
@@ -221,15 +247,14 @@ def run_multi(args, rank, world, local_rank):
             "metric": METRIC, "value": round(value, 2), "unit": "Mpts/s", "n_gpus": world, "steps": args.steps,
             "warmup": step, "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic",
-            "config": {"workload": CONFIGS[args.config][1] + f"; global batch {world} x 1M striped over ranks",
-                       "batch_points": BATCH * world, "tree": PARAMS,
+            "config": bench_config(args),
+            "notes": {"global_batch": f"{world} x 1M points striped over ranks per step (weak scaling)",
                        "parallelism": f"octant-prefix partition depth {plan.depth} x{world}, "
                                       + (f"{backend.upper()} all-to-all routing (peer windows unavailable: "
                                          f"{ins.no_peers})" if ins.no_peers else
                                          f"peer-memory routing (bucket scatter into CUDA IPC windows), "
                                          f"{backend.upper()} barriers"),
-                       "imbalance_max_over_mean": round(partition.imbalance(plan), 3),
-                       "l2": "inputs larger than L2: distinct 16 MB stripes per step"},
+                       "imbalance_max_over_mean": round(partition.imbalance(plan), 3)},
             "e2e": {"value": round(pts / (t_e2e * 1e-3) / 1e6, 2), "unit": "Mpts/s",
                     "h2d_bytes_per_step": h2d // max(args.steps, 1),
                     "d2h_bytes_per_step": timed.d2h // max(args.steps, 1),
@@ -264,7 +289,10 @@ def run_ours(args, rank, world, local_rank):
     dist = None
     kind = CONFIGS[args.config][0]
     total = args.warmup + args.steps
-    batches = gen_batches(kind, total)
+    n_gen = max(total, FULL_STREAM) if not args.no_rows else total
+    batches = gen_batches(kind, n_gen)
+    full_stream = batches if len(batches) >= FULL_STREAM else None
+    batches = batches[:total]
     if args.presort:  # experiment only: z-ordered input batches (changes the workload)
         batches = [morton_sorted(x, c) for x, c in batches]
     n_points = [len(c) for _, c in batches]
@@ -336,6 +364,8 @@ def run_ours(args, rank, world, local_rank):
     _, per_prof, _, phases, _, _ = timed_stream(dev_b, profile=True, keep=kept)
     rows = secondary_rows(args, kept[0], kept[1], dev_b, dev) if not args.no_rows else None
     kept[0].close()
+    if rows is not None and full_stream is not None:
+        rows["full_stream"] = full_stream_row(args, full_stream[:FULL_STREAM], dev, arena_bytes)
 
     timed_pts = sum(n_points[args.warmup:])
     t_max = ms
@@ -360,20 +390,16 @@ def run_ours(args, rank, world, local_rank):
     roof["peak"] = peak
     roof["peak_source"] = peak_kind
     roof["frac"] = round(roof["achieved"] / peak, 4) if roof.get("achieved") else None
-    traffic = load_traffic(roof.get("kernel"))
-    if traffic is not None:
-        roof["traffic"] = traffic
+    roof["traffic"], roof["traffic_source"] = load_traffic(roof.get("kernel"), args)
     cpu = cpu_baseline(args, kind) if not args.no_cpu else None
     srt = sorted(per)
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "Mpts/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic",
-        "config": {"workload": CONFIGS[args.config][1], "batch_points": BATCH, "tree": PARAMS,
-                   "parallelism": f"octant-prefix partition x{world}" if world > 1 else "single tree",
-                   "l2": "inputs larger than L2: every step inserts a distinct 16 MB batch; "
-                         f"{total} batches ({total * 16} MB) resident",
-                   "final_nodes": info["nodes"], "voxels_created": info["voxels_created"]},
+        "config": bench_config(args),
+        "notes": {"parallelism": "single tree", "resident_batches_mb": total * 16, "final_nodes": info["nodes"],
+                  "voxels_created": info["voxels_created"]},
         "batch_ms": {"avg": round(statistics.mean(per), 4), "p50": round(srt[len(srt) // 2], 4),
                      "p99": round(srt[min(len(srt) - 1, int(0.99 * len(srt)))], 4), "max": round(srt[-1], 4)},
         "e2e": {"value": round(e2e, 2), "unit": "Mpts/s", "h2d_bytes_per_step": h2d // max(args.steps, 1),
@@ -388,6 +414,47 @@ def run_ours(args, rank, world, local_rank):
     if dist is not None:
         dist.destroy_process_group()
     return line
+
+
+def full_stream_row(args, batches, dev, arena_bytes) -> dict:
+    """The whole 100-batch config stream into a fresh tree (BASELINE config
+    2's 100M points for the terrain config), device-resident, each batch's
+    device time from its own CUDA events: avg / p50 / p99 / max ms per 1M
+    batch and M points/s over the whole stream."""
+    import torch
+
+    from paper_2310_03567_b200 import insert_batch, wait_settled
+
+    dev_b = [(torch.from_numpy(x).cuda(), torch.from_numpy(c.view(np.int32)).cuda()) for x, c in batches]
+    tree, state = new_tree(dev, arena_bytes)
+    torch.cuda.synchronize()
+    per = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for x, c in dev_b:
+        insert_batch(tree, x, c, state)
+        b = state._bstats
+        if b.device_ms_prev >= 0 and per and per[-1] < 0:
+            per[-1] = float(b.device_ms_prev)
+        per.append(float(b.device_ms))
+    last = wait_settled(tree)
+    if per[-1] < 0:
+        per[-1] = last
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    srt = sorted(per)
+    pts = sum(int(c.numel()) for _, c in dev_b)
+    out = {"batches": len(dev_b), "points": pts, "mpts_per_s": round(pts / (ms * 1e-3) / 1e6, 1),
+           "stream_ms": round(ms, 3),
+           "batch_ms": {"avg": round(statistics.mean(per), 4), "p50": round(srt[len(srt) // 2], 4),
+                        "p99": round(srt[min(len(srt) - 1, int(0.99 * len(srt)))], 4), "max": round(srt[-1], 4)},
+           "worst_batch": int(np.argmax(per)), "batches_over_1ms": int(sum(p > 1.0 for p in per)),
+           "final_nodes": tree.num_nodes, "voxels_created": state.stats.voxels_created,
+           "note": "per-batch device time from CUDA events on the tree stream (inputs resident in HBM); "
+                   "stream_ms = events around the whole stream"}
+    tree.close()
+    return out
 
 
 def secondary_rows(args, tree, state, dev_b, dev) -> dict:
@@ -566,15 +633,21 @@ def cas_peak():
         return None
 
 
-def load_traffic(kernel: str | None):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu
-    capture (profiles/ncu_traffic.json, written by tools/ncu_summary.py)."""
+def load_traffic(kernel: str | None, args):
+    """DRAM bytes per launch of the dominant kernel over THIS run's timed
+    batch range, from the committed ncu capture of the same batches
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.sh); null when no
+    capture covers this config and range."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            d = json.load(f)
-        return d.get(kernel)
+            caps = json.load(f)["captures"]
     except Exception:
-        return None
+        return None, "no committed ncu capture"
+    want = [args.warmup, args.warmup + args.steps]
+    for c in caps:
+        if c.get("config") == args.config and c.get("batches") == want and kernel in c.get("per_launch_bytes", {}):
+            return c["per_launch_bytes"][kernel], f"ncu over the same batches: {c['command']} ({c['when']})"
+    return None, f"no committed ncu capture of {args.config} batches {want[0]}..{want[1] - 1}"
 
 
 def cpu_baseline(args, kind) -> dict:
@@ -620,7 +693,7 @@ def run_reference(args, rank, world):
         "metric": METRIC, "value": round(value, 3), "unit": "Mpts/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic", "impl": "reference",
-        "config": {"workload": CONFIGS[args.config][1], "batch_points": BATCH, "tree": PARAMS},
+        "config": bench_config(args),
         "cpu_baseline": {"value": round(value, 3), "unit": "Mpts/s", "cores": 1, "kind": "port",
                          "sample": f"{args.steps} timed 1M-point batches after {args.warmup} warm-up batches",
                          "host_nproc": os.cpu_count()},

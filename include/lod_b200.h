@@ -173,6 +173,41 @@ int lod_read_nodes(LodTree *tree, int64_t n, int32_t *parent, uint8_t *octant, i
 int lod_read_pool(LodTree *tree, int64_t n, int32_t *next, int64_t *payload_off,
                   int32_t *occupied, int32_t *free_list, int64_t n_free);
 
+/* Structural edits outside an update cycle (the reference's Octree / ChunkPool
+ * mutators, used by its unit tests and by callers that build trees by hand):
+ *   lod_split_node        Octree.split (octree.py:222-264) after the caller
+ *                         gathered the leaf's samples (lod_gather) into its
+ *                         spill buffer: the chunk chain goes onto the free
+ *                         stack in walk order, the node turns inner with a
+ *                         zeroed 64-aligned grid (LOD_E_OUT_OF_ARENA past
+ *                         capacity) and gets 8 children, ids *first_child + o
+ *                         in octant order; LOD_E_ARG unless nid is a leaf
+ *                         below max depth;
+ *   lod_append_chunk      Octree.append_chunk + ChunkPool.acquire
+ *                         (octree.py:328-337, store.py:110-123): LIFO free
+ *                         stack first, else a 16-aligned arena cut;
+ *   lod_grid_test_and_set Octree.grid_test_and_set (octree.py:281-288).
+ * Host edits of the mirrored columns are written back with lod_write_nodes /
+ * lod_write_pool / lod_write_arena (same layouts as the readers; NULL skips a
+ * column); the device-only indexes (descent records, chunk directory, chunk
+ * owners) are rebuilt from the written columns. */
+int lod_split_node(LodTree *tree, int64_t nid, int32_t *first_child);
+int lod_append_chunk(LodTree *tree, int64_t nid, int32_t *cid);
+int lod_grid_test_and_set(LodTree *tree, int64_t nid, int64_t cell, int32_t *was_clear);
+int lod_write_nodes(LodTree *tree, int64_t n, const int32_t *parent, const uint8_t *octant, const int32_t *level,
+                    const int32_t *children, const uint8_t *inner, const uint8_t *final_, const int64_t *count,
+                    const int64_t *pending, const int32_t *chunk_head, const int32_t *chunk_tail,
+                    const int32_t *chunk_count, const int64_t *grid_off, const double *bmin);
+int lod_write_pool(LodTree *tree, int64_t n, const int32_t *next, const int64_t *payload_off, const int32_t *occupied);
+int lod_write_arena(LodTree *tree, uint64_t off, uint64_t size, const void *src);
+
+/* The device-only chunk directory (inspection / tests): per node its region
+ * offset and capacity, the entries [0, *dir_top) (node n's chunk ids in list
+ * order are cdir[dir_off[n] + i], i < chunk_count[n]).  cdir may be NULL to
+ * read *dir_top only; cdir_len is its capacity in entries. */
+int lod_read_directory(LodTree *tree, int64_t n, int64_t *dir_off, int32_t *dir_cap, int32_t *cdir,
+                       int64_t cdir_len, uint64_t *dir_top);
+
 /* Octree.gather_samples (octree.py:298-326): samples [start, count) of node nid
  * in storage order.  xyz is (k,3) f32, rgba (k,) u32, k = count - start. */
 int lod_gather(LodTree *tree, int64_t nid, int64_t start, float *xyz, uint32_t *rgba);

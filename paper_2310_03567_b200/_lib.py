@@ -125,6 +125,13 @@ SIGNATURES = {
     "lod_read_nodes": (ctypes.c_int, [_P, _I64] + [_P] * 13),
     "lod_read_pool": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _I64]),
     "lod_gather": (ctypes.c_int, [_P, _I64, _I64, _P, _P]),
+    "lod_read_directory": (ctypes.c_int, [_P, _I64, _P, _P, _P, _I64, ctypes.POINTER(ctypes.c_uint64)]),
+    "lod_split_node": (ctypes.c_int, [_P, _I64, ctypes.POINTER(ctypes.c_int32)]),
+    "lod_append_chunk": (ctypes.c_int, [_P, _I64, ctypes.POINTER(ctypes.c_int32)]),
+    "lod_grid_test_and_set": (ctypes.c_int, [_P, _I64, _I64, ctypes.POINTER(ctypes.c_int32)]),
+    "lod_write_nodes": (ctypes.c_int, [_P, _I64] + [_P] * 13),
+    "lod_write_pool": (ctypes.c_int, [_P, _I64, _P, _P, _P]),
+    "lod_write_arena": (ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P]),
     "lod_dump_records": (ctypes.c_int, [_P, _I64, _P, _P]),
     "lod_delta_info": (ctypes.c_int, [_P, ctypes.POINTER(LodDeltaInfo)]),
     "lod_read_delta": (ctypes.c_int, [_P] + [_P] * 9),

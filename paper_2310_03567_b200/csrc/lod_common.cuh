@@ -134,6 +134,11 @@ struct NodeCols {
   // device-only descent record: {first child id (children are 8 consecutive
   // ids) or -1 for a leaf, grid offset / 64}; 8 bytes per node, L1-resident
   int2 *desc;
+  // device-only chunk directory: the node's chunk ids in list order are
+  // PoolCols::cdir[dir_off[n] + i], i < chunk_count[n] (region of dir_cap[n]
+  // entries; relocated with doubling when it fills, kept across a split)
+  long long *dir_off;
+  int32_t *dir_cap;
 };
 
 struct PoolCols {
@@ -141,8 +146,9 @@ struct PoolCols {
   long long *payload_off;
   int32_t *occupied;
   int32_t *owner;  // node owning the chunk, -1 when free (render work list)
-  int32_t *cidx;   // position of the chunk in its owner's list (parallel spill gather)
+  int32_t *cidx;   // position of the chunk in its owner's list
   int32_t *free_stack;
+  int32_t *cdir;   // chunk directory (NodeCols::dir_off / dir_cap): spill gather and render work lists
 };
 
 struct Geo {

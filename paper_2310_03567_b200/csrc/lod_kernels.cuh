@@ -68,7 +68,30 @@ struct Ctrl {
   long long redescend;        // k_decide: points in the splitting nodes (stored + pending) -- the only
                               // points the next count pass re-descends, each claiming at most one cell
   long long n_wins;           // k_resolve_list: entries of the win list (burst path)
+  unsigned long long dir_top;  // chunk directory entries handed out (bump pointer)
+  unsigned long long pad2;
 };
+
+// Chunk directory of node n after `need` chunks were appended to its list
+// (chunk_count already includes them): relocate the region with doubling when
+// it is full (one thread per node), then record the new chunk ids, `acq(t)`
+// for t < need, at list positions chunk_count - need + t.
+template <typename Acq>
+__device__ __forceinline__ void dir_append(const NodeCols &nd, const PoolCols &pool, unsigned long long *dir_top,
+                                           int n, long long need, Acq acq) {
+  if (need <= 0) return;
+  const long long cc1 = nd.chunk_count[n], cc0 = cc1 - need;
+  long long off = nd.dir_off[n];
+  if (cc1 > (long long)nd.dir_cap[n]) {
+    const long long cap = cc1 * 2 > 4 ? cc1 * 2 : 4;
+    const long long noff = (long long)atomicAdd(dir_top, (unsigned long long)cap);
+    for (long long i = 0; i < cc0; ++i) pool.cdir[noff + i] = pool.cdir[off + i];
+    off = noff;
+    nd.dir_off[n] = noff;
+    nd.dir_cap[n] = (int32_t)cap;
+  }
+  for (long long t = 0; t < need; ++t) pool.cdir[off + cc0 + t] = acq(t);
+}
 
 __device__ __forceinline__ void set_error(Ctrl *c, int code) { atomicCAS(&c->error, 0, code); }
 
@@ -278,7 +301,14 @@ __global__ void __launch_bounds__(256, LOD_COUNT_MINB)
           const int cur = nid;
           nid = d.x + octant_step(x, y, z, bx, by, bz, s, inv_s);
           d = __ldg(nd.desc + nid);
-          if (!(w & (1u << (cell & 31)))) hash_claim(h, stg, claim_key(cur, cell), v, col, ctrl);
+          if (!(w & (1u << (cell & 31)))) {
+            // lanes of a warp are consecutive indices: the lowest lane on a
+            // (node, cell) is its lowest claimant, the others need not
+            // touch the table (sorted input puts many lanes on one cell)
+            const unsigned long long key = claim_key(cur, cell);
+            const unsigned peers = __match_any_sync(__activemask(), key);
+            if (lane_id() == (unsigned)(__ffs(peers) - 1)) hash_claim(h, stg, key, v, col, ctrl);
+          }
         } while (d.x >= 0);
         node_of[j] = nid;
         if (!nd.final_[nid]) leaf = nid;
@@ -429,48 +459,31 @@ __global__ void __launch_bounds__(kDecideBlock)
   if (tid == 0) ctrl->n_touched = 0;  // phase 6: the touched list restarts next iteration
 }
 
-// Octree.split, part 1 (octree.py:231-237, store.py:125-143), in parallel over
-// the chunk table: every chunk owned by a splitting node copies its records to
-// the node's spill segment (chunk position cidx = storage order) and pushes
-// itself onto the free stack at its walk-order slot.  One warp per chunk.
-// The chunks owned by splitting nodes, listed in one coalesced pass over the
-// pool (a large tree holds millions of chunks; a split touches a few
-// thousand): thread per chunk, warp-aggregated appends, order irrelevant.
-__global__ void k_split_chunk_list(PoolCols pool, long long nchunks, const int32_t *__restrict__ srank,
-                                   int32_t *__restrict__ list, Ctrl *ctrl) { lod::pdl_wait();
-  for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < nchunks; i0 += gstride()) {
-    const long long cid = i0 + threadIdx.x;
-    bool hit = false;
-    if (cid < nchunks) {
-      const int owner = pool.owner[cid];
-      hit = owner >= 0 && srank[owner] >= 0;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, hit);
-    if (!m) continue;
-    unsigned base = 0;
-    if (lane_id() == 0) base = atomicAdd(&ctrl->n_xchunks, (unsigned)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (hit) list[base + __popc(m & lanemask_lt())] = (int32_t)cid;
-  }
-}
-
-// One warp per listed chunk: copy its records to the node's spill segment
-// (chunk position cidx = storage order) and push the chunk onto the free
-// stack at its walk-order slot.
-__global__ void k_exec_chunks(PoolCols pool, Geo geo, const uint8_t *__restrict__ arena,
-                              const int32_t *__restrict__ list, const int32_t *__restrict__ srank,
+// Octree.split, part 1 (octree.py:231-237, store.py:125-143): the chunks of
+// the splitting nodes, read from their directories -- the work list is the
+// exclusive scan of their chunk counts k_decide already made (chunk_off), so
+// a split touches only its own chunks, never the pool.  One warp per chunk:
+// copy its records to the node's spill segment (list position = storage
+// order) and push the chunk onto the free stack at its walk-order slot.
+__global__ void k_exec_chunks(NodeCols nd, PoolCols pool, Geo geo, const uint8_t *__restrict__ arena,
+                              const int32_t *__restrict__ split_list, long long ns,
                               const long long *__restrict__ spill_off, const long long *__restrict__ chunk_off,
-                              float4 *spill_buf, int32_t *spill_node_of, const Ctrl *ctrl) { lod::pdl_wait();
+                              long long nchunks, float4 *spill_buf, int32_t *spill_node_of, const Ctrl *ctrl) {
+  lod::pdl_wait();
   const long long warp = gtid() >> 5, nwarps = gstride() >> 5;
   const int lane = threadIdx.x & 31;
-  const long long nlist = (long long)ctrl->n_xchunks;
-  for (long long li = warp; li < nlist; li += nwarps) {
-    const int cid = list[li];
-    const int owner = pool.owner[cid];
-    const int r = srank[owner];
-    const int ci = pool.cidx[cid];
+  for (long long q = warp; q < nchunks; q += nwarps) {
+    long long lo = 0, hi = ns - 1;  // last split rank whose chunks start at or before q
+    while (lo < hi) {
+      const long long mid = (lo + hi + 1) >> 1;
+      if (chunk_off[mid] <= q) lo = mid;
+      else hi = mid - 1;
+    }
+    const long long r = lo, ci = q - chunk_off[r];
+    const int owner = split_list[r];
+    const int cid = pool.cdir[nd.dir_off[owner] + ci];
     const int occ = pool.occupied[cid];
-    const long long sp = ctrl->plan_spill0 + spill_off[r] + (long long)ci * geo.C;
+    const long long sp = ctrl->plan_spill0 + spill_off[r] + ci * geo.C;
     const float4 *src = reinterpret_cast<const float4 *>(arena + pool.payload_off[cid]);
     for (int k = lane; k < occ; k += 32) {
       spill_buf[sp + k] = src[k];
@@ -513,6 +526,8 @@ __global__ void k_exec_nodes(NodeCols nd, Geo geo, const int32_t *__restrict__ s
     nd.chunk_count[c] = 0;
     nd.grid_off[c] = -1;
     nd.desc[c] = make_int2(-1, 0);
+    nd.dir_off[c] = 0;
+    nd.dir_cap[c] = 0;
     nd.bmin[3 * c + 0] = nd.bmin[3 * nid + 0] + ((o & 1) ? half : 0.0);
     nd.bmin[3 * c + 1] = nd.bmin[3 * nid + 1] + ((o & 2) ? half : 0.0);
     nd.bmin[3 * c + 2] = nd.bmin[3 * nid + 2] + ((o & 4) ? half : 0.0);
@@ -857,8 +872,11 @@ __global__ void k_store(StoreSink sink, const uint32_t *__restrict__ skeys, cons
 }
 
 // clear_marks (_kernels.py:280-287) + count advance: pending drains into count.
-__global__ void k_epilogue(NodeCols nd, const int32_t *__restrict__ seg_node, const long long *__restrict__ seg_start,
-                           const Ctrl *ctrl, uint32_t *__restrict__ ghist, const int *guard) { lod::pdl_wait();
+// + the chunk directory of every node that got chunks (dir_append).
+__global__ void k_epilogue(NodeCols nd, PoolCols pool, const int32_t *__restrict__ seg_node,
+                           const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
+                           const U64x2 *__restrict__ plan_ex, Ctrl *ctrl, uint32_t *__restrict__ ghist,
+                           const int *guard) { lod::pdl_wait();
   if (guard && *guard) return;
   // the sort is the last reader of the digit totals: zeroed for the next cycle
   for (long long i = gtid(); i < kMaxPassesHist; i += gstride()) ghist[i] = 0;
@@ -869,6 +887,9 @@ __global__ void k_epilogue(NodeCols nd, const int32_t *__restrict__ seg_node, co
     nd.count[n] += seg_start[d + 1] - seg_start[d];
     nd.pending[n] = 0;
     nd.final_[n] = 0;
+    const long long A0 = (long long)plan_ex[d].a;
+    dir_append(nd, pool, &ctrl->dir_top, n, (long long)plan[d].a,
+               [&](long long t) { return acq_cid(pool, ctrl, A0 + t); });
   }
 }
 

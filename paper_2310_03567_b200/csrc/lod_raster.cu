@@ -2,10 +2,10 @@
 //
 // Projection, depth and packing restate _kernels.py:290-372 exactly (f64, no
 // FMA, IEEE division, float32 depth bits << 32 | rgba, min-combine).  The
-// per-node chunk walk of rasterize_nodes becomes a flat pass over the chunk
-// table: each warp takes one chunk, skips it unless its owning node is in the
-// visible set, and splats its occupied records with an early depth test before
-// the 64-bit atomicMin.  Chunk ownership is maintained by the update path.
+// per-node chunk walk of rasterize_nodes becomes a work list over the listed
+// nodes' chunks (each node's chunk directory, maintained by the update path),
+// cut into pieces of kPiece records, one warp per piece, with an early depth
+// test before the 64-bit atomicMin: O(visible samples).
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -23,9 +23,8 @@ cudaStream_t lod_tree_stream(LodTree *t);
 int lod_tree_device(LodTree *t);
 const uint8_t *lod_tree_arena(LodTree *t);
 PoolCols lod_tree_pool(LodTree *t);
-long long lod_tree_allocated(LodTree *t);
 long long lod_tree_num_nodes(LodTree *t);
-uint32_t *lod_tree_visflag(LodTree *t);
+int lod_tree_ensure_woff(LodTree *t, long long n, long long **p);
 int lod_tree_ensure_vislist(LodTree *t, long long n, int32_t **p);
 int lod_tree_ensure_fb(LodTree *t, long long n, unsigned long long **p);
 unsigned long long *lod_tree_counter(LodTree *t);
@@ -66,35 +65,71 @@ __global__ void k_raster_points(const float *__restrict__ xyz, const uint32_t *_
           __ldg(rgba + i), fb);
 }
 
-// One warp per chunk; visflag holds each node's multiplicity in the visible
-// list (samples_drawn counts every listed occurrence, _kernels.py:307-317).
-__global__ void k_raster_chunks(PoolCols pool, const uint8_t *__restrict__ arena, long long nchunks,
-                                const uint32_t *__restrict__ visflag, Cam cam, unsigned long long *fb,
-                                long long w, long long h, unsigned long long *samples) { lod::pdl_wait();
+// rasterize_nodes (_kernels.py:290-339) over a work list that is O(visible):
+// every listed node contributes chunk_count x ppc pieces of at most kPiece
+// records (ppc = ceil(C / kPiece)), addressed through the node's chunk
+// directory -- so the cost follows the visible samples, not the pool size or
+// the chunk capacity (acceptance C9: render time flat across C).  `woff` is
+// the exclusive scan of the entries' piece counts (k_select / k_vis_plan),
+// plan[0] = samples drawn (every listed occurrence, _kernels.py:307-317),
+// plan[2] = pieces.  One warp per piece.
+constexpr int kPiece = 256;
+__global__ void __launch_bounds__(256)
+    k_raster_work(NodeCols nd, PoolCols pool, const uint8_t *__restrict__ arena, const int32_t *__restrict__ list,
+                  const long long *__restrict__ woff, const unsigned long long *__restrict__ plan, int ppc, Cam cam,
+                  unsigned long long *fb, long long w, long long h) { lod::pdl_wait();
   const long long warp = gtid() >> 5, nwarps = gstride() >> 5;
   const int lane = threadIdx.x & 31;
-  unsigned long long drawn = 0;
-  for (long long cid = warp; cid < nchunks; cid += nwarps) {
-    const int owner = pool.owner[cid];
-    if (owner < 0) continue;
-    const uint32_t mult = visflag[owner];
-    if (!mult) continue;
-    const int occ = pool.occupied[cid];
-    drawn += (unsigned long long)occ * mult;
+  const long long n = (long long)plan[1], pieces = (long long)plan[2];
+  for (long long p = warp; p < pieces; p += nwarps) {
+    long long lo = 0, hi = n - 1;  // last entry whose pieces start at or before p
+    while (lo < hi) {
+      const long long mid = (lo + hi + 1) >> 1;
+      if (woff[mid] <= p) lo = mid;
+      else hi = mid - 1;
+    }
+    const int nid = list[lo];
+    const long long k = p - woff[lo], ci = k / ppc, r0 = (k % ppc) * kPiece;
+    const int cid = pool.cdir[nd.dir_off[nid] + ci];
+    const long long r1 = min((long long)pool.occupied[cid], r0 + kPiece);
     const float4 *rec = reinterpret_cast<const float4 *>(arena + pool.payload_off[cid]);
-    for (int r = lane; r < occ; r += 32) {
+    for (long long r = r0 + lane; r < r1; r += 32) {
       const float4 v = __ldg(rec + r);
       splat(cam, w, h, (double)v.x, (double)v.y, (double)v.z, __float_as_uint(v.w), fb);
     }
   }
-  if (lane == 0 && drawn) atomicAdd(samples, drawn);
 }
 
-__global__ void k_set_vis(const int32_t *__restrict__ vis, long long n, uint32_t *visflag, int add) { lod::pdl_wait();
-  for (long long i = gtid(); i < n; i += gstride()) {
-    if (add) atomicAdd(visflag + vis[i], 1u);
-    else visflag[vis[i]] = 0;
+// Work-list plan of an explicit node list (lod_rasterize): piece offsets,
+// samples, count.  One CTA.
+constexpr int kPlanBlock = 1024;
+__device__ __forceinline__ void plan_entries(const NodeCols &nd, const int32_t *list, long long n, int ppc,
+                                             long long *woff, unsigned long long *plan, U64x2 *sh) {
+  U64x2 carry = u64x2(0, 0);
+  for (long long base = 0; base < n; base += kPlanBlock) {
+    const long long i = base + threadIdx.x;
+    U64x2 v = u64x2(0, 0);
+    if (i < n) {
+      const int nid = list[i];
+      v = u64x2((unsigned long long)nd.chunk_count[nid] * (unsigned long long)ppc, (unsigned long long)nd.count[nid]);
+    }
+    U64x2 tot;
+    const U64x2 ex = block_exclusive_scan<U64x2, kPlanBlock>(v, sh, tot);
+    if (i < n) woff[i] = (long long)(ex.a + carry.a);
+    carry = carry + tot;
   }
+  if (threadIdx.x == 0) {
+    plan[0] = carry.b;
+    plan[1] = (unsigned long long)n;
+    plan[2] = carry.a;
+  }
+}
+
+__global__ void __launch_bounds__(kPlanBlock)
+    k_vis_plan(NodeCols nd, const int32_t *__restrict__ list, long long n, int ppc, long long *woff,
+               unsigned long long *plan) { lod::pdl_wait();
+  __shared__ U64x2 sh[kPlanBlock / 32 + 1];
+  plan_entries(nd, list, n, ppc, woff, plan, sh);
 }
 
 // ---------------------------------------------------------------- selection
@@ -160,12 +195,13 @@ __device__ __forceinline__ int sel_decide(const NodeCols &nd, const Geo &geo, co
 
 constexpr int kSelBlock = 1024;
 // Entries: nid >= 0 pending, -(nid + 1) final.  Result: the final list of
-// node ids in *out_list (one of the two buffers), its length in *nsel; with
-// `mark`, every selected node's visflag is set for the chunk rasterizer.
+// node ids in sel_out, and the splat's work list over them (plan_entries).
+static_assert(kSelBlock == kPlanBlock, "k_select plans the work list with the plan block size");
 __global__ void __launch_bounds__(kSelBlock)
     k_select(NodeCols nd, Geo geo, SelParams sp, int32_t *bufA, int32_t *bufB, int32_t *sel_out,
-             unsigned long long *nsel, uint32_t *visflag, int mark) { lod::pdl_wait();
+             unsigned long long *plan, long long *woff, int ppc) { lod::pdl_wait();
   __shared__ uint32_t sh[kSelBlock / 32 + 1];
+  __shared__ U64x2 sh64[kSelBlock / 32 + 1];
   int32_t *cur = bufA, *nxt = bufB;
   long long n = 1;
   if (!nd.inner[0] && nd.count[0] == 0) n = 0;  // a tree holding nothing selects nothing
@@ -203,23 +239,17 @@ __global__ void __launch_bounds__(kSelBlock)
     nxt = t;
     if (!more) break;
   }
-  for (long long i = threadIdx.x; i < n; i += kSelBlock) {
-    const int nid = -cur[i] - 1;
-    sel_out[i] = nid;
-    if (mark) visflag[nid] = 1;
-  }
-  if (threadIdx.x == 0) *nsel = (unsigned long long)n;
-}
-
-__global__ void k_clear_vis(const int32_t *__restrict__ sel, const unsigned long long *__restrict__ nsel,
-                            uint32_t *visflag) { lod::pdl_wait();
-  const long long n = (long long)*nsel;
-  for (long long i = gtid(); i < n; i += gstride()) visflag[sel[i]] = 0;
+  for (long long i = threadIdx.x; i < n; i += kSelBlock) sel_out[i] = -cur[i] - 1;
+  __syncthreads();
+  // the splat's work list over the selection (O(visible chunks))
+  plan_entries(nd, sel_out, n, ppc, woff, plan, reinterpret_cast<U64x2 *>(sh64));
 }
 
 __global__ void k_fill_u64(unsigned long long *p, long long n, unsigned long long v) { lod::pdl_wait();
   for (long long i = gtid(); i < n; i += gstride()) p[i] = v;
 }
+
+constexpr unsigned kRasterGrid = 148 * 8;  // 8 CTAs x 8 warps per SM, grid-stride over the pieces
 
 inline unsigned grid_for(long long n, int block = 256) {
   long long b = (n + block - 1) / block;
@@ -276,16 +306,18 @@ int lod_rasterize(LodTree *t, const int32_t *vis, int64_t nvis, const double *ca
   int32_t *dvis = nullptr;
   int rc = lod_tree_ensure_vislist(t, nvis, &dvis);
   if (rc) return rc;
+  long long *woff = nullptr;
+  if ((rc = lod_tree_ensure_woff(t, nvis, &woff))) return rc;
   if (nvis) CK(cudaMemcpyAsync(dvis, vis, nvis * 4, cudaMemcpyHostToDevice, st));
-  unsigned long long *cnt = lod_tree_counter(t);
-  CK(cudaMemsetAsync(cnt, 0, 8, st));
-  uint32_t *vf = lod_tree_visflag(t);
-  const long long nchunks = lod_tree_allocated(t);
+  unsigned long long *cnt = lod_tree_counter(t);  // [0] samples, [1] entries, [2] pieces
+  CK(cudaMemsetAsync(cnt, 0, 24, st));
+  const Geo geo = lod_tree_geo(t);
+  const int ppc = (int)((geo.C + kPiece - 1) / kPiece);
   if (nvis) {
-    lod::launch(k_set_vis, grid_for(nvis), 256, 0, st, dvis, nvis, vf, 1);
-    lod::launch(k_raster_chunks, grid_for(nchunks * 32), 256, 0, st, lod_tree_pool(t), lod_tree_arena(t), nchunks, vf, c,
-                                                             dfb, width, height, cnt);
-    lod::launch(k_set_vis, grid_for(nvis), 256, 0, st, dvis, nvis, vf, 0);
+    const NodeCols nd = lod_tree_nodes(t);
+    lod::launch(k_vis_plan, 1, kPlanBlock, 0, st, nd, dvis, (long long)nvis, ppc, woff, cnt);
+    lod::launch(k_raster_work, kRasterGrid, 256, 0, st, nd, lod_tree_pool(t), lod_tree_arena(t), dvis,
+                (const long long *)woff, (const unsigned long long *)cnt, ppc, c, dfb, width, height);
   }
   unsigned long long drawn = 0;
   CK(cudaMemcpyAsync(&drawn, cnt, 8, cudaMemcpyDeviceToHost, st));
@@ -312,9 +344,12 @@ static int render_impl(LodTree *t, const double *planes, const double *cam, doub
   int32_t *la = nullptr, *lb = nullptr;
   int rc = lod_tree_ensure_sel(t, nn, &la, &lb);
   if (rc) return rc;
-  unsigned long long *cnt = lod_tree_counter(t);  // [0] samples, [1] selected
-  CK(cudaMemsetAsync(cnt, 0, 16, st));
-  uint32_t *vf = lod_tree_visflag(t);
+  unsigned long long *cnt = lod_tree_counter(t);  // [0] samples, [1] selected, [2] pieces
+  CK(cudaMemsetAsync(cnt, 0, 24, st));
+  long long *woff = nullptr;
+  if ((rc = lod_tree_ensure_woff(t, nn, &woff))) return rc;
+  const Geo geo = lod_tree_geo(t);
+  const int ppc = (int)((geo.C + kPiece - 1) / kPiece);
   int32_t *sel = la;  // k_select decodes the final list into la[0, n) (same index as it reads)
   unsigned long long *dfb = reinterpret_cast<unsigned long long *>(fb);
   const long long npx = fb ? width * height : 0;
@@ -326,15 +361,13 @@ static int render_impl(LodTree *t, const double *planes, const double *cam, doub
     else
       CK(cudaMemcpyAsync(dfb, fb, npx * 8, cudaMemcpyHostToDevice, st));
   }
-  lod::launch(k_select, 1, kSelBlock, 0, st, lod_tree_nodes(t), lod_tree_geo(t), sp, la, lb, sel, cnt + 1, vf,
-              fb ? 1 : 0);
+  const NodeCols nd = lod_tree_nodes(t);
+  lod::launch(k_select, 1, kSelBlock, 0, st, nd, geo, sp, la, lb, sel, cnt, woff, ppc);
   if (fb) {
     Cam c;
     memcpy(c.c, cam, sizeof(c.c));
-    const long long nchunks = lod_tree_allocated(t);
-    lod::launch(k_raster_chunks, grid_for(nchunks * 32), 256, 0, st, lod_tree_pool(t), lod_tree_arena(t), nchunks, vf,
-                c, dfb, width, height, cnt);
-    lod::launch(k_clear_vis, grid_for(nn), 256, 0, st, sel, cnt + 1, vf);
+    lod::launch(k_raster_work, kRasterGrid, 256, 0, st, nd, lod_tree_pool(t), lod_tree_arena(t), (const int32_t *)sel,
+                (const long long *)woff, (const unsigned long long *)cnt, ppc, c, dfb, width, height);
   }
   unsigned long long h[2] = {0, 0};
   CK(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, st));

@@ -36,7 +36,7 @@ constexpr long long kSmallAllMax = 1 << 16;  // bound on [spill || batch] points
 struct SmallResult {
   long long n_spill, n_voxels, n_splits, iterations;
   long long num_nodes, splits_total, max_level, allocated_total, free_count, released_total;
-  unsigned long long arena_off;
+  unsigned long long arena_off, dir_top;
   long long device_ns;
   int error;
   unsigned seq;
@@ -282,6 +282,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_cycle(SmallArgs a) {
         ++ci;
       }
     }
+    __syncthreads();  // the gather reads the split nodes' chunk lists, which part 2 resets
     // Octree.split part 2 (octree.py:238-264): the node turns inner with a
     // zeroed grid and gets 8 children with bmin = base + half (f64)
     for (long long t = tid; t < 8ll * S; t += kSmallBlock) {
@@ -304,6 +305,8 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_cycle(SmallArgs a) {
       nd.chunk_count[c] = 0;
       nd.grid_off[c] = -1;
       nd.desc[c] = make_int2(-1, 0);
+      nd.dir_off[c] = 0;
+      nd.dir_cap[c] = 0;
       nd.bmin[3 * c + 0] = nd.bmin[3 * nid + 0] + ((o & 1) ? half : 0.0);
       nd.bmin[3 * c + 1] = nd.bmin[3 * nid + 1] + ((o & 2) ? half : 0.0);
       nd.bmin[3 * c + 2] = nd.bmin[3 * nid + 2] + ((o & 4) ? half : 0.0);
@@ -556,7 +559,14 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_cycle(SmallArgs a) {
   }
   for (int d = tid; d < K; d += kSmallBlock) {
     const int nid = a.touched[d];
-    if (!s_err) nd.count[nid] += nd.inner[nid] ? a.nnew[nid] : (long long)nd.pending[nid];
+    if (!s_err) {
+      nd.count[nid] += nd.inner[nid] ? a.nnew[nid] : (long long)nd.pending[nid];
+      const long long F = s_F, A = s_A, A0 = a.pl[3 * d + 1];
+      dir_append(nd, pool, &a.ctrl->dir_top, nid, a.pl[3 * d], [&](long long t) {
+        const long long q = A0 + t;
+        return q < F ? pool.free_stack[F - 1 - q] : (int)(A + (q - F));
+      });
+    }
     nd.pending[nid] = 0;
     nd.final_[nid] = 0;
     a.nnew[nid] = 0;
@@ -585,6 +595,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_cycle(SmallArgs a) {
     r->free_count = s_free;
     r->released_total = s_rel;
     r->arena_off = s_arena;
+    r->dir_top = c->dir_top;
     r->device_ns = dt;
     r->error = s_err;
     if (a.async_call) {

@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <vector>
 
@@ -93,6 +94,8 @@ __global__ void k_init_root(NodeCols nd, double b0, double b1, double b2) { lod:
   nd.chunk_tail[0] = LOD_NO_CHUNK;
   nd.chunk_count[0] = 0;
   nd.grid_off[0] = -1;
+  nd.dir_off[0] = 0;
+  nd.dir_cap[0] = 0;
   nd.bmin[0] = b0;
   nd.bmin[1] = b1;
   nd.bmin[2] = b2;
@@ -162,7 +165,7 @@ struct LodTree {
   unsigned *h_seq_dev = nullptr;
   unsigned seq = 0;
   // expansion scratch
-  DBuf<int32_t> split_list, node_b, node_all, xlist;  // xlist: chunks of splitting nodes  // node_b: batch points' node cache; node_all: spilled points'
+  DBuf<int32_t> split_list, node_b, node_all;  // node_b: batch points' node cache; node_all: spilled points'
   DBuf<uint32_t> bitmap;  // split flags over node ids (k_decide_mark -> k_decide)
   DBuf<long long> scnt, schk, spill_off, chunk_off;
   DBuf<float4> spill;
@@ -194,7 +197,7 @@ struct LodTree {
   DBuf<float4> gbuf;
   DBuf<int32_t> gnodes;
   DBuf<long long> goff, gstart;
-  DBuf<uint32_t> visflag;
+  DBuf<long long> woff;  // render work list: piece offsets per listed node
   DBuf<int32_t> vislist;
   DBuf<unsigned long long> fb;
   DBuf<unsigned long long> counter;
@@ -222,6 +225,7 @@ struct LodTree {
                             // (inputs resident, settled) pairs, alternating between calls
   int ev_slot = 0;          // pair of the last call
   bool tail_pending = false;  // the last call returned before its sort + store finished
+  DBuf<int32_t> cdir;  // chunk directory entries (pool.cdir)
   // host copies of counters (authoritative after every call)
   long long num_nodes = 1;
   long long d2h_bytes = 0;  // control-block readbacks since the last reset
@@ -239,7 +243,7 @@ struct LodTree {
   long long sm_unfolded = 0;  // asynchronous small cycles not yet reported by lod_tree_settle
   // upper bounds of the counters while asynchronous small cycles are queued
   // (exact whenever sm_queued == 0)
-  long long ub_nodes = 1, ub_alloc = 0;
+  long long ub_nodes = 1, ub_alloc = 0, ub_dir = 0;
   unsigned long long ub_arena = 0;
   long long ingested = 0;  // points inserted so far (bounds the spill of a cycle)
 };
@@ -366,9 +370,12 @@ static int sync_ctrl(LodTree *t) {
     t->d2h_bytes += (long long)sizeof(Ctrl);
     CK(cudaMemcpyAsync(t->h_ctrl, t->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, t->st));
     CK(cudaStreamSynchronize(t->st));
-    return LOD_OK;
+  } else {
+    RK(wait_ctrl(t, publish_ctrl(t)));
   }
-  return wait_ctrl(t, publish_ctrl(t));
+  // published behind everything queued: the directory's bump pointer is exact
+  t->ub_dir = (long long)t->h_ctrl->dir_top;
+  return LOD_OK;
 }
 
 // Queue a publication of the control block on the tree stream (no wait).
@@ -452,6 +459,8 @@ static int ensure_nodes(LodTree *t, long long want, long long live) {
   RK(grow_col(t->nd.grid_off, t->ncap, nc, live, st));
   RK(grow_col(t->nd.bmin, t->ncap * 3, nc * 3, live * 3, st));
   RK(grow_col(t->nd.desc, t->ncap, nc, live, st));
+  RK(grow_col(t->nd.dir_off, t->ncap, nc, live, st));
+  RK(grow_col(t->nd.dir_cap, t->ncap, nc, live, st));
   // node-indexed scratch
   long long words = (nc + 31) / 32 + 1;
   long long oldw = t->bitmap.cap;
@@ -466,9 +475,6 @@ static int ensure_nodes(LodTree *t, long long want, long long live) {
   long long olds = t->srank.cap;
   RK(t->srank.ensure(nc, st, olds));
   if (t->srank.cap > olds) CK(cudaMemsetAsync(t->srank.p + olds, 0xFF, (size_t)(t->srank.cap - olds) * 4, st));
-  long long oldv = t->visflag.cap;
-  RK(t->visflag.ensure(nc, st, oldv));
-  if (t->visflag.cap > oldv) CK(cudaMemsetAsync(t->visflag.p + oldv, 0, (size_t)(t->visflag.cap - oldv) * 4, st));
   long long oldnn = t->sm_nnew.cap;  // zero between cycles
   RK(t->sm_nnew.ensure(nc, st, oldnn));
   if (t->sm_nnew.cap > oldnn) CK(cudaMemsetAsync(t->sm_nnew.p + oldnn, 0, (size_t)(t->sm_nnew.cap - oldnn) * 8, st));
@@ -492,6 +498,23 @@ static int ensure_chunks(LodTree *t, long long want, long long live) {
   RK(grow_col(t->pool.cidx, t->ccap, nc, live, st));
   RK(grow_col(t->pool.free_stack, t->ccap, nc, live, st));
   t->ccap = nc;
+  return LOD_OK;
+}
+
+// Chunk-directory capacity for a cycle that may append `acq` chunks to up to
+// `touched` nodes: every region relocation takes max(4, 2 x the node's new
+// chunk count), so a cycle hands out at most 2 (chunks after it) + 4 touched
+// entries past the current bump pointer (h_ctrl->dir_top, exact between calls).
+// t->ub_dir bounds dir_top after everything launched so far: exact after every
+// sync_ctrl (published behind all queued work), plus the reserve of every
+// cycle launched since.
+static int ensure_dir(LodTree *t, long long chunks_after, long long touched) {
+  const long long keep = t->ub_dir;
+  t->ub_dir += 2 * chunks_after + 4 * touched + 1024;
+  if (t->ub_dir > t->cdir.cap) {
+    RK(t->cdir.ensure(t->ub_dir, t->st, keep));
+    t->pool.cdir = t->cdir.p;
+  }
   return LOD_OK;
 }
 
@@ -623,6 +646,9 @@ static int small_insert(LodTree *t, const float *xyz, const uint32_t *rgba, long
     RK(refresh(t));
   RK(ensure_nodes(t, t->ub_nodes + 8 * s_max + 1, t->ub_nodes));
   RK(ensure_chunks(t, t->ub_alloc + chunks_max + 1, t->ub_alloc));
+  if (t->sm_queued && t->ub_dir + 2 * (t->ub_alloc + chunks_max) + 4 * touched_max + 1024 > t->cdir.cap)
+    RK(refresh(t));  // exact bump pointer before growing the directory
+  RK(ensure_dir(t, t->ub_alloc + chunks_max, touched_max));
   const bool async_call = nv_max <= backlog_cap && spill_max <= spill_cap && t->ub_arena + arena_max <= t->arena_cap;
   RK(t->sm_brec.ensure(kSmallMaxBatch, st));
   RK(t->sm_node_b.ensure(kSmallMaxBatch, st));
@@ -741,6 +767,7 @@ static int small_insert(LodTree *t, const float *xyz, const uint32_t *rgba, long
   t->ub_nodes = r->num_nodes;
   t->ub_alloc = r->allocated_total;
   t->ub_arena = r->arena_off;
+  t->ub_dir = (long long)r->dir_top;
   t->sm_queued = 0;
   t->prev_used = r->n_voxels;
   return r->error;
@@ -874,7 +901,8 @@ int lod_tree_destroy(LodTree *t) {
   f(t->arena);
   f(t->nd.parent); f(t->nd.octant); f(t->nd.level); f(t->nd.children); f(t->nd.inner);
   f(t->nd.final_); f(t->nd.count); f(t->nd.pending); f(t->nd.chunk_head); f(t->nd.chunk_tail);
-  f(t->nd.chunk_count); f(t->nd.grid_off); f(t->nd.bmin); f(t->nd.desc);
+  f(t->nd.chunk_count); f(t->nd.grid_off); f(t->nd.bmin); f(t->nd.desc); f(t->nd.dir_off); f(t->nd.dir_cap);
+  t->cdir.release();
   f(t->pool.next); f(t->pool.payload_off); f(t->pool.occupied); f(t->pool.owner); f(t->pool.cidx);
   f(t->pool.free_stack);
   f(t->d_ctrl);
@@ -888,7 +916,7 @@ int lod_tree_destroy(LodTree *t) {
   t->sm_nnew.release(); t->sm_cur.release(); t->sm_wls.release(); t->sm_pl.release(); t->sm_wl.release();
   t->sm_sp.release(); t->sm_backlog.release();
   if (t->h_seq) cudaFreeHost(t->h_seq);
-  t->xlist.release(); t->split_list.release(); t->node_b.release(); t->node_all.release();
+  t->split_list.release(); t->node_b.release(); t->node_all.release();
   t->bitmap.release(); t->scnt.release(); t->schk.release();
   t->spill_off.release(); t->chunk_off.release(); t->spill.release(); t->hslots.release(); t->hslots2.release();
   t->hused.release(); t->srank.release(); t->wcount.release(); t->wbase.release();
@@ -898,7 +926,7 @@ int lod_tree_destroy(LodTree *t) {
   t->seg_node.release(); t->pairs.release(); t->wlo.release(); t->sinfo.release(); t->seg_start.release();
   t->plan.release(); t->plan_ex.release(); t->in_xyz.release();
   t->in_rgba.release(); t->in_rec.release(); t->gbuf.release(); t->gnodes.release(); t->goff.release(); t->gstart.release();
-  t->visflag.release(); t->vislist.release(); t->fb.release(); t->counter.release();
+  t->woff.release(); t->vislist.release(); t->fb.release(); t->counter.release();
   release_scan_lb(t->lb32);
   release_scan_lb(t->lb64);
   t->dsplits.release(); t->dvnode.release(); t->dpnode.release(); t->dvstart.release(); t->dvcount.release();
@@ -1159,6 +1187,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     RK(t->sinfo.ensure(Kb, st));
     const long long alloc0 = t->h_ctrl->allocated_total;
     RK(ensure_chunks(t, alloc0 + acq_bound + 1, alloc0));
+    RK(ensure_dir(t, alloc0 + acq_bound + 1, Kb));
     const long long lbw = radix_lb_elems(n_items);
     long long *n_items_dev = &t->d_ctrl->n_items;
     {
@@ -1238,7 +1267,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     }
     mark(5);
     // ---- cleanup (update.py:375-380)
-    lod::launch(k_epilogue, grid_for(Kb), 256, 0, st, t->nd, t->seg_node.p, t->seg_start.p, t->d_ctrl, t->ghist.p,
+    lod::launch(k_epilogue, grid_for(Kb), 256, 0, st, t->nd, t->pool, t->seg_node.p, t->seg_start.p, t->plan.p,
+                t->plan_ex.p, t->d_ctrl, t->ghist.p,
                 guard);
     return LOD_OK;
   };
@@ -1301,11 +1331,10 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       if (!first) return abort_cycle(t, LOD_E_ARG);  // only iteration 1 can spill (update.py:9-11)
       RK(t->spill.ensure(h.spill_total, st));
       RK(t->node_all.ensure(h.spill_total, st));
-      RK(t->xlist.ensure(std::max<long long>(h.allocated_total, 1), st));
-      lod::launch(k_split_chunk_list, grid_for(h.allocated_total), 256, 0, st, t->pool, h.allocated_total, t->srank.p,
-                  t->xlist.p, t->d_ctrl);
-      lod::launch(k_exec_chunks, grid_for(h.allocated_total * 32), 256, 0, st, t->pool, t->geo, t->arena, t->xlist.p,
-                  t->srank.p, t->spill_off.p, t->chunk_off.p, t->spill.p, t->node_all.p, t->d_ctrl);
+      const long long xchunks = h.free_count - h.plan_free0;  // chunks of the splitting nodes
+      lod::launch(k_exec_chunks, grid_for(xchunks * 32), 256, 0, st, t->nd, t->pool, t->geo, t->arena,
+                  t->split_list.p, ns, t->spill_off.p, t->chunk_off.p, xchunks, t->spill.p, t->node_all.p,
+                  t->d_ctrl);
     }
     lod::launch(k_exec_nodes, grid_for(8 * ns), 256, 0, st, t->nd, t->geo, t->split_list.p, t->srank.p, ns,
                                                    t->d_ctrl);
@@ -1524,6 +1553,280 @@ int lod_read_pool(LodTree *t, int64_t n, int32_t *next, int64_t *payload_off, in
   return LOD_OK;
 }
 
+}  // extern "C"
+
+// ---------------------------------------------------------------- structural edits
+
+// Octree.split of one leaf (octree.py:222-264); one thread.
+__global__ void k_split_one(NodeCols nd, PoolCols pool, Geo geo, Ctrl *c, int nid, unsigned long long arena_cap,
+                            int *status) {
+  lod::pdl_wait();
+  if (nd.inner[nid] || nd.level[nid] >= geo.max_depth) {
+    *status = -LOD_E_ARG;
+    return;
+  }
+  // release the chain onto the free stack in walk order (store.py:125-143)
+  for (int cid = nd.chunk_head[nid]; cid != LOD_NO_CHUNK;) {
+    const int nxt = pool.next[cid];
+    pool.free_stack[c->free_count++] = cid;
+    ++c->released_total;
+    pool.occupied[cid] = 0;
+    pool.next[cid] = LOD_NO_CHUNK;
+    pool.owner[cid] = -1;
+    pool.cidx[cid] = -1;
+    cid = nxt;
+  }
+  nd.chunk_head[nid] = LOD_NO_CHUNK;
+  nd.chunk_tail[nid] = LOD_NO_CHUNK;
+  nd.chunk_count[nid] = 0;
+  nd.count[nid] = 0;
+  nd.pending[nid] = 0;
+  const unsigned long long gb = (unsigned long long)geo.grid_bytes;
+  const unsigned long long g0 = (c->arena_off + 63ull) / 64ull * 64ull;  // Arena.alloc(grid_bytes, 64)
+  if (g0 + gb > arena_cap) {
+    *status = -LOD_E_OUT_OF_ARENA;
+    return;
+  }
+  c->arena_off = g0 + gb;
+  const long long first = c->num_nodes;
+  const int lvl = nd.level[nid];
+  const double half = geo.size_by_level[lvl] * 0.5;
+  for (int o = 0; o < 8; ++o) {
+    const int k = (int)first + o;
+    nd.parent[k] = nid;
+    nd.octant[k] = (uint8_t)o;
+    nd.level[k] = lvl + 1;
+    for (int q = 0; q < 8; ++q) nd.children[8 * k + q] = LOD_NO_NODE;
+    nd.inner[k] = 0;
+    nd.final_[k] = 0;
+    nd.count[k] = 0;
+    nd.pending[k] = 0;
+    nd.chunk_head[k] = LOD_NO_CHUNK;
+    nd.chunk_tail[k] = LOD_NO_CHUNK;
+    nd.chunk_count[k] = 0;
+    nd.grid_off[k] = -1;
+    nd.desc[k] = make_int2(-1, 0);
+    nd.dir_off[k] = 0;
+    nd.dir_cap[k] = 0;
+    nd.bmin[3 * k + 0] = nd.bmin[3 * nid + 0] + ((o & 1) ? half : 0.0);
+    nd.bmin[3 * k + 1] = nd.bmin[3 * nid + 1] + ((o & 2) ? half : 0.0);
+    nd.bmin[3 * k + 2] = nd.bmin[3 * nid + 2] + ((o & 4) ? half : 0.0);
+    nd.children[8 * nid + o] = k;
+  }
+  nd.inner[nid] = 1;
+  nd.grid_off[nid] = (long long)g0;
+  nd.desc[nid] = make_int2((int)first, (int)(uint32_t)(g0 >> 6));
+  c->num_nodes = first + 8;
+  c->splits_total += 1;
+  if (lvl + 1 > c->max_level) c->max_level = lvl + 1;
+  *status = (int)first;  // >= 1: the first child
+}
+
+// Octree.append_chunk + ChunkPool.acquire (octree.py:328-337, store.py:110-123); one thread.
+__global__ void k_append_one(NodeCols nd, PoolCols pool, Geo geo, Ctrl *c, int nid, unsigned long long arena_cap,
+                             int *status) {
+  lod::pdl_wait();
+  int cid;
+  if (c->free_count > 0) {
+    cid = pool.free_stack[--c->free_count];
+  } else {
+    const unsigned long long off = (c->arena_off + 15ull) / 16ull * 16ull;  // alloc(payload, RECORD_BYTES)
+    const unsigned long long end = off + (unsigned long long)geo.C * 16ull;
+    if (end > arena_cap) {
+      *status = -LOD_E_OUT_OF_ARENA;
+      return;
+    }
+    cid = (int)c->allocated_total++;
+    pool.payload_off[cid] = (long long)off;
+    c->arena_off = end;
+  }
+  pool.next[cid] = LOD_NO_CHUNK;
+  pool.occupied[cid] = 0;
+  const int tail = nd.chunk_tail[nid];
+  if (tail != LOD_NO_CHUNK) pool.next[tail] = cid;
+  else nd.chunk_head[nid] = cid;
+  nd.chunk_tail[nid] = cid;
+  pool.owner[cid] = nid;
+  pool.cidx[cid] = nd.chunk_count[nid];
+  nd.chunk_count[nid] += 1;
+  dir_append(nd, pool, &c->dir_top, nid, 1, [&](long long) { return cid; });
+  *status = cid;
+}
+
+__global__ void k_grid_tas(NodeCols nd, uint8_t *arena, int nid, long long cell, int *status) {
+  lod::pdl_wait();
+  uint32_t *w = reinterpret_cast<uint32_t *>(arena + nd.grid_off[nid]) + (cell >> 5);
+  const uint32_t bit = 1u << (cell & 31);
+  *status = (atomicOr(w, bit) & bit) ? 0 : 1;
+}
+
+// The device-only indexes after host edits of the node / pool columns:
+// descent records from inner / children / grid_off, and per chunk list (walk
+// order) the owners, positions and a fresh directory region.  One thread per node.
+__global__ void k_rebuild_indexes(NodeCols nd, PoolCols pool, long long n, Ctrl *c) {
+  lod::pdl_wait();
+  for (long long i = gtid(); i < n; i += gstride()) {
+    const int nid = (int)i;
+    nd.desc[nid] = nd.inner[nid] ? make_int2(nd.children[8 * nid], (int)(uint32_t)(nd.grid_off[nid] >> 6))
+                                 : make_int2(-1, 0);
+    const long long cc = nd.chunk_count[nid];
+    long long off = nd.dir_off[nid];
+    if (cc > nd.dir_cap[nid]) {
+      const long long cap = cc * 2 > 4 ? cc * 2 : 4;
+      off = (long long)atomicAdd(&c->dir_top, (unsigned long long)cap);
+      nd.dir_off[nid] = off;
+      nd.dir_cap[nid] = (int32_t)cap;
+    }
+    long long ci = 0;
+    for (int cid = nd.chunk_head[nid]; cid != LOD_NO_CHUNK && ci < cc; cid = pool.next[cid], ++ci) {
+      pool.owner[cid] = nid;
+      pool.cidx[cid] = (int)ci;
+      pool.cdir[off + ci] = cid;
+    }
+  }
+}
+
+static int one_shot(LodTree *t, int *status_host, const std::function<void(int *)> &launch_fn) {
+  RK(refresh(t));
+  RK(t->counter.ensure(4, t->st));
+  int *d_status = reinterpret_cast<int *>(t->counter.p + 3);
+  CK(cudaMemsetAsync(d_status, 0, 4, t->st));
+  launch_fn(d_status);
+  CK(cudaMemcpyAsync(status_host, d_status, 4, cudaMemcpyDeviceToHost, t->st));
+  RK(sync_ctrl(t));  // also waits for the copy
+  exact_bounds(t);
+  return LOD_OK;
+}
+
+extern "C" {
+
+int lod_split_node(LodTree *t, int64_t nid, int32_t *first_child) {
+  if (!t || nid < 0) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  RK(refresh(t));
+  if (nid >= t->num_nodes) return LOD_E_ARG;
+  RK(ensure_nodes(t, t->num_nodes + 8, t->num_nodes));
+  int status = 0;
+  RK(one_shot(t, &status, [&](int *d) {
+    lod::launch(k_split_one, 1, 1, 0, t->st, t->nd, t->pool, t->geo, t->d_ctrl, (int)nid, t->arena_cap, d);
+  }));
+  if (status <= 0) return status == 0 ? LOD_E_CUDA : -status;  // errors come back negated
+  if (first_child) *first_child = status;
+  return LOD_OK;
+}
+
+int lod_append_chunk(LodTree *t, int64_t nid, int32_t *cid) {
+  if (!t || nid < 0) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  RK(refresh(t));
+  if (nid >= t->num_nodes) return LOD_E_ARG;
+  RK(ensure_chunks(t, t->h_ctrl->allocated_total + 1, t->h_ctrl->allocated_total));
+  RK(ensure_dir(t, t->h_ctrl->allocated_total + 1, 1));
+  int status = 0;
+  RK(one_shot(t, &status, [&](int *d) {
+    lod::launch(k_append_one, 1, 1, 0, t->st, t->nd, t->pool, t->geo, t->d_ctrl, (int)nid, t->arena_cap, d);
+  }));
+  if (status < 0) return -status;
+  if (cid) *cid = status;
+  return LOD_OK;
+}
+
+int lod_grid_test_and_set(LodTree *t, int64_t nid, int64_t cell, int32_t *was_clear) {
+  if (!t || nid < 0 || cell < 0 || cell >= t->geo.g * t->geo.g * t->geo.g || !was_clear) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  RK(refresh(t));
+  if (nid >= t->num_nodes) return LOD_E_ARG;
+  long long goff = -1;
+  CK(cudaMemcpyAsync(&goff, t->nd.grid_off + nid, 8, cudaMemcpyDeviceToHost, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  if (goff < 0) return LOD_E_ARG;  // leaves have no grid
+  int status = 0;
+  RK(one_shot(t, &status, [&](int *d) {
+    lod::launch(k_grid_tas, 1, 1, 0, t->st, t->nd, t->arena, (int)nid, (long long)cell, d);
+  }));
+  *was_clear = status;
+  return LOD_OK;
+}
+
+int lod_write_nodes(LodTree *t, int64_t n, const int32_t *parent, const uint8_t *octant, const int32_t *level,
+                    const int32_t *children, const uint8_t *inner, const uint8_t *final_, const int64_t *count,
+                    const int64_t *pending, const int32_t *chunk_head, const int32_t *chunk_tail,
+                    const int32_t *chunk_count, const int64_t *grid_off, const double *bmin) {
+  if (!t || n < 0) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  RK(refresh(t));
+  if (n > t->num_nodes) return LOD_E_ARG;
+  cudaStream_t st = t->st;
+  auto cp = [&](void *dst, const void *src, size_t bytes) -> int {
+    if (src && bytes) return cuda_rc(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    return LOD_OK;
+  };
+  RK(cp(t->nd.parent, parent, n * 4));
+  RK(cp(t->nd.octant, octant, n));
+  RK(cp(t->nd.level, level, n * 4));
+  RK(cp(t->nd.children, children, n * 32));
+  RK(cp(t->nd.inner, inner, n));
+  RK(cp(t->nd.final_, final_, n));
+  RK(cp(t->nd.count, count, n * 8));
+  RK(cp(t->nd.pending, pending, n * 8));
+  RK(cp(t->nd.chunk_head, chunk_head, n * 4));
+  RK(cp(t->nd.chunk_tail, chunk_tail, n * 4));
+  RK(cp(t->nd.chunk_count, chunk_count, n * 4));
+  RK(cp(t->nd.grid_off, grid_off, n * 8));
+  RK(cp(t->nd.bmin, bmin, n * 24));
+  const long long alloc = t->h_ctrl->allocated_total;
+  RK(ensure_dir(t, alloc, n));
+  lod::launch(k_rebuild_indexes, grid_for(n), 256, 0, st, t->nd, t->pool, (long long)n, t->d_ctrl);
+  RK(sync_ctrl(t));
+  exact_bounds(t);
+  return LOD_OK;
+}
+
+int lod_write_pool(LodTree *t, int64_t n, const int32_t *next, const int64_t *payload_off, const int32_t *occupied) {
+  if (!t || n < 0) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  RK(refresh(t));
+  if (n > t->h_ctrl->allocated_total) return LOD_E_ARG;
+  cudaStream_t st = t->st;
+  if (next && n) CK(cudaMemcpyAsync(t->pool.next, next, n * 4, cudaMemcpyHostToDevice, st));
+  if (payload_off && n) CK(cudaMemcpyAsync(t->pool.payload_off, payload_off, n * 8, cudaMemcpyHostToDevice, st));
+  if (occupied && n) CK(cudaMemcpyAsync(t->pool.occupied, occupied, n * 4, cudaMemcpyHostToDevice, st));
+  if (next) {  // the chain links define the owners and the directory
+    const long long nn = t->num_nodes;
+    RK(ensure_dir(t, t->h_ctrl->allocated_total, nn));
+    lod::launch(k_rebuild_indexes, grid_for(nn), 256, 0, st, t->nd, t->pool, nn, t->d_ctrl);
+  }
+  RK(sync_ctrl(t));
+  exact_bounds(t);
+  return LOD_OK;
+}
+
+int lod_write_arena(LodTree *t, uint64_t off, uint64_t size, const void *src) {
+  if (!t || (size && !src) || off + size > t->arena_cap) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  RK(refresh(t));
+  if (size) CK(cudaMemcpyAsync(t->arena + off, src, size, cudaMemcpyHostToDevice, t->st));
+  CK(cudaStreamSynchronize(t->st));
+  return LOD_OK;
+}
+
+int lod_read_directory(LodTree *t, int64_t n, int64_t *dir_off, int32_t *dir_cap, int32_t *cdir, int64_t cdir_len,
+                       uint64_t *dir_top) {
+  if (!t || n < 0 || n > t->ncap || !dir_top) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  RK(sync_ctrl(t));
+  exact_bounds(t);
+  *dir_top = t->h_ctrl->dir_top;
+  if (n && dir_off) CK(cudaMemcpyAsync(dir_off, t->nd.dir_off, n * 8, cudaMemcpyDeviceToHost, t->st));
+  if (n && dir_cap) CK(cudaMemcpyAsync(dir_cap, t->nd.dir_cap, n * 4, cudaMemcpyDeviceToHost, t->st));
+  if (cdir) {
+    if (cdir_len < (int64_t)*dir_top) return LOD_E_ARG;
+    if (*dir_top) CK(cudaMemcpyAsync(cdir, t->pool.cdir, *dir_top * 4, cudaMemcpyDeviceToHost, t->st));
+  }
+  CK(cudaStreamSynchronize(t->st));
+  return LOD_OK;
+}
+
 static int gather_impl(LodTree *t, const std::vector<int32_t> &nodes, const std::vector<long long> &starts,
                        const std::vector<long long> &offs, long long total, float4 *host_out) {
   cudaStream_t st = t->st;
@@ -1699,16 +2002,15 @@ cudaStream_t lod_tree_stream(LodTree *t) { return t->st; }
 int lod_tree_device(LodTree *t) { return t->dev; }
 const uint8_t *lod_tree_arena(LodTree *t) { return t->arena; }
 PoolCols lod_tree_pool(LodTree *t) { return t->pool; }
-long long lod_tree_allocated(LodTree *t) {
-  cudaMemcpyAsync(t->h_ctrl, t->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, t->st);
-  cudaStreamSynchronize(t->st);
-  return t->h_ctrl->allocated_total;
-}
 long long lod_tree_num_nodes(LodTree *t) {
   refresh(t);
   return t->num_nodes;
 }
-uint32_t *lod_tree_visflag(LodTree *t) { return t->visflag.p; }
+int lod_tree_ensure_woff(LodTree *t, long long n, long long **p) {
+  RK(t->woff.ensure(std::max<long long>(n, 1), t->st));
+  *p = t->woff.p;
+  return LOD_OK;
+}
 int lod_tree_ensure_vislist(LodTree *t, long long n, int32_t **p) {
   int rc = t->vislist.ensure(std::max<long long>(n, 1), t->st);
   *p = t->vislist.p;
@@ -1764,9 +2066,9 @@ PackLayout pack_layout(const Ctrl &c) {
   const size_t n = (size_t)c.num_nodes, a = (size_t)c.allocated_total, f = (size_t)c.free_count;
   const size_t sizes[] = {sizeof(PackHeader),
                           n * 4, n * 1, n * 4, n * 32, n * 1, n * 1, n * 8, n * 8, n * 4, n * 4, n * 4, n * 8,
-                          n * 24, n * 8,
+                          n * 24, n * 8, n * 8, n * 4,
                           a * 4, a * 8, a * 4, a * 4, a * 4,
-                          f * 4,
+                          f * 4, (size_t)c.dir_top * 4,
                           (size_t)c.arena_off};
   size_t o = 0;
   int k = 0;
@@ -1816,11 +2118,13 @@ int lod_tree_pack(LodTree *t, void *dev_buf, uint64_t bytes) {
   const size_t n = (size_t)c.num_nodes, a = (size_t)c.allocated_total, f = (size_t)c.free_count;
   const void *src[] = {t->nd.parent, t->nd.octant, t->nd.level, t->nd.children, t->nd.inner, t->nd.final_,
                        t->nd.count, t->nd.pending, t->nd.chunk_head, t->nd.chunk_tail, t->nd.chunk_count,
-                       t->nd.grid_off, t->nd.bmin, t->nd.desc, t->pool.next, t->pool.payload_off,
-                       t->pool.occupied, t->pool.owner, t->pool.cidx, t->pool.free_stack, t->arena};
+                       t->nd.grid_off, t->nd.bmin, t->nd.desc, t->nd.dir_off, t->nd.dir_cap, t->pool.next,
+                       t->pool.payload_off, t->pool.occupied, t->pool.owner, t->pool.cidx, t->pool.free_stack,
+                       t->pool.cdir, t->arena};
   const size_t sz[] = {n * 4, n, n * 4, n * 32, n, n, n * 8, n * 8, n * 4, n * 4, n * 4, n * 8, n * 24, n * 8,
-                       a * 4, a * 8, a * 4, a * 4, a * 4, f * 4, (size_t)c.arena_off};
-  for (int k = 0; k < 21; ++k)
+                       n * 8, n * 4, a * 4, a * 8, a * 4, a * 4, a * 4, f * 4, (size_t)c.dir_top * 4,
+                       (size_t)c.arena_off};
+  for (int k = 0; k < 24; ++k)
     if (sz[k]) CK(cudaMemcpyAsync(b + L.off[k + 1], src[k], sz[k], cudaMemcpyDeviceToDevice, st));
   CK(cudaStreamSynchronize(st));
   return LOD_OK;
@@ -1840,14 +2144,18 @@ int lod_tree_unpack(LodTree *t, const void *dev_buf, uint64_t bytes) {
   if (bytes < L.total || c.arena_off > t->arena_cap) return LOD_E_ARG;
   RK(ensure_nodes(t, std::max<long long>(c.num_nodes, 1), 0));
   RK(ensure_chunks(t, std::max<long long>(c.allocated_total + 1, 1), 0));
+  t->ub_dir = 0;
+  RK(ensure_dir(t, (long long)c.dir_top, 0));
   const size_t n = (size_t)c.num_nodes, a = (size_t)c.allocated_total, f = (size_t)c.free_count;
   void *dst[] = {t->nd.parent, t->nd.octant, t->nd.level, t->nd.children, t->nd.inner, t->nd.final_,
                  t->nd.count, t->nd.pending, t->nd.chunk_head, t->nd.chunk_tail, t->nd.chunk_count,
-                 t->nd.grid_off, t->nd.bmin, t->nd.desc, t->pool.next, t->pool.payload_off,
-                 t->pool.occupied, t->pool.owner, t->pool.cidx, t->pool.free_stack, t->arena};
+                 t->nd.grid_off, t->nd.bmin, t->nd.desc, t->nd.dir_off, t->nd.dir_cap, t->pool.next,
+                 t->pool.payload_off, t->pool.occupied, t->pool.owner, t->pool.cidx, t->pool.free_stack,
+                 t->pool.cdir, t->arena};
   const size_t sz[] = {n * 4, n, n * 4, n * 32, n, n, n * 8, n * 8, n * 4, n * 4, n * 4, n * 8, n * 24, n * 8,
-                       a * 4, a * 8, a * 4, a * 4, a * 4, f * 4, (size_t)c.arena_off};
-  for (int k = 0; k < 21; ++k)
+                       n * 8, n * 4, a * 4, a * 8, a * 4, a * 4, a * 4, f * 4, (size_t)c.dir_top * 4,
+                       (size_t)c.arena_off};
+  for (int k = 0; k < 24; ++k)
     if (sz[k]) CK(cudaMemcpyAsync(dst[k], b + L.off[k + 1], sz[k], cudaMemcpyDeviceToDevice, st));
   // the rest of the arena must stay zeroed (regions are handed out zeroed)
   if (t->arena_cap > c.arena_off) CK(cudaMemsetAsync(t->arena + c.arena_off, 0, t->arena_cap - c.arena_off, st));
@@ -1859,6 +2167,7 @@ int lod_tree_unpack(LodTree *t, const void *dev_buf, uint64_t bytes) {
   nc.allocated_total = c.allocated_total;
   nc.free_count = c.free_count;
   nc.released_total = c.released_total;
+  nc.dir_top = c.dir_top;
   CK(cudaMemcpyAsync(t->d_ctrl, &nc, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
   RK(sync_ctrl(t));
   exact_bounds(t);

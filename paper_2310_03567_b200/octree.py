@@ -168,6 +168,7 @@ class Octree:
         pool._bind(self)
         self._gen = 0
         self._cache: dict = {}
+        self._arena_edits: list = []  # (offset, host copy handed out, snapshot) of pool.records() views
 
     # -- lifetime -----------------------------------------------------------------
     def close(self) -> None:
@@ -184,11 +185,51 @@ class Octree:
 
     @property
     def handle(self) -> ctypes.c_void_p:
+        """The C handle; host edits of the mirrors reach the device first."""
+        if self._cache or self._arena_edits:
+            self._sync_edits()
         return self._h
 
     def _invalidate(self) -> None:
         self._gen += 1
         self._cache.clear()
+        self._arena_edits.clear()  # payload copies handed out before a device update are detached
+
+    def _sync_edits(self) -> None:
+        """Write host edits of the mirrored columns back to the device.
+
+        Callers may edit ``tree.count``, ``pool.occupied``, the arrays
+        ``pool.records(cid)`` returned, ... in place, as the reference's unit
+        tests do with its numpy-backed tree; the mirrors are compared with
+        the snapshot taken when they were read, and changed columns are
+        written back (lod_write_nodes / lod_write_pool / lod_write_arena,
+        which rebuild the device-only indexes) before the next device call."""
+        c = self._cache
+        if "cols" in c:
+            cols, snap = c["cols"], c["cols_snap"]
+            n = len(snap["count"])
+            changed = {k for k in snap if not np.array_equal(cols[k][:n], snap[k])}
+            if changed:
+                keep = [np.ascontiguousarray(cols[k][:n]) if k in changed else None for k, *_ in _NODE_COLS]
+                _lib.check(self._L.lod_write_nodes(self._h, n, *(_lib.ptr(a) for a in keep)), "lod_write_nodes")
+                for k in changed:
+                    snap[k] = cols[k][:n].copy()
+                c.pop("info", None)
+        if "pool" in c:
+            pc, snap = c["pool"], c["pool_snap"]
+            n = len(snap["occupied"])
+            changed = {k for k in snap if not np.array_equal(pc[k][:n], snap[k])}
+            if changed:
+                args = [np.ascontiguousarray(pc[k][:n]) if k in changed else None
+                        for k in ("next", "payload_off", "occupied")]
+                _lib.check(self._L.lod_write_pool(self._h, n, *(_lib.ptr(a) for a in args)), "lod_write_pool")
+                for k in changed:
+                    snap[k] = pc[k][:n].copy()
+        for off, raw, snap in self._arena_edits:
+            if not np.array_equal(raw, snap):
+                _lib.check(self._L.lod_write_arena(self._h, off, raw.nbytes, _lib.ptr(raw)), "lod_write_arena")
+                snap[...] = raw
+
 
     # -- mirrors ----------------------------------------------------------------------
     def _info(self) -> _lib.LodTreeInfo:
@@ -208,6 +249,7 @@ class Octree:
             args = [_lib.ptr(cols[name]) for name, *_ in _NODE_COLS]
             _lib.check(self._L.lod_read_nodes(self._h, n, *args), "lod_read_nodes")
             self._cache["cols"] = cols
+            self._cache["cols_snap"] = {name: cols[name][:n].copy() for name, *_ in _NODE_COLS}
         return self._cache["cols"]
 
     def _pool_cols(self) -> dict:
@@ -222,12 +264,14 @@ class Octree:
             _lib.check(self._L.lod_read_pool(self._h, n, _lib.ptr(nxt), _lib.ptr(poff), _lib.ptr(occ),
                                              _lib.ptr(free), nf), "lod_read_pool")
             self._cache["pool"] = {"next": nxt, "payload_off": poff, "occupied": occ, "free_list": free}
+            self._cache["pool_snap"] = {"next": nxt[:n].copy(), "payload_off": poff[:n].copy(),
+                                        "occupied": occ[:n].copy()}
         return self._cache["pool"]
 
     def _arena_bytes(self, off: int, size: int) -> np.ndarray:
         out = np.empty(size, np.uint8)
         if size:
-            _lib.check(self._L.lod_read_arena(self._h, off, size, _lib.ptr(out)), "lod_read_arena")
+            _lib.check(self._L.lod_read_arena(self.handle, off, size, _lib.ptr(out)), "lod_read_arena")
         return out
 
     def _live_chunks(self) -> int:
@@ -279,28 +323,67 @@ class Octree:
         xyz = np.empty((k, 3), dtype=np.float32)
         rgba = np.empty(k, dtype=np.uint32)
         if k:
-            _lib.check(self._L.lod_gather(self._h, nid, start, _lib.ptr(xyz), _lib.ptr(rgba)), "lod_gather")
+            _lib.check(self._L.lod_gather(self.handle, nid, start, _lib.ptr(xyz), _lib.ptr(rgba)), "lod_gather")
         return xyz, rgba
+
+    def chunk_directory(self) -> list[np.ndarray]:
+        """Every node's chunk ids in list order as the device directory holds
+        them (the spill gather and the render read chunks through it)."""
+        n = self.num_nodes
+        top = ctypes.c_uint64(0)
+        _lib.check(self._L.lod_read_directory(self._h, 0, None, None, None, 0, ctypes.byref(top)), "directory")
+        off, cap = np.zeros(n, np.int64), np.zeros(n, np.int32)
+        cdir = np.zeros(max(int(top.value), 1), np.int32)
+        _lib.check(self._L.lod_read_directory(self._h, n, _lib.ptr(off), _lib.ptr(cap), _lib.ptr(cdir), len(cdir),
+                                              ctypes.byref(top)), "directory")
+        cc = self.chunk_count[:n]
+        assert np.all(cc <= cap), "directory region smaller than the chunk list"
+        return [cdir[off[i]:off[i] + cc[i]] for i in range(n)]
 
     def dump_records(self) -> tuple[np.ndarray, np.ndarray]:
         """All samples packed by node id: (offsets (n+1,), records (total, 4) as f32 view)."""
         n = self.num_nodes
         offsets = np.zeros(n + 1, np.int64)
-        _lib.check(self._L.lod_dump_records(self._h, n, _lib.ptr(offsets), None), "lod_dump_records")
+        _lib.check(self._L.lod_dump_records(self.handle, n, _lib.ptr(offsets), None), "lod_dump_records")
         rec = np.empty((int(offsets[-1]), 4), np.float32)
         _lib.check(self._L.lod_dump_records(self._h, n, _lib.ptr(offsets), _lib.ptr(rec)), "lod_dump_records")
         return offsets, rec
 
     # -- structure outside the update cycle -------------------------------------------
     def split(self, nid: int, spill) -> list[int]:
-        raise NotImplementedError(
-            "structural edits run inside insert_batch on the GPU; Octree.split is not exposed"
-        )
+        """Turn a leaf into an inner node with 8 fresh leaf children
+        (octree.py:222-264): stored samples go to ``spill`` in storage order
+        (SpillOverflow past its capacity), the chunks back to the pool in walk
+        order, the node gets a zeroed grid (OutOfArena past the arena).  The
+        device kernel is the same split the update cycle performs."""
+        assert not self.inner[nid], "split target must be a leaf"
+        assert self.level[nid] < self.max_depth, "cannot split at max depth"
+        if int(self.count[nid]):
+            xyz, rgba = self.gather_samples(nid)
+            spill.append(xyz, rgba)
+        first = ctypes.c_int32(0)
+        rc = self._L.lod_split_node(self.handle, nid, ctypes.byref(first))
+        self._invalidate()
+        _lib.check(rc, "split")
+        return list(range(first.value, first.value + 8))
 
     def append_chunk(self, nid: int) -> int:
-        raise NotImplementedError(
-            "chunks are linked inside insert_batch on the GPU; Octree.append_chunk is not exposed"
-        )
+        """Link one freshly acquired chunk at the tail of a node's list
+        (octree.py:328-337; LIFO reuse before the arena, store.py:110-123)."""
+        cid = ctypes.c_int32(0)
+        rc = self._L.lod_append_chunk(self.handle, nid, ctypes.byref(cid))
+        self._invalidate()
+        _lib.check(rc, "append_chunk")
+        return int(cid.value)
+
+    def grid_test_and_set(self, nid: int, cell: int) -> bool:
+        """Set a cell bit; True when the cell was previously empty (octree.py:281-288)."""
+        assert int(self.grid_off[nid]) >= 0, "leaf nodes have no grid"
+        was = ctypes.c_int32(0)
+        rc = self._L.lod_grid_test_and_set(self.handle, nid, int(cell), ctypes.byref(was))
+        self._invalidate()
+        _lib.check(rc, "grid_test_and_set")
+        return bool(was.value)
 
     # -- whole-tree helpers (octree.py:341-377) ---------------------------------------
     def leaves(self) -> np.ndarray:
@@ -324,20 +407,22 @@ class Octree:
         count, ccount, head = self.count, self.chunk_count, self.chunk_head
         inner, children, grid_off = self.inner, self.children, self.grid_off
         nxt, occ = self.pool.next, self.pool.occupied
+        dirs = self.chunk_directory()  # device-only index of every chunk list (B200 extra)
         for nid in range(n):
             cnt = int(count[nid])
             want = (cnt + cap - 1) // cap
             assert ccount[nid] == want, (nid, cnt, int(ccount[nid]))
-            walked = 0
+            walked = []
             cid = int(head[nid])
             seen = cnt
             while cid != NO_CHUNK:
-                walked += 1
+                walked.append(cid)
                 got = int(occ[cid])
                 assert got == min(seen, cap), (nid, cid, got)
                 seen -= got
                 cid = int(nxt[cid])
-            assert walked == want
+            assert len(walked) == want
+            assert walked == dirs[nid].tolist(), (nid, "chunk directory differs from the list")
             if inner[nid]:
                 assert all(children[nid, o] != NO_NODE for o in range(8))
                 assert self.grid_popcount(nid) == cnt, (nid, cnt)

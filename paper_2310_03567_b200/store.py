@@ -205,11 +205,15 @@ class ChunkPool:
     def records(self, cid: int) -> tuple[np.ndarray, np.ndarray]:
         """(xyz (capacity, 3) f32, rgba (capacity,) u32) of one payload (store.py:153-158).
 
-        Bound pools return copies read from HBM; unbound pools return views.
+        Bound pools return views of a host copy read from HBM, written back
+        on the tree's next device call if edited; unbound pools return views.
         """
         off = int(self.payload_off[cid])
         if self._tree is not None:
+            # a host copy of the payload; edits made through the returned
+            # views are written back before the tree's next device call
             raw = self._tree._arena_bytes(off, self.payload_bytes)
+            self._tree._arena_edits.append((off, raw, raw.copy()))
             f = raw.view(np.float32).reshape(self.capacity, 4)
             u = raw.view(np.uint32).reshape(self.capacity, 4)
             return f[:, :3], u[:, 3]

@@ -90,16 +90,37 @@ class BudgetClock:
 
 
 class SpillBuffer:
-    """Spill accounting.  The spilled records themselves live in an HBM buffer
-    of the tree for the duration of one cycle (update.py:106-140); between
-    cycles the buffer is empty, which is all callers can observe."""
+    """Spill buffer (update.py:106-140).  Inside insert_batch the spilled
+    records live in an HBM buffer of the tree for one cycle; between cycles
+    the buffer is empty, which is all callers of the update can observe.
+    Host segments are held only for ``Octree.split`` called directly
+    (octree.py:222-264), which appends the split leaf's samples here."""
 
     def __init__(self, capacity: int) -> None:
         self.capacity = capacity
         self.total = 0
         self.high_water = 0
+        self._xyz: list[np.ndarray] = []
+        self._rgba: list[np.ndarray] = []
+
+    def append(self, xyz: np.ndarray, rgba: np.ndarray) -> None:
+        from .errors import SpillOverflow
+
+        if self.total + len(rgba) > self.capacity:
+            raise SpillOverflow(f"spill buffer past capacity {self.capacity}")
+        self._xyz.append(xyz)
+        self._rgba.append(rgba)
+        self.total += len(rgba)
+        self.high_water = max(self.high_water, self.total)
+
+    def concat(self) -> tuple[np.ndarray, np.ndarray]:
+        if not self._xyz:
+            return np.empty((0, 3), np.float32), np.empty(0, np.uint32)
+        return np.concatenate(self._xyz), np.concatenate(self._rgba)
 
     def clear(self) -> None:
+        self._xyz.clear()
+        self._rgba.clear()
         self.total = 0
 
     def __len__(self) -> int:
@@ -273,11 +294,13 @@ def _insert_small(tree: Octree, xyz: np.ndarray, rgba: np.ndarray, n_batch: int,
     lim.spill_capacity = state.config.spill_capacity
     lim.input_stream = None
     bs = state._bstats
-    rc = tree._L.lod_insert_batch(tree._h, xyz.ctypes.data, rgba.ctypes.data, n_batch, ctypes.byref(lim), 0,
+    rc = tree._L.lod_insert_batch(tree.handle, xyz.ctypes.data, rgba.ctypes.data, n_batch, ctypes.byref(lim), 0,
                                   ctypes.byref(bs))
     tree._gen += 1
     if tree._cache:
         tree._cache.clear()
+    if tree._arena_edits:
+        tree._arena_edits.clear()
     _lib.check(rc, "insert_batch")
     st = state._stats
     if bs.iterations < 0:  # queued: counts folded in when the state settles

@@ -86,6 +86,7 @@ def test_matches_oracle(gpu, label, n, seed, kind, bs, params):
     assert per == oper
     assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label=label)
     _hygiene(tree, state)
+    tree.validate()
 
 
 def test_config1_one_million_uniform(gpu):
@@ -218,6 +219,7 @@ def test_skew_stream_burst_matches_oracle(gpu):
     assert per == oper
     assert max(p[4] for p in per) > 5_000_000  # the spill burst happened
     assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label="skew_burst")
+    tree.validate()
 
 
 def test_frame_budget_semantics(gpu):

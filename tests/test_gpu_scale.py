@@ -1,0 +1,168 @@
+"""Bit-exact parity at BASELINE scale (the configs bench.py and DESIGN quote).
+
+* config 2: the full 100 x 1M-point terrain stream exactly as bench.py
+  generates it (gen_surface, seeds 1000+i), paper parameters (G=128,
+  T=50,000, C=1,000, depth 20), every batch's UpdateStats and the settled tree
+  vs the oracle, plus the render at the bench camera vs the oracle's splat;
+* config 4: the density-skew stream through its split waves of > 20M spilled
+  points (claim-table growth, rehash, burst resolve and 16-bit-histogram
+  fallbacks all trigger there);
+* config 3: the mesh stream, insert + rasterize per frame at the bench
+  camera, every frame's framebuffer vs the oracle's splat of the same
+  selection, and the tree at the end;
+* config 5: the partition protocol at paper parameters on a 24M-point
+  terrain prefix, 2/4/8 ranks emulated on one GPU: every rank's prefix
+  subtrees equal the single-tree run path by path.
+
+The oracle (oracle/lod_oracle.c, a 1-thread C restatement pinned to the
+reference's own outputs) runs live; these tests take minutes.
+"""
+import numpy as np
+import pytest
+
+from common import assert_same_state, make_product, oracle_state, product_state, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+PAPER = dict(bmin=(0.0, 0.0, 0.0), size=1.0, arena_bytes=8 << 30, chunk_capacity=1000, grid_res=128,
+             leaf_threshold=50_000, max_depth=20, backlog_capacity=64_000_000, spill_capacity=100_000_000)
+BENCH_CAM = dict(position=(0.5, 0.5, -1.5), target=(0.5, 0.5, 0.5), fov_deg=60.0, near=0.05, far=100.0, width=1024,
+                 height=768)
+
+
+def _stream(kind, count, seed0=1000):
+    import sys
+
+    sys.path.insert(0, __file__.rsplit("/", 2)[0])
+    from bench import gen_batches
+
+    return gen_batches(kind, count, seed0)
+
+
+def _run_stream(params, batches, frames=None):
+    """Oracle and product over the same batches, batch by batch; returns
+    (oracle tree, product tree, product state, per-batch stats of both)."""
+    from paper_2310_03567_b200 import insert_batch
+
+    import oracle
+
+    ot = oracle.OracleTree(params["bmin"], params["size"], grid_res=params["grid_res"],
+                           leaf_threshold=params["leaf_threshold"], max_depth=params["max_depth"],
+                           chunk_capacity=params["chunk_capacity"], arena_bytes=params["arena_bytes"],
+                           backlog_capacity=params["backlog_capacity"], spill_capacity=params["spill_capacity"])
+    tree, state = make_product(params)
+    o_per, p_per = [], []
+    for i, (x, c) in enumerate(batches):
+        s = ot.insert_batch(x, c)
+        o_per.append((s["n_voxels"], s["n_spill"], s["n_splits"]))
+        insert_batch(tree, x, c, state)
+        b = state._bstats
+        p_per.append((int(b.n_voxels), int(b.n_spill), int(b.n_splits)))
+        if frames is not None:
+            frames(i, ot, tree)
+    return ot, tree, state, o_per, p_per
+
+
+def _render_vs_oracle(ot, tree, threshold=128.0):
+    from paper_2310_03567_b200.render import Camera, Framebuffer, rasterize
+
+    cam = Camera(**BENCH_CAM)
+    fb, rep = rasterize(tree, cam, threshold=threshold)
+    ofb = Framebuffer(cam.width, cam.height)
+    drawn = ot.rasterize_nodes(rep.selected, cam.packed(), ofb.cells)
+    assert drawn == rep.samples_drawn
+    assert np.array_equal(fb.cells, ofb.cells)
+    return rep
+
+
+def test_config2_full_terrain_stream(gpu):
+    batches = _stream("surface", 100)
+    ot, tree, state, o_per, p_per = _run_stream(PAPER, batches)
+    assert p_per == o_per
+    st = state.stats
+    assert st.voxels_created == ot.voxels_created and st.points == 100_000_000
+    assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label="config2_100M")
+    rep = _render_vs_oracle(ot, tree)
+    assert rep.samples_drawn > 1_000_000
+    print(f"config 2: {tree.num_nodes} nodes, max spill {max(s for _, s, _ in p_per)}, "
+          f"max new voxels {max(v for v, _, _ in p_per)}, render {rep.samples_drawn} samples")
+
+
+def test_config4_skew_split_waves(gpu):
+    batches = _stream("skew", 60)
+    ot, tree, state, o_per, p_per = _run_stream(PAPER, batches)
+    assert p_per == o_per
+    spills = [s for _, s, _ in p_per]
+    print("config 4 spill per batch (M):", [round(s / 1e6, 1) for s in spills])
+    assert max(spills) > 20_000_000, "the stream must reach a split wave of > 20M spilled points"
+    assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label="config4_skew")
+    tree.validate()
+
+
+def test_config3_mesh_frames(gpu):
+    """Insert + render per frame (config 3's loop) on a 20M-point mesh prefix."""
+    frames = []
+
+    def each_frame(i, ot, tree):
+        rep = _render_vs_oracle(ot, tree)
+        frames.append(rep.samples_drawn)
+
+    batches = _stream("mesh", 20)
+    ot, tree, state, o_per, p_per = _run_stream(PAPER, batches, frames=each_frame)
+    assert p_per == o_per
+    assert len(frames) == 20 and min(frames) > 0
+    assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label="config3_mesh")
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_config5_partition_protocol_paper_params(gpu, world):
+    """The warm-up / hand-off / partitioned protocol at paper parameters: the
+    single-tree run vs `world` emulated rank trees fed by exact octant-prefix
+    routing (plan over depth 1 for 2/4 ranks, depth 2 for 8)."""
+    from paper_2310_03567_b200 import insert_batch, multigpu, partition
+    from oracle.rebuild import tree_paths
+
+    params = dict(PAPER, arena_bytes=6 << 30)
+    batches = _stream("surface", 24, seed0=5000)
+    plan = partition.plan_owners(batches[:2], world)
+    g, gs = make_product(params)
+    ranks = [make_product(params) for _ in range(world)]
+    handed = False
+    for x, c in batches:
+        insert_batch(g, x, c, gs)
+        if not handed:
+            insert_batch(ranks[0][0], x, c, ranks[0][1])
+            if multigpu.top_is_inner(ranks[0][0], plan.depth):
+                buf = multigpu.pack_tree(ranks[0][0])
+                for r in range(1, world):
+                    multigpu.unpack_tree(ranks[r][0], buf)
+                handed = True
+            continue
+        for r in range(world):
+            xr, cr = partition.take(plan, x, c, r)
+            if len(cr):
+                insert_batch(ranks[r][0], xr, cr, ranks[r][1])
+    assert handed
+    gp = tree_paths(g.inner, g.children)
+    rp = [tree_paths(t.inner, t.children) for t, _ in ranks]
+    g_off, g_rec = g.dump_records()
+    r_dump = [t.dump_records() for t, _ in ranks]
+    checked = 0
+    for path, nid in gp.items():
+        if len(path) < plan.depth:
+            continue
+        prefix = 0
+        for o in path[:plan.depth]:
+            prefix = prefix * 8 + o
+        r = int(plan.owner[prefix])
+        t = ranks[r][0]
+        assert path in rp[r], path
+        rid = rp[r][path]
+        assert bool(t.inner[rid]) == bool(g.inner[nid]), path
+        ro, rr = r_dump[r]
+        a = g_rec[g_off[nid]:g_off[nid + 1]].view(np.uint32)
+        b = rr[ro[rid]:ro[rid + 1]].view(np.uint32)
+        assert np.array_equal(a, b), path
+        checked += 1
+    assert checked > 100
+    print(f"config 5 x{world}: {checked} prefix nodes equal, single tree {g.num_nodes} nodes")

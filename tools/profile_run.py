@@ -23,7 +23,7 @@ def main():
     ap.add_argument("--profiled", type=int, default=1)
     ap.add_argument("--arena-gib", type=float, default=8.0)
     a = ap.parse_args()
-    batches = gen_batches(a.config, a.warmup + a.profiled)
+    batches = gen_batches(a.config, a.warmup + a.profiled)  # bench.py's stream: seeds 1000+i
     dev = [(torch.from_numpy(x).cuda(), torch.from_numpy(c.view(np.int32)).cuda()) for x, c in batches]
     tree, state = new_tree(0, int(a.arena_gib * (1 << 30)))
     for i in range(a.warmup):

@@ -161,6 +161,31 @@ int lod_tree_wait(LodTree *tree, float *last_device_ms);
 int lod_prefetch_batch(LodTree *tree, const float *xyz, const uint32_t *rgba, int64_t n);
 int lod_prefetch_drain(LodTree *tree);
 
+/* lod_prefetch_batch for a batch of n packed 16-byte records (the SIM file
+ * layout, io.py:38-40; page-locked), consumed by a later lod_insert_batch with
+ * LOD_FLAG_PACKED and the same pointer and n. */
+int lod_prefetch_records(LodTree *tree, const void *records, int64_t n);
+
+/* Disk feed (io.py:218-290 _DirectReader + io.py:340-413 BatchSource): a
+ * reader thread reads a SIM file (16-byte records, io.py:60-92) batch after
+ * batch with O_DIRECT (buffered when the filesystem refuses) into a ring of
+ * `slots` page-locked buffers; lod_sim_next hands out the next batch in file
+ * order (blocking; *n = 0 at end of file), valid until lod_sim_release.
+ * batch_records * 16 must be a multiple of 4096.  LOD_E_ARG for an empty or
+ * truncated file (io.py: EmptyFile / Truncated).  No GPU is needed. */
+typedef struct LodSim LodSim;
+typedef struct {
+    uint64_t file_bytes, bytes_read;
+    double read_seconds;   /* time the reader thread spent in read calls */
+    int32_t direct;        /* 1: O_DIRECT (page cache bypassed)         */
+    int32_t pinned;        /* 1: slots are page-locked (a CUDA device)  */
+} LodSimInfo;
+int lod_sim_open(const char *path, int64_t batch_records, int32_t slots, LodSim **out);
+int lod_sim_next(LodSim *sim, const void **records, int64_t *n);
+int lod_sim_release(LodSim *sim, const void *records);
+int lod_sim_info(LodSim *sim, LodSimInfo *info);
+int lod_sim_close(LodSim *sim);
+
 /* D2H mirror of the node table columns (octree.py:169-182), rows [0, n).
  * Any pointer may be NULL to skip that column. children is (n,8), bmin (n,3). */
 int lod_read_nodes(LodTree *tree, int64_t n, int32_t *parent, uint8_t *octant, int32_t *level,

@@ -101,6 +101,11 @@ class LodSettleStats(ctypes.Structure):
                 ("error", ctypes.c_int32)]
 
 
+class LodSimInfo(ctypes.Structure):
+    _fields_ = [("file_bytes", ctypes.c_uint64), ("bytes_read", ctypes.c_uint64), ("read_seconds", ctypes.c_double),
+                ("direct", ctypes.c_int32), ("pinned", ctypes.c_int32)]
+
+
 class LodDeltaInfo(ctypes.Structure):
     _fields_ = [("n_splits", ctypes.c_int64), ("n_voxel_groups", ctypes.c_int64), ("n_voxels", ctypes.c_int64),
                 ("n_point_groups", ctypes.c_int64)]
@@ -120,6 +125,12 @@ SIGNATURES = {
                                         ctypes.POINTER(LodBatchStats)]),
     "lod_prefetch_batch": (ctypes.c_int, [_P, _P, _P, _I64]),
     "lod_prefetch_drain": (ctypes.c_int, [_P]),
+    "lod_prefetch_records": (ctypes.c_int, [_P, _P, _I64]),
+    "lod_sim_open": (ctypes.c_int, [ctypes.c_char_p, _I64, ctypes.c_int32, ctypes.POINTER(_P)]),
+    "lod_sim_next": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(_I64)]),
+    "lod_sim_release": (ctypes.c_int, [_P, _P]),
+    "lod_sim_info": (ctypes.c_int, [_P, ctypes.POINTER(LodSimInfo)]),
+    "lod_sim_close": (ctypes.c_int, [_P]),
     "lod_tree_wait": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_float)]),
     "lod_tree_settle": (ctypes.c_int, [_P, ctypes.POINTER(LodSettleStats)]),
     "lod_read_nodes": (ctypes.c_int, [_P, _I64] + [_P] * 13),

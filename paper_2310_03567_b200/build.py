@@ -20,8 +20,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lodb200.so")
-SOURCES = ["lod_tree.cu", "lod_raster.cu", "lod_morton.cu", "lod_route.cu"]
-HEADERS = ["lod_common.cuh", "lod_kernels.cuh", "radix.cuh", "scan.cuh"]
+SOURCES = ["lod_tree.cu", "lod_raster.cu", "lod_morton.cu", "lod_route.cu", "lod_ingest.cu"]
+HEADERS = ["lod_common.cuh", "lod_kernels.cuh", "lod_small.cuh", "radix.cuh", "scan.cuh"]
 
 
 def nvcc() -> str:

@@ -212,6 +212,8 @@ struct LodTree {
   struct Stage {
     DBuf<float> xyz;
     DBuf<uint32_t> rgba;
+    DBuf<float4> rec;      // packed batches (lod_prefetch_records)
+    bool packed = false;   // hx = the packed host records, hc = null
     const void *hx = nullptr, *hc = nullptr;
     long long n = 0;
     bool valid = false;
@@ -937,6 +939,7 @@ int lod_tree_destroy(LodTree *t) {
   for (auto &sg : t->stage) {
     sg.xyz.release();
     sg.rgba.release();
+    sg.rec.release();
     if (sg.ready) cudaEventDestroy(sg.ready);
   }
   if (t->cst) cudaStreamDestroy(t->cst);
@@ -1048,7 +1051,24 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   const uint32_t *bc = rgba;
   const float4 *brec = nullptr;  // packed 16-byte input records
   LodTree::Stage *staged = nullptr;
-  if (packed) {
+  if (!(flags & LOD_FLAG_DEVICE_INPUT)) {
+    for (auto &sg : t->stage)
+      if (sg.valid && sg.packed == packed && sg.hx == (const void *)xyz && (packed || sg.hc == rgba) && sg.n == n)
+        staged = &sg;
+  }
+  if (staged) {  // prefetched on the copy stream: wait for it, no copy here
+    // a copy not issued yet goes behind the work queued so far on the tree
+    // stream: an earlier early-returning insert's tail may still read this slot
+    if (staged->pending) RK(issue_pending(t));
+    CK(cudaStreamWaitEvent(st, staged->ready, 0));
+    staged->valid = false;
+    if (packed) {
+      brec = staged->rec.p;
+    } else {
+      bx = staged->xyz.p;
+      bc = staged->rgba.p;
+    }
+  } else if (packed) {
     if (flags & LOD_FLAG_DEVICE_INPUT) {
       brec = reinterpret_cast<const float4 *>(xyz);
     } else {
@@ -1057,18 +1077,6 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       brec = t->in_rec.p;
     }
   } else if (!(flags & LOD_FLAG_DEVICE_INPUT)) {
-    for (auto &sg : t->stage)
-      if (sg.valid && sg.hx == xyz && sg.hc == rgba && sg.n == n) staged = &sg;
-  }
-  if (staged) {  // prefetched on the copy stream: wait for it, no copy here
-    // a copy not issued yet goes behind the work queued so far on the tree
-    // stream: an earlier early-returning insert's tail may still read this slot
-    if (staged->pending) RK(issue_pending(t));
-    CK(cudaStreamWaitEvent(st, staged->ready, 0));
-    staged->valid = false;
-    bx = staged->xyz.p;
-    bc = staged->rgba.p;
-  } else if (!packed && !(flags & LOD_FLAG_DEVICE_INPUT)) {
     RK(t->in_xyz.ensure(3 * n, st));
     RK(t->in_rgba.ensure(n, st));
     CK(cudaMemcpyAsync(t->in_xyz.p, xyz, (size_t)n * 12, cudaMemcpyHostToDevice, st));
@@ -1905,17 +1913,29 @@ int lod_read_arena(LodTree *t, uint64_t off, uint64_t size, void *dst) {
 
 }  // extern "C"
 
+static int prefetch_impl(LodTree *t, const void *xyz, const uint32_t *rgba, int64_t n, bool packed);
+
 int lod_prefetch_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t n) {
   if (!t || n < 0 || (n > 0 && (!xyz || !rgba))) return LOD_E_ARG;
+  return prefetch_impl(t, xyz, rgba, n, false);
+}
+
+int lod_prefetch_records(LodTree *t, const void *records, int64_t n) {
+  if (!t || n < 0 || (n > 0 && !records)) return LOD_E_ARG;
+  return prefetch_impl(t, records, nullptr, n, true);
+}
+
+static int prefetch_impl(LodTree *t, const void *xyz, const uint32_t *rgba, int64_t n, bool packed) {
   if (n == 0) return LOD_OK;
   // only page-locked host memory can be copied asynchronously; anything else
   // is left to lod_insert_batch's own copy
   cudaPointerAttributes ax{}, ac{};
-  if (cudaPointerGetAttributes(&ax, xyz) != cudaSuccess || cudaPointerGetAttributes(&ac, rgba) != cudaSuccess) {
+  if (cudaPointerGetAttributes(&ax, xyz) != cudaSuccess ||
+      (!packed && cudaPointerGetAttributes(&ac, rgba) != cudaSuccess)) {
     cudaGetLastError();
     return LOD_OK;
   }
-  if (ax.type != cudaMemoryTypeHost || ac.type != cudaMemoryTypeHost) return LOD_OK;
+  if (ax.type != cudaMemoryTypeHost || (!packed && ac.type != cudaMemoryTypeHost)) return LOD_OK;
   cudaSetDevice(t->dev);
   if (!t->cst) {
     CK(cudaStreamCreateWithFlags(&t->cst, cudaStreamNonBlocking));
@@ -1923,18 +1943,24 @@ int lod_prefetch_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64
     CK(cudaEventCreateWithFlags(&t->ev_counted, cudaEventDisableTiming));
   }
   for (auto &sg : t->stage)
-    if (sg.valid && sg.hx == xyz && sg.hc == rgba && sg.n == n) return LOD_OK;  // already staged
+    if (sg.valid && sg.packed == packed && sg.hx == xyz && sg.hc == rgba && sg.n == n) return LOD_OK;  // staged
   LodTree::Stage &sg = t->stage[t->stage_next];
   t->stage_next = (t->stage_next + 1) % 3;
   // the slot's previous batch was consumed by an earlier insert (or is
   // superseded); that insert's tail may still read it on the tree stream, so
   // a growing slot frees its old buffers only behind the tree stream
-  if (3 * n > sg.xyz.cap || n > sg.rgba.cap) {
+  const bool grow = packed ? n > sg.rec.cap : (3 * n > sg.xyz.cap || n > sg.rgba.cap);
+  if (grow) {
     CK(cudaEventRecord(t->ev_counted, t->st));
     CK(cudaStreamWaitEvent(t->cst, t->ev_counted, 0));
   }
-  RK(sg.xyz.ensure(3 * n, t->cst));
-  RK(sg.rgba.ensure(n, t->cst));
+  if (packed) {
+    RK(sg.rec.ensure(n, t->cst));
+  } else {
+    RK(sg.xyz.ensure(3 * n, t->cst));
+    RK(sg.rgba.ensure(n, t->cst));
+  }
+  sg.packed = packed;
   // The copy itself is issued by the next lod_insert_batch behind its first
   // count pass: a 16 MB DMA into HBM running alongside the claim-heavy count
   // slows it by ~50 % (L2 pressure), while the rest of the cycle hides it.
@@ -1947,8 +1973,12 @@ int lod_prefetch_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64
 }
 
 static int issue_stage(LodTree *t, LodTree::Stage &sg) {
-  CK(cudaMemcpyAsync(sg.xyz.p, sg.hx, (size_t)sg.n * 12, cudaMemcpyHostToDevice, t->cst));
-  CK(cudaMemcpyAsync(sg.rgba.p, sg.hc, (size_t)sg.n * 4, cudaMemcpyHostToDevice, t->cst));
+  if (sg.packed) {
+    CK(cudaMemcpyAsync(sg.rec.p, sg.hx, (size_t)sg.n * 16, cudaMemcpyHostToDevice, t->cst));
+  } else {
+    CK(cudaMemcpyAsync(sg.xyz.p, sg.hx, (size_t)sg.n * 12, cudaMemcpyHostToDevice, t->cst));
+    CK(cudaMemcpyAsync(sg.rgba.p, sg.hc, (size_t)sg.n * 4, cudaMemcpyHostToDevice, t->cst));
+  }
   CK(cudaEventRecord(sg.ready, t->cst));
   sg.pending = false;
   return LOD_OK;

@@ -107,6 +107,9 @@ def pack_rgba(r: int, g: int, b: int, a: int = 255) -> int:
     return (r & 0xFF) | (g & 0xFF) << 8 | (b & 0xFF) << 16 | (a & 0xFF) << 24
 
 
+_DUMP_CACHE_MAX = 8 << 20    # samples: trees up to 128 MB of records are read back whole for gathers
+_ARENA_CACHE_MAX = 128 << 20  # bytes: arenas up to this much in use are read back whole for grids
+
 _NODE_COLS = (
     # name, dtype, per-row shape, fill beyond the live rows (octree.py:169-182)
     ("parent", np.int32, (), NO_NODE),
@@ -215,6 +218,7 @@ class Octree:
                 for k in changed:
                     snap[k] = cols[k][:n].copy()
                 c.pop("info", None)
+                c["_edited"] = True
         if "pool" in c:
             pc, snap = c["pool"], c["pool_snap"]
             n = len(snap["occupied"])
@@ -225,10 +229,16 @@ class Octree:
                 _lib.check(self._L.lod_write_pool(self._h, n, *(_lib.ptr(a) for a in args)), "lod_write_pool")
                 for k in changed:
                     snap[k] = pc[k][:n].copy()
+                c["_edited"] = True
+        wrote = False
         for off, raw, snap in self._arena_edits:
             if not np.array_equal(raw, snap):
                 _lib.check(self._L.lod_write_arena(self._h, off, raw.nbytes, _lib.ptr(raw)), "lod_write_arena")
                 snap[...] = raw
+                wrote = True
+        if wrote or c.pop("_edited", False):
+            for k in ("dump", "dump_gen", "arena", "arena_gen"):
+                c.pop(k, None)
 
 
     # -- mirrors ----------------------------------------------------------------------
@@ -307,6 +317,9 @@ class Octree:
         """Copy of an inner node's occupancy bitgrid bytes (octree.py:275-279)."""
         off = int(self.grid_off[nid])
         assert off >= 0, "leaf nodes have no grid"
+        cached = self._cached_arena()
+        if cached is not None:
+            return cached[off: off + self.grid_bytes].copy()
         return self._arena_bytes(off, self.grid_bytes)
 
     def grid_popcount(self, nid: int) -> int:
@@ -317,14 +330,39 @@ class Octree:
         return np.nonzero(np.unpackbits(self.grid(nid), bitorder="little"))[0]
 
     def gather_samples(self, nid: int, start: int = 0) -> tuple[np.ndarray, np.ndarray]:
-        """Samples [start, count) in storage (= insertion) order (octree.py:298-326)."""
+        """Samples [start, count) in storage (= insertion) order (octree.py:298-326).
+
+        Trees up to _DUMP_CACHE_MAX samples are read back whole once per
+        update (lod_dump_records) and served from that copy, so walking every
+        node (as the reference's oracles do) costs one device round trip,
+        not one per node."""
         total = int(self.count[nid])
         k = max(total - start, 0)
+        if k and self._cached_dump() is not None:
+            off, rec = self._cache["dump"]
+            r = rec[off[nid] + start: off[nid + 1]]
+            return np.ascontiguousarray(r[:, :3]), r[:, 3].view(np.uint32).copy()
         xyz = np.empty((k, 3), dtype=np.float32)
         rgba = np.empty(k, dtype=np.uint32)
         if k:
             _lib.check(self._L.lod_gather(self.handle, nid, start, _lib.ptr(xyz), _lib.ptr(rgba)), "lod_gather")
         return xyz, rgba
+
+    def _cached_dump(self):
+        if self._cache.get("dump_gen") != self._gen:
+            n = self.num_nodes
+            total = int(self.count[:n].sum())
+            self._cache["dump"] = self.dump_records() if total <= _DUMP_CACHE_MAX else None
+            self._cache["dump_gen"] = self._gen
+        return self._cache["dump"]
+
+    def _cached_arena(self):
+        """The used arena bytes (grids and payloads), one read per update, for small trees."""
+        if self._cache.get("arena_gen") != self._gen:
+            used = self.arena.offset
+            self._cache["arena"] = self._arena_bytes(0, used) if used <= _ARENA_CACHE_MAX else None
+            self._cache["arena_gen"] = self._gen
+        return self._cache["arena"]
 
     def chunk_directory(self) -> list[np.ndarray]:
         """Every node's chunk ids in list order as the device directory holds

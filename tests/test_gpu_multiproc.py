@@ -30,4 +30,5 @@ def test_bench_two_ranks_over_gloo(gpu, tmp_path):
     assert len(lines) == 1, r.stdout  # rank 0 alone prints the line
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["steps"] == 3 and d["value"] > 0 and d["e2e"]["value"] > 0
-    assert d["config"]["batch_points"] == 2_000_000 and "GLOO" in d["config"]["parallelism"]
+    assert d["config"]["batch_points"] == 1_000_000 and "GLOO" in d["notes"]["parallelism"]
+    assert d["notes"]["global_batch"].startswith("2 x 1M")

@@ -89,7 +89,7 @@ def test_config2_full_terrain_stream(gpu):
 
 
 def test_config4_skew_split_waves(gpu):
-    batches = _stream("skew", 60)
+    batches = _stream("skew", 100)
     ot, tree, state, o_per, p_per = _run_stream(PAPER, batches)
     assert p_per == o_per
     spills = [s for _, s, _ in p_per]

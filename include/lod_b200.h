@@ -226,6 +226,24 @@ int lod_write_nodes(LodTree *tree, int64_t n, const int32_t *parent, const uint8
 int lod_write_pool(LodTree *tree, int64_t n, const int32_t *next, const int64_t *payload_off, const int32_t *occupied);
 int lod_write_arena(LodTree *tree, uint64_t off, uint64_t size, const void *src);
 
+/* Replicated top nodes of an octant-prefix partitioned tree (multigpu.py,
+ * SURVEY 8(e) "all-gathered and merged by global index"):
+ *   lod_last_voxels   the voxels the last lod_insert_batch created at nodes
+ *                     of level < max_level: node, cell, rgba and the winner's
+ *                     batch position (all-array index - spill length), in no
+ *                     particular order; capacity 0 queries *n.  Call before
+ *                     the next insert (it reads that cycle's backlog);
+ *   lod_merge_voxels  rewrite each listed node's voxel sequence from gstart[g]
+ *                     on with the items goff[g] .. goff[g+1]-1 (cells and
+ *                     colours in their final order; the node's own voxels of
+ *                     the last cycle are among them), extending its chunk
+ *                     list and setting the cells' grid bits -- so every rank's
+ *                     copy of a top node holds the single-tree sequence. */
+int lod_last_voxels(LodTree *tree, int32_t max_level, int64_t capacity, int32_t *node, uint32_t *cell,
+                    uint32_t *rgba, int64_t *winner, int64_t *n);
+int lod_merge_voxels(LodTree *tree, int64_t n_groups, const int32_t *gnode, const int64_t *gstart,
+                     const int64_t *goff, const uint32_t *cell, const uint32_t *rgba);
+
 /* The device-only chunk directory (inspection / tests): per node its region
  * offset and capacity, the entries [0, *dir_top) (node n's chunk ids in list
  * order are cdir[dir_off[n] + i], i < chunk_count[n]).  cdir may be NULL to
@@ -311,20 +329,22 @@ int lod_morton_sort(int32_t device, const double *bmin, double scale, int32_t bi
  * owner rank -- owner_of_prefix[octant path over `depth` levels], the path
  * computed with the reference's float64 descent rule -- keeping input order
  * inside each bucket, as packed 16-byte records in out_records (bucket r at
- * starts[r], counts[r] records).  xyz / rgba / out_records / counts / starts
+ * starts[r], counts[r] records), and (out_positions, may be NULL) each
+ * record's position in the stripe.  xyz / rgba / out_records / counts / starts
  * are DEVICE pointers; owner_of_prefix is a host array of 8^depth ranks;
  * `stream` is the cudaStream_t to order the work on (NULL = legacy default).
  * Asynchronous: counts / starts are valid once the stream reaches them. */
 int lod_route_bucket(int32_t device, const double *bmin, double size, int32_t depth, const int32_t *owner_of_prefix,
                      int32_t world, const float *xyz, const uint32_t *rgba, int64_t n, void *out_records,
-                     int64_t *counts, int64_t *starts, void *stream);
+                     uint32_t *out_positions, int64_t *counts, int64_t *starts, void *stream);
 
 /* Multi-GPU routing and composite over peer memory (the fused
  * replacement for the all-to-all and the all-reduce): each rank owns one
  * receive window -- an IPC-shareable device allocation (NVLink peer memory
  * between GPUs) laid out as the int64 count matrix [source][owner] in the
  * first LOD_WINDOW_HEADER_BYTES, then two halves of `half_records` 16-byte
- * records -- and maps every peer's window (`windows[r]` = rank r's window as
+ * records, then two halves of `half_records` uint32 stripe positions (each
+ * record's index in its source stripe) -- and maps every peer's window (`windows[r]` = rank r's window as
  * seen by this process, its own included).  Per batch:
  *   lod_route_peers_begin   owners + bucket sizes of this rank's stripe, the
  *                           sizes stored as row `rank` of every peer's matrix;

@@ -155,7 +155,9 @@ SIGNATURES = {
     "lod_morton_sort": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_double, ctypes.c_int32, _P, _P, _I64, _P, _P,
                                        _P, ctypes.c_int]),
     "lod_route_bucket": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_double, ctypes.c_int32, _P, ctypes.c_int32, _P, _P,
-                                        _I64, _P, _P, _P, _P]),
+                                        _I64, _P, _P, _P, _P, _P]),
+    "lod_last_voxels": (ctypes.c_int, [_P, ctypes.c_int32, _I64, _P, _P, _P, _P, ctypes.POINTER(_I64)]),
+    "lod_merge_voxels": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _P]),
     "lod_ipc_alloc": (ctypes.c_int, [ctypes.c_int32, ctypes.c_uint64, ctypes.POINTER(_P), _P]),
     "lod_ipc_open": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.POINTER(_P)]),
     "lod_ipc_close": (ctypes.c_int, [_P]),

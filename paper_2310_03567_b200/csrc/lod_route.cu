@@ -110,20 +110,33 @@ __global__ void __launch_bounds__(1024)
 // into owner o's receive window over NVLink, behind the records of the lower
 // source ranks (offset = sum over s < rank of the window count matrix's
 // column o, identical on every rank after the count exchange).
+// Every record also carries its position in the source stripe (a uint32 in
+// a parallel array) so the owner can name each point's global index -- the
+// order the replicated top nodes' voxels are merged in (lod_merge_voxels).
 struct LocalDest {
   const long long *starts;
   float4 *out;
+  uint32_t *pos;  // may be null
   __device__ float4 *base(int o) const { return out + starts[o]; }
+  __device__ uint32_t *pos_base(int o) const { return pos ? pos + starts[o] : nullptr; }
 };
 struct PeerDest {
   PeerWindows win;
   int rank, world, half;
   long long half_records;
-  __device__ float4 *base(int o) const {
+  __device__ long long offset(int o) const {
     const long long *m = reinterpret_cast<const long long *>(win.p[rank]);  // my copy of the matrix
     long long off = 0;
     for (int s = 0; s < rank; ++s) off += m[s * world + o];
-    return reinterpret_cast<float4 *>(win.p[o] + kWindowHeader) + (long long)half * half_records + off;
+    return off;
+  }
+  __device__ float4 *base(int o) const {
+    return reinterpret_cast<float4 *>(win.p[o] + kWindowHeader) + (long long)half * half_records + offset(o);
+  }
+  // window layout: header | records half 0 | records half 1 | positions half 0 | positions half 1
+  __device__ uint32_t *pos_base(int o) const {
+    return reinterpret_cast<uint32_t *>(win.p[o] + kWindowHeader + 2 * half_records * 16) +
+           (long long)half * half_records + offset(o);
   }
 };
 
@@ -135,7 +148,11 @@ __global__ void __launch_bounds__(kRouteBlock)
   __shared__ uint32_t wtot[kRouteBlock / 32][kRouteMaxWorld];  // per-warp bucket totals -> warp offsets
   __shared__ uint16_t lrank[kRouteTile];
   __shared__ float4 *s_base[kRouteMaxWorld];
-  for (int d = threadIdx.x; d < world; d += kRouteBlock) s_base[d] = dest.base(d);
+  __shared__ uint32_t *s_pos[kRouteMaxWorld];
+  for (int d = threadIdx.x; d < world; d += kRouteBlock) {
+    s_base[d] = dest.base(d);
+    s_pos[d] = dest.pos_base(d);
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = lanemask_lt();
   const long long t0 = (long long)blockIdx.x * kRouteTile;
@@ -179,6 +196,7 @@ __global__ void __launch_bounds__(kRouteBlock)
     const long long pos = tile_off[(long long)blockIdx.x * world + o] + wtot[warp][o] + lrank[li];
     s_base[o][pos] = make_float4(__ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1), __ldg(xyz + 3 * i + 2),
                            __uint_as_float(__ldg(rgba + i)));
+    if (s_pos[o]) s_pos[o][pos] = (uint32_t)i;
   }
 }
 
@@ -306,7 +324,7 @@ extern "C" {
 
 int lod_route_bucket(int32_t device, const double *bmin, double size, int32_t depth, const int32_t *owner_of_prefix,
                      int32_t world, const float *xyz, const uint32_t *rgba, int64_t n, void *out_records,
-                     int64_t *counts, int64_t *starts, void *stream) {
+                     uint32_t *out_positions, int64_t *counts, int64_t *starts, void *stream) {
   if (!bmin || !owner_of_prefix || depth < 0 || depth > 8 || world < 1 || world > kRouteMaxWorld || n < 0 ||
       (n > 0 && (!xyz || !rgba || !out_records)) || !counts || !starts || device < 0 || device >= 64)
     return LOD_E_ARG;
@@ -320,7 +338,7 @@ int lod_route_bucket(int32_t device, const double *bmin, double size, int32_t de
   if (n > 0)
     lod::launch(k_route_scatter<LocalDest>, cdiv(n, kRouteTile), kRouteBlock, 0, st, xyz, rgba, (long long)n,
                 (int)world, s.owner, s.tiles,
-                LocalDest{(const long long *)starts, reinterpret_cast<float4 *>(out_records)});
+                LocalDest{(const long long *)starts, reinterpret_cast<float4 *>(out_records), out_positions});
   return cuda_rc(cudaGetLastError());
 }
 

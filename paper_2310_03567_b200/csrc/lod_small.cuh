@@ -65,7 +65,7 @@ struct SmallArgs {
   long long *nnew;           // per node: new voxels this cycle (zero between cycles)
   long long *cur;            // per node: next slot (store)
   long long *wls;            // per node: first write-list entry
-  uint4 *backlog;            // new voxels {node, cell, rgba, 0} in claim order
+  uint4 *backlog;            // new voxels {node, cell, rgba, winner index} in claim order
   int32_t *tl;               // leaves touched in the running iteration
   int32_t *cand;             // split candidates of the running iteration
   int32_t *splits;           // split candidates in ascending id
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_cycle(SmallArgs a) {
         if (win) {
           atomicOr(grid32 + ((unsigned long long)(uint32_t)d.y << 4) + (cell >> 5), 1u << (cell & 31));
           const long long pos = nv + __popc(wm & lanemask_lt());
-          if (pos < a.vox_cap) a.backlog[pos] = make_uint4((uint32_t)nid, (uint32_t)cell, rgba, 0u);
+          if (pos < a.vox_cap) a.backlog[pos] = make_uint4((uint32_t)nid, (uint32_t)cell, rgba, (uint32_t)j);
         }
         const unsigned npeers = __match_any_sync(0xffffffffu, win ? nid : -1);
         if (win && (int)(__ffs(npeers) - 1) == lane) {

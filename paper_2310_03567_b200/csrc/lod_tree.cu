@@ -179,7 +179,7 @@ struct LodTree {
   long long prev_used = 0;  // claims of the previous cycle (sizes the table)
   int last_iters = 0;       // expansion iterations of the previous cycle (speculation policy)
   long long spec_hits = 0;  // cycles whose pipeline ran speculatively
-  DBuf<uint4> backlog;  // the cycle's new voxels in backlog order: {node, cell, rgba, 0}
+  DBuf<uint4> backlog;  // the cycle's new voxels in backlog order: {node, cell, rgba, winner index}
   DBuf<uint4> wins;     // burst path: k_resolve_list's win list {winner, node, cell, rgba}
   // sort / alloc scratch
   DBuf<uint32_t> keys, keys_b, vals_a, vals_b, hist, ghist, nodecnt;
@@ -248,6 +248,9 @@ struct LodTree {
   long long ub_nodes = 1, ub_alloc = 0, ub_dir = 0;
   unsigned long long ub_arena = 0;
   long long ingested = 0;  // points inserted so far (bounds the spill of a cycle)
+  // the last cycle's backlog (lod_last_voxels): which buffer, entries, spill length
+  const uint4 *last_backlog = nullptr;
+  long long last_nv = 0, last_ns = 0;
 };
 
 static constexpr int kSmallRing = 512;  // batch slots of kSmallMaxBatch records each
@@ -317,7 +320,7 @@ struct WinSink {
   uint4 *backlog;
   __device__ __forceinline__ void operator()(uint32_t pos, uint32_t, uint32_t val) const {
     const uint4 e = wins[val];
-    backlog[pos] = make_uint4(e.y, e.z, e.w, 0u);
+    backlog[pos] = make_uint4(e.y, e.z, e.w, e.x);
   }
 };
 
@@ -741,6 +744,7 @@ static int small_insert(LodTree *t, const float *xyz, const uint32_t *rgba, long
     t->ub_arena += arena_max;
     ++t->sm_queued;
     ++t->sm_unfolded;
+    t->last_backlog = nullptr;  // counts unknown until settled: lod_last_voxels runs the cycle synchronously
     S.iterations = -1;  // queued: lod_tree_settle reports the counts
     S.device_ms = -1.f;
     S.device_ms_prev = -1.f;
@@ -772,6 +776,9 @@ static int small_insert(LodTree *t, const float *xyz, const uint32_t *rgba, long
   t->ub_dir = (long long)r->dir_top;
   t->sm_queued = 0;
   t->prev_used = r->n_voxels;
+  t->last_backlog = t->sm_backlog.p;
+  t->last_nv = r->n_voxels;
+  t->last_ns = r->n_spill;
   return r->error;
 }
 
@@ -1290,8 +1297,25 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   for (;;) {
     ++iters;
     if (prof) cudaEventRecord(t->ev[12], st);
-    lod::launch(k_count, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, node_of, n_all, first, grid32, hs,
-                t->d_ctrl);
+    // iteration 1 (batch points from the root): the TMA-staged count pass on
+    // request (LOD_COUNT_STAGED=1; batch 16-byte aligned, >= one full tile).
+    // Off by default: same-box A/B on the terrain stream, count phase 0.183 ms
+    // staged vs 0.177 ms with direct loads (k_count_staged's comment)
+    static const int staged_mode = getenv("LOD_COUNT_STAGED") ? atoi(getenv("LOD_COUNT_STAGED")) : 0;
+    const bool aligned = brec ? ((uintptr_t)brec % 16 == 0)
+                              : ((uintptr_t)bx % 16 == 0 && (uintptr_t)bc % 16 == 0);
+    if (first && staged_mode && aligned && n_all >= kCountTile) {
+      const unsigned g = (unsigned)((n_all + kCountTile - 1) / kCountTile);  // one tile per CTA
+      if (brec)
+        lod::launch(k_count_staged<true>, g, kCountTile, 0, st, t->nd, t->geo, src, node_of, n_all, grid32, hs,
+                    t->d_ctrl);
+      else
+        lod::launch(k_count_staged<false>, g, kCountTile, 0, st, t->nd, t->geo, src, node_of, n_all, grid32, hs,
+                    t->d_ctrl);
+    } else {
+      lod::launch(k_count, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, node_of, n_all, first, grid32, hs,
+                  t->d_ctrl);
+    }
     if (first) RK(issue_pending(t));  // queued batches' copies start once this count pass is done
     if (prof) cudaEventRecord(t->ev[13], st);
     lod::launch(k_decide_mark, grid_for(t->num_nodes), 256, 0, st, t->nd, t->geo, (long long)t->num_nodes, t->bitmap.p);
@@ -1433,6 +1457,9 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   fill_stats(t, &S);
   exact_bounds(t);  // the counters published behind k_alloc are final
   t->ingested += n;
+  t->last_backlog = t->backlog.p;
+  t->last_nv = n_v;
+  t->last_ns = n_s;
   float ms = -1.f;
   if (early) {  // the tail is still running: its time is reported by the next call / lod_tree_wait
     t->tail_pending = true;
@@ -1558,6 +1585,189 @@ int lod_read_pool(LodTree *t, int64_t n, int32_t *next, int64_t *payload_off, in
   if (free_list && n_free)
     CK(cudaMemcpyAsync(free_list, t->pool.free_stack, n_free * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  return LOD_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- replicated top nodes
+
+// The last cycle's new voxels at nodes above `max_level`, with their winner's
+// batch position (all-array index - spill length): compacted, unordered.
+__global__ void k_last_voxels(NodeCols nd, const uint4 *__restrict__ backlog, long long nv, int max_level,
+                              long long n_s, long long cap, int32_t *node, uint32_t *cell, uint32_t *rgba,
+                              long long *winner, unsigned long long *count) {
+  lod::pdl_wait();
+  for (long long i = gtid(); i < nv; i += gstride()) {
+    const uint4 e = backlog[i];
+    if (nd.level[e.x] >= max_level) continue;
+    const unsigned long long k = atomicAdd(count, 1ull);
+    if ((long long)k >= cap) continue;
+    node[k] = (int32_t)e.x;
+    cell[k] = e.y;
+    rgba[k] = e.z;
+    winner[k] = (long long)e.w - n_s;
+  }
+}
+
+// Rewrite / extend the voxel sequences of listed nodes (lod_merge_voxels):
+// one warp per group; lane 0 links the chunks the longer sequence needs
+// (acquisitions numbered by an atomic counter: LIFO free stack first, then
+// arena cuts, k_merge_finish settles the counters), the warp writes the
+// records and sets the cells' grid bits.
+__global__ void k_merge_groups(NodeCols nd, PoolCols pool, Geo geo, uint8_t *arena, long long n_groups,
+                               const int32_t *__restrict__ gnode, const long long *__restrict__ gstart,
+                               const long long *__restrict__ goff, const uint32_t *__restrict__ cell,
+                               const uint32_t *__restrict__ rgba, Ctrl *c, unsigned long long *acq,
+                               unsigned long long arena_cap) {
+  lod::pdl_wait();
+  const long long warp = gtid() >> 5, nw = gstride() >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long F = c->free_count, A = c->allocated_total, C = geo.C;
+  const unsigned long long base = (c->arena_off + 15ull) / 16ull * 16ull;
+  uint32_t *grid32 = reinterpret_cast<uint32_t *>(arena);
+  for (long long g = warp; g < n_groups; g += nw) {
+    const int nid = gnode[g];
+    const long long start = gstart[g], len = goff[g + 1] - goff[g], cnt1 = start + len;
+    if (lane == 0) {
+      const long long cc = nd.chunk_count[nid], need = ceil_div(cnt1, C) - cc;
+      if (need > 0) {
+        const long long a0 = (long long)atomicAdd(acq, (unsigned long long)need);
+        auto cid_of = [&](long long a) { return a < F ? pool.free_stack[F - 1 - a] : (int)(A + (a - F)); };
+        int tail = nd.chunk_tail[nid];
+        for (long long q = 0; q < need; ++q) {
+          const long long a = a0 + q;
+          const int cid = cid_of(a);
+          if (a >= F) {
+            const unsigned long long off = base + (unsigned long long)(a - F) * (unsigned long long)C * 16ull;
+            if (off + (unsigned long long)C * 16ull > arena_cap) c->error = 1;  // LOD_E_OUT_OF_ARENA
+            pool.payload_off[cid] = (long long)off;
+          }
+          pool.next[cid] = LOD_NO_CHUNK;
+          pool.owner[cid] = nid;
+          pool.cidx[cid] = (int)(cc + q);
+          if (tail != LOD_NO_CHUNK) pool.next[tail] = cid;
+          else nd.chunk_head[nid] = cid;
+          tail = cid;
+        }
+        nd.chunk_tail[nid] = tail;
+        nd.chunk_count[nid] = (int)(cc + need);
+        dir_append(nd, pool, &c->dir_top, nid, need, [&](long long q) { return cid_of(a0 + q); });
+      }
+    }
+    __syncwarp();
+    const long long off0 = nd.dir_off[nid];
+    const double step = geo.size_by_level[nd.level[nid]] / (double)geo.g;
+    const double b0 = nd.bmin[3 * nid], b1 = nd.bmin[3 * nid + 1], b2 = nd.bmin[3 * nid + 2];
+    const long long gg = geo.g;
+    for (long long i = lane; i < len; i += 32) {
+      const long long slot = start + i, cl = cell[goff[g] + i];
+      const long long cx = cl % gg, cy = (cl / gg) % gg, cz = cl / (gg * gg);
+      const float4 rec = make_float4(__double2float_rn(b0 + ((double)cx + 0.5) * step),
+                                     __double2float_rn(b1 + ((double)cy + 0.5) * step),
+                                     __double2float_rn(b2 + ((double)cz + 0.5) * step),
+                                     __uint_as_float(rgba[goff[g] + i]));
+      const int cid = pool.cdir[off0 + slot / C];
+      reinterpret_cast<float4 *>(arena + pool.payload_off[cid])[slot % C] = rec;
+      atomicOr(grid32 + (nd.grid_off[nid] >> 2) + (cl >> 5), 1u << (cl & 31));
+    }
+    __syncwarp();
+    if (lane == 0) {
+      for (long long pos = start / C; pos * C < cnt1; ++pos)  // occupancy of the rewritten chunks
+        pool.occupied[pool.cdir[off0 + pos]] = (int)min(C, cnt1 - pos * C);
+      nd.count[nid] = cnt1;
+    }
+  }
+}
+
+__global__ void k_merge_finish(Ctrl *c, const unsigned long long *acq, unsigned long long arena_cap, Geo geo) {
+  lod::pdl_wait();
+  const long long M = (long long)*acq, F = c->free_count;
+  const long long fresh = M > F ? M - F : 0;
+  if (fresh > 0) {
+    const unsigned long long end =
+        (c->arena_off + 15ull) / 16ull * 16ull + (unsigned long long)fresh * (unsigned long long)geo.C * 16ull;
+    if (end > arena_cap) c->error = 1;
+    else c->arena_off = end;
+  }
+  c->free_count = F - (M < F ? M : F);
+  c->allocated_total += fresh;
+}
+
+extern "C" {
+
+int lod_last_voxels(LodTree *t, int32_t max_level, int64_t capacity, int32_t *node, uint32_t *cell, uint32_t *rgba,
+                    int64_t *winner, int64_t *n) {
+  if (!t || !n || capacity < 0 || (capacity > 0 && (!node || !cell || !rgba || !winner))) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  if (!t->last_backlog && t->last_nv) return LOD_E_ARG;
+  cudaStream_t st = t->st;
+  const long long nv = t->last_backlog ? t->last_nv : 0;
+  RK(t->counter.ensure(4, st));
+  RK(t->gnodes.ensure(std::max<long long>(capacity, 1), st));
+  RK(t->goff.ensure(std::max<long long>(capacity, 1), st));
+  RK(t->dvcell.ensure(std::max<long long>(2 * capacity, 1), st));
+  unsigned long long *cnt = t->counter.p + 2;
+  CK(cudaMemsetAsync(cnt, 0, 8, st));
+  if (nv)
+    lod::launch(k_last_voxels, grid_for(nv), 256, 0, st, t->nd, t->last_backlog, nv, (int)max_level, t->last_ns,
+                (long long)capacity, t->gnodes.p, t->dvcell.p, t->dvcell.p + std::max<long long>(capacity, 1),
+                t->goff.p, cnt);
+  unsigned long long k = 0;
+  CK(cudaMemcpyAsync(&k, cnt, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *n = (int64_t)k;
+  if ((long long)k > capacity) return capacity == 0 ? LOD_OK : LOD_E_ARG;  // query: *n is the size
+  if (k) {
+    CK(cudaMemcpyAsync(node, t->gnodes.p, k * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(cell, t->dvcell.p, k * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rgba, t->dvcell.p + std::max<long long>(capacity, 1), k * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(winner, t->goff.p, k * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return LOD_OK;
+}
+
+int lod_merge_voxels(LodTree *t, int64_t n_groups, const int32_t *gnode, const int64_t *gstart, const int64_t *goff,
+                     const uint32_t *cell, const uint32_t *rgba) {
+  if (!t || n_groups < 0 || (n_groups > 0 && (!gnode || !gstart || !goff))) return LOD_E_ARG;
+  if (n_groups == 0) return LOD_OK;
+  cudaSetDevice(t->dev);
+  RK(refresh(t));
+  cudaStream_t st = t->st;
+  const long long items = goff[n_groups];
+  if (items > 0 && (!cell || !rgba)) return LOD_E_ARG;
+  for (long long g = 0; g < n_groups; ++g)
+    if (gnode[g] < 0 || gnode[g] >= t->num_nodes || gstart[g] < 0 || goff[g + 1] < goff[g]) return LOD_E_ARG;
+  const long long acq_bound = items / t->geo.C + n_groups + 1;
+  const long long alloc = t->h_ctrl->allocated_total;
+  RK(ensure_chunks(t, alloc + acq_bound + 1, alloc));
+  RK(ensure_dir(t, alloc + acq_bound + 1, n_groups));
+  RK(t->gnodes.ensure(n_groups, st));
+  RK(t->gstart.ensure(n_groups, st));
+  RK(t->goff.ensure(n_groups + 1, st));
+  RK(t->dvcell.ensure(std::max<long long>(items, 1), st));
+  RK(t->dvrgba.ensure(std::max<long long>(items, 1), st));
+  RK(t->counter.ensure(4, st));
+  CK(cudaMemcpyAsync(t->gnodes.p, gnode, n_groups * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(t->gstart.p, gstart, n_groups * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(t->goff.p, goff, (n_groups + 1) * 8, cudaMemcpyHostToDevice, st));
+  if (items) {
+    CK(cudaMemcpyAsync(t->dvcell.p, cell, items * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(t->dvrgba.p, rgba, items * 4, cudaMemcpyHostToDevice, st));
+  }
+  unsigned long long *acq = t->counter.p + 3;
+  CK(cudaMemsetAsync(acq, 0, 8, st));
+  lod::launch(k_merge_groups, grid_for(n_groups * 32), 256, 0, st, t->nd, t->pool, t->geo, t->arena, (long long)n_groups,
+              t->gnodes.p, t->gstart.p, t->goff.p, t->dvcell.p, t->dvrgba.p, t->d_ctrl, acq, t->arena_cap);
+  lod::launch(k_merge_finish, 1, 1, 0, st, t->d_ctrl, (const unsigned long long *)acq, t->arena_cap, t->geo);
+  RK(sync_ctrl(t));
+  exact_bounds(t);
+  if (t->h_ctrl->error) {
+    const int e = t->h_ctrl->error;
+    CK(cudaMemsetAsync(&t->d_ctrl->error, 0, 4, st));
+    return e;
+  }
   return LOD_OK;
 }
 

@@ -91,16 +91,19 @@ def owners_device(xyz, plan: partition.Plan, bmin=(0.0, 0.0, 0.0), size: float =
     return owner[key]
 
 
-def bucket(xyz, rgba, plan: partition.Plan, world: int, bmin=(0.0, 0.0, 0.0), size: float = 1.0):
+def bucket(xyz, rgba, plan: partition.Plan, world: int, bmin=(0.0, 0.0, 0.0), size: float = 1.0,
+           positions: bool = False):
     """Stable bucketing of one stripe by owner rank into packed 16-byte records
     (CUDA tensors in; lod_route_bucket: owner prefix + per-tile counts, scans,
     warp-ordered stable scatter).  Returns (records (n, 4) int32, counts (world,)
-    int64, starts (world,) int64), all on the device."""
+    int64, starts (world,) int64), all on the device, plus with ``positions``
+    every record's index in the stripe (int32)."""
     import torch
 
     dev = xyz.device
     n = int(rgba.shape[0])
     out = torch.empty((n, 4), dtype=torch.int32, device=dev)
+    pos = torch.empty(n, dtype=torch.int32, device=dev) if positions else None
     counts = torch.empty(world, dtype=torch.int64, device=dev)
     starts = torch.empty(world, dtype=torch.int64, device=dev)
     table = np.ascontiguousarray(plan.owner, np.int32)
@@ -109,17 +112,20 @@ def bucket(xyz, rgba, plan: partition.Plan, world: int, bmin=(0.0, 0.0, 0.0), si
     c = rgba.contiguous()
     L = _lib.load()
     _lib.check(L.lod_route_bucket(dev.index, _lib.ptr(b), float(size), int(plan.depth), _lib.ptr(table), int(world),
-                                  _lib.ptr(x), _lib.ptr(c), n, _lib.ptr(out), _lib.ptr(counts), _lib.ptr(starts),
-                                  torch.cuda.current_stream(dev).cuda_stream), "route_bucket")
-    return out, counts, starts
+                                  _lib.ptr(x), _lib.ptr(c), n, _lib.ptr(out), _lib.ptr(pos), _lib.ptr(counts),
+                                  _lib.ptr(starts), torch.cuda.current_stream(dev).cuda_stream), "route_bucket")
+    return (out, counts, starts, pos) if positions else (out, counts, starts)
 
 
-def route(xyz, rgba, plan: partition.Plan, world: int, group=None, bmin=(0.0, 0.0, 0.0), size: float = 1.0):
+def route(xyz, rgba, plan: partition.Plan, world: int, group=None, bmin=(0.0, 0.0, 0.0), size: float = 1.0,
+          with_index: bool = False):
     """All-to-all routing of one stripe (global order) to the owners of its
     points; returns this rank's points as packed 16-byte records (n, 4) int32
-    in global order (receivers concatenate by source rank).  ``bmin`` / ``size``
-    are the tree's root cube (``tree.bounds``): the octant prefix is computed
-    against it, like ``partition.plan_owners`` must be.
+    in global order (receivers concatenate by source rank), and with
+    ``with_index`` each point's index in the global batch (int64; the order
+    the replicated top nodes' voxels merge in).  ``bmin`` / ``size`` are the
+    tree's root cube (``tree.bounds``): the octant prefix is computed against
+    it, like ``partition.plan_owners`` must be.
 
     CUDA tensors are bucketed by the lod_route_bucket kernels; CPU tensors
     (the gloo test path) by the same rule in torch."""
@@ -127,18 +133,31 @@ def route(xyz, rgba, plan: partition.Plan, world: int, group=None, bmin=(0.0, 0.
     import torch.distributed as dist
 
     if xyz.is_cuda:
-        rec, send_counts, _ = bucket(xyz, rgba, plan, world, bmin, size)
+        rec, send_counts, _, pos = bucket(xyz, rgba, plan, world, bmin, size, positions=True)
     else:
         own = owners_device(xyz, plan, bmin, size)
         order = torch.sort(own, stable=True).indices  # bucket by owner, keep order
         rec = torch.cat([xyz.contiguous().view(torch.int32), rgba.view(torch.int32).reshape(-1, 1)], dim=1)[order]
+        pos = order.to(torch.int32)
         send_counts = torch.bincount(own, minlength=world).to(torch.int64)
-    if xyz.is_cuda and dist.get_backend(group) == "gloo":
-        # gloo has no CUDA all-to-all: the exchange goes through host copies
-        # (single-box validation of this path; NCCL moves device memory)
-        out = _all_to_all_records(rec.cpu(), send_counts.cpu(), group)
-        return out.to(xyz.device)
-    return _all_to_all_records(rec, send_counts, group)
+    # every rank's stripe length -> the global index of a stripe position
+    n_local = torch.tensor([int(rgba.shape[0])], dtype=torch.int64, device=send_counts.device)
+    sizes = [torch.zeros_like(n_local) for _ in range(world)]
+    dist.all_gather(sizes, n_local, group=group)
+    stripe_off = np.concatenate([[0], np.cumsum([int(t.item()) for t in sizes])])[:-1]
+    gloo_cuda = xyz.is_cuda and dist.get_backend(group) == "gloo"
+    dev = xyz.device
+    if gloo_cuda:  # gloo has no CUDA all-to-all: the exchange goes through host copies
+        rec, send_counts, pos = rec.cpu(), send_counts.cpu(), pos.cpu()
+    out, recv_counts = _all_to_all_records(rec, send_counts, group)
+    if not with_index:
+        return out.to(dev) if gloo_cuda else out
+    got_pos, _ = _all_to_all_records(pos.reshape(-1, 1), send_counts, group)
+    src = torch.repeat_interleave(torch.arange(world, device=got_pos.device), recv_counts.to(got_pos.device))
+    gidx = torch.as_tensor(stripe_off, device=got_pos.device)[src] + got_pos.reshape(-1).to(torch.int64)
+    if gloo_cuda:
+        out, gidx = out.to(dev), gidx.to(dev)
+    return out, gidx
 
 
 def _all_to_all_records(rec, send_counts, group):
@@ -148,9 +167,9 @@ def _all_to_all_records(rec, send_counts, group):
     recv_counts = torch.empty_like(send_counts)
     dist.all_to_all_single(recv_counts, send_counts, group=group)
     rc, sc = recv_counts.tolist(), send_counts.tolist()
-    out = torch.empty((sum(rc), 4), dtype=torch.int32, device=rec.device)
+    out = torch.empty((sum(rc),) + tuple(rec.shape[1:]), dtype=rec.dtype, device=rec.device)
     dist.all_to_all_single(out, rec.contiguous(), rc, sc, group=group)
-    return out
+    return out, recv_counts
 
 
 def composite_min(fb_cells_dev, group=None):
@@ -274,7 +293,8 @@ class PeerRouter:
 
     @staticmethod
     def _bytes(half_records: int) -> int:
-        return _lib.LOD_WINDOW_HEADER_BYTES + 2 * 16 * half_records
+        # header | records half 0 | records half 1 | positions half 0 | positions half 1
+        return _lib.LOD_WINDOW_HEADER_BYTES + 2 * 16 * half_records + 2 * 4 * half_records
 
     def _begin(self, x, n: int, stream: int) -> None:
         import ctypes
@@ -312,7 +332,21 @@ class PeerRouter:
         self.k += 1
         mine = int(self.matrix[:, self.rank].sum())
         base = self.win.own + _lib.LOD_WINDOW_HEADER_BYTES + half * 16 * self.half_records
+        pbase = self.win.own + _lib.LOD_WINDOW_HEADER_BYTES + 2 * 16 * self.half_records + half * 4 * self.half_records
+        self.last_positions = _device_view(pbase, (mine,), torch.int32, self.device)
         return _device_view(base, (mine, 4), torch.int32, self.device)
+
+    def global_index(self):
+        """Global-batch index of every record of the last route(): the
+        records from source s sit behind the lower sources' (column of the
+        count matrix) and carry their position in s's stripe."""
+        import torch
+
+        col = self.matrix[:, self.rank]
+        stripe_off = np.concatenate([[0], np.cumsum(self.matrix.sum(axis=1))])[:-1]
+        dev = self.last_positions.device
+        src = torch.repeat_interleave(torch.arange(self.world, device=dev), torch.as_tensor(col, device=dev))
+        return torch.as_tensor(stripe_off, device=dev)[src] + self.last_positions.to(torch.int64)
 
     def close(self) -> None:
         self.win.close()
@@ -392,6 +426,57 @@ def owned_cut(tree, selected, plan: partition.Plan, rank: int) -> list[int]:
     return keep
 
 
+def last_top_voxels(tree, depth: int):
+    """(node, cell, rgba, winner) of the voxels the tree's last insert created
+    at nodes above the partition depth (level < depth), the winner as its
+    batch position (lod_last_voxels; in no particular order)."""
+    import ctypes
+
+    L = tree._L
+    n = ctypes.c_int64(0)
+    _lib.check(L.lod_last_voxels(tree.handle, int(depth), 0, None, None, None, None, ctypes.byref(n)), "last_voxels")
+    k = int(n.value)
+    node, cell = np.empty(k, np.int32), np.empty(k, np.uint32)
+    rgba, win = np.empty(k, np.uint32), np.empty(k, np.int64)
+    if k:
+        _lib.check(L.lod_last_voxels(tree.handle, int(depth), k, _lib.ptr(node), _lib.ptr(cell), _lib.ptr(rgba),
+                                     _lib.ptr(win), ctypes.byref(n)), "last_voxels")
+    assert (win >= 0).all(), "a spilled point claimed a replicated top-node cell"
+    return node, cell, rgba, win
+
+
+def merge_top_voxels(tree, own_nodes: np.ndarray, everyone) -> int:
+    """Make this rank's copies of the replicated top nodes hold the
+    single-tree voxel sequences ("all-gathered and merged by
+    global index").  ``everyone`` lists every rank's (node, cell, rgba,
+    global index) of the voxels its last cycle created at top nodes --
+    top-node cells split along prefix boundaries, so each cell was claimed on
+    exactly one rank and the winners are the single tree's; only their order
+    in a node's sequence interleaves across ranks: ascending global index.
+    ``own_nodes``: the node column of this rank's own items.  Each top node
+    that got voxels anywhere is rewritten from the position its sequence had
+    before the cycle (lod_merge_voxels).  Returns the voxels merged."""
+    import ctypes
+
+    node = np.concatenate([np.asarray(e[0], np.int32) for e in everyone])
+    if not len(node):
+        return 0
+    cell = np.concatenate([np.asarray(e[1], np.uint32) for e in everyone])
+    rgba = np.concatenate([np.asarray(e[2], np.uint32) for e in everyone])
+    gidx = np.concatenate([np.asarray(e[3], np.int64) for e in everyone])
+    order = np.lexsort((gidx, node))  # by node, then global index
+    node, cell, rgba = node[order], np.ascontiguousarray(cell[order]), np.ascontiguousarray(rgba[order])
+    gnode, first = np.unique(node, return_index=True)
+    goff = np.append(first, len(node)).astype(np.int64)
+    own = np.bincount(np.asarray(own_nodes, np.int64), minlength=int(gnode.max()) + 1)
+    gstart = (tree.count[gnode] - own[gnode]).astype(np.int64)
+    gnode = gnode.astype(np.int32)
+    _lib.check(tree._L.lod_merge_voxels(tree.handle, len(gnode), _lib.ptr(gnode), _lib.ptr(gstart), _lib.ptr(goff),
+                                        _lib.ptr(cell), _lib.ptr(rgba)), "merge_voxels")
+    tree._invalidate()
+    return len(node)
+
+
 def check_plan(tree, plan: partition.Plan) -> None:
     """The partition invariants the protocol relies on: the plan covers every
     depth-L prefix, and no cell of a replicated top node straddles a prefix
@@ -419,6 +504,7 @@ class PartitionedInserter:
         self.partitioned = world == 1
         self.router = None  # PeerRouter, created at the first partitioned batch
         self.no_peers = ""  # why the peer route is unavailable (then: NCCL all-to-all)
+        self.merged_top = 0  # top-node voxels merged across ranks so far
 
     def insert(self, xyz, rgba) -> int:
         """Insert this rank's stripe of one global batch; returns points inserted here."""
@@ -440,9 +526,11 @@ class PartitionedInserter:
                     self.no_peers = str(e)
             if self.router is not None:
                 rec = self.router.route(xyz, rgba)
+                gidx = self.router.global_index()
             else:
-                rec = route(xyz, rgba, self.plan, self.world, self.group, self.bmin, self.size)
+                rec, gidx = route(xyz, rgba, self.plan, self.world, self.group, self.bmin, self.size, with_index=True)
             insert_records(self.tree, rec, self.state)
+            self._merge_top(gidx)
             return int(rec.shape[0])
         # warm-up: gather stripes to rank 0 (rank order = global order)
         n = torch.tensor([rgba.shape[0]], dtype=torch.int64, device=xyz.device)
@@ -465,6 +553,18 @@ class PartitionedInserter:
         if int(flag.item()):
             self.hand_off()
         return got
+
+    def _merge_top(self, gidx) -> None:
+        """All-gather the top-node voxels of this batch with their winners'
+        global indices and merge them into every rank's top nodes."""
+        import torch
+        import torch.distributed as dist
+
+        node, cell, rgba, win = last_top_voxels(self.tree, self.plan.depth)
+        g = gidx[torch.from_numpy(win).to(gidx.device)].cpu().numpy() if len(win) else np.empty(0, np.int64)
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, (node, cell, rgba, g), group=self.group)
+        self.merged_top += merge_top_voxels(self.tree, node, everyone)
 
     def close(self) -> None:
         """Release the peer windows (collective)."""

@@ -234,3 +234,83 @@ def assert_same_state(got: dict, want: dict, *, chunk_ids: bool, label: str = ""
         raise AssertionError(f"{label}: {len(bad)} sample records differ, first at node {node}")
     assert np.array_equal(got["cell_offsets"], want["cell_offsets"]), f"{label}: bitgrid popcounts differ"
     assert np.array_equal(got["cells"], want["cells"]), f"{label}: occupied cells differ"
+
+
+# -- multi-GPU protocol, emulated on one GPU -------------------------------------------
+
+
+def emulate_partitioned(params: dict, batches, plan, merge: bool = True):
+    """The warm-up / hand-off / partitioned protocol (multigpu.py) with
+    len(plan.load) ranks as trees on one GPU: every batch goes into the single
+    tree `g`; rank 0 takes whole batches until the top is inner, its packed
+    state is unpacked into the other ranks; later batches are routed by exact
+    octant prefix (partition.take: global order within a rank) and, with
+    `merge`, the top-node voxels of every batch are merged across ranks by the
+    winners' global indices (multigpu.merge_top_voxels).  Returns
+    (g, ranks [(tree, state)], handed_off_at)."""
+    from paper_2310_03567_b200 import insert_batch, multigpu, partition
+
+    world = len(plan.load)
+    g, gs = make_product(params)
+    ranks = [make_product(params) for _ in range(world)]
+    handed = None
+    for bi, (x, c) in enumerate(batches):
+        insert_batch(g, x, c, gs)
+        if handed is None:
+            insert_batch(ranks[0][0], x, c, ranks[0][1])
+            if multigpu.top_is_inner(ranks[0][0], plan.depth):
+                buf = multigpu.pack_tree(ranks[0][0])
+                for r in range(1, world):
+                    multigpu.unpack_tree(ranks[r][0], buf)
+                handed = bi
+            continue
+        owner = plan.owner[partition.prefix_of(x, plan.depth, params["bmin"], params["size"])]
+        everyone, own_nodes = [], []
+        for r in range(world):
+            pos = np.flatnonzero(owner == r)
+            if len(pos):
+                insert_batch(ranks[r][0], np.ascontiguousarray(x[pos]), np.ascontiguousarray(c[pos]), ranks[r][1])
+                node, cell, rgba, win = multigpu.last_top_voxels(ranks[r][0], plan.depth)
+                everyone.append((node, cell, rgba, pos[win]))
+                own_nodes.append(node)
+            else:
+                everyone.append((np.empty(0, np.int32),) * 2 + (np.empty(0, np.uint32), np.empty(0, np.int64)))
+                own_nodes.append(np.empty(0, np.int32))
+        if merge:
+            for r in range(world):
+                multigpu.merge_top_voxels(ranks[r][0], own_nodes[r], everyone)
+    return g, ranks, handed
+
+
+def assert_union_equals_single(g, ranks, plan, label: str = "") -> int:
+    """Node for node, by octant path: prefix subtrees on their owner, and the
+    replicated top nodes on EVERY rank, equal the single tree (kind, sample
+    sequence, occupied cells).  Returns the nodes compared."""
+    from oracle.rebuild import tree_paths
+
+    gp = tree_paths(g.inner, g.children)
+    g_off, g_rec = g.dump_records()
+    rp = [tree_paths(t.inner, t.children) for t, _ in ranks]
+    dumps = [t.dump_records() for t, _ in ranks]
+    checked = 0
+    for path, nid in gp.items():
+        if len(path) < plan.depth:
+            holders = range(len(ranks))
+        else:
+            prefix = 0
+            for o in path[:plan.depth]:
+                prefix = prefix * 8 + o
+            holders = [int(plan.owner[prefix])]
+        want = g_rec[g_off[nid]:g_off[nid + 1]].view(np.uint32)
+        for r in holders:
+            t = ranks[r][0]
+            assert path in rp[r], f"{label}: rank {r} lacks {path}"
+            rid = rp[r][path]
+            assert bool(t.inner[rid]) == bool(g.inner[nid]), f"{label}: kind at {path} on rank {r}"
+            ro, rr = dumps[r]
+            got = rr[ro[rid]:ro[rid + 1]].view(np.uint32)
+            assert got.shape == want.shape and np.array_equal(got, want), f"{label}: samples at {path} on rank {r}"
+            if g.inner[nid]:
+                assert np.array_equal(t.occupied_cells(rid), g.occupied_cells(nid)), f"{label}: cells {path} r{r}"
+            checked += 1
+    return checked

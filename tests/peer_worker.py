@@ -5,7 +5,9 @@ over gloo).  Every global batch arrives striped (rank r holds points
 off and then routes the stripes through PeerRouter (bucket scatter straight
 into the owners' IPC windows).  The rank then renders its tree into its
 PeerFramebuffers window, composites over peer memory, and writes its owned
-prefix subtrees (path -> samples) and the composite to OUT/rank<r>.npz.
+prefix subtrees (path -> samples), its copies of the replicated top nodes
+(merged by global index after every batch) and the composite to
+OUT/rank<r>.npz.
 
 A second, standalone PeerRouter with a deliberately small window checks the
 collective window growth and the routed records against the bucketing rule
@@ -65,7 +67,11 @@ def main() -> None:
     assert ins.partitioned
     res = {}
     for path, nid in tree_paths(tree.inner, tree.children).items():
-        if len(path) < plan.depth:
+        if len(path) < plan.depth:  # a replicated top node: merged, every rank holds the single-tree sequence
+            xs, cs = tree.gather_samples(nid)
+            key = "t_" + "".join(map(str, path))
+            res[key] = np.concatenate([xs.view(np.uint32), cs.reshape(-1, 1)], axis=1)
+            res["tg_" + key[2:]] = tree.occupied_cells(nid)
             continue
         prefix = 0
         for o in path[: plan.depth]:

@@ -2,10 +2,12 @@
 
 Warm-up batches go to rank 0 until the top is inner; its state is packed and
 unpacked into the other ranks (lod_tree_pack/unpack); later batches are routed
-by exact octant prefix.  Every prefix subtree of its owner must equal the
-single-tree run path by path; top nodes must hold the common prefix plus
-rank-disjoint new voxels whose union is the single-tree sequence; and the
-min-composite of the ranks' renders must equal the single-tree render.
+by exact octant prefix, and after every batch the replicated top nodes'
+new voxels are merged across ranks by their winners' global indices
+(multigpu.merge_top_voxels).  The union must equal the single-tree run node
+for node: every prefix subtree on its owner and every top node on every rank
+(kind, sample sequence, bitgrid); and the min-composite of the ranks' renders
+must equal the single-tree render.
 """
 import numpy as np
 import pytest
@@ -31,63 +33,19 @@ def _samples(tree, nid):
 
 @pytest.mark.parametrize("world", [2, 4])
 def test_partitioned_ranks_match_single_tree(gpu, world):
-    from paper_2310_03567_b200 import insert_batch, multigpu, partition, synth
+    from paper_2310_03567_b200 import partition, synth
     from paper_2310_03567_b200.render import Camera, Framebuffer, rasterize
+
+    from common import assert_union_equals_single, emulate_partitioned
 
     batches = [synth.gen_surface(40_000, 300 + i) for i in range(12)]
     plan = partition.plan_owners(batches[:2], world, depth=1)
-    g, gs = make_product(P)
-    ranks = [make_product(P) for _ in range(world)]
-    handed_off = False
-    pre = None
-    for x, c in batches:
-        insert_batch(g, x, c, gs)
-        if not handed_off:
-            insert_batch(ranks[0][0], x, c, ranks[0][1])
-            if multigpu.top_is_inner(ranks[0][0], plan.depth):
-                buf = multigpu.pack_tree(ranks[0][0])
-                for r in range(1, world):
-                    multigpu.unpack_tree(ranks[r][0], buf)
-                handed_off = True
-                pre = {p: _samples(ranks[0][0], nid) for p, nid in _paths(ranks[0][0]).items() if len(p) < plan.depth}
-            continue
-        for r in range(world):
-            xr, cr = partition.take(plan, x, c, r)
-            if len(cr):
-                insert_batch(ranks[r][0], xr, cr, ranks[r][1])
-    assert handed_off
-    gp = _paths(g)
+    g, ranks, handed = emulate_partitioned(P, batches, plan)
+    assert handed is not None and handed < len(batches) - 2
+    # every node of the single tree, node for node: prefix subtrees on their
+    # owner, the merged top nodes on every rank
+    assert assert_union_equals_single(g, ranks, plan, label=f"x{world}") > 50
     rp = [_paths(t) for t, _ in ranks]
-    # prefix subtrees: identical to the single tree, path by path
-    for path, nid in gp.items():
-        if len(path) < plan.depth:
-            continue
-        prefix = 0
-        for o in path[: plan.depth]:
-            prefix = prefix * 8 + o
-        r = int(plan.owner[prefix])
-        t = ranks[r][0]
-        assert path in rp[r], path
-        rid = rp[r][path]
-        assert bool(t.inner[rid]) == bool(g.inner[nid]), path
-        assert np.array_equal(_samples(t, rid), _samples(g, nid)), path
-        if g.inner[nid]:
-            assert np.array_equal(t.occupied_cells(rid), g.occupied_cells(nid)), path
-    # top nodes: common prefix + rank-disjoint appended voxels
-    for path, nid in gp.items():
-        if len(path) >= plan.depth:
-            continue
-        want = _samples(g, nid)
-        base = pre[path]
-        assert np.array_equal(want[: len(base)], base), path
-        rest = [_samples(t, rp[r][path])[len(base):] for r, (t, _) in enumerate(ranks)]
-        cat = np.concatenate(rest)
-        assert len(cat) == len(want) - len(base), path
-        keys = lambda a: set(map(tuple, a.tolist()))
-        assert keys(cat) == keys(want[len(base):]), path
-        for a in range(world):
-            for b in range(a + 1, world):
-                assert not (keys(rest[a]) & keys(rest[b])), path
     # render: min-composite of per-rank renders (owned subtrees + top) == single tree
     cam = Camera((0.5, 0.45, -1.3), (0.5, 0.5, 0.5), fov_deg=60.0, near=0.05, far=50.0, width=320, height=240)
     for thr in (-1.0, 64.0):

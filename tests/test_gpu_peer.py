@@ -3,8 +3,9 @@ PeerFramebuffers: CUDA IPC windows, bucket scatter straight into the owners'
 windows, depth-min composite over peer memory) run for real: N processes under
 torchrun sharing the test box's GPU, ordered over gloo (tests/peer_worker.py).
 Every owned prefix subtree must equal the single-tree run path by path
-(samples and grid cells), and every rank's composite must equal the
-single-tree render."""
+(samples and grid cells), every rank's copy of every top node must equal the
+single tree's (the voxels merged by global index), and every rank's
+composite must equal the single-tree render."""
 import os
 import socket
 import subprocess
@@ -60,6 +61,15 @@ def test_peer_route_and_composite_match_single_tree(gpu, tmp_path, world, depth)
         assert np.array_equal(d["p_" + key], np.concatenate([xs.view(np.uint32), cs.reshape(-1, 1)], axis=1)), path
         if g.inner[gp[path]]:
             assert np.array_equal(d["g_" + key], g.occupied_cells(gp[path])), path
+    # the replicated top nodes: every rank's copy is the single-tree sequence
+    top = [p for p in gp if len(p) < depth]
+    for path in top:
+        key = "".join(map(str, path))
+        xs, cs = g.gather_samples(gp[path])
+        want = np.concatenate([xs.view(np.uint32), cs.reshape(-1, 1)], axis=1)
+        for k, d in enumerate(ranks):
+            assert np.array_equal(d["t_" + key], want), (path, k)
+            assert np.array_equal(d["tg_" + key], g.occupied_cells(gp[path])), (path, k)
     cam = Camera((0.5, 0.45, -1.3), (0.5, 0.5, 0.5), fov_deg=60.0, near=0.05, far=50.0, width=320, height=240)
     for thr, name in ((-1.0, "comp_all"), (64.0, "comp_64")):
         want, _ = rasterize(g, cam, threshold=thr)

@@ -11,8 +11,8 @@
   camera, every frame's framebuffer vs the oracle's splat of the same
   selection, and the tree at the end;
 * config 5: the partition protocol at paper parameters on a 24M-point
-  terrain prefix, 2/4/8 ranks emulated on one GPU: every rank's prefix
-  subtrees equal the single-tree run path by path.
+  terrain prefix, 2/4/8 ranks emulated on one GPU, top-node voxels merged by
+  global index: the union equals the single-tree run node for node.
 
 The oracle (oracle/lod_oracle.c, a 1-thread C restatement pinned to the
 reference's own outputs) runs live; these tests take minutes.
@@ -118,51 +118,19 @@ def test_config3_mesh_frames(gpu):
 def test_config5_partition_protocol_paper_params(gpu, world):
     """The warm-up / hand-off / partitioned protocol at paper parameters: the
     single-tree run vs `world` emulated rank trees fed by exact octant-prefix
-    routing (plan over depth 1 for 2/4 ranks, depth 2 for 8)."""
-    from paper_2310_03567_b200 import insert_batch, multigpu, partition
-    from oracle.rebuild import tree_paths
+    routing (plan over depth 1 for 2/4 ranks, depth 2 for 8), the top nodes'
+    voxels merged across ranks by global index after every batch: the union
+    equals the single tree node for node."""
+    from paper_2310_03567_b200 import partition
+
+    from common import assert_union_equals_single, emulate_partitioned
 
     params = dict(PAPER, arena_bytes=6 << 30)
     batches = _stream("surface", 24, seed0=5000)
     plan = partition.plan_owners(batches[:2], world)
-    g, gs = make_product(params)
-    ranks = [make_product(params) for _ in range(world)]
-    handed = False
-    for x, c in batches:
-        insert_batch(g, x, c, gs)
-        if not handed:
-            insert_batch(ranks[0][0], x, c, ranks[0][1])
-            if multigpu.top_is_inner(ranks[0][0], plan.depth):
-                buf = multigpu.pack_tree(ranks[0][0])
-                for r in range(1, world):
-                    multigpu.unpack_tree(ranks[r][0], buf)
-                handed = True
-            continue
-        for r in range(world):
-            xr, cr = partition.take(plan, x, c, r)
-            if len(cr):
-                insert_batch(ranks[r][0], xr, cr, ranks[r][1])
-    assert handed
-    gp = tree_paths(g.inner, g.children)
-    rp = [tree_paths(t.inner, t.children) for t, _ in ranks]
-    g_off, g_rec = g.dump_records()
-    r_dump = [t.dump_records() for t, _ in ranks]
-    checked = 0
-    for path, nid in gp.items():
-        if len(path) < plan.depth:
-            continue
-        prefix = 0
-        for o in path[:plan.depth]:
-            prefix = prefix * 8 + o
-        r = int(plan.owner[prefix])
-        t = ranks[r][0]
-        assert path in rp[r], path
-        rid = rp[r][path]
-        assert bool(t.inner[rid]) == bool(g.inner[nid]), path
-        ro, rr = r_dump[r]
-        a = g_rec[g_off[nid]:g_off[nid + 1]].view(np.uint32)
-        b = rr[ro[rid]:ro[rid + 1]].view(np.uint32)
-        assert np.array_equal(a, b), path
-        checked += 1
+    g, ranks, handed = emulate_partitioned(params, batches, plan)
+    assert handed is not None and handed < 20
+    checked = assert_union_equals_single(g, ranks, plan, label=f"config5 x{world}")
     assert checked > 100
-    print(f"config 5 x{world}: {checked} prefix nodes equal, single tree {g.num_nodes} nodes")
+    print(f"config 5 x{world}: {checked} (node, rank) copies equal, single tree {g.num_nodes} nodes, "
+          f"hand-off after batch {handed}")

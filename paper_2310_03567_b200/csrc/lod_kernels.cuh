@@ -119,9 +119,12 @@ struct Hash {
   unsigned long long *used;  // slots inserted this cycle
   unsigned long long limit;  // capacity of `used` (= table capacity)
   unsigned long long tag;    // this cycle's epoch << 56 (0..254)
+  int cbits;                 // bits of a cell index (ceil log2 g^3): keys are {epoch:8, node:56-cbits, cell:cbits}
 };
 
-// Keys carry the cycle's epoch in their top byte ({epoch:8, node:24, cell:32});
+// Keys carry the cycle's epoch in their top byte ({epoch:8, node, cell}: the
+// node field takes the 56 - cbits bits the cell leaves, 35 at G = 128, so
+// node ids reach the reference's int32 range);
 // a slot is occupied iff its epoch is the current one.  Slots of earlier
 // cycles are simply stale -- nothing clears the table between cycles (the
 // clearing writes dirtied ~1.5M random sectors per batch that the next count
@@ -158,8 +161,13 @@ __device__ __forceinline__ unsigned long long next_slot(const Hash &h, unsigned 
   return s + 1 == h.cap ? 0ull : s + 1;
 }
 
-__device__ __forceinline__ unsigned long long claim_key(int nid, long long cell) {
-  return ((unsigned long long)(uint32_t)nid << 32) | (unsigned long long)cell;
+__device__ __forceinline__ unsigned long long claim_key(int nid, long long cell, int cbits) {
+  return ((unsigned long long)(uint32_t)nid << cbits) | (unsigned long long)cell;
+}
+constexpr unsigned long long kKeyLow56 = (1ull << 56) - 1;
+__device__ __forceinline__ int key_node(const Hash &h, unsigned long long k) { return (int)((k & kKeyLow56) >> h.cbits); }
+__device__ __forceinline__ uint32_t key_cell(const Hash &h, unsigned long long k) {
+  return (uint32_t)(k & ((1ull << h.cbits) - 1));
 }
 
 __device__ __forceinline__ void used_init(UsedStage &stg) {
@@ -247,7 +255,7 @@ __device__ __forceinline__ void probe_cell(const NodeCols &nd, const Geo &geo, c
                                            double inv_s, uint32_t v, uint32_t rgba) {
   const long long cell = cell_of(geo, x, y, z, bx, by, bz, s, inv_s);
   const uint32_t w = __ldg(grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5));
-  if (!(w & (1u << (cell & 31)))) hash_claim(h, stg, claim_key(nid, cell), v, rgba, ctrl);
+  if (!(w & (1u << (cell & 31)))) hash_claim(h, stg, claim_key(nid, cell, h.cbits), v, rgba, ctrl);
 }
 
 // Grow the claim table between expansion iterations: re-insert every key
@@ -294,7 +302,7 @@ __device__ __forceinline__ int count_descend(const NodeCols &nd, const Geo &geo,
       // lanes of a warp on one (node, cell): only the lowest claimant index
       // can win, the others need not touch the table (sorted input puts
       // many lanes on one cell)
-      const unsigned long long key = claim_key(cur, cell);
+      const unsigned long long key = claim_key(cur, cell, h.cbits);
       const unsigned peers = __match_any_sync(__activemask(), key);
       if (__reduce_min_sync(peers, v) == v) hash_claim(h, stg, key, v, col, ctrl);
     }
@@ -683,8 +691,8 @@ __global__ void __launch_bounds__(256)
   for (long long sidx = gtid(); sidx < H; sidx += gstride()) {
     const ulonglong2 kv = __ldcg(reinterpret_cast<const ulonglong2 *>(h.slots + sidx));
     if (!live(h, kv.x)) continue;
-    const int nid = (int)((kv.x >> 32) & 0xFFFFFFu);
-    const uint32_t cell = (uint32_t)(kv.x & 0xFFFFFFFFu);
+    const int nid = key_node(h, kv.x);
+    const uint32_t cell = key_cell(h, kv.x);
     atomicOr(grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5), 1u << (cell & 31));
     atomicAdd(wcount + claim_index((uint32_t)(kv.y >> 32), n_s), 1u);
   }
@@ -702,7 +710,7 @@ __global__ void __launch_bounds__(256)
     if (!live(h, kv.x)) continue;  // left in place: stale from the next cycle on
     const long long j = claim_index((uint32_t)(kv.y >> 32), n_s);
     const uint32_t b = __ldg(wbase + j) + atomicSub(wcount + j, 1u) - 1u;
-    backlog[b] = make_uint4((uint32_t)((kv.x >> 32) & 0xFFFFFFu), (uint32_t)(kv.x & 0xFFFFFFFFu), (uint32_t)kv.y,
+    backlog[b] = make_uint4((uint32_t)key_node(h, kv.x), key_cell(h, kv.x), (uint32_t)kv.y,
                             (uint32_t)j);  // .w: the winner's all-array index (lod_last_voxels)
   }
 }

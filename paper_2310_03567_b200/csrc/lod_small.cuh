@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_cycle(SmallArgs a) {
           cell = cell_of(geo, x, y, z, bx, by, bz, s, inv_s);
           const uint32_t w = __ldcg(grid32 + ((unsigned long long)(uint32_t)d.y << 4) + (cell >> 5));
           clear = !(w & (1u << (cell & 31)));
-          if (clear) key = claim_key(nid, cell);
+          if (clear) key = ((unsigned long long)(uint32_t)nid << 32) | (unsigned long long)cell;  // warp-local match key
         }
         const unsigned peers = __match_any_sync(0xffffffffu, key);
         const bool win = clear && (int)(__ffs(peers) - 1) == lane;

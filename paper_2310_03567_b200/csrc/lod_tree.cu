@@ -298,8 +298,8 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int k = 0; k < kResolveItems; ++k) {
       if (!live(h, kv[k].x)) continue;  // stale from the next cycle on: no clearing write
-      const int nid = (int)((kv[k].x >> 32) & 0xFFFFFFu);
-      const uint32_t cell = (uint32_t)(kv[k].x & 0xFFFFFFFFu);
+      const int nid = key_node(h, kv[k].x);
+      const uint32_t cell = key_cell(h, kv[k].x);
       const uint32_t j = (uint32_t)claim_index((uint32_t)(kv[k].y >> 32), n_s);
       atomicOr(grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5), 1u << (cell & 31));
       wins[pos] = make_uint4(j, (uint32_t)nid, cell, (uint32_t)kv[k].y);
@@ -442,10 +442,23 @@ static int grow_col(T *&ptr, long long old_cap, long long new_cap, long long kee
   return LOD_OK;
 }
 
+// Bits of a cell index (g^3 cells) and the node ids a claim key can hold
+// (int32 ids, like the reference's, capped by the key's 56 - cbits bits).
+static int cell_bits(long long g) {
+  const unsigned long long cells = (unsigned long long)g * g * g;
+  int b = 1;
+  while ((1ull << b) < cells) ++b;
+  return b;
+}
+static long long max_nodes(const LodTree *t) {
+  const int nb = 56 - cell_bits(t->geo.g);
+  return nb >= 31 ? (1LL << 31) - 1 : (1LL << nb);
+}
+
 // Node table capacity (Octree._grow doubling, octree.py:192-209).
 static int ensure_nodes(LodTree *t, long long want, long long live) {
   if (want <= t->ncap) return LOD_OK;
-  if (want > (1LL << 24)) return LOD_E_NOMEM;  // claim keys hold 24-bit node ids
+  if (want > max_nodes(t)) return LOD_E_NOMEM;  // claim keys hold 56 - cbits bits of node id
   long long nc = std::max<long long>(t->ncap, 1024);
   while (nc < want) nc *= 2;
   if (lod_debug()) fprintf(stderr, "[lod] grow node table %lld -> %lld\n", t->ncap, nc);
@@ -1121,7 +1134,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   if (t->hepoch == 0 && t->hslots.p)
     CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
   const unsigned long long htag = (unsigned long long)t->hepoch << 56;
-  Hash hs{t->hslots.p, t->hcap, t->hused.p, t->hcap, htag};
+  const int cbits = cell_bits(t->geo.g);
+  Hash hs{t->hslots.p, t->hcap, t->hused.p, t->hcap, htag, cbits};
   uint32_t *grid32 = reinterpret_cast<uint32_t *>(t->arena);
   // ---- post-expansion pipeline: resolve -> backlog -> alloc -> sort+store ->
   // [delta] -> epilogue.  Launched either after the expansion settled (guard
@@ -1134,6 +1148,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     const long long num_nodes = t->num_nodes;
     // sort scratch first: the burst resolve sorts its win list with it
     const long long n_items = n_all + nv;  // exact, or an upper bound (the device count is Ctrl.n_items)
+    // the packed node plans count touched nodes in 24 bits (kPackShift)
+    if (num_nodes >= (1LL << 24) && n_items >= (1LL << 24)) return LOD_E_ARG;
     const int passes = radix_passes((uint32_t)(num_nodes - 1));
     RK(t->keys.ensure(n_items, st));
     RK(t->keys_b.ensure(n_items, st));
@@ -1390,7 +1406,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       RK(t->hslots2.ensure((long long)H, st));
       CK(cudaMemsetAsync(t->hslots2.p, 0xFF, (size_t)t->hslots2.cap * sizeof(HSlot), st));
       RK(t->hused.ensure((long long)H, st, (long long)h.n_used));
-      Hash nh{t->hslots2.p, H, t->hused.p, H, htag};
+      Hash nh{t->hslots2.p, H, t->hused.p, H, htag, cbits};
       lod::launch(k_rehash, grid_for(std::max<long long>((long long)h.n_used, 1)), 256, 0, st, t->hslots.p, nh, t->d_ctrl);
       // the old table goes back to empty for later cycles
       CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
@@ -1420,7 +1436,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
       t->hcap = H;
       RK(t->hused.ensure(bound + 1, st));
-      hs = Hash{t->hslots.p, t->hcap, t->hused.p, (unsigned long long)bound + 1, htag};
+      hs = Hash{t->hslots.p, t->hcap, t->hused.p, (unsigned long long)bound + 1, htag, cbits};
       CK(cudaMemsetAsync(&t->d_ctrl->n_used, 0, 8, st));
       CK(cudaMemsetAsync(&t->d_ctrl->hash_overflow, 0, 4, st));
       lod::launch(k_claim, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, grid32, n_all, hs, t->d_ctrl);

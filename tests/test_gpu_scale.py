@@ -134,3 +134,53 @@ def test_config5_partition_protocol_paper_params(gpu, world):
     assert checked > 100
     print(f"config 5 x{world}: {checked} (node, rank) copies equal, single tree {g.num_nodes} nodes, "
           f"hand-off after batch {handed}")
+
+
+def test_node_ids_past_2_24(gpu):
+    """Claim keys pack {epoch:8, node:56-cbits, cell:cbits}: with G = 2 the
+    node field takes 53 bits and ids run to the reference's int32 range.  A
+    tree of > 2^24 nodes (T = 0: every touched leaf splits down to depth 9;
+    3M uniform points) against the oracle: node columns, counters, every
+    grid byte and the sample sequences of 2000 random nodes."""
+    import oracle
+    from paper_2310_03567_b200 import insert_batch, synth
+
+    params = dict(bmin=(0.0, 0.0, 0.0), size=1.0, arena_bytes=1 << 30, chunk_capacity=1, grid_res=2,
+                  leaf_threshold=0, max_depth=9, backlog_capacity=100_000_000, spill_capacity=100_000_000)
+    xyz, rgba = synth.gen_uniform(3_000_000, 24)
+    batches = [(xyz[i:i + 1_000_000], rgba[i:i + 1_000_000]) for i in range(0, 3_000_000, 1_000_000)]
+    ot = oracle.OracleTree(params["bmin"], params["size"], grid_res=2, leaf_threshold=0, max_depth=9,
+                           chunk_capacity=1, arena_bytes=params["arena_bytes"],
+                           backlog_capacity=params["backlog_capacity"], spill_capacity=params["spill_capacity"])
+    tree, state = make_product(params)
+    for x, c in batches:
+        ot.insert_batch(x, c)
+        insert_batch(tree, x, c, state)
+    want = ot.state()
+    n = want["num_nodes"]
+    assert n > (1 << 24), n
+    assert tree.num_nodes == n
+    for k in ("splits_total", "max_level", "allocated_total", "free_count", "arena_offset"):
+        got = {"arena_offset": tree.arena.offset, "allocated_total": tree.pool.allocated_total,
+               "free_count": tree.pool.free_count}.get(k, getattr(tree, k, None))
+        assert int(got) == int(want[k]), k
+    for k in ("parent", "level", "inner", "children", "count", "chunk_count", "grid_off"):
+        assert np.array_equal(getattr(tree, k)[:n], want[k]), k
+    assert np.array_equal(tree.bmin[:n].view(np.uint64), want["bmin"].view(np.uint64))
+    inner = np.flatnonzero(want["inner"])
+    v = ot._view()
+    o_arena = np.ctypeslib.as_array(ctypes_u8(v.arena), shape=(int(v.arena_offset),))
+    p_arena = tree._arena_bytes(0, int(v.arena_offset))
+    offs = want["grid_off"][inner]
+    assert np.array_equal(p_arena[offs], o_arena[offs])  # G = 2: one byte per grid
+    rng = np.random.default_rng(0)
+    for nid in rng.choice(n, 2000, replace=False):
+        gx, gc = tree.gather_samples(int(nid))
+        ox, oc = ot.gather_samples(int(nid))
+        assert np.array_equal(gx, ox) and np.array_equal(gc, oc), nid
+
+
+def ctypes_u8(addr):
+    import ctypes
+
+    return ctypes.cast(addr, ctypes.POINTER(ctypes.c_uint8))

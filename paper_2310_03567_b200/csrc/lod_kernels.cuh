@@ -964,7 +964,10 @@ __global__ void k_store(StoreSink sink, const uint32_t *__restrict__ skeys, cons
 }
 
 // clear_marks (_kernels.py:280-287) + count advance: pending drains into count.
-// + the chunk directory of every node that got chunks (dir_append).
+// + the chunk directory of every node that got chunks: one warp per touched
+// node, lane 0 relocates a full region (doubling), the warp copies the old
+// entries and records the new chunk ids (a large inner node's region holds
+// thousands of entries: a thread per node made its copy the pass's tail).
 __global__ void k_epilogue(NodeCols nd, PoolCols pool, const int32_t *__restrict__ seg_node,
                            const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
                            const U64x2 *__restrict__ plan_ex, Ctrl *ctrl, uint32_t *__restrict__ ghist,
@@ -974,14 +977,38 @@ __global__ void k_epilogue(NodeCols nd, PoolCols pool, const int32_t *__restrict
   for (long long i = gtid(); i < kMaxPassesHist; i += gstride()) ghist[i] = 0;
   if (ctrl->error) return;
   const long long K = (long long)ctrl->n_keys;
-  for (long long d = gtid(); d < K; d += gstride()) {
+  const int lane = threadIdx.x & 31;
+  for (long long d = gtid() >> 5; d < K; d += gstride() >> 5) {
     const int n = seg_node[d];
-    nd.count[n] += seg_start[d + 1] - seg_start[d];
-    nd.pending[n] = 0;
-    nd.final_[n] = 0;
+    const long long need = (long long)plan[d].a;
+    long long off = 0, off_old = 0, cc0 = 0;
+    int moved = 0;
+    if (lane == 0) {
+      nd.count[n] += seg_start[d + 1] - seg_start[d];
+      nd.pending[n] = 0;
+      nd.final_[n] = 0;
+      if (need > 0) {
+        const long long cc1 = nd.chunk_count[n];
+        cc0 = cc1 - need;
+        off = off_old = nd.dir_off[n];
+        if (cc1 > (long long)nd.dir_cap[n]) {
+          const long long cap = cc1 * 2 > 4 ? cc1 * 2 : 4;
+          off = (long long)atomicAdd(&ctrl->dir_top, (unsigned long long)cap);
+          nd.dir_off[n] = off;
+          nd.dir_cap[n] = (int32_t)cap;
+          moved = 1;
+        }
+      }
+    }
+    if (!__shfl_sync(0xffffffffu, (int)(need > 0), 0)) continue;
+    off = __shfl_sync(0xffffffffu, off, 0);
+    off_old = __shfl_sync(0xffffffffu, off_old, 0);
+    cc0 = __shfl_sync(0xffffffffu, cc0, 0);
+    moved = __shfl_sync(0xffffffffu, moved, 0);
+    if (moved)
+      for (long long i = lane; i < cc0; i += 32) pool.cdir[off + i] = pool.cdir[off_old + i];
     const long long A0 = (long long)plan_ex[d].a;
-    dir_append(nd, pool, &ctrl->dir_top, n, (long long)plan[d].a,
-               [&](long long t) { return acq_cid(pool, ctrl, A0 + t); });
+    for (long long t = lane; t < need; t += 32) pool.cdir[off + cc0 + t] = acq_cid(pool, ctrl, A0 + t);
   }
 }
 

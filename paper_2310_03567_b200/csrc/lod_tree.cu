@@ -1298,7 +1298,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     }
     mark(5);
     // ---- cleanup (update.py:375-380)
-    lod::launch(k_epilogue, grid_for(Kb), 256, 0, st, t->nd, t->pool, t->seg_node.p, t->seg_start.p, t->plan.p,
+    lod::launch(k_epilogue, grid_for(Kb * 32), 256, 0, st, t->nd, t->pool, t->seg_node.p, t->seg_start.p, t->plan.p,
                 t->plan_ex.p, t->d_ctrl, t->ghist.p,
                 guard);
     return LOD_OK;

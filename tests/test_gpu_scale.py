@@ -140,15 +140,15 @@ def test_node_ids_past_2_24(gpu):
     """Claim keys pack {epoch:8, node:56-cbits, cell:cbits}: with G = 2 the
     node field takes 53 bits and ids run to the reference's int32 range.  A
     tree of > 2^24 nodes (T = 0: every touched leaf splits down to depth 9;
-    3M uniform points) against the oracle: node columns, counters, every
+    1.5M uniform points, ~22M nodes) against the oracle: node columns, counters, every
     grid byte and the sample sequences of 2000 random nodes."""
     import oracle
     from paper_2310_03567_b200 import insert_batch, synth
 
     params = dict(bmin=(0.0, 0.0, 0.0), size=1.0, arena_bytes=1 << 30, chunk_capacity=1, grid_res=2,
                   leaf_threshold=0, max_depth=9, backlog_capacity=100_000_000, spill_capacity=100_000_000)
-    xyz, rgba = synth.gen_uniform(3_000_000, 24)
-    batches = [(xyz[i:i + 1_000_000], rgba[i:i + 1_000_000]) for i in range(0, 3_000_000, 1_000_000)]
+    xyz, rgba = synth.gen_uniform(1_500_000, 24)
+    batches = [(xyz[i:i + 500_000], rgba[i:i + 500_000]) for i in range(0, 1_500_000, 500_000)]
     ot = oracle.OracleTree(params["bmin"], params["size"], grid_res=2, leaf_threshold=0, max_depth=9,
                            chunk_capacity=1, arena_bytes=params["arena_bytes"],
                            backlog_capacity=params["backlog_capacity"], spill_capacity=params["spill_capacity"])

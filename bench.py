@@ -192,9 +192,16 @@ def run_multi(args, rank, world, local_rank):
     local_rank = local_rank % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local_rank)
     if backend == "nccl":
+        os.environ.setdefault("NCCL_DEBUG", "WARN")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     else:
         dist.init_process_group(backend)
+    # communicator check, logged per rank: every rank contributes its rank
+    probe = torch.tensor([rank], dtype=torch.int64, device="cuda" if backend == "nccl" else "cpu")
+    dist.all_reduce(probe)
+    print(f"[bench] comm ready: backend={backend} rank={rank} nranks={dist.get_world_size()} "
+          f"device=cuda:{local_rank} sum_of_ranks={int(probe.item())} (expected {world * (world - 1) // 2})",
+          file=sys.stderr, flush=True)
     kind = CONFIGS[args.config][0]
     sample = [gen_stripe(kind, s, 0) for s in range(2)]
     plan = partition.plan_owners(sample, world)  # deterministic: same on every rank

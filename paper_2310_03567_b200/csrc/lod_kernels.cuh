@@ -299,12 +299,16 @@ __device__ __forceinline__ int count_descend(const NodeCols &nd, const Geo &geo,
     nid = d.x + octant_step(x, y, z, bx, by, bz, s, inv_s);
     d = __ldg(nd.desc + nid);
     if (!(w & (1u << (cell & 31)))) {
-      // lanes of a warp on one (node, cell): only the lowest claimant index
-      // can win, the others need not touch the table (sorted input puts
-      // many lanes on one cell)
+      // a lane whose left neighbour (the next lower index: the lanes of a
+      // warp are consecutive points) claims the same (node, cell) cannot
+      // win: it need not touch the table (locality-ordered input puts runs
+      // of lanes on one cell; one shuffle, where a MATCH.ANY + REDUX per
+      // claim cost the random-order stream 7 % of the pass)
       const unsigned long long key = claim_key(cur, cell, h.cbits);
-      const unsigned peers = __match_any_sync(__activemask(), key);
-      if (__reduce_min_sync(peers, v) == v) hash_claim(h, stg, key, v, col, ctrl);
+      const unsigned m = __activemask();
+      const unsigned lane = lane_id();
+      const unsigned long long left = __shfl_up_sync(m, key, 1);
+      if (!(lane > 0 && ((m >> (lane - 1)) & 1u) && left == key)) hash_claim(h, stg, key, v, col, ctrl);
     }
   } while (d.x >= 0);
   return nid;

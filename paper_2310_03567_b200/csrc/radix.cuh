@@ -81,8 +81,15 @@ static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
       const bool ok = i < n;
       if (ok) keys[i] = key[q];
       if (smem_nodes) {  // shared-memory counters: the atomic units resolve same-node lanes
-        // (per-warp MATCH.ANY aggregation first was 1.7 % slower end to end)
-        if (ok) atomicAdd(&nc2[key[q] >> 1], 1u << (16 * (key[q] & 1)));
+        // (per-warp MATCH.ANY aggregation first was 1.7 % slower end to end);
+        // a warp whose 32 items share one node (locality-ordered input: 32
+        // serialised atomics on one word) adds them with one
+        const uint32_t k0 = __shfl_sync(0xffffffffu, key[q], 0);
+        if (__all_sync(0xffffffffu, ok && key[q] == k0)) {
+          if (lane_id() == 0) atomicAdd(&nc2[k0 >> 1], 32u << (16 * (k0 & 1)));
+        } else if (ok) {
+          atomicAdd(&nc2[key[q] >> 1], 1u << (16 * (key[q] & 1)));
+        }
         continue;
       }
       const unsigned act = __ballot_sync(0xffffffffu, ok);

@@ -45,8 +45,9 @@ def read_sim(path) -> tuple[np.ndarray, np.ndarray]:
 
 
 class SimSource:
-    """Batches of a SIM file in file order, read ahead by a native reader
-    thread with O_DIRECT into ``slots`` page-locked buffers.  ``next_batch``
+    """Batches of a SIM file in file order, read ahead by native reader
+    threads (``slots`` - 2 of them, at most 8: several reads in flight) with
+    O_DIRECT into ``slots`` page-locked buffers.  ``next_batch``
     returns a packed (n, 4) uint32 record array (a view of its slot, valid
     until ``release``), or None at end of file."""
 
@@ -96,8 +97,8 @@ class SimSource:
             pass
 
 
-def stream_sim(tree, path, state, batch_size: int = 1_000_000, camera=None, threshold: float = 128.0,
-               render_every: int = 1, slots: int = 4) -> dict:
+def stream_sim(tree, path, state, batch_size: int = 1 << 20, camera=None, threshold: float = 128.0,
+               render_every: int = 1, slots: int = 8) -> dict:
     """Disk -> insert -> render: every batch of the SIM file into the tree
     (insert_records), rendering ``camera`` into a device framebuffer every
     ``render_every`` batches (render.rasterize's device path: selection + splat,

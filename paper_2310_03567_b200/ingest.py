@@ -46,8 +46,8 @@ def read_sim(path) -> tuple[np.ndarray, np.ndarray]:
 
 class SimSource:
     """Batches of a SIM file in file order, read ahead by native reader
-    threads (``slots`` - 2 of them, at most 8: several reads in flight) with
-    O_DIRECT into ``slots`` page-locked buffers.  ``next_batch``
+    threads (LOD_SIM_READERS, default 1; several reads in flight help striped
+    volumes) with O_DIRECT into ``slots`` page-locked buffers.  ``next_batch``
     returns a packed (n, 4) uint32 record array (a view of its slot, valid
     until ``release``), or None at end of file."""
 

@@ -32,14 +32,15 @@ def test_sim_layout_matches_the_record_layout(tmp_path):
     assert np.array_equal(x2, xyz) and np.array_equal(c2, rgba)
 
 
-@pytest.mark.parametrize("slots", [3, 8])
+@pytest.mark.parametrize("readers", [1, 6])
 @pytest.mark.parametrize("n,batch", [(1_000_000, 65_536), (300_000, 1_048_576), (256, 256), (5000, 512)])
-def test_reader_threads_return_every_batch_in_order(tmp_path, n, batch, slots):
-    """1 reader thread (3 slots) or 6 (8 slots) reading batches concurrently."""
+def test_reader_threads_return_every_batch_in_order(tmp_path, monkeypatch, n, batch, readers):
+    """1 reader thread, or 6 reading batches concurrently (LOD_SIM_READERS)."""
+    monkeypatch.setenv("LOD_SIM_READERS", str(readers))
     xyz, rgba = synth.gen_surface(n, 2)
     p = tmp_path / "b.sim"
     ingest.write_sim(p, xyz, rgba)
-    src = ingest.SimSource(p, batch, slots=slots)
+    src = ingest.SimSource(p, batch, slots=8)
     got = [b.copy() for b in src]
     info = src.info()
     src.close()

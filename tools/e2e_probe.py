@@ -1,0 +1,54 @@
+"""bench.py's e2e measurement repeated: 5 warm-up + 20 timed pinned host
+batches of the terrain stream through run_frame_updates (10 ms budget), five
+fresh trees; plus the same with one frame for all batches and with a plain
+insert_batch loop (no ingest feed), to see where the end-to-end time goes."""
+import collections
+import json
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+
+
+def main():
+    import torch
+
+    from bench import gen_batches, new_tree
+    from paper_2310_03567_b200 import insert_batch, run_frame_updates, wait_settled
+
+    bs = gen_batches("surface", 25)
+    pin = []
+    for x, c in bs:
+        px = torch.from_numpy(x).pin_memory().numpy()
+        pc = torch.from_numpy(c.view(np.int32)).pin_memory().numpy().view(np.uint32)
+        pin.append((px, pc))
+    for mode in ("frames_10ms", "one_frame", "insert_loop"):
+        vals = []
+        for rep in range(4):
+            tree, state = new_tree(0, 8 << 30)
+            for i in range(5):
+                insert_batch(tree, *pin[i], state)
+            wait_settled(tree, state)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            if mode == "insert_loop":
+                for i in range(5, 25):
+                    insert_batch(tree, *pin[i], state)
+            else:
+                if mode == "one_frame":
+                    state.clock.budget_ms = 1e9
+                q = collections.deque(pin[5:25])
+                while q:
+                    run_frame_updates(tree, q, state)
+            wait_settled(tree, state)
+            e1.record()
+            torch.cuda.synchronize()
+            vals.append(round(20e3 / e0.elapsed_time(e1), 1))
+            tree.close()
+        print(json.dumps({"mode": mode, "mpts_per_s": vals}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

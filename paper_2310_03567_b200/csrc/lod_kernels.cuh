@@ -683,18 +683,41 @@ __global__ void k_claim(NodeCols nd, Geo geo, PointSrc src, const uint32_t *__re
 // appends per point, _kernels.py:100-151, and a point wins at most one cell
 // per node), so a point's own wins -- all at different nodes -- may take any
 // order: the stable node sort separates them.
+// The same two passes over the cycle's used-slot list instead of the whole
+// table (the list holds exactly the installed slots, h.used[0 .. n_used)):
+// while the table is L2-resident the random slot reads are cheaper than a
+// sweep over every slot (~40 % of which are live).
+template <bool LIST>
+__device__ __forceinline__ bool claim_slot(const Hash &h, const Ctrl *ctrl, long long i, ulonglong2 &kv,
+                                           long long &sidx) {
+  if (LIST) {
+    if (i >= (long long)min(ctrl->n_used, h.limit)) return false;
+    sidx = (long long)h.used[i];
+  } else {
+    if (i >= (long long)h.cap) return false;
+    sidx = i;
+  }
+  kv = __ldcg(reinterpret_cast<const ulonglong2 *>(h.slots + sidx));
+  return live(h, kv.x);
+}
+
 __device__ __forceinline__ long long claim_index(uint32_t v, long long n_s) {
   return (v & kBatchTag) ? n_s + (long long)(v & ~kBatchTag) : (long long)v;
 }
 
+template <bool LIST>
 __global__ void __launch_bounds__(256)
-    k_resolve(NodeCols nd, Hash h, uint32_t *grid32, long long n_s, uint32_t *__restrict__ wcount,
+    k_resolve(NodeCols nd, Hash h, uint32_t *grid32, long long n_s, uint32_t *__restrict__ wcount, const Ctrl *ctrl,
               const int *guard) { lod::pdl_wait();
   if (guard && *guard) return;
-  const long long H = (long long)h.cap;
-  for (long long sidx = gtid(); sidx < H; sidx += gstride()) {
-    const ulonglong2 kv = __ldcg(reinterpret_cast<const ulonglong2 *>(h.slots + sidx));
-    if (!live(h, kv.x)) continue;
+  const long long H = LIST ? (long long)h.limit : (long long)h.cap;
+  for (long long i = gtid(); i < H; i += gstride()) {
+    ulonglong2 kv;
+    long long sidx;
+    if (!claim_slot<LIST>(h, ctrl, i, kv, sidx)) {
+      if (LIST) break;
+      continue;
+    }
     const int nid = key_node(h, kv.x);
     const uint32_t cell = key_cell(h, kv.x);
     atomicOr(grid32 + (nd.grid_off[nid] >> 2) + (cell >> 5), 1u << (cell & 31));
@@ -702,16 +725,19 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+template <bool LIST>
 __global__ void __launch_bounds__(256)
     k_scatter(Hash h, long long n_s, const uint32_t *__restrict__ wbase, uint32_t *__restrict__ wcount, PointSrc src,
-              uint4 *__restrict__ backlog,
-              const int *guard) { lod::pdl_wait();
+              uint4 *__restrict__ backlog, const Ctrl *ctrl, const int *guard) { lod::pdl_wait();
   if (guard && *guard) return;
-  const long long H = (long long)h.cap;
-  for (long long sidx = gtid(); sidx < H; sidx += gstride()) {
-    HSlot *sl = h.slots + sidx;
-    const ulonglong2 kv = __ldcg(reinterpret_cast<const ulonglong2 *>(sl));
-    if (!live(h, kv.x)) continue;  // left in place: stale from the next cycle on
+  const long long H = LIST ? (long long)h.limit : (long long)h.cap;
+  for (long long i = gtid(); i < H; i += gstride()) {
+    ulonglong2 kv;
+    long long sidx;
+    if (!claim_slot<LIST>(h, ctrl, i, kv, sidx)) {  // stale slots are left in place
+      if (LIST) break;
+      continue;
+    }
     const long long j = claim_index((uint32_t)(kv.y >> 32), n_s);
     const uint32_t b = __ldg(wbase + j) + atomicSub(wcount + j, 1u) - 1u;
     backlog[b] = make_uint4((uint32_t)key_node(h, kv.x), key_cell(h, kv.x), (uint32_t)kv.y,

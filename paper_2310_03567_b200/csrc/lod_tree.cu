@@ -223,7 +223,8 @@ struct LodTree {
   cudaEvent_t ev_counted = nullptr;  // the running cycle's first count pass is done
   cudaEvent_t ev_input = nullptr;    // the caller's input stream (LOD_FLAG_INPUT_STREAM)
   int stage_next = 0;
-  cudaEvent_t ev[16] = {};  // 12, 13: per-iteration k_count brackets; 10/11 and 14/15: the two
+  cudaEvent_t ev[16] = {};  // 8: the store's end (device inputs released); 12, 13: per-iteration
+                            // k_count brackets; 10/11 and 14/15: the two
                             // (inputs resident, settled) pairs, alternating between calls
   int ev_slot = 0;          // pair of the last call
   bool tail_pending = false;  // the last call returned before its sort + store finished
@@ -1194,13 +1195,30 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       }
       RK(t->wbase.ensure(n_all, st));
       RK(ensure_scan_lb<uint32_t>(t->lb32, n_all));
-      if (nv > 0) lod::launch(k_resolve, grid_for((long long)t->hcap), 256, 0, st, t->nd, hs, grid32, n_s, t->wcount.p, guard);
+      // the used-slot list while the table fits L2 comfortably, else a sweep
+      static const long long list_max = getenv("LOD_RESOLVE_LIST_MAX_MB")
+                                            ? atoll(getenv("LOD_RESOLVE_LIST_MAX_MB")) << 20
+                                            : (64LL << 20);
+      const bool use_list = (long long)t->hcap * (long long)sizeof(HSlot) <= list_max;
+      const unsigned rgrid = use_list ? grid_for(nv) : grid_for((long long)t->hcap);
+      if (nv > 0) {
+        if (use_list)
+          lod::launch(k_resolve<true>, rgrid, 256, 0, st, t->nd, hs, grid32, n_s, t->wcount.p,
+                      (const Ctrl *)t->d_ctrl, guard);
+        else
+          lod::launch(k_resolve<false>, rgrid, 256, 0, st, t->nd, hs, grid32, n_s, t->wcount.p,
+                      (const Ctrl *)t->d_ctrl, guard);
+      }
       mark(1);
       tp("resolve_launched");
       if (nv > 0) {
         exclusive_scan_lb<uint32_t>(t->wcount.p, t->wbase.p, n_all, &t->d_ctrl->n_v, t->lb32, st, guard);
-        lod::launch(k_scatter, grid_for((long long)t->hcap), 256, 0, st, hs, n_s, t->wbase.p, t->wcount.p, src,
-                    t->backlog.p, guard);
+        if (use_list)
+          lod::launch(k_scatter<true>, rgrid, 256, 0, st, hs, n_s, t->wbase.p, t->wcount.p, src, t->backlog.p,
+                      (const Ctrl *)t->d_ctrl, guard);
+        else
+          lod::launch(k_scatter<false>, rgrid, 256, 0, st, hs, n_s, t->wbase.p, t->wcount.p, src, t->backlog.p,
+                      (const Ctrl *)t->d_ctrl, guard);
       }
     }
     mark(2);
@@ -1280,6 +1298,10 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     }
     mark(4);
     tp("sort_launched");
+    // the store was the last reader of the batch: device inputs are released
+    // to the caller's stream here, not behind the epilogue (the caller's next
+    // insert waits on its stream, so this shortens the call-to-call handshake)
+    CK(cudaEventRecord(t->ev[8], st));
     if (delta) {  // ---- BatchDelta (update.py:333-355), before the counts advance
       RK(t->dvnode.ensure(Kb, st));
       RK(t->dvstart.ensure(Kb, st));
@@ -1479,8 +1501,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   float ms = -1.f;
   if (early) {  // the tail is still running: its time is reported by the next call / lod_tree_wait
     t->tail_pending = true;
-    if (flags & LOD_FLAG_DEVICE_INPUT)  // the store re-reads the batch: the caller's stream waits
-      CK(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(limits->input_stream), EE, 0));
+    if (flags & LOD_FLAG_DEVICE_INPUT)  // the store re-reads the batch: the caller's stream waits for it
+      CK(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(limits->input_stream), t->ev[8], 0));
   } else {
     cudaEventElapsedTime(&ms, EB, EE);
   }

@@ -223,8 +223,7 @@ struct LodTree {
   cudaEvent_t ev_counted = nullptr;  // the running cycle's first count pass is done
   cudaEvent_t ev_input = nullptr;    // the caller's input stream (LOD_FLAG_INPUT_STREAM)
   int stage_next = 0;
-  cudaEvent_t ev[16] = {};  // 8: the store's end (device inputs released); 12, 13: per-iteration
-                            // k_count brackets; 10/11 and 14/15: the two
+  cudaEvent_t ev[16] = {};  // 12, 13: per-iteration k_count brackets; 10/11 and 14/15: the two
                             // (inputs resident, settled) pairs, alternating between calls
   int ev_slot = 0;          // pair of the last call
   bool tail_pending = false;  // the last call returned before its sort + store finished
@@ -1298,10 +1297,6 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     }
     mark(4);
     tp("sort_launched");
-    // the store was the last reader of the batch: device inputs are released
-    // to the caller's stream here, not behind the epilogue (the caller's next
-    // insert waits on its stream, so this shortens the call-to-call handshake)
-    CK(cudaEventRecord(t->ev[8], st));
     if (delta) {  // ---- BatchDelta (update.py:333-355), before the counts advance
       RK(t->dvnode.ensure(Kb, st));
       RK(t->dvstart.ensure(Kb, st));
@@ -1501,8 +1496,12 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   float ms = -1.f;
   if (early) {  // the tail is still running: its time is reported by the next call / lod_tree_wait
     t->tail_pending = true;
-    if (flags & LOD_FLAG_DEVICE_INPUT)  // the store re-reads the batch: the caller's stream waits for it
-      CK(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(limits->input_stream), t->ev[8], 0));
+    // the store re-reads the batch: the caller's stream waits for the tail.
+    // (Releasing it by an event recorded right after the store instead broke
+    // the programmatic dependent launch into the epilogue, +5 us, and the
+    // call-to-call gap stayed ~10 us: measured with tools/kineto_gaps.py.)
+    if (flags & LOD_FLAG_DEVICE_INPUT)
+      CK(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(limits->input_stream), EE, 0));
   } else {
     cudaEventElapsedTime(&ms, EB, EE);
   }

@@ -149,6 +149,7 @@ struct PoolCols {
   int32_t *cidx;   // position of the chunk in its owner's list
   int32_t *free_stack;
   int32_t *cdir;   // chunk directory (NodeCols::dir_off / dir_cap): spill gather and render work lists
+  unsigned long long cdir_cap;  // entries of cdir: a relocation past it sets Ctrl::dir_overflow instead
 };
 
 struct Geo {

@@ -69,8 +69,23 @@ struct Ctrl {
                               // points the next count pass re-descends, each claiming at most one cell
   long long n_wins;           // k_resolve_list: entries of the win list (burst path)
   unsigned long long dir_top;  // chunk directory entries handed out (bump pointer)
-  unsigned long long pad2;
+  unsigned long long dir_overflow;  // a relocation found no room: directories are stale until the host
+                                    // rebuilds them (fix_directory; chains stay authoritative)
 };
+static_assert(offsetof(Ctrl, dir_overflow) == offsetof(Ctrl, dir_top) + 8, "dir_claim flags dir_top + 1");
+
+// A fresh directory region of `cap` entries, or -1 (and the overflow flag)
+// when the bump pointer ran past the allocation: the host sized it from a
+// soft bound (small cycles) and rebuilds every directory at its next sync.
+__device__ __forceinline__ long long dir_claim(const PoolCols &pool, unsigned long long *dir_top,
+                                              long long cap) {
+  const unsigned long long noff = atomicAdd(dir_top, (unsigned long long)cap);
+  if (noff + (unsigned long long)cap > pool.cdir_cap) {
+    atomicExch(dir_top + 1, 1ull);  // Ctrl::dir_overflow follows dir_top
+    return -1;
+  }
+  return (long long)noff;
+}
 
 // Chunk directory of node n after `need` chunks were appended to its list
 // (chunk_count already includes them): relocate the region with doubling when
@@ -84,7 +99,8 @@ __device__ __forceinline__ void dir_append(const NodeCols &nd, const PoolCols &p
   long long off = nd.dir_off[n];
   if (cc1 > (long long)nd.dir_cap[n]) {
     const long long cap = cc1 * 2 > 4 ? cc1 * 2 : 4;
-    const long long noff = (long long)atomicAdd(dir_top, (unsigned long long)cap);
+    const long long noff = dir_claim(pool, dir_top, cap);
+    if (noff < 0) return;
     for (long long i = 0; i < cc0; ++i) pool.cdir[noff + i] = pool.cdir[off + i];
     off = noff;
     nd.dir_off[n] = noff;
@@ -1023,10 +1039,14 @@ __global__ void k_epilogue(NodeCols nd, PoolCols pool, const int32_t *__restrict
         off = off_old = nd.dir_off[n];
         if (cc1 > (long long)nd.dir_cap[n]) {
           const long long cap = cc1 * 2 > 4 ? cc1 * 2 : 4;
-          off = (long long)atomicAdd(&ctrl->dir_top, (unsigned long long)cap);
-          nd.dir_off[n] = off;
-          nd.dir_cap[n] = (int32_t)cap;
-          moved = 1;
+          off = dir_claim(pool, &ctrl->dir_top, cap);
+          if (off >= 0) {
+            nd.dir_off[n] = off;
+            nd.dir_cap[n] = (int32_t)cap;
+            moved = 1;
+          } else {
+            moved = -1;  // no room: this node's entries are written by the rebuild
+          }
         }
       }
     }
@@ -1035,6 +1055,7 @@ __global__ void k_epilogue(NodeCols nd, PoolCols pool, const int32_t *__restrict
     off_old = __shfl_sync(0xffffffffu, off_old, 0);
     cc0 = __shfl_sync(0xffffffffu, cc0, 0);
     moved = __shfl_sync(0xffffffffu, moved, 0);
+    if (moved < 0) continue;
     if (moved)
       for (long long i = lane; i < cc0; i += 32) pool.cdir[off + i] = pool.cdir[off_old + i];
     const long long A0 = (long long)plan_ex[d].a;

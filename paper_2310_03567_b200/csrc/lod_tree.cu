@@ -246,6 +246,8 @@ struct LodTree {
   // upper bounds of the counters while asynchronous small cycles are queued
   // (exact whenever sm_queued == 0)
   long long ub_nodes = 1, ub_alloc = 0, ub_dir = 0;
+  bool fixing_dir = false;  // fix_directory running (its own sync must not recurse)
+  long long dir_rebuilds = 0;
   unsigned long long ub_arena = 0;
   long long ingested = 0;  // points inserted so far (bounds the spill of a cycle)
   // the last cycle's backlog (lod_last_voxels): which buffer, entries, spill length
@@ -412,20 +414,22 @@ static int wait_ctrl(LodTree *t, unsigned want) {
 
 // The counters as the host last saw them become exact again (after queued
 // asynchronous small cycles: one publication behind everything queued).
-static void exact_bounds(LodTree *t) {
+static int fix_directory(LodTree *t);
+
+static int exact_bounds(LodTree *t) {
   const Ctrl &c = *t->h_ctrl;
   t->num_nodes = c.num_nodes;
   t->ub_nodes = c.num_nodes;
   t->ub_alloc = c.allocated_total;
   t->ub_arena = c.arena_off;
   t->sm_queued = 0;
+  return c.dir_overflow ? fix_directory(t) : LOD_OK;
 }
 
 static int refresh(LodTree *t) {
   if (t->sm_queued == 0) return LOD_OK;
   RK(sync_ctrl(t));
-  exact_bounds(t);
-  return LOD_OK;
+  return exact_bounds(t);
 }
 
 template <typename T>
@@ -526,14 +530,19 @@ static int ensure_chunks(LodTree *t, long long want, long long live) {
 // t->ub_dir bounds dir_top after everything launched so far: exact after every
 // sync_ctrl (published behind all queued work), plus the reserve of every
 // cycle launched since.
-static int ensure_dir(LodTree *t, long long chunks_after, long long touched) {
-  const long long keep = t->ub_dir;
-  t->ub_dir += 2 * chunks_after + 4 * touched + 1024;
-  if (t->ub_dir > t->cdir.cap) {
-    RK(t->cdir.ensure(t->ub_dir, t->st, keep));
-    t->pool.cdir = t->cdir.p;
-  }
+static int grow_dir(LodTree *t, long long want) {
+  if (want <= t->cdir.cap) return LOD_OK;
+  // the whole old allocation travels: a soft-bounded small cycle may have
+  // handed out entries past t->ub_dir
+  RK(t->cdir.ensure(want, t->st, t->cdir.cap));
+  t->pool.cdir = t->cdir.p;
+  t->pool.cdir_cap = (unsigned long long)t->cdir.cap;
   return LOD_OK;
+}
+
+static int ensure_dir(LodTree *t, long long chunks_after, long long touched) {
+  t->ub_dir += 2 * chunks_after + 4 * touched + 1024;
+  return grow_dir(t, t->ub_dir);
 }
 
 // Look-back state of the single-pass scan for up to `tiles` tiles of T.
@@ -612,7 +621,7 @@ static int abort_cycle(LodTree *t, int code) {
   cudaStreamSynchronize(t->st);
   // counters: the device ctrl keeps whatever was applied before the failure
   sync_ctrl(t);
-  exact_bounds(t);
+  (void)exact_bounds(t);
   return code;
 }
 
@@ -659,14 +668,21 @@ static int small_insert(LodTree *t, const float *xyz, const uint32_t *rgba, long
   *handled = true;
   cudaStream_t st = t->st;
   // capacities for the worst case (stream-ordered growth; exact counters first)
-  if (t->sm_queued && (t->ub_nodes + 8 * s_max + 1 > t->ncap || t->ub_alloc + chunks_max + 1 > t->ccap ||
+  // Node and chunk rows are bounded rigorously; growth leaves headroom for
+  // many more worst cases so that the exact counters are re-read (a sync)
+  // only every few dozen calls at least, not whenever the bound grazes the
+  // capacity.  The directory is sized softly: a relocation takes 2 x the
+  // node's chunk count, which the host does not track; a cycle that finds no
+  // room flags it and the host rebuilds every directory from the chains at
+  // its next sync (fix_directory).
+  const long long Rn = 8 * s_max + 1, Rc = chunks_max + 1, Rd = 4 * touched_max + 2 * chunks_max + 1024;
+  if (t->sm_queued && (t->ub_nodes + Rn > t->ncap || t->ub_alloc + Rc > t->ccap ||
                        t->ub_arena + arena_max > t->arena_cap || t->sm_queued >= 4096))
     RK(refresh(t));
-  RK(ensure_nodes(t, t->ub_nodes + 8 * s_max + 1, t->ub_nodes));
-  RK(ensure_chunks(t, t->ub_alloc + chunks_max + 1, t->ub_alloc));
-  if (t->sm_queued && t->ub_dir + 2 * (t->ub_alloc + chunks_max) + 4 * touched_max + 1024 > t->cdir.cap)
-    RK(refresh(t));  // exact bump pointer before growing the directory
-  RK(ensure_dir(t, t->ub_alloc + chunks_max, touched_max));
+  RK(ensure_nodes(t, t->ub_nodes + Rn + std::min(63 * Rn, t->ub_nodes + 4096), t->ub_nodes));
+  RK(ensure_chunks(t, t->ub_alloc + Rc + std::min(63 * Rc, t->ub_alloc + 4096), t->ub_alloc));
+  if (t->sm_queued == 0) RK(grow_dir(t, 2 * t->ub_dir + 64 * Rd));  // ub_dir is an upper bound here
+  t->ub_dir += Rd;
   const bool async_call = nv_max <= backlog_cap && spill_max <= spill_cap && t->ub_arena + arena_max <= t->arena_cap;
   RK(t->sm_brec.ensure(kSmallMaxBatch, st));
   RK(t->sm_node_b.ensure(kSmallMaxBatch, st));
@@ -746,6 +762,8 @@ static int small_insert(LodTree *t, const float *xyz, const uint32_t *rgba, long
   a.acc = t->sm_acc;
   a.seq = seq;
   a.async_call = async_call ? 1 : 0;
+  static const bool force_overflow = getenv("LOD_DIR_FORCE_OVERFLOW") != nullptr;  // test switch
+  if (force_overflow) a.pool.cdir_cap = 0;  // every relocation of this cycle finds no room
   t->sm_seq = seq;
   CK(lod::launch(k_small_cycle, 1, kSmallBlock, 0, st, a));
   t->ingested += n;
@@ -792,7 +810,12 @@ static int small_insert(LodTree *t, const float *xyz, const uint32_t *rgba, long
   t->last_backlog = t->sm_backlog.p;
   t->last_nv = r->n_voxels;
   t->last_ns = r->n_spill;
-  return r->error;
+  const int err = r->error;
+  if (r->dir_top > (unsigned long long)t->cdir.cap) {  // a relocation found no room
+    RK(sync_ctrl(t));
+    RK(exact_bounds(t));
+  }
+  return err;
 }
 
 // ---------------------------------------------------------------- C ABI
@@ -973,7 +996,7 @@ int lod_tree_info(LodTree *t, LodTreeInfo *info) {
   if (!t || !info) return LOD_E_ARG;
   cudaSetDevice(t->dev);
   RK(sync_ctrl(t));
-  exact_bounds(t);  // between calls the published counters are exact
+  RK(exact_bounds(t));  // between calls the published counters are exact
   const Ctrl &c = *t->h_ctrl;
   info->num_nodes = c.num_nodes;
   info->node_capacity = t->ncap;
@@ -1018,7 +1041,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     if (handled) {
       if (rc) {  // the structure stays walkable (partial state, errors.py:1-5)
         RK(sync_ctrl(t));
-        exact_bounds(t);
+        RK(exact_bounds(t));
       }
       return rc;
     }
@@ -1488,7 +1511,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   S.n_splits = splits_cycle;
   S.iterations = iters;
   fill_stats(t, &S);
-  exact_bounds(t);  // the counters published behind k_alloc are final
+  RK(exact_bounds(t));  // the counters published behind k_alloc are final
   t->ingested += n;
   t->last_backlog = t->backlog.p;
   t->last_nv = n_v;
@@ -1561,7 +1584,7 @@ int lod_tree_settle(LodTree *t, LodSettleStats *out) {
   }
   t->sm_unfolded = 0;
   RK(sync_ctrl(t));
-  exact_bounds(t);
+  RK(exact_bounds(t));
   out->num_nodes = t->h_ctrl->num_nodes;
   out->splits_total = t->h_ctrl->splits_total;
   out->max_level = t->h_ctrl->max_level;
@@ -1799,7 +1822,7 @@ int lod_merge_voxels(LodTree *t, int64_t n_groups, const int32_t *gnode, const i
               t->gnodes.p, t->gstart.p, t->goff.p, t->dvcell.p, t->dvrgba.p, t->d_ctrl, acq, t->arena_cap);
   lod::launch(k_merge_finish, 1, 1, 0, st, t->d_ctrl, (const unsigned long long *)acq, t->arena_cap, t->geo);
   RK(sync_ctrl(t));
-  exact_bounds(t);
+  RK(exact_bounds(t));
   if (t->h_ctrl->error) {
     const int e = t->h_ctrl->error;
     CK(cudaMemsetAsync(&t->d_ctrl->error, 0, 4, st));
@@ -1928,17 +1951,51 @@ __global__ void k_rebuild_indexes(NodeCols nd, PoolCols pool, long long n, Ctrl 
     long long off = nd.dir_off[nid];
     if (cc > nd.dir_cap[nid]) {
       const long long cap = cc * 2 > 4 ? cc * 2 : 4;
-      off = (long long)atomicAdd(&c->dir_top, (unsigned long long)cap);
-      nd.dir_off[nid] = off;
-      nd.dir_cap[nid] = (int32_t)cap;
+      off = dir_claim(pool, &c->dir_top, cap);
+      if (off >= 0) {
+        nd.dir_off[nid] = off;
+        nd.dir_cap[nid] = (int32_t)cap;
+      }
     }
     long long ci = 0;
     for (int cid = nd.chunk_head[nid]; cid != LOD_NO_CHUNK && ci < cc; cid = pool.next[cid], ++ci) {
       pool.owner[cid] = nid;
       pool.cidx[cid] = (int)ci;
-      pool.cdir[off + ci] = cid;
+      if (off >= 0) pool.cdir[off + ci] = cid;
     }
   }
+}
+
+__global__ void k_dir_reset(NodeCols nd, long long n, Ctrl *c) {
+  lod::pdl_wait();
+  for (long long i = gtid(); i < n; i += gstride()) {
+    nd.dir_off[i] = 0;
+    nd.dir_cap[i] = 0;
+  }
+  if (gtid() == 0) {
+    c->dir_top = 0;
+    c->dir_overflow = 0;
+  }
+}
+
+// Every node's directory handed out again from the chains (which stay
+// authoritative) after a soft-sized small cycle ran out of room: at most
+// 4 + 2 x chunk_count entries per node.  Only between cycles (exact_bounds),
+// with every node row initialised.
+static int fix_directory(LodTree *t) {
+  if (t->fixing_dir) return LOD_OK;
+  t->fixing_dir = true;
+  const long long nn = t->h_ctrl->num_nodes, alloc = t->h_ctrl->allocated_total;
+  if (lod_debug()) fprintf(stderr, "[lod] chunk directory overflow: rebuilding (%lld nodes)\n", nn);
+  int rc = grow_dir(t, 2 * alloc + 4 * nn + 1024);
+  if (rc == LOD_OK) {
+    lod::launch(k_dir_reset, grid_for(nn), 256, 0, t->st, t->nd, nn, t->d_ctrl);
+    lod::launch(k_rebuild_indexes, grid_for(nn), 256, 0, t->st, t->nd, t->pool, nn, t->d_ctrl);
+    ++t->dir_rebuilds;
+    rc = sync_ctrl(t);
+  }
+  t->fixing_dir = false;
+  return rc;
 }
 
 static int one_shot(LodTree *t, int *status_host, const std::function<void(int *)> &launch_fn) {
@@ -1949,7 +2006,7 @@ static int one_shot(LodTree *t, int *status_host, const std::function<void(int *
   launch_fn(d_status);
   CK(cudaMemcpyAsync(status_host, d_status, 4, cudaMemcpyDeviceToHost, t->st));
   RK(sync_ctrl(t));  // also waits for the copy
-  exact_bounds(t);
+  RK(exact_bounds(t));
   return LOD_OK;
 }
 
@@ -2033,7 +2090,7 @@ int lod_write_nodes(LodTree *t, int64_t n, const int32_t *parent, const uint8_t 
   RK(ensure_dir(t, alloc, n));
   lod::launch(k_rebuild_indexes, grid_for(n), 256, 0, st, t->nd, t->pool, (long long)n, t->d_ctrl);
   RK(sync_ctrl(t));
-  exact_bounds(t);
+  RK(exact_bounds(t));
   return LOD_OK;
 }
 
@@ -2052,7 +2109,7 @@ int lod_write_pool(LodTree *t, int64_t n, const int32_t *next, const int64_t *pa
     lod::launch(k_rebuild_indexes, grid_for(nn), 256, 0, st, t->nd, t->pool, nn, t->d_ctrl);
   }
   RK(sync_ctrl(t));
-  exact_bounds(t);
+  RK(exact_bounds(t));
   return LOD_OK;
 }
 
@@ -2070,7 +2127,7 @@ int lod_read_directory(LodTree *t, int64_t n, int64_t *dir_off, int32_t *dir_cap
   if (!t || n < 0 || n > t->ncap || !dir_top) return LOD_E_ARG;
   cudaSetDevice(t->dev);
   RK(sync_ctrl(t));
-  exact_bounds(t);
+  RK(exact_bounds(t));
   *dir_top = t->h_ctrl->dir_top;
   if (n && dir_off) CK(cudaMemcpyAsync(dir_off, t->nd.dir_off, n * 8, cudaMemcpyDeviceToHost, t->st));
   if (n && dir_cap) CK(cudaMemcpyAsync(dir_cap, t->nd.dir_cap, n * 4, cudaMemcpyDeviceToHost, t->st));
@@ -2365,6 +2422,7 @@ int lod_tree_pack_size(LodTree *t, uint64_t *bytes) {
   if (!t || !bytes) return LOD_E_ARG;
   cudaSetDevice(t->dev);
   RK(sync_ctrl(t));
+  RK(exact_bounds(t));  // a pending directory rebuild first
   *bytes = pack_layout(*t->h_ctrl).total;
   return LOD_OK;
 }
@@ -2373,6 +2431,7 @@ int lod_tree_pack(LodTree *t, void *dev_buf, uint64_t bytes) {
   if (!t || !dev_buf) return LOD_E_ARG;
   cudaSetDevice(t->dev);
   RK(sync_ctrl(t));
+  RK(exact_bounds(t));
   const Ctrl c = *t->h_ctrl;
   const PackLayout L = pack_layout(c);
   if (bytes < L.total) return LOD_E_ARG;
@@ -2447,7 +2506,7 @@ int lod_tree_unpack(LodTree *t, const void *dev_buf, uint64_t bytes) {
   nc.dir_top = c.dir_top;
   CK(cudaMemcpyAsync(t->d_ctrl, &nc, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
   RK(sync_ctrl(t));
-  exact_bounds(t);
+  RK(exact_bounds(t));
   t->ingested = 1LL << 40;  // unknown: the spill of a cycle is then bounded by n * T alone
   return LOD_OK;
 }

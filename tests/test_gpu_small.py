@@ -150,3 +150,49 @@ print(json.dumps(per[-1]))
     (a, pa), (b, pb) = outs
     assert pa == pb
     assert_same_state(a, b, chunk_ids=False, label="small_vs_pipeline")
+
+
+def test_directory_overflow_rebuild(gpu):
+    """Small cycles size the chunk directory softly; a relocation that finds
+    no room flags the control block and the host rebuilds every directory
+    from the chains at its next sync.  LOD_DIR_FORCE_OVERFLOW=1 (child
+    process) makes every small-cycle relocation fail: the tree, the
+    directory (validate walks it against the lists) and a render through it
+    must still equal the oracle's."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = f"""
+import sys, numpy as np
+sys.path.insert(0, {os.path.dirname(here)!r}); sys.path.insert(0, {here!r})
+from common import run_oracle, run_product, product_state, oracle_state, assert_same_state
+from test_gpu_small import _cloud, _split, _params
+from paper_2310_03567_b200 import insert_batch
+from paper_2310_03567_b200.render import Camera, Framebuffer, rasterize
+params = _params(grid_res=8, leaf_threshold=30, chunk_capacity=4)
+xyz, rgba = _cloud(12000, 9, "surface")
+batches = _split(xyz, rgba, [1, 7, 300, 5])
+ot, oerr, oper = run_oracle(params, batches)
+tree, state, err, per = run_product(params, batches)
+assert err == oerr == "" and per == oper
+assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label="dir_overflow")
+tree.validate()
+# queued cycles only, then a render (the rebuild runs at the render's sync)
+more = _split(*_cloud(3000, 10, "surface"), [1, 3])
+for x, c in more:
+    insert_batch(tree, x, c, state)
+    ot.insert_batch(x, c)
+cam = Camera((0.5, 0.45, -1.3), (0.5, 0.5, 0.5), fov_deg=60.0, near=0.05, far=50.0, width=256, height=192)
+fb, rep = rasterize(tree, cam, threshold=-1.0)
+ofb = Framebuffer(cam.width, cam.height)
+assert ot.rasterize_nodes(rep.selected, cam.packed(), ofb.cells) == rep.samples_drawn
+assert np.array_equal(fb.cells, ofb.cells)
+tree.validate()
+print("ok")
+"""
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, LOD_DIR_FORCE_OVERFLOW="1", LOD_DEBUG="1"),
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "chunk directory overflow: rebuilding" in r.stderr

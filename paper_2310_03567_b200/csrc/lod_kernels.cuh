@@ -281,8 +281,22 @@ __global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl
   for (long long u = gtid(); u < (long long)nu; u += gstride()) {
     const HSlot o = old_slots[h.used[u]];
     unsigned long long slot = home_slot(h, o.key);
-    const ulonglong2 empty = make_ulonglong2(kEmptyKey, kEmptyHi), nv = make_ulonglong2(o.key, o.claim);
-    while (cas_slot(h.slots + slot, empty, nv).x != kEmptyKey) slot = next_slot(h, slot);
+    const ulonglong2 nv = make_ulonglong2(o.key, o.claim);
+    for (;;) {  // empty or stale (an earlier cycle's epoch): install over exactly what was read
+      HSlot *sl = h.slots + slot;
+      ulonglong2 cur = __ldcg(reinterpret_cast<const ulonglong2 *>(sl));
+      bool done = false;
+      while (!live(h, cur.x)) {
+        const ulonglong2 old = cas_slot(sl, cur, nv);
+        if (old.x == cur.x && old.y == cur.y) {
+          done = true;
+          break;
+        }
+        cur = old;
+      }
+      if (done) break;
+      slot = next_slot(h, slot);
+    }
     h.used[u] = slot;
   }
 }

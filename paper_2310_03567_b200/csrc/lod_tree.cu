@@ -41,9 +41,15 @@ struct DBuf {
   T *p = nullptr;
   long long cap = 0;
   // Grow to hold n elements; keep the first `keep` elements when growing.
-  int ensure(long long n, cudaStream_t st, long long keep = 0) {
+  // 2x the request: a burst (a spill wave) leaves room for the next one, so
+  // scratch growth (allocation + copy, host work inside the update) happens
+  // a few times per stream instead of at every new high-water mark.  `tight`
+  // (the claim tables, memset whole on growth; the chunk directory) and
+  // requests past 256 MB: max(n, 2x the old capacity).
+  int ensure(long long n, cudaStream_t st, long long keep = 0, bool tight = false) {
     if (n <= cap) return 0;
-    long long nc = std::max<long long>(n, std::max<long long>(2 * cap, 1024));
+    const bool exact = tight || (unsigned long long)n * sizeof(T) > (256ull << 20);
+    long long nc = std::max<long long>(exact ? n : 2 * n, std::max<long long>(2 * cap, 1024));
     if (lod_debug())
       fprintf(stderr, "[lod] grow buffer %lld -> %lld elems (%.1f MB)\n", cap, nc, nc * sizeof(T) / 1e6);
     T *q = nullptr;
@@ -176,6 +182,7 @@ struct LodTree {
   DBuf<unsigned long long> hused;
   DBuf<uint32_t> wcount, wbase;  // per-point win counts (zero between cycles) / their exclusive scan
   unsigned long long hcap = 0;
+  int h2_epoch = -1;  // epoch whose keys the spare claim table (hslots2) may still hold
   long long prev_used = 0;  // claims of the previous cycle (sizes the table)
   int last_iters = 0;       // expansion iterations of the previous cycle (speculation policy)
   long long spec_hits = 0;  // cycles whose pipeline ran speculatively
@@ -246,6 +253,7 @@ struct LodTree {
   // upper bounds of the counters while asynchronous small cycles are queued
   // (exact whenever sm_queued == 0)
   long long ub_nodes = 1, ub_alloc = 0, ub_dir = 0;
+  long long ncap_hint = 0, ccap_hint = 0;  // node / chunk rows at the first large batch
   bool fixing_dir = false;  // fix_directory running (its own sync must not recurse)
   long long dir_rebuilds = 0;
   unsigned long long ub_arena = 0;
@@ -350,8 +358,14 @@ static int cuda_rc(cudaError_t e) {
 // which the host polls -- no copy-engine round trip and no stream-sync wake-up
 // on the critical path of the expansion loop.  A stream error while polling
 // (or LOD_SYNC_MEMCPY=1) falls back to copy + synchronize.
-__global__ void k_publish(const Ctrl *__restrict__ d, Ctrl *h, volatile unsigned *seq_out, unsigned seq) {
+// release != 0: the next kernel may start as soon as this one has waited (it
+// must then skip its own wait: k_onesweep's nowait) -- the system-scope fence
+// below takes 4-5 us, and ~20 us while the copy engines stream a batch in
+// over PCIe, which would otherwise stall the stream behind the publication.
+__global__ void k_publish(const Ctrl *__restrict__ d, Ctrl *h, volatile unsigned *seq_out, unsigned seq,
+                          int release) {
   lod::pdl_wait();
+  if (release) lod::pdl_trigger();
   constexpr int kWords = (int)(sizeof(Ctrl) / 8);
   static_assert(sizeof(Ctrl) % 8 == 0, "Ctrl is copied in 8-byte words");
   const unsigned long long *src = reinterpret_cast<const unsigned long long *>(d);
@@ -362,7 +376,7 @@ __global__ void k_publish(const Ctrl *__restrict__ d, Ctrl *h, volatile unsigned
   if (threadIdx.x == 0) *seq_out = seq;
 }
 
-static unsigned publish_ctrl(LodTree *t);
+static unsigned publish_ctrl(LodTree *t, bool release = false);
 static int wait_ctrl(LodTree *t, unsigned want);
 
 // Control-block reads through mapped pinned memory (k_publish), unless
@@ -372,13 +386,20 @@ static bool mapped_sync(const LodTree *t) {
   return !memcpy_sync && t->h_seq_dev;
 }
 
-static int sync_ctrl(LodTree *t) {
+// then_issue: the queued batches' H2D copies are issued behind the
+// publication (a copy streaming over PCIe slows the publication's
+// system-scope write from ~5 to ~20 us).
+static int issue_pending(LodTree *t);
+static int sync_ctrl(LodTree *t, bool then_issue = false) {
   if (!mapped_sync(t)) {
+    if (then_issue) RK(issue_pending(t));
     t->d2h_bytes += (long long)sizeof(Ctrl);
     CK(cudaMemcpyAsync(t->h_ctrl, t->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, t->st));
     CK(cudaStreamSynchronize(t->st));
   } else {
-    RK(wait_ctrl(t, publish_ctrl(t)));
+    const unsigned want = publish_ctrl(t);
+    if (then_issue) RK(issue_pending(t));
+    RK(wait_ctrl(t, want));
   }
   // published behind everything queued: the directory's bump pointer is exact
   t->ub_dir = (long long)t->h_ctrl->dir_top;
@@ -386,10 +407,10 @@ static int sync_ctrl(LodTree *t) {
 }
 
 // Queue a publication of the control block on the tree stream (no wait).
-static unsigned publish_ctrl(LodTree *t) {
+static unsigned publish_ctrl(LodTree *t, bool release) {
   const unsigned want = ++t->seq;
   t->d2h_bytes += (long long)sizeof(Ctrl);
-  lod::launch(k_publish, 1, 32, 0, t->st, t->d_ctrl, t->h_ctrl_dev, t->h_seq_dev, want);
+  lod::launch(k_publish, 1, 32, 0, t->st, t->d_ctrl, t->h_ctrl_dev, t->h_seq_dev, want, release ? 1 : 0);
   return want;
 }
 
@@ -534,7 +555,7 @@ static int grow_dir(LodTree *t, long long want) {
   if (want <= t->cdir.cap) return LOD_OK;
   // the whole old allocation travels: a soft-bounded small cycle may have
   // handed out entries past t->ub_dir
-  RK(t->cdir.ensure(want, t->st, t->cdir.cap));
+  RK(t->cdir.ensure(want, t->st, t->cdir.cap, true));
   t->pool.cdir = t->cdir.p;
   t->pool.cdir_cap = (unsigned long long)t->cdir.cap;
   return LOD_OK;
@@ -547,28 +568,26 @@ static int ensure_dir(LodTree *t, long long chunks_after, long long touched) {
 
 // Look-back state of the single-pass scan for up to `tiles` tiles of T.
 template <typename T>
-static int ensure_scan_lb(ScanLB &lb, long long n) {
+static int ensure_scan_lb(ScanLB &lb, long long n, cudaStream_t st) {
   const long long tiles = std::max<long long>((n + kScanTile - 1) / kScanTile, 1);
   if (tiles <= lb.cap_tiles) return LOD_OK;
-  const long long c = std::max<long long>(tiles, 2 * lb.cap_tiles);
-  cudaDeviceSynchronize();  // rare (growth); no launch may still use the old arrays
-  if (lb.status) cudaFree(lb.status);
-  if (lb.agg) cudaFree(lb.agg);
-  if (lb.incl) cudaFree(lb.incl);
+  const long long c = std::max<long long>(2 * tiles, 2 * lb.cap_tiles);
+  // stream-ordered: the old arrays go back to the pool behind the launches
+  // that still use them (a device-wide sync here stalled the update ~0.2 ms)
+  if (lb.status) CK(cudaFreeAsync(lb.status, st));
+  if (lb.agg) CK(cudaFreeAsync(lb.agg, st));
+  if (lb.incl) CK(cudaFreeAsync(lb.incl, st));
   if (!lb.ticket) {
-    CK(cudaMalloc(&lb.ticket, 8));
-    CK(cudaMemset(lb.ticket, 0, 8));
+    CK(cudaMallocAsync(reinterpret_cast<void **>(&lb.ticket), 8, st));
+    CK(cudaMemsetAsync(lb.ticket, 0, 8, st));
     lb.tickets = 0;
   }
-  CK(cudaMalloc(&lb.status, (size_t)c * 4));
-  CK(cudaMemset(lb.status, 0, (size_t)c * 4));
-  CK(cudaMalloc(&lb.agg, (size_t)c * sizeof(T)));
-  CK(cudaMalloc(&lb.incl, (size_t)c * sizeof(T)));
+  CK(cudaMallocAsync(reinterpret_cast<void **>(&lb.status), (size_t)c * 4, st));
+  CK(cudaMemsetAsync(lb.status, 0, (size_t)c * 4, st));
+  CK(cudaMallocAsync(&lb.agg, (size_t)c * sizeof(T), st));
+  CK(cudaMallocAsync(&lb.incl, (size_t)c * sizeof(T), st));
   lb.epoch = 0;
   lb.cap_tiles = c;
-  // the memsets ran on the legacy stream, which the (non-blocking) tree
-  // streams do not wait for
-  CK(cudaDeviceSynchronize());
   return LOD_OK;
 }
 
@@ -919,6 +938,18 @@ int lod_tree_create(const LodParams *params, LodTree **out) {
   CK(cudaMemsetAsync(t->arena, 0, t->arena_cap, t->st));
   RK(ensure_nodes(t, 1024, 0));
   RK(ensure_chunks(t, 1024, 0));
+  {
+    // Node / chunk rows a tree fed large batches gets at its first one: what
+    // the arena can hold (an inner node owns a grid, a chunk C records),
+    // capped at a few tens of MB.  Growth copies every column inside the
+    // update that needs it (~140 us of host time per doubling of the node
+    // table, measured), so a tree sized like the bench's never grows its node
+    // table mid-stream; trees fed tiny batches stay small.
+    const long long gsz = std::max<long long>(((long long)g.grid_bytes + 63) / 64 * 64, 64);
+    t->ncap_hint = std::min<long long>(std::min<long long>(8 * ((long long)t->arena_cap / gsz) + 1, 1 << 17),
+                                       max_nodes(t));
+    t->ccap_hint = std::min<long long>((long long)t->arena_cap / std::max<long long>(16 * (long long)g.C, 16), 1 << 18);
+  }
   CK(cudaMalloc(&t->d_ctrl, sizeof(Ctrl)));
   CK(cudaHostAlloc(&t->h_ctrl, sizeof(Ctrl), cudaHostAllocMapped));
   CK(cudaHostGetDevicePointer(&t->h_ctrl_dev, t->h_ctrl, 0));
@@ -1047,6 +1078,10 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     }
   }
   RK(refresh(t));  // the pipeline sizes its launches from exact host copies
+  if (n >= (1 << 16) && (t->ncap < t->ncap_hint || t->ccap < t->ccap_hint)) {  // first large batch
+    RK(ensure_nodes(t, t->ncap_hint, t->num_nodes));
+    RK(ensure_chunks(t, t->ccap_hint, t->h_ctrl->allocated_total));
+  }
   // device-time events: this call's pair, the previous call's kept for its
   // report when that call returned before its tail ran
   const bool prev_pending = t->tail_pending;
@@ -1146,7 +1181,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     const long long want = std::max<long long>(LOD_HASH_FACTOR_X4 * (t->prev_used + n) / 4, 1 << 20);
     const unsigned long long H = round_slots((unsigned long long)want);
     if ((long long)H > t->hslots.cap) {
-      RK(t->hslots.ensure((long long)H, st));
+      RK(t->hslots.ensure((long long)H, st, 0, true));
       CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
     }
     t->hcap = H;
@@ -1154,8 +1189,11 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   }
   // this cycle's epoch; the table is reset when the epochs wrap
   t->hepoch = (t->hepoch + 1) % kEpochs;
-  if (t->hepoch == 0 && t->hslots.p)
-    CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
+  if (t->hepoch == 0) {  // epochs wrap: both tables back to the all-ones state
+    if (t->hslots.p) CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
+    if (t->hslots2.p) CK(cudaMemsetAsync(t->hslots2.p, 0xFF, (size_t)t->hslots2.cap * sizeof(HSlot), st));
+    t->h2_epoch = -1;
+  }
   const unsigned long long htag = (unsigned long long)t->hepoch << 56;
   const int cbits = cell_bits(t->geo.g);
   Hash hs{t->hslots.p, t->hcap, t->hused.p, t->hcap, htag, cbits};
@@ -1216,7 +1254,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
         if (t->wcount.cap > oldw) CK(cudaMemsetAsync(t->wcount.p, 0, (size_t)t->wcount.cap * 4, st));
       }
       RK(t->wbase.ensure(n_all, st));
-      RK(ensure_scan_lb<uint32_t>(t->lb32, n_all));
+      RK(ensure_scan_lb<uint32_t>(t->lb32, n_all, st));
       // the used-slot list while the table fits L2 comfortably, else a sweep
       static const long long list_max = getenv("LOD_RESOLVE_LIST_MAX_MB")
                                             ? atoll(getenv("LOD_RESOLVE_LIST_MAX_MB")) << 20
@@ -1252,7 +1290,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     RK(t->dense.ensure(Kb, st));
     RK(t->plan.ensure(Kb, st));
     RK(t->plan_ex.ensure(Kb, st));
-    RK(ensure_scan_lb<U64x2>(t->lb64, Kb));
+    RK(ensure_scan_lb<U64x2>(t->lb64, Kb, st));
     const long long acq_bound = n_items / C + Kb + 1;
     RK(t->wlo.ensure(acq_bound + Kb + 1, st));
     RK(t->sinfo.ensure(Kb, st));
@@ -1298,7 +1336,10 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     lod::launch(k_alloc, std::max(grid_for(Kb), grid_for(acq_bound)), 256, 0, st, t->nd, t->pool, t->geo,
                 t->seg_node.p, t->seg_start.p, t->plan.p, t->plan_ex.p, t->wlo.p, t->sinfo.p, t->d_ctrl,
                 t->arena_cap, guard);
-    if (early) mid_seq = publish_ctrl(t);
+    // the early return's publication: the sort's first pass starts without
+    // waiting for its host write (publish_ctrl release + first_nowait)
+    const bool release = early && !prof;
+    if (early) mid_seq = publish_ctrl(t, release);
     mark(3);
     tp("alloc_launched");
     // ---- sort + store (update.py:357-373): stable by node id = slot order
@@ -1316,7 +1357,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
                         n_items_dev, guard);
       lod::launch(k_store, grid_for(n_items), 256, 0, st, sink, skeys, svals, (const long long *)n_items_dev, guard);
     } else {
-      stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals, nullptr, 0, &sink, n_items_dev, guard);
+      stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals, nullptr, 0, &sink, n_items_dev, guard,
+                        release);
     }
     mark(4);
     tp("sort_launched");
@@ -1372,7 +1414,6 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       lod::launch(k_count, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, node_of, n_all, first, grid32, hs,
                   t->d_ctrl);
     }
-    if (first) RK(issue_pending(t));  // queued batches' copies start once this count pass is done
     if (prof) cudaEventRecord(t->ev[13], st);
     lod::launch(k_decide_mark, grid_for(t->num_nodes), 256, 0, st, t->nd, t->geo, (long long)t->num_nodes, t->bitmap.p);
     // a speculative pipeline's host-side sizes: nodes as of now (no further
@@ -1387,13 +1428,14 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
                 t->scnt.p, t->schk.p, t->spill_off.p, t->chunk_off.p, t->d_ctrl, spill_cap, t->arena_cap,
                 std::min<long long>(backlog_cap, nv_bound));
     if (speculate) {
+      if (first) RK(issue_pending(t));  // queued batches' copies overlap the speculative pipeline
       RK(pipeline(&t->d_ctrl->spec_abort, nv_bound));
       CK(cudaEventRecord(EE, st));
       pipeline_launched = true;
     }
     tp("pre_sync");
     if (pipeline_launched && early) RK(wait_ctrl(t, mid_seq));
-    else RK(sync_ctrl(t));
+    else RK(sync_ctrl(t, first && !speculate));  // queued batches' copies start behind the publication
     tp("sync");
     if (prof) {
       float x = 0.f;
@@ -1415,10 +1457,12 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     }
     // capacity for the new children and the spill segment
     RK(ensure_nodes(t, h.num_nodes, h.plan_num_nodes0));
+    tp("nodes_ok");
     if (h.spill_add > 0) {
       if (!first) return abort_cycle(t, LOD_E_ARG);  // only iteration 1 can spill (update.py:9-11)
       RK(t->spill.ensure(h.spill_total, st));
       RK(t->node_all.ensure(h.spill_total, st));
+      tp("spill_ok");
       const long long xchunks = h.free_count - h.plan_free0;  // chunks of the splitting nodes
       lod::launch(k_exec_chunks, grid_for(xchunks * 32), 256, 0, st, t->nd, t->pool, t->geo, t->arena,
                   t->split_list.p, ns, t->spill_off.p, t->chunk_off.p, xchunks, t->spill.p, t->node_all.p,
@@ -1427,6 +1471,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     lod::launch(k_exec_nodes, grid_for(8 * ns), 256, 0, st, t->nd, t->geo, t->split_list.p, t->srank.p, ns,
                                                    t->d_ctrl);
     t->num_nodes = h.num_nodes;
+    tp("exec_launched");
     if (first) {
       n_s = h.spill_total;
       if (n_s > 0) {
@@ -1443,16 +1488,22 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     if ((long long)h.n_used + h.redescend > (long long)(3 * t->hcap / 4)) {
       const unsigned long long H = round_slots((unsigned long long)(2 * ((long long)h.n_used + h.redescend)));
       if (lod_debug()) fprintf(stderr, "[lod] claim table grow %llu -> %llu (rehash %llu)\n", t->hcap, H, h.n_used);
-      RK(t->hslots2.ensure((long long)H, st));
-      CK(cudaMemsetAsync(t->hslots2.p, 0xFF, (size_t)t->hslots2.cap * sizeof(HSlot), st));
+      // the spare table needs no clearing: k_rehash installs over stale
+      // slots like the claims do -- unless it is fresh memory, or still holds
+      // this cycle's keys (a second rehash in one cycle)
+      const long long old2 = t->hslots2.cap;
+      RK(t->hslots2.ensure((long long)H, st, 0, true));
+      if (t->hslots2.cap != old2 || t->h2_epoch == (int)t->hepoch)
+        CK(cudaMemsetAsync(t->hslots2.p, 0xFF, (size_t)t->hslots2.cap * sizeof(HSlot), st));
       RK(t->hused.ensure((long long)H, st, (long long)h.n_used));
       Hash nh{t->hslots2.p, H, t->hused.p, H, htag, cbits};
       lod::launch(k_rehash, grid_for(std::max<long long>((long long)h.n_used, 1)), 256, 0, st, t->hslots.p, nh, t->d_ctrl);
-      // the old table goes back to empty for later cycles
-      CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
+      // the old table keeps this cycle's keys: stale from the next cycle on
+      t->h2_epoch = (int)t->hepoch;
       std::swap(t->hslots, t->hslots2);
       t->hcap = H;
       hs = nh;
+      tp("rehashed");
     }
   }
   mark(0);
@@ -1472,7 +1523,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       // fallback: clean table sized by the reference's backlog bound, full claim pass
       const long long bound = std::min<long long>(n_all * D, backlog_cap + 1);
       const unsigned long long H = round_slots((unsigned long long)std::max<long long>(2 * bound, 1 << 20));
-      if ((long long)H > t->hslots.cap) RK(t->hslots.ensure((long long)H, st));
+      if ((long long)H > t->hslots.cap) RK(t->hslots.ensure((long long)H, st, 0, true));
       CK(cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), st));
       t->hcap = H;
       RK(t->hused.ensure(bound + 1, st));

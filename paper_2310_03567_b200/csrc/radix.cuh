@@ -144,7 +144,10 @@ template <class Sink>
 static __global__ void __launch_bounds__(kRadixBlock, LOD_RADIX_MINB)
     k_onesweep(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in, long long n_max,
                const long long *__restrict__ n_dev, int shift, const uint32_t *__restrict__ ghist_pass, uint32_t *lb,
-               long long ntiles, Sink sink, uint32_t *lb_next, const int *guard) { lod::pdl_wait();
+               long long ntiles, Sink sink, uint32_t *lb_next, const int *guard, int nowait) {
+  // nowait: launched behind a k_publish that released its dependents after
+  // its own wait -- everything this pass reads was complete before that
+  if (!nowait) lod::pdl_wait();
   if (guard && *guard) return;
   // item count: n_max, or the device count when launched for an upper bound
   // (tiles past it take their ticket and leave)
@@ -325,7 +328,7 @@ template <class LastSink = KVSink>
 inline void stable_multisplit(uint32_t *keys, long long n, int passes, RadixScratch &s, cudaStream_t st,
                               uint32_t **keys_res, uint32_t **vals_res, const uint32_t *vals0 = nullptr,
                               int shift0 = 0, const LastSink *last = nullptr, const long long *n_dev = nullptr,
-                              const int *guard = nullptr) {
+                              const int *guard = nullptr, bool first_nowait = false) {
   const long long ntiles = radix_tiles(n);
   uint32_t *kin = keys, *kout = s.keys_b;
   const uint32_t *vin = vals0;
@@ -334,13 +337,15 @@ inline void stable_multisplit(uint32_t *keys, long long n, int passes, RadixScra
     if (n > 0) {
       // look-back buffer p&1 was zeroed by k_radix_prep (p = 0) or by pass p-1
       uint32_t *lbn = p + 1 < passes ? s.lb[(p + 1) & 1] : (uint32_t *)nullptr;
+      const int nowait = (first_nowait && p == 0) ? 1 : 0;
       if (last && p + 1 == passes)
         lod::launch(k_onesweep<LastSink>, (unsigned)ntiles, kRadixBlock, 0, st, kin, vin, n, n_dev,
-                    shift0 + p * kRadixBits, s.ghist + p * kRadixDigits, s.lb[p & 1], ntiles, *last, lbn, guard);
+                    shift0 + p * kRadixBits, s.ghist + p * kRadixDigits, s.lb[p & 1], ntiles, *last, lbn, guard,
+                    nowait);
       else
         lod::launch(k_onesweep<KVSink>, (unsigned)ntiles, kRadixBlock, 0, st, kin, vin, n, n_dev,
                     shift0 + p * kRadixBits, s.ghist + p * kRadixDigits, s.lb[p & 1], ntiles, KVSink{kout, vout}, lbn,
-                    guard);
+                    guard, nowait);
     }
     uint32_t *kt = kin;
     kin = kout;

@@ -2,7 +2,10 @@
 kernel / memcpy on the GPU with start and duration, and the idle gaps between
 them, to see how much of a batch is launch / host-round-trip latency.
 
-    python tools/kineto_gaps.py [--warm 20] [--batches 4]
+    python tools/kineto_gaps.py [--warm 20] [--batches 4] [--e2e]
+
+--e2e: pinned host batches through the frame loop (run_frame_updates, the
+bench's e2e path) instead of device-resident insert_batch calls.
 """
 import argparse
 import json
@@ -20,22 +23,39 @@ def main():
     from torch.profiler import ProfilerActivity, profile
 
     from bench import gen_batches, new_tree
-    from paper_2310_03567_b200 import insert_batch, wait_settled
+    import collections
+
+    from paper_2310_03567_b200 import insert_batch, run_frame_updates, wait_settled
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--warm", type=int, default=20)
     ap.add_argument("--batches", type=int, default=4)
+    ap.add_argument("--e2e", action="store_true")
     a = ap.parse_args()
     bs = gen_batches("surface", a.warm + a.batches)
-    dev = [(torch.from_numpy(x).cuda(), torch.from_numpy(c.view(np.int32)).cuda()) for x, c in bs]
+    if a.e2e:
+        src = []
+        for x, c in bs:
+            src.append((torch.from_numpy(x).pin_memory().numpy(),
+                        torch.from_numpy(c.view(np.int32)).pin_memory().numpy().view(np.uint32)))
+    else:
+        src = [(torch.from_numpy(x).cuda(), torch.from_numpy(c.view(np.int32)).cuda()) for x, c in bs]
     tree, state = new_tree(0, 16 << 30)
-    for i in range(a.warm):
-        insert_batch(tree, *dev[i], state)
+
+    def feed(lo, hi):
+        if a.e2e:
+            q = collections.deque(src[lo:hi])
+            while q:
+                run_frame_updates(tree, q, state)
+        else:
+            for i in range(lo, hi):
+                insert_batch(tree, *src[i], state)
+
+    feed(0, a.warm)
     wait_settled(tree, state)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        for i in range(a.warm, a.warm + a.batches):
-            insert_batch(tree, *dev[i], state)
+        feed(a.warm, a.warm + a.batches)
         wait_settled(tree, state)
         torch.cuda.synchronize()
     path = os.path.join(tempfile.mkdtemp(), "trace.json")

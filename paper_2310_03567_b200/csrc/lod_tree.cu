@@ -254,6 +254,7 @@ struct LodTree {
   // (exact whenever sm_queued == 0)
   long long ub_nodes = 1, ub_alloc = 0, ub_dir = 0;
   long long ncap_hint = 0, ccap_hint = 0;  // node / chunk rows at the first large batch
+  bool sized_large = false;
   bool fixing_dir = false;  // fix_directory running (its own sync must not recurse)
   long long dir_rebuilds = 0;
   unsigned long long ub_arena = 0;
@@ -1078,9 +1079,20 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     }
   }
   RK(refresh(t));  // the pipeline sizes its launches from exact host copies
-  if (n >= (1 << 16) && (t->ncap < t->ncap_hint || t->ccap < t->ccap_hint)) {  // first large batch
-    RK(ensure_nodes(t, t->ncap_hint, t->num_nodes));
-    RK(ensure_chunks(t, t->ccap_hint, t->h_ctrl->allocated_total));
+  if (n >= (1 << 16) && !t->sized_large) {  // first large batch
+    t->sized_large = true;
+    RK(ensure_nodes(t, std::max<long long>(t->ncap_hint, t->ncap), t->num_nodes));
+    RK(ensure_chunks(t, std::max<long long>(t->ccap_hint, t->ccap), t->h_ctrl->allocated_total));
+    // both claim tables for 16 x the batch: the re-descent after a split burst
+    // (spill of several batches) then rehashes into a table that is already
+    // there, instead of allocating and clearing one inside that update
+    const long long H = std::min<long long>(16 * n, 1LL << 27);
+    for (DBuf<HSlot> *tb : {&t->hslots, &t->hslots2}) {
+      const long long old = tb->cap;
+      RK(tb->ensure(H, st, 0, true));
+      if (tb->cap != old) CK(cudaMemsetAsync(tb->p, 0xFF, (size_t)tb->cap * sizeof(HSlot), st));
+    }
+    t->h2_epoch = -1;
   }
   // device-time events: this call's pair, the previous call's kept for its
   // report when that call returned before its tail ran

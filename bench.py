@@ -231,6 +231,7 @@ def run_multi(args, rank, world, local_rank):
                 h2d += 16 * c.numel()
             ins.insert(x, c)
             launches += int(state._bstats.launches)
+        ins.flush()  # the last batch's replicated-top merge is inside the timed region
         e1.record()
         torch.cuda.synchronize()
         dist.barrier()
@@ -260,8 +261,11 @@ def run_multi(args, rank, world, local_rank):
                        "parallelism": f"octant-prefix partition depth {plan.depth} x{world}, "
                                       + (f"{backend.upper()} all-to-all routing (peer windows unavailable: "
                                          f"{ins.no_peers})" if ins.no_peers else
-                                         f"peer-memory routing (bucket scatter into CUDA IPC windows), "
-                                         f"{backend.upper()} barriers"),
+                                         f"peer-memory routing (bucket scatter into CUDA IPC windows, "
+                                         f"sequence flags in the windows: no per-batch host barrier; "
+                                         f"replicated-top voxels logged on the device, merged "
+                                         f"{ins.flushes}x), {backend.upper()} for the warm-up, hand-off and "
+                                         f"the top-node merges"),
                        "imbalance_max_over_mean": round(partition.imbalance(plan), 3)},
             "e2e": {"value": round(pts / (t_e2e * 1e-3) / 1e6, 2), "unit": "Mpts/s",
                     "h2d_bytes_per_step": h2d // max(args.steps, 1),

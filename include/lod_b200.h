@@ -233,6 +233,18 @@ int lod_write_arena(LodTree *tree, uint64_t off, uint64_t size, const void *src)
  *                     batch position (all-array index - spill length), in no
  *                     particular order; capacity 0 queries *n.  Call before
  *                     the next insert (it reads that cycle's backlog);
+ *   lod_last_voxels_count  how many there are, written to the device word
+ *                     *dev_count (-1 when the last insert's counts are
+ *                     unknown: a queued small cycle) without a host wait;
+ *                     `stream` is ordered behind the write;
+ *   lod_last_voxels_log  append them to a device log instead (no host
+ *                     wait): node, cell, rgba and an order key = key_base +
+ *                     gidx[winner's batch position] (gidx: a device int64
+ *                     array, NULL = the position itself); *dev_count (device
+ *                     int64) is advanced by every voxel, entries past
+ *                     `capacity` are dropped (the caller sizes the log from
+ *                     the batch's n_voxels); ordered after `stream`'s work
+ *                     and `stream` after it (NULL = the legacy stream);
  *   lod_merge_voxels  rewrite each listed node's voxel sequence from gstart[g]
  *                     on with the items goff[g] .. goff[g+1]-1 (cells and
  *                     colours in their final order; the node's own voxels of
@@ -241,6 +253,10 @@ int lod_write_arena(LodTree *tree, uint64_t off, uint64_t size, const void *src)
  *                     copy of a top node holds the single-tree sequence. */
 int lod_last_voxels(LodTree *tree, int32_t max_level, int64_t capacity, int32_t *node, uint32_t *cell,
                     uint32_t *rgba, int64_t *winner, int64_t *n);
+int lod_last_voxels_count(LodTree *tree, int32_t max_level, int64_t *dev_count, void *stream);
+int lod_last_voxels_log(LodTree *tree, int32_t max_level, const int64_t *gidx, int64_t key_base, int32_t *node,
+                        uint32_t *cell, uint32_t *rgba, int64_t *key, int64_t capacity, int64_t *dev_count,
+                        void *stream);
 int lod_merge_voxels(LodTree *tree, int64_t n_groups, const int32_t *gnode, const int64_t *gstart,
                      const int64_t *goff, const uint32_t *cell, const uint32_t *rgba);
 
@@ -341,33 +357,52 @@ int lod_route_bucket(int32_t device, const double *bmin, double size, int32_t de
 /* Multi-GPU routing and composite over peer memory (the fused
  * replacement for the all-to-all and the all-reduce): each rank owns one
  * receive window -- an IPC-shareable device allocation (NVLink peer memory
- * between GPUs) laid out as the int64 count matrix [source][owner] in the
- * first LOD_WINDOW_HEADER_BYTES, then two halves of `half_records` 16-byte
- * records, then two halves of `half_records` uint32 stripe positions (each
- * record's index in its source stripe) -- and maps every peer's window (`windows[r]` = rank r's window as
- * seen by this process, its own included).  Per batch:
- *   lod_route_peers_begin   owners + bucket sizes of this rank's stripe, the
- *                           sizes stored as row `rank` of every peer's matrix;
- *   (host: stream sync + barrier; every rank reads the full matrix)
+ * between GPUs) -- and maps every peer's window (`windows[r]` = rank r's
+ * window as seen by this process, its own included).  Window layout: the
+ * header (LOD_WINDOW_HEADER_BYTES: two int64 count matrices [source][owner],
+ * one per half, then per half every source's count-ready and data-ready
+ * sequence flags and its extra word), two halves of `half_records` 16-byte records, two halves
+ * of `half_records` uint32 stripe positions (each record's index in its
+ * source stripe).  Batch k of a stream uses half k & 1 and sequence k + 1;
+ * the ranks synchronise through the flags alone (no host barrier):
+ *   lod_route_peers_begin   owners + bucket sizes of this rank's stripe,
+ *                           stored as row `rank` of every peer's matrix with
+ *                           a system-scope release of the count flag; then
+ *                           waits (device warp + mapped host word) until
+ *                           every rank's counts are in and copies the full
+ *                           world x world matrix to `matrix` (host); one
+ *                           int64 per rank rides along (`extra_dev`: a device
+ *                           word of this rank, NULL = 0; `extra`: every
+ *                           rank's, host, may be NULL);
  *   lod_route_peers_finish  the stable bucket scatter, each record written
- *                           straight into its owner's window half `half`
- *                           behind the lower source ranks' records;
- *   (host: stream sync + barrier; the owner inserts its half, global order).
+ *                           straight into its owner's window half behind the
+ *                           lower source ranks' records, then the data flags;
+ *                           the stream then waits on the device until every
+ *                           source's records are in (work queued behind it
+ *                           -- the insert -- reads the half in global order).
+ * A rank must not begin batch k before its own use of batch k - 2's half is
+ * ordered on `stream` (the facade inserts on a stream ordered behind it).
+ * host_wait != 0 (ranks time-sliced on ONE device, where a spinning wait
+ * kernel holds the device for its whole time slice): both waits poll the
+ * flags from the host with small copies instead, and finish returns once
+ * every source's records are in.
  * lod_composite_min_peers: the depth-min of all ranks' framebuffers (`fbs`,
  * mapped windows of npix u64 each) over this rank's pixel slice, written back
  * into every framebuffer; after all ranks ran it (stream sync + barrier)
  * every framebuffer holds the composite.  Handles are
  * LOD_IPC_HANDLE_BYTES-byte cudaIpcMemHandle_t blobs. */
 #define LOD_IPC_HANDLE_BYTES 64
-#define LOD_WINDOW_HEADER_BYTES (64 * 64 * 8)
+#define LOD_WINDOW_HEADER_BYTES (2 * 64 * 64 * 8 + 6 * 64 * 8)
 int lod_ipc_alloc(int32_t device, uint64_t bytes, void **ptr, void *handle); /* zeroed; free: lod_device_free */
 int lod_ipc_open(int32_t device, const void *handle, void **ptr);
 int lod_ipc_close(void *ptr);
 int lod_route_peers_begin(int32_t device, const double *bmin, double size, int32_t depth,
                           const int32_t *owner_of_prefix, int32_t world, int32_t rank, const float *xyz, int64_t n,
-                          void *const *windows, void *stream);
+                          void *const *windows, int32_t half, uint64_t seq, const int64_t *extra_dev,
+                          int64_t *matrix, int64_t *extra, int32_t host_wait, void *stream);
 int lod_route_peers_finish(int32_t device, int32_t world, int32_t rank, const float *xyz, const uint32_t *rgba,
-                           int64_t n, void *const *windows, int32_t half, int64_t half_records, void *stream);
+                           int64_t n, void *const *windows, int32_t half, int64_t half_records, uint64_t seq,
+                           int32_t host_wait, void *stream);
 int lod_composite_min_peers(int32_t device, int32_t world, int32_t rank, void *const *fbs, int64_t npix,
                             void *stream);
 

@@ -34,7 +34,7 @@ LOD_FLAG_INPUT_STREAM = 32
 LOD_FLAG_FB_CLEAR = 64
 LOD_NPHASE = 10
 LOD_IPC_HANDLE_BYTES = 64
-LOD_WINDOW_HEADER_BYTES = 64 * 64 * 8
+LOD_WINDOW_HEADER_BYTES = 2 * 64 * 64 * 8 + 6 * 64 * 8
 PHASES = ("count", "split", "resolve", "backlog", "alloc", "sort", "delta", "epilogue", "h2d", "total")
 
 
@@ -157,14 +157,17 @@ SIGNATURES = {
     "lod_route_bucket": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_double, ctypes.c_int32, _P, ctypes.c_int32, _P, _P,
                                         _I64, _P, _P, _P, _P, _P]),
     "lod_last_voxels": (ctypes.c_int, [_P, ctypes.c_int32, _I64, _P, _P, _P, _P, ctypes.POINTER(_I64)]),
+    "lod_last_voxels_count": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P]),
+    "lod_last_voxels_log": (ctypes.c_int, [_P, ctypes.c_int32, _P, _I64, _P, _P, _P, _P, _I64, _P, _P]),
     "lod_merge_voxels": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _P]),
     "lod_ipc_alloc": (ctypes.c_int, [ctypes.c_int32, ctypes.c_uint64, ctypes.POINTER(_P), _P]),
     "lod_ipc_open": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.POINTER(_P)]),
     "lod_ipc_close": (ctypes.c_int, [_P]),
     "lod_route_peers_begin": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_double, ctypes.c_int32, _P, ctypes.c_int32,
-                                             ctypes.c_int32, _P, _I64, _P, _P]),
+                                             ctypes.c_int32, _P, _I64, _P, ctypes.c_int32, ctypes.c_uint64, _P, _P,
+                                             _P, ctypes.c_int32, _P]),
     "lod_route_peers_finish": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P, _I64, _P,
-                                              ctypes.c_int32, _I64, _P]),
+                                              ctypes.c_int32, _I64, ctypes.c_uint64, ctypes.c_int32, _P]),
     "lod_composite_min_peers": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _I64, _P]),
     "lod_device_alloc": (ctypes.c_int, [ctypes.c_int32, ctypes.c_uint64, ctypes.POINTER(_P)]),
     "lod_device_free": (ctypes.c_int, [_P]),

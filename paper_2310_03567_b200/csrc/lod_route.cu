@@ -14,6 +14,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <chrono>
 #include <mutex>
 
 #include "../../include/lod_b200.h"
@@ -30,12 +32,64 @@ constexpr int kRouteTile = kRouteBlock * kRouteRounds;
 constexpr int kRouteMaxWorld = 64;
 
 // A rank's receive window (one cudaMalloc, shared with the other ranks over
-// CUDA IPC; NVLink peer memory between GPUs): the int64 count matrix
-// [source rank][owner rank] in the first kWindowHeader bytes, then two halves
-// of 16-byte records (batches alternate halves, so a sender's next batch never
-// lands on records the owner's previous insert may still read).
+// CUDA IPC; NVLink peer memory between GPUs).  Header: two int64 count
+// matrices [source rank][owner rank] (one per half), then per half the
+// sources' count-ready and data-ready sequence flags (u64 each); then two
+// halves of 16-byte records and two halves of uint32 stripe positions.
+// Batch k (sequence k + 1) uses half k & 1, so a sender's next batch never
+// lands on records or counts the owner may still read.
 constexpr size_t kWindowHeader = LOD_WINDOW_HEADER_BYTES;
-static_assert(kWindowHeader == (size_t)kRouteMaxWorld * kRouteMaxWorld * 8, "window header");
+constexpr size_t kMatBytes = (size_t)kRouteMaxWorld * kRouteMaxWorld * 8;
+constexpr size_t kFlagsOff = 2 * kMatBytes;  // u64 cflag[2][64], u64 dflag[2][64], i64 extra[2][64]
+static_assert(kWindowHeader == 2 * kMatBytes + 6 * kRouteMaxWorld * 8, "window header");
+__device__ __forceinline__ long long *win_matrix(char *w, int half) {
+  return reinterpret_cast<long long *>(w + (size_t)half * kMatBytes);
+}
+__device__ __forceinline__ unsigned long long *win_cflag(char *w, int half, int src) {
+  return reinterpret_cast<unsigned long long *>(w + kFlagsOff) + half * kRouteMaxWorld + src;
+}
+__device__ __forceinline__ unsigned long long *win_dflag(char *w, int half, int src) {
+  return reinterpret_cast<unsigned long long *>(w + kFlagsOff) + (2 + half) * kRouteMaxWorld + src;
+}
+// one int64 per source rank that rides on the count exchange (the facade:
+// the source's count of new replicated-top voxels in its previous batch)
+__device__ __forceinline__ long long *win_extra(char *w, int half, int src) {
+  return reinterpret_cast<long long *>(w + kFlagsOff) + (4 + half) * kRouteMaxWorld + src;
+}
+// system-scope release / acquire on the sequence flags (peer memory)
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// One warp: wait until every source's count-ready (data = false) or
+// data-ready flag of this half reached `seq`.  Gives up after 30 s (a peer
+// that died) so a broken run fails instead of hanging the device; returns
+// whether every flag arrived.
+constexpr unsigned long long kFlagTimeoutNs = 30ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ bool wait_flags(char *own, int world, int half, unsigned long long seq, bool data) {
+  const unsigned long long t0 = globaltimer();
+  bool ok = true;
+  for (int s = threadIdx.x & 31; s < world && ok; s += 32) {
+    const unsigned long long *f = data ? win_dflag(own, half, s) : win_cflag(own, half, s);
+    while (ld_acquire_sys(f) < seq) {
+      if (globaltimer() - t0 > kFlagTimeoutNs) {
+        ok = false;
+        break;
+      }
+      __nanosleep(200);
+    }
+  }
+  return __all_sync(0xffffffffu, ok);
+}
 struct PeerWindows {
   char *p[kRouteMaxWorld];  // p[r] = rank r's window as mapped in this process (own window: local)
 };
@@ -114,6 +168,7 @@ __global__ void __launch_bounds__(1024)
 // a parallel array) so the owner can name each point's global index -- the
 // order the replicated top nodes' voxels are merged in (lod_merge_voxels).
 struct LocalDest {
+  static constexpr bool kRemote = false;
   const long long *starts;
   float4 *out;
   uint32_t *pos;  // may be null
@@ -121,11 +176,12 @@ struct LocalDest {
   __device__ uint32_t *pos_base(int o) const { return pos ? pos + starts[o] : nullptr; }
 };
 struct PeerDest {
+  static constexpr bool kRemote = true;
   PeerWindows win;
   int rank, world, half;
   long long half_records;
   __device__ long long offset(int o) const {
-    const long long *m = reinterpret_cast<const long long *>(win.p[rank]);  // my copy of the matrix
+    const long long *m = win_matrix(win.p[rank], half);  // my copy of this half's matrix
     long long off = 0;
     for (int s = 0; s < rank; ++s) off += m[s * world + o];
     return off;
@@ -198,18 +254,57 @@ __global__ void __launch_bounds__(kRouteBlock)
                            __uint_as_float(__ldg(rgba + i)));
     if (s_pos[o]) s_pos[o][pos] = (uint32_t)i;
   }
+  if (Dest::kRemote) __threadfence_system();  // the records are performed before k_route_signal's flags
 }
 
-// The count exchange: this rank's bucket sizes become row `rank` of every
-// peer's count matrix (world x world remote 8-byte stores).
-__global__ void k_route_publish(const long long *__restrict__ counts, int rank, int world, PeerWindows win) {
+// The count exchange (one CTA): this rank's bucket sizes become row `rank`
+// of every peer's count matrix for this half (world x world remote 8-byte
+// stores), then each peer's count-ready flag of this rank is released.
+// A rank publishes batch k only after its own insert of batch k - 2 (the
+// caller's stream is ordered behind it), so a peer that sees every rank's
+// flag of batch k knows every window's half k & 1 is free again.
+__global__ void __launch_bounds__(1024)
+    k_route_publish(const long long *__restrict__ counts, int rank, int world, PeerWindows win, int half,
+                    unsigned long long seq, const long long *extra) {
   lod::pdl_wait();
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < world * world) {
+  for (int t = threadIdx.x; t < world * world; t += blockDim.x) {
     const int peer = t / world, o = t % world;
-    reinterpret_cast<long long *>(win.p[peer])[rank * world + o] = counts[o];
+    win_matrix(win.p[peer], half)[rank * world + o] = counts[o];
   }
+  if (threadIdx.x < world) *win_extra(win.p[threadIdx.x], half, rank) = extra ? *extra : 0;
+  __syncthreads();
+  if (threadIdx.x < world) {
+    __threadfence_system();
+    st_release_sys(win_cflag(win.p[threadIdx.x], half, rank), seq);
+  }
+}
+
+// Wait (one warp) for every rank's counts of batch `seq`, then hand this
+// half's matrix to the host through mapped memory (host_seq last).
+__global__ void k_route_wait_counts(char *own, int world, int half, unsigned long long seq, long long *host_mat,
+                                    volatile unsigned long long *host_seq) {
+  lod::pdl_wait();
+  const bool ok = wait_flags(own, world, half, seq, false);
+  const long long *m = win_matrix(own, half);
+  for (int t = threadIdx.x; t < world * world; t += 32) host_mat[t] = __ldcg(m + t);
+  for (int t = threadIdx.x; t < world; t += 32) host_mat[world * world + t] = __ldcg(win_extra(own, half, t));
   __threadfence_system();
+  __syncwarp();
+  if (threadIdx.x == 0) *host_seq = ok ? seq : ~0ull;
+}
+
+// After the scatter: release this rank's data-ready flag in every owner's
+// window (the scatter fenced its records at system scope).
+__global__ void k_route_signal(PeerWindows win, int rank, int world, int half, unsigned long long seq) {
+  lod::pdl_wait();
+  if (threadIdx.x < world) st_release_sys(win_dflag(win.p[threadIdx.x], half, rank), seq);
+}
+
+// The owner's side: wait (one warp) until every source's records of batch
+// `seq` are in; the insert behind it on the stream reads them.
+__global__ void k_route_wait_data(char *own, int world, int half, unsigned long long seq) {
+  lod::pdl_wait();
+  wait_flags(own, world, half, seq, true);
 }
 
 // Depth-min composite over peer memory, reduce-scatter and all-gather fused:
@@ -263,6 +358,10 @@ struct RouteScratch {
   uint32_t *tiles = nullptr;
   int32_t *table = nullptr;
   long long *counts = nullptr, *starts = nullptr;  // device, for the peer route
+  long long *h_mat = nullptr, *h_mat_dev = nullptr;  // mapped: a half's count matrix + its sequence word
+  volatile unsigned long long *h_seq = nullptr;
+  unsigned long long *h_flags = nullptr;  // pinned: polled flags (host-wait mode)
+  cudaStream_t pst = nullptr;             // polling stream (host-wait mode)
   long long cap = 0, tcap = 0, table_cap = 0;
 };
 std::mutex g_mu;
@@ -303,6 +402,33 @@ int route_prepare(RouteScratch &s, const double *bmin, double size, int depth, c
     CK(cudaMemsetAsync(s.tiles, 0, (size_t)world * 4, st));
   lod::launch(k_route_scan, 1, 1024, 0, st, s.tiles, ntiles, world, counts, starts);
   return LOD_OK;
+}
+
+#define RK_(expr)            \
+  do {                       \
+    int rc__ = (expr);       \
+    if (rc__) return rc__;   \
+  } while (0)
+
+// Host-wait mode (ranks time-sliced on one device, where a spinning wait
+// kernel would hold the device until its time slice ends): poll this half's
+// count-ready (data = false) or data-ready flags in the own window with small
+// copies on a private stream until every source's reached `seq` (30 s cap).
+int host_poll(RouteScratch &s, char *own, int world, int half, unsigned long long seq, bool data) {
+  if (!s.pst) {
+    CK(cudaStreamCreateWithFlags(&s.pst, cudaStreamNonBlocking));
+    CK(cudaHostAlloc(&s.h_flags, kRouteMaxWorld * 8, cudaHostAllocDefault));
+  }
+  const char *f = own + kFlagsOff + (size_t)((data ? 2 : 0) + half) * kRouteMaxWorld * 8;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    CK(cudaMemcpyAsync(s.h_flags, f, (size_t)world * 8, cudaMemcpyDeviceToHost, s.pst));
+    CK(cudaStreamSynchronize(s.pst));
+    bool all = true;
+    for (int r = 0; r < world; ++r) all &= s.h_flags[r] >= seq;
+    if (all) return LOD_OK;
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30)) return LOD_E_CUDA;
+  }
 }
 
 bool windows_ok(void *const *w, int world) {
@@ -369,9 +495,11 @@ int lod_ipc_close(void *ptr) { return cuda_rc(cudaIpcCloseMemHandle(ptr)); }
 
 int lod_route_peers_begin(int32_t device, const double *bmin, double size, int32_t depth,
                           const int32_t *owner_of_prefix, int32_t world, int32_t rank, const float *xyz, int64_t n,
-                          void *const *windows, void *stream) {
+                          void *const *windows, int32_t half, uint64_t seq, const int64_t *extra_dev,
+                          int64_t *matrix, int64_t *extra, int32_t host_wait, void *stream) {
   if (!bmin || !owner_of_prefix || depth < 0 || depth > 8 || world < 1 || world > kRouteMaxWorld || rank < 0 ||
-      rank >= world || n < 0 || (n > 0 && !xyz) || !windows_ok(windows, world) || device < 0 || device >= 64)
+      rank >= world || n < 0 || (n > 0 && !xyz) || !windows_ok(windows, world) || device < 0 || device >= 64 ||
+      half < 0 || half > 1 || seq == 0 || seq == ~0ull || !matrix)
     return LOD_E_ARG;
   std::lock_guard<std::mutex> lk(g_mu);
   cudaSetDevice(device);
@@ -380,28 +508,69 @@ int lod_route_peers_begin(int32_t device, const double *bmin, double size, int32
   if (!s.counts) {
     CK(cudaMalloc(&s.counts, 2 * kRouteMaxWorld * sizeof(long long)));
     s.starts = s.counts + kRouteMaxWorld;
+    CK(cudaHostAlloc(&s.h_mat, kMatBytes + kRouteMaxWorld * 8 + 8, cudaHostAllocMapped));
+    s.h_seq = reinterpret_cast<volatile unsigned long long *>(reinterpret_cast<char *>(s.h_mat) + kMatBytes +
+                                                              kRouteMaxWorld * 8);
+    *s.h_seq = 0;
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s.h_mat_dev), s.h_mat, 0));
   }
   int rc = route_prepare(s, bmin, size, depth, owner_of_prefix, world, xyz, n, s.counts, s.starts, st);
   if (rc) return rc;
-  lod::launch(k_route_publish, cdiv(world * world, 256), 256, 0, st, (const long long *)s.counts, (int)rank,
-              (int)world, pack_windows(windows, world));
-  return cuda_rc(cudaGetLastError());
+  const PeerWindows pw = pack_windows(windows, world);
+  *s.h_seq = 0;  // the previous wait kernel is done (its word was seen): no stale match
+  lod::launch(k_route_publish, 1, 1024, 0, st, (const long long *)s.counts, (int)rank, (int)world, pw, (int)half,
+              (unsigned long long)seq, (const long long *)extra_dev);
+  if (host_wait) {
+    RK_(host_poll(s, pw.p[rank], world, half, seq, false));
+    CK(cudaMemcpyAsync(s.h_mat, pw.p[rank] + (size_t)half * kMatBytes, (size_t)world * world * 8,
+                       cudaMemcpyDeviceToHost, s.pst));
+    CK(cudaMemcpyAsync(s.h_mat + world * world, pw.p[rank] + kFlagsOff + (size_t)(4 + half) * kRouteMaxWorld * 8,
+                       (size_t)world * 8, cudaMemcpyDeviceToHost, s.pst));
+    CK(cudaStreamSynchronize(s.pst));
+    for (int t = 0; t < world * world; ++t) matrix[t] = s.h_mat[t];
+    if (extra)
+      for (int t = 0; t < world; ++t) extra[t] = s.h_mat[world * world + t];
+    return LOD_OK;
+  }
+  lod::launch(k_route_wait_counts, 1, 32, 0, st, pw.p[rank], (int)world, (int)half, (unsigned long long)seq,
+              s.h_mat_dev, (volatile unsigned long long *)(s.h_mat_dev + kMatBytes / 8 + kRouteMaxWorld));
+  CK(cudaGetLastError());
+  // the host needs the matrix (window sizes, this rank's record count):
+  // poll the mapped sequence word the wait kernel writes last
+  for (unsigned spins = 0; *s.h_seq != seq; ++spins) {
+    if (*s.h_seq == ~0ull) return LOD_E_CUDA;  // a peer's counts never arrived
+    if ((spins & 1023) == 1023) {
+      const cudaError_t e = cudaStreamQuery(st);
+      if (e != cudaSuccess && e != cudaErrorNotReady) return cuda_rc(e);
+      if (e == cudaSuccess && *s.h_seq != seq) return LOD_E_CUDA;  // drained without the write
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  for (int t = 0; t < world * world; ++t) matrix[t] = s.h_mat[t];
+  if (extra)
+    for (int t = 0; t < world; ++t) extra[t] = s.h_mat[world * world + t];
+  return LOD_OK;
 }
 
 int lod_route_peers_finish(int32_t device, int32_t world, int32_t rank, const float *xyz, const uint32_t *rgba,
-                           int64_t n, void *const *windows, int32_t half, int64_t half_records, void *stream) {
+                           int64_t n, void *const *windows, int32_t half, int64_t half_records, uint64_t seq,
+                           int32_t host_wait, void *stream) {
   if (world < 1 || world > kRouteMaxWorld || rank < 0 || rank >= world || n < 0 || (n > 0 && (!xyz || !rgba)) ||
-      !windows_ok(windows, world) || half < 0 || half > 1 || half_records < 0 || device < 0 || device >= 64)
+      !windows_ok(windows, world) || half < 0 || half > 1 || half_records < 0 || device < 0 || device >= 64 ||
+      seq == 0 || seq == ~0ull)
     return LOD_E_ARG;
   std::lock_guard<std::mutex> lk(g_mu);
   cudaSetDevice(device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   RouteScratch &s = g_rs[device];
   if (n > s.cap) return LOD_E_ARG;  // begin() sized the scratch for this stripe
+  const PeerWindows pw = pack_windows(windows, world);
   if (n > 0)
     lod::launch(k_route_scatter<PeerDest>, cdiv(n, kRouteTile), kRouteBlock, 0, st, xyz, rgba, (long long)n,
-                (int)world, s.owner, s.tiles,
-                PeerDest{pack_windows(windows, world), (int)rank, (int)world, (int)half, (long long)half_records});
+                (int)world, s.owner, s.tiles, PeerDest{pw, (int)rank, (int)world, (int)half, (long long)half_records});
+  lod::launch(k_route_signal, 1, 64, 0, st, pw, (int)rank, (int)world, (int)half, (unsigned long long)seq);
+  if (host_wait) return host_poll(s, pw.p[rank], world, half, seq, true);
+  lod::launch(k_route_wait_data, 1, 32, 0, st, pw.p[rank], (int)world, (int)half, (unsigned long long)seq);
   return cuda_rc(cudaGetLastError());
 }
 

@@ -228,6 +228,7 @@ struct LodTree {
     cudaEvent_t ready = nullptr;
   } stage[3];
   cudaEvent_t ev_counted = nullptr;  // the running cycle's first count pass is done
+  cudaEvent_t ev_aux = nullptr;      // lod_last_voxels_count -> caller stream
   cudaEvent_t ev_input = nullptr;    // the caller's input stream (LOD_FLAG_INPUT_STREAM)
   int stage_next = 0;
   cudaEvent_t ev[16] = {};  // 12, 13: per-iteration k_count brackets; 10/11 and 14/15: the two
@@ -1010,6 +1011,7 @@ int lod_tree_destroy(LodTree *t) {
   t->dpstart.release(); t->dpcount.release(); t->dvbase.release(); t->dvcell.release(); t->dvrgba.release();
   if (t->cst) cudaStreamSynchronize(t->cst);
   if (t->ev_counted) cudaEventDestroy(t->ev_counted);
+  if (t->ev_aux) cudaEventDestroy(t->ev_aux);
   if (t->ev_input) cudaEventDestroy(t->ev_input);
   for (auto &sg : t->stage) {
     sg.xyz.release();
@@ -1733,6 +1735,27 @@ __global__ void k_last_voxels(NodeCols nd, const uint4 *__restrict__ backlog, lo
   }
 }
 
+// lod_last_voxels_log: append the last cycle's voxels at nodes of level <
+// max_level to a device log (node, cell, rgba, order key = key_base + the
+// winner's batch position mapped through `gidx`, when given).
+__global__ void k_last_voxels_log(NodeCols nd, const uint4 *__restrict__ backlog, long long nv, int max_level,
+                                  long long n_s, const long long *__restrict__ gidx, long long key_base,
+                                  int32_t *node, uint32_t *cell, uint32_t *rgba, long long *key, long long cap,
+                                  unsigned long long *count) {
+  lod::pdl_wait();
+  for (long long i = gtid(); i < nv; i += gstride()) {
+    const uint4 e = backlog[i];
+    if (nd.level[e.x] >= max_level) continue;
+    const unsigned long long k = atomicAdd(count, 1ull);
+    if ((long long)k >= cap) continue;
+    const long long w = (long long)e.w - n_s;
+    node[k] = (int32_t)e.x;
+    cell[k] = e.y;
+    rgba[k] = e.z;
+    key[k] = key_base + (gidx ? gidx[w] : w);
+  }
+}
+
 // Rewrite / extend the voxel sequences of listed nodes (lod_merge_voxels):
 // one warp per group; lane 0 links the chunks the longer sequence needs
 // (acquisitions numbered by an atomic counter: LIFO free stack first, then
@@ -1848,6 +1871,49 @@ int lod_last_voxels(LodTree *t, int32_t max_level, int64_t capacity, int32_t *no
     CK(cudaMemcpyAsync(winner, t->goff.p, k * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   }
+  return LOD_OK;
+}
+
+int lod_last_voxels_count(LodTree *t, int32_t max_level, int64_t *dev_count, void *stream) {
+  if (!t || !dev_count) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  cudaStream_t st = t->st;
+  if (!t->last_backlog && t->last_nv) {  // a queued small cycle: unknown
+    CK(cudaMemsetAsync(dev_count, 0xFF, 8, st));
+  } else {
+    CK(cudaMemsetAsync(dev_count, 0, 8, st));
+    const long long nv = t->last_backlog ? t->last_nv : 0;
+    if (nv)  // counting only (capacity 0: nothing is written)
+      lod::launch(k_last_voxels, grid_for(nv), 256, 0, st, t->nd, t->last_backlog, nv, (int)max_level, t->last_ns,
+                  0LL, (int32_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr, (long long *)nullptr,
+                  reinterpret_cast<unsigned long long *>(dev_count));
+  }
+  if (!t->ev_aux) CK(cudaEventCreateWithFlags(&t->ev_aux, cudaEventDisableTiming));
+  CK(cudaEventRecord(t->ev_aux, st));
+  CK(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), t->ev_aux, 0));
+  return LOD_OK;
+}
+
+int lod_last_voxels_log(LodTree *t, int32_t max_level, const int64_t *gidx, int64_t key_base, int32_t *node,
+                        uint32_t *cell, uint32_t *rgba, int64_t *key, int64_t capacity, int64_t *dev_count,
+                        void *stream) {
+  if (!t || !dev_count || capacity < 0 || (capacity > 0 && (!node || !cell || !rgba || !key))) return LOD_E_ARG;
+  cudaSetDevice(t->dev);
+  if (!t->last_backlog && t->last_nv) return LOD_E_ARG;  // a queued small cycle: unknown
+  cudaStream_t st = t->st;
+  // the log and the index map were written on the caller's stream (NULL: the
+  // legacy default stream, which the tree's non-blocking stream does not
+  // follow implicitly)
+  if (!t->ev_aux) CK(cudaEventCreateWithFlags(&t->ev_aux, cudaEventDisableTiming));
+  CK(cudaEventRecord(t->ev_aux, reinterpret_cast<cudaStream_t>(stream)));
+  CK(cudaStreamWaitEvent(st, t->ev_aux, 0));
+  const long long nv = t->last_backlog ? t->last_nv : 0;
+  if (nv)
+    lod::launch(k_last_voxels_log, grid_for(nv), 256, 0, st, t->nd, t->last_backlog, nv, (int)max_level, t->last_ns,
+                (const long long *)gidx, (long long)key_base, node, cell, rgba, (long long *)key, (long long)capacity,
+                reinterpret_cast<unsigned long long *>(dev_count));
+  CK(cudaEventRecord(t->ev_aux, st));
+  CK(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), t->ev_aux, 0));
   return LOD_OK;
 }
 

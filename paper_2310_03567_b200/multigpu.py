@@ -32,6 +32,8 @@ device-side spin waits, so ranks that share one GPU (the single-GPU test box:
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib, partition
@@ -221,8 +223,18 @@ class PeerWindows:
         h = ctypes.create_string_buffer(_lib.LOD_IPC_HANDLE_BYTES)
         _lib.check(L.lod_ipc_alloc(device, self.nbytes, ctypes.byref(own), h), "lod_ipc_alloc")
         self.own = int(own.value)
+        import torch
+
         handles = [None] * world
-        dist.all_gather_object(handles, bytes(h.raw), group=group)
+        uuid = str(torch.cuda.get_device_properties(device).uuid)
+        dist.all_gather_object(handles, (bytes(h.raw), uuid), group=group)
+        # ranks time-sliced on one device: the route's waits poll from the
+        # host (a spinning wait kernel would hold the device for a time slice)
+        self.shared_device = len({u for _, u in handles}) < world
+        forced = os.environ.get("LOD_ROUTE_WAIT", "")  # "device" / "host": force a mode (tests)
+        if forced in ("device", "host"):
+            self.shared_device = forced == "host"
+        handles = [hb for hb, _ in handles]
         self.ptrs = (ctypes.c_void_p * world)()
         self._opened = []
         err = ""
@@ -276,10 +288,13 @@ class PeerRouter:
     """Routing of striped batches to the owners of their octant prefixes over
     peer memory (``lod_route_peers_begin`` / ``_finish``): the bucket sizes
     are exchanged through every window's count matrix, then the stable bucket
-    scatter stores each record directly in its owner's window.  Windows hold
-    two halves of ``half_records`` records (batches alternate halves) and grow
-    collectively -- every rank reads the same full count matrix, so all ranks
-    take the same decision."""
+    scatter stores each record directly in its owner's window.  The ranks
+    synchronise through sequence flags in the windows (system-scope release /
+    acquire on the device, one mapped host word for the matrix) -- no process
+    group barrier and no stream sync per batch.  Windows hold two halves of
+    ``half_records`` records (batches alternate halves) and grow collectively
+    -- every rank reads the same full count matrix, so all ranks take the
+    same decision (the only step that uses the process group)."""
 
     def __init__(self, device: int, rank: int, world: int, plan: partition.Plan, half_records: int = 1 << 20,
                  group=None, bmin=(0.0, 0.0, 0.0), size: float = 1.0):
@@ -290,26 +305,29 @@ class PeerRouter:
         self.win = PeerWindows(device, rank, world, self._bytes(self.half_records), group)
         self.k = 0
         self.matrix = np.zeros((world, world), np.int64)
+        self.extra = np.zeros(world, np.int64)
 
     @staticmethod
     def _bytes(half_records: int) -> int:
         # header | records half 0 | records half 1 | positions half 0 | positions half 1
         return _lib.LOD_WINDOW_HEADER_BYTES + 2 * 16 * half_records + 2 * 4 * half_records
 
-    def _begin(self, x, n: int, stream: int) -> None:
+    def _begin(self, x, n: int, stream: int, extra_dev) -> None:
         import ctypes
 
         _lib.check(self.win._L.lod_route_peers_begin(
             self.device, _lib.ptr(self.bmin), self.size, int(self.plan.depth), _lib.ptr(self.table), self.world,
-            self.rank, _lib.ptr(x), n, self.win.ptrs, ctypes.c_void_p(stream)), "lod_route_peers_begin")
-        _sync_barrier(self.device, self.group)
-        _lib.check(self.win._L.lod_memcpy_d2h(_lib.ptr(self.matrix), self.win.own, self.matrix.nbytes),
-                   "count matrix")
+            self.rank, _lib.ptr(x), n, self.win.ptrs, self.k & 1, self.k + 1,
+            None if extra_dev is None else _lib.ptr(extra_dev), _lib.ptr(self.matrix), _lib.ptr(self.extra),
+            int(self.win.shared_device), ctypes.c_void_p(stream)), "lod_route_peers_begin")
 
-    def route(self, xyz, rgba):
+    def route(self, xyz, rgba, extra_dev=None):
         """This rank's stripe (CUDA tensors) in; this rank's points of the
         global batch out, as an (n, 4) int32 view of its window in global order
-        (valid until the batch after next is routed)."""
+        (valid until the batch after next is routed; the current stream waits
+        on the device until every source's records are in).  ``extra_dev``:
+        an optional int64 CUDA scalar published with this rank's counts;
+        afterwards ``self.extra[r]`` holds rank r's."""
         import ctypes
 
         import torch
@@ -317,18 +335,18 @@ class PeerRouter:
         x, c = xyz.contiguous(), rgba.contiguous()
         n = int(c.shape[0])
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        self._begin(x, n, stream)
+        self._begin(x, n, stream, extra_dev)
         need = int(self.matrix.sum(axis=0).max())
-        if need > self.half_records:  # identical decision on every rank
+        if need > self.half_records:  # identical decision on every rank (collective re-allocation)
             self.win.close()
             self.half_records = max(need, 2 * self.half_records)
             self.win = PeerWindows(self.device, self.rank, self.world, self._bytes(self.half_records), self.group)
-            self._begin(x, n, stream)
+            self._begin(x, n, stream, extra_dev)  # fresh windows: the counts again
         half = self.k & 1
         _lib.check(self.win._L.lod_route_peers_finish(
             self.device, self.world, self.rank, _lib.ptr(x), _lib.ptr(c), n, self.win.ptrs, half,
-            self.half_records, ctypes.c_void_p(stream)), "lod_route_peers_finish")
-        _sync_barrier(self.device, self.group)
+            self.half_records, self.k + 1, int(self.win.shared_device), ctypes.c_void_p(stream)),
+            "lod_route_peers_finish")
         self.k += 1
         mine = int(self.matrix[:, self.rank].sum())
         base = self.win.own + _lib.LOD_WINDOW_HEADER_BYTES + half * 16 * self.half_records
@@ -345,7 +363,8 @@ class PeerRouter:
         col = self.matrix[:, self.rank]
         stripe_off = np.concatenate([[0], np.cumsum(self.matrix.sum(axis=1))])[:-1]
         dev = self.last_positions.device
-        src = torch.repeat_interleave(torch.arange(self.world, device=dev), torch.as_tensor(col, device=dev))
+        src = torch.repeat_interleave(torch.arange(self.world, device=dev), torch.as_tensor(col, device=dev),
+                                      output_size=int(col.sum()))  # no device sync
         return torch.as_tensor(stripe_off, device=dev)[src] + self.last_positions.to(torch.int64)
 
     def close(self) -> None:
@@ -505,9 +524,26 @@ class PartitionedInserter:
         self.router = None  # PeerRouter, created at the first partitioned batch
         self.no_peers = ""  # why the peer route is unavailable (then: NCCL all-to-all)
         self.merged_top = 0  # top-node voxels merged across ranks so far
+        self.flushes = 0  # top-voxel log merges (peer route)
+        self.flush_at = int(os.environ.get("LOD_TOP_FLUSH_AT", 1 << 22))  # merge when some rank's log holds more
+        # peer route: this rank's replicated-top voxels since the last merge,
+        # on the device (node, cell, rgba, order key = batch << 40 | global index)
+        self._log = None
+        self._log_count = None  # int64 CUDA scalar: entries appended (published with the counts)
+        self._log_used = 0  # its value as of the last route
+        self._batch = 0
 
     def insert(self, xyz, rgba) -> int:
-        """Insert this rank's stripe of one global batch; returns points inserted here."""
+        """Insert this rank's stripe of one global batch; returns points inserted here.
+        With the peer route, the voxels each rank creates at the replicated
+        top nodes go to a device log and are merged across ranks when a log
+        fills up or at ``flush`` (collective) -- not per batch.  Claims are
+        unaffected (each top-node cell is claimed on exactly one rank), and a
+        depth-min composite of the ranks' renders is the same either way;
+        only a rank's own copy of a top node lacks the other ranks' voxels
+        until the merge."""
+        import ctypes
+
         import torch
         import torch.distributed as dist
 
@@ -522,13 +558,29 @@ class PartitionedInserter:
                     self.router = PeerRouter(self.tree.device, self.rank, self.world, self.plan,
                                              half_records=2 * int(rgba.shape[0]), group=self.group,
                                              bmin=self.bmin, size=self.size)
+                    self._log_count = torch.zeros(1, dtype=torch.int64, device=xyz.device)
                 except PeerUnavailable as e:  # GPUs without a peer path: route with the collective
                     self.no_peers = str(e)
             if self.router is not None:
-                rec = self.router.route(xyz, rgba)
+                # every rank's top-voxel log fill rides on the count exchange,
+                # so all ranks take the same flush decision without a collective
+                rec = self.router.route(xyz, rgba, extra_dev=self._log_count)
+                self._log_used = int(self.router.extra[self.rank])
+                if int(self.router.extra.max()) > self.flush_at:
+                    self._flush_log(self._log_used)
                 gidx = self.router.global_index()
-            else:
-                rec, gidx = route(xyz, rgba, self.plan, self.world, self.group, self.bmin, self.size, with_index=True)
+                insert_records(self.tree, rec, self.state)
+                nv = max(int(self.state._bstats.n_voxels), 0)  # bounds this batch's top voxels
+                self._ensure_log(self._log_used + nv)
+                stream = torch.cuda.current_stream(self.tree.device).cuda_stream
+                lg = self._log
+                _lib.check(self.tree._L.lod_last_voxels_log(
+                    self.tree.handle, int(self.plan.depth), _lib.ptr(gidx), self._batch << 40, _lib.ptr(lg[0]),
+                    _lib.ptr(lg[1]), _lib.ptr(lg[2]), _lib.ptr(lg[3]), int(lg[0].shape[0]), _lib.ptr(self._log_count),
+                    ctypes.c_void_p(stream)), "last_voxels_log")
+                self._batch += 1
+                return int(rec.shape[0])
+            rec, gidx = route(xyz, rgba, self.plan, self.world, self.group, self.bmin, self.size, with_index=True)
             insert_records(self.tree, rec, self.state)
             self._merge_top(gidx)
             return int(rec.shape[0])
@@ -566,8 +618,50 @@ class PartitionedInserter:
         dist.all_gather_object(everyone, (node, cell, rgba, g), group=self.group)
         self.merged_top += merge_top_voxels(self.tree, node, everyone)
 
+    def _ensure_log(self, n: int) -> None:
+        import torch
+
+        cap = 0 if self._log is None else int(self._log[0].shape[0])
+        if n <= cap:
+            return
+        new_cap = max(n, 2 * cap, 1 << 16)
+        dev = self._log_count.device
+        lg = (torch.empty(new_cap, dtype=torch.int32, device=dev), torch.empty(new_cap, dtype=torch.int32, device=dev),
+              torch.empty(new_cap, dtype=torch.int32, device=dev), torch.empty(new_cap, dtype=torch.int64, device=dev))
+        if self._log is not None and self._log_used:
+            for a, b in zip(lg, self._log):
+                a[: self._log_used].copy_(b[: self._log_used])
+        self._log = lg
+
+    def _flush_log(self, used: int) -> None:
+        """Merge every rank's logged top voxels (collective: all ranks call
+        it with their own entry count) and empty the logs."""
+        import torch.distributed as dist
+
+        if used:
+            node = self._log[0][:used].cpu().numpy()
+            cell = self._log[1][:used].cpu().numpy().view(np.uint32)
+            rgba = self._log[2][:used].cpu().numpy().view(np.uint32)
+            key = self._log[3][:used].cpu().numpy()
+        else:
+            node, cell, rgba = np.empty(0, np.int32), np.empty(0, np.uint32), np.empty(0, np.uint32)
+            key = np.empty(0, np.int64)
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, (node, cell, rgba, key), group=self.group)
+        self.merged_top += merge_top_voxels(self.tree, node, everyone)
+        self._log_count.zero_()
+        self._log_used = 0
+        self.flushes += 1
+
+    def flush(self) -> None:
+        """Merge the replicated-top voxels logged since the last merge
+        (collective; before reading a rank's top nodes as the single tree's)."""
+        if self._log_count is not None:
+            self._flush_log(int(self._log_count.item()))
+
     def close(self) -> None:
-        """Release the peer windows (collective)."""
+        """Merge what is pending and release the peer windows (collective)."""
+        self.flush()
         if self.router is not None:
             self.router.close()
             self.router = None

@@ -64,6 +64,7 @@ def main() -> None:
     for x, c in batches:
         sl = slice(rank * stripe, (rank + 1) * stripe)
         ins.insert(torch.from_numpy(x[sl]).cuda(), torch.from_numpy(c[sl].view(np.int32)).cuda())
+    ins.flush()  # the last batch's replicated-top merge
     assert ins.partitioned
     res = {}
     for path, nid in tree_paths(tree.inner, tree.children).items():

@@ -23,8 +23,11 @@ P = dict(bmin=(0.0, 0.0, 0.0), size=1.0, arena_bytes=512 << 20, chunk_capacity=2
          leaf_threshold=400, max_depth=14, backlog_capacity=10_000_000, spill_capacity=100_000_000)
 
 
-@pytest.mark.parametrize("world,depth", [(2, 1), (4, 2)])
-def test_peer_route_and_composite_match_single_tree(gpu, tmp_path, world, depth):
+@pytest.mark.parametrize("world,depth,wait", [(2, 1, "host"), (4, 2, "host"), (2, 1, "device")])
+def test_peer_route_and_composite_match_single_tree(gpu, tmp_path, world, depth, wait):
+    """wait: how the ranks wait on the window flags -- "device" (spinning
+    wait kernels: the multi-GPU mode) or "host" (polled from the host: the
+    mode ranks sharing one GPU select, as here)."""
     from oracle.rebuild import tree_paths
     from paper_2310_03567_b200 import insert_batch, synth
     from paper_2310_03567_b200.render import Camera, rasterize
@@ -33,7 +36,7 @@ def test_peer_route_and_composite_match_single_tree(gpu, tmp_path, world, depth)
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    env = dict(os.environ, LOD_POOL_RESERVE_MIB="256")
+    env = dict(os.environ, LOD_POOL_RESERVE_MIB="256", LOD_ROUTE_WAIT=wait)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(HERE, "peer_worker.py"),
            str(tmp_path), str(n_batches), str(stripe), str(depth)]
@@ -68,7 +71,9 @@ def test_peer_route_and_composite_match_single_tree(gpu, tmp_path, world, depth)
         xs, cs = g.gather_samples(gp[path])
         want = np.concatenate([xs.view(np.uint32), cs.reshape(-1, 1)], axis=1)
         for k, d in enumerate(ranks):
-            assert np.array_equal(d["t_" + key], want), (path, k)
+            got = d["t_" + key]
+            diff = np.flatnonzero((got != want).any(axis=1))[:5] if got.shape == want.shape else None
+            assert np.array_equal(got, want), (path, k, got.shape, want.shape, diff)
             assert np.array_equal(d["tg_" + key], g.occupied_cells(gp[path])), (path, k)
     cam = Camera((0.5, 0.45, -1.3), (0.5, 0.5, 0.5), fov_deg=60.0, near=0.05, far=50.0, width=320, height=240)
     for thr, name in ((-1.0, "comp_all"), (64.0, "comp_64")):

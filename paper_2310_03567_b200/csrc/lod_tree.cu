@@ -225,8 +225,10 @@ struct LodTree {
     long long n = 0;
     bool valid = false;
     bool pending = false;  // copy requested, not yet issued (issued behind the next count pass)
+    unsigned long long order = 0;  // prefetch order (copies are issued oldest first)
     cudaEvent_t ready = nullptr;
   } stage[3];
+  unsigned long long stage_order = 0;
   cudaEvent_t ev_counted = nullptr;  // the running cycle's first count pass is done
   cudaEvent_t ev_aux = nullptr;      // lod_last_voxels_count -> caller stream
   cudaEvent_t ev_input = nullptr;    // the caller's input stream (LOD_FLAG_INPUT_STREAM)
@@ -391,7 +393,7 @@ static bool mapped_sync(const LodTree *t) {
 // then_issue: the queued batches' H2D copies are issued behind the
 // publication (a copy streaming over PCIe slows the publication's
 // system-scope write from ~5 to ~20 us).
-static int issue_pending(LodTree *t);
+static int issue_pending(LodTree *t, const LodTree::Stage *upto = nullptr);
 static int sync_ctrl(LodTree *t, bool then_issue = false) {
   if (!mapped_sync(t)) {
     if (then_issue) RK(issue_pending(t));
@@ -603,17 +605,27 @@ static void release_scan_lb(ScanLB &lb) {
 
 static int issue_stage(LodTree *t, LodTree::Stage &sg);
 
-// Issue the queued batches' deferred H2D copies behind the work queued so far.
-static int issue_pending(LodTree *t) {
+// Issue the oldest queued batch's deferred H2D copy behind the work queued so
+// far (through `upto`, when given: every copy up to that slot).  One copy
+// per cycle keeps pace with the inserts and leaves the copy engines idle for
+// part of each cycle -- where the split iteration's publication lands (a
+// copy streaming over PCIe slows that system-scope write from ~5 to ~20 us).
+static int issue_pending(LodTree *t, const LodTree::Stage *upto) {
   if (!t->cst) return LOD_OK;
-  bool any = false;
-  for (auto &sg : t->stage) any |= sg.valid && sg.pending;
-  if (!any) return LOD_OK;
-  CK(cudaEventRecord(t->ev_counted, t->st));
-  CK(cudaStreamWaitEvent(t->cst, t->ev_counted, 0));
-  for (auto &sg : t->stage)
-    if (sg.valid && sg.pending) RK(issue_stage(t, sg));
-  return LOD_OK;
+  bool recorded = false;
+  for (;;) {
+    LodTree::Stage *old = nullptr;
+    for (auto &sg : t->stage)
+      if (sg.valid && sg.pending && (!old || sg.order < old->order)) old = &sg;
+    if (!old) return LOD_OK;
+    if (!recorded) {
+      CK(cudaEventRecord(t->ev_counted, t->st));
+      CK(cudaStreamWaitEvent(t->cst, t->ev_counted, 0));
+      recorded = true;
+    }
+    RK(issue_stage(t, *old));
+    if (!upto || old == upto || !upto->pending) return LOD_OK;
+  }
 }
 
 static void fill_stats(LodTree *t, LodBatchStats *s) {
@@ -1151,7 +1163,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   if (staged) {  // prefetched on the copy stream: wait for it, no copy here
     // a copy not issued yet goes behind the work queued so far on the tree
     // stream: an earlier early-returning insert's tail may still read this slot
-    if (staged->pending) RK(issue_pending(t));
+    if (staged->pending) RK(issue_pending(t, staged));
     CK(cudaStreamWaitEvent(st, staged->ready, 0));
     staged->valid = false;
     if (packed) {
@@ -2402,6 +2414,7 @@ static int prefetch_impl(LodTree *t, const void *xyz, const uint32_t *rgba, int6
   sg.n = n;
   sg.valid = true;
   sg.pending = true;
+  sg.order = ++t->stage_order;
   return LOD_OK;
 }
 

@@ -163,6 +163,8 @@ struct Geo {
   long long T;               // leaf_threshold
   int max_depth;
   long long C;               // chunk capacity (records)
+  int fresh;                 // arena < 128 GiB: desc .y bit 31 marks a grid still all clear (kFresh)
+  uint32_t gmask;            // desc .y bits of the grid offset / 64 (0x7fffffff with `fresh`)
 };
 
 // One point source over the reference's all-array [spill || batch]

@@ -25,6 +25,11 @@
 
 namespace lod {
 
+// NodeCols::desc .y bit 31 (Geo::fresh, arenas < 128 GiB, where grid
+// offsets / 64 stay below 2^31): the node split in the running cycle, its
+// grid is still all clear.
+constexpr int kFresh = (int)0x80000000u;
+
 // Device-side control block; pinned host mirror is read at each sync point.
 struct Ctrl {
   long long num_nodes;
@@ -324,7 +329,11 @@ __device__ __forceinline__ int count_descend(const NodeCols &nd, const Geo &geo,
   // table; grid words bypass L1 so they do not evict it
   do {
     const long long cell = cell_of(geo, x, y, z, bx, by, bz, s, inv_s);
-    const uint32_t w = ld_nol1(grid32 + ((unsigned long long)(uint32_t)d.y << 4) + (cell >> 5));
+    // a node split in this cycle has an all-clear grid (fresh arena, bits
+    // are set only by k_resolve): its claims need no grid word
+    const uint32_t w = (geo.fresh && d.y < 0)
+                           ? 0u
+                           : ld_nol1(grid32 + ((unsigned long long)((uint32_t)d.y & geo.gmask) << 4) + (cell >> 5));
     const int cur = nid;
     nid = d.x + octant_step(x, y, z, bx, by, bz, s, inv_s);
     d = __ldg(nd.desc + nid);
@@ -668,7 +677,9 @@ __global__ void k_exec_nodes(NodeCols nd, Geo geo, const int32_t *__restrict__ s
       const unsigned long long gstride_b = ((unsigned long long)geo.grid_bytes + 63ull) / 64ull * 64ull;
       const unsigned long long goff = ctrl->plan_grid0 + (unsigned long long)k * gstride_b;
       nd.grid_off[nid] = (long long)goff;
-      nd.desc[nid] = make_int2((int)(ctrl->plan_num_nodes0 + 8ll * k), (int)(uint32_t)(goff >> 6));
+      // kFresh: the grid is all clear until k_resolve (k_epilogue drops the bit)
+      nd.desc[nid] = make_int2((int)(ctrl->plan_num_nodes0 + 8ll * k),
+                               (int)((uint32_t)(goff >> 6) | (geo.fresh ? (uint32_t)kFresh : 0u)));
       srank[nid] = -1;
     }
   }
@@ -1031,7 +1042,7 @@ __global__ void k_store(StoreSink sink, const uint32_t *__restrict__ skeys, cons
 __global__ void k_epilogue(NodeCols nd, PoolCols pool, const int32_t *__restrict__ seg_node,
                            const long long *__restrict__ seg_start, const U64x2 *__restrict__ plan,
                            const U64x2 *__restrict__ plan_ex, Ctrl *ctrl, uint32_t *__restrict__ ghist,
-                           const int *guard) { lod::pdl_wait();
+                           const int *guard, int geo_fresh) { lod::pdl_wait();
   if (guard && *guard) return;
   // the sort is the last reader of the digit totals: zeroed for the next cycle
   for (long long i = gtid(); i < kMaxPassesHist; i += gstride()) ghist[i] = 0;
@@ -1047,6 +1058,10 @@ __global__ void k_epilogue(NodeCols nd, PoolCols pool, const int32_t *__restrict
       nd.count[n] += seg_start[d + 1] - seg_start[d];
       nd.pending[n] = 0;
       nd.final_[n] = 0;
+      // a node split this cycle got voxels (every re-descending point claims
+      // a cell of its all-clear grid), so it is a segment: its grid is no
+      // longer fresh
+      if (geo_fresh && nd.desc[n].y < 0) nd.desc[n].y &= ~kFresh;
       if (need > 0) {
         const long long cc1 = nd.chunk_count[n];
         cc0 = cc1 - need;
@@ -1157,11 +1172,12 @@ __global__ void k_delta_vox(const uint32_t *__restrict__ skeys, const uint32_t *
 }
 
 // Safety net after a fatal error: pending/final of every node back to zero.
-__global__ void k_clear_marks_all(NodeCols nd, int32_t *srank, long long n) { lod::pdl_wait();
+__global__ void k_clear_marks_all(NodeCols nd, int32_t *srank, long long n, int geo_fresh) { lod::pdl_wait();
   for (long long i = gtid(); i < n; i += gstride()) {
     nd.pending[i] = 0;
     nd.final_[i] = 0;
     srank[i] = -1;
+    if (geo_fresh && nd.desc[i].y < 0) nd.desc[i].y &= ~kFresh;
   }
 }
 

@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_cycle(SmallArgs a) {
         bool clear = false;
         if (in) {
           cell = cell_of(geo, x, y, z, bx, by, bz, s, inv_s);
-          const uint32_t w = __ldcg(grid32 + ((unsigned long long)(uint32_t)d.y << 4) + (cell >> 5));
+          const uint32_t w = __ldcg(grid32 + ((unsigned long long)((uint32_t)d.y & a.geo.gmask) << 4) + (cell >> 5));
           clear = !(w & (1u << (cell & 31)));
           if (clear) key = ((unsigned long long)(uint32_t)nid << 32) | (unsigned long long)cell;  // warp-local match key
         }
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_cycle(SmallArgs a) {
         const bool win = clear && (int)(__ffs(peers) - 1) == lane;
         const unsigned wm = __ballot_sync(0xffffffffu, win);
         if (win) {
-          atomicOr(grid32 + ((unsigned long long)(uint32_t)d.y << 4) + (cell >> 5), 1u << (cell & 31));
+          atomicOr(grid32 + ((unsigned long long)((uint32_t)d.y & a.geo.gmask) << 4) + (cell >> 5), 1u << (cell & 31));
           const long long pos = nv + __popc(wm & lanemask_lt());
           if (pos < a.vox_cap) a.backlog[pos] = make_uint4((uint32_t)nid, (uint32_t)cell, rgba, (uint32_t)j);
         }

@@ -36,6 +36,20 @@ inline bool lod_debug() {
   return v == 1;
 }
 
+// Bytes of the stream-ordered pool kept backed per device (the warm-up
+// reserve); freed scratch beyond it goes back to the driver when a tree is
+// destroyed or an allocation fails (cudaMemPoolTrimTo), so the pool never
+// hoards memory that plain cudaMalloc (arenas) or another tree needs.
+static unsigned long long g_pool_keep[64];
+static void trim_pool(int dev, bool all) {
+  cudaMemPool_t pool;
+  if (dev >= 0 && dev < 64 && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(pool, all ? 0 : (size_t)g_pool_keep[dev]);
+  }
+  cudaGetLastError();
+}
+
 template <typename T>
 struct DBuf {
   T *p = nullptr;
@@ -55,9 +69,15 @@ struct DBuf {
     T *q = nullptr;
     // stream-ordered: growth never synchronizes the device
     cudaError_t e = cudaMallocAsync(&q, (size_t)nc * sizeof(T), st);
-    if (e != cudaSuccess) {
+    if (e != cudaSuccess) {  // give the pool's unused memory back and retry once
       cudaGetLastError();
-      return LOD_E_NOMEM;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      trim_pool(dev, true);
+      if (cudaMallocAsync(&q, (size_t)nc * sizeof(T), st) != cudaSuccess) {
+        cudaGetLastError();
+        return LOD_E_NOMEM;
+      }
     }
     if (p) {
       if (keep > 0) cudaMemcpyAsync(q, p, (size_t)std::min(keep, cap) * sizeof(T), cudaMemcpyDeviceToDevice, st);
@@ -642,7 +662,8 @@ static void fill_stats(LodTree *t, LodBatchStats *s) {
 // After a fatal error: drop per-cycle marks and the claim table so the
 // structure stays walkable (the reference leaves partial state, errors.py:1-5).
 static int abort_cycle(LodTree *t, int code) {
-  lod::launch(k_clear_marks_all, grid_for(t->num_nodes), 256, 0, t->st, t->nd, t->srank.p, t->num_nodes);
+  lod::launch(k_clear_marks_all, grid_for(t->num_nodes), 256, 0, t->st, t->nd, t->srank.p, t->num_nodes,
+              t->geo.fresh);
   if (t->hslots.p) {
     cudaMemsetAsync(t->hslots.p, 0xFF, (size_t)t->hslots.cap * sizeof(HSlot), t->st);
     if (t->wcount.p) cudaMemsetAsync(t->wcount.p, 0, (size_t)t->wcount.cap * 4, t->st);
@@ -917,6 +938,7 @@ int lod_tree_create(const LodParams *params, LodTree **out) {
         if (want && cudaMallocAsync(&q, want, t->st) == cudaSuccess) {
           cudaFreeAsync(q, t->st);
           cudaStreamSynchronize(t->st);
+          g_pool_keep[t->dev] = want;
         }
         if (lod_debug())
           fprintf(stderr, "[lod] pool reserve %.1f GiB in %.1f ms\n", want / 1073741824.0,
@@ -943,11 +965,17 @@ int lod_tree_create(const LodParams *params, LodTree **out) {
   g.T = p.leaf_threshold;
   g.max_depth = (int)p.max_depth;
   g.C = p.chunk_capacity;
+  g.fresh = p.arena_bytes < (1ull << 37) ? 1 : 0;  // grid offsets / 64 below 2^31 leave bit 31 free
+  g.gmask = g.fresh ? 0x7fffffffu : 0xffffffffu;
   t->arena_cap = (p.arena_bytes + 15ull) / 16ull * 16ull;  // store.py:41-42
   if (cudaMalloc(&t->arena, t->arena_cap) != cudaSuccess) {
     cudaGetLastError();
-    delete t;
-    return LOD_E_NOMEM;
+    trim_pool(t->dev, true);
+    if (cudaMalloc(&t->arena, t->arena_cap) != cudaSuccess) {
+      cudaGetLastError();
+      delete t;
+      return LOD_E_NOMEM;
+    }
   }
   CK(cudaMemsetAsync(t->arena, 0, t->arena_cap, t->st));
   RK(ensure_nodes(t, 1024, 0));
@@ -1034,7 +1062,9 @@ int lod_tree_destroy(LodTree *t) {
   if (t->cst) cudaStreamDestroy(t->cst);
   for (auto &e : t->ev) if (e) cudaEventDestroy(e);
   cudaStreamDestroy(t->st);
+  const int dev = t->dev;
   delete t;
+  trim_pool(dev, false);
   return LOD_OK;
 }
 
@@ -1407,8 +1437,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     mark(5);
     // ---- cleanup (update.py:375-380)
     lod::launch(k_epilogue, grid_for(Kb * 32), 256, 0, st, t->nd, t->pool, t->seg_node.p, t->seg_start.p, t->plan.p,
-                t->plan_ex.p, t->d_ctrl, t->ghist.p,
-                guard);
+                t->plan_ex.p, t->d_ctrl, t->ghist.p, guard, t->geo.fresh);
     return LOD_OK;
   };
   // speculate on "this iteration settles the expansion" from the second

@@ -38,3 +38,23 @@ def gpu():
 
 # the staged reference suite runs in its own pytest process (test_ref_suite.py)
 collect_ignore_glob = ["ref_suite/*"]
+
+
+@pytest.fixture(autouse=True)
+def _release_device_memory(request):
+    """After each GPU test, collect unreachable trees (facade objects can sit
+    in reference cycles until the cyclic GC runs) so their arenas and node
+    tables go back before the next test allocates its own."""
+    yield
+    if request.node.get_closest_marker("gpu") is None:
+        return
+    import gc
+
+    gc.collect()
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            torch.cuda.empty_cache()
+    except Exception:
+        pass

@@ -1276,7 +1276,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     {
       long long oldg = t->ghist.cap, oldn = t->nodecnt.cap;
       RK(t->ghist.ensure(kMaxPasses * kRadixDigits, st));
-      RK(t->nodecnt.ensure(num_nodes, st, oldn));
+      RK(t->nodecnt.ensure(std::max<long long>(num_nodes, t->ncap), st, oldn));
       // zero once when (re)allocated; afterwards k_seg_list / k_epilogue leave them zeroed
       if (t->ghist.cap > oldg) CK(cudaMemsetAsync(t->ghist.p, 0, (size_t)t->ghist.cap * 4, st));
       if (t->nodecnt.cap > oldn) CK(cudaMemsetAsync(t->nodecnt.p + oldn, 0, (size_t)(t->nodecnt.cap - oldn) * 4, st));
@@ -1341,15 +1341,18 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     // ---- sort: every new sample by node id, stable (slot order)
     // allocation scratch (segments, chunk needs, write lists, pool rows)
     const long long Kb = num_nodes + 1;  // bound on touched nodes
-    RK(t->seg_node.ensure(Kb, st));
-    RK(t->seg_start.ensure(Kb + 1, st));
-    RK(t->dense.ensure(Kb, st));
-    RK(t->plan.ensure(Kb, st));
-    RK(t->plan_ex.ensure(Kb, st));
-    RK(ensure_scan_lb<U64x2>(t->lb64, Kb, st));
+    // per-node scratch follows the node table's capacity (grows with it, not
+    // with every new node-count high-water mark inside an update)
+    const long long Kc = std::max<long long>(Kb, t->ncap + 1);
+    RK(t->seg_node.ensure(Kc, st));
+    RK(t->seg_start.ensure(Kc + 1, st));
+    RK(t->dense.ensure(Kc, st));
+    RK(t->plan.ensure(Kc, st));
+    RK(t->plan_ex.ensure(Kc, st));
+    RK(ensure_scan_lb<U64x2>(t->lb64, Kc, st));
     const long long acq_bound = n_items / C + Kb + 1;
     RK(t->wlo.ensure(acq_bound + Kb + 1, st));
-    RK(t->sinfo.ensure(Kb, st));
+    RK(t->sinfo.ensure(Kc, st));
     const long long alloc0 = t->h_ctrl->allocated_total;
     RK(ensure_chunks(t, alloc0 + acq_bound + 1, alloc0));
     RK(ensure_dir(t, alloc0 + acq_bound + 1, Kb));
@@ -1378,7 +1381,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       lod::launch(k_radix_prep, grid, kRadixBlock, (size_t)nc_words * 4, st, node_of, n_all, t->backlog.p, nc_words,
                   t->keys.p, t->nodecnt.p, t->hist.p, lbw, &t->d_ctrl->n_used, n_items_dev, guard);
     }
-    RK(t->pairs.ensure(Kb, st));
+    RK(t->pairs.ensure(Kc, st));
     lod::launch(k_radix_ghist<NodePlanOf>, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p,
                 num_nodes, passes, t->ghist.p, t->pairs.p, NodePlanOf{t->nd, t->geo}, guard);
     // ---- allocation (update.py:317-331): touched nodes = nodes with new samples, ascending id.

@@ -489,7 +489,8 @@ constexpr int kDecideBlock = 1024;
 __global__ void __launch_bounds__(kDecideBlock)
     k_decide(NodeCols nd, Geo geo, uint32_t *bitmap, int32_t *split_list, int32_t *srank, long long *scnt,
              long long *schk, long long *spill_off, long long *chunk_off, Ctrl *ctrl, long long spill_cap,
-             unsigned long long arena_cap, long long backlog_cap) { lod::pdl_wait();
+             unsigned long long arena_cap, long long backlog_cap, Ctrl *host, volatile unsigned *host_seq,
+             unsigned seq) { lod::pdl_wait();
   __shared__ uint32_t sh32[kDecideBlock / 32 + 1];
   __shared__ U64x2 sh64[kDecideBlock / 32 + 1];
   __shared__ unsigned int s_maxlvl;
@@ -591,6 +592,20 @@ __global__ void __launch_bounds__(kDecideBlock)
     }
   }
   if (tid == 0) ctrl->n_touched = 0;  // phase 6: the touched list restarts next iteration
+  // phase 7 (host != null): the decision goes straight to the host's mapped
+  // copy of the control block (k_publish's job, without its launch)
+  if (host) {
+    __syncthreads();
+    if (tid < 32) {
+      constexpr int kWords = (int)(sizeof(Ctrl) / 8);
+      const unsigned long long *src = reinterpret_cast<const unsigned long long *>(ctrl);
+      volatile unsigned long long *dst = reinterpret_cast<volatile unsigned long long *>(host);
+      for (int k = tid; k < kWords; k += 32) dst[k] = __ldcg(src + k);
+      __threadfence_system();
+      __syncwarp();
+      if (tid == 0) *host_seq = seq;
+    }
+  }
 }
 
 // Octree.split, part 1 (octree.py:231-237, store.py:125-143): the chunks of

@@ -1482,9 +1482,15 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     const bool speculate = may_speculate && (iters >= 2 || t->last_iters == 1);
     const long long nv_bound = iters >= 2 ? std::min<long long>((long long)t->hcap, spec_used + spec_redesc)
                                           : (long long)t->hcap;
+    // without a speculative pipeline behind it the host reads this decision
+    // next: k_decide publishes it itself (no k_publish launch on the path)
+    const bool fused_pub = !speculate && mapped_sync(t);
+    const unsigned dec_seq = fused_pub ? ++t->seq : 0u;
+    if (fused_pub) t->d2h_bytes += (long long)sizeof(Ctrl);
     lod::launch(k_decide, 1, kDecideBlock, 0, st, t->nd, t->geo, t->bitmap.p, t->split_list.p, t->srank.p,
                 t->scnt.p, t->schk.p, t->spill_off.p, t->chunk_off.p, t->d_ctrl, spill_cap, t->arena_cap,
-                std::min<long long>(backlog_cap, nv_bound));
+                std::min<long long>(backlog_cap, nv_bound), fused_pub ? t->h_ctrl_dev : (Ctrl *)nullptr,
+                fused_pub ? (volatile unsigned *)t->h_seq_dev : (volatile unsigned *)nullptr, dec_seq);
     if (speculate) {
       if (first) RK(issue_pending(t));  // queued batches' copies overlap the speculative pipeline
       RK(pipeline(&t->d_ctrl->spec_abort, nv_bound));
@@ -1492,8 +1498,15 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       pipeline_launched = true;
     }
     tp("pre_sync");
-    if (pipeline_launched && early) RK(wait_ctrl(t, mid_seq));
-    else RK(sync_ctrl(t, first && !speculate));  // queued batches' copies start behind the publication
+    if (pipeline_launched && early) {
+      RK(wait_ctrl(t, mid_seq));
+    } else if (fused_pub) {
+      if (first) RK(issue_pending(t));  // queued batches' copies start behind the publication
+      RK(wait_ctrl(t, dec_seq));
+      t->ub_dir = (long long)t->h_ctrl->dir_top;  // as sync_ctrl: published behind all queued work
+    } else {
+      RK(sync_ctrl(t, first && !speculate));  // queued batches' copies start behind the publication
+    }
     tp("sync");
     if (prof) {
       float x = 0.f;

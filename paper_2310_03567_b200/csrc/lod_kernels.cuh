@@ -76,6 +76,9 @@ struct Ctrl {
   unsigned long long dir_top;  // chunk directory entries handed out (bump pointer)
   unsigned long long dir_overflow;  // a relocation found no room: directories are stale until the host
                                     // rebuilds them (fix_directory; chains stay authoritative)
+  int exec_go;  // k_decide: the iteration splits and its nodes / spill fit the buffers as allocated
+                // (k_exec_chunks / k_exec_nodes launched ahead of the host's read run)
+  int pad3;
 };
 static_assert(offsetof(Ctrl, dir_overflow) == offsetof(Ctrl, dir_top) + 8, "dir_claim flags dir_top + 1");
 
@@ -490,7 +493,7 @@ __global__ void __launch_bounds__(kDecideBlock)
     k_decide(NodeCols nd, Geo geo, uint32_t *bitmap, int32_t *split_list, int32_t *srank, long long *scnt,
              long long *schk, long long *spill_off, long long *chunk_off, Ctrl *ctrl, long long spill_cap,
              unsigned long long arena_cap, long long backlog_cap, Ctrl *host, volatile unsigned *host_seq,
-             unsigned seq) { lod::pdl_wait();
+             unsigned seq, long long spill_buf_cap, long long node_cap) { lod::pdl_wait();
   __shared__ uint32_t sh32[kDecideBlock / 32 + 1];
   __shared__ U64x2 sh64[kDecideBlock / 32 + 1];
   __shared__ unsigned int s_maxlvl;
@@ -581,6 +584,8 @@ __global__ void __launch_bounds__(kDecideBlock)
     ctrl->spec_abort = (ctrl->error != 0 || ns > 0 || ctrl->hash_overflow != 0 ||
                         (long long)ctrl->n_used > backlog_cap) ? 1 : 0;
     ctrl->n_xchunks = 0;
+    ctrl->exec_go = (ctrl->error == 0 && ns > 0 && spill0 + (long long)carry.a <= spill_buf_cap &&
+                     nn + 8ll * ns <= node_cap) ? 1 : 0;
     if (ctrl->error == 0 && ns > 0) {
       ctrl->num_nodes = nn + 8ll * ns;
       ctrl->splits_total += ns;
@@ -619,6 +624,11 @@ __global__ void k_exec_chunks(NodeCols nd, PoolCols pool, Geo geo, const uint8_t
                               const long long *__restrict__ spill_off, const long long *__restrict__ chunk_off,
                               long long nchunks, float4 *spill_buf, int32_t *spill_node_of, const Ctrl *ctrl) {
   lod::pdl_wait();
+  if (nchunks < 0) {  // launched ahead of the host's read of the decision (k_exec_nodes)
+    if (!ctrl->exec_go) return;
+    ns = ctrl->n_splits;
+    nchunks = ctrl->free_count - ctrl->plan_free0;
+  }
   const long long warp = gtid() >> 5, nwarps = gstride() >> 5;
   const int lane = threadIdx.x & 31;
   for (long long q = warp; q < nchunks; q += nwarps) {
@@ -652,8 +662,14 @@ __global__ void k_exec_chunks(NodeCols nd, PoolCols pool, Geo geo, const uint8_t
 // Octree.split, part 2 (octree.py:238-264): the node turns inner with a zeroed
 // grid (arena regions are zeroed and never reused) and gets 8 children in
 // octant order with bmin = base + half (f64).  One thread per (split, octant).
+// ns < 0: launched ahead of the host's read of the decision -- the count is
+// the device's, and nothing runs unless k_decide set exec_go.
 __global__ void k_exec_nodes(NodeCols nd, Geo geo, const int32_t *__restrict__ split_list, int32_t *srank,
                              long long ns, const Ctrl *ctrl) { lod::pdl_wait();
+  if (ns < 0) {
+    if (!ctrl->exec_go) return;
+    ns = ctrl->n_splits;
+  }
   for (long long t = gtid(); t < ns * 8; t += gstride()) {
     const long long k = t >> 3;
     const int o = (int)(t & 7);

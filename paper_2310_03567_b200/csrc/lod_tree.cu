@@ -1487,10 +1487,22 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     const bool fused_pub = !speculate && mapped_sync(t);
     const unsigned dec_seq = fused_pub ? ++t->seq : 0u;
     if (fused_pub) t->d2h_bytes += (long long)sizeof(Ctrl);
+    // ... and the split's execution is launched behind it before the host
+    // has read it: it runs iff the decision splits and its children and spill
+    // fit the buffers as allocated (Ctrl.exec_go; else the host launches it)
+    const bool spec_exec = fused_pub && !prof;
+    const long long spill_buf = spec_exec ? std::min<long long>(t->spill.cap, t->node_all.cap) : -1;
     lod::launch(k_decide, 1, kDecideBlock, 0, st, t->nd, t->geo, t->bitmap.p, t->split_list.p, t->srank.p,
                 t->scnt.p, t->schk.p, t->spill_off.p, t->chunk_off.p, t->d_ctrl, spill_cap, t->arena_cap,
                 std::min<long long>(backlog_cap, nv_bound), fused_pub ? t->h_ctrl_dev : (Ctrl *)nullptr,
-                fused_pub ? (volatile unsigned *)t->h_seq_dev : (volatile unsigned *)nullptr, dec_seq);
+                fused_pub ? (volatile unsigned *)t->h_seq_dev : (volatile unsigned *)nullptr, dec_seq, spill_buf,
+                spec_exec ? t->ncap : -1LL);
+    if (spec_exec) {
+      lod::launch(k_exec_chunks, 148u * 4u, 256, 0, st, t->nd, t->pool, t->geo, t->arena, t->split_list.p, -1LL,
+                  t->spill_off.p, t->chunk_off.p, -1LL, t->spill.p, t->node_all.p, t->d_ctrl);
+      lod::launch(k_exec_nodes, 148u * 2u, 256, 0, st, t->nd, t->geo, t->split_list.p, t->srank.p, -1LL,
+                  t->d_ctrl);
+    }
     if (speculate) {
       if (first) RK(issue_pending(t));  // queued batches' copies overlap the speculative pipeline
       RK(pipeline(&t->d_ctrl->spec_abort, nv_bound));
@@ -1526,6 +1538,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       CK(cudaMemcpyAsync(t->dsplits.p + t->d_nsplits, t->split_list.p, (size_t)ns * 4, cudaMemcpyDeviceToDevice, st));
       t->d_nsplits += ns;
     }
+    const bool exec_ran = spec_exec && h.exec_go;  // (then no buffer below grows)
     // capacity for the new children and the spill segment
     RK(ensure_nodes(t, h.num_nodes, h.plan_num_nodes0));
     tp("nodes_ok");
@@ -1535,12 +1548,14 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       RK(t->node_all.ensure(h.spill_total, st));
       tp("spill_ok");
       const long long xchunks = h.free_count - h.plan_free0;  // chunks of the splitting nodes
-      lod::launch(k_exec_chunks, grid_for(xchunks * 32), 256, 0, st, t->nd, t->pool, t->geo, t->arena,
-                  t->split_list.p, ns, t->spill_off.p, t->chunk_off.p, xchunks, t->spill.p, t->node_all.p,
-                  t->d_ctrl);
+      if (!exec_ran)
+        lod::launch(k_exec_chunks, grid_for(xchunks * 32), 256, 0, st, t->nd, t->pool, t->geo, t->arena,
+                    t->split_list.p, ns, t->spill_off.p, t->chunk_off.p, xchunks, t->spill.p, t->node_all.p,
+                    t->d_ctrl);
     }
-    lod::launch(k_exec_nodes, grid_for(8 * ns), 256, 0, st, t->nd, t->geo, t->split_list.p, t->srank.p, ns,
-                                                   t->d_ctrl);
+    if (!exec_ran)
+      lod::launch(k_exec_nodes, grid_for(8 * ns), 256, 0, st, t->nd, t->geo, t->split_list.p, t->srank.p, ns,
+                  t->d_ctrl);
     t->num_nodes = h.num_nodes;
     tp("exec_launched");
     if (first) {

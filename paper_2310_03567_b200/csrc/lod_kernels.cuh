@@ -25,6 +25,12 @@
 
 namespace lod {
 
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // NodeCols::desc .y bit 31 (Geo::fresh, arenas < 128 GiB, where grid
 // offsets / 64 stay below 2^31): the node split in the running cycle, its
 // grid is still all clear.
@@ -79,6 +85,9 @@ struct Ctrl {
   int exec_go;  // k_decide: the iteration splits and its nodes / spill fit the buffers as allocated
                 // (k_exec_chunks / k_exec_nodes launched ahead of the host's read run)
   int pad3;
+  // device time of a cycle (globaltimer ns): k_cycle_begin stamps the start
+  // (and keeps the previous cycle's pair), every k_epilogue block the end
+  unsigned long long t_begin, t_end, t_prev_begin, t_prev_end;
 };
 static_assert(offsetof(Ctrl, dir_overflow) == offsetof(Ctrl, dir_top) + 8, "dir_claim flags dir_top + 1");
 
@@ -368,7 +377,8 @@ __device__ __forceinline__ void count_pending(const NodeCols &nd, int leaf) {
 
 __global__ void __launch_bounds__(256, LOD_COUNT_MINB)
     k_count(NodeCols nd, Geo geo, PointSrc src, NodeOf node_of, long long n, int first,
-            const uint32_t *__restrict__ grid32, Hash h, Ctrl *ctrl) { lod::pdl_wait();
+            const uint32_t *__restrict__ grid32, Hash h, Ctrl *ctrl, float4 *__restrict__ copy_out) {
+  lod::pdl_wait();
   __shared__ UsedStage stg;
   used_init(stg);
   for (long long j0 = (long long)blockIdx.x * blockDim.x; j0 < n; j0 += gstride()) {
@@ -377,6 +387,10 @@ __global__ void __launch_bounds__(256, LOD_COUNT_MINB)
     if (j < n) {
       int nid = first ? 0 : node_of[j];
       int2 d = __ldg(nd.desc + nid);  // {first child | -1, grid offset / 64}
+      // copy_out (iteration 1 of a device batch): the batch as packed records,
+      // which every later pass reads, so the caller's arrays are released
+      // after this pass instead of after the cycle
+      if (copy_out) __stcg(copy_out + j, src.record(j));
       if (d.x >= 0) {
         float xf, yf, zf;
         src.xyz(j, xf, yf, zf);
@@ -1121,6 +1135,8 @@ __global__ void k_epilogue(NodeCols nd, PoolCols pool, const int32_t *__restrict
     const long long A0 = (long long)plan_ex[d].a;
     for (long long t = lane; t < need; t += 32) pool.cdir[off + cc0 + t] = acq_cid(pool, ctrl, A0 + t);
   }
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&ctrl->t_end, gtimer_ns());  // the cycle's device end
 }
 
 // ---------------------------------------------------------------- BatchDelta

@@ -129,6 +129,10 @@ __global__ void k_init_root(NodeCols nd, double b0, double b1, double b2) { lod:
 }
 
 __global__ void k_cycle_begin(Ctrl *c) { lod::pdl_wait();
+  c->t_prev_begin = c->t_begin;
+  c->t_prev_end = c->t_end;
+  c->t_begin = gtimer_ns();
+  c->t_end = 0;
   c->n_touched = 0;
   c->n_splits = 0;
   c->error = 0;
@@ -220,6 +224,8 @@ struct LodTree {
   // inputs / outputs
   DBuf<float> in_xyz;
   DBuf<float4> in_rec;  // packed host input (LOD_FLAG_PACKED)
+  DBuf<float4> dcopy;   // device batch as packed records (released early, k_count copy_out)
+  cudaEvent_t ev_release = nullptr;
   DBuf<uint32_t> in_rgba;
   DBuf<float4> gbuf;
   DBuf<int32_t> gnodes;
@@ -257,6 +263,7 @@ struct LodTree {
                             // (inputs resident, settled) pairs, alternating between calls
   int ev_slot = 0;          // pair of the last call
   bool tail_pending = false;  // the last call returned before its sort + store finished
+  bool tail_ev = false;       // ... and is timed by its event pair (else by the Ctrl stamps)
   DBuf<int32_t> cdir;  // chunk directory entries (pool.cdir)
   // host copies of counters (authoritative after every call)
   long long num_nodes = 1;
@@ -646,6 +653,10 @@ static int issue_pending(LodTree *t, const LodTree::Stage *upto) {
     RK(issue_stage(t, *old));
     if (!upto || old == upto || !upto->pending) return LOD_OK;
   }
+}
+
+static float stamp_ms(unsigned long long b, unsigned long long e) {
+  return e > b ? (float)((double)(e - b) * 1e-6) : -1.f;
 }
 
 static void fill_stats(LodTree *t, LodBatchStats *s) {
@@ -1043,7 +1054,7 @@ int lod_tree_destroy(LodTree *t) {
   t->dense.release();
   t->seg_node.release(); t->pairs.release(); t->wlo.release(); t->sinfo.release(); t->seg_start.release();
   t->plan.release(); t->plan_ex.release(); t->in_xyz.release();
-  t->in_rgba.release(); t->in_rec.release(); t->gbuf.release(); t->gnodes.release(); t->goff.release(); t->gstart.release();
+  t->in_rgba.release(); t->in_rec.release(); t->dcopy.release(); t->gbuf.release(); t->gnodes.release(); t->goff.release(); t->gstart.release();
   t->woff.release(); t->vislist.release(); t->fb.release(); t->counter.release();
   release_scan_lb(t->lb32);
   release_scan_lb(t->lb64);
@@ -1052,6 +1063,7 @@ int lod_tree_destroy(LodTree *t) {
   if (t->cst) cudaStreamSynchronize(t->cst);
   if (t->ev_counted) cudaEventDestroy(t->ev_counted);
   if (t->ev_aux) cudaEventDestroy(t->ev_aux);
+  if (t->ev_release) cudaEventDestroy(t->ev_release);
   if (t->ev_input) cudaEventDestroy(t->ev_input);
   for (auto &sg : t->stage) {
     sg.xyz.release();
@@ -1140,7 +1152,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   }
   // device-time events: this call's pair, the previous call's kept for its
   // report when that call returned before its tail ran
-  const bool prev_pending = t->tail_pending;
+  const bool prev_pending = t->tail_pending, prev_ev = t->tail_ev;
   const int prev_slot = t->ev_slot, es = t->ev_slot ^ 1;
   t->ev_slot = es;
   t->tail_pending = false;
@@ -1175,11 +1187,19 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     tlpos += snprintf(tlbuf + tlpos, sizeof(tlbuf) - tlpos, " %s=%.0f", what, us);
   };
   if ((flags & LOD_FLAG_INPUT_STREAM) && limits) {  // device inputs produced on the caller's stream
-    if (!t->ev_input) CK(cudaEventCreateWithFlags(&t->ev_input, cudaEventDisableTiming));
-    CK(cudaEventRecord(t->ev_input, reinterpret_cast<cudaStream_t>(limits->input_stream)));
-    CK(cudaStreamWaitEvent(st, t->ev_input, 0));
+    // an idle caller stream has nothing to wait for (a cross-stream wait costs
+    // the device ~5 us between calls even when it is already satisfied)
+    const cudaStream_t in = reinterpret_cast<cudaStream_t>(limits->input_stream);
+    const cudaError_t q = cudaStreamQuery(in);
+    if (q != cudaSuccess) {
+      if (q != cudaErrorNotReady) return cuda_rc(q);
+      cudaGetLastError();
+      if (!t->ev_input) CK(cudaEventCreateWithFlags(&t->ev_input, cudaEventDisableTiming));
+      CK(cudaEventRecord(t->ev_input, in));
+      CK(cudaStreamWaitEvent(st, t->ev_input, 0));
+    }
   }
-  CK(cudaEventRecord(t->ev[0], st));
+  if (prof) CK(cudaEventRecord(t->ev[0], st));
   // ---- inputs
   const float *bx = xyz;
   const uint32_t *bc = rgba;
@@ -1218,10 +1238,20 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     bx = t->in_xyz.p;
     bc = t->in_rgba.p;
   }
-  CK(cudaEventRecord(EB, st));  // inputs resident
+  // a device batch (xyz + rgba arrays) with an input stream to release: the
+  // first count pass copies it into packed records (staged count: off)
+  static const int staged_cfg = getenv("LOD_COUNT_STAGED") ? atoi(getenv("LOD_COUNT_STAGED")) : 0;
+  const bool release_early = early && (flags & LOD_FLAG_DEVICE_INPUT) && !brec && !staged_cfg;
+  // events around the cycle only for the phase profile and for handing a
+  // device batch back to its stream at the end (each event between two
+  // kernels breaks the programmatic launch: ~6 us per call); the cycle's
+  // device time comes from the Ctrl stamps otherwise
+  const bool use_ev = prof || (early && (flags & LOD_FLAG_DEVICE_INPUT) && !release_early);
+  if (use_ev) CK(cudaEventRecord(EB, st));  // inputs resident
   lod::launch(k_cycle_begin, 1, 1, 0, st, t->d_ctrl);
   // ---- expansion (update.py:273-296) with the voxel claims folded in
   RK(t->node_b.ensure(n, st));
+  if (release_early) RK(t->dcopy.ensure(n, st));
   PointSrc src{nullptr, 0, bx, bc, n, brec};
   NodeOf node_of{nullptr, t->node_b.p, 0};
   long long n_all = n, n_s = 0;
@@ -1470,7 +1500,17 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
                     t->d_ctrl);
     } else {
       lod::launch(k_count, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, node_of, n_all, first, grid32, hs,
-                  t->d_ctrl);
+                  t->d_ctrl, (first && release_early) ? t->dcopy.p : (float4 *)nullptr);
+    }
+    if (first && release_early) {
+      // the caller's xyz / rgba are no longer read: its stream may go on
+      // (the next call's input handshake then finds it long satisfied)
+      if (!t->ev_release) CK(cudaEventCreateWithFlags(&t->ev_release, cudaEventDisableTiming));
+      CK(cudaEventRecord(t->ev_release, st));
+      CK(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(limits->input_stream), t->ev_release, 0));
+      src.bxyz = nullptr;
+      src.brgba = nullptr;
+      src.brec = t->dcopy.p;
     }
     if (prof) cudaEventRecord(t->ev[13], st);
     lod::launch(k_decide_mark, grid_for(t->num_nodes), 256, 0, st, t->nd, t->geo, (long long)t->num_nodes, t->bitmap.p);
@@ -1506,7 +1546,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     if (speculate) {
       if (first) RK(issue_pending(t));  // queued batches' copies overlap the speculative pipeline
       RK(pipeline(&t->d_ctrl->spec_abort, nv_bound));
-      CK(cudaEventRecord(EE, st));
+      if (use_ev) CK(cudaEventRecord(EE, st));
       pipeline_launched = true;
     }
     tp("pre_sync");
@@ -1624,7 +1664,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     if (h1.hash_overflow) return abort_cycle(t, LOD_E_NOMEM);
     RK(pipeline(nullptr, (long long)h1.n_used));
     mark(6);
-    CK(cudaEventRecord(EE, st));
+    if (use_ev) CK(cudaEventRecord(EE, st));
     tp("all_launched");
     if (early) RK(wait_ctrl(t, mid_seq));
     else RK(sync_ctrl(t));
@@ -1656,21 +1696,28 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   float ms = -1.f;
   if (early) {  // the tail is still running: its time is reported by the next call / lod_tree_wait
     t->tail_pending = true;
+    t->tail_ev = use_ev;
     // the store re-reads the batch: the caller's stream waits for the tail.
     // (Releasing it by an event recorded right after the store instead broke
     // the programmatic dependent launch into the epilogue, +5 us, and the
     // call-to-call gap stayed ~10 us: measured with tools/kineto_gaps.py.)
-    if (flags & LOD_FLAG_DEVICE_INPUT)
+    if ((flags & LOD_FLAG_DEVICE_INPUT) && !release_early)
       CK(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(limits->input_stream), EE, 0));
-  } else {
+  } else if (use_ev) {
     cudaEventElapsedTime(&ms, EB, EE);
+  } else {  // settled: the final publication carries this cycle's stamps
+    ms = stamp_ms(h3.t_begin, h3.t_end);
   }
   S.device_ms = ms;
   S.device_ms_prev = -1.f;
   if (prev_pending) {  // queued before this call's last publication: complete by now
-    cudaEvent_t pb = prev_slot ? t->ev[14] : t->ev[11], pe = prev_slot ? t->ev[15] : t->ev[10];
-    if (cudaEventQuery(pe) == cudaSuccess) cudaEventElapsedTime(&S.device_ms_prev, pb, pe);
-    else cudaGetLastError();
+    if (prev_ev) {
+      cudaEvent_t pb = prev_slot ? t->ev[14] : t->ev[11], pe = prev_slot ? t->ev[15] : t->ev[10];
+      if (cudaEventQuery(pe) == cudaSuccess) cudaEventElapsedTime(&S.device_ms_prev, pb, pe);
+      else cudaGetLastError();
+    } else {  // this cycle's k_cycle_begin kept the previous cycle's stamps
+      S.device_ms_prev = stamp_ms(h3.t_prev_begin, h3.t_prev_end);
+    }
   }
   if (lod_debug())
     fprintf(stderr, "[lod] batch n=%lld n_s=%lld n_v=%lld iters=%d splits=%lld nodes=%lld %.3f ms\n", (long long)n,
@@ -1695,6 +1742,18 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   return LOD_OK;
 }
 
+// Device time of an early-returned cycle whose tail has finished (the stream
+// is idle): its event pair, or the Ctrl stamps (one publication).
+static int tail_ms(LodTree *t, float *ms) {
+  if (t->tail_ev) {
+    cudaEventElapsedTime(ms, t->ev_slot ? t->ev[14] : t->ev[11], t->ev_slot ? t->ev[15] : t->ev[10]);
+    return LOD_OK;
+  }
+  RK(sync_ctrl(t));
+  *ms = stamp_ms(t->h_ctrl->t_begin, t->h_ctrl->t_end);
+  return LOD_OK;
+}
+
 int lod_tree_settle(LodTree *t, LodSettleStats *out) {
   if (!t || !out) return LOD_E_ARG;
   cudaSetDevice(t->dev);
@@ -1703,7 +1762,7 @@ int lod_tree_settle(LodTree *t, LodSettleStats *out) {
   float ms = 0.f;
   if (t->tail_pending) {
     float x = 0.f;
-    cudaEventElapsedTime(&x, t->ev_slot ? t->ev[14] : t->ev[11], t->ev_slot ? t->ev[15] : t->ev[10]);
+    RK(tail_ms(t, &x));
     ms += x;
     t->tail_pending = false;
   }
@@ -1736,7 +1795,7 @@ int lod_tree_wait(LodTree *t, float *last_device_ms) {
   RK(refresh(t));
   float ms = -1.f;
   if (t->tail_pending) {
-    cudaEventElapsedTime(&ms, t->ev_slot ? t->ev[14] : t->ev[11], t->ev_slot ? t->ev[15] : t->ev[10]);
+    RK(tail_ms(t, &ms));
     t->tail_pending = false;
   }
   if (last_device_ms) *last_device_ms = ms;

@@ -1214,7 +1214,14 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     // a copy not issued yet goes behind the work queued so far on the tree
     // stream: an earlier early-returning insert's tail may still read this slot
     if (staged->pending) RK(issue_pending(t, staged));
-    CK(cudaStreamWaitEvent(st, staged->ready, 0));
+    // a copy that has already landed needs no cross-stream wait (which would
+    // also break the programmatic launch into this cycle)
+    const cudaError_t q = cudaEventQuery(staged->ready);
+    if (q != cudaSuccess) {
+      if (q != cudaErrorNotReady) return cuda_rc(q);
+      cudaGetLastError();
+      CK(cudaStreamWaitEvent(st, staged->ready, 0));
+    }
     staged->valid = false;
     if (packed) {
       brec = staged->rec.p;

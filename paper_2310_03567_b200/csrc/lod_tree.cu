@@ -251,6 +251,7 @@ struct LodTree {
     long long n = 0;
     bool valid = false;
     bool pending = false;  // copy requested, not yet issued (issued behind the next count pass)
+    int parts = 0;         // parts not issued yet: 1 = colours, 2 = positions (packed records: 2)
     unsigned long long order = 0;  // prefetch order (copies are issued oldest first)
     cudaEvent_t ready = nullptr;
   } stage[3];
@@ -420,7 +421,7 @@ static bool mapped_sync(const LodTree *t) {
 // then_issue: the queued batches' H2D copies are issued behind the
 // publication (a copy streaming over PCIe slows the publication's
 // system-scope write from ~5 to ~20 us).
-static int issue_pending(LodTree *t, const LodTree::Stage *upto = nullptr);
+static int issue_pending(LodTree *t, const LodTree::Stage *upto = nullptr, int mask = 3);
 static int sync_ctrl(LodTree *t, bool then_issue = false) {
   if (!mapped_sync(t)) {
     if (then_issue) RK(issue_pending(t));
@@ -630,27 +631,32 @@ static void release_scan_lb(ScanLB &lb) {
   lb = ScanLB{};
 }
 
-static int issue_stage(LodTree *t, LodTree::Stage &sg);
+static int issue_stage(LodTree *t, LodTree::Stage &sg, int mask);
+constexpr int kPartSmall = 1, kPartBig = 2, kPartsAll = 3;
 
 // Issue the oldest queued batch's deferred H2D copy behind the work queued so
 // far (through `upto`, when given: every copy up to that slot).  One copy
 // per cycle keeps pace with the inserts and leaves the copy engines idle for
 // part of each cycle -- where the split iteration's publication lands (a
 // copy streaming over PCIe slows that system-scope write from ~5 to ~20 us).
-static int issue_pending(LodTree *t, const LodTree::Stage *upto) {
+// `mask` = the parts to issue: the colours (1/4 of the bytes) go at the
+// start of a cycle, the positions behind the split decision -- so the copy of
+// the next batch is done by the end of this cycle without a DMA under the
+// decision's publication.
+static int issue_pending(LodTree *t, const LodTree::Stage *upto, int mask) {
   if (!t->cst) return LOD_OK;
   bool recorded = false;
   for (;;) {
     LodTree::Stage *old = nullptr;
     for (auto &sg : t->stage)
-      if (sg.valid && sg.pending && (!old || sg.order < old->order)) old = &sg;
+      if (sg.valid && sg.pending && (sg.parts & mask) && (!old || sg.order < old->order)) old = &sg;
     if (!old) return LOD_OK;
     if (!recorded) {
       CK(cudaEventRecord(t->ev_counted, t->st));
       CK(cudaStreamWaitEvent(t->cst, t->ev_counted, 0));
       recorded = true;
     }
-    RK(issue_stage(t, *old));
+    RK(issue_stage(t, *old, upto ? kPartsAll : mask));
     if (!upto || old == upto || !upto->pending) return LOD_OK;
   }
 }
@@ -1255,6 +1261,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   // device time comes from the Ctrl stamps otherwise
   const bool use_ev = prof || (early && (flags & LOD_FLAG_DEVICE_INPUT) && !release_early);
   if (use_ev) CK(cudaEventRecord(EB, st));  // inputs resident
+  RK(issue_pending(t, nullptr, kPartSmall));  // the next batch's colours overlap the first count pass
   lod::launch(k_cycle_begin, 1, 1, 0, st, t->d_ctrl);
   // ---- expansion (update.py:273-296) with the voxel claims folded in
   RK(t->node_b.ensure(n, st));
@@ -2540,19 +2547,24 @@ static int prefetch_impl(LodTree *t, const void *xyz, const uint32_t *rgba, int6
   sg.n = n;
   sg.valid = true;
   sg.pending = true;
+  sg.parts = packed ? kPartBig : kPartsAll;
   sg.order = ++t->stage_order;
   return LOD_OK;
 }
 
-static int issue_stage(LodTree *t, LodTree::Stage &sg) {
+static int issue_stage(LodTree *t, LodTree::Stage &sg, int mask) {
+  const int go = sg.parts & mask;
   if (sg.packed) {
-    CK(cudaMemcpyAsync(sg.rec.p, sg.hx, (size_t)sg.n * 16, cudaMemcpyHostToDevice, t->cst));
+    if (go & kPartBig) CK(cudaMemcpyAsync(sg.rec.p, sg.hx, (size_t)sg.n * 16, cudaMemcpyHostToDevice, t->cst));
   } else {
-    CK(cudaMemcpyAsync(sg.xyz.p, sg.hx, (size_t)sg.n * 12, cudaMemcpyHostToDevice, t->cst));
-    CK(cudaMemcpyAsync(sg.rgba.p, sg.hc, (size_t)sg.n * 4, cudaMemcpyHostToDevice, t->cst));
+    if (go & kPartSmall) CK(cudaMemcpyAsync(sg.rgba.p, sg.hc, (size_t)sg.n * 4, cudaMemcpyHostToDevice, t->cst));
+    if (go & kPartBig) CK(cudaMemcpyAsync(sg.xyz.p, sg.hx, (size_t)sg.n * 12, cudaMemcpyHostToDevice, t->cst));
   }
-  CK(cudaEventRecord(sg.ready, t->cst));
-  sg.pending = false;
+  sg.parts &= ~go;
+  if (sg.parts == 0) {  // the last part: the slot is ready once it lands
+    CK(cudaEventRecord(sg.ready, t->cst));
+    sg.pending = false;
+  }
   return LOD_OK;
 }
 

@@ -17,10 +17,13 @@ T=50,000, C=1,000, G=128, max depth 20); W + K batches = the stream prefix.
   read-backs inside the timed region.
 * ``roofline``: the dominant phase of the update (per-phase CUDA events on the
   tree stream in a profiled replay), algorithmic bytes / time vs measured HBM.
-* ``cpu_baseline``: the C oracle (a 1-thread port of the reference's
-  sequential path) on a bounded prefix of the same stream.
-* ``--impl reference``: the oracle port on the same steps (the reference is
-  Python + numba and single-threaded; the port is the same algorithm in C).
+* ``cpu_baseline``: the reference's own implementation (``lodstream``,
+  numba, single-threaded by design) on a bounded prefix of the same stream --
+  the unmodified package staged by ``__graft_entry__.build()`` under
+  tests/ref_suite/_ref, which travels with the working tree; where it is not
+  staged, the C oracle (a 1-thread port of the same sequential path, slower
+  than numba on terrain: tools/ref_vs_port.py).
+* ``--impl reference``: the same implementation on the same steps.
 
 Multi-GPU (torchrun, N > 1): points are partitioned by octant prefix across
 ranks (paper_2310_03567_b200/partition.py); each rank runs its own subtree
@@ -744,42 +747,69 @@ def load_traffic(kernel: str | None, args):
     return None, f"no committed ncu capture of {args.config} batches {want[0]}..{want[1] - 1}"
 
 
-def cpu_baseline(args, kind) -> dict:
-    """The oracle (1-thread C port of the reference path) on a bounded prefix."""
+REF_STAGED = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "ref_suite", "_ref")
+
+
+def cpu_tree(args):
+    """(insert(x, c), kind) for the CPU legs: the reference package itself
+    (unmodified lodstream, numba) when staged, else the C oracle port."""
+    if os.path.isdir(os.path.join(REF_STAGED, "lodstream")) and not os.environ.get("LOD_BENCH_PORT"):
+        try:
+            if REF_STAGED not in sys.path:
+                sys.path.insert(0, REF_STAGED)
+            from lodstream.octree import CubeBounds as RCube, Octree as ROctree
+            from lodstream.store import Arena as RArena, ChunkPool as RPool
+            from lodstream.update import UpdateConfig as RConfig, UpdateState as RState
+            from lodstream.update import insert_batch as r_insert
+
+            arena = RArena(int(args.arena_gib * (1 << 30)))
+            tree = ROctree(RCube((0.0, 0.0, 0.0), 1.0), arena, RPool(arena, PARAMS["chunk_capacity"]),
+                           grid_res=PARAMS["grid_res"], leaf_threshold=PARAMS["leaf_threshold"],
+                           max_depth=PARAMS["max_depth"])
+            state = RState(RConfig(backlog_capacity=64_000_000))
+            return (lambda x, c: r_insert(tree, x, c, state)), "reference"
+        except ImportError:  # numba missing on this host: the port
+            pass
     import oracle
 
-    n_b = args.cpu_batches
-    batches = gen_batches(kind, n_b)
     t = oracle.OracleTree(grid_res=PARAMS["grid_res"], leaf_threshold=PARAMS["leaf_threshold"],
                           max_depth=PARAMS["max_depth"], chunk_capacity=PARAMS["chunk_capacity"],
                           arena_bytes=int(args.arena_gib * (1 << 30)), backlog_capacity=64_000_000)
+    return t.insert_batch, "port"
+
+
+def cpu_baseline(args, kind) -> dict:
+    """The reference implementation (or its port) on a bounded prefix; the
+    first two batches are untimed (numba compiles its kernels on first use)."""
+    n_b = args.cpu_batches
+    batches = gen_batches(kind, n_b)
+    insert, how = cpu_tree(args)
+    for x, c in batches[:2]:
+        insert(x, c)
     t0 = time.perf_counter()
-    for x, c in batches:
-        t.insert_batch(x, c)
+    for x, c in batches[2:]:
+        insert(x, c)
     dt = time.perf_counter() - t0
-    return {"value": round(n_b * BATCH / dt / 1e6, 3), "unit": "Mpts/s", "cores": 1, "kind": "port",
-            "sample": f"first {n_b} x 1M-point batches of the same stream ({n_b}M points, {dt:.1f} s)",
+    return {"value": round((n_b - 2) * BATCH / dt / 1e6, 3), "unit": "Mpts/s", "cores": 1, "kind": how,
+            "sample": f"batches 2..{n_b - 1} of the same stream ({n_b - 2}M points, {dt:.1f} s) after 2 untimed",
             "host_nproc": os.cpu_count()}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the oracle port (reference algorithm, 1 thread) on the same steps."""
+    """--impl reference: the reference implementation (lodstream itself when
+    staged, else the C port; 1 thread by design) on the same steps."""
     if rank != 0:
         return None
-    import oracle
-
     kind = CONFIGS[args.config][0]
     total = args.warmup + args.steps
     batches = gen_batches(kind, total)
-    t = oracle.OracleTree(grid_res=PARAMS["grid_res"], leaf_threshold=PARAMS["leaf_threshold"],
-                          max_depth=PARAMS["max_depth"], chunk_capacity=PARAMS["chunk_capacity"],
-                          arena_bytes=int(args.arena_gib * (1 << 30)), backlog_capacity=64_000_000)
+    insert, how = cpu_tree(args)
     for i in range(args.warmup):
-        t.insert_batch(*batches[i])
+        insert(*batches[i])
     per = []
     for i in range(args.warmup, total):
         t0 = time.perf_counter()
-        t.insert_batch(*batches[i])
+        insert(*batches[i])
         per.append(time.perf_counter() - t0)
     secs = sum(per)
     value = args.steps * BATCH / secs / 1e6
@@ -788,7 +818,7 @@ def run_reference(args, rank, world):
         "warmup": args.warmup, "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic", "impl": "reference",
         "config": bench_config(args),
-        "cpu_baseline": {"value": round(value, 3), "unit": "Mpts/s", "cores": 1, "kind": "port",
+        "cpu_baseline": {"value": round(value, 3), "unit": "Mpts/s", "cores": 1, "kind": how,
                          "sample": f"{args.steps} timed 1M-point batches after {args.warmup} warm-up batches",
                          "host_nproc": os.cpu_count()},
         "e2e": {"value": round(value, 3), "unit": "Mpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

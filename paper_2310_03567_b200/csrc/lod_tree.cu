@@ -1777,7 +1777,7 @@ int lod_tree_settle(LodTree *t, LodSettleStats *out) {
   if (t->tail_pending) {
     float x = 0.f;
     RK(tail_ms(t, &x));
-    ms += x;
+    if (x > 0.f) ms += x;  // (-1: an aborted cycle left no end stamp)
     t->tail_pending = false;
   }
   if (t->sm_acc && t->sm_unfolded) {

@@ -165,6 +165,7 @@ struct Geo {
   long long C;               // chunk capacity (records)
   int fresh;                 // arena < 128 GiB: desc .y bit 31 marks a grid still all clear (kFresh)
   uint32_t gmask;            // desc .y bits of the grid offset / 64 (0x7fffffff with `fresh`)
+  int f32ok;                 // the count pass may descend in f32 (count_descend<float>; set by the host)
 };
 
 // One point source over the reference's all-array [spill || batch]
@@ -232,6 +233,32 @@ __device__ __forceinline__ int octant_step(double x, double y, double z, double 
   return octant_step(x, y, z, bx, by, bz, s);
 }
 
+// f32 twins of octant_step / cell_of for Geo::f32ok trees: a power-of-two
+// root size and grid_res, a root in the non-negative orthant whose corner lies
+// on the finest plane grid q = size * 2^-max_depth, with (corner + size) / q <=
+// 2^24.  Then every plane bx + h is an f32, every x - bx (x >= bx >= 0) is
+// exact in f32, and g * (x - bx) * 2^k only scales by powers of two: the
+// compares and floors are the f64 ones bit for bit,
+// in half the registers.
+__device__ __forceinline__ int octant_step(float x, float y, float z, float &bx, float &by, float &bz, float &s,
+                                           float &inv_s) {
+  const float h = s * 0.5f;
+  int o = 0;
+  if (x >= bx + h) { o |= 1; bx += h; }
+  if (y >= by + h) { o |= 2; by += h; }
+  if (z >= bz + h) { o |= 4; bz += h; }
+  s = h;
+  inv_s = inv_s * 2.0f;
+  return o;
+}
+__device__ __forceinline__ int clamp_cell(float v, int g) {
+  const float f = floorf(v);
+  if (!(f < 9223372036854775808.0f)) return 0;  // NaN, +inf, >= 2^63 -> INT64_MIN -> 0
+  if (f < 0.0f) return 0;
+  if (f > (float)(g - 1)) return g - 1;
+  return (int)f;
+}
+
 // Clamp of np.int64(np.floor(v)) to [0, g-1] (_kernels.py:107-121) with the
 // x86 conversion semantics: NaN and |v| >= 2^63 become INT64_MIN, i.e. cell 0.
 __device__ __forceinline__ int clamp_cell(double v, int g) {
@@ -259,6 +286,14 @@ __device__ __forceinline__ long long cell_of(const Geo &geo, double x, double y,
     cy = clamp_cell(gd * (y - by) / s, geo.g);
     cz = clamp_cell(gd * (z - bz) / s, geo.g);
   }
+  return (long long)cx + (long long)geo.g * cy + (long long)geo.g * geo.g * cz;
+}
+__device__ __forceinline__ long long cell_of(const Geo &geo, float x, float y, float z, float bx, float by, float bz,
+                                             float s, float inv_s) {
+  const float gf = (float)geo.g;
+  const int cx = clamp_cell(gf * (x - bx) * inv_s, geo.g);
+  const int cy = clamp_cell(gf * (y - by) * inv_s, geo.g);
+  const int cz = clamp_cell(gf * (z - bz) * inv_s, geo.g);
   return (long long)cx + (long long)geo.g * cy + (long long)geo.g * geo.g * cz;
 }
 

@@ -328,15 +328,21 @@ __global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl
 #ifndef LOD_COUNT_MINB
 #define LOD_COUNT_MINB 6  // blocks per SM (40 registers; same-box A/B: 6 > 5 > 4, 8)
 #endif
+#ifndef LOD_COUNT_MINB_F32
+#define LOD_COUNT_MINB_F32 6  // 40 registers, no spills (A/B on terrain: 6 > 8; f64 at 6 is 3 % slower)
+#endif
 
 // One point's descent from inner node `nid` (descent record d) to its leaf,
 // claiming every clear cell it crosses (claimant index v, colour col).
+// T = float on Geo::f32ok trees (the f32 twins in lod_common.cuh: identical
+// results, half the registers of the f64 state -> more resident warps).
+template <typename T>
 __device__ __forceinline__ int count_descend(const NodeCols &nd, const Geo &geo, const uint32_t *__restrict__ grid32,
-                                             const Hash &h, UsedStage &stg, Ctrl *ctrl, int nid, int2 d, double x,
-                                             double y, double z, uint32_t v, uint32_t col) {
-  double bx = nd.bmin[3 * nid], by = nd.bmin[3 * nid + 1], bz = nd.bmin[3 * nid + 2];
+                                             const Hash &h, UsedStage &stg, Ctrl *ctrl, int nid, int2 d, T x, T y,
+                                             T z, uint32_t v, uint32_t col) {
+  T bx = (T)nd.bmin[3 * nid], by = (T)nd.bmin[3 * nid + 1], bz = (T)nd.bmin[3 * nid + 2];
   const int lvl0 = nd.level[nid];
-  double s = geo.size_by_level[lvl0], inv_s = geo.inv_by_level[lvl0];
+  T s = (T)geo.size_by_level[lvl0], inv_s = (T)geo.inv_by_level[lvl0];
   // one dependent load per level, from the compact (L1-resident) descent
   // table; grid words bypass L1 so they do not evict it
   do {
@@ -375,7 +381,8 @@ __device__ __forceinline__ void count_pending(const NodeCols &nd, int leaf) {
   }
 }
 
-__global__ void __launch_bounds__(256, LOD_COUNT_MINB)
+template <typename T>
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? LOD_COUNT_MINB_F32 : LOD_COUNT_MINB)
     k_count(NodeCols nd, Geo geo, PointSrc src, NodeOf node_of, long long n, int first,
             const uint32_t *__restrict__ grid32, Hash h, Ctrl *ctrl, float4 *__restrict__ copy_out) {
   lod::pdl_wait();
@@ -395,7 +402,7 @@ __global__ void __launch_bounds__(256, LOD_COUNT_MINB)
         float xf, yf, zf;
         src.xyz(j, xf, yf, zf);
         const uint32_t v = first ? ((uint32_t)j | kBatchTag) : (uint32_t)j;
-        nid = count_descend(nd, geo, grid32, h, stg, ctrl, nid, d, xf, yf, zf, v, src.rgba(j));
+        nid = count_descend<T>(nd, geo, grid32, h, stg, ctrl, nid, d, (T)xf, (T)yf, (T)zf, v, src.rgba(j));
         node_of[j] = nid;
         if (!nd.final_[nid]) leaf = nid;
       } else if (first) {
@@ -471,7 +478,8 @@ __global__ void __launch_bounds__(kCountTile, LOD_COUNT_MINB)
   int leaf = -1;
   if (j < n) {
     int nid = 0;
-    if (d0.x >= 0) nid = count_descend(nd, geo, grid32, h, stg, ctrl, 0, d0, xf, yf, zf, (uint32_t)j | kBatchTag, col);
+    if (d0.x >= 0)
+      nid = count_descend<double>(nd, geo, grid32, h, stg, ctrl, 0, d0, xf, yf, zf, (uint32_t)j | kBatchTag, col);
     node_of[j] = nid;
     if (!nd.final_[nid]) leaf = nid;
   }

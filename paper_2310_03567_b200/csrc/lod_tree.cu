@@ -983,6 +983,18 @@ int lod_tree_create(const LodParams *params, LodTree **out) {
   g.max_depth = (int)p.max_depth;
   g.C = p.chunk_capacity;
   g.fresh = p.arena_bytes < (1ull << 37) ? 1 : 0;  // grid offsets / 64 below 2^31 leave bit 31 free
+  {
+    // the count pass may descend in f32 (lod_common.cuh, the f32 twins)
+    static const bool no_f32 = getenv("LOD_COUNT_F64") != nullptr;  // A/B switch
+    bool ok = g.pow2 && p.grid_res >= 2 && (p.grid_res & (p.grid_res - 1)) == 0 && p.max_depth >= 0 &&
+              p.max_depth <= 23 && !no_f32;
+    const double q = p.size * std::ldexp(1.0, -(int)p.max_depth);
+    for (int k = 0; k < 3 && ok; ++k) {
+      const double r = p.bmin[k] / q, top = (p.bmin[k] + p.size) / q;
+      ok = p.bmin[k] >= 0.0 && r == std::floor(r) && top <= 16777216.0 && (double)(float)p.bmin[k] == p.bmin[k];
+    }
+    g.f32ok = ok ? 1 : 0;
+  }
   g.gmask = g.fresh ? 0x7fffffffu : 0xffffffffu;
   t->arena_cap = (p.arena_bytes + 15ull) / 16ull * 16ull;  // store.py:41-42
   if (cudaMalloc(&t->arena, t->arena_cap) != cudaSuccess) {
@@ -1513,8 +1525,12 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
         lod::launch(k_count_staged<false>, g, kCountTile, 0, st, t->nd, t->geo, src, node_of, n_all, grid32, hs,
                     t->d_ctrl);
     } else {
-      lod::launch(k_count, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, node_of, n_all, first, grid32, hs,
-                  t->d_ctrl, (first && release_early) ? t->dcopy.p : (float4 *)nullptr);
+      if (t->geo.f32ok)
+        lod::launch(k_count<float>, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, node_of, n_all, first, grid32,
+                    hs, t->d_ctrl, (first && release_early) ? t->dcopy.p : (float4 *)nullptr);
+      else
+        lod::launch(k_count<double>, grid_for(n_all), 256, 0, st, t->nd, t->geo, src, node_of, n_all, first, grid32,
+                    hs, t->d_ctrl, (first && release_early) ? t->dcopy.p : (float4 *)nullptr);
     }
     if (first && release_early) {
       // the caller's xyz / rgba are no longer read: its stream may go on

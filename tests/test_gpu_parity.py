@@ -314,3 +314,36 @@ def test_claim_epoch_wraparound_matches_oracle(gpu):
     assert err == ""
     assert per == oper
     assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label="epoch_wrap")
+
+
+@pytest.mark.parametrize("label,bmin,size", [
+    ("unit", (0.0, 0.0, 0.0), 1.0),               # f32 descent (the bench's trees)
+    ("offset_pow2", (2.0, 0.5, 0.25), 0.5),       # f32 descent, root off the origin
+    ("straddles_zero", (-0.5, -0.5, -0.5), 1.0),  # f64 only: x - bx is not exact in f32 near 0
+])
+def test_f32_descent_matches_oracle(gpu, label, bmin, size):
+    """The count pass descends in f32 when the root, grid and depth make every
+    plane, difference and cell product exact in f32 (Geo::f32ok); the trees
+    must equal the oracle's (f64, the reference's arithmetic) -- including
+    points on cell and split planes, which the f32 compares must place exactly
+    like the f64 ones."""
+    from paper_2310_03567_b200 import synth
+
+    params = dict(bmin=bmin, size=size, arena_bytes=256 << 20, chunk_capacity=64, grid_res=32, leaf_threshold=300,
+                  max_depth=12, backlog_capacity=10_000_000, spill_capacity=100_000_000)
+    rng = np.random.default_rng(7)
+    batches = []
+    for i in range(6):
+        x, c = synth.gen_surface(40_000, 900 + i)
+        x = (np.asarray(x, np.float64) * size + np.asarray(bmin)).astype(np.float32)
+        # a share of the points exactly on the planes of a level-1..6 grid
+        k = rng.integers(1, 7)
+        q = size / (32 * 2 ** k)
+        on = rng.random(len(c)) < 0.2
+        snapped = (np.floor((x.astype(np.float64) - np.asarray(bmin)) / q) * q + np.asarray(bmin)).astype(np.float32)
+        x[on] = snapped[on]
+        batches.append((np.ascontiguousarray(x), c))
+    ot, oerr, oper = run_oracle(params, batches)
+    tree, state, err, per = run_product(params, batches)
+    assert err == oerr == "" and per == oper
+    assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label=label)

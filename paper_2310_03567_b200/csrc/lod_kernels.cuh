@@ -651,33 +651,44 @@ __global__ void k_exec_chunks(NodeCols nd, PoolCols pool, Geo geo, const uint8_t
     ns = ctrl->n_splits;
     nchunks = ctrl->free_count - ctrl->plan_free0;
   }
-  const long long warp = gtid() >> 5, nwarps = gstride() >> 5;
-  const int lane = threadIdx.x & 31;
-  for (long long q = warp; q < nchunks; q += nwarps) {
-    long long lo = 0, hi = ns - 1;  // last split rank whose chunks start at or before q
-    while (lo < hi) {
-      const long long mid = (lo + hi + 1) >> 1;
-      if (chunk_off[mid] <= q) lo = mid;
-      else hi = mid - 1;
+  // one CTA per chunk (a chunk is C records: a warp each left most of the GPU
+  // idle on the few hundred chunks a split moves)
+  __shared__ long long s_r, s_ci, s_sp;
+  __shared__ int s_owner, s_cid, s_occ;
+  for (long long q = blockIdx.x; q < nchunks; q += gridDim.x) {
+    if (threadIdx.x == 0) {
+      long long lo = 0, hi = ns - 1;  // last split rank whose chunks start at or before q
+      while (lo < hi) {
+        const long long mid = (lo + hi + 1) >> 1;
+        if (chunk_off[mid] <= q) lo = mid;
+        else hi = mid - 1;
+      }
+      const long long ci = q - chunk_off[lo];
+      const int owner = split_list[lo];
+      const int cid = pool.cdir[nd.dir_off[owner] + ci];
+      s_r = lo;
+      s_ci = ci;
+      s_owner = owner;
+      s_cid = cid;
+      s_occ = pool.occupied[cid];
+      s_sp = ctrl->plan_spill0 + spill_off[lo] + ci * geo.C;
     }
-    const long long r = lo, ci = q - chunk_off[r];
-    const int owner = split_list[r];
-    const int cid = pool.cdir[nd.dir_off[owner] + ci];
-    const int occ = pool.occupied[cid];
-    const long long sp = ctrl->plan_spill0 + spill_off[r] + ci * geo.C;
+    __syncthreads();
+    const int owner = s_owner, cid = s_cid, occ = s_occ;
+    const long long sp = s_sp;
     const float4 *src = reinterpret_cast<const float4 *>(arena + pool.payload_off[cid]);
-    for (int k = lane; k < occ; k += 32) {
+    for (int k = threadIdx.x; k < occ; k += blockDim.x) {
       spill_buf[sp + k] = src[k];
       spill_node_of[sp + k] = owner;
     }
-    __syncwarp();
-    if (lane == 0) {
-      pool.free_stack[ctrl->plan_free0 + chunk_off[r] + ci] = (int32_t)cid;
+    if (threadIdx.x == 0) {
+      pool.free_stack[ctrl->plan_free0 + chunk_off[s_r] + s_ci] = (int32_t)cid;
       pool.occupied[cid] = 0;
       pool.next[cid] = LOD_NO_CHUNK;
       pool.owner[cid] = -1;
       pool.cidx[cid] = -1;
     }
+    __syncthreads();  // the shared slots are reused by the next chunk
   }
 }
 

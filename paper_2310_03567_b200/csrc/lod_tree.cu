@@ -1568,7 +1568,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
                 fused_pub ? (volatile unsigned *)t->h_seq_dev : (volatile unsigned *)nullptr, dec_seq, spill_buf,
                 spec_exec ? t->ncap : -1LL);
     if (spec_exec) {
-      lod::launch(k_exec_chunks, 148u * 4u, 256, 0, st, t->nd, t->pool, t->geo, t->arena, t->split_list.p, -1LL,
+      lod::launch(k_exec_chunks, 148u * 8u, 256, 0, st, t->nd, t->pool, t->geo, t->arena, t->split_list.p, -1LL,
                   t->spill_off.p, t->chunk_off.p, -1LL, t->spill.p, t->node_all.p, t->d_ctrl);
       lod::launch(k_exec_nodes, 148u * 2u, 256, 0, st, t->nd, t->geo, t->split_list.p, t->srank.p, -1LL,
                   t->d_ctrl);
@@ -1619,7 +1619,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       tp("spill_ok");
       const long long xchunks = h.free_count - h.plan_free0;  // chunks of the splitting nodes
       if (!exec_ran)
-        lod::launch(k_exec_chunks, grid_for(xchunks * 32), 256, 0, st, t->nd, t->pool, t->geo, t->arena,
+        lod::launch(k_exec_chunks, (unsigned)std::min<long long>(std::max<long long>(xchunks, 1), 148LL * 16), 256, 0,
+                    st, t->nd, t->pool, t->geo, t->arena,
                     t->split_list.p, ns, t->spill_off.p, t->chunk_off.p, xchunks, t->spill.p, t->node_all.p,
                     t->d_ctrl);
     }

@@ -84,7 +84,7 @@ struct Ctrl {
                                     // rebuilds them (fix_directory; chains stay authoritative)
   int exec_go;  // k_decide: the iteration splits and its nodes / spill fit the buffers as allocated
                 // (k_exec_chunks / k_exec_nodes launched ahead of the host's read run)
-  int pad3;
+  unsigned int mark_done;  // k_decide: blocks done with the split test (the last one decides)
   // device time of a cycle (globaltimer ns): k_cycle_begin stamps the start
   // (and keeps the previous cycle's pair), every k_epilogue block the end
   unsigned long long t_begin, t_end, t_prev_begin, t_prev_end;
@@ -371,7 +371,7 @@ __device__ __forceinline__ int count_descend(const NodeCols &nd, const Geo &geo,
   return nid;
 }
 
-// The leaf's pending count (fire-and-forget, warp-aggregated): k_decide_mark
+// The leaf's pending count (fire-and-forget, warp-aggregated): k_decide
 // finds the touched leaves by their pending counts.
 __device__ __forceinline__ void count_pending(const NodeCols &nd, int leaf) {
   const unsigned act = __ballot_sync(0xffffffffu, leaf >= 0);
@@ -488,18 +488,26 @@ __global__ void __launch_bounds__(kCountTile, LOD_COUNT_MINB)
 }
 
 // _split_pass (update.py:226-249): split iff count + pending > T and
-// level < max_depth, else mark final.  k_decide_mark tests every leaf touched
+// level < max_depth, else mark final.  k_decide's first phase tests every leaf touched
 // in this iteration -- a leaf, not final, with pending points (pending 0 -> 1
 // is the reference's touched rule, _kernels.py:59-61; every leaf touched in an
 // earlier iteration is final or split by now) -- over all nodes grid-wide
 // (a large tree touches tens of thousands per batch) and flags the
-// splits in a bitmap over node ids; k_decide (1 CTA) ranks them by ascending
+// splits in a bitmap over node ids; the last of its CTAs to finish ranks them by ascending
 // node id (popcount prefix over the bitmap words), so child ids
 // num_nodes + 8*rank match the reference's sorted-id split order
 // (octree.py:249-261), and plans the spill segments (ascending id, stored
 // order), free-stack pushes (walk order) and grid offsets, detecting
 // SpillOverflow / OutOfArena in reference order.
-__global__ void k_decide_mark(NodeCols nd, Geo geo, long long num_nodes, uint32_t *bitmap) { lod::pdl_wait();
+constexpr int kDecideBlock = 1024;
+__global__ void __launch_bounds__(kDecideBlock)
+    k_decide(NodeCols nd, Geo geo, uint32_t *bitmap, int32_t *split_list, int32_t *srank, long long *scnt,
+             long long *schk, long long *spill_off, long long *chunk_off, Ctrl *ctrl, long long spill_cap,
+             unsigned long long arena_cap, long long backlog_cap, Ctrl *host, volatile unsigned *host_seq,
+             unsigned seq, long long spill_buf_cap, long long node_cap, long long num_nodes) { lod::pdl_wait();
+  // phase 1, every block: the split test over a
+  // grid-stride share of the nodes; the last block to finish then ranks and
+  // plans (one launch per decision instead of two)
   for (long long t = gtid(); t < num_nodes; t += gstride()) {
     const int nid = (int)t;
     const unsigned long long pend = nd.pending[nid];
@@ -508,14 +516,17 @@ __global__ void k_decide_mark(NodeCols nd, Geo geo, long long num_nodes, uint32_
     if (tot > geo.T && nd.level[nid] < geo.max_depth) atomicOr(&bitmap[nid >> 5], 1u << (nid & 31));
     else nd.final_[nid] = 1;
   }
-}
-
-constexpr int kDecideBlock = 1024;
-__global__ void __launch_bounds__(kDecideBlock)
-    k_decide(NodeCols nd, Geo geo, uint32_t *bitmap, int32_t *split_list, int32_t *srank, long long *scnt,
-             long long *schk, long long *spill_off, long long *chunk_off, Ctrl *ctrl, long long spill_cap,
-             unsigned long long arena_cap, long long backlog_cap, Ctrl *host, volatile unsigned *host_seq,
-             unsigned seq, long long spill_buf_cap, long long node_cap) { lod::pdl_wait();
+  if (gridDim.x > 1) {
+    __shared__ unsigned s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&ctrl->mark_done, 1u) == gridDim.x - 1 ? 1u : 0u;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) ctrl->mark_done = 0;
+  }
+  __syncthreads();
   __shared__ uint32_t sh32[kDecideBlock / 32 + 1];
   __shared__ U64x2 sh64[kDecideBlock / 32 + 1];
   __shared__ unsigned int s_maxlvl;

@@ -196,7 +196,7 @@ struct LodTree {
   unsigned seq = 0;
   // expansion scratch
   DBuf<int32_t> split_list, node_b, node_all;  // node_b: batch points' node cache; node_all: spilled points'
-  DBuf<uint32_t> bitmap;  // split flags over node ids (k_decide_mark -> k_decide)
+  DBuf<uint32_t> bitmap;  // split flags over node ids (k_decide: the test phase -> the ranking block)
   DBuf<long long> scnt, schk, spill_off, chunk_off;
   DBuf<float4> spill;
   // sampling scratch
@@ -1543,7 +1543,6 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       src.brec = t->dcopy.p;
     }
     if (prof) cudaEventRecord(t->ev[13], st);
-    lod::launch(k_decide_mark, grid_for(t->num_nodes), 256, 0, st, t->nd, t->geo, (long long)t->num_nodes, t->bitmap.p);
     // a speculative pipeline's host-side sizes: nodes as of now (no further
     // split if it runs); new voxels at most the claims so far + one per
     // re-descending point (known after an iteration), else the claim table's
@@ -1562,11 +1561,12 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     // fit the buffers as allocated (Ctrl.exec_go; else the host launches it)
     const bool spec_exec = fused_pub && !prof;
     const long long spill_buf = spec_exec ? std::min<long long>(t->spill.cap, t->node_all.cap) : -1;
-    lod::launch(k_decide, 1, kDecideBlock, 0, st, t->nd, t->geo, t->bitmap.p, t->split_list.p, t->srank.p,
+    lod::launch(k_decide, (unsigned)std::min<long long>(std::max<long long>((t->num_nodes + kDecideBlock - 1) / kDecideBlock, 1), 148LL * 2),
+                kDecideBlock, 0, st, t->nd, t->geo, t->bitmap.p, t->split_list.p, t->srank.p,
                 t->scnt.p, t->schk.p, t->spill_off.p, t->chunk_off.p, t->d_ctrl, spill_cap, t->arena_cap,
                 std::min<long long>(backlog_cap, nv_bound), fused_pub ? t->h_ctrl_dev : (Ctrl *)nullptr,
                 fused_pub ? (volatile unsigned *)t->h_seq_dev : (volatile unsigned *)nullptr, dec_seq, spill_buf,
-                spec_exec ? t->ncap : -1LL);
+                spec_exec ? t->ncap : -1LL, (long long)t->num_nodes);
     if (spec_exec) {
       lod::launch(k_exec_chunks, 148u * 8u, 256, 0, st, t->nd, t->pool, t->geo, t->arena, t->split_list.p, -1LL,
                   t->spill_off.p, t->chunk_off.p, -1LL, t->spill.p, t->node_all.p, t->d_ctrl);

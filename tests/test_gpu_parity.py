@@ -347,3 +347,23 @@ def test_f32_descent_matches_oracle(gpu, label, bmin, size):
     tree, state, err, per = run_product(params, batches)
     assert err == oerr == "" and per == oper
     assert_same_state(product_state(tree), oracle_state(ot), chunk_ids=False, label=label)
+
+
+@pytest.mark.parametrize("switch", ["LOD_SYNC_MEMCPY=1", "LOD_NO_EARLY=1", "LOD_NO_SPEC=1", "LOD_COUNT_STAGED=1",
+                                    "LOD_COUNT_F64=1", "LOD_RESOLVE_LIST_MAX_MB=0", "LOD_NO_SMALL=1"])
+def test_runtime_switches_keep_parity(gpu, switch):
+    """Every runtime switch of DESIGN.md's table selects an alternative with
+    the same results: a child process with the switch set runs oracle-checked
+    cases (the skew and big-batch streams, a device-resident stream)."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    name, value = switch.split("=")
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_parity.py"), "-x", "-q",
+                        "-p", "no:cacheprovider", "-k",
+                        "skew_bs5000 or uniform_big_batches or offset_cube or device_resident"],
+                       env=dict(os.environ, **{name: value}), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout

@@ -30,7 +30,7 @@ constexpr int kRadixWarps = kRadixBlock / 32;
 #define LOD_RADIX_ROUNDS 8  // measured: 8 > 6, 12 > 4 (update bench, same box)
 #endif
 #ifndef LOD_RADIX_MINB
-#define LOD_RADIX_MINB 4
+#define LOD_RADIX_MINB 5  // same-box A/B, driver range: 5 (2385-2392 Mpts/s) > 6 (2376) > 4 (2352-2366) > 3 > 8
 #endif
 constexpr int kRadixRounds = LOD_RADIX_ROUNDS;  // per warp: 8 rounds x 32 lanes (2048-item tile, ~27 KB smem)
 constexpr int kRadixTile = kRadixBlock * kRadixRounds;

@@ -49,6 +49,8 @@ __device__ __forceinline__ long long f2i64(double v) {
   return (long long)0x8000000000000000ULL;
 }
 
+constexpr int kDirTile = 2048;  // direct placement (radix.cuh): items per tile = per warp
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 __device__ __forceinline__ unsigned lanemask_lt() {

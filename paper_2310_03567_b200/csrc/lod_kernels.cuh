@@ -1071,11 +1071,15 @@ struct StoreSink {
   PointSrc src;
   const uint4 *backlog;  // new voxels in backlog order: {node, cell, rgba, winner index}
   const Ctrl *ctrl;
+  // p: the item's position in the node-sorted order (LSD sort)
   __device__ __forceinline__ void operator()(uint32_t p, uint32_t key, uint32_t item) const {
     if (ctrl->error) return;
+    store_rank((long long)p - sinfo[(int)key].seg_start, key, item);
+  }
+  // rank: the item's rank among this cycle's items of its node
+  __device__ __forceinline__ void store_rank(long long rank, uint32_t key, uint32_t item) const {
     const int n = (int)key;
     const SinkInfo si = sinfo[n];
-    const long long rank = (long long)p - si.seg_start;
     const long long cnt = si.cnt;
     const long long slot = cnt + rank;
     const long long rel = slot / geo.C - cnt / geo.C;
@@ -1101,6 +1105,23 @@ struct StoreSink {
     *dst = rec;
   }
 };
+
+// Direct placement (radix.cuh k_rank_prep / k_tile_colscan): every item in
+// input order, rank = its node's items in earlier tiles + its in-tile rank.
+// nowait: as k_onesweep's (launched behind k_publish's early release).
+__global__ void k_store_direct(StoreSink sink, const uint32_t *__restrict__ keys, const uint16_t *__restrict__ rank,
+                               const uint32_t *__restrict__ mat, long long nn,
+                               const long long *__restrict__ n_items_dev, const int *guard, int nowait) {
+  if (!nowait) lod::pdl_wait();
+  if (guard && *guard) return;
+  if (sink.ctrl->error) return;
+  const long long n_items = *n_items_dev;
+  for (long long i = gtid(); i < n_items; i += gstride()) {
+    const uint32_t key = keys[i];
+    const long long t = i / kDirTile;
+    sink.store_rank((long long)mat[t * nn + key] + rank[i], key, (uint32_t)i);
+  }
+}
 
 __global__ void k_store(StoreSink sink, const uint32_t *__restrict__ skeys, const uint32_t *__restrict__ svals,
                         const long long *__restrict__ n_items_dev, const int *guard) { lod::pdl_wait();

@@ -214,6 +214,8 @@ struct LodTree {
   DBuf<uint4> wins;     // burst path: k_resolve_list's win list {winner, node, cell, rgba}
   // sort / alloc scratch
   DBuf<uint32_t> keys, keys_b, vals_a, vals_b, hist, ghist, nodecnt;
+  DBuf<uint32_t> dmat, dlb;  // direct placement: tiles x nodes counts -> prefixes; column-scan look-back
+  DBuf<uint16_t> drank;      // direct placement: in-tile ranks
   DBuf<int32_t> seg_node, dense;
   DBuf<U64x2> pairs;     // packed per-node plans, scanned in place (k_radix_ghist -> k_seg_list)
   DBuf<long long> wlo;   // write list: payload offsets of every touched node's chunks in slot order
@@ -1069,6 +1071,7 @@ int lod_tree_destroy(LodTree *t) {
   t->hused.release(); t->srank.release(); t->wcount.release(); t->wbase.release();
   t->backlog.release(); t->wins.release(); t->keys.release(); t->keys_b.release();
   t->vals_a.release(); t->vals_b.release(); t->hist.release(); t->ghist.release(); t->nodecnt.release();
+  t->dmat.release(); t->dlb.release(); t->drank.release();
   t->dense.release();
   t->seg_node.release(); t->pairs.release(); t->wlo.release(); t->sinfo.release(); t->seg_start.release();
   t->plan.release(); t->plan_ex.release(); t->in_xyz.release();
@@ -1414,7 +1417,39 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     RK(ensure_dir(t, alloc0 + acq_bound + 1, Kb));
     const long long lbw = radix_lb_elems(n_items);
     long long *n_items_dev = &t->d_ctrl->n_items;
-    {
+    // direct placement (radix.cuh) instead of the LSD multisplit when its
+    // tiles x nodes matrix stays small; LOD_STORE_LSD=1 keeps the LSD sort
+    static const bool store_lsd = getenv("LOD_STORE_LSD") != nullptr;
+    static const long long dir_max = getenv("LOD_DIRECT_MAX_ENTRIES") ? atoll(getenv("LOD_DIRECT_MAX_ENTRIES"))
+                                                                      : (8LL << 20);
+    const long long dtiles = (n_items + kDirTile - 1) / kDirTile;
+    const long long nn_pad = (num_nodes + 1) & ~1LL;
+    const bool direct = !delta && !store_lsd && nn_pad * 2 <= 49152 && num_nodes * dtiles <= dir_max &&
+                        n_items < (1LL << 30);
+    const long long drb = (dtiles + kDirRowBlock - 1) / kDirRowBlock;
+    const long long dcb = (num_nodes + kDirScanBlock - 1) / kDirScanBlock;
+    if (direct) {
+      RK(t->dmat.ensure(num_nodes * dtiles, st));
+      RK(t->dlb.ensure(drb * num_nodes + 1, st));
+      RK(t->drank.ensure(n_items, st));
+      // warps per CTA: as many per-warp counter arrays as fit 48 KB
+      const long long wfit = 49152 / (nn_pad * 2);
+      const int W = wfit >= 8 ? 8 : wfit >= 4 ? 4 : wfit >= 2 ? 2 : 1;
+      const unsigned grid = (unsigned)std::max<long long>((dtiles + W - 1) / W, 1);
+      const size_t sm = (size_t)W * nn_pad * 2;
+      const long long lbwd = drb * num_nodes + 1;
+      auto go = [&](auto kern) {
+        lod::launch(kern, grid, 32 * W, sm, st, node_of, n_all, (const uint4 *)t->backlog.p, num_nodes, nn_pad,
+                    t->keys.p, t->drank.p, t->dmat.p, t->dlb.p, lbwd, (const unsigned long long *)&t->d_ctrl->n_used,
+                    n_items_dev, guard);
+      };
+      if (W == 8) go(k_rank_prep<8>);
+      else if (W == 4) go(k_rank_prep<4>);
+      else if (W == 2) go(k_rank_prep<2>);
+      else go(k_rank_prep<1>);
+      lod::launch(k_tile_colscan, (unsigned)std::max<long long>(drb * dcb, 1), kDirScanBlock, 0, st, t->dmat.p,
+                  num_nodes, dcb, drb, (const long long *)n_items_dev, t->dlb.p, t->nodecnt.p, guard);
+    } else {
       // node counts in per-CTA shared memory (16-bit counters) up to
       // kNodeHistSmemMax nodes, as long as no CTA can see 65535 items
       // kNodeHistSmemMax nodes, as long as no CTA can see 65535 items; one
@@ -1436,7 +1471,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       }
       lod::launch(k_radix_prep, grid, kRadixBlock, (size_t)nc_words * 4, st, node_of, n_all, t->backlog.p, nc_words,
                   t->keys.p, t->nodecnt.p, t->hist.p, lbw, &t->d_ctrl->n_used, n_items_dev, guard);
-    }
+    }  // direct / LSD prep
     RK(t->pairs.ensure(Kc, st));
     lod::launch(k_radix_ghist<NodePlanOf>, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p,
                 num_nodes, passes, t->ghist.p, t->pairs.p, NodePlanOf{t->nd, t->geo}, guard);
@@ -1467,7 +1502,11 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     rs.lb[1] = t->hist.p + lbw;
     const StoreSink sink{t->nd, t->pool, t->geo, t->arena, t->sinfo.p, t->wlo.p, n_all, src, t->backlog.p, t->d_ctrl};
     uint32_t *skeys = nullptr, *svals = nullptr;
-    if (delta) {  // the delta reads the sorted order: materialise it, then store
+    if (direct) {
+      lod::launch(k_store_direct, grid_for(n_items), 256, 0, st, sink, (const uint32_t *)t->keys.p,
+                  (const uint16_t *)t->drank.p, (const uint32_t *)t->dmat.p, num_nodes, (const long long *)n_items_dev,
+                  guard, release ? 1 : 0);
+    } else if (delta) {  // the delta reads the sorted order: materialise it, then store
       stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals, nullptr, 0, (const KVSink *)nullptr,
                         n_items_dev, guard);
       lod::launch(k_store, grid_for(n_items), 256, 0, st, sink, skeys, svals, (const long long *)n_items_dev, guard);

@@ -107,6 +107,129 @@ static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
   }
 }
 
+// ---- direct placement (one pass instead of the LSD passes) -------------------
+// The store only needs every item's rank among the earlier items of its node
+// (slot order = all-array / backlog order, _kernels.py:155-250).  Cut the item
+// list into tiles of kDirTile items, one warp per tile: the warp walks its
+// tile in order and ranks each item against the tile's earlier items of the
+// same node (per-warp u16 counters in shared memory, MATCH.ANY per 32 items),
+// then writes the tile's per-node counts as one dense row of a tiles x nodes
+// matrix.  A column scan over that matrix (k_tile_colscan) turns each count
+// into the node's items in earlier tiles; rank = that + the in-tile rank.
+// Chosen when the matrix is small (a few thousand nodes: L2-resident);
+// otherwise the LSD multisplit runs.
+constexpr int kDirRowBlock = 32;    // tiles per row block of the column scan
+constexpr int kDirScanBlock = 256;  // node columns per column-scan CTA
+
+// Keys (node ids), in-tile ranks and the tile's node-count row.  Also zeroes
+// the column scan's look-back words + ticket (lb_words) and publishes the
+// item count like k_radix_prep.  Dynamic smem: W * nn_pad u16 counters.
+template <int W>
+static __global__ void __launch_bounds__(32 * W)
+    k_rank_prep(NodeOf node_of, long long n_all, const uint4 *__restrict__ backlog, long long nn, long long nn_pad,
+                uint32_t *__restrict__ keys, uint16_t *__restrict__ rank, uint32_t *__restrict__ mat,
+                uint32_t *__restrict__ lb, long long lb_words, const unsigned long long *__restrict__ n_v_dev,
+                long long *__restrict__ n_items_out, const int *guard) {
+  lod::pdl_wait();
+  if (guard && *guard) return;
+  extern __shared__ uint16_t dcnt[];
+  const long long n_v = (long long)*n_v_dev;
+  const long long n = n_all + n_v;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_items_out = n;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < lb_words;
+       i += (long long)gridDim.x * blockDim.x)
+    lb[i] = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long tile = (long long)blockIdx.x * W + warp;
+  const long long i0 = tile * kDirTile;
+  if (i0 >= n) return;  // warp-uniform
+  uint16_t *cnt = dcnt + (long long)warp * nn_pad;
+  for (long long k = lane; k < nn; k += 32) cnt[k] = 0;
+  __syncwarp();
+  const unsigned lt = lanemask_lt();
+  constexpr int kAhead = 8;  // rounds of keys loaded ahead
+  for (int r0 = 0; r0 < kDirTile / 32; r0 += kAhead) {
+    if (i0 + (long long)r0 * 32 >= n) break;  // warp-uniform
+    uint32_t key[kAhead];
+#pragma unroll
+    for (int q = 0; q < kAhead; ++q) {
+      const long long i = i0 + (long long)(r0 + q) * 32 + lane;
+      key[q] = 0xFFFFFFFFu;
+      if (i < n) key[q] = (uint32_t)(i < n_all ? node_of[i] : __ldg(&backlog[i - n_all].x));
+    }
+#pragma unroll
+    for (int q = 0; q < kAhead; ++q) {
+      const long long i = i0 + (long long)(r0 + q) * 32 + lane;
+      const bool ok = i < n;
+      const unsigned peers = __match_any_sync(0xffffffffu, key[q]);
+      const uint32_t b = ok ? cnt[key[q]] : 0u;
+      if (ok) {
+        keys[i] = key[q];
+        rank[i] = (uint16_t)(b + __popc(peers & lt));
+      }
+      __syncwarp();
+      if (ok && lane == __ffs(peers) - 1) cnt[key[q]] = (uint16_t)(b + __popc(peers));
+      __syncwarp();
+    }
+  }
+  uint32_t *row = mat + tile * nn;
+  for (long long k = lane; k < nn; k += 32) row[k] = cnt[k];
+}
+
+// Column scan of the tiles x nodes count matrix, in place: entry (t, k)
+// becomes node k's items in tiles < t; the node totals go to nodecnt.  One CTA
+// per (row block of kDirRowBlock tiles, kDirScanBlock node columns), taken in
+// ticket order; row blocks chain per column with a decoupled look-back
+// (status bits as in the onesweep).  lb: rb_cap * nn words + the ticket.
+static __global__ void __launch_bounds__(kDirScanBlock)
+    k_tile_colscan(uint32_t *__restrict__ mat, long long nn, long long ncb, long long rb_cap,
+                   const long long *__restrict__ n_items_dev, uint32_t *lb, uint32_t *__restrict__ nodecnt,
+                   const int *guard) {
+  lod::pdl_wait();
+  if (guard && *guard) return;
+  __shared__ uint32_t s_ticket;
+  if (threadIdx.x == 0) s_ticket = atomicAdd(lb + rb_cap * nn, 1u);
+  __syncthreads();
+  const long long n = *n_items_dev;
+  const long long ntiles = (n + kDirTile - 1) / kDirTile;
+  const long long nrb = (ntiles + kDirRowBlock - 1) / kDirRowBlock;
+  const long long rb = s_ticket / ncb, cb = s_ticket % ncb;
+  if (rb >= nrb) return;
+  const long long k = cb * kDirScanBlock + threadIdx.x;
+  if (k >= nn) return;
+  const long long t0 = rb * kDirRowBlock;
+  const int nt = (int)min((long long)kDirRowBlock, ntiles - t0);
+  uint32_t c[kDirRowBlock];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int q = 0; q < kDirRowBlock; ++q) {
+    c[q] = q < nt ? mat[(t0 + q) * nn + k] : 0u;
+    sum += c[q];
+  }
+  uint32_t *mine = lb + rb * nn + k;
+  uint32_t excl = 0;
+  if (rb == 0) {
+    atomicExch(mine, kLbPre | sum);
+  } else {
+    atomicExch(mine, kLbAgg | sum);
+    for (long long p = rb - 1;;) {
+      const uint32_t v = *((volatile uint32_t *)(lb + p * nn + k));
+      if ((v & ~kLbMask) == 0) continue;  // not published yet
+      excl += v & kLbMask;
+      if ((v & ~kLbMask) == kLbPre) break;
+      --p;
+    }
+    atomicExch(mine, kLbPre | (excl + sum));
+  }
+  if (rb == nrb - 1) nodecnt[k] = excl + sum;
+  uint32_t run = excl;
+#pragma unroll
+  for (int q = 0; q < kDirRowBlock; ++q) {
+    if (q < nt) mat[(t0 + q) * nn + k] = run;
+    run += c[q];
+  }
+}
+
 // Digit totals of every pass from the per-node counts (keys are node ids).
 // Also writes each node's plan record for the segment scan (plan_of(n, count)).
 template <class PlanOf>

@@ -49,7 +49,10 @@ __device__ __forceinline__ long long f2i64(double v) {
   return (long long)0x8000000000000000ULL;
 }
 
-constexpr int kDirTile = 2048;  // direct placement (radix.cuh): items per tile = per warp
+#ifndef LOD_DIR_TILE
+#define LOD_DIR_TILE 2048
+#endif
+constexpr int kDirTile = LOD_DIR_TILE;  // direct placement (radix.cuh): items per tile = per warp
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 

@@ -1433,7 +1433,10 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       RK(t->dlb.ensure(drb * num_nodes + 1, st));
       RK(t->drank.ensure(n_items, st));
       // warps per CTA: as many per-warp counter arrays as fit 48 KB
-      const long long wfit = 49152 / (nn_pad * 2);
+      // (LOD_DIR_W; default one warp per CTA: same-box A/B, driver range,
+      // 1 warp 2596-2603 Mpts/s > 2: 2590-2593 > 4: 2560-2564 > 8: 2534)
+      static const long long wenv = getenv("LOD_DIR_W") ? atoll(getenv("LOD_DIR_W")) : 1;
+      const long long wfit = std::min<long long>(49152 / (nn_pad * 2), std::max<long long>(wenv, 1));
       const int W = wfit >= 8 ? 8 : wfit >= 4 ? 4 : wfit >= 2 ? 2 : 1;
       const unsigned grid = (unsigned)std::max<long long>((dtiles + W - 1) / W, 1);
       const size_t sm = (size_t)W * nn_pad * 2;

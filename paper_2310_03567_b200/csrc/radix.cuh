@@ -212,12 +212,22 @@ static __global__ void __launch_bounds__(kDirScanBlock)
     atomicExch(mine, kLbPre | sum);
   } else {
     atomicExch(mine, kLbAgg | sum);
-    for (long long p = rb - 1;;) {
-      const uint32_t v = *((volatile uint32_t *)(lb + p * nn + k));
-      if ((v & ~kLbMask) == 0) continue;  // not published yet
-      excl += v & kLbMask;
-      if ((v & ~kLbMask) == kLbPre) break;
-      --p;
+    // 4 predecessors per round trip; an unpublished one ends the round
+    long long p = rb - 1;
+    for (bool done = false; !done;) {
+      uint32_t v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = p - q >= 0 ? *((volatile uint32_t *)(lb + (p - q) * nn + k)) : (2u << 30);  // kLbPre
+      int q = 0;
+      for (; q < 4; ++q) {
+        if ((v[q] & ~kLbMask) == 0) break;
+        excl += v[q] & kLbMask;
+        if ((v[q] & ~kLbMask) == kLbPre) {
+          done = true;
+          break;
+        }
+      }
+      p -= q;
     }
     atomicExch(mine, kLbPre | (excl + sum));
   }

@@ -350,7 +350,8 @@ def test_f32_descent_matches_oracle(gpu, label, bmin, size):
 
 
 @pytest.mark.parametrize("switch", ["LOD_SYNC_MEMCPY=1", "LOD_NO_EARLY=1", "LOD_NO_SPEC=1", "LOD_COUNT_STAGED=1",
-                                    "LOD_COUNT_F64=1", "LOD_RESOLVE_LIST_MAX_MB=0", "LOD_NO_SMALL=1"])
+                                    "LOD_COUNT_F64=1", "LOD_RESOLVE_LIST_MAX_MB=0", "LOD_NO_SMALL=1",
+                                    "LOD_STORE_LSD=1", "LOD_DIR_W=8"])
 def test_runtime_switches_keep_parity(gpu, switch):
     """Every runtime switch of DESIGN.md's table selects an alternative with
     the same results: a child process with the switch set runs oracle-checked

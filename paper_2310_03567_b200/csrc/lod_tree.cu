@@ -1450,8 +1450,10 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       else if (W == 4) go(k_rank_prep<4>);
       else if (W == 2) go(k_rank_prep<2>);
       else go(k_rank_prep<1>);
-      lod::launch(k_tile_colscan, (unsigned)std::max<long long>(drb * dcb, 1), kDirScanBlock, 0, st, t->dmat.p,
-                  num_nodes, dcb, drb, (const long long *)n_items_dev, t->dlb.p, t->nodecnt.p, guard);
+      RK(t->pairs.ensure(Kc, st));
+      lod::launch(k_tile_colscan<NodePlanOf>, (unsigned)std::max<long long>(drb * dcb, dcb), kDirScanBlock, 0, st,
+                  t->dmat.p, num_nodes, dcb, drb, (const long long *)n_items_dev, t->dlb.p, t->nodecnt.p, t->pairs.p,
+                  NodePlanOf{t->nd, t->geo}, guard);
     } else {
       // node counts in per-CTA shared memory (16-bit counters) up to
       // kNodeHistSmemMax nodes, as long as no CTA can see 65535 items
@@ -1476,7 +1478,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
                   t->keys.p, t->nodecnt.p, t->hist.p, lbw, &t->d_ctrl->n_used, n_items_dev, guard);
     }  // direct / LSD prep
     RK(t->pairs.ensure(Kc, st));
-    lod::launch(k_radix_ghist<NodePlanOf>, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p,
+    if (!direct)  // (direct: the column scan wrote the plans)
+      lod::launch(k_radix_ghist<NodePlanOf>, std::min<unsigned>(grid_for(num_nodes), 64), 256, 0, st, t->nodecnt.p,
                 num_nodes, passes, t->ghist.p, t->pairs.p, NodePlanOf{t->nd, t->geo}, guard);
     // ---- allocation (update.py:317-331): touched nodes = nodes with new samples, ascending id.
     // It needs only the per-node counts, so it runs before the sort, whose last

@@ -181,10 +181,13 @@ static __global__ void __launch_bounds__(32 * W)
 // per (row block of kDirRowBlock tiles, kDirScanBlock node columns), taken in
 // ticket order; row blocks chain per column with a decoupled look-back
 // (status bits as in the onesweep).  lb: rb_cap * nn words + the ticket.
+// The last row block also writes each node's plan record (k_radix_ghist's
+// other job; the digit totals are not needed here).
+template <class PlanOf>
 static __global__ void __launch_bounds__(kDirScanBlock)
     k_tile_colscan(uint32_t *__restrict__ mat, long long nn, long long ncb, long long rb_cap,
                    const long long *__restrict__ n_items_dev, uint32_t *lb, uint32_t *__restrict__ nodecnt,
-                   const int *guard) {
+                   U64x2 *__restrict__ pairs, PlanOf plan_of, const int *guard) {
   lod::pdl_wait();
   if (guard && *guard) return;
   __shared__ uint32_t s_ticket;
@@ -194,8 +197,15 @@ static __global__ void __launch_bounds__(kDirScanBlock)
   const long long ntiles = (n + kDirTile - 1) / kDirTile;
   const long long nrb = (ntiles + kDirRowBlock - 1) / kDirRowBlock;
   const long long rb = s_ticket / ncb, cb = s_ticket % ncb;
-  if (rb >= nrb) return;
   const long long k = cb * kDirScanBlock + threadIdx.x;
+  if (nrb == 0) {  // no items: zero counts, plans of untouched nodes
+    if (rb == 0 && k < nn) {
+      nodecnt[k] = 0;
+      pairs[k] = plan_of(k, 0u);
+    }
+    return;
+  }
+  if (rb >= nrb) return;
   if (k >= nn) return;
   const long long t0 = rb * kDirRowBlock;
   const int nt = (int)min((long long)kDirRowBlock, ntiles - t0);
@@ -231,7 +241,10 @@ static __global__ void __launch_bounds__(kDirScanBlock)
     }
     atomicExch(mine, kLbPre | (excl + sum));
   }
-  if (rb == nrb - 1) nodecnt[k] = excl + sum;
+  if (rb == nrb - 1) {
+    nodecnt[k] = excl + sum;
+    pairs[k] = plan_of(k, excl + sum);
+  }
   uint32_t run = excl;
 #pragma unroll
   for (int q = 0; q < kDirRowBlock; ++q) {

@@ -1423,13 +1423,13 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     static const long long dir_max = getenv("LOD_DIRECT_MAX_ENTRIES") ? atoll(getenv("LOD_DIRECT_MAX_ENTRIES"))
                                                                       : (8LL << 20);
     const long long dtiles = (n_items + kDirTile - 1) / kDirTile;
-    const long long nn_pad = (num_nodes + 1) & ~1LL;
+    const long long nn_pad = (num_nodes + 7) & ~7LL;  // matrix row stride, per-warp counters
     const bool direct = !delta && !store_lsd && nn_pad * 2 <= 49152 && num_nodes * dtiles <= dir_max &&
                         n_items < (1LL << 30);
     const long long drb = (dtiles + kDirRowBlock - 1) / kDirRowBlock;
     const long long dcb = (num_nodes + kDirScanBlock - 1) / kDirScanBlock;
     if (direct) {
-      RK(t->dmat.ensure(num_nodes * dtiles, st));
+      RK(t->dmat.ensure(nn_pad * dtiles, st));
       RK(t->dlb.ensure(drb * num_nodes + 1, st));
       RK(t->drank.ensure(n_items, st));
       // warps per CTA: as many per-warp counter arrays as fit 48 KB
@@ -1452,7 +1452,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       else go(k_rank_prep<1>);
       RK(t->pairs.ensure(Kc, st));
       lod::launch(k_tile_colscan<NodePlanOf>, (unsigned)std::max<long long>(drb * dcb, dcb), kDirScanBlock, 0, st,
-                  t->dmat.p, num_nodes, dcb, drb, (const long long *)n_items_dev, t->dlb.p, t->nodecnt.p, t->pairs.p,
+                  t->dmat.p, num_nodes, nn_pad, dcb, drb, (const long long *)n_items_dev, t->dlb.p, t->nodecnt.p, t->pairs.p,
                   NodePlanOf{t->nd, t->geo}, guard);
     } else {
       // node counts in per-CTA shared memory (16-bit counters) up to
@@ -1510,7 +1510,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     uint32_t *skeys = nullptr, *svals = nullptr;
     if (direct) {
       lod::launch(k_store_direct, grid_for(n_items), 256, 0, st, sink, (const uint32_t *)t->keys.p,
-                  (const uint16_t *)t->drank.p, (const uint32_t *)t->dmat.p, num_nodes, (const long long *)n_items_dev,
+                  (const uint16_t *)t->drank.p, (const uint32_t *)t->dmat.p, nn_pad, (const long long *)n_items_dev,
                   guard, release ? 1 : 0);
     } else if (delta) {  // the delta reads the sorted order: materialise it, then store
       stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals, nullptr, 0, (const KVSink *)nullptr,

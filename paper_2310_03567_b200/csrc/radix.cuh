@@ -120,6 +120,9 @@ static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
 // otherwise the LSD multisplit runs.
 constexpr int kDirRowBlock = 32;    // tiles per row block of the column scan
 constexpr int kDirScanBlock = 256;  // node columns per column-scan CTA
+#ifndef LOD_COLSCAN_KEEP
+#define LOD_COLSCAN_KEEP 1  // counts kept in registers between the two sweeps (A/B: 2607-2610 vs 2581-2596 re-read)
+#endif
 
 // Keys (node ids), in-tile ranks and the tile's node-count row.  Also zeroes
 // the column scan's look-back words + ticket (lb_words) and publishes the
@@ -132,7 +135,7 @@ static __global__ void __launch_bounds__(32 * W)
                 long long *__restrict__ n_items_out, const int *guard) {
   lod::pdl_wait();
   if (guard && *guard) return;
-  extern __shared__ uint16_t dcnt[];
+  extern __shared__ __align__(16) uint16_t dcnt[];  // nn_pad (a multiple of 8) per warp
   const long long n_v = (long long)*n_v_dev;
   const long long n = n_all + n_v;
   if (blockIdx.x == 0 && threadIdx.x == 0) *n_items_out = n;
@@ -144,7 +147,7 @@ static __global__ void __launch_bounds__(32 * W)
   const long long i0 = tile * kDirTile;
   if (i0 >= n) return;  // warp-uniform
   uint16_t *cnt = dcnt + (long long)warp * nn_pad;
-  for (long long k = lane; k < nn; k += 32) cnt[k] = 0;
+  for (long long k = lane; k < nn_pad / 8; k += 32) reinterpret_cast<uint4 *>(cnt)[k] = make_uint4(0, 0, 0, 0);
   __syncwarp();
   const unsigned lt = lanemask_lt();
   constexpr int kAhead = 8;  // rounds of keys loaded ahead
@@ -172,11 +175,16 @@ static __global__ void __launch_bounds__(32 * W)
       __syncwarp();
     }
   }
-  uint32_t *row = mat + tile * nn;
-  for (long long k = lane; k < nn; k += 32) row[k] = cnt[k];
+  // the dense row (stride nn_pad), 8 counters per lane step
+  uint4 *row = reinterpret_cast<uint4 *>(mat + tile * nn_pad);
+  for (long long k = lane; k < nn_pad / 8; k += 32) {
+    const uint4 v = reinterpret_cast<const uint4 *>(cnt)[k];
+    row[2 * k] = make_uint4(v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16);
+    row[2 * k + 1] = make_uint4(v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16);
+  }
 }
 
-// Column scan of the tiles x nodes count matrix, in place: entry (t, k)
+// Column scan of the tiles x nodes count matrix (row stride ms), in place: entry (t, k)
 // becomes node k's items in tiles < t; the node totals go to nodecnt.  One CTA
 // per (row block of kDirRowBlock tiles, kDirScanBlock node columns), taken in
 // ticket order; row blocks chain per column with a decoupled look-back
@@ -185,7 +193,7 @@ static __global__ void __launch_bounds__(32 * W)
 // other job; the digit totals are not needed here).
 template <class PlanOf>
 static __global__ void __launch_bounds__(kDirScanBlock)
-    k_tile_colscan(uint32_t *__restrict__ mat, long long nn, long long ncb, long long rb_cap,
+    k_tile_colscan(uint32_t *__restrict__ mat, long long nn, long long ms, long long ncb, long long rb_cap,
                    const long long *__restrict__ n_items_dev, uint32_t *lb, uint32_t *__restrict__ nodecnt,
                    U64x2 *__restrict__ pairs, PlanOf plan_of, const int *guard) {
   lod::pdl_wait();
@@ -209,12 +217,17 @@ static __global__ void __launch_bounds__(kDirScanBlock)
   if (k >= nn) return;
   const long long t0 = rb * kDirRowBlock;
   const int nt = (int)min((long long)kDirRowBlock, ntiles - t0);
+#if LOD_COLSCAN_KEEP
   uint32_t c[kDirRowBlock];
+#endif
   uint32_t sum = 0;
 #pragma unroll
   for (int q = 0; q < kDirRowBlock; ++q) {
-    c[q] = q < nt ? mat[(t0 + q) * nn + k] : 0u;
-    sum += c[q];
+    const uint32_t v = q < nt ? mat[(t0 + q) * ms + k] : 0u;
+#if LOD_COLSCAN_KEEP
+    c[q] = v;
+#endif
+    sum += v;
   }
   uint32_t *mine = lb + rb * nn + k;
   uint32_t excl = 0;
@@ -246,11 +259,19 @@ static __global__ void __launch_bounds__(kDirScanBlock)
     pairs[k] = plan_of(k, excl + sum);
   }
   uint32_t run = excl;
+#if LOD_COLSCAN_KEEP
 #pragma unroll
   for (int q = 0; q < kDirRowBlock; ++q) {
-    if (q < nt) mat[(t0 + q) * nn + k] = run;
+    if (q < nt) mat[(t0 + q) * ms + k] = run;
     run += c[q];
   }
+#else
+  for (int q = 0; q < nt; ++q) {  // second read of the block's entries (L1 / L2)
+    const uint32_t v = mat[(t0 + q) * ms + k];
+    mat[(t0 + q) * ms + k] = run;
+    run += v;
+  }
+#endif
 }
 
 // Digit totals of every pass from the per-node counts (keys are node ids).

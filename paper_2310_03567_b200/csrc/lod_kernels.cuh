@@ -377,7 +377,7 @@ __device__ __forceinline__ void count_pending(const NodeCols &nd, int leaf) {
   const unsigned act = __ballot_sync(0xffffffffu, leaf >= 0);
   if (leaf >= 0) {
     const unsigned peers = __match_any_sync(act, leaf);
-    if (lane_id() == (unsigned)(__ffs(peers) - 1)) atomicAdd(&nd.pending[leaf], (unsigned long long)__popc(peers));
+    if ((peers & lanemask_lt()) == 0) atomicAdd(&nd.pending[leaf], (unsigned long long)__popc(peers));
   }
 }
 

@@ -160,18 +160,23 @@ static __global__ void __launch_bounds__(32 * W)
       key[q] = 0xFFFFFFFFu;
       if (i < n) key[q] = (uint32_t)(i < n_all ? node_of[i] : __ldg(&backlog[i - n_all].x));
     }
+    // the rounds' lane groups first (independent MATCHes), then the counter
+    // chain; a group's leader is its lowest lane (no lanes below it)
+    unsigned peers[kAhead];
+#pragma unroll
+    for (int q = 0; q < kAhead; ++q) peers[q] = __match_any_sync(0xffffffffu, key[q]);
 #pragma unroll
     for (int q = 0; q < kAhead; ++q) {
       const long long i = i0 + (long long)(r0 + q) * 32 + lane;
       const bool ok = i < n;
-      const unsigned peers = __match_any_sync(0xffffffffu, key[q]);
+      const uint32_t below = __popc(peers[q] & lt);
       const uint32_t b = ok ? cnt[key[q]] : 0u;
       if (ok) {
         keys[i] = key[q];
-        rank[i] = (uint16_t)(b + __popc(peers & lt));
+        rank[i] = (uint16_t)(b + below);
       }
       __syncwarp();
-      if (ok && lane == __ffs(peers) - 1) cnt[key[q]] = (uint16_t)(b + __popc(peers));
+      if (ok && below == 0) cnt[key[q]] = (uint16_t)(b + __popc(peers[q]));
       __syncwarp();
     }
   }
@@ -363,17 +368,25 @@ static __global__ void __launch_bounds__(kRadixBlock, LOD_RADIX_MINB)
   mbar_wait(&s_bar, 0);
   __syncthreads();
   // 1) warp-ordered ranking over the staged tile (input order)
+  unsigned peers[kRadixRounds];  // the rounds' lane groups first (independent MATCHes)
+  int dig[kRadixRounds];
+#pragma unroll
+  for (int r = 0; r < kRadixRounds; ++r) {
+    const int li = wofs + r * 32 + lane;
+    dig[r] = li < valid ? (int)((sk[li] >> shift) & (kRadixDigits - 1)) : kRadixDigits + 1;
+    peers[r] = __match_any_sync(0xffffffffu, dig[r]);
+  }
+#pragma unroll
   for (int r = 0; r < kRadixRounds; ++r) {
     const int li = wofs + r * 32 + lane;
     const bool ok = li < valid;
-    const uint32_t key = ok ? sk[li] : 0u;
-    const int d = ok ? (int)((key >> shift) & (kRadixDigits - 1)) : kRadixDigits + 1;
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const int d = dig[r];
+    const uint32_t below = __popc(peers[r] & lt);
     const uint32_t b = ok ? wh[warp][d] : 0u;
     if (!vals_in) sv[li] = (uint32_t)(t0 + li);
-    sloc[li] = (uint16_t)(b + __popc(peers & lt));
+    sloc[li] = (uint16_t)(b + below);
     __syncwarp();
-    if (ok && lane == __ffs(peers) - 1) wh[warp][d] = b + __popc(peers);
+    if (ok && below == 0) wh[warp][d] = b + __popc(peers[r]);
     __syncwarp();
   }
   __syncthreads();

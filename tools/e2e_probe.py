@@ -23,6 +23,13 @@ def main():
         px = torch.from_numpy(x).pin_memory().numpy()
         pc = torch.from_numpy(c.view(np.int32)).pin_memory().numpy().view(np.uint32)
         pin.append((px, pc))
+    import os
+    if os.environ.get("E2E_PRETOUCH"):  # one untimed DMA of every pinned buffer first
+        scratch = torch.empty(16_000_000, dtype=torch.uint8, device="cuda")
+        for x, c in pin:
+            scratch[: x.nbytes].copy_(torch.from_numpy(x.view(np.uint8).reshape(-1)), non_blocking=True)
+            scratch[: c.nbytes].copy_(torch.from_numpy(c.view(np.uint8).reshape(-1)), non_blocking=True)
+        torch.cuda.synchronize()
     for mode in ("frames_10ms", "one_frame", "insert_loop"):
         vals = []
         for rep in range(4):

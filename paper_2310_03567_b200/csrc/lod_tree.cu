@@ -216,6 +216,7 @@ struct LodTree {
   DBuf<uint32_t> keys, keys_b, vals_a, vals_b, hist, ghist, nodecnt;
   DBuf<uint32_t> dmat, dlb;  // direct placement: tiles x nodes counts -> prefixes; column-scan look-back
   DBuf<uint16_t> drank;      // direct placement: in-tile ranks
+  DBuf<U64x2> dpscan;        // direct placement: the plan scan's per-column-block aggregates / prefixes
   DBuf<int32_t> seg_node, dense;
   DBuf<U64x2> pairs;     // packed per-node plans, scanned in place (k_radix_ghist -> k_seg_list)
   DBuf<long long> wlo;   // write list: payload offsets of every touched node's chunks in slot order
@@ -1071,7 +1072,7 @@ int lod_tree_destroy(LodTree *t) {
   t->hused.release(); t->srank.release(); t->wcount.release(); t->wbase.release();
   t->backlog.release(); t->wins.release(); t->keys.release(); t->keys_b.release();
   t->vals_a.release(); t->vals_b.release(); t->hist.release(); t->ghist.release(); t->nodecnt.release();
-  t->dmat.release(); t->dlb.release(); t->drank.release();
+  t->dmat.release(); t->dlb.release(); t->drank.release(); t->dpscan.release();
   t->dense.release();
   t->seg_node.release(); t->pairs.release(); t->wlo.release(); t->sinfo.release(); t->seg_start.release();
   t->plan.release(); t->plan_ex.release(); t->in_xyz.release();
@@ -1430,7 +1431,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     const long long dcb = (num_nodes + kDirScanBlock - 1) / kDirScanBlock;
     if (direct) {
       RK(t->dmat.ensure(nn_pad * dtiles, st));
-      RK(t->dlb.ensure(drb * num_nodes + 1, st));
+      RK(t->dlb.ensure(drb * num_nodes + 1 + dcb, st));  // look-back words, ticket, plan-scan flags
       RK(t->drank.ensure(n_items, st));
       // warps per CTA: as many per-warp counter arrays as fit 48 KB
       // (LOD_DIR_W; default one warp per CTA: same-box A/B, driver range,
@@ -1440,7 +1441,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       const int W = wfit >= 8 ? 8 : wfit >= 4 ? 4 : wfit >= 2 ? 2 : 1;
       const unsigned grid = (unsigned)std::max<long long>((dtiles + W - 1) / W, 1);
       const size_t sm = (size_t)W * nn_pad * 2;
-      const long long lbwd = drb * num_nodes + 1;
+      const long long lbwd = drb * num_nodes + 1 + dcb;
       auto go = [&](auto kern) {
         lod::launch(kern, grid, 32 * W, sm, st, node_of, n_all, (const uint4 *)t->backlog.p, num_nodes, nn_pad,
                     t->keys.p, t->drank.p, t->dmat.p, t->dlb.p, lbwd, (const unsigned long long *)&t->d_ctrl->n_used,
@@ -1451,9 +1452,10 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       else if (W == 2) go(k_rank_prep<2>);
       else go(k_rank_prep<1>);
       RK(t->pairs.ensure(Kc, st));
+      RK(t->dpscan.ensure(2 * dcb, st));
       lod::launch(k_tile_colscan<NodePlanOf>, (unsigned)std::max<long long>(drb * dcb, dcb), kDirScanBlock, 0, st,
-                  t->dmat.p, num_nodes, nn_pad, dcb, drb, (const long long *)n_items_dev, t->dlb.p, t->nodecnt.p, t->pairs.p,
-                  NodePlanOf{t->nd, t->geo}, guard);
+                  t->dmat.p, num_nodes, nn_pad, dcb, drb, (const long long *)n_items_dev, t->dlb.p, t->nodecnt.p,
+                  t->pairs.p, NodePlanOf{t->nd, t->geo}, t->dpscan.p, (U64x2 *)&t->d_ctrl->pack_tot, guard);
     } else {
       // node counts in per-CTA shared memory (16-bit counters) up to
       // kNodeHistSmemMax nodes, as long as no CTA can see 65535 items
@@ -1486,7 +1488,8 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     // pass then writes every record straight into its chunk slot.
     // one scan of the packed node plans: dense ids, segment starts, acquisition
     // and write-list starts (k_seg_list unpacks them per touched node)
-    exclusive_scan_lb<U64x2>(t->pairs.p, t->pairs.p, num_nodes, &t->d_ctrl->pack_tot, t->lb64, st, guard);
+    if (!direct)  // (direct: the column scan scanned the plans)
+      exclusive_scan_lb<U64x2>(t->pairs.p, t->pairs.p, num_nodes, &t->d_ctrl->pack_tot, t->lb64, st, guard);
     lod::launch(k_seg_list, grid_for(num_nodes), 256, 0, st, t->nd, t->geo, t->nodecnt.p, num_nodes, t->pairs.p,
                 t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->plan_ex.p, t->d_ctrl, guard);
     lod::launch(k_alloc, std::max(grid_for(Kb), grid_for(acq_bound)), 256, 0, st, t->nd, t->pool, t->geo,

@@ -195,12 +195,14 @@ static __global__ void __launch_bounds__(32 * W)
 // ticket order; row blocks chain per column with a decoupled look-back
 // (status bits as in the onesweep).  lb: rb_cap * nn words + the ticket.
 // The last row block also writes each node's plan record (k_radix_ghist's
-// other job; the digit totals are not needed here).
+// other job; the digit totals are not needed here) and scans them (the
+// segment scan the LSD path runs as its own launch).
 template <class PlanOf>
 static __global__ void __launch_bounds__(kDirScanBlock)
     k_tile_colscan(uint32_t *__restrict__ mat, long long nn, long long ms, long long ncb, long long rb_cap,
                    const long long *__restrict__ n_items_dev, uint32_t *lb, uint32_t *__restrict__ nodecnt,
-                   U64x2 *__restrict__ pairs, PlanOf plan_of, const int *guard) {
+                   U64x2 *__restrict__ pairs, PlanOf plan_of, U64x2 *pscan, U64x2 *__restrict__ pack_tot,
+                   const int *guard) {
   lod::pdl_wait();
   if (guard && *guard) return;
   __shared__ uint32_t s_ticket;
@@ -209,74 +211,109 @@ static __global__ void __launch_bounds__(kDirScanBlock)
   const long long n = *n_items_dev;
   const long long ntiles = (n + kDirTile - 1) / kDirTile;
   const long long nrb = (ntiles + kDirRowBlock - 1) / kDirRowBlock;
+  const long long last_rb = nrb > 0 ? nrb - 1 : 0;  // no items: row block 0 writes the zero plans
   const long long rb = s_ticket / ncb, cb = s_ticket % ncb;
+  if (rb > last_rb) return;  // CTA-uniform
   const long long k = cb * kDirScanBlock + threadIdx.x;
-  if (nrb == 0) {  // no items: zero counts, plans of untouched nodes
-    if (rb == 0 && k < nn) {
-      nodecnt[k] = 0;
-      pairs[k] = plan_of(k, 0u);
+  const bool live = k < nn;
+  uint32_t node_total = 0;
+  if (nrb > 0 && live) {
+    const long long t0 = rb * kDirRowBlock;
+    const int nt = (int)min((long long)kDirRowBlock, ntiles - t0);
+#if LOD_COLSCAN_KEEP
+    uint32_t c[kDirRowBlock];
+#endif
+    uint32_t sum = 0;
+#pragma unroll
+    for (int q = 0; q < kDirRowBlock; ++q) {
+      const uint32_t v = q < nt ? mat[(t0 + q) * ms + k] : 0u;
+#if LOD_COLSCAN_KEEP
+      c[q] = v;
+#endif
+      sum += v;
     }
-    return;
-  }
-  if (rb >= nrb) return;
-  if (k >= nn) return;
-  const long long t0 = rb * kDirRowBlock;
-  const int nt = (int)min((long long)kDirRowBlock, ntiles - t0);
-#if LOD_COLSCAN_KEEP
-  uint32_t c[kDirRowBlock];
-#endif
-  uint32_t sum = 0;
+    uint32_t *mine = lb + rb * nn + k;
+    uint32_t excl = 0;
+    if (rb == 0) {
+      atomicExch(mine, kLbPre | sum);
+    } else {
+      atomicExch(mine, kLbAgg | sum);
+      // 4 predecessors per round trip; an unpublished one ends the round
+      long long p = rb - 1;
+      for (bool done = false; !done;) {
+        uint32_t v[4];
 #pragma unroll
-  for (int q = 0; q < kDirRowBlock; ++q) {
-    const uint32_t v = q < nt ? mat[(t0 + q) * ms + k] : 0u;
+        for (int q = 0; q < 4; ++q) v[q] = p - q >= 0 ? *((volatile uint32_t *)(lb + (p - q) * nn + k)) : (2u << 30);  // kLbPre
+        int q = 0;
+        for (; q < 4; ++q) {
+          if ((v[q] & ~kLbMask) == 0) break;
+          excl += v[q] & kLbMask;
+          if ((v[q] & ~kLbMask) == kLbPre) {
+            done = true;
+            break;
+          }
+        }
+        p -= q;
+      }
+      atomicExch(mine, kLbPre | (excl + sum));
+    }
+    node_total = excl + sum;
+    uint32_t run = excl;
 #if LOD_COLSCAN_KEEP
-    c[q] = v;
-#endif
-    sum += v;
-  }
-  uint32_t *mine = lb + rb * nn + k;
-  uint32_t excl = 0;
-  if (rb == 0) {
-    atomicExch(mine, kLbPre | sum);
-  } else {
-    atomicExch(mine, kLbAgg | sum);
-    // 4 predecessors per round trip; an unpublished one ends the round
-    long long p = rb - 1;
-    for (bool done = false; !done;) {
-      uint32_t v[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = p - q >= 0 ? *((volatile uint32_t *)(lb + (p - q) * nn + k)) : (2u << 30);  // kLbPre
-      int q = 0;
-      for (; q < 4; ++q) {
-        if ((v[q] & ~kLbMask) == 0) break;
-        excl += v[q] & kLbMask;
-        if ((v[q] & ~kLbMask) == kLbPre) {
-          done = true;
+    for (int q = 0; q < kDirRowBlock; ++q) {
+      if (q < nt) mat[(t0 + q) * ms + k] = run;
+      run += c[q];
+    }
+#else
+    for (int q = 0; q < nt; ++q) {  // second read of the block's entries (L1 / L2)
+      const uint32_t v = mat[(t0 + q) * ms + k];
+      mat[(t0 + q) * ms + k] = run;
+      run += v;
+    }
+#endif
+  }
+  if (rb != last_rb) return;  // CTA-uniform
+  // the last row block: node totals, plan records and their exclusive scan in
+  // node order (the segment scan), chained over the column blocks
+  // (flags after the ticket word: 1 aggregate, 2 inclusive prefix)
+  U64x2 v = u64x2(0, 0);
+  if (live) {
+    nodecnt[k] = node_total;
+    v = plan_of(k, node_total);
+  }
+  __shared__ U64x2 sh64[kDirScanBlock / 32 + 1];
+  __shared__ U64x2 s_excl;
+  U64x2 btot;
+  const U64x2 ex = block_exclusive_scan<U64x2, kDirScanBlock>(v, sh64, btot);
+  if (threadIdx.x == 0) {
+    uint32_t *flag = lb + rb_cap * nn + 1;
+    U64x2 *agg = pscan, *inc = pscan + ncb;
+    U64x2 excl = u64x2(0, 0);
+    if (cb > 0) {
+      agg[cb] = btot;
+      __threadfence();
+      atomicExch(flag + cb, 1u);
+      for (long long p = cb - 1;;) {
+        const uint32_t f = *((volatile uint32_t *)(flag + p));
+        if (f == 0) continue;
+        __threadfence();
+        if (f == 2u) {
+          excl = excl + ld_cg(inc + p);
           break;
         }
+        excl = excl + ld_cg(agg + p);
+        --p;
       }
-      p -= q;
     }
-    atomicExch(mine, kLbPre | (excl + sum));
+    inc[cb] = excl + btot;
+    __threadfence();
+    atomicExch(flag + cb, 2u);
+    s_excl = excl;
+    if (cb == ncb - 1) *pack_tot = excl + btot;
   }
-  if (rb == nrb - 1) {
-    nodecnt[k] = excl + sum;
-    pairs[k] = plan_of(k, excl + sum);
-  }
-  uint32_t run = excl;
-#if LOD_COLSCAN_KEEP
-#pragma unroll
-  for (int q = 0; q < kDirRowBlock; ++q) {
-    if (q < nt) mat[(t0 + q) * ms + k] = run;
-    run += c[q];
-  }
-#else
-  for (int q = 0; q < nt; ++q) {  // second read of the block's entries (L1 / L2)
-    const uint32_t v = mat[(t0 + q) * ms + k];
-    mat[(t0 + q) * ms + k] = run;
-    run += v;
-  }
-#endif
+  __syncthreads();
+  if (live) pairs[k] = s_excl + ex;
 }
 
 // Digit totals of every pass from the per-node counts (keys are node ids).

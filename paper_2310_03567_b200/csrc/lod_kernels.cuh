@@ -898,6 +898,41 @@ struct NodePlanOf {
   __device__ __forceinline__ U64x2 operator()(long long n, uint32_t len) const { return node_plan(nd, geo, n, len); }
 };
 
+// k_seg_list's work, per node and for the totals, for a kernel that has the
+// node's count and its scanned plan prefix in registers (direct placement:
+// the column scan's last row block, radix.cuh k_tile_colscan).
+struct SegFinish {
+  NodeCols nd;
+  Geo geo;
+  int32_t *seg_node;
+  long long *seg_start;
+  int32_t *dense;
+  U64x2 *plan;
+  U64x2 *plan_ex;
+  Ctrl *ctrl;
+  __device__ __forceinline__ U64x2 plan_of(long long n, uint32_t len) const { return node_plan(nd, geo, n, len); }
+  __device__ __forceinline__ void node(long long i, uint32_t len, const U64x2 &ex, const U64x2 &own) const {
+    if (!len) return;
+    const long long d = (long long)(ex.a >> kPackShift);
+    seg_node[d] = (int32_t)i;
+    seg_start[d] = (long long)(ex.a & kPackLow);
+    dense[i] = (int32_t)d;
+    plan[d] = u64x2(own.b >> 32, own.b & 0xFFFFFFFFull);
+    plan_ex[d] = u64x2(ex.b >> 32, ex.b & 0xFFFFFFFFull);
+  }
+  __device__ __forceinline__ void total(const U64x2 &tot) const {
+    ctrl->pack_tot = tot;
+    const unsigned long long K = tot.a >> kPackShift;
+    ctrl->seg_tot = u64x2(K, tot.a & kPackLow);
+    ctrl->acq_tot = u64x2(tot.b >> 32, tot.b & 0xFFFFFFFFull);
+    seg_start[K] = (long long)(tot.a & kPackLow);
+    ctrl->n_keys = (unsigned)K;
+    ctrl->alloc_F = ctrl->free_count;
+    ctrl->alloc_A = ctrl->allocated_total;
+    ctrl->chunk_base = (ctrl->arena_off + 15ull) / 16ull * 16ull;
+  }
+};
+
 __global__ void k_seg_list(NodeCols nd, Geo geo, uint32_t *__restrict__ nodecnt, long long num_nodes,
                            const U64x2 *__restrict__ pairs_ex, int32_t *__restrict__ seg_node,
                            long long *__restrict__ seg_start, int32_t *__restrict__ dense, U64x2 *__restrict__ plan,

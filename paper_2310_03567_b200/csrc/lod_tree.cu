@@ -1451,11 +1451,11 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       else if (W == 4) go(k_rank_prep<4>);
       else if (W == 2) go(k_rank_prep<2>);
       else go(k_rank_prep<1>);
-      RK(t->pairs.ensure(Kc, st));
       RK(t->dpscan.ensure(2 * dcb, st));
-      lod::launch(k_tile_colscan<NodePlanOf>, (unsigned)std::max<long long>(drb * dcb, dcb), kDirScanBlock, 0, st,
-                  t->dmat.p, num_nodes, nn_pad, dcb, drb, (const long long *)n_items_dev, t->dlb.p, t->nodecnt.p,
-                  t->pairs.p, NodePlanOf{t->nd, t->geo}, t->dpscan.p, (U64x2 *)&t->d_ctrl->pack_tot, guard);
+      const SegFinish seg{t->nd, t->geo, t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->plan_ex.p, t->d_ctrl};
+      lod::launch(k_tile_colscan<SegFinish>, (unsigned)std::max<long long>(drb * dcb, dcb), kDirScanBlock, 0, st,
+                  t->dmat.p, num_nodes, nn_pad, dcb, drb, (const long long *)n_items_dev, t->dlb.p, seg, t->dpscan.p,
+                  guard);
     } else {
       // node counts in per-CTA shared memory (16-bit counters) up to
       // kNodeHistSmemMax nodes, as long as no CTA can see 65535 items
@@ -1488,9 +1488,10 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     // pass then writes every record straight into its chunk slot.
     // one scan of the packed node plans: dense ids, segment starts, acquisition
     // and write-list starts (k_seg_list unpacks them per touched node)
-    if (!direct)  // (direct: the column scan scanned the plans)
+    if (!direct)  // (direct: the column scan scanned and unpacked the plans)
       exclusive_scan_lb<U64x2>(t->pairs.p, t->pairs.p, num_nodes, &t->d_ctrl->pack_tot, t->lb64, st, guard);
-    lod::launch(k_seg_list, grid_for(num_nodes), 256, 0, st, t->nd, t->geo, t->nodecnt.p, num_nodes, t->pairs.p,
+    if (!direct)
+      lod::launch(k_seg_list, grid_for(num_nodes), 256, 0, st, t->nd, t->geo, t->nodecnt.p, num_nodes, t->pairs.p,
                 t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->plan_ex.p, t->d_ctrl, guard);
     lod::launch(k_alloc, std::max(grid_for(Kb), grid_for(acq_bound)), 256, 0, st, t->nd, t->pool, t->geo,
                 t->seg_node.p, t->seg_start.p, t->plan.p, t->plan_ex.p, t->wlo.p, t->sinfo.p, t->d_ctrl,

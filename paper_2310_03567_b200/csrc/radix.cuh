@@ -194,14 +194,14 @@ static __global__ void __launch_bounds__(32 * W)
 // per (row block of kDirRowBlock tiles, kDirScanBlock node columns), taken in
 // ticket order; row blocks chain per column with a decoupled look-back
 // (status bits as in the onesweep).  lb: rb_cap * nn words + the ticket.
-// The last row block also writes each node's plan record (k_radix_ghist's
-// other job; the digit totals are not needed here) and scans them (the
-// segment scan the LSD path runs as its own launch).
-template <class PlanOf>
+// The last row block also makes each node's plan record (k_radix_ghist's
+// other job; the digit totals are not needed here), scans them (the segment
+// scan the LSD path runs as its own launch) and unpacks them (Seg: the
+// per-node and total work of k_seg_list).
+template <class Seg>
 static __global__ void __launch_bounds__(kDirScanBlock)
     k_tile_colscan(uint32_t *__restrict__ mat, long long nn, long long ms, long long ncb, long long rb_cap,
-                   const long long *__restrict__ n_items_dev, uint32_t *lb, uint32_t *__restrict__ nodecnt,
-                   U64x2 *__restrict__ pairs, PlanOf plan_of, U64x2 *pscan, U64x2 *__restrict__ pack_tot,
+                   const long long *__restrict__ n_items_dev, uint32_t *lb, Seg seg, U64x2 *pscan,
                    const int *guard) {
   lod::pdl_wait();
   if (guard && *guard) return;
@@ -277,11 +277,7 @@ static __global__ void __launch_bounds__(kDirScanBlock)
   // the last row block: node totals, plan records and their exclusive scan in
   // node order (the segment scan), chained over the column blocks
   // (flags after the ticket word: 1 aggregate, 2 inclusive prefix)
-  U64x2 v = u64x2(0, 0);
-  if (live) {
-    nodecnt[k] = node_total;
-    v = plan_of(k, node_total);
-  }
+  const U64x2 v = live ? seg.plan_of(k, node_total) : u64x2(0, 0);
   __shared__ U64x2 sh64[kDirScanBlock / 32 + 1];
   __shared__ U64x2 s_excl;
   U64x2 btot;
@@ -310,10 +306,10 @@ static __global__ void __launch_bounds__(kDirScanBlock)
     __threadfence();
     atomicExch(flag + cb, 2u);
     s_excl = excl;
-    if (cb == ncb - 1) *pack_tot = excl + btot;
+    if (cb == ncb - 1) seg.total(excl + btot);
   }
   __syncthreads();
-  if (live) pairs[k] = s_excl + ex;
+  if (live) seg.node(k, node_total, s_excl + ex, v);  // k_seg_list's per-node work
 }
 
 // Digit totals of every pass from the per-node counts (keys are node ids).

@@ -118,7 +118,10 @@ static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
 // into the node's items in earlier tiles; rank = that + the in-tile rank.
 // Chosen when the matrix is small (a few thousand nodes: L2-resident);
 // otherwise the LSD multisplit runs.
-constexpr int kDirRowBlock = 32;    // tiles per row block of the column scan
+#ifndef LOD_DIR_ROWBLOCK
+#define LOD_DIR_ROWBLOCK 32  // A/B, driver range: 16 / 32 / 64 all 2628-2633 Mpts/s
+#endif
+constexpr int kDirRowBlock = LOD_DIR_ROWBLOCK;  // tiles per row block of the column scan
 constexpr int kDirScanBlock = 256;  // node columns per column-scan CTA
 #ifndef LOD_COLSCAN_KEEP
 #define LOD_COLSCAN_KEEP 1  // counts kept in registers between the two sweeps (A/B: 2607-2610 vs 2581-2596 re-read)

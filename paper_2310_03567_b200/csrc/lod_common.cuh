@@ -49,10 +49,10 @@ __device__ __forceinline__ long long f2i64(double v) {
   return (long long)0x8000000000000000ULL;
 }
 
-#ifndef LOD_DIR_TILE
-#define LOD_DIR_TILE 2048
-#endif
-constexpr int kDirTile = LOD_DIR_TILE;  // direct placement (radix.cuh): items per tile = per warp
+// direct placement (radix.cuh): items per tile (= per warp) are 1 << tsh,
+// tsh from kDirTileShift up to kDirTileShiftMax (large updates: keeps the
+// tiles x nodes matrix small; u16 in-tile ranks)
+constexpr int kDirTileShift = 11, kDirTileShiftMax = 14;
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 

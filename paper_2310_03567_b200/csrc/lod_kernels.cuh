@@ -1145,7 +1145,7 @@ struct StoreSink {
 // input order, rank = its node's items in earlier tiles + its in-tile rank.
 // nowait: as k_onesweep's (launched behind k_publish's early release).
 __global__ void k_store_direct(StoreSink sink, const uint32_t *__restrict__ keys, const uint16_t *__restrict__ rank,
-                               const uint32_t *__restrict__ mat, long long ms,
+                               const uint32_t *__restrict__ mat, long long ms, int tsh,
                                const long long *__restrict__ n_items_dev, const int *guard, int nowait) {
   if (!nowait) lod::pdl_wait();
   if (guard && *guard) return;
@@ -1153,7 +1153,7 @@ __global__ void k_store_direct(StoreSink sink, const uint32_t *__restrict__ keys
   const long long n_items = *n_items_dev;
   for (long long i = gtid(); i < n_items; i += gstride()) {
     const uint32_t key = keys[i];
-    const long long t = i / kDirTile;
+    const long long t = i >> tsh;
     sink.store_rank((long long)mat[t * ms + key] + rank[i], key, (uint32_t)i);
   }
 }

@@ -1423,7 +1423,11 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     static const bool store_lsd = getenv("LOD_STORE_LSD") != nullptr;
     static const long long dir_max = getenv("LOD_DIRECT_MAX_ENTRIES") ? atoll(getenv("LOD_DIRECT_MAX_ENTRIES"))
                                                                       : (8LL << 20);
-    const long long dtiles = (n_items + kDirTile - 1) / kDirTile;
+    // the smallest tile (2048 items and up) whose matrix fits the cap
+    int tsh = kDirTileShift;
+    auto tiles_of = [&](int sh) { return (n_items + (1LL << sh) - 1) >> sh; };
+    while (tsh < kDirTileShiftMax && num_nodes * tiles_of(tsh) > dir_max) ++tsh;
+    const long long dtiles = tiles_of(tsh);
     const long long nn_pad = (num_nodes + 7) & ~7LL;  // matrix row stride, per-warp counters
     const bool direct = !delta && !store_lsd && nn_pad * 2 <= 49152 && num_nodes * dtiles <= dir_max &&
                         n_items < (1LL << 30);
@@ -1445,7 +1449,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       auto go = [&](auto kern) {
         lod::launch(kern, grid, 32 * W, sm, st, node_of, n_all, (const uint4 *)t->backlog.p, num_nodes, nn_pad,
                     t->keys.p, t->drank.p, t->dmat.p, t->dlb.p, lbwd, (const unsigned long long *)&t->d_ctrl->n_used,
-                    n_items_dev, guard);
+                    n_items_dev, tsh, guard);
       };
       if (W == 8) go(k_rank_prep<8>);
       else if (W == 4) go(k_rank_prep<4>);
@@ -1455,7 +1459,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
       const SegFinish seg{t->nd, t->geo, t->seg_node.p, t->seg_start.p, t->dense.p, t->plan.p, t->plan_ex.p, t->d_ctrl};
       lod::launch(k_tile_colscan<SegFinish>, (unsigned)std::max<long long>(drb * dcb, dcb), kDirScanBlock, 0, st,
                   t->dmat.p, num_nodes, nn_pad, dcb, drb, (const long long *)n_items_dev, t->dlb.p, seg, t->dpscan.p,
-                  guard);
+                  tsh, guard);
     } else {
       // node counts in per-CTA shared memory (16-bit counters) up to
       // kNodeHistSmemMax nodes, as long as no CTA can see 65535 items
@@ -1514,7 +1518,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
     uint32_t *skeys = nullptr, *svals = nullptr;
     if (direct) {
       lod::launch(k_store_direct, grid_for(n_items), 256, 0, st, sink, (const uint32_t *)t->keys.p,
-                  (const uint16_t *)t->drank.p, (const uint32_t *)t->dmat.p, nn_pad, (const long long *)n_items_dev,
+                  (const uint16_t *)t->drank.p, (const uint32_t *)t->dmat.p, nn_pad, tsh, (const long long *)n_items_dev,
                   guard, release ? 1 : 0);
     } else if (delta) {  // the delta reads the sorted order: materialise it, then store
       stable_multisplit(t->keys.p, n_items, passes, rs, st, &skeys, &svals, nullptr, 0, (const KVSink *)nullptr,

@@ -110,7 +110,7 @@ static __global__ void __launch_bounds__(kRadixBlock, kPrepBlocksPerSM)
 // ---- direct placement (one pass instead of the LSD passes) -------------------
 // The store only needs every item's rank among the earlier items of its node
 // (slot order = all-array / backlog order, _kernels.py:155-250).  Cut the item
-// list into tiles of kDirTile items, one warp per tile: the warp walks its
+// list into tiles of 1 << tsh items, one warp per tile: the warp walks its
 // tile in order and ranks each item against the tile's earlier items of the
 // same node (per-warp u16 counters in shared memory, MATCH.ANY per 32 items),
 // then writes the tile's per-node counts as one dense row of a tiles x nodes
@@ -135,7 +135,7 @@ static __global__ void __launch_bounds__(32 * W)
     k_rank_prep(NodeOf node_of, long long n_all, const uint4 *__restrict__ backlog, long long nn, long long nn_pad,
                 uint32_t *__restrict__ keys, uint16_t *__restrict__ rank, uint32_t *__restrict__ mat,
                 uint32_t *__restrict__ lb, long long lb_words, const unsigned long long *__restrict__ n_v_dev,
-                long long *__restrict__ n_items_out, const int *guard) {
+                long long *__restrict__ n_items_out, int tsh, const int *guard) {
   lod::pdl_wait();
   if (guard && *guard) return;
   extern __shared__ __align__(16) uint16_t dcnt[];  // nn_pad (a multiple of 8) per warp
@@ -147,14 +147,14 @@ static __global__ void __launch_bounds__(32 * W)
     lb[i] = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long tile = (long long)blockIdx.x * W + warp;
-  const long long i0 = tile * kDirTile;
+  const long long i0 = tile << tsh;
   if (i0 >= n) return;  // warp-uniform
   uint16_t *cnt = dcnt + (long long)warp * nn_pad;
   for (long long k = lane; k < nn_pad / 8; k += 32) reinterpret_cast<uint4 *>(cnt)[k] = make_uint4(0, 0, 0, 0);
   __syncwarp();
   const unsigned lt = lanemask_lt();
   constexpr int kAhead = 8;  // rounds of keys loaded ahead
-  for (int r0 = 0; r0 < kDirTile / 32; r0 += kAhead) {
+  for (int r0 = 0; r0 < (1 << tsh) / 32; r0 += kAhead) {
     if (i0 + (long long)r0 * 32 >= n) break;  // warp-uniform
     uint32_t key[kAhead];
 #pragma unroll
@@ -204,7 +204,7 @@ static __global__ void __launch_bounds__(32 * W)
 template <class Seg>
 static __global__ void __launch_bounds__(kDirScanBlock)
     k_tile_colscan(uint32_t *__restrict__ mat, long long nn, long long ms, long long ncb, long long rb_cap,
-                   const long long *__restrict__ n_items_dev, uint32_t *lb, Seg seg, U64x2 *pscan,
+                   const long long *__restrict__ n_items_dev, uint32_t *lb, Seg seg, U64x2 *pscan, int tsh,
                    const int *guard) {
   lod::pdl_wait();
   if (guard && *guard) return;
@@ -212,7 +212,7 @@ static __global__ void __launch_bounds__(kDirScanBlock)
   if (threadIdx.x == 0) s_ticket = atomicAdd(lb + rb_cap * nn, 1u);
   __syncthreads();
   const long long n = *n_items_dev;
-  const long long ntiles = (n + kDirTile - 1) / kDirTile;
+  const long long ntiles = (n + (1LL << tsh) - 1) >> tsh;
   const long long nrb = (ntiles + kDirRowBlock - 1) / kDirRowBlock;
   const long long last_rb = nrb > 0 ? nrb - 1 : 0;  // no items: row block 0 writes the zero plans
   const long long rb = s_ticket / ncb, cb = s_ticket % ncb;

@@ -339,6 +339,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_cycle(SmallArgs a) {
     if (first) n_s = s_spill0;  // only iteration 1 spills (update.py:9-11)
     __syncthreads();
   }
+  __syncthreads();  // every warp has left the split loop (it reads s_err) before warp 0 may set it below
   const long long n_all = n_s + a.n;
 
   // ---------------------------------------------------------------- sampling
@@ -348,7 +349,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_cycle(SmallArgs a) {
   // 32 consecutive points per step, lockstep by level: claims at one node
   // come from one level, and the lowest lane of a matching group is the
   // lowest index, so this is the sequential rule.
-  if (!s_err && warp == 0) {
+  if (warp == 0 && !s_err) {  // (warp first: the other warps never read s_err while warp 0 may set it)
     long long nv = 0;
     for (long long j0 = 0; j0 < n_all; j0 += 32) {
       const long long j = j0 + lane;
@@ -503,7 +504,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_cycle(SmallArgs a) {
   // ---------------------------------------------------------------- store
   // store_points / store_voxels (_kernels.py:155-250): slot = count + rank in
   // all-array order (points, warp 0) / backlog order (voxels, warp 1)
-  if (!s_err && warp < 2) {
+  if (warp < 2 && !s_err) {
     const long long total = warp == 0 ? n_all : s_nv;
     for (long long i0 = 0; i0 < total; i0 += 32) {
       const long long i = i0 + lane;

@@ -336,6 +336,9 @@ __global__ void k_rehash(const HSlot *__restrict__ old_slots, Hash h, const Ctrl
 // claiming every clear cell it crosses (claimant index v, colour col).
 // T = float on Geo::f32ok trees (the f32 twins in lod_common.cuh: identical
 // results, half the registers of the f64 state -> more resident warps).
+#ifndef LOD_COUNT_PIPE
+#define LOD_COUNT_PIPE 1  // f32 descent only (the f64 state spills with it); A/B: count phase 0.139-0.141 vs 0.143 ms
+#endif
 template <typename T>
 __device__ __forceinline__ int count_descend(const NodeCols &nd, const Geo &geo, const uint32_t *__restrict__ grid32,
                                              const Hash &h, UsedStage &stg, Ctrl *ctrl, int nid, int2 d, T x, T y,
@@ -345,6 +348,35 @@ __device__ __forceinline__ int count_descend(const NodeCols &nd, const Geo &geo,
   T s = (T)geo.size_by_level[lvl0], inv_s = (T)geo.inv_by_level[lvl0];
   // one dependent load per level, from the compact (L1-resident) descent
   // table; grid words bypass L1 so they do not evict it
+  if constexpr (LOD_COUNT_PIPE && sizeof(T) == 4) {
+  // the next level's grid word is loaded before this level's claim (claims
+  // never set grid bits -- k_resolve does -- so the word is the same either way)
+  long long cell = cell_of(geo, x, y, z, bx, by, bz, s, inv_s);
+  uint32_t w = (geo.fresh && d.y < 0)
+                   ? 0u
+                   : ld_nol1(grid32 + ((unsigned long long)((uint32_t)d.y & geo.gmask) << 4) + (cell >> 5));
+  do {
+    const int cur = nid;
+    const long long ccur = cell;
+    const uint32_t wcur = w;
+    nid = d.x + octant_step(x, y, z, bx, by, bz, s, inv_s);
+    d = __ldg(nd.desc + nid);
+    if (d.x >= 0) {
+      cell = cell_of(geo, x, y, z, bx, by, bz, s, inv_s);
+      w = (geo.fresh && d.y < 0)
+              ? 0u
+              : ld_nol1(grid32 + ((unsigned long long)((uint32_t)d.y & geo.gmask) << 4) + (cell >> 5));
+    }
+    if (!(wcur & (1u << (ccur & 31)))) {
+      const unsigned long long key = claim_key(cur, ccur, h.cbits);
+      const unsigned m = __activemask();
+      const unsigned lane = lane_id();
+      const unsigned long long left = __shfl_up_sync(m, key, 1);
+      if (!(lane > 0 && ((m >> (lane - 1)) & 1u) && left == key)) hash_claim(h, stg, key, v, col, ctrl);
+    }
+  } while (d.x >= 0);
+  return nid;
+  } else {
   do {
     const long long cell = cell_of(geo, x, y, z, bx, by, bz, s, inv_s);
     // a node split in this cycle has an all-clear grid (fresh arena, bits
@@ -369,6 +401,7 @@ __device__ __forceinline__ int count_descend(const NodeCols &nd, const Geo &geo,
     }
   } while (d.x >= 0);
   return nid;
+  }
 }
 
 // The leaf's pending count (fire-and-forget, warp-aggregated): k_decide

@@ -13,6 +13,11 @@
 // per-warp digit histogram in shared memory; warps are combined in order.
 // The tile is then reordered by digit in shared memory so the global writes
 // go out as contiguous digit runs.
+//
+// On trees of up to 24,576 nodes the update does not sort at all: the direct
+// placement below (k_rank_prep / k_tile_colscan / k_store_direct) gives every
+// item its rank within its node from per-tile node counts, and the LSD passes
+// serve the larger trees, the burst resolve's win list and delta emission.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>

@@ -1292,7 +1292,7 @@ int lod_insert_batch(LodTree *t, const float *xyz, const uint32_t *rgba, int64_t
   // table that still fills up falls back to a separate claim pass
   {
 #ifndef LOD_HASH_FACTOR_X4
-#define LOD_HASH_FACTOR_X4 6  // table slots ~ 1.5 x (previous cycle's claims + batch), next power of two
+#define LOD_HASH_FACTOR_X4 6  // table slots ~ 1.5 x (previous cycle's claims + batch), next power of two (A/B: 5 within 0.2 %, 8 -1.3 %)
 #endif
     const long long want = std::max<long long>(LOD_HASH_FACTOR_X4 * (t->prev_used + n) / 4, 1 << 20);
     const unsigned long long H = round_slots((unsigned long long)want);
